@@ -1,0 +1,136 @@
+/*
+ * hgb200.h — C-ABI of the B200-native ReFresh per-iteration data path.
+ *
+ * The reference (`histgnn`, /root/reference/pkg/src/histgnn) is a pure-Python
+ * package: its "plugin boundary" is its Python module API, and there is no FFI.
+ * Each entry point below replaces the compute inside one reference function;
+ * the Python package `paper_2301_07482_b200` keeps the reference signatures and
+ * binds these symbols with ctypes.
+ *
+ * Conventions (all functions):
+ *   - plain pointers + sizes, no torch types; every pointer is device memory
+ *     (or UVA-mapped host memory where stated) owned by the caller;
+ *   - asynchronous on the given stream; no host synchronisation inside;
+ *   - counts produced on the device are passed as `const int32_t* *_dev`
+ *     together with a host upper bound `*_max` that sizes the launch grid;
+ *   - return 0 on success, < 0 on error; hg_last_error() describes it;
+ *   - node ids and local ids are int32 (N < 2^31); full-graph CSR2 offsets int64;
+ *   - scratch memory is caller supplied; *_scratch_bytes() give the sizes.
+ * Compiled for sm_100a only.
+ */
+#ifndef HGB200_H_
+#define HGB200_H_
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+int hg_version(void);
+const char* hg_last_error(void);
+int hg_device_sync(void);
+
+/* ---- K1+K2 sampler: histgnn/sampler.py:118-163 (_sample_in_neighbors,
+ * _build_block), called per layer by sampler.py:166-190 (sample_layered).
+ * PCG64 state/inc are the 128-bit halves of
+ * default_rng(SeedSequence((seed, batch))) (sampler.py:104-106);
+ * *stream_pos_dev = draws consumed before this layer, advanced by sum(deg).
+ * Outputs: block CSR offsets blk_off[F+1] (start = blk_off[i], end = blk_end[i]),
+ * dst_deg[F], col_local[E], src_out = frontier ++ sorted new nodes,
+ * counts_dev[0] = E, counts_dev[1] = n_src. g2l (int64[N]) must start as -1;
+ * bitmap (uint32[ceil(N/32)]) must start zero and is left zero. */
+long long hg_sample_layer_scratch_bytes(long long F_max, long long num_nodes);
+int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t* g_col, long long num_nodes,
+                    const int32_t* frontier, const int32_t* F_dev, long long F_max, int fanout,
+                    unsigned long long st_hi, unsigned long long st_lo, unsigned long long inc_hi,
+                    unsigned long long inc_lo, unsigned long long* stream_pos_dev, unsigned epoch, int64_t* g2l,
+                    uint32_t* bitmap, int64_t* cand_off, int32_t* blk_off, int32_t* blk_end, int32_t* dst_deg,
+                    int32_t* src_flat, int32_t* col_local, int32_t* src_out, int32_t* counts_dev, void* scratch,
+                    long long scratch_bytes, cudaStream_t stream);
+
+/* ---- K3 prune: histgnn/trainer.py:166-207 (prune_with_cache) for one block,
+ * incl. graphs.py:123-127 (Csr2Graph.prune_many). counts_dev[0] = |compute_rows|,
+ * counts_dev[1] = |layer_live|; global_ctr[2] += prune writes. */
+long long hg_prune_scratch_bytes(long long n_src_max);
+int hg_prune_block(const int32_t* n_dst_dev, long long n_dst_max, const int32_t* n_src_dev, long long n_src_max,
+                   const uint8_t* live_dst, const uint8_t* inj_dst, const int32_t* start, int32_t* end,
+                   const int32_t* col, uint8_t* keep, int32_t* compute_rows, int32_t* pos_of, uint8_t* src_mask,
+                   int32_t* live_src, int32_t* counts_dev, long long* global_ctr, void* scratch,
+                   long long scratch_bytes, cudaStream_t stream);
+
+/* ---- K4 cache lookup: histgnn/cache.py:103-129 (_LayerCache.lookup) via
+ * cache.py:269-285 (HistCache.lookup, layer >= 1). t_stale may be +inf. */
+int hg_cache_lookup(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const int32_t* src_nodes,
+                    long long n_src_max, int32_t* row_of, const int32_t* admit_iter, int32_t* row_owner, int it,
+                    double t_stale, uint8_t* hit_flag, int32_t* hit_row, long long* layer_ctr, cudaStream_t stream);
+
+/* ---- K5 feature load: histgnn/trainer.py:326-343 (Trainer._load_input),
+ * cache.py:274-284 (feature region), trainer.py:213-228 (FeatureSource.fetch).
+ * feats may be a UVA pointer to pinned host memory. dtype 0 = fp32, 1 = fp16. */
+int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const int32_t* src_nodes,
+                     const int32_t* feature_row_of, const void* region, const void* feats, int dim, int dtype,
+                     float* h_out, long long* global_ctr, cudaStream_t stream);
+
+/* ---- K6 block aggregation: histgnn/nn.py:101-128,142-156 (_gcn_matrix,
+ * _mean_matrix, _layer_forward_ctx). kind 0 = GCN, 1 = SAGE_MEAN. */
+int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
+                     const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
+                     const float* h_in, int d, float* A, int ldA, cudaStream_t stream);
+
+/* ---- K7 dense transform: nn.py:150,156,170-176 (the GEMMs). Row-major. */
+int hg_gemm_rm(int transA, int transB, long long M, long long N, long long K, const float* A, long long lda,
+               const float* B, long long ldb, float beta, float* C, long long ldc, cudaStream_t stream);
+
+/* ---- forward epilogue: nn.py:161-162,288-293 (ReLU, h_full[rows], injected rows) */
+int hg_scatter_rows(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* Z, int dout, int relu,
+                    float* h_out, cudaStream_t stream);
+int hg_inject_rows(const int32_t* n_dev, long long n_max, const uint8_t* flag, const int32_t* hit_row,
+                   const float* table, int dim, float* h_out, cudaStream_t stream);
+
+/* ---- loss: nn.py:326-343 (cross_entropy, fp64) */
+int hg_cross_entropy(const float* logits, const int32_t* labels, int B, int C, float* dlogits, double* row_logp,
+                     double* loss, cudaStream_t stream);
+
+/* ---- K8 backward: nn.py:166-177,300-320 (_layer_backward, backward) */
+int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* d_h, const float* h_out,
+                 int dout, int relu, float* dz, cudaStream_t stream);
+long long hg_csc_scratch_bytes(long long E_max);
+int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t* keep, const int32_t* pos_of,
+                 const int32_t* col, long long E_max, long long n_src_max, unsigned* keys_sorted,
+                 unsigned* vals_sorted, int32_t* seg_lo, int32_t* seg_hi, void* scratch, long long scratch_bytes,
+                 cudaStream_t stream);
+/* K8 + K9 fused: transposed aggregation + nn.py:346-349 (node_grad_norms) */
+int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
+                     const int32_t* seg_lo, const int32_t* seg_hi, const unsigned* vals_sorted, const int32_t* rows,
+                     const int32_t* start, const int32_t* end, const int32_t* dst_deg, const int32_t* src_deg,
+                     const int32_t* n_dst_dev, const int32_t* pos_of, const float* SG, int ldSG, int d,
+                     float* d_in, double* norms, cudaStream_t stream);
+int hg_row_norms(const float* x, long long n, int d, double* out, cudaStream_t stream);
+
+/* ---- K11 optimizer: nn.py:355-360 (sgd_step) */
+int hg_sgd(float* params, const float* grads, long long n, float eta, cudaStream_t stream);
+
+/* ---- K10 cache update: histgnn/cache.py:188-204 (_LayerCache.update) via
+ * cache.py:289-322 (HistCache.update_cache), with _write/_release/
+ * _count_overwrites cache.py:131-186. Two stages so the host can size the
+ * ring table on first use (cache.py:79-91) after reading n_write. */
+long long hg_cache_update_scratch_bytes(long long n_max);
+int hg_cache_rank(int n, int k, const int32_t* live, const int32_t* src_nodes, const double* norms,
+                  const uint8_t* computed_flag, int32_t* row_of, int32_t* row_owner, long long* layer_ctr,
+                  void* scratch, long long scratch_bytes, cudaStream_t stream);
+int hg_cache_write(int n, int k, int cap, int H, int it, double t_stale, int refresh_retained, const int32_t* live,
+                   const float* emb, float* table, int32_t* row_of, int32_t* row_owner, int32_t* admit_iter,
+                   long long* layer_ctr, void* scratch, long long scratch_bytes, cudaStream_t stream);
+
+/* ---- static feature region: histgnn/cache.py:338-351 (backfill_features) */
+long long hg_degree_order_scratch_bytes(long long n);
+int hg_feature_region(const int64_t* g_start, const int64_t* g_end, long long n, long long k, int32_t* chosen,
+                      int32_t* feature_row_of, void* scratch, long long scratch_bytes, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HGB200_H_ */

@@ -1,0 +1,108 @@
+"""ctypes binding of the C-ABI library `libhgb200.so` (include/hgb200.h).
+
+The product path has no CPU fallback: if the library is missing, or no CUDA
+device is visible, every entry point raises instead of computing something
+else. `load()` returns the CDLL with argtypes declared from the header.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhgb200.so")
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int
+U32 = ctypes.c_uint
+I64 = ctypes.c_longlong
+U64 = ctypes.c_ulonglong
+F64 = ctypes.c_double
+F32 = ctypes.c_float
+
+# name -> (restype, argtypes); mirrors include/hgb200.h
+SIGNATURES = {
+    "hg_version": (I32, []),
+    "hg_last_error": (ctypes.c_char_p, []),
+    "hg_device_sync": (I32, []),
+    "hg_sample_layer_scratch_bytes": (I64, [I64, I64]),
+    "hg_sample_layer": (I32, [P, P, P, I64, P, P, I64, I32, U64, U64, U64, U64, P, U32, P, P, P, P, P,
+                              P, P, P, P, P, P, I64, P]),
+    "hg_prune_scratch_bytes": (I64, [I64]),
+    "hg_prune_block": (I32, [P, I64, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P]),
+    "hg_cache_lookup": (I32, [P, I64, P, P, I64, P, P, P, I32, F64, P, P, P, P]),
+    "hg_load_features": (I32, [P, I64, P, P, P, P, P, I32, I32, P, P, P]),
+    "hg_aggregate_fwd": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, P, I32, P]),
+    "hg_gemm_rm": (I32, [I32, I32, I64, I64, I64, P, I64, P, I64, F32, P, I64, P]),
+    "hg_scatter_rows": (I32, [P, I64, P, P, I32, I32, P, P]),
+    "hg_inject_rows": (I32, [P, I64, P, P, P, I32, P, P]),
+    "hg_cross_entropy": (I32, [P, P, I32, I32, P, P, P, P]),
+    "hg_gather_dz": (I32, [P, I64, P, P, P, I32, I32, P, P]),
+    "hg_csc_scratch_bytes": (I64, [I64]),
+    "hg_build_csc": (I32, [P, P, P, P, P, I64, I64, P, P, P, P, P, I64, P]),
+    "hg_transpose_agg": (I32, [I32, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P]),
+    "hg_row_norms": (I32, [P, I64, I32, P, P]),
+    "hg_sgd": (I32, [P, P, I64, F32, P]),
+    "hg_cache_update_scratch_bytes": (I64, [I64]),
+    "hg_cache_rank": (I32, [I32, I32, P, P, P, P, P, P, P, P, I64, P]),
+    "hg_cache_write": (I32, [I32, I32, I32, I32, I32, F64, I32, P, P, P, P, P, P, P, P, I64, P]),
+    "hg_degree_order_scratch_bytes": (I64, [I64]),
+    "hg_feature_region": (I32, [P, P, I64, I64, P, P, P, I64, P]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class HgError(RuntimeError):
+    pass
+
+
+def load():
+    """The loaded library (no GPU needed to load it)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise HgError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise HgError("paper_2301_07482_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+
+
+def call(name, *args):
+    """Invoke an int-status entry point and raise on failure."""
+    lib = load()
+    st = getattr(lib, name)(*args)
+    if st != 0:
+        raise HgError(f"{name} failed ({st}): {lib.hg_last_error().decode()}")
+    return st
+
+
+def query(name, *args):
+    return getattr(load(), name)(*args)
+
+
+def ptr(t):
+    """Device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)

@@ -1,0 +1,39 @@
+// Library-wide entry points: version, last error, launch checking.
+#include "hgb200.h"
+#include <mutex>
+#include <string>
+
+#include "hg_common.cuh"
+
+namespace hg {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* where, const std::string& msg) { g_last_error = std::string(where) + ": " + msg; }
+
+int fail(const char* where, int code, const std::string& msg) {
+  set_error(where, msg);
+  return code;
+}
+
+int check_launch(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(where, kCuda, cudaGetErrorString(e));
+  return kOk;
+}
+
+}  // namespace hg
+
+extern "C" {
+
+int hg_version(void) { return 10000; }  // 1.0.0
+
+const char* hg_last_error(void) { return hg::g_last_error.c_str(); }
+
+int hg_device_sync(void) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return hg::fail("hg_device_sync", hg::kCuda, cudaGetErrorString(e));
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+// Shared helpers for the hgb200 sm_100a kernels: status codes, launch checks,
+// device-count-aware grid sizing and warp utilities.
+//
+// Conventions of every hg_* entry point (see include/hgb200.h):
+//   * all memory is owned by the caller (PyTorch); pointers are device pointers
+//     unless named *_host; nothing is allocated here except cuBLAS handles;
+//   * every launch is asynchronous on the caller's stream;
+//   * element counts that are produced on the device are passed as device
+//     pointers (`const int32_t* n_dev`) together with a host upper bound
+//     (`n_max`) that sizes the grid, so a whole iteration can run without a
+//     host round trip;
+//   * functions return 0 on success and a negative status otherwise; the
+//     message is kept per thread and read with hg_last_error().
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+namespace hg {
+
+enum Status : int {
+  kOk = 0,
+  kBadArg = -1,
+  kCuda = -2,
+  kCublas = -3,
+  kUnsupported = -4,
+};
+
+void set_error(const char* where, const std::string& msg);
+int fail(const char* where, int code, const std::string& msg);
+int check_launch(const char* where);
+
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+inline unsigned grid_for(long long n, int per_block, unsigned cap = 148u * 64u) {
+  long long g = (n + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > (long long)cap) g = cap;
+  return (unsigned)g;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fixed-order tree reduction (identical result on every run)
+__device__ __forceinline__ double warp_sum_fixed(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
+// warp-aggregated integer counter bump: one atomic per warp
+__device__ __forceinline__ void warp_count_add(unsigned long long* ctr, bool pred) {
+  unsigned m = __ballot_sync(__activemask(), pred);
+  if (m && (lane_id() == (__ffs(__activemask()) - 1)))
+    atomicAdd(ctr, (unsigned long long)__popc(m));
+}
+
+// 128-bit vector load that bypasses L1 allocation (streaming gathers)
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint4 ldg_stream_u4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+}  // namespace hg
+
+#define HG_CHECK_CUDA(where, expr)                                         \
+  do {                                                                     \
+    cudaError_t _e = (expr);                                               \
+    if (_e != cudaSuccess)                                                 \
+      return hg::fail(where, hg::kCuda, cudaGetErrorString(_e));           \
+  } while (0)
+
+#define HG_LAUNCHED(where)                        \
+  do {                                            \
+    int _s = hg::check_launch(where);             \
+    if (_s) return _s;                            \
+  } while (0)

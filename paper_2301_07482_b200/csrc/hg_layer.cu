@@ -1,0 +1,441 @@
+// K6/K8/K9 + loss + SGD: the block convolutions around the dense transform.
+// Restates histgnn/nn.py (oracle: oracle/step.py):
+//   _mean_matrix / _gcn_matrix + a @ h_in   nn.py:101-128,148-156  -> k_aggregate
+//   h_full[rows] = z ; h_full[inj] = cached  nn.py:288-293          -> k_scatter_rows, k_inject
+//   cross_entropy (fp64 log-sum-exp)         nn.py:326-343          -> k_ce_rows, k_ce_loss
+//   dz = relu_mask * d_out                   nn.py:167              -> k_gather_dz
+//   d_in = A^T (dz W^T) (+ self)             nn.py:171,175-176      -> CSC build + k_transpose_agg
+//   node_grad_norms (fp64)                   nn.py:346-349          -> fused in k_transpose_agg
+//   sgd_step                                 nn.py:355-360          -> k_sgd
+//
+// Layout: the GEMM operand of block b is A[R x ldA] with ldA = K + 4:
+//   SAGE: A = [h_self | mean_nbr | 1 | 0 0 0], K = 2 d_in
+//   GCN : A = [A_hat h            | 1 | 0 0 0], K = d_in
+// and the parameters P[(K+1) x d_out] = [W (W_self; W_neigh) ; bias], so
+// z = A[:, :K+1] @ P carries the bias and dP = A[:, :K+1]^T dz carries db.
+// Sparse accumulation mirrors scipy's CSR/CSC loops: per edge
+// sum = sum + coef * x with separate fp32 roundings (no FMA contraction), in
+// CSR order forward and ascending dst-row order backward; fixed-order warp
+// trees for the fp64 norms, so every run is bit-identical.
+#include "hgb200.h"
+#include <cub/device/device_radix_sort.cuh>
+
+#include "hg_scan.cuh"
+#include "hg_state.h"
+
+namespace hg {
+namespace {
+
+constexpr int kKindGCN = 0;
+constexpr int kKindSAGE = 1;
+constexpr int kMaxVecPerLane = 4;  // d_in <= 512 floats
+
+__device__ __forceinline__ float4 f4_fmadd_rn(float4 acc, float c, float4 x) {
+  return make_float4(__fadd_rn(acc.x, __fmul_rn(c, x.x)), __fadd_rn(acc.y, __fmul_rn(c, x.y)),
+                     __fadd_rn(acc.z, __fmul_rn(c, x.z)), __fadd_rn(acc.w, __fmul_rn(c, x.w)));
+}
+
+__device__ __forceinline__ float gcn_coef(int dd, int sd) {
+  return (float)(1.0 / sqrt(((double)dd + 1.0) * ((double)sd + 1.0)));
+}
+
+// one warp per compute row
+template <int kKind>
+__global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
+                                                   const int32_t* __restrict__ start, const int32_t* __restrict__ end,
+                                                   const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
+                                                   const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
+                                                   int d, float* __restrict__ A, int ldA) {
+  const int R = *R_dev;
+  const int lane = threadIdx.x & 31;
+  const int nv = d >> 2;
+  const int K = kKind == kKindSAGE ? 2 * d : d;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < R; i += warps) {
+    const int r = rows[i];
+    const int e0 = start[r], e1 = end[r];
+    const int cnt = e1 - e0;
+    float4 acc[kMaxVecPerLane];
+#pragma unroll
+    for (int t = 0; t < kMaxVecPerLane; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float cs = 0.f;
+    if (kKind == kKindSAGE) cs = cnt > 0 ? (float)(1.0 / (double)cnt) : 0.f;
+    const int dd = kKind == kKindGCN ? dst_deg[r] : 0;
+    int e = e0;
+    for (; e + 4 <= e1; e += 4) {
+      int c[4];
+      float w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        c[q] = col[e + q];
+        w[q] = kKind == kKindSAGE ? cs : gcn_coef(dd, src_deg[c[q]]);
+      }
+#pragma unroll
+      for (int t = 0; t < kMaxVecPerLane; ++t) {
+        const int v = lane + 32 * t;
+        if (v < nv) {
+          float4 x[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = reinterpret_cast<const float4*>(h_in + (long long)c[q] * d)[v];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[t] = f4_fmadd_rn(acc[t], w[q], x[q]);
+        }
+      }
+    }
+    for (; e < e1; ++e) {
+      const int c0 = col[e];
+      const float w0 = kKind == kKindSAGE ? cs : gcn_coef(dd, src_deg[c0]);
+#pragma unroll
+      for (int t = 0; t < kMaxVecPerLane; ++t) {
+        const int v = lane + 32 * t;
+        if (v < nv) acc[t] = f4_fmadd_rn(acc[t], w0, reinterpret_cast<const float4*>(h_in + (long long)c0 * d)[v]);
+      }
+    }
+    float* arow = A + (long long)i * ldA;
+    const float4* hs = reinterpret_cast<const float4*>(h_in + (long long)r * d);
+#pragma unroll
+    for (int t = 0; t < kMaxVecPerLane; ++t) {
+      const int v = lane + 32 * t;
+      if (v < nv) {
+        if (kKind == kKindSAGE) {
+          reinterpret_cast<float4*>(arow)[v] = hs[v];
+          reinterpret_cast<float4*>(arow + d)[v] = acc[t];
+        } else {
+          const float ws = gcn_coef(dd, src_deg[r]);
+          reinterpret_cast<float4*>(arow)[v] = f4_fmadd_rn(acc[t], ws, hs[v]);
+        }
+      }
+    }
+    if (lane == 0) reinterpret_cast<float4*>(arow + K)[0] = make_float4(1.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__global__ void k_scatter_rows(const int32_t* R_dev, const int32_t* __restrict__ rows, const float* __restrict__ Z,
+                               int dout, int relu, float* __restrict__ h_out) {
+  const long long n = (long long)(*R_dev) * dout;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / dout), j = (int)(t - (long long)i * dout);
+    float z = Z[t];
+    if (relu) z = z > 0.f ? z : 0.f;
+    h_out[(long long)rows[i] * dout + j] = z;
+  }
+}
+
+__global__ void k_inject(const int32_t* n_dev, const uint8_t* __restrict__ flag, const int32_t* __restrict__ hit_row,
+                         const float* __restrict__ table, int dim, float* __restrict__ h_out) {
+  const int n = *n_dev;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+    if (!flag[r]) continue;
+    const float* src = table + (long long)hit_row[r] * dim;
+    float* dst = h_out + (long long)r * dim;
+    for (int j = lane; j < dim; j += 32) dst[j] = src[j];
+  }
+}
+
+// one warp per seed row; fp64 throughout like the reference
+__global__ void k_ce_rows(const float* __restrict__ logits, const int32_t* __restrict__ labels, int B, int C,
+                          float* __restrict__ dlogits, double* __restrict__ row_logp) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < B; i += warps) {
+    const float* z = logits + (long long)i * C;
+    double m = -INFINITY;
+    for (int j = lane; j < C; j += 32) m = fmax(m, (double)z[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    double s = 0.0;
+    for (int j = lane; j < C; j += 32) s += exp((double)z[j] - m);
+    s = warp_sum_fixed(s);
+    const double lse = log(s);
+    const int y = labels[i];
+    for (int j = lane; j < C; j += 32) {
+      const double lp = ((double)z[j] - m) - lse;
+      double g = exp(lp);
+      if (j == y) {
+        g -= 1.0;
+        row_logp[i] = lp;
+      }
+      dlogits[(long long)i * C + j] = (float)(g / (double)B);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_ce_loss(const double* __restrict__ row_logp, int B, double* loss) {
+  __shared__ double part[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) s += row_logp[i];
+  s = warp_sum_fixed(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.0;
+    t = warp_sum_fixed(t);
+    if (threadIdx.x == 0) *loss = -t / (double)B;
+  }
+}
+
+__global__ void k_gather_dz(const int32_t* R_dev, const int32_t* __restrict__ rows, const float* __restrict__ d_h,
+                            const float* __restrict__ h_out, int dout, int relu, float* __restrict__ dz) {
+  const long long n = (long long)(*R_dev) * dout;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / dout), j = (int)(t - (long long)i * dout);
+    const long long src = (long long)rows[i] * dout + j;
+    float g = d_h[src];
+    if (relu && !(h_out[src] > 0.f)) g = 0.f;
+    dz[t] = g;
+  }
+}
+
+// CSC keys over the block's original edge extents: surviving edges keep their
+// source column, pruned rows' edges (and the tail up to E_max) get the sentinel.
+__global__ void k_csc_keys(const int32_t* n_dst_dev, const int32_t* __restrict__ blk_off,
+                           const uint8_t* __restrict__ keep, const int32_t* __restrict__ pos_of,
+                           const int32_t* __restrict__ col, long long E_max, unsigned sentinel,
+                           unsigned* __restrict__ keys, unsigned* __restrict__ vals) {
+  const int n = *n_dst_dev;
+  const long long E = blk_off[n];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long str = (long long)gridDim.x * blockDim.x;
+  for (long long r = tid; r < n; r += str) {
+    const bool k = keep[r];
+    const unsigned p = (unsigned)pos_of[r];
+    for (int e = blk_off[r]; e < blk_off[r + 1]; ++e) {
+      keys[e] = k ? (unsigned)col[e] : sentinel;
+      vals[e] = p;
+    }
+  }
+  for (long long e = E + tid; e < E_max; e += str) {
+    keys[e] = sentinel;
+    vals[e] = 0u;
+  }
+}
+
+__global__ void k_csc_segments(const unsigned* __restrict__ keys, long long E_max, unsigned sentinel,
+                               int32_t* __restrict__ seg_lo, int32_t* __restrict__ seg_hi) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < E_max;
+       p += (long long)gridDim.x * blockDim.x) {
+    const unsigned k = keys[p];
+    if (k == sentinel) continue;
+    if (p == 0 || keys[p - 1] != k) seg_lo[k] = (int32_t)p;
+    if (p == E_max - 1 || keys[p + 1] != k) seg_hi[k] = (int32_t)(p + 1);
+  }
+}
+
+// d_in rows for the live sources of block l + their fp64 norms (one warp per source)
+template <int kKind>
+__global__ void __launch_bounds__(256) k_transpose_agg(
+    const int32_t* n_live_dev, const int32_t* __restrict__ live, const int32_t* __restrict__ seg_lo,
+    const int32_t* __restrict__ seg_hi, const unsigned* __restrict__ srt_vals, const int32_t* __restrict__ rows,
+    const int32_t* __restrict__ start, const int32_t* __restrict__ end, const int32_t* __restrict__ dst_deg,
+    const int32_t* __restrict__ src_deg, const int32_t* n_dst_dev, const int32_t* __restrict__ pos_of,
+    const float* __restrict__ SG, int ldSG, int d, float* __restrict__ d_in, double* __restrict__ norms) {
+  const int n = *n_live_dev;
+  const int n_dst = *n_dst_dev;
+  const int lane = threadIdx.x & 31;
+  const int nv = d >> 2;
+  const int goff = kKind == kKindSAGE ? d : 0;  // neighbour half of [S | G]
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const int c = live[i];
+    float4 acc[kMaxVecPerLane];
+#pragma unroll
+    for (int t = 0; t < kMaxVecPerLane; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int p0 = seg_lo[c], p1 = seg_hi[c];
+    const int sd = kKind == kKindGCN ? src_deg[c] : 0;
+    for (int p = p0; p < p1; ++p) {
+      const int pos = (int)srt_vals[p];
+      const int r = rows[pos];
+      float w;
+      if (kKind == kKindSAGE) {
+        const int cnt = end[r] - start[r];
+        w = (float)(1.0 / (double)cnt);
+      } else {
+        w = gcn_coef(dst_deg[r], sd);
+      }
+      const float4* g = reinterpret_cast<const float4*>(SG + (long long)pos * ldSG + goff);
+#pragma unroll
+      for (int t = 0; t < kMaxVecPerLane; ++t) {
+        const int v = lane + 32 * t;
+        if (v < nv) acc[t] = f4_fmadd_rn(acc[t], w, g[v]);
+      }
+    }
+    const int self = c < n_dst ? pos_of[c] : -1;
+    if (self >= 0) {
+      const float4* s = reinterpret_cast<const float4*>(SG + (long long)self * ldSG);
+      const float ws = kKind == kKindSAGE ? 1.f : gcn_coef(dst_deg[c], sd);
+#pragma unroll
+      for (int t = 0; t < kMaxVecPerLane; ++t) {
+        const int v = lane + 32 * t;
+        if (v < nv) {
+          if (kKind == kKindSAGE) {
+            const float4 x = s[v];
+            acc[t] = make_float4(__fadd_rn(acc[t].x, x.x), __fadd_rn(acc[t].y, x.y), __fadd_rn(acc[t].z, x.z),
+                                 __fadd_rn(acc[t].w, x.w));
+          } else {
+            acc[t] = f4_fmadd_rn(acc[t], ws, s[v]);
+          }
+        }
+      }
+    }
+    double sq = 0.0;
+    float4* out = reinterpret_cast<float4*>(d_in + (long long)c * d);
+#pragma unroll
+    for (int t = 0; t < kMaxVecPerLane; ++t) {
+      const int v = lane + 32 * t;
+      if (v < nv) {
+        out[v] = acc[t];
+        sq += (double)acc[t].x * acc[t].x + (double)acc[t].y * acc[t].y + (double)acc[t].z * acc[t].z +
+              (double)acc[t].w * acc[t].w;
+      }
+    }
+    sq = warp_sum_fixed(sq);
+    if (lane == 0) norms[i] = sqrt(sq);
+  }
+}
+
+__global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, long long n, float eta) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = __fsub_rn(p[i], __fmul_rn(eta, g[i]));
+}
+
+// row norms of arbitrary fp32 rows (API node_grad_norms)
+__global__ void k_row_norms(const float* __restrict__ x, long long n, int d, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    double s = 0.0;
+    for (int j = lane; j < d; j += 32) {
+      const double v = x[i * d + j];
+      s += v * v;
+    }
+    s = warp_sum_fixed(s);
+    if (lane == 0) out[i] = sqrt(s);
+  }
+}
+
+}  // namespace
+}  // namespace hg
+
+using namespace hg;
+
+extern "C" {
+
+int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
+                     const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
+                     const float* h_in, int d, float* A, int ldA, cudaStream_t stream) {
+  const char* W = "hg_aggregate_fwd";
+  if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 512");
+  const int K = kind == kKindSAGE ? 2 * d : d;
+  if (ldA != K + 4) return fail(W, kBadArg, "ldA must be K + 4");
+  const unsigned grid = grid_for(R_max * 32, 256, 148 * 16);
+  if (kind == kKindSAGE)
+    k_aggregate<kKindSAGE><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, A, ldA);
+  else
+    k_aggregate<kKindGCN><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, A, ldA);
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+int hg_scatter_rows(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* Z, int dout, int relu,
+                    float* h_out, cudaStream_t stream) {
+  k_scatter_rows<<<grid_for(R_max * dout, 256), 256, 0, stream>>>(R_dev, rows, Z, dout, relu, h_out);
+  HG_LAUNCHED("hg_scatter_rows");
+  return kOk;
+}
+
+int hg_inject_rows(const int32_t* n_dev, long long n_max, const uint8_t* flag, const int32_t* hit_row,
+                   const float* table, int dim, float* h_out, cudaStream_t stream) {
+  k_inject<<<grid_for(n_max * 32, 256, 148 * 16), 256, 0, stream>>>(n_dev, flag, hit_row, table, dim, h_out);
+  HG_LAUNCHED("hg_inject_rows");
+  return kOk;
+}
+
+int hg_cross_entropy(const float* logits, const int32_t* labels, int B, int C, float* dlogits, double* row_logp,
+                     double* loss, cudaStream_t stream) {
+  if (B < 1 || C < 1) return fail("hg_cross_entropy", kBadArg, "empty logits");
+  k_ce_rows<<<grid_for((long long)B * 32, 256, 148 * 16), 256, 0, stream>>>(logits, labels, B, C, dlogits, row_logp);
+  HG_LAUNCHED("hg_cross_entropy");
+  k_ce_loss<<<1, 1024, 0, stream>>>(row_logp, B, loss);
+  HG_LAUNCHED("hg_cross_entropy");
+  return kOk;
+}
+
+int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* d_h, const float* h_out,
+                 int dout, int relu, float* dz, cudaStream_t stream) {
+  k_gather_dz<<<grid_for(R_max * dout, 256), 256, 0, stream>>>(R_dev, rows, d_h, h_out, dout, relu, dz);
+  HG_LAUNCHED("hg_gather_dz");
+  return kOk;
+}
+
+long long hg_csc_scratch_bytes(long long E_max) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                  (const unsigned*)nullptr, (unsigned*)nullptr, (int)(E_max > 0 ? E_max : 1), 0, 32);
+  // keys_in, vals_in, keys_out, vals_out + cub temp
+  return (long long)(4 * 4 * (E_max + 16)) + (long long)tmp + 1024;
+}
+
+// Transposed (CSC) view of the surviving edges of a pruned block, sorted by
+// source column (stable: ascending dst-row order inside every segment).
+int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t* keep, const int32_t* pos_of,
+                 const int32_t* col, long long E_max, long long n_src_max, unsigned* keys_sorted,
+                 unsigned* vals_sorted, int32_t* seg_lo, int32_t* seg_hi, void* scratch, long long scratch_bytes,
+                 cudaStream_t stream) {
+  const char* W = "hg_build_csc";
+  if (scratch_bytes < hg_csc_scratch_bytes(E_max)) return fail(W, kBadArg, "scratch too small");
+  unsigned* keys_in = reinterpret_cast<unsigned*>(scratch);
+  unsigned* vals_in = keys_in + (E_max + 16);
+  void* tmp = vals_in + (E_max + 16);
+  size_t tmp_bytes = (size_t)(scratch_bytes - 2 * 4 * (E_max + 16));
+  const unsigned sentinel = (unsigned)n_src_max;
+  int bits = 1;
+  while ((1ll << bits) <= (long long)sentinel) ++bits;
+  HG_CHECK_CUDA(W, cudaMemsetAsync(seg_lo, 0, (size_t)n_src_max * 4, stream));
+  HG_CHECK_CUDA(W, cudaMemsetAsync(seg_hi, 0, (size_t)n_src_max * 4, stream));
+  if (E_max == 0) return kOk;
+  k_csc_keys<<<grid_for(E_max, 256), 256, 0, stream>>>(n_dst_dev, blk_off, keep, pos_of, col, E_max, sentinel,
+                                                       keys_in, vals_in);
+  HG_LAUNCHED(W);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_sorted, vals_in, vals_sorted,
+                                                  (int)E_max, 0, bits, stream);
+  if (e != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(e));
+  k_csc_segments<<<grid_for(E_max, 256), 256, 0, stream>>>(keys_sorted, E_max, sentinel, seg_lo, seg_hi);
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
+                     const int32_t* seg_lo, const int32_t* seg_hi, const unsigned* vals_sorted, const int32_t* rows,
+                     const int32_t* start, const int32_t* end, const int32_t* dst_deg, const int32_t* src_deg,
+                     const int32_t* n_dst_dev, const int32_t* pos_of, const float* SG, int ldSG, int d,
+                     float* d_in, double* norms, cudaStream_t stream) {
+  const char* W = "hg_transpose_agg";
+  if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 512");
+  const unsigned grid = grid_for(n_live_max * 32, 256, 148 * 16);
+  if (kind == kKindSAGE)
+    k_transpose_agg<kKindSAGE><<<grid, 256, 0, stream>>>(n_live_dev, live, seg_lo, seg_hi, vals_sorted, rows, start,
+                                                         end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d,
+                                                         d_in, norms);
+  else
+    k_transpose_agg<kKindGCN><<<grid, 256, 0, stream>>>(n_live_dev, live, seg_lo, seg_hi, vals_sorted, rows, start,
+                                                        end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d, d_in,
+                                                        norms);
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+int hg_sgd(float* params, const float* grads, long long n, float eta, cudaStream_t stream) {
+  k_sgd<<<grid_for(n, 256), 256, 0, stream>>>(params, grads, n, eta);
+  HG_LAUNCHED("hg_sgd");
+  return kOk;
+}
+
+int hg_row_norms(const float* x, long long n, int d, double* out, cudaStream_t stream) {
+  k_row_norms<<<grid_for(n * 32, 256, 148 * 16), 256, 0, stream>>>(x, n, d, out);
+  HG_LAUNCHED("hg_row_norms");
+  return kOk;
+}
+
+}  // extern "C"

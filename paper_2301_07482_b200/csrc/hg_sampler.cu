@@ -1,0 +1,370 @@
+// K1 + K2: one layer of the layered fan-out sampler, bit-exact with
+// histgnn/sampler.py:118-163 (see oracle/sampling.py for the restatement).
+//
+// Per layer (frontier F rows, device-side counts):
+//   k_stamp     g2l[frontier[i]] = epoch<<32 | i ; src_out[i] = frontier[i]
+//   scan        (deg, min(deg,fanout)) -> cand_off (PCG stream offsets), blk_off
+//   k_select    one warp per frontier row: jump the PCG64 stream to the row's
+//               first candidate, draw one 53-bit key per candidate in-edge,
+//               keep the `fanout` smallest (key, position) pairs with a
+//               ballot-filtered warp bitonic merge, emit the global sources in
+//               key order and mark non-frontier sources in a node bitmap
+//   bitmap scan sorted-unique "new" nodes fall out of the bitmap in id order:
+//               popcount scan -> src_out[F + rank], g2l[new] = epoch<<32 | F+rank,
+//               the bitmap is cleared as it is consumed
+//   k_relabel   col_local[e] = low32(g2l[src_flat[e]])
+// No O(N) memset per call: g2l entries are epoch-stamped, the bitmap is
+// self-clearing.
+#include "hgb200.h"
+#include "hg_pcg.cuh"
+#include "hg_scan.cuh"
+
+namespace hg {
+
+__device__ JumpTable g_jump;
+
+namespace {
+
+struct KeyJ {
+  unsigned long long k;
+  unsigned j;
+};
+
+__device__ __forceinline__ bool kj_less(unsigned long long ak, unsigned aj, unsigned long long bk, unsigned bj) {
+  return ak < bk || (ak == bk && aj < bj);
+}
+
+__device__ __forceinline__ void cmpx(unsigned long long& k, unsigned& j, int partner_mask, bool keep_min) {
+  unsigned long long pk = __shfl_xor_sync(0xffffffffu, k, partner_mask);
+  unsigned pj = __shfl_xor_sync(0xffffffffu, j, partner_mask);
+  bool p_less = kj_less(pk, pj, k, j);
+  bool s_less = kj_less(k, j, pk, pj);
+  if (keep_min ? p_less : s_less) {
+    k = pk;
+    j = pj;
+  }
+}
+
+// ascending bitonic sort of 32 (key, j) pairs held one per lane
+__device__ __forceinline__ void bitonic_sort32(unsigned long long& k, unsigned& j) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      bool ascending = (lane & size) == 0 || size == 32;
+      bool lower = (lane & stride) == 0;
+      cmpx(k, j, stride, lower == ascending);
+    }
+  }
+}
+
+// ascending bitonic merge of a bitonic sequence of 32
+__device__ __forceinline__ void bitonic_merge32(unsigned long long& k, unsigned& j) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) cmpx(k, j, stride, (lane & stride) == 0);
+}
+
+struct DegCount {
+  const int64_t* g_start;
+  const int64_t* g_end;
+  const int32_t* frontier;
+  int fanout;
+  __device__ I64x2 operator()(long long i) const {
+    int v = frontier[i];
+    long long d = g_end[v] - g_start[v];
+    return {d, d < fanout ? d : (long long)fanout};
+  }
+};
+
+struct EmitDegCount {
+  int64_t* cand_off;
+  int32_t* blk_off;
+  int32_t* blk_end;
+  int32_t* dst_deg;
+  int fanout;
+  const int64_t* g_start;
+  const int64_t* g_end;
+  const int32_t* frontier;
+  __device__ void operator()(long long i, I64x2 excl, I64x2 v) const {
+    cand_off[i] = excl.a;
+    blk_off[i] = (int32_t)excl.b;
+    blk_end[i] = (int32_t)(excl.b + v.b);
+    dst_deg[i] = (int32_t)v.b;
+  }
+};
+
+struct TotalDegCount {
+  const int32_t* F_dev;
+  int64_t* cand_off;
+  int32_t* blk_off;
+  int32_t* counts_dev;
+  __device__ void operator()(I64x2 t) const {
+    int F = *F_dev;
+    cand_off[F] = t.a;
+    blk_off[F] = (int32_t)t.b;
+    counts_dev[0] = (int32_t)t.b;  // E
+  }
+};
+
+__global__ void k_stamp(const int32_t* __restrict__ frontier, const int32_t* F_dev, unsigned epoch,
+                        int64_t* __restrict__ g2l, int32_t* __restrict__ src_out) {
+  const int F = *F_dev;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
+    int v = frontier[i];
+    g2l[v] = (int64_t)(((unsigned long long)epoch << 32) | (unsigned)i);
+    src_out[i] = v;
+  }
+}
+
+constexpr int kSelThreads = 256;
+
+template <bool kSmallFanout>
+__global__ void __launch_bounds__(kSelThreads) k_select(
+    const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end, const int32_t* __restrict__ g_col,
+    const int32_t* __restrict__ frontier, const int32_t* F_dev, int fanout, u128 s0, u128 inc,
+    const unsigned long long* stream_pos, const int64_t* __restrict__ cand_off,
+    const int32_t* __restrict__ blk_off, unsigned epoch, const int64_t* __restrict__ g2l,
+    uint32_t* __restrict__ bitmap, int32_t* __restrict__ src_flat) {
+  __shared__ JumpTable tab;
+  {
+    const u128* srcA = &g_jump.A[0][0];
+    u128* dstA = &tab.A[0][0];
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) {
+      dstA[t] = srcA[t];
+      (&tab.S[0][0])[t] = (&g_jump.S[0][0])[t];
+    }
+  }
+  __syncthreads();
+  const int F = *F_dev;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const unsigned long long base0 = *stream_pos;
+  const u128 a32 = tab.A[1][2];            // MULT^32
+  const u128 c32 = mul128(inc, tab.S[1][2]);
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < F; row += warps) {
+    const int v = frontier[row];
+    const long long lo = g_start[v];
+    const long long deg = g_end[v] - lo;
+    const int out0 = blk_off[row];
+    const int count = (int)(deg < fanout ? deg : fanout);
+    if (deg == 0) continue;
+    const unsigned long long k0 = base0 + (unsigned long long)cand_off[row];
+    // lane state: output index k0+lane needs k0+lane+1 steps
+    const u128 first = pcg_jump(tab, s0, inc, k0 + (unsigned long long)lane + 1ull);
+    unsigned long long pick_k;
+    unsigned pick_j;
+    if (kSmallFanout) {
+      unsigned long long bk = ~0ull;
+      unsigned bj = ~0u;
+      u128 s = first;
+      for (long long c = 0; c < deg; c += 32) {
+        const long long jj = c + lane;
+        const bool valid = jj < deg;
+        unsigned long long key = valid ? pcg_key53(s) : ~0ull;
+        unsigned j = valid ? (unsigned)jj : ~0u;
+        if (c + 32 < deg) s = fma128(a32, s, c32);
+        const unsigned long long tk = __shfl_sync(0xffffffffu, bk, fanout - 1);
+        const unsigned tj = __shfl_sync(0xffffffffu, bj, fanout - 1);
+        if (!__ballot_sync(0xffffffffu, valid && kj_less(key, j, tk, tj))) continue;
+        bitonic_sort32(key, j);
+        unsigned long long rk = __shfl_sync(0xffffffffu, key, 31 - lane);
+        unsigned rj = __shfl_sync(0xffffffffu, j, 31 - lane);
+        if (kj_less(rk, rj, bk, bj)) {
+          bk = rk;
+          bj = rj;
+        }
+        bitonic_merge32(bk, bj);
+      }
+      pick_k = bk;
+      pick_j = bj;
+      if (lane < count) {
+        const int u = g_col[lo + pick_j];
+        src_flat[out0 + lane] = u;
+        if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
+      }
+    } else {
+      // generic fanout: repeated warp-min selection (O(count * deg / 32))
+      unsigned long long pk = 0;
+      unsigned pj = 0;
+      bool have_prev = false;
+      for (int r = 0; r < count; ++r) {
+        unsigned long long bk = ~0ull;
+        unsigned bj = ~0u;
+        u128 s = first;
+        for (long long c = 0; c < deg; c += 32) {
+          const long long jj = c + lane;
+          if (jj < deg) {
+            unsigned long long key = pcg_key53(s);
+            unsigned j = (unsigned)jj;
+            bool after = !have_prev || kj_less(pk, pj, key, j);
+            if (after && kj_less(key, j, bk, bj)) {
+              bk = key;
+              bj = j;
+            }
+          }
+          if (c + 32 < deg) s = fma128(a32, s, c32);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+          unsigned oj = __shfl_xor_sync(0xffffffffu, bj, o);
+          if (kj_less(ok, oj, bk, bj)) {
+            bk = ok;
+            bj = oj;
+          }
+        }
+        pk = bk;
+        pj = bj;
+        have_prev = true;
+        if (lane == 0) {
+          const int u = g_col[lo + pj];
+          src_flat[out0 + r] = u;
+          if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
+        }
+      }
+      (void)pick_k;
+      (void)pick_j;
+    }
+  }
+}
+
+struct PopWord {
+  const uint32_t* bitmap;
+  __device__ int operator()(long long i) const { return __popc(bitmap[i]); }
+};
+
+struct EmitNew {
+  uint32_t* bitmap;
+  const int32_t* F_dev;
+  unsigned epoch;
+  int64_t* g2l;
+  int32_t* src_out;
+  __device__ void operator()(long long w, int excl, int v) const {
+    if (!v) return;
+    uint32_t bits = bitmap[w];
+    const int pos0 = *F_dev + excl;
+    int r = 0;
+    while (bits) {
+      int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int id = (int)(w * 32 + b);
+      const int pos = pos0 + r++;
+      src_out[pos] = id;
+      g2l[id] = (int64_t)(((unsigned long long)epoch << 32) | (unsigned)pos);
+    }
+    bitmap[w] = 0u;
+  }
+};
+
+struct TotalNew {
+  const int32_t* F_dev;
+  int32_t* counts_dev;
+  unsigned long long* stream_pos;
+  const int64_t* cand_off;
+  __device__ void operator()(int t) const {
+    const int F = *F_dev;
+    counts_dev[1] = F + t;  // n_src of this block = next frontier size
+    *stream_pos += (unsigned long long)cand_off[F];
+  }
+};
+
+__global__ void k_relabel(const int32_t* __restrict__ src_flat, const int32_t* counts_dev,
+                          const int64_t* __restrict__ g2l, int32_t* __restrict__ col_local) {
+  const int E = counts_dev[0];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x)
+    col_local[e] = (int32_t)(g2l[src_flat[e]] & 0xffffffffll);
+}
+
+}  // namespace
+
+int ensure_jump_table() {
+  static int done_dev = -1;
+  int dev = 0;
+  HG_CHECK_CUDA("jump_table", cudaGetDevice(&dev));
+  if (done_dev == dev) return kOk;
+  JumpTable* h = new JumpTable;
+  const unsigned __int128 mult = ((unsigned __int128)kMultHi << 64) | kMultLo;
+  unsigned __int128 base = mult;  // MULT^(16^w)
+  unsigned __int128 base_s = 1;   // S for m = 16^w
+  for (int w = 0; w < 16; ++w) {
+    unsigned __int128 a = 1, s = 0;  // map for m = d*16^w, accumulated
+    for (int d = 0; d < 16; ++d) {
+      h->A[w][d] = {(unsigned long long)(a >> 64), (unsigned long long)a};
+      h->S[w][d] = {(unsigned long long)(s >> 64), (unsigned long long)s};
+      // compose one more base step: x -> base*x + base_s  (after current map)
+      s = base * s + base_s;
+      a = base * a;
+    }
+    // next window base: apply base 16 times
+    unsigned __int128 na = 1, ns = 0;
+    for (int d = 0; d < 16; ++d) {
+      ns = base * ns + base_s;
+      na = base * na;
+    }
+    base = na;
+    base_s = ns;
+  }
+  cudaError_t e = cudaMemcpyToSymbol(g_jump, h, sizeof(JumpTable));
+  delete h;
+  if (e != cudaSuccess) return fail("jump_table", kCuda, cudaGetErrorString(e));
+  done_dev = dev;
+  return kOk;
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+extern "C" {
+
+long long hg_sample_layer_scratch_bytes(long long F_max, long long num_nodes) {
+  long long words = (num_nodes + 31) / 32;
+  return (scan_tiles(F_max) + 1) * (long long)sizeof(I64x2) + (scan_tiles(words) + 1) * 4 + 256;
+}
+
+int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t* g_col, long long num_nodes,
+                    const int32_t* frontier, const int32_t* F_dev, long long F_max, int fanout,
+                    unsigned long long st_hi, unsigned long long st_lo, unsigned long long inc_hi,
+                    unsigned long long inc_lo, unsigned long long* stream_pos_dev, unsigned epoch, int64_t* g2l,
+                    uint32_t* bitmap, int64_t* cand_off, int32_t* blk_off, int32_t* blk_end, int32_t* dst_deg, int32_t* src_flat,
+                    int32_t* col_local, int32_t* src_out, int32_t* counts_dev, void* scratch,
+                    long long scratch_bytes, cudaStream_t stream) {
+  const char* W = "hg_sample_layer";
+  if (fanout < 1 || F_max < 1 || num_nodes < 1) return fail(W, kBadArg, "fanout, F_max and num_nodes must be >= 1");
+  if (scratch_bytes < hg_sample_layer_scratch_bytes(F_max, num_nodes)) return fail(W, kBadArg, "scratch too small");
+  int st = ensure_jump_table();
+  if (st) return st;
+  const long long words = (num_nodes + 31) / 32;
+  I64x2* part_dc = reinterpret_cast<I64x2*>(scratch);
+  int* part_w = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + (scan_tiles(F_max) + 1) * sizeof(I64x2));
+
+  k_stamp<<<grid_for(F_max, 256), 256, 0, stream>>>(frontier, F_dev, epoch, g2l, src_out);
+  HG_LAUNCHED(W);
+  DegCount f{g_start, g_end, frontier, fanout};
+  st = scan_launch<I64x2>(W, f, DevCount{F_dev}, F_max, part_dc,
+                          EmitDegCount{cand_off, blk_off, blk_end, dst_deg, fanout, g_start, g_end, frontier},
+                          TotalDegCount{F_dev, cand_off, blk_off, counts_dev}, stream);
+  if (st) return st;
+  const u128 s0{st_hi, st_lo}, inc{inc_hi, inc_lo};
+  const unsigned sel_grid = grid_for(F_max * 32, kSelThreads, 148 * 16);
+  if (fanout <= 32)
+    k_select<true><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, g_col, frontier, F_dev, fanout, s0, inc,
+                                                          stream_pos_dev, cand_off, blk_off, epoch, g2l, bitmap,
+                                                          src_flat);
+  else
+    k_select<false><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, g_col, frontier, F_dev, fanout, s0, inc,
+                                                           stream_pos_dev, cand_off, blk_off, epoch, g2l, bitmap,
+                                                           src_flat);
+  HG_LAUNCHED(W);
+  st = scan_launch<int>(W, PopWord{bitmap}, ConstCount{words}, words, part_w,
+                        EmitNew{bitmap, F_dev, epoch, g2l, src_out},
+                        TotalNew{F_dev, counts_dev, stream_pos_dev, cand_off}, stream);
+  if (st) return st;
+  k_relabel<<<grid_for(F_max * (long long)fanout, 256), 256, 0, stream>>>(src_flat, counts_dev, g2l, col_local);
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+}  // extern "C"

@@ -1,0 +1,430 @@
+"""Block GNN compute on the GPU (drop-in for histgnn/nn.py).
+
+Names and semantics follow the reference: `LayerKind` (nn.py:28-30),
+`LayerParams`/`Network` (:33-70), `init_network` (:73-85, host RNG so weights
+are bit-identical), `forward_pass` (:260-297), `backward` (:300-320),
+`cross_entropy` (:326-343), `node_grad_norms` (:346-349), `sgd_step`
+(:355-360). The work is done by hg_aggregate_fwd / hg_gemm_rm /
+hg_scatter_rows / hg_inject_rows / hg_gather_dz / hg_build_csc /
+hg_transpose_agg / hg_cross_entropy / hg_sgd.
+
+Parameters of all layers live in ONE flat fp32 device buffer (one gradient
+bucket for the data-parallel all-reduce); layer l occupies a
+[(K_l + 1) x d_out] row-major slab = [W_self ; W_neigh ; bias] (SAGE, K = 2 d_in)
+or [W ; bias] (GCN, K = d_in). `LayerParams` exposes reference-shaped views.
+
+Dead rows: rows of an output that are neither computed nor injected are not
+written on the device (no kernel reads them); numpy views of `h_layers` and
+node gradients fill them with zeros like the reference.
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .graphs import _np
+
+KIND_GCN, KIND_SAGE = 0, 1
+
+
+class LayerKind(enum.Enum):
+    GCN = "gcn"
+    SAGE_MEAN = "sage_mean"
+
+
+def _kind_code(kind: LayerKind) -> int:
+    return KIND_SAGE if kind is LayerKind.SAGE_MEAN else KIND_GCN
+
+
+@dataclass
+class LayerParams:
+    """Views into the flat parameter (or gradient) buffer."""
+
+    weight: torch.Tensor
+    bias: torch.Tensor
+    weight_neigh: torch.Tensor | None = None
+
+    def named_arrays(self):
+        pairs = [("weight", self.weight), ("bias", self.bias)]
+        if self.weight_neigh is not None:
+            pairs.append(("weight_neigh", self.weight_neigh))
+        return pairs
+
+    def numpy(self):
+        return {k: _np(v) for k, v in self.named_arrays()}
+
+
+def _slab_views(flat: torch.Tensor, kind: LayerKind, dims, offsets):
+    out = []
+    for l, (fi, fo) in enumerate(zip(dims[:-1], dims[1:])):
+        K = 2 * fi if kind is LayerKind.SAGE_MEAN else fi
+        slab = flat[offsets[l]:offsets[l] + (K + 1) * fo].view(K + 1, fo)
+        if kind is LayerKind.SAGE_MEAN:
+            out.append(LayerParams(slab[:fi], slab[K], slab[fi:K]))
+        else:
+            out.append(LayerParams(slab[:fi], slab[K], None))
+    return out
+
+
+def _offsets(kind, dims):
+    offs, o = [], 0
+    for fi, fo in zip(dims[:-1], dims[1:]):
+        K = 2 * fi if kind is LayerKind.SAGE_MEAN else fi
+        offs.append(o)
+        o += (K + 1) * fo
+    return offs, o
+
+
+@dataclass
+class Network:
+    kind: LayerKind
+    dims: list
+    flat: torch.Tensor                       # all parameters, fp32, device
+    offsets: list
+    layers: list = field(default_factory=list)
+
+    def __post_init__(self):
+        if not self.layers:
+            self.layers = _slab_views(self.flat, self.kind, self.dims, self.offsets)
+
+    @property
+    def num_layers(self) -> int:
+        return len(self.dims) - 1
+
+    @property
+    def dtype(self):
+        return np.float32
+
+    def slab(self, l: int) -> torch.Tensor:
+        fi, fo = self.dims[l], self.dims[l + 1]
+        K = 2 * fi if self.kind is LayerKind.SAGE_MEAN else fi
+        return self.flat[self.offsets[l]:self.offsets[l] + (K + 1) * fo].view(K + 1, fo)
+
+    def checksum_bytes(self) -> bytes:
+        """Same byte order as histgnn Network.checksum_bytes (nn.py:65-70)."""
+        return b"".join(np.ascontiguousarray(_np(a)).tobytes() for p in self.layers for _, a in p.named_arrays())
+
+    def new_grads(self) -> "Grads":
+        return Grads(self, torch.zeros_like(self.flat))
+
+
+@dataclass
+class Grads:
+    net: Network
+    flat: torch.Tensor
+
+    @property
+    def layers(self):
+        return _slab_views(self.flat, self.net.kind, self.net.dims, self.net.offsets)
+
+    def __getitem__(self, l):
+        return self.layers[l]
+
+    def __len__(self):
+        return self.net.num_layers
+
+    def slab(self, l):
+        fi, fo = self.net.dims[l], self.net.dims[l + 1]
+        K = 2 * fi if self.net.kind is LayerKind.SAGE_MEAN else fi
+        return self.flat[self.net.offsets[l]:self.net.offsets[l] + (K + 1) * fo].view(K + 1, fo)
+
+
+def init_network(kind: LayerKind, dims, rng: np.random.Generator, dtype=np.float32, device=None) -> Network:
+    """Glorot-uniform weights, zero biases (nn.py:73-85); host RNG, then upload."""
+    _lib.require_cuda()
+    if np.dtype(dtype) != np.float32:
+        raise ValueError("the device network computes in fp32")
+    dims = [int(d) for d in dims]
+    offs, total = _offsets(kind, dims)
+    host = np.zeros(total, dtype=np.float32)
+    for l, (fi, fo) in enumerate(zip(dims[:-1], dims[1:])):
+        s = np.sqrt(6.0 / (fi + fo))
+        w = rng.uniform(-s, s, size=(fi, fo)).astype(np.float32)
+        K = 2 * fi if kind is LayerKind.SAGE_MEAN else fi
+        slab = host[offs[l]:offs[l] + (K + 1) * fo].reshape(K + 1, fo)
+        slab[:fi] = w
+        if kind is LayerKind.SAGE_MEAN:
+            slab[fi:K] = rng.uniform(-s, s, size=(fi, fo)).astype(np.float32)
+    flat = torch.from_numpy(host).to(torch.device(device or "cuda"))
+    return Network(kind, dims, flat, offs)
+
+
+def network_from_numpy(kind: LayerKind, layers, device=None) -> Network:
+    """Pack reference-style per-layer arrays (weight, bias, weight_neigh)."""
+    dims = [layers[0]["weight"].shape[0]] + [p["weight"].shape[1] for p in layers]
+    offs, total = _offsets(kind, dims)
+    host = np.zeros(total, dtype=np.float32)
+    for l, p in enumerate(layers):
+        fi, fo = p["weight"].shape
+        K = 2 * fi if kind is LayerKind.SAGE_MEAN else fi
+        slab = host[offs[l]:offs[l] + (K + 1) * fo].reshape(K + 1, fo)
+        slab[:fi] = p["weight"]
+        slab[K] = p["bias"]
+        if kind is LayerKind.SAGE_MEAN:
+            slab[fi:K] = p["weight_neigh"]
+    return Network(kind, dims, torch.from_numpy(host).to(torch.device(device or "cuda")), offs)
+
+
+# ---------------------------------------------------------------- tapes
+
+
+@dataclass
+class LayerTape:
+    rows: torch.Tensor          # int32 [R] compute rows (sorted)
+    R: int
+    R_dev: torch.Tensor         # int32 [1]
+    A: torch.Tensor             # [R, K+4] GEMM operand (self|agg|1|pad)
+    K: int
+    relu: bool
+    h_out: torch.Tensor         # [n_dst, d_out] (dead rows unwritten)
+    valid_rows: torch.Tensor    # bool [n_dst] rows that hold data (computed or injected)
+
+
+@dataclass
+class BatchTape:
+    h_input: torch.Tensor
+    entries: list
+    h_layers: list              # device tensors (dead rows unwritten)
+
+    @property
+    def logits(self) -> torch.Tensor:
+        return self.h_layers[-1]
+
+    def h_layer_np(self, l: int) -> np.ndarray:
+        """Reference view of h_layers[l]: dead rows are zeros."""
+        h = self.h_layers[l]
+        valid = self.entries[l].valid_rows
+        return _np(torch.where(valid[:, None], h, torch.zeros((), dtype=h.dtype, device=h.device)))
+
+
+@dataclass
+class Injection:
+    """Rows of a block output served from a table instead of computed."""
+
+    flag: torch.Tensor          # uint8 [n_dst]
+    row: torch.Tensor           # int32 [n_dst] row in `table`
+    table: torch.Tensor         # [*, d_out] fp32
+    locals_dev: torch.Tensor | None = None
+
+
+def _dev_count(n: int, dev) -> torch.Tensor:
+    return torch.tensor([n], dtype=torch.int32, device=dev)
+
+
+def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch.Tensor, R: int,
+                      R_dev: torch.Tensor, act: bool, inj: Injection | None, stream) -> LayerTape:
+    dev = h_in.device
+    d_in = net.dims[l]
+    d_out = net.dims[l + 1]
+    if h_in.shape[0] != blk.num_src:
+        raise ValueError(f"h_in has {h_in.shape[0]} rows, frontier needs {blk.num_src}")
+    kind = _kind_code(net.kind)
+    K = 2 * d_in if kind == KIND_SAGE else d_in
+    ldA = K + 4
+    A = torch.empty((R, ldA), dtype=torch.float32, device=dev)
+    _lib.call("hg_aggregate_fwd", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(blk.adj.start),
+              _lib.ptr(blk.adj.end), _lib.ptr(blk.adj.col_indices), _lib.ptr(blk.dst_deg), _lib.ptr(blk.src_deg),
+              _lib.ptr(h_in), d_in, _lib.ptr(A), ldA, stream)
+    Z = torch.empty((R, d_out), dtype=torch.float32, device=dev)
+    _lib.call("hg_gemm_rm", 0, 0, R, d_out, K + 1, _lib.ptr(A), ldA, _lib.ptr(net.slab(l)), d_out, 0.0,
+              _lib.ptr(Z), d_out, stream)
+    n_dst = blk.num_dst
+    h_out = torch.empty((n_dst, d_out), dtype=torch.float32, device=dev)
+    _lib.call("hg_scatter_rows", _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(Z), d_out, int(act),
+              _lib.ptr(h_out), stream)
+    valid = torch.zeros(n_dst, dtype=torch.bool, device=dev)
+    if R:
+        valid[rows.long()] = True
+    if inj is not None:
+        _lib.call("hg_inject_rows", _lib.ptr(_dev_count(n_dst, dev)), n_dst, _lib.ptr(inj.flag),
+                  _lib.ptr(inj.row), _lib.ptr(inj.table), d_out, _lib.ptr(h_out), stream)
+        valid |= inj.flag.bool()
+    return LayerTape(rows, R, R_dev, A, K, act, h_out, valid)
+
+
+def _rows_tensor(rows, n_dst, dev):
+    if rows is None:
+        return torch.arange(n_dst, dtype=torch.int32, device=dev), n_dst
+    r = torch.as_tensor(np.asarray(rows if not isinstance(rows, torch.Tensor) else _np(rows), dtype=np.int64)
+                        .astype(np.int32), device=dev)
+    return r, int(r.shape[0])
+
+
+def _injection_from_values(inj, n_dst, d_out, dev) -> Injection | None:
+    if inj is None:
+        return None
+    loc = np.asarray(_np(inj[0]), dtype=np.int64)
+    if len(loc) == 0:
+        return None
+    vals = inj[1]
+    table = (vals if isinstance(vals, torch.Tensor) else torch.as_tensor(np.asarray(vals, np.float32)))
+    table = table.to(dev, torch.float32).contiguous()
+    flag = torch.zeros(n_dst, dtype=torch.uint8, device=dev)
+    row = torch.full((n_dst,), -1, dtype=torch.int32, device=dev)
+    li = torch.as_tensor(loc, device=dev)
+    flag[li] = 1
+    row[li] = torch.arange(len(loc), dtype=torch.int32, device=dev)
+    return Injection(flag, row, table)
+
+
+def forward_pass(network: Network, blocks, h_input, compute_rows=None, injected=None) -> BatchTape:
+    """Run all blocks; rows absent from compute_rows[l] are dead unless
+    injected[l] overwrites them. ReLU on every layer except the last.
+    injected[l] may be (locals, values) like the reference, or an Injection."""
+    if len(blocks) != network.num_layers:
+        raise ValueError("block count does not match network depth")
+    dev = network.flat.device
+    stream = _lib.stream_ptr()
+    h = h_input if isinstance(h_input, torch.Tensor) else torch.as_tensor(np.asarray(h_input, np.float32))
+    h = h.to(dev, torch.float32).contiguous()
+    ents, hs = [], []
+    h_prev = h
+    for l, blk in enumerate(blocks):
+        rows, R = _rows_tensor(None if compute_rows is None else compute_rows[l], blk.num_dst, dev)
+        inj = None if injected is None else injected[l]
+        if inj is not None and not isinstance(inj, Injection):
+            inj = _injection_from_values(inj, blk.num_dst, network.dims[l + 1], dev)
+        t = layer_forward_dev(network, l, blk, h_prev, rows, R, _dev_count(R, dev), l < network.num_layers - 1,
+                              inj, stream)
+        ents.append(t)
+        hs.append(t.h_out)
+        h_prev = t.h_out
+    return BatchTape(h, ents, hs)
+
+
+# --------------------------------------------------------------- backward
+
+
+@dataclass
+class BlockCsc:
+    vals: torch.Tensor
+    seg_lo: torch.Tensor
+    seg_hi: torch.Tensor
+
+
+def build_csc(blk, keep: torch.Tensor, pos_of: torch.Tensor, n_dst_dev, stream, scratch=None) -> BlockCsc:
+    dev = keep.device
+    E = blk.num_edges_built
+    n_src = blk.num_src
+    keys = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+    vals = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+    seg_lo = torch.empty(max(n_src, 1), dtype=torch.int32, device=dev)
+    seg_hi = torch.empty(max(n_src, 1), dtype=torch.int32, device=dev)
+    sb = _lib.query("hg_csc_scratch_bytes", E)
+    if scratch is None or scratch.numel() < sb:
+        scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+    _lib.call("hg_build_csc", _lib.ptr(n_dst_dev), _lib.ptr(blk.blk_off), _lib.ptr(keep), _lib.ptr(pos_of),
+              _lib.ptr(blk.adj.col_indices), E, n_src, _lib.ptr(keys), _lib.ptr(vals), _lib.ptr(seg_lo),
+              _lib.ptr(seg_hi), _lib.ptr(scratch), sb, stream)
+    return BlockCsc(vals, seg_lo, seg_hi)
+
+
+def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tensor, grads: Grads,
+                       need_input: bool, keep, pos_of, live, n_live, stream):
+    """Writes dP into grads; returns (d_in [n_src, d_in] with rows valid on
+    `live`, fp64 norms aligned with `live`) or (None, None)."""
+    dev = d_h.device
+    d_in_dim, d_out = net.dims[l], net.dims[l + 1]
+    R, K = t.R, t.K
+    dz = torch.empty((R, d_out), dtype=torch.float32, device=dev)
+    _lib.call("hg_gather_dz", _lib.ptr(t.R_dev), R, _lib.ptr(t.rows), _lib.ptr(d_h), _lib.ptr(t.h_out), d_out,
+              int(t.relu), _lib.ptr(dz), stream)
+    dP = grads.slab(l)
+    ldA = K + 4
+    _lib.call("hg_gemm_rm", 1, 0, K + 1, d_out, R, _lib.ptr(t.A), ldA, _lib.ptr(dz), d_out, 0.0,
+              _lib.ptr(dP), d_out, stream)
+    if not need_input:
+        return None, None
+    SG = torch.empty((R, K), dtype=torch.float32, device=dev)
+    _lib.call("hg_gemm_rm", 0, 1, R, K, d_out, _lib.ptr(dz), d_out, _lib.ptr(net.slab(l)), d_out, 0.0,
+              _lib.ptr(SG), K, stream)
+    n_dst_dev = _dev_count(blk.num_dst, dev)
+    csc = build_csc(blk, keep, pos_of, n_dst_dev, stream)
+    d_in = torch.empty((blk.num_src, d_in_dim), dtype=torch.float32, device=dev)
+    norms = torch.empty(max(n_live, 1), dtype=torch.float64, device=dev)
+    _lib.call("hg_transpose_agg", _kind_code(net.kind), _lib.ptr(_dev_count(n_live, dev)), n_live, _lib.ptr(live),
+              _lib.ptr(csc.seg_lo), _lib.ptr(csc.seg_hi), _lib.ptr(csc.vals), _lib.ptr(t.rows),
+              _lib.ptr(blk.adj.start), _lib.ptr(blk.adj.end), _lib.ptr(blk.dst_deg), _lib.ptr(blk.src_deg),
+              _lib.ptr(n_dst_dev), _lib.ptr(pos_of), _lib.ptr(SG), K, d_in_dim, _lib.ptr(d_in), _lib.ptr(norms),
+              stream)
+    return d_in, norms[:n_live]
+
+
+def _keep_pos(rows: torch.Tensor, R: int, n_dst: int, dev):
+    keep = torch.zeros(n_dst, dtype=torch.uint8, device=dev)
+    pos = torch.full((n_dst,), -1, dtype=torch.int32, device=dev)
+    if R:
+        keep[rows.long()] = 1
+        pos[rows.long()] = torch.arange(R, dtype=torch.int32, device=dev)
+    return keep, pos
+
+
+def backward(network: Network, blocks, tape: BatchTape, d_logits, need_input: bool = True):
+    """Reverse pass (nn.py:300-320). Returns (grads, node_grads, input_grad);
+    node_grads[l] = dL/dh_layers[l] for every dst row (device tensors, fully
+    materialised here, zeros where the reference has zeros)."""
+    dev = network.flat.device
+    stream = _lib.stream_ptr()
+    grads = network.new_grads()
+    L = network.num_layers
+    node_grads = [None] * L
+    d_h = d_logits if isinstance(d_logits, torch.Tensor) else torch.as_tensor(np.asarray(d_logits, np.float32))
+    d_h = d_h.to(dev, torch.float32).contiguous()
+    for l in range(L - 1, -1, -1):
+        node_grads[l] = d_h
+        t = tape.entries[l]
+        blk = blocks[l]
+        want = need_input or l > 0
+        keep, pos = _keep_pos(t.rows, t.R, blk.num_dst, dev)
+        live = torch.arange(blk.num_src, dtype=torch.int32, device=dev)
+        d_prev, _ = layer_backward_dev(network, l, blk, t, d_h, grads, want, keep, pos, live, blk.num_src, stream)
+        d_h = d_prev
+    return grads, node_grads, d_h
+
+
+def cross_entropy(logits, labels):
+    """Mean softmax cross entropy, fp64 (nn.py:326-343). Returns (loss, d_logits)."""
+    lab = np.asarray(labels)
+    if logits.shape[0] != len(lab):
+        raise ValueError("labels do not match logit rows")
+    if len(lab) and (lab.min() < 0 or lab.max() >= logits.shape[1]):
+        raise ValueError("label id out of range")
+    dev = logits.device if isinstance(logits, torch.Tensor) else torch.device("cuda")
+    z = logits if isinstance(logits, torch.Tensor) else torch.as_tensor(np.asarray(logits, np.float32), device=dev)
+    z = z.contiguous()
+    B, C = z.shape
+    labels_dev = torch.as_tensor(lab.astype(np.int32), device=dev)
+    d, loss = cross_entropy_dev(z, labels_dev, B, C, _lib.stream_ptr())
+    return float(loss.item()), d
+
+
+def cross_entropy_dev(z, labels_dev, B, C, stream):
+    dev = z.device
+    d = torch.empty((B, C), dtype=torch.float32, device=dev)
+    row = torch.empty(B, dtype=torch.float64, device=dev)
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    _lib.call("hg_cross_entropy", _lib.ptr(z), _lib.ptr(labels_dev), B, C, _lib.ptr(d), _lib.ptr(row),
+              _lib.ptr(loss), stream)
+    return d, loss
+
+
+def node_grad_norms(node_grads) -> torch.Tensor:
+    """Per-row Euclidean norms in fp64 (nn.py:346-349)."""
+    g = node_grads if isinstance(node_grads, torch.Tensor) else torch.as_tensor(np.asarray(node_grads, np.float32))
+    g = g.to(torch.device("cuda"), torch.float32).contiguous()
+    n, d = g.shape
+    out = torch.empty(n, dtype=torch.float64, device=g.device)
+    if n:
+        _lib.call("hg_row_norms", _lib.ptr(g), n, d, _lib.ptr(out), _lib.stream_ptr())
+    return out
+
+
+def sgd_step(network: Network, grads: Grads, eta: float) -> None:
+    """p -= float32(eta) * g over the whole flat buffer (nn.py:355-360)."""
+    _lib.call("hg_sgd", _lib.ptr(network.flat), _lib.ptr(grads.flat), network.flat.numel(),
+              float(np.float32(eta)), _lib.stream_ptr())

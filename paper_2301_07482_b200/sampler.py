@@ -1,0 +1,334 @@
+"""Layered fan-out sampling on the GPU (drop-in for histgnn/sampler.py).
+
+Same names, argument meaning and errors as the reference:
+`SamplePlan` (sampler.py:26-41), `LayerBlock` (:44-71), `LayeredSubgraph`
+(:74-92), `split_batches` (:95-101), `batch_rng` (:104-106),
+`sample_layered` (:166-190) and `SubgraphProducer` (:193-263).
+
+`sample_layered` runs one `hg_sample_layer` launch chain per fanout on the
+device. The caller's numpy Generator supplies the PCG64 state (host-side
+seeding, identical streams) and is advanced by exactly the number of draws the
+reference would have consumed, so callers that reuse one generator across
+calls see the same stream as with the reference. Blocks are bit-identical to
+the reference's (tests/test_gpu_sampler.py).
+"""
+
+from __future__ import annotations
+
+import queue
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .graphs import Csr2Graph, _np
+
+_DONE = object()
+_M64 = (1 << 64) - 1
+
+
+@dataclass(frozen=True)
+class SamplePlan:
+    """fanouts are listed outermost first: fanouts[0] expands the seeds."""
+
+    fanouts: tuple
+    batch_size: int
+    rng_seed: int = 0
+
+    def __post_init__(self):
+        object.__setattr__(self, "fanouts", tuple(int(f) for f in self.fanouts))
+        if len(self.fanouts) == 0:
+            raise ValueError("need at least one fanout")
+        if any(f < 1 for f in self.fanouts):
+            raise ValueError(f"all fanouts must be >= 1, got {self.fanouts}")
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
+
+
+@dataclass
+class LayerBlock:
+    """One bipartite block; device tensors (int32 local ids / offsets).
+
+    dst_nodes is a prefix view of src_nodes. `blk_off` keeps the build-time
+    row extents (pruning only touches adj.end)."""
+
+    dst_nodes: torch.Tensor
+    src_nodes: torch.Tensor
+    adj: Csr2Graph
+    dst_deg: torch.Tensor
+    src_deg: torch.Tensor = None
+    blk_off: torch.Tensor = field(default=None, repr=False)
+
+    @property
+    def num_dst(self) -> int:
+        return int(self.dst_nodes.shape[0])
+
+    @property
+    def num_src(self) -> int:
+        return int(self.src_nodes.shape[0])
+
+    @property
+    def num_edges_built(self) -> int:
+        return int(self.adj.col_indices.shape[0])
+
+    def copy(self) -> "LayerBlock":
+        return LayerBlock(self.dst_nodes, self.src_nodes, self.adj.copy(), self.dst_deg, self.src_deg,
+                          self.blk_off)
+
+    def record_stream(self, s):
+        for t in (self.src_nodes, self.adj.start, self.adj.end, self.adj.col_indices, self.dst_deg,
+                  self.src_deg, self.blk_off):
+            if t is not None:
+                t.record_stream(s)
+
+    def as_numpy(self) -> dict:
+        return {"dst": _np(self.dst_nodes).astype(np.int64), "src": _np(self.src_nodes).astype(np.int64),
+                "start": self.adj.start_np, "end": self.adj.end_np, "col": self.adj.col_np,
+                "dst_deg": _np(self.dst_deg).astype(np.int64),
+                "src_deg": _np(self.src_deg).astype(np.int64)}
+
+
+@dataclass
+class LayeredSubgraph:
+    """layers[0] is the innermost block; layers[-1].dst_nodes are the seeds."""
+
+    seeds: np.ndarray
+    layers: list
+
+    @property
+    def num_layers(self) -> int:
+        return len(self.layers)
+
+    @property
+    def input_nodes(self) -> torch.Tensor:
+        return self.layers[0].src_nodes
+
+    def copy(self) -> "LayeredSubgraph":
+        return LayeredSubgraph(self.seeds, [b.copy() for b in self.layers])
+
+    def record_stream(self, s):
+        for b in self.layers:
+            b.record_stream(s)
+
+
+def split_batches(ids, batch_size: int, rng: np.random.Generator) -> list:
+    """Host permutation, identical to the reference (sampler.py:95-101)."""
+    ids = np.asarray(ids, dtype=np.int64)
+    if batch_size < 1:
+        raise ValueError("batch_size must be >= 1")
+    perm = rng.permutation(ids)
+    return [perm[i:i + batch_size] for i in range(0, len(perm), batch_size)]
+
+
+def batch_rng(rng_seed: int, batch_index: int) -> np.random.Generator:
+    return np.random.default_rng(np.random.SeedSequence((int(rng_seed), int(batch_index))))
+
+
+class SamplerWorkspace:
+    """Per-sampler O(N) scratch: epoch-stamped global->local map and the
+    self-clearing node bitmap. One workspace serves one stream at a time."""
+
+    def __init__(self, num_nodes: int, device):
+        self.num_nodes = int(num_nodes)
+        self.device = device
+        self.g2l = torch.full((self.num_nodes,), -1, dtype=torch.int64, device=device)
+        self.bitmap = torch.zeros(((self.num_nodes + 31) // 32,), dtype=torch.int32, device=device)
+        self.stream_pos = torch.zeros(1, dtype=torch.int64, device=device)
+        self.epoch = 0
+        self.lock = threading.Lock()
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        if self.epoch >= 0xFFFFFFFE:  # never collide with the -1 fill
+            self.g2l.fill_(-1)
+            self.epoch = 1
+        return self.epoch
+
+
+_default_ws: dict = {}
+_default_ws_lock = threading.Lock()
+
+
+def default_workspace(g: Csr2Graph) -> SamplerWorkspace:
+    key = (id(g), g.col_indices.data_ptr())
+    with _default_ws_lock:
+        ws = _default_ws.get(key)
+        if ws is None:
+            ws = SamplerWorkspace(g.num_nodes, g.start.device)
+            _default_ws.clear()
+            _default_ws[key] = ws
+    return ws
+
+
+def _pcg_state(rng: np.random.Generator):
+    bg = rng.bit_generator
+    if not isinstance(bg, np.random.PCG64):
+        raise ValueError("sample_layered needs a PCG64-backed Generator (batch_rng / default_rng)")
+    st = bg.state
+    return int(st["state"]["state"]), int(st["state"]["inc"])
+
+
+def _advance(rng: np.random.Generator, draws: int) -> None:
+    """Consume exactly `draws` uniform doubles, like rng.random(draws)."""
+    if draws <= 0:
+        return
+    bg = rng.bit_generator
+    before = bg.state
+    bg.advance(draws)
+    after = bg.state
+    after["has_uint32"], after["uinteger"] = before["has_uint32"], before["uinteger"]
+    bg.state = after
+
+
+def sample_layered(g: Csr2Graph, seeds, plan: SamplePlan, rng: np.random.Generator, *,
+                   workspace: SamplerWorkspace | None = None, stream=None) -> LayeredSubgraph:
+    """Expand seeds through len(plan.fanouts) sampling blocks on the GPU."""
+    _lib.require_cuda()
+    seeds = np.asarray(seeds, dtype=np.int64)
+    if len(seeds) == 0:
+        raise ValueError("empty seed set")
+    if len(np.unique(seeds)) != len(seeds):
+        raise ValueError("seed ids must be unique")
+    if seeds.min() < 0 or seeds.max() >= g.num_nodes:
+        raise ValueError("seed id out of range")
+    ws = workspace or default_workspace(g)
+    dev = g.start.device
+    s = stream or torch.cuda.current_stream(dev)
+    state, inc = _pcg_state(rng)
+    N = g.num_nodes
+    with ws.lock, torch.cuda.stream(s):
+        sp = _lib.stream_ptr(s)
+        ws.stream_pos.zero_()
+        B = len(seeds)
+        frontier = torch.from_numpy(seeds.astype(np.int32)).pin_memory().to(dev, non_blocking=True)
+        F_dev = torch.tensor([B], dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
+        F_max = B
+        raw = []
+        for fanout in plan.fanouts:
+            E_max = max(1, F_max * fanout)
+            Fn_max = min(N, F_max + E_max)
+            cand_off = torch.empty(F_max + 1, dtype=torch.int64, device=dev)
+            blk_off = torch.empty(F_max + 1, dtype=torch.int32, device=dev)
+            blk_end = torch.empty(F_max, dtype=torch.int32, device=dev)
+            dst_deg = torch.empty(F_max, dtype=torch.int32, device=dev)
+            src_flat = torch.empty(E_max, dtype=torch.int32, device=dev)
+            col_local = torch.empty(E_max, dtype=torch.int32, device=dev)
+            src_out = torch.empty(Fn_max, dtype=torch.int32, device=dev)
+            counts = torch.zeros(4, dtype=torch.int32, device=dev)
+            sb = _lib.query("hg_sample_layer_scratch_bytes", F_max, N)
+            scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+            _lib.call("hg_sample_layer", _lib.ptr(g.start), _lib.ptr(g.end), _lib.ptr(g.col_indices), N,
+                      _lib.ptr(frontier), _lib.ptr(F_dev), F_max, fanout,
+                      (state >> 64) & _M64, state & _M64, (inc >> 64) & _M64, inc & _M64,
+                      _lib.ptr(ws.stream_pos), ws.next_epoch(), _lib.ptr(ws.g2l), _lib.ptr(ws.bitmap),
+                      _lib.ptr(cand_off), _lib.ptr(blk_off), _lib.ptr(blk_end), _lib.ptr(dst_deg),
+                      _lib.ptr(src_flat), _lib.ptr(col_local), _lib.ptr(src_out), _lib.ptr(counts),
+                      _lib.ptr(scratch), sb, sp)
+            raw.append((F_dev, blk_off, blk_end, dst_deg, col_local, src_out, counts))
+            frontier, F_dev, F_max = src_out, counts[1:2], Fn_max
+        # one host round trip per batch: all block sizes + the draw count
+        sizes = torch.cat([torch.stack([r[0][0] for r in raw]).to(torch.int64),
+                           torch.stack([r[6][0] for r in raw]).to(torch.int64),
+                           torch.stack([r[6][1] for r in raw]).to(torch.int64),
+                           ws.stream_pos]).cpu().tolist()
+    L = len(plan.fanouts)
+    n_dst, n_e, n_src, draws = sizes[:L], sizes[L:2 * L], sizes[2 * L:3 * L], sizes[3 * L]
+    _advance(rng, draws)
+    blocks = []
+    for li, (F_dev, blk_off, blk_end, dst_deg, col_local, src_out, counts) in enumerate(raw):
+        F, E, S = n_dst[li], n_e[li], n_src[li]
+        src_nodes = src_out[:S]
+        adj = Csr2Graph(blk_off[:F], blk_end[:F], col_local[:E], F)
+        blocks.append(LayerBlock(src_nodes[:F], src_nodes, adj, dst_deg[:F], None, blk_off[:F + 1]))
+    blocks.reverse()
+    for i, b in enumerate(blocks):
+        b.src_deg = (torch.zeros(b.num_src, dtype=torch.int32, device=dev) if i == 0
+                     else blocks[i - 1].dst_deg)
+    return LayeredSubgraph(seeds=seeds, layers=blocks)
+
+
+class SubgraphProducer:
+    """Samples batches on a worker thread (own CUDA stream + workspace) into a
+    bounded FIFO (sampler.py:193-263): at most `queue_capacity` finished
+    subgraphs plus one in flight; yields (batch_index, subgraph) in order;
+    close() stops the worker promptly."""
+
+    def __init__(self, graph, batches, plan: SamplePlan, queue_capacity: int = 2):
+        if queue_capacity < 1:
+            raise ValueError("queue_capacity must be >= 1")
+        self._graph = graph
+        self._batches = list(batches)
+        self._plan = plan
+        self._queue: queue.Queue = queue.Queue(maxsize=queue_capacity)
+        self._stop = threading.Event()
+        self._thread = threading.Thread(target=self._work, daemon=True)
+        self._started = False
+        self._error = None
+        self.batches_sampled = 0
+        self._device = graph.start.device
+        self._stream = torch.cuda.Stream(self._device)
+        self._ws = SamplerWorkspace(graph.num_nodes, self._device)
+
+    def _put(self, item) -> bool:
+        while not self._stop.is_set():
+            try:
+                self._queue.put(item, timeout=0.05)
+                return True
+            except queue.Full:
+                continue
+        return False
+
+    def _work(self):
+        try:
+            torch.cuda.set_device(self._device)
+            for idx, seeds in enumerate(self._batches):
+                if self._stop.is_set():
+                    return
+                sub = sample_layered(self._graph, seeds, self._plan, batch_rng(self._plan.rng_seed, idx),
+                                     workspace=self._ws, stream=self._stream)
+                ev = torch.cuda.Event()
+                ev.record(self._stream)
+                self.batches_sampled += 1
+                if not self._put((idx, sub, ev)):
+                    return
+        except BaseException as e:  # surface worker failures to the consumer
+            self._error = e
+        self._put(_DONE)
+
+    def start(self):
+        if not self._started:
+            self._started = True
+            self._thread.start()
+
+    def __iter__(self):
+        self.start()
+        while True:
+            item = self._queue.get()
+            if item is _DONE:
+                if self._error is not None:
+                    raise self._error
+                return
+            idx, sub, ev = item
+            cur = torch.cuda.current_stream(self._device)
+            cur.wait_event(ev)
+            sub.record_stream(cur)
+            yield idx, sub
+
+    def close(self):
+        self._stop.set()
+        if self._started:
+            while True:
+                try:
+                    self._queue.get_nowait()
+                except queue.Empty:
+                    break
+            self._thread.join(timeout=5.0)
+
+    def __enter__(self):
+        self.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -1,0 +1,400 @@
+"""Mini-batch training driver on the GPU (drop-in for histgnn/trainer.py).
+
+Keeps the reference API: `TrainConfig` (trainer.py:59-83), `IterMetrics`
+(:86-104), `write_metrics_csv`/`io_saving` (:110-123), `PrunedBatch`
+(:138-150), `prune_with_cache` (:166-207), `make_batches` (:277-282),
+`Trainer` (:285-433: `train_iteration`, `train`, `_load_input`) and
+`run_plain_loop` (:439-469). Every per-iteration byte moves through the
+hg_* kernels; the host keeps the integer policy decisions the reference makes
+once per run or per window (batch permutation, PCG64 seeding, cache capacity).
+
+Per iteration the host synchronises three times: after sampling (block
+sizes, RNG draw count), after the prune walk (compute/live counts, which size
+the GEMMs) and at the end (loss + counters for IterMetrics).
+"""
+
+from __future__ import annotations
+
+import csv
+import math
+from dataclasses import dataclass, fields
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._state import GCTR_FEATURE_HITS, GCTR_FEATURE_MISSES, LAYER_CTR_LEN, CTR_VALID
+from .cache import COUNTER_NAMES, CachePolicy, HistCache
+from .graphs import Csr2Graph, _np, csr2_from_arrays
+from .nn import (Injection, LayerKind, Network, backward, cross_entropy_dev, forward_pass, init_network,
+                 layer_backward_dev, layer_forward_dev, sgd_step, _dev_count)
+from .sampler import LayeredSubgraph, SamplePlan, SubgraphProducer, batch_rng, sample_layered, split_batches
+
+_NET_TAG = 16807
+_PERM_TAG = 1000000007
+
+
+def _network_rng(seed: int) -> np.random.Generator:
+    return np.random.default_rng(np.random.SeedSequence((seed, _NET_TAG)))
+
+
+def _perm_rng(seed: int, epoch: int) -> np.random.Generator:
+    return np.random.default_rng(np.random.SeedSequence((seed, _PERM_TAG, epoch)))
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    fanouts: tuple
+    hidden: int = 64
+    batch_size: int = 1024
+    epochs: int = 1
+    eta: float = 0.01
+    kind: LayerKind = LayerKind.GCN
+    p_grad: float = 0.9
+    t_stale: float = 20
+    capacity: int | None = None
+    feature_rows: int | None = None
+    refresh_retained: bool = False
+    seed: int = 0
+    probe_every: int = 0
+    probe_layer: int = 1
+    dtype: type = np.float32
+    # B200 additions (not in the reference): where the raw feature table lives
+    feature_placement: str = "hbm"      # "hbm" | "host" (pinned, read through UVA)
+
+    def __post_init__(self):
+        if len(self.fanouts) == 0 or any(f < 1 for f in self.fanouts):
+            raise ValueError("fanouts must be a non-empty tuple of positives")
+        if self.batch_size < 1 or self.epochs < 1 or self.hidden < 1:
+            raise ValueError("batch_size, epochs and hidden must be >= 1")
+        if not math.isfinite(self.eta):
+            raise ValueError("eta must be finite")
+        if self.probe_every:
+            raise ValueError("estimation probes are out of scope for the device trainer (probe_every=0)")
+        if self.feature_placement not in ("hbm", "host"):
+            raise ValueError("feature_placement must be 'hbm' or 'host'")
+
+
+@dataclass
+class IterMetrics:
+    iteration: int
+    epoch: int
+    num_seeds: int
+    loss: float
+    fetched_bytes: int
+    baseline_bytes: int
+    prune_writes: int
+    hits: int
+    misses: int
+    admissions: int
+    gradient_evictions: int
+    staleness_evictions: int
+    forced_evictions: int
+    feature_hits: int
+    feature_misses: int
+    valid_entries: int
+    estimation_error: float
+
+
+METRIC_FIELDS = [f.name for f in fields(IterMetrics)]
+
+
+def write_metrics_csv(path, metrics) -> None:
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(METRIC_FIELDS)
+        for m in metrics:
+            w.writerow([getattr(m, name) for name in METRIC_FIELDS])
+
+
+def io_saving(metrics) -> float:
+    base = sum(m.baseline_bytes for m in metrics)
+    if base == 0:
+        return 0.0
+    return 1.0 - sum(m.fetched_bytes for m in metrics) / base
+
+
+# ------------------------------------------------------ cache-aware pruning
+
+
+@dataclass
+class PrunedBatch:
+    """Device outcome of the cache walk. layer_live[l] / compute_rows[b] are
+    int32 device tensors; injected[b] is an Injection (flags + cache rows) or
+    None; keep/pos_of are the computed-row flags and positions per block."""
+
+    sub: LayeredSubgraph
+    compute_rows: list
+    injected: list
+    layer_live: list
+    keep: list
+    pos_of: list
+    counts: list          # [(R_b, n_live_b)]
+
+    def injected_np(self, b: int):
+        """Reference form (local rows sorted ascending, values) of injected[b]."""
+        inj = self.injected[b]
+        if inj is None:
+            return None
+        f = inj.flag.bool()
+        loc = torch.nonzero(f).flatten()
+        vals = inj.table[inj.row[loc].long()]
+        return _np(loc).astype(np.int64), _np(vals)
+
+
+def prune_with_cache(sub: LayeredSubgraph, cache: HistCache, current_iter: int, stream=None) -> PrunedBatch:
+    """Walk blocks outermost-in (trainer.py:166-207); prunes sub in place."""
+    dev = sub.layers[0].src_nodes.device
+    s = stream or torch.cuda.current_stream(dev)
+    sp = _lib.stream_ptr(s)
+    L = sub.num_layers
+    B = len(sub.seeds)
+    sizes = []
+    for b in range(L):
+        blk = sub.layers[b]
+        sizes += [blk.num_dst, blk.num_src]
+    size_dev = torch.tensor(sizes, dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
+    counts = torch.zeros(2 * L, dtype=torch.int32, device=dev)
+    live_dst = torch.ones(B, dtype=torch.uint8, device=dev)
+    inj_flag = None
+    compute, injected, live, keep_l, pos_l = [None] * L, [None] * L, [None] * (L + 1), [None] * L, [None] * L
+    rows_buf, live_buf = [None] * L, [None] * L
+    max_n = max(sizes)
+    sb = _lib.query("hg_prune_scratch_bytes", max_n)
+    scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+    for b in range(L - 1, -1, -1):
+        blk = sub.layers[b]
+        n_dst, n_src = blk.num_dst, blk.num_src
+        keep = torch.empty(n_dst, dtype=torch.uint8, device=dev)
+        rows = torch.empty(n_dst, dtype=torch.int32, device=dev)
+        pos = torch.empty(n_dst, dtype=torch.int32, device=dev)
+        src_mask = torch.empty(n_src, dtype=torch.uint8, device=dev)
+        lv = torch.empty(n_src, dtype=torch.int32, device=dev)
+        _lib.call("hg_prune_block", _lib.ptr(size_dev[2 * b:2 * b + 1]), n_dst, _lib.ptr(size_dev[2 * b + 1:2 * b + 2]),
+                  n_src, _lib.ptr(live_dst), _lib.ptr(inj_flag), _lib.ptr(blk.adj.start), _lib.ptr(blk.adj.end),
+                  _lib.ptr(blk.adj.col_indices), _lib.ptr(keep), _lib.ptr(rows), _lib.ptr(pos), _lib.ptr(src_mask),
+                  _lib.ptr(lv), _lib.ptr(counts[2 * b:2 * b + 2]), _lib.ptr(cache.gctr), _lib.ptr(scratch), sb, sp)
+        keep_l[b], pos_l[b], rows_buf[b], live_buf[b] = keep, pos, rows, lv
+        live_dst, inj_flag = src_mask, None
+        if b >= 1:
+            lc = cache._layer(b)
+            hit_flag = torch.empty(n_src, dtype=torch.uint8, device=dev)
+            hit_row = torch.empty(n_src, dtype=torch.int32, device=dev)
+            lc.lookup_dev(counts[2 * b + 1:2 * b + 2], n_src, lv, blk.src_nodes, n_src, current_iter, hit_flag,
+                          hit_row, sp)
+            if lc.table is not None:
+                inj_flag = hit_flag
+                injected[b - 1] = Injection(hit_flag, hit_row, lc.table)
+    host = counts.cpu().tolist()
+    cnt = []
+    for b in range(L):
+        R, nl = host[2 * b], host[2 * b + 1]
+        cnt.append((R, nl))
+        compute[b] = rows_buf[b][:R]
+        live[b] = live_buf[b][:nl]
+        sub.layers[b].adj.prune_writes += sub.layers[b].num_dst - R
+    live[L] = torch.arange(B, dtype=torch.int32, device=dev)
+    return PrunedBatch(sub, compute, injected, live, keep_l, pos_l, cnt)
+
+
+# ----------------------------------------------------------------- trainer
+
+
+def make_batches(train_ids, cfg: TrainConfig) -> list:
+    out = []
+    for epoch in range(cfg.epochs):
+        out.extend(split_batches(train_ids, cfg.batch_size, _perm_rng(cfg.seed, epoch)))
+    return out
+
+
+def _device_graph(graph) -> Csr2Graph:
+    if isinstance(graph, Csr2Graph) and isinstance(graph.start, torch.Tensor):
+        return graph
+    # reference (numpy) Csr2Graph or an (start, end, col) triple
+    if isinstance(graph, tuple):
+        return csr2_from_arrays(*graph)
+    return csr2_from_arrays(graph.start, graph.end, graph.col_indices)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float16:
+        return 1
+    if t.dtype == torch.float32:
+        return 0
+    raise ValueError(f"unsupported feature dtype {t.dtype} (fp32 / fp16)")
+
+
+class Trainer:
+    def __init__(self, graph, features, labels, train_ids, cfg: TrainConfig, num_classes=None, probe_nodes=None):
+        _lib.require_cuda()
+        self.graph = _device_graph(graph)
+        self.device = self.graph.start.device
+        self.cfg = cfg
+        self.labels = np.asarray(labels, dtype=np.int64)
+        self.train_ids = np.asarray(train_ids, dtype=np.int64)
+        self.num_classes = int(num_classes or self.labels.max() + 1)
+        if isinstance(features, torch.Tensor):
+            feats = features
+        else:
+            feats = torch.from_numpy(np.ascontiguousarray(features))
+        if cfg.feature_placement == "hbm":
+            feats = feats.to(self.device)
+        elif feats.device.type != "cpu" or not feats.is_pinned():
+            feats = feats.cpu().pin_memory()
+        self.features = feats
+        self.feature_dim = int(feats.shape[1])
+        self.row_bytes = self.feature_dim * feats.element_size()
+        depth = len(cfg.fanouts)
+        dims = [self.feature_dim] + [cfg.hidden] * (depth - 1) + [self.num_classes]
+        self.network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, self.device)
+        policy = CachePolicy(cfg.p_grad, cfg.t_stale, cfg.capacity)
+        feature_rows = self.graph.num_nodes // 10 if cfg.feature_rows is None else cfg.feature_rows
+        self.cache = HistCache(self.graph.num_nodes, [cfg.hidden] * (depth - 1), policy, feature_rows=feature_rows,
+                               refresh_retained=cfg.refresh_retained, dtype=cfg.dtype, device=self.device)
+        if feature_rows > 0:
+            self.cache.backfill_features(self.features, graph=self.graph)
+        self.plan = SamplePlan(cfg.fanouts, cfg.batch_size, cfg.seed)
+        self.metrics = []
+        self.last = None
+        self._dtype_code = _dtype_code(self.features)
+        # host placement: pinned (cudaHostAlloc) memory is UVA-mapped, so the
+        # kernels dereference the host pointer directly over PCIe
+        self.probe_nodes = probe_nodes
+
+    # ------------------------------------------------------------ pieces
+
+    def sample(self, iteration: int, seeds) -> LayeredSubgraph:
+        return sample_layered(self.graph, seeds, self.plan, batch_rng(self.cfg.seed, iteration))
+
+    def _load_input(self, pruned: PrunedBatch, current_iter: int, stream=None):
+        """trainer.py:326-343: feature-region hits + source fetches into the
+        block-0 input matrix; returns (h, baseline_bytes)."""
+        b0 = pruned.sub.layers[0]
+        dev = self.device
+        sp = _lib.stream_ptr(stream)
+        h = torch.empty((b0.num_src, self.feature_dim), dtype=torch.float32, device=dev)
+        n_live0 = pruned.counts[0][1]
+        region = self.cache.feature_table if self.cache.feature_table is not None else self.features
+        _lib.call("hg_load_features", _lib.ptr(_dev_count(n_live0, dev)), n_live0, _lib.ptr(pruned.layer_live[0]),
+                  _lib.ptr(b0.src_nodes), _lib.ptr(self.cache.feature_row_of_dev), _lib.ptr(region),
+                  _lib.ptr(self.features), self.feature_dim, self._dtype_code, _lib.ptr(h),
+                  _lib.ptr(self.cache.gctr), sp)
+        return h, b0.num_src * self.row_bytes
+
+    # --------------------------------------------------------- main loop
+
+    def train_iteration(self, iteration: int, epoch: int, sub: LayeredSubgraph, probe: bool = False) -> IterMetrics:
+        if probe:
+            raise ValueError("estimation probes are out of scope for the device trainer")
+        dev = self.device
+        stream = torch.cuda.current_stream(dev)
+        sp = _lib.stream_ptr(stream)
+        net, cache, cfg = self.network, self.cache, self.cfg
+        before = cache.counters_vector().clone()
+        pruned = prune_with_cache(sub, cache, iteration, stream)
+        h0, baseline = self._load_input(pruned, iteration, stream)
+        L = sub.num_layers
+        tapes = []
+        h = h0
+        for b in range(L):
+            R, _ = pruned.counts[b]
+            t = layer_forward_dev(net, b, sub.layers[b], h, pruned.compute_rows[b], R, _dev_count(R, dev),
+                                  b < L - 1, pruned.injected[b], sp)
+            tapes.append(t)
+            h = t.h_out
+        B = len(sub.seeds)
+        labels_dev = torch.from_numpy(self.labels[sub.seeds].astype(np.int32)).pin_memory().to(dev, non_blocking=True)
+        d_h, loss_dev = cross_entropy_dev(tapes[-1].h_out, labels_dev, B, net.dims[-1], sp)
+        grads = net.new_grads()
+        norms = [None] * L
+        for l in range(L - 1, -1, -1):
+            n_live = pruned.counts[l][1]
+            d_prev, nrm = layer_backward_dev(net, l, sub.layers[l], tapes[l], d_h, grads, l >= 1, pruned.keep[l],
+                                             pruned.pos_of[l], pruned.layer_live[l], n_live, sp)
+            norms[l] = nrm
+            d_h = d_prev
+        sgd_step(net, grads, cfg.eta)
+        for layer in range(1, L):
+            n_live = pruned.counts[layer][1]
+            if n_live == 0:
+                continue
+            cache._layer(layer).update_dev(n_live, pruned.layer_live[layer], sub.layers[layer].src_nodes,
+                                           norms[layer], pruned.keep[layer - 1], tapes[layer - 1].h_out,
+                                           iteration, cache.refresh_retained, sp)
+        cache.end_iteration(iteration)
+        after = cache.counters_vector()
+        host = torch.cat([loss_dev.view(1), (after - before).double(), after[CTR_VALID::LAYER_CTR_LEN]
+                          [:cache.num_layers].double()]).cpu().tolist()
+        loss, delta = host[0], [int(x) for x in host[1:1 + after.numel()]]
+        valid = int(sum(host[1 + after.numel():]))
+        self.last = (pruned, tapes, grads, norms)
+        return self._metrics(iteration, epoch, len(sub.seeds), loss, delta, baseline, valid, sub)
+
+    def _metrics(self, iteration, epoch, num_seeds, loss, delta, baseline, valid, sub):
+        nl = self.cache.num_layers
+        tot = dict.fromkeys(COUNTER_NAMES, 0)
+        from .cache import _LAYER_IDX
+        for l in range(nl):
+            for k, i in _LAYER_IDX.items():
+                tot[k] += delta[l * LAYER_CTR_LEN + i]
+        g = delta[nl * LAYER_CTR_LEN:]
+        fh, fm = g[GCTR_FEATURE_HITS], g[GCTR_FEATURE_MISSES]
+        return IterMetrics(
+            iteration=iteration, epoch=epoch, num_seeds=num_seeds, loss=float(loss),
+            fetched_bytes=fm * self.row_bytes, baseline_bytes=baseline,
+            prune_writes=sum(b.adj.prune_writes for b in sub.layers),
+            hits=tot["hits"], misses=tot["misses"], admissions=tot["admissions"],
+            gradient_evictions=tot["gradient_evictions"], staleness_evictions=tot["staleness_evictions"],
+            forced_evictions=tot["forced_evictions"], feature_hits=fh, feature_misses=fm,
+            valid_entries=valid, estimation_error=math.nan)
+
+    def train(self) -> list:
+        cfg = self.cfg
+        batches = make_batches(self.train_ids, cfg)
+        per_epoch = max(1, math.ceil(len(self.train_ids) / cfg.batch_size))
+        with SubgraphProducer(self.graph, batches, self.plan, queue_capacity=2) as producer:
+            for iteration, sub in producer:
+                m = self.train_iteration(iteration, iteration // per_epoch, sub)
+                self.metrics.append(m)
+        return self.metrics
+
+
+# ------------------------------------------------------ reference baseline
+
+
+def run_plain_loop(graph, features, labels, train_ids, cfg: TrainConfig, num_classes=None, on_step=None):
+    """Cache-free loop sharing the trainer's rng streams and update order
+    (trainer.py:439-469). Returns (network, per-iteration losses)."""
+    _lib.require_cuda()
+    g = _device_graph(graph)
+    dev = g.start.device
+    labels = np.asarray(labels, dtype=np.int64)
+    train_ids = np.asarray(train_ids, dtype=np.int64)
+    ncls = int(num_classes or labels.max() + 1)
+    feats = features if isinstance(features, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(features))
+    feats = feats.to(dev)
+    d = int(feats.shape[1])
+    depth = len(cfg.fanouts)
+    dims = [d] + [cfg.hidden] * (depth - 1) + [ncls]
+    network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, dev)
+    plan = SamplePlan(cfg.fanouts, cfg.batch_size, cfg.seed)
+    losses = []
+    gctr = torch.zeros(8, dtype=torch.int64, device=dev)
+    sp = _lib.stream_ptr()
+    for idx, seeds in enumerate(make_batches(train_ids, cfg)):
+        sub = sample_layered(g, seeds, plan, batch_rng(cfg.seed, idx))
+        b0 = sub.layers[0]
+        h = torch.empty((b0.num_src, d), dtype=torch.float32, device=dev)
+        live = torch.arange(b0.num_src, dtype=torch.int32, device=dev)
+        _lib.call("hg_load_features", _lib.ptr(_dev_count(b0.num_src, dev)), b0.num_src, _lib.ptr(live),
+                  _lib.ptr(b0.src_nodes), None, _lib.ptr(feats), _lib.ptr(feats), d, _dtype_code(feats),
+                  _lib.ptr(h), _lib.ptr(gctr), sp)
+        tape = forward_pass(network, sub.layers, h)
+        labels_dev = torch.as_tensor(labels[seeds].astype(np.int32), device=dev)
+        d_logits, loss = cross_entropy_dev(tape.logits.contiguous(), labels_dev, len(seeds), ncls, sp)
+        grads, _, _ = backward(network, sub.layers, tape, d_logits, need_input=False)
+        sgd_step(network, grads, cfg.eta)
+        losses.append(float(loss.item()))
+        if on_step is not None:
+            on_step(idx, network)
+    return network, losses

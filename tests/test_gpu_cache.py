@@ -1,0 +1,82 @@
+"""GPU historical cache: every lookup / update / sweep of the reference's
+scripted op sequences (tests/golden/cache.npz) reproduced bit-exactly —
+hits, served rows, misses, row_of, admit_iter, row_owner, ring table,
+header/capacity/window scalars and all counters."""
+
+import math
+
+import numpy as np
+import pytest
+
+from tests.goldens import load
+
+pytestmark = pytest.mark.gpu
+
+CNAMES = sorted(("hits", "misses", "admissions", "gradient_evictions", "staleness_evictions",
+                 "forced_evictions", "staleness_violations", "feature_hits", "feature_misses"))
+
+
+@pytest.mark.parametrize("ci", range(7))
+def test_cache_sequences_match_reference(ci):
+    import paper_2301_07482_b200 as hg
+    z = load("cache")
+    p, t, cap, refresh = z[f"c{ci}_policy"]
+    cache = hg.HistCache(24, [3], hg.CachePolicy(float(p), float(t), None if cap < 0 else int(cap)),
+                         refresh_retained=bool(refresh), dtype=np.float32)
+    for it in range(25):
+        pfx = f"c{ci}_i{it}_"
+        batch = z[pfx + "batch"]
+        hits, rows, miss = cache.lookup(1, batch, it)
+        np.testing.assert_array_equal(hits, z[pfx + "hits"], err_msg=f"it {it}")
+        np.testing.assert_array_equal(rows, z[pfx + "hitrows"], err_msg=f"it {it}")
+        np.testing.assert_array_equal(miss, z[pfx + "miss"], err_msg=f"it {it}")
+        emb = (batch[:, None] * 100.0 + it + np.arange(3)).astype(np.float32)
+        cache.update_cache(1, batch, miss, emb, z[pfx + "grads"], it)
+        cache.end_iteration(it)
+        lc = cache.layers[1]
+        np.testing.assert_array_equal(lc.row_of, z[pfx + "row_of"], err_msg=f"it {it}")
+        np.testing.assert_array_equal(lc.admit_iter, z[pfx + "admit_iter"], err_msg=f"it {it}")
+        if lc.row_owner is not None:
+            np.testing.assert_array_equal(lc.row_owner, z[pfx + "row_owner"], err_msg=f"it {it}")
+            np.testing.assert_array_equal(lc.table.cpu().numpy(), z[pfx + "table"], err_msg=f"it {it}")
+        np.testing.assert_array_equal([lc.header, lc.capacity, lc.window_admissions, lc.window_forced],
+                                      z[pfx + "scalars"], err_msg=f"it {it}")
+        c = cache.counters()
+        np.testing.assert_array_equal([c[k] for k in CNAMES], z[pfx + "counters"], err_msg=f"it {it}")
+        cache.check_integrity()
+
+
+def test_feature_backfill_matches_reference():
+    import paper_2301_07482_b200 as hg
+    z = load("cache")
+    cache = hg.HistCache(10, [2], hg.CachePolicy(1.0, 1), feature_rows=4)
+    cache.backfill_features(np.arange(20, dtype=np.float32).reshape(10, 2),
+                            np.array([3, 7, 7, 1, 0, 7, 2, 3, 3, 9]))
+    np.testing.assert_array_equal(cache.feature_row_of, z["backfill_row_of"])
+    np.testing.assert_array_equal(cache.feature_table.cpu().numpy(), z["backfill_table"])
+
+
+def test_policy_validation_and_errors():
+    import paper_2301_07482_b200 as hg
+    for bad in ((-0.1, 1), (1.5, 1), (0.5, -1)):
+        with pytest.raises(ValueError):
+            hg.CachePolicy(*bad)
+    with pytest.raises(ValueError):
+        hg.CachePolicy(0.5, 1, capacity=0)
+    cache = hg.HistCache(8, [2], hg.CachePolicy(1.0, math.inf))
+    with pytest.raises(ValueError):
+        cache.lookup(3, [0], 0)
+    with pytest.raises(ValueError):
+        cache.update_cache(1, [0, 1], [0], np.zeros((1, 2), np.float32), [0.0, 0.0], 0)
+
+
+def test_oversized_batch_keeps_trailing_writes():
+    import paper_2301_07482_b200 as hg
+    cache = hg.HistCache(8, [2], hg.CachePolicy(1.0, math.inf, 2))
+    batch = np.array([0, 1, 2])
+    emb = (batch[:, None] * 1000.0 + np.arange(2)).astype(np.float32)
+    cache.update_cache(1, batch, batch, emb, np.array([0.0, 1.0, 2.0]), 0)
+    hits, _, miss = cache.lookup(1, batch, 0)
+    assert sorted(hits) == [1, 2] and list(miss) == [0]
+    assert cache.valid_entries() == 2
+    cache.check_integrity()

@@ -1,0 +1,149 @@
+"""End-to-end GPU trainer parity.
+
+* Lockstep (SURVEY §8(c) Mode B): the oracle trainer's cache admission is
+  fed the GPU's fp64 norms; then every sampled/pruned subgraph and every
+  integer IterMetrics field must match bit-for-bit over whole runs, and the
+  loss must stay within 1e-3 relative.
+* Degenerate mode (p_grad=0, t_stale=0): free-running integer metrics equal the
+  reference's golden run, and the GPU trainer is bitwise identical to the GPU
+  cache-free loop (reference acceptance criterion 1).
+"""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+from oracle.datagen import csr2_from_edges, power_law_dataset
+from oracle.step import GCN, SAGE, OTrainConfig, OTrainer
+from tests.goldens import load
+
+pytestmark = pytest.mark.gpu
+
+INT_FIELDS = ["fetched_bytes", "baseline_bytes", "prune_writes", "hits", "misses", "admissions",
+              "gradient_evictions", "staleness_evictions", "forced_evictions", "feature_hits",
+              "feature_misses", "valid_entries"]
+_DS = {}
+
+
+def _pl3000():
+    if "ds" not in _DS:
+        ds = power_law_dataset(3000, np.random.default_rng(0), m=4, feature_dim=16)
+        _DS["ds"] = (ds, csr2_from_edges(ds.src, ds.dst, ds.num_nodes))
+    return _DS["ds"]
+
+
+def _kinds(kind):
+    import paper_2301_07482_b200 as hg
+    return (hg.LayerKind.SAGE_MEAN if kind == SAGE else hg.LayerKind.GCN), kind
+
+
+@pytest.mark.parametrize("kind", [SAGE, GCN])
+@pytest.mark.parametrize("p,t,cap", [(0.9, 5, None), (0.6, math.inf, None), (0.9, 3, 700), (1.0, 2, 64)])
+def test_lockstep_with_oracle(kind, p, t, cap):
+    import paper_2301_07482_b200 as hg
+    ds, g = _pl3000()
+    lk, ok = _kinds(kind)
+    common = dict(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=2, eta=0.05, p_grad=p, t_stale=t,
+                  capacity=cap, seed=3)
+    tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, hg.TrainConfig(kind=lk, **common), ds.num_classes)
+    otr = OTrainer(g, ds.features, ds.labels, ds.train_ids, OTrainConfig(kind=ok, **common), ds.num_classes)
+    batches = hg.make_batches(ds.train_ids, tr.cfg)
+    per_epoch = math.ceil(len(ds.train_ids) / 128)
+    for it, seeds in enumerate(batches):
+        sub = tr.sample(it, seeds)
+        osub = otr.sample(it, seeds)
+        m = tr.train_iteration(it, it // per_epoch, sub)
+        norms = {l: tr.last[3][l].cpu().numpy() for l in range(1, 3)}
+        om = otr.train_iteration(it, it // per_epoch, osub, norms_override=norms)
+        for f in INT_FIELDS:
+            assert getattr(m, f) == getattr(om, f), (it, f, getattr(m, f), getattr(om, f))
+        assert abs(m.loss - om.loss) <= 1e-3 * abs(om.loss), (it, m.loss, om.loss)
+        # the pruned structure itself
+        pr, opr = tr.last[0], otr.last[0]
+        for b in range(3):
+            np.testing.assert_array_equal(pr.layer_live[b].cpu().numpy(), opr.layer_live[b])
+            np.testing.assert_array_equal(pr.compute_rows[b].cpu().numpy(), opr.compute_rows[b])
+    tr.cache.check_integrity()
+    for l in range(3):
+        w = tr.network.layers[l].weight.cpu().numpy()
+        ow = otr.network.layers[l].weight
+        assert np.linalg.norm(w - ow) <= 1e-3 * np.linalg.norm(ow)
+
+
+@pytest.mark.parametrize("kind", [SAGE, GCN])
+def test_degenerate_mode_matches_reference_golden(kind):
+    import paper_2301_07482_b200 as hg
+    z = load("trainer")
+    ds, g = _pl3000()
+    lk, _ = _kinds(kind)
+    cfg = hg.TrainConfig(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=2, eta=0.05, kind=lk,
+                         p_grad=0.0, t_stale=0, seed=3)
+    tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
+    ms = tr.train()
+    names = list(z["int_names"])
+    got = np.array([[getattr(m, f) for f in names] for m in ms], np.int64)
+    np.testing.assert_array_equal(got, z[f"{kind}_0.0_0_ints"])
+    np.testing.assert_allclose([m.loss for m in ms], z[f"{kind}_0.0_0_loss"], rtol=1e-3)
+
+
+@pytest.mark.parametrize("kind", [SAGE, GCN])
+def test_degenerate_trainer_bitwise_equals_plain_loop(kind):
+    import paper_2301_07482_b200 as hg
+    ds, g = _pl3000()
+    lk, _ = _kinds(kind)
+    cfg = hg.TrainConfig(fanouts=(5, 5, 5), hidden=32, batch_size=128, epochs=1, eta=0.05, kind=lk,
+                         p_grad=0.0, t_stale=0, seed=7)
+    plain = []
+    hg.run_plain_loop(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes,
+                      on_step=lambda it, net: plain.append(hashlib.sha256(net.checksum_bytes()).hexdigest()))
+    tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
+    live = []
+    for idx, seeds in enumerate(hg.make_batches(ds.train_ids, cfg)):
+        tr.train_iteration(idx, 0, tr.sample(idx, seeds))
+        live.append(hashlib.sha256(tr.network.checksum_bytes()).hexdigest())
+    assert live == plain
+
+
+def test_gpu_runs_are_bitwise_reproducible():
+    import paper_2301_07482_b200 as hg
+    ds, g = _pl3000()
+    cfg = hg.TrainConfig(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=1, eta=0.05,
+                         kind=hg.LayerKind.SAGE_MEAN, p_grad=0.9, t_stale=5, seed=1)
+    runs = []
+    for _ in range(2):
+        tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
+        ms = tr.train()
+        runs.append((hashlib.sha256(tr.network.checksum_bytes()).hexdigest(),
+                     [(m.loss, m.hits, m.admissions) for m in ms]))
+    assert runs[0] == runs[1]
+
+
+def test_host_feature_placement_uva_matches_hbm():
+    import paper_2301_07482_b200 as hg
+    ds, g = _pl3000()
+    base = dict(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=1, eta=0.05,
+                kind=hg.LayerKind.SAGE_MEAN, p_grad=0.9, t_stale=5, seed=1)
+    a = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, hg.TrainConfig(**base), ds.num_classes).train()
+    b = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, hg.TrainConfig(feature_placement="host", **base),
+                   ds.num_classes).train()
+    assert [(m.loss, m.fetched_bytes) for m in a] == [(m.loss, m.fetched_bytes) for m in b]
+
+
+def test_fp16_feature_table():
+    import paper_2301_07482_b200 as hg
+    ds, g = _pl3000()
+    cfg = hg.TrainConfig(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=1, eta=0.05,
+                         kind=hg.LayerKind.SAGE_MEAN, p_grad=0.9, t_stale=5, seed=1)
+    f16 = ds.features.astype(np.float16)
+    tr = hg.Trainer(g, f16, ds.labels, ds.train_ids, cfg, ds.num_classes)
+    otr = OTrainer(g, f16, ds.labels, ds.train_ids,
+                   OTrainConfig(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=1, eta=0.05, kind=SAGE,
+                                p_grad=0.9, t_stale=5, seed=1), ds.num_classes)
+    for it, seeds in enumerate(hg.make_batches(ds.train_ids, cfg)[:4]):
+        m = tr.train_iteration(it, 0, tr.sample(it, seeds))
+        om = otr.train_iteration(it, 0, otr.sample(it, seeds),
+                                 norms_override={l: tr.last[3][l].cpu().numpy() for l in (1, 2)})
+        assert m.fetched_bytes == om.fetched_bytes and m.hits == om.hits
+        assert abs(m.loss - om.loss) <= 1e-3 * abs(om.loss)
