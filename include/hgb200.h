@@ -129,6 +129,12 @@ long long hg_degree_order_scratch_bytes(long long n);
 int hg_feature_region(const int64_t* g_start, const int64_t* g_end, long long n, long long k, int32_t* chosen,
                       int32_t* feature_row_of, void* scratch, long long scratch_bytes, cudaStream_t stream);
 
+/* ---- native synthetic data: the histgnn/data.py:243-270 process (preferential
+ * attachment, both edge directions) with its own PRNG, for the benchmark
+ * shapes the reference generator cannot reach. Host function; writes
+ * 2*m*(n-m) edges into host int32 arrays; returns the edge count or -1. */
+long long hg_synth_power_law(long long n, int m, unsigned long long seed, int32_t* src_out, int32_t* dst_out);
+
 #ifdef __cplusplus
 }
 #endif

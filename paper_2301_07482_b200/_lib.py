@@ -52,6 +52,7 @@ SIGNATURES = {
     "hg_cache_write": (I32, [I32, I32, I32, I32, I32, F64, I32, P, P, P, P, P, P, P, P, I64, P]),
     "hg_degree_order_scratch_bytes": (I64, [I64]),
     "hg_feature_region": (I32, [P, P, I64, I64, P, P, P, I64, P]),
+    "hg_synth_power_law": (I64, [I64, I32, U64, P, P]),
 }
 
 _lib = None

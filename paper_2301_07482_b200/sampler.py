@@ -183,16 +183,23 @@ def _advance(rng: np.random.Generator, draws: int) -> None:
 
 
 def sample_layered(g: Csr2Graph, seeds, plan: SamplePlan, rng: np.random.Generator, *,
-                   workspace: SamplerWorkspace | None = None, stream=None) -> LayeredSubgraph:
-    """Expand seeds through len(plan.fanouts) sampling blocks on the GPU."""
+                   workspace: SamplerWorkspace | None = None, stream=None,
+                   seeds_dev: torch.Tensor | None = None) -> LayeredSubgraph:
+    """Expand seeds through len(plan.fanouts) sampling blocks on the GPU.
+
+    `seeds_dev` (int32 device tensor) lets a device-resident pipeline skip the
+    host copy; the caller then guarantees unique, in-range seeds."""
     _lib.require_cuda()
-    seeds = np.asarray(seeds, dtype=np.int64)
-    if len(seeds) == 0:
-        raise ValueError("empty seed set")
-    if len(np.unique(seeds)) != len(seeds):
-        raise ValueError("seed ids must be unique")
-    if seeds.min() < 0 or seeds.max() >= g.num_nodes:
-        raise ValueError("seed id out of range")
+    if seeds_dev is None:
+        seeds = np.asarray(seeds, dtype=np.int64)
+        if len(seeds) == 0:
+            raise ValueError("empty seed set")
+        if len(np.unique(seeds)) != len(seeds):
+            raise ValueError("seed ids must be unique")
+        if seeds.min() < 0 or seeds.max() >= g.num_nodes:
+            raise ValueError("seed id out of range")
+    else:
+        seeds = seeds_dev
     ws = workspace or default_workspace(g)
     dev = g.start.device
     s = stream or torch.cuda.current_stream(dev)
@@ -201,8 +208,11 @@ def sample_layered(g: Csr2Graph, seeds, plan: SamplePlan, rng: np.random.Generat
     with ws.lock, torch.cuda.stream(s):
         sp = _lib.stream_ptr(s)
         ws.stream_pos.zero_()
-        B = len(seeds)
-        frontier = torch.from_numpy(seeds.astype(np.int32)).pin_memory().to(dev, non_blocking=True)
+        B = int(seeds.shape[0])
+        if seeds_dev is None:
+            frontier = torch.from_numpy(seeds.astype(np.int32)).pin_memory().to(dev, non_blocking=True)
+        else:
+            frontier = seeds_dev
         F_dev = torch.tensor([B], dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
         F_max = B
         raw = []

@@ -118,7 +118,7 @@ def test_c1_subgraphs_match_reference_hashes():
     """Config C1 (100K nodes / 2M edges, fanout 15,10,5, batch 1024)."""
     hg = _hg()
     gold = load_json("c1")
-    ds = power_law_dataset(100_000, np.random.default_rng(0), m=10, feature_dim=8)
+    ds = power_law_dataset(100_000, np.random.default_rng(0), m=10, feature_dim=128)
     g = hg.build_csr2(hg.CooGraph(ds.src, ds.dst, ds.num_nodes))
     assert sha(g.col_np) == gold["csr2"]["col"]
     cfg = hg.TrainConfig(fanouts=(15, 10, 5), hidden=256, batch_size=1024, kind=hg.LayerKind.SAGE_MEAN)
