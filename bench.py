@@ -1,0 +1,286 @@
+#!/usr/bin/env python
+"""Benchmark: ReFresh per-iteration training throughput (seeds/s) on B200.
+
+Workload (N=1 default, BASELINE.json configs[1]): ogbn-products-shaped
+synthetic power-law graph (2.4M nodes, 62.4M edges, 100-d fp32 features,
+47 classes), 3-layer GraphSAGE hidden 256, fanouts (15,10,5), batch 1024,
+historical cache (p_grad 0.9, t_stale 20). A step = sample one batch + one
+train_iteration (prune, feature gather, forward, loss, backward, SGD, cache
+update). Inputs (graph 0.5 GB + features 0.96 GB) are far larger than L2,
+batches touch random rows, so no L2 flush is needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c2|c1]
+
+--impl reference times the CPU oracle port (oracle/, the reference algorithm
+restated in numpy) on the host cores, on the same dataset.
+Multi-GPU (torchrun): data parallel, each rank trains its own batches with its
+own cache replica; gradients are all-reduced (NCCL) before SGD; weak scaling.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training seeds/sec per iteration"
+CONFIGS = {
+    "c2": dict(workload="ogbn-products-shape synthetic power-law (2.4M nodes, 62.4M edges, 100-d fp32), "
+                        "3-layer GraphSAGE hidden 256, fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
+               n=2_400_000, m=13, d=100, classes=47),
+    "c1": dict(workload="synthetic power-law 100K nodes / 2M edges, 128-d fp32, 3-layer GraphSAGE hidden 256, "
+                        "fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
+               n=100_000, m=10, d=128, classes=8),
+}
+FANOUTS, HIDDEN, BATCH, P_GRAD, T_STALE, ETA = (15, 10, 5), 256, 1024, 0.9, 20, 0.01
+
+
+def make_data(cfg, seed=0):
+    """Native power-law graph (C++) + numpy N(0,1) features; identical for both arms."""
+    from paper_2301_07482_b200.data import synth_edges
+    src, dst = synth_edges(cfg["n"], cfg["m"], seed)
+    rng = np.random.default_rng(seed)
+    feats = rng.standard_normal((cfg["n"], cfg["d"]), dtype=np.float32)
+    labels = rng.integers(0, cfg["classes"], size=cfg["n"])
+    perm = rng.permutation(cfg["n"])
+    train = np.sort(perm[: int(0.6 * cfg["n"])])
+    return src, dst, feats, labels, train
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 8 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) > 8 for i in range(4) if "Active" in r[5 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_reference(cfg, data, steps, warmup, budget_s=150.0):
+    """Oracle port (numpy restatement of the reference) on the host cores."""
+    from oracle.datagen import csr2_from_edges
+    from oracle.step import SAGE, OTrainConfig, OTrainer, make_batches
+    src, dst, feats, labels, train = data
+    g = csr2_from_edges(src.astype(np.int64), dst.astype(np.int64), cfg["n"])
+    ocfg = OTrainConfig(fanouts=FANOUTS, hidden=HIDDEN, batch_size=BATCH, eta=ETA, kind=SAGE, p_grad=P_GRAD,
+                        t_stale=T_STALE, seed=0)
+    tr = OTrainer(g, feats, labels, train, ocfg, cfg["classes"])
+    batches = make_batches(train, ocfg)
+    it = 0
+    t_start = time.perf_counter()
+    for _ in range(warmup):
+        tr.train_iteration(it, 0, tr.sample(it, batches[it]))
+        it += 1
+        if time.perf_counter() - t_start > budget_s / 3:
+            break
+    done, seeds, t0 = 0, 0, time.perf_counter()
+    while done < steps:
+        m = tr.train_iteration(it, 0, tr.sample(it, batches[it]))
+        seeds += m.num_seeds
+        it += 1
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0))
+    return {"value": seeds / dt, "ms_per_step": 1e3 * dt / done, "steps": done, "cores": cores,
+            "sample": f"{done} full iterations (batch {BATCH}) of OTrainer on the same graph after "
+                      f"{it - done} warm-up iterations; numpy/OpenBLAS threads = {cores}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    cfgd = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": cfgd["workload"], "nodes": cfgd["n"], "edges": 2 * cfgd["m"] * (cfgd["n"] - cfgd["m"]),
+              "feature_dim": cfgd["d"], "global_batch": BATCH * world, "fanouts": list(FANOUTS),
+              "hidden": HIDDEN, "parallelism": f"dp{world}", "l2": "inputs > L2 (1.5 GB resident, random rows)"}
+    base = {"metric": METRIC, "unit": "seeds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic (native power-law generator, N(0,1) features)", "config": config}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        data = make_data(cfgd)
+        r = cpu_reference(cfgd, data, args.steps, args.warmup, budget_s=150.0)
+        out = dict(base, impl="reference", value=r["value"], ms_per_step=r["ms_per_step"],
+                   cpu_baseline={"value": r["value"], "unit": "seeds/s", "cores": r["cores"], "kind": "port",
+                                 "sample": r["sample"]},
+                   e2e={"value": r["value"], "unit": "seeds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        out["steps"] = r["steps"]
+        print(json.dumps(out))
+        return
+
+    import torch
+    import paper_2301_07482_b200 as hg
+    from paper_2301_07482_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    data = make_data(cfgd)
+    src, dst, feats, labels, train = data
+    from paper_2301_07482_b200.data import csr2_from_edges_device
+    graph = csr2_from_edges_device(src, dst, cfgd["n"], dev)
+    feats_dev = torch.from_numpy(feats).to(dev)
+    tcfg = hg.TrainConfig(fanouts=FANOUTS, hidden=HIDDEN, batch_size=BATCH, eta=ETA, kind=hg.LayerKind.SAGE_MEAN,
+                          p_grad=P_GRAD, t_stale=T_STALE, seed=0)
+    tr = hg.Trainer(graph, feats_dev, labels, train, tcfg, cfgd["classes"])
+    if world > 1:
+        def allreduce(grads):
+            dist.all_reduce(grads.flat)
+            grads.flat.div_(world)
+        tr.grad_hook = allreduce
+    batches = hg.make_batches(train, tcfg)
+    need = (args.warmup + 2 * args.steps) * world
+    if need > len(batches):
+        raise SystemExit(f"need {need} batches, epoch has {len(batches)}")
+    # rank r takes batch indices world*s + r (iteration number = global batch index)
+    mine = [world * s + rank for s in range(args.warmup + 2 * args.steps)]
+    seeds_dev = [torch.as_tensor(batches[i].astype(np.int32), device=dev) for i in mine]
+    labels_dev = [torch.as_tensor(labels[batches[i]].astype(np.int32), device=dev) for i in mine]
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    for s in range(args.warmup):
+        tr.train_step_device(mine[s], seeds_dev[s], labels_dev[s])
+    torch.cuda.synchronize()
+
+    # ---- timed region 1: device-resident steps (value) ----
+    clocks = ClockSampler(local)
+    prof_names = ["hg_load_features", "hg_aggregate_fwd", "hg_transpose_agg", "hg_sample_layer"]
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = _lib.load().hg_kernel_launches()
+    _lib.enable_profile(prof_names)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    losses = []
+    for s in range(args.warmup, args.warmup + args.steps):
+        losses.append(tr.train_step_device(mine[s], seeds_dev[s], labels_dev[s]))
+    e1.record()
+    torch.cuda.synchronize()
+    prof = _lib.disable_profile()
+    launches = _lib.load().hg_kernel_launches() - launches0
+    barrier()
+    clk = clocks.stop()
+    t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    value = BATCH * world * args.steps / t_dev
+
+    # roofline of the feature gather (hg_load_features): algorithmic bytes per launch
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6551.4, "fallback"
+    if os.path.exists(peaks_path):
+        peak, peak_src = json.load(open(peaks_path))["hbm_gbs"], "measured"
+    per_kernel = {}
+    for name, recs in prof.items():
+        ms = sum(a.elapsed_time(b) for a, b, _ in recs)
+        per_kernel[name] = {"launches": len(recs), "ms_total": ms}
+    gather = prof["hg_load_features"]
+    g_bytes = 0
+    for _, _, a in gather:
+        n_live, dim, dtype = a[1], a[7], a[8]
+        isz = 2 if dtype == 1 else 4
+        g_bytes += n_live * (dim * isz + dim * 4 + 12)  # row read + fp32 row write + 3 index reads
+    g_time = per_kernel["hg_load_features"]["ms_total"] / 1e3
+    achieved = g_bytes / g_time / 1e9 if g_time > 0 else 0.0
+    roofline = {"kernel": "k_load_rows (hg_load_features, feature gather)", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_source": peak_src, "traffic": None,
+                "bytes_per_launch": g_bytes / max(1, len(gather)),
+                "share_of_step": g_time / (t_dev) if t_dev else None}
+
+    # ---- timed region 2: end-to-end through the public API (host in, host out) ----
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h2d = d2h = 0
+    for s in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
+        it = mine[s]
+        sub = tr.sample(it, batches[it])
+        m = tr.train_iteration(it, 0, sub)
+        h2d += batches[it].size * 4 * 2          # seed ids + labels (int32)
+        d2h += (1 + tr.cache.counters_vector().numel() + tr.cache.num_layers) * 8
+    torch.cuda.synchronize()
+    t_e2e = max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": BATCH * world * args.steps / t_e2e, "unit": "seeds/s",
+           "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+           "api": "Trainer.sample + Trainer.train_iteration (IterMetrics read back every step)"}
+
+    out = dict(base, value=value, ms_per_step=1e3 * t_dev / args.steps, e2e=e2e, roofline=roofline,
+               gpu_launches=int(launches), clocks=clk, per_kernel=per_kernel,
+               loss_last=float(losses[-1].item()), io_saving_last=None)
+    out["io_saving_e2e_last"] = 1.0 - m.fetched_bytes / m.baseline_bytes if m.baseline_bytes else None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference(cfgd, data, steps=3, warmup=1, budget_s=args.cpu_budget)
+        out["cpu_baseline"] = {"value": r["value"], "unit": "seeds/s", "cores": r["cores"], "kind": "port",
+                               "sample": r["sample"]}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -31,6 +31,8 @@ extern "C" {
 int hg_version(void);
 const char* hg_last_error(void);
 int hg_device_sync(void);
+/* number of hand-written hg kernels launched by this process (library GEMMs excluded) */
+long long hg_kernel_launches(void);
 
 /* ---- K1+K2 sampler: histgnn/sampler.py:118-163 (_sample_in_neighbors,
  * _build_block), called per layer by sampler.py:166-190 (sample_layered).

@@ -29,6 +29,7 @@ SIGNATURES = {
     "hg_version": (I32, []),
     "hg_last_error": (ctypes.c_char_p, []),
     "hg_device_sync": (I32, []),
+    "hg_kernel_launches": (I64, []),
     "hg_sample_layer_scratch_bytes": (I64, [I64, I64]),
     "hg_sample_layer": (I32, [P, P, P, I64, P, P, I64, I32, U64, U64, U64, U64, P, U32, P, P, P, P, P,
                               P, P, P, P, P, P, I64, P]),
@@ -84,10 +85,33 @@ def require_cuda():
         raise HgError("paper_2301_07482_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
 
 
+_prof = None   # {entry point: [(start_event, end_event, args)]} while profiling
+
+
+def enable_profile(names):
+    """Record CUDA events around the named entry points (on the current
+    stream, which is the stream every caller in this package passes)."""
+    global _prof
+    _prof = {n: [] for n in names}
+
+
+def disable_profile():
+    global _prof
+    p, _prof = _prof, None
+    return p
+
+
 def call(name, *args):
     """Invoke an int-status entry point and raise on failure."""
     lib = load()
-    st = getattr(lib, name)(*args)
+    if _prof is not None and name in _prof:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = getattr(lib, name)(*args)
+        e1.record()
+        _prof[name].append((e0, e1, args))
+    else:
+        st = getattr(lib, name)(*args)
     if st != 0:
         raise HgError(f"{name} failed ({st}): {lib.hg_last_error().decode()}")
     return st

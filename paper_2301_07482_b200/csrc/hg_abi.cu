@@ -1,5 +1,6 @@
 // Library-wide entry points: version, last error, launch checking.
 #include "hgb200.h"
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -16,7 +17,10 @@ int fail(const char* where, int code, const std::string& msg) {
   return code;
 }
 
+static std::atomic<long long> g_launches{0};
+
 int check_launch(const char* where) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(where, kCuda, cudaGetErrorString(e));
   return kOk;
@@ -27,6 +31,9 @@ int check_launch(const char* where) {
 extern "C" {
 
 int hg_version(void) { return 10000; }  // 1.0.0
+
+// number of hand-written hg kernels launched by this process so far
+long long hg_kernel_launches(void) { return hg::g_launches.load(std::memory_order_relaxed); }
 
 const char* hg_last_error(void) { return hg::g_last_error.c_str(); }
 

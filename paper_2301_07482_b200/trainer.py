@@ -260,6 +260,7 @@ class Trainer:
         # host placement: pinned (cudaHostAlloc) memory is UVA-mapped, so the
         # kernels dereference the host pointer directly over PCIe
         self.probe_nodes = probe_nodes
+        self.grad_hook = None   # callable(Grads) run between backward and SGD (data parallel)
 
     # ------------------------------------------------------------ pieces
 
@@ -284,13 +285,33 @@ class Trainer:
     # --------------------------------------------------------- main loop
 
     def train_iteration(self, iteration: int, epoch: int, sub: LayeredSubgraph, probe: bool = False) -> IterMetrics:
+        """trainer.py:362-421. Returns IterMetrics (one device->host read)."""
         if probe:
             raise ValueError("estimation probes are out of scope for the device trainer")
+        dev = self.device
+        cache = self.cache
+        before = cache.counters_vector().clone()
+        labels_dev = torch.from_numpy(self.labels[sub.seeds].astype(np.int32)).pin_memory().to(dev, non_blocking=True)
+        loss_dev, baseline = self._step(iteration, sub, labels_dev)
+        after = cache.counters_vector()
+        host = torch.cat([loss_dev.view(1), (after - before).double(), after[CTR_VALID::LAYER_CTR_LEN]
+                          [:cache.num_layers].double()]).cpu().tolist()
+        loss, delta = host[0], [int(x) for x in host[1:1 + after.numel()]]
+        valid = int(sum(host[1 + after.numel():]))
+        return self._metrics(iteration, epoch, len(sub.seeds), loss, delta, baseline, valid, sub)
+
+    def train_step_device(self, iteration: int, seeds_dev: torch.Tensor, labels_dev: torch.Tensor):
+        """Device-resident step for throughput runs: seeds/labels already in
+        HBM, loss and counters stay on the device (read them after timing)."""
+        sub = sample_layered(self.graph, None, self.plan, batch_rng(self.cfg.seed, iteration), seeds_dev=seeds_dev)
+        loss_dev, _ = self._step(iteration, sub, labels_dev)
+        return loss_dev
+
+    def _step(self, iteration: int, sub: LayeredSubgraph, labels_dev: torch.Tensor):
         dev = self.device
         stream = torch.cuda.current_stream(dev)
         sp = _lib.stream_ptr(stream)
         net, cache, cfg = self.network, self.cache, self.cfg
-        before = cache.counters_vector().clone()
         pruned = prune_with_cache(sub, cache, iteration, stream)
         h0, baseline = self._load_input(pruned, iteration, stream)
         L = sub.num_layers
@@ -302,8 +323,7 @@ class Trainer:
                                   b < L - 1, pruned.injected[b], sp)
             tapes.append(t)
             h = t.h_out
-        B = len(sub.seeds)
-        labels_dev = torch.from_numpy(self.labels[sub.seeds].astype(np.int32)).pin_memory().to(dev, non_blocking=True)
+        B = int(sub.seeds.shape[0])
         d_h, loss_dev = cross_entropy_dev(tapes[-1].h_out, labels_dev, B, net.dims[-1], sp)
         grads = net.new_grads()
         norms = [None] * L
@@ -313,6 +333,8 @@ class Trainer:
                                              pruned.pos_of[l], pruned.layer_live[l], n_live, sp)
             norms[l] = nrm
             d_h = d_prev
+        if self.grad_hook is not None:
+            self.grad_hook(grads)          # e.g. NCCL all-reduce of the flat bucket
         sgd_step(net, grads, cfg.eta)
         for layer in range(1, L):
             n_live = pruned.counts[layer][1]
@@ -322,13 +344,8 @@ class Trainer:
                                            norms[layer], pruned.keep[layer - 1], tapes[layer - 1].h_out,
                                            iteration, cache.refresh_retained, sp)
         cache.end_iteration(iteration)
-        after = cache.counters_vector()
-        host = torch.cat([loss_dev.view(1), (after - before).double(), after[CTR_VALID::LAYER_CTR_LEN]
-                          [:cache.num_layers].double()]).cpu().tolist()
-        loss, delta = host[0], [int(x) for x in host[1:1 + after.numel()]]
-        valid = int(sum(host[1 + after.numel():]))
         self.last = (pruned, tapes, grads, norms)
-        return self._metrics(iteration, epoch, len(sub.seeds), loss, delta, baseline, valid, sub)
+        return loss_dev, baseline
 
     def _metrics(self, iteration, epoch, num_seeds, loss, delta, baseline, valid, sub):
         nl = self.cache.num_layers
