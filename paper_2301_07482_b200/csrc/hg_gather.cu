@@ -8,9 +8,9 @@
 // matrix at their local frontier position. Non-live rows are not touched
 // (no kernel ever reads them).
 //
-// Work is flattened to (row, 16-byte vector) items so consecutive threads
-// read consecutive 16 B of the same row (coalesced 128-bit loads, no L1
-// allocation) and each thread keeps kUnroll independent loads in flight.
+// A warp owns groups of kRows rows; consecutive lanes read consecutive 16 B of
+// a row (coalesced 128-bit loads, no L1 allocation), and all loads of the group
+// are issued before any store (memory-level parallelism per warp = kRows rows).
 #include "hgb200.h"
 #include <cuda_fp16.h>
 
@@ -20,9 +20,14 @@
 namespace hg {
 namespace {
 
-constexpr int kUnroll = 4;
+constexpr int kRows = 8;        // rows a warp keeps in flight
+constexpr int kMaxT = 4;        // 16-byte vectors per lane per row (rows <= 2 KB)
 
-template <typename TIn>
+// One warp per group of kRows live rows. Lanes < kRows resolve the index chain
+// (live -> node id -> region row) for the whole group at once, then every lane
+// issues its 16-byte loads for all kRows rows before the first store, so each
+// warp has up to kRows * kMaxT independent 128-bit loads in flight.
+template <typename TIn, int kT>
 __global__ void __launch_bounds__(256) k_load_rows(const int32_t* n_live_dev, const int32_t* __restrict__ live,
                                                    const int32_t* __restrict__ src_nodes,
                                                    const int32_t* __restrict__ feature_row_of,
@@ -31,50 +36,56 @@ __global__ void __launch_bounds__(256) k_load_rows(const int32_t* n_live_dev, co
                                                    unsigned long long* __restrict__ gctr) {
   constexpr int kPerVec = 16 / sizeof(TIn);  // elements per 16-byte vector
   const int nvec = dim / kPerVec;
-  const long long n_items = (long long)(*n_live_dev) * nvec;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long base = (long long)blockIdx.x * blockDim.x + threadIdx.x; base < n_items;
-       base += stride * kUnroll) {
-    uint4 val[kUnroll];
-    float* dst[kUnroll];
-    bool hit[kUnroll], first[kUnroll], ok[kUnroll];
+  const int n = *n_live_dev;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g * kRows < n; g += warps) {
+    const int i = g * kRows + lane;
+    int loc = -1;
+    const TIn* row = nullptr;
+    bool hit = false;
+    if (lane < kRows && i < n) {
+      loc = live[i];
+      const int id = src_nodes[loc];
+      const int fr = feature_row_of ? feature_row_of[id] : -1;
+      hit = fr >= 0;
+      row = hit ? region + (long long)fr * dim : feats + (long long)id * dim;
+    }
+    const unsigned hits = __ballot_sync(0xffffffffu, hit);
+    const unsigned valid = __ballot_sync(0xffffffffu, loc >= 0);
+    uint4 val[kRows][kT];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const long long it = base + u * stride;
-      ok[u] = it < n_items;
-      first[u] = false;
-      hit[u] = false;
-      dst[u] = nullptr;
-      if (ok[u]) {
-        const int i = (int)(it / nvec);
-        const int v = (int)(it - (long long)i * nvec);
-        const int loc = live[i];
-        const int id = src_nodes[loc];
-        const int fr = feature_row_of ? feature_row_of[id] : -1;
-        hit[u] = fr >= 0;
-        first[u] = v == 0;
-        const TIn* row = hit[u] ? region + (long long)fr * dim : feats + (long long)id * dim;
-        val[u] = ldg_stream_u4(reinterpret_cast<const uint4*>(row) + v);
-        dst[u] = out + (long long)loc * dim + (long long)v * kPerVec;
+    for (int r = 0; r < kRows; ++r) {
+      const TIn* p = reinterpret_cast<const TIn*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(row), r));
+#pragma unroll
+      for (int t = 0; t < kT; ++t) {
+        const int v = lane + 32 * t;
+        if (((valid >> r) & 1u) && v < nvec) val[r][t] = ldg_stream_u4(reinterpret_cast<const uint4*>(p) + v);
       }
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (!ok[u]) continue;
-      if (sizeof(TIn) == 4) {
-        *reinterpret_cast<uint4*>(dst[u]) = val[u];
-      } else {
-        const __half2* h = reinterpret_cast<const __half2*>(&val[u]);
-        float2 a = __half22float2(h[0]), b = __half22float2(h[1]);
-        float2 c = __half22float2(h[2]), d = __half22float2(h[3]);
-        reinterpret_cast<float4*>(dst[u])[0] = make_float4(a.x, a.y, b.x, b.y);
-        reinterpret_cast<float4*>(dst[u])[1] = make_float4(c.x, c.y, d.x, d.y);
+    for (int r = 0; r < kRows; ++r) {
+      const int lr = __shfl_sync(0xffffffffu, loc, r);
+      if (!((valid >> r) & 1u)) continue;
+      float* dst = out + (long long)lr * dim;
+#pragma unroll
+      for (int t = 0; t < kT; ++t) {
+        const int v = lane + 32 * t;
+        if (v >= nvec) continue;
+        if (sizeof(TIn) == 4) {
+          reinterpret_cast<uint4*>(dst)[v] = val[r][t];
+        } else {
+          const __half2* h = reinterpret_cast<const __half2*>(&val[r][t]);
+          float2 a = __half22float2(h[0]), b = __half22float2(h[1]);
+          float2 c = __half22float2(h[2]), d = __half22float2(h[3]);
+          reinterpret_cast<float4*>(dst)[2 * v] = make_float4(a.x, a.y, b.x, b.y);
+          reinterpret_cast<float4*>(dst)[2 * v + 1] = make_float4(c.x, c.y, d.x, d.y);
+        }
       }
     }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      warp_count_add(gctr + kGCtrFeatureHits, ok[u] && first[u] && hit[u]);
-      warp_count_add(gctr + kGCtrFeatureMisses, ok[u] && first[u] && !hit[u]);
+    if (lane == 0) {
+      if (hits) atomicAdd(gctr + kGCtrFeatureHits, (unsigned long long)__popc(hits));
+      if (valid & ~hits) atomicAdd(gctr + kGCtrFeatureMisses, (unsigned long long)__popc(valid & ~hits));
     }
   }
 }
@@ -95,17 +106,20 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
   if ((dim * isz) % 16) return fail(W, kBadArg, "feature row bytes must be a multiple of 16");
   if ((reinterpret_cast<uintptr_t>(feats) | reinterpret_cast<uintptr_t>(h_out)) & 15)
     return fail(W, kBadArg, "feature / output pointers must be 16-byte aligned");
-  const long long items = n_live_max * (dim * isz / 16);
-  const unsigned grid = grid_for((items + kUnroll - 1) / kUnroll, 256, 148 * 8);
+  if (dim * isz > 16 * 32 * kMaxT) return fail(W, kBadArg, "feature rows above 2 KB are not supported");
+  const unsigned grid = grid_for((n_live_max + kRows - 1) / kRows * 32, 256, 148 * 8);
   auto* g = reinterpret_cast<unsigned long long*>(global_ctr);
-  if (dtype == 1)
-    k_load_rows<__half><<<grid, 256, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,
-                                                  static_cast<const __half*>(region),
-                                                  static_cast<const __half*>(feats), dim, h_out, g);
-  else
-    k_load_rows<float><<<grid, 256, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,
-                                                 static_cast<const float*>(region), static_cast<const float*>(feats),
-                                                 dim, h_out, g);
+  const int T = (dim * isz / 16 + 31) / 32;
+#define HG_LOAD(TT, KT)                                                                                     \
+  k_load_rows<TT, KT><<<grid, 256, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,               \
+                                                static_cast<const TT*>(region), static_cast<const TT*>(feats), \
+                                                dim, h_out, g)
+  if (dtype == 1) {
+    if (T == 1) HG_LOAD(__half, 1); else if (T == 2) HG_LOAD(__half, 2); else HG_LOAD(__half, 4);
+  } else {
+    if (T == 1) HG_LOAD(float, 1); else if (T == 2) HG_LOAD(float, 2); else HG_LOAD(float, 4);
+  }
+#undef HG_LOAD
   HG_LAUNCHED(W);
   return kOk;
 }

@@ -27,7 +27,7 @@ __global__ void k_prune_rows(const int32_t* n_dst_dev, const uint8_t* __restrict
                              unsigned long long* prune_writes) {
   const int n = *n_dst_dev;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    const bool k = live_dst[r] && !(inj_dst && inj_dst[r]);
+    const bool k = (!live_dst || live_dst[r]) && !(inj_dst && inj_dst[r]);
     keep[r] = k;
     if (!k) {
       end[r] = start[r];

@@ -109,8 +109,9 @@ class Network:
         """Same byte order as histgnn Network.checksum_bytes (nn.py:65-70)."""
         return b"".join(np.ascontiguousarray(_np(a)).tobytes() for p in self.layers for _, a in p.named_arrays())
 
-    def new_grads(self) -> "Grads":
-        return Grads(self, torch.zeros_like(self.flat))
+    def new_grads(self, zero: bool = True) -> "Grads":
+        """zero=False: every slab is fully overwritten by the dP GEMMs (beta=0)."""
+        return Grads(self, torch.zeros_like(self.flat) if zero else torch.empty_like(self.flat))
 
 
 @dataclass
@@ -182,7 +183,17 @@ class LayerTape:
     K: int
     relu: bool
     h_out: torch.Tensor         # [n_dst, d_out] (dead rows unwritten)
-    valid_rows: torch.Tensor    # bool [n_dst] rows that hold data (computed or injected)
+    inj: object = None          # Injection or None
+
+    @property
+    def valid_rows(self) -> torch.Tensor:
+        """bool [n_dst]: rows that hold data (computed or injected)."""
+        valid = torch.zeros(self.h_out.shape[0], dtype=torch.bool, device=self.h_out.device)
+        if self.R:
+            valid[self.rows.long()] = True
+        if self.inj is not None:
+            valid |= self.inj.flag.bool()
+        return valid
 
 
 @dataclass
@@ -217,7 +228,8 @@ def _dev_count(n: int, dev) -> torch.Tensor:
 
 
 def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch.Tensor, R: int,
-                      R_dev: torch.Tensor, act: bool, inj: Injection | None, stream) -> LayerTape:
+                      R_dev: torch.Tensor, act: bool, inj: Injection | None, stream,
+                      n_dst_dev: torch.Tensor | None = None) -> LayerTape:
     dev = h_in.device
     d_in = net.dims[l]
     d_out = net.dims[l + 1]
@@ -237,14 +249,11 @@ def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch
     h_out = torch.empty((n_dst, d_out), dtype=torch.float32, device=dev)
     _lib.call("hg_scatter_rows", _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(Z), d_out, int(act),
               _lib.ptr(h_out), stream)
-    valid = torch.zeros(n_dst, dtype=torch.bool, device=dev)
-    if R:
-        valid[rows.long()] = True
     if inj is not None:
-        _lib.call("hg_inject_rows", _lib.ptr(_dev_count(n_dst, dev)), n_dst, _lib.ptr(inj.flag),
+        nd = n_dst_dev if n_dst_dev is not None else _dev_count(n_dst, dev)
+        _lib.call("hg_inject_rows", _lib.ptr(nd), n_dst, _lib.ptr(inj.flag),
                   _lib.ptr(inj.row), _lib.ptr(inj.table), d_out, _lib.ptr(h_out), stream)
-        valid |= inj.flag.bool()
-    return LayerTape(rows, R, R_dev, A, K, act, h_out, valid)
+    return LayerTape(rows, R, R_dev, A, K, act, h_out, inj)
 
 
 def _rows_tensor(rows, n_dst, dev):
@@ -325,7 +334,7 @@ def build_csc(blk, keep: torch.Tensor, pos_of: torch.Tensor, n_dst_dev, stream, 
 
 
 def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tensor, grads: Grads,
-                       need_input: bool, keep, pos_of, live, n_live, stream):
+                       need_input: bool, keep, pos_of, live, n_live, stream, n_dst_dev=None, n_live_dev=None):
     """Writes dP into grads; returns (d_in [n_src, d_in] with rows valid on
     `live`, fp64 norms aligned with `live`) or (None, None)."""
     dev = d_h.device
@@ -343,11 +352,14 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
     SG = torch.empty((R, K), dtype=torch.float32, device=dev)
     _lib.call("hg_gemm_rm", 0, 1, R, K, d_out, _lib.ptr(dz), d_out, _lib.ptr(net.slab(l)), d_out, 0.0,
               _lib.ptr(SG), K, stream)
-    n_dst_dev = _dev_count(blk.num_dst, dev)
+    if n_dst_dev is None:
+        n_dst_dev = _dev_count(blk.num_dst, dev)
+    if n_live_dev is None:
+        n_live_dev = _dev_count(n_live, dev)
     csc = build_csc(blk, keep, pos_of, n_dst_dev, stream)
     d_in = torch.empty((blk.num_src, d_in_dim), dtype=torch.float32, device=dev)
     norms = torch.empty(max(n_live, 1), dtype=torch.float64, device=dev)
-    _lib.call("hg_transpose_agg", _kind_code(net.kind), _lib.ptr(_dev_count(n_live, dev)), n_live, _lib.ptr(live),
+    _lib.call("hg_transpose_agg", _kind_code(net.kind), _lib.ptr(n_live_dev), n_live, _lib.ptr(live),
               _lib.ptr(csc.seg_lo), _lib.ptr(csc.seg_hi), _lib.ptr(csc.vals), _lib.ptr(t.rows),
               _lib.ptr(blk.adj.start), _lib.ptr(blk.adj.end), _lib.ptr(blk.dst_deg), _lib.ptr(blk.src_deg),
               _lib.ptr(n_dst_dev), _lib.ptr(pos_of), _lib.ptr(SG), K, d_in_dim, _lib.ptr(d_in), _lib.ptr(norms),

@@ -130,6 +130,17 @@ class PrunedBatch:
     keep: list
     pos_of: list
     counts: list          # [(R_b, n_live_b)]
+    counts_dev: torch.Tensor = None   # int32 [2L]: R_b, n_live_b on the device
+    sizes_dev: torch.Tensor = None    # int32 [2L]: n_dst_b, n_src_b on the device
+
+    def R_dev(self, b):
+        return self.counts_dev[2 * b:2 * b + 1]
+
+    def n_live_dev(self, b):
+        return self.counts_dev[2 * b + 1:2 * b + 2]
+
+    def n_dst_dev(self, b):
+        return self.sizes_dev[2 * b:2 * b + 1]
 
     def injected_np(self, b: int):
         """Reference form (local rows sorted ascending, values) of injected[b]."""
@@ -155,7 +166,7 @@ def prune_with_cache(sub: LayeredSubgraph, cache: HistCache, current_iter: int, 
         sizes += [blk.num_dst, blk.num_src]
     size_dev = torch.tensor(sizes, dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
     counts = torch.zeros(2 * L, dtype=torch.int32, device=dev)
-    live_dst = torch.ones(B, dtype=torch.uint8, device=dev)
+    live_dst = None          # NULL = every seed row is live
     inj_flag = None
     compute, injected, live, keep_l, pos_l = [None] * L, [None] * L, [None] * (L + 1), [None] * L, [None] * L
     rows_buf, live_buf = [None] * L, [None] * L
@@ -194,7 +205,7 @@ def prune_with_cache(sub: LayeredSubgraph, cache: HistCache, current_iter: int, 
         live[b] = live_buf[b][:nl]
         sub.layers[b].adj.prune_writes += sub.layers[b].num_dst - R
     live[L] = torch.arange(B, dtype=torch.int32, device=dev)
-    return PrunedBatch(sub, compute, injected, live, keep_l, pos_l, cnt)
+    return PrunedBatch(sub, compute, injected, live, keep_l, pos_l, cnt, counts, size_dev)
 
 
 # ----------------------------------------------------------------- trainer
@@ -276,7 +287,7 @@ class Trainer:
         h = torch.empty((b0.num_src, self.feature_dim), dtype=torch.float32, device=dev)
         n_live0 = pruned.counts[0][1]
         region = self.cache.feature_table if self.cache.feature_table is not None else self.features
-        _lib.call("hg_load_features", _lib.ptr(_dev_count(n_live0, dev)), n_live0, _lib.ptr(pruned.layer_live[0]),
+        _lib.call("hg_load_features", _lib.ptr(pruned.n_live_dev(0)), n_live0, _lib.ptr(pruned.layer_live[0]),
                   _lib.ptr(b0.src_nodes), _lib.ptr(self.cache.feature_row_of_dev), _lib.ptr(region),
                   _lib.ptr(self.features), self.feature_dim, self._dtype_code, _lib.ptr(h),
                   _lib.ptr(self.cache.gctr), sp)
@@ -319,18 +330,19 @@ class Trainer:
         h = h0
         for b in range(L):
             R, _ = pruned.counts[b]
-            t = layer_forward_dev(net, b, sub.layers[b], h, pruned.compute_rows[b], R, _dev_count(R, dev),
-                                  b < L - 1, pruned.injected[b], sp)
+            t = layer_forward_dev(net, b, sub.layers[b], h, pruned.compute_rows[b], R, pruned.R_dev(b),
+                                  b < L - 1, pruned.injected[b], sp, pruned.n_dst_dev(b))
             tapes.append(t)
             h = t.h_out
         B = int(sub.seeds.shape[0])
         d_h, loss_dev = cross_entropy_dev(tapes[-1].h_out, labels_dev, B, net.dims[-1], sp)
-        grads = net.new_grads()
+        grads = net.new_grads(zero=False)
         norms = [None] * L
         for l in range(L - 1, -1, -1):
             n_live = pruned.counts[l][1]
             d_prev, nrm = layer_backward_dev(net, l, sub.layers[l], tapes[l], d_h, grads, l >= 1, pruned.keep[l],
-                                             pruned.pos_of[l], pruned.layer_live[l], n_live, sp)
+                                             pruned.pos_of[l], pruned.layer_live[l], n_live, sp,
+                                             pruned.n_dst_dev(l), pruned.n_live_dev(l))
             norms[l] = nrm
             d_h = d_prev
         if self.grad_hook is not None:
