@@ -85,6 +85,18 @@ int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int3
 int hg_gemm_rm(int transA, int transB, long long M, long long N, long long K, const float* A, long long lda,
                const float* B, long long ldb, float beta, float* C, long long ldc, cudaStream_t stream);
 
+/* ---- K7 on tcgen05 (3 x bf16 split, fp32 accumulate in TMEM; hg_tcgemm.cu) ----
+ * forward: h_out[rows[i]] = relu?( A[i, :K1] . P )           nn.py:150,156,161-162,289
+ * dgrad:   SG = dz . P[:K]^T                                   nn.py:171,175-176
+ * wgrad:   dP = A[:, :K1]^T . dz  (split-K, fixed-order sum)   nn.py:170,173-174
+ * R (rows) may live on the device (R_dev), R_max sizes the grid. */
+int hg_tc_linear_fwd(const int32_t* R_dev, long long R_max, const float* A, long long ldA, int K1, const float* P,
+                     int N, const int32_t* rows, int relu, float* h_out, cudaStream_t stream);
+int hg_tc_linear_dgrad(const int32_t* R_dev, long long R_max, const float* dz, int N, const float* P, int K,
+                       float* SG, cudaStream_t stream);
+int hg_tc_linear_wgrad(const int32_t* R_dev, long long R_max, const float* A, long long ldA, int K1, const float* dz,
+                       int N, float* dP, float* partial, int splits, cudaStream_t stream);
+
 /* ---- forward epilogue: nn.py:161-162,288-293 (ReLU, h_full[rows], injected rows) */
 int hg_scatter_rows(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* Z, int dout, int relu,
                     float* h_out, cudaStream_t stream);

@@ -54,6 +54,9 @@ SIGNATURES = {
     "hg_degree_order_scratch_bytes": (I64, [I64]),
     "hg_feature_region": (I32, [P, P, I64, I64, P, P, P, I64, P]),
     "hg_synth_power_law": (I64, [I64, I32, U64, P, P]),
+    "hg_tc_linear_fwd": (I32, [P, I64, P, I64, I32, P, I32, P, I32, P, P]),
+    "hg_tc_linear_dgrad": (I32, [P, I64, P, I32, P, I32, P, P]),
+    "hg_tc_linear_wgrad": (I32, [P, I64, P, I64, I32, P, I32, P, P, I32, P]),
 }
 
 _lib = None

@@ -21,6 +21,7 @@ node gradients fill them with zeros like the reference.
 from __future__ import annotations
 
 import enum
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -30,6 +31,17 @@ from . import _lib
 from .graphs import _np
 
 KIND_GCN, KIND_SAGE = 0, 1
+
+# Dense transform engine: the tcgen05 kernels (hg_tc_linear_*). "cublas"
+# (fp32 SGEMM) is kept only as a cross-check for tests/diagnostics.
+GEMM_ENGINE = os.environ.get("HG_GEMM", "tcgen05")
+
+
+def _wgrad_splits(R: int, K1: int, n: int) -> int:
+    """Split-K factor for dP = A^T dz: fill ~2 CTAs per SM, >= 8 chunks each."""
+    tiles = ((K1 + 127) // 128) * ((n + 255) // 256)
+    chunks = max(1, (R + 31) // 32)
+    return max(1, min(2 * 148 // tiles, chunks // 8))
 
 
 class LayerKind(enum.Enum):
@@ -242,13 +254,18 @@ def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch
     _lib.call("hg_aggregate_fwd", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(blk.adj.start),
               _lib.ptr(blk.adj.end), _lib.ptr(blk.adj.col_indices), _lib.ptr(blk.dst_deg), _lib.ptr(blk.src_deg),
               _lib.ptr(h_in), d_in, _lib.ptr(A), ldA, stream)
-    Z = torch.empty((R, d_out), dtype=torch.float32, device=dev)
-    _lib.call("hg_gemm_rm", 0, 0, R, d_out, K + 1, _lib.ptr(A), ldA, _lib.ptr(net.slab(l)), d_out, 0.0,
-              _lib.ptr(Z), d_out, stream)
     n_dst = blk.num_dst
     h_out = torch.empty((n_dst, d_out), dtype=torch.float32, device=dev)
-    _lib.call("hg_scatter_rows", _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(Z), d_out, int(act),
-              _lib.ptr(h_out), stream)
+    if GEMM_ENGINE == "tcgen05":
+        # z = [A | 1] . P on tcgen05, ReLU + scatter to h_out[rows] in the epilogue
+        _lib.call("hg_tc_linear_fwd", _lib.ptr(R_dev), R, _lib.ptr(A), ldA, K + 1, _lib.ptr(net.slab(l)), d_out,
+                  _lib.ptr(rows), int(act), _lib.ptr(h_out), stream)
+    else:
+        Z = torch.empty((R, d_out), dtype=torch.float32, device=dev)
+        _lib.call("hg_gemm_rm", 0, 0, R, d_out, K + 1, _lib.ptr(A), ldA, _lib.ptr(net.slab(l)), d_out, 0.0,
+                  _lib.ptr(Z), d_out, stream)
+        _lib.call("hg_scatter_rows", _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(Z), d_out, int(act),
+                  _lib.ptr(h_out), stream)
     if inj is not None:
         nd = n_dst_dev if n_dst_dev is not None else _dev_count(n_dst, dev)
         _lib.call("hg_inject_rows", _lib.ptr(nd), n_dst, _lib.ptr(inj.flag),
@@ -345,13 +362,23 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
               int(t.relu), _lib.ptr(dz), stream)
     dP = grads.slab(l)
     ldA = K + 4
-    _lib.call("hg_gemm_rm", 1, 0, K + 1, d_out, R, _lib.ptr(t.A), ldA, _lib.ptr(dz), d_out, 0.0,
-              _lib.ptr(dP), d_out, stream)
+    if GEMM_ENGINE == "tcgen05":
+        splits = _wgrad_splits(R, K + 1, d_out)
+        part = torch.empty(splits * (K + 1) * d_out, dtype=torch.float32, device=dev)
+        _lib.call("hg_tc_linear_wgrad", _lib.ptr(t.R_dev), R, _lib.ptr(t.A), ldA, K + 1, _lib.ptr(dz), d_out,
+                  _lib.ptr(dP), _lib.ptr(part), splits, stream)
+    else:
+        _lib.call("hg_gemm_rm", 1, 0, K + 1, d_out, R, _lib.ptr(t.A), ldA, _lib.ptr(dz), d_out, 0.0,
+                  _lib.ptr(dP), d_out, stream)
     if not need_input:
         return None, None
     SG = torch.empty((R, K), dtype=torch.float32, device=dev)
-    _lib.call("hg_gemm_rm", 0, 1, R, K, d_out, _lib.ptr(dz), d_out, _lib.ptr(net.slab(l)), d_out, 0.0,
-              _lib.ptr(SG), K, stream)
+    if GEMM_ENGINE == "tcgen05":
+        _lib.call("hg_tc_linear_dgrad", _lib.ptr(t.R_dev), R, _lib.ptr(dz), d_out, _lib.ptr(net.slab(l)), K,
+                  _lib.ptr(SG), stream)
+    else:
+        _lib.call("hg_gemm_rm", 0, 1, R, K, d_out, _lib.ptr(dz), d_out, _lib.ptr(net.slab(l)), d_out, 0.0,
+                  _lib.ptr(SG), K, stream)
     if n_dst_dev is None:
         n_dst_dev = _dev_count(blk.num_dst, dev)
     if n_live_dev is None:
