@@ -263,21 +263,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_tcgemm(GemmShape sh, OpA opA, O
     if (uses[st] > 0) mbar_wait(&mbar[st], (uses[st] - 1) & 1);
   tc_fence_after();
 
-  const int row = m0 + warp * 32 + (tid & 31);
+  // Epilogue: TMEM lane = tile row, so each thread holds one row; stage 32x32
+  // sub-tiles through shared memory (the operand stages are free now) so the
+  // global stores are row-contiguous (one 128 B segment per row per warp op).
+  const int lane = tid & 31;
   const bool have = c_end > c_begin;
-  for (int c0 = 0; c0 < n_valid; c0 += 16) {
-    float acc[16];
+  float* stage_f = reinterpret_cast<float*>(smem) + warp * 32 * 33;
+  for (int c0 = 0; c0 < n_valid; c0 += 32) {
+    float acc[32];
     if (have) {
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, acc);
+      float* a0 = acc;
+      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, *reinterpret_cast<float(*)[16]>(a0));
+      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c0 + 16), *reinterpret_cast<float(*)[16]>(a0 + 16));
     } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+      for (int j = 0; j < 32; ++j) acc[j] = 0.f;
     }
-    if (row < M) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (c0 + j < n_valid) epi.store(row, n0 + c0 + j, acc[j]);
+    for (int j = 0; j < 32; ++j) stage_f[lane * 33 + j] = acc[j];
+    __syncwarp();
+    const int col = c0 + lane;
+    for (int r = 0; r < 32; ++r) {
+      const int row = m0 + warp * 32 + r;
+      if (row < M && col < n_valid) epi.store(row, n0 + col, stage_f[r * 33 + lane]);
     }
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
