@@ -208,7 +208,8 @@ def main():
 
     # ---- timed region 1: device-resident steps (value) ----
     clocks = ClockSampler(local)
-    prof_names = ["hg_load_features", "hg_aggregate_fwd", "hg_transpose_agg", "hg_sample_layer"]
+    # events only around the roofline kernel (2 events per step; negligible)
+    prof_names = ["hg_load_features"]
     barrier()
     torch.cuda.synchronize()
     clocks.start()

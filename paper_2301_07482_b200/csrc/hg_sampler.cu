@@ -120,6 +120,45 @@ __global__ void k_stamp(const int32_t* __restrict__ frontier, const int32_t* F_d
 
 constexpr int kSelThreads = 256;
 
+// packed (key53 << 11 | j) compare-exchange: one 64-bit order == (key, j) order
+__device__ __forceinline__ void cmpx64(unsigned long long& k, int partner_mask, bool keep_min) {
+  const unsigned long long p = __shfl_xor_sync(0xffffffffu, k, partner_mask);
+  if (keep_min ? (p < k) : (k < p)) k = p;
+}
+__device__ __forceinline__ void bitonic_sort32_u64(unsigned long long& k) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const bool ascending = (lane & size) == 0 || size == 32;
+      cmpx64(k, stride, ((lane & stride) == 0) == ascending);
+    }
+  }
+}
+__device__ __forceinline__ void bitonic_merge32_u64(unsigned long long& k) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) cmpx64(k, stride, (lane & stride) == 0);
+}
+
+// jump with the per-batch constants C = inc * S precomputed (one 128-bit
+// multiply-add per non-zero nibble of the offset)
+struct JumpTableC {
+  u128 A[16][16];
+  u128 C[16][16];
+};
+__device__ __forceinline__ u128 pcg_jump_c(const JumpTableC& tab, u128 s, unsigned long long k) {
+  int w = 0;
+  while (k) {
+    const unsigned d = (unsigned)(k & 15ull);
+    if (d) s = fma128(tab.A[w][d], s, tab.C[w][d]);
+    k >>= 4;
+    ++w;
+  }
+  return s;
+}
+
 template <bool kSmallFanout>
 __global__ void __launch_bounds__(kSelThreads) k_select(
     const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end, const int32_t* __restrict__ g_col,
@@ -127,22 +166,18 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
     const unsigned long long* stream_pos, const int64_t* __restrict__ cand_off,
     const int32_t* __restrict__ blk_off, unsigned epoch, const int64_t* __restrict__ g2l,
     uint32_t* __restrict__ bitmap, int32_t* __restrict__ src_flat) {
-  __shared__ JumpTable tab;
-  {
-    const u128* srcA = &g_jump.A[0][0];
-    u128* dstA = &tab.A[0][0];
-    for (int t = threadIdx.x; t < 256; t += blockDim.x) {
-      dstA[t] = srcA[t];
-      (&tab.S[0][0])[t] = (&g_jump.S[0][0])[t];
-    }
+  __shared__ JumpTableC tab;
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) {
+    (&tab.A[0][0])[t] = (&g_jump.A[0][0])[t];
+    (&tab.C[0][0])[t] = mul128(inc, (&g_jump.S[0][0])[t]);
   }
   __syncthreads();
   const int F = *F_dev;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const unsigned long long base0 = *stream_pos;
-  const u128 a32 = tab.A[1][2];            // MULT^32
-  const u128 c32 = mul128(inc, tab.S[1][2]);
+  const u128 a32 = tab.A[1][2];            // MULT^32 and its increment term
+  const u128 c32 = tab.C[1][2];
   for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < F; row += warps) {
     const int v = frontier[row];
     const long long lo = g_start[v];
@@ -152,10 +187,34 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
     if (deg == 0) continue;
     const unsigned long long k0 = base0 + (unsigned long long)cand_off[row];
     // lane state: output index k0+lane needs k0+lane+1 steps
-    const u128 first = pcg_jump(tab, s0, inc, k0 + (unsigned long long)lane + 1ull);
-    unsigned long long pick_k;
-    unsigned pick_j;
-    if (kSmallFanout) {
+    const u128 first = pcg_jump_c(tab, s0, k0 + (unsigned long long)lane + 1ull);
+    if (kSmallFanout && deg <= 2048) {
+      // fast path: (key53, j) packed into one u64, j < 2^11
+      unsigned long long best = ~0ull;
+      u128 s = first;
+      for (long long c = 0; c < deg; c += 32) {
+        const long long jj = c + lane;
+        const bool valid = jj < deg;
+        unsigned long long key = valid ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
+        if (c + 32 < deg) s = fma128(a32, s, c32);
+        if (c == 0) {
+          bitonic_sort32_u64(key);
+          best = key;
+          continue;
+        }
+        const unsigned long long thr = __shfl_sync(0xffffffffu, best, fanout - 1);
+        if (!__ballot_sync(0xffffffffu, key < thr)) continue;
+        bitonic_sort32_u64(key);
+        const unsigned long long r = __shfl_sync(0xffffffffu, key, 31 - lane);
+        if (r < best) best = r;
+        bitonic_merge32_u64(best);
+      }
+      if (lane < count) {
+        const int u = g_col[lo + (long long)(best & 2047ull)];
+        src_flat[out0 + lane] = u;
+        if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
+      }
+    } else if (kSmallFanout) {
       unsigned long long bk = ~0ull;
       unsigned bj = ~0u;
       u128 s = first;
@@ -177,10 +236,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
         }
         bitonic_merge32(bk, bj);
       }
-      pick_k = bk;
-      pick_j = bj;
       if (lane < count) {
-        const int u = g_col[lo + pick_j];
+        const int u = g_col[lo + bj];
         src_flat[out0 + lane] = u;
         if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
       }
@@ -224,8 +281,6 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
           if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
         }
       }
-      (void)pick_k;
-      (void)pick_j;
     }
   }
 }
