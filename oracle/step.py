@@ -392,9 +392,10 @@ class OTrainer:
         return sample_layered(self.start, self.end, self.col, self.num_nodes, seeds,
                               self.cfg.fanouts, batch_rng(self.cfg.seed, idx))
 
-    def train_iteration(self, it, epoch, sub: OSubgraph, norms_override=None):
+    def train_iteration(self, it, epoch, sub: OSubgraph, norms_override=None, grad_hook=None):
         """norms_override: optional {layer: fp64 norms aligned with the live
-        rows} — the teacher-forced (lockstep) mode of SURVEY §8(c) Mode B."""
+        rows} — the teacher-forced (lockstep) mode of SURVEY §8(c) Mode B.
+        grad_hook(grads): called before SGD (data-parallel gradient averaging)."""
         before = self.cache.counters()
         f0 = self.source.fetched_bytes
         pr = prune_with_cache(sub, self.cache, it)
@@ -402,6 +403,8 @@ class OTrainer:
         tape = forward_pass(self.network, sub.layers, h0, pr.compute_rows, pr.injected)
         loss, dlog = cross_entropy(tape.logits, self.labels[sub.seeds])
         grads, ng, _ = backward(self.network, sub.layers, tape, dlog, need_input=False)
+        if grad_hook is not None:
+            grad_hook(grads)
         sgd_step(self.network, grads, self.cfg.eta)
         used_norms = {}
         for layer in range(1, sub.num_layers):

@@ -1,0 +1,70 @@
+"""Data-parallel GPU path with two ranks sharing one B200 (gloo carries the
+CUDA-tensor all-reduce because NCCL refuses duplicate GPUs): both ranks end
+with bitwise-identical weights, and step 0 (no cache history yet) matches the
+serial DP oracle's loss within 1e-3 and its integer metrics exactly."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+WORLD, STEPS = 2, 4
+
+
+def _data():
+    from oracle.datagen import csr2_from_edges, power_law_dataset
+    ds = power_law_dataset(1500, np.random.default_rng(2), m=3, feature_dim=8)
+    return ds, csr2_from_edges(ds.src, ds.dst, ds.num_nodes)
+
+
+def _worker(rank, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    torch.cuda.set_device(0)
+    import paper_2301_07482_b200 as hg
+    from paper_2301_07482_b200.distributed import make_allreduce_hook, rank_batch_indices
+    ds, g = _data()
+    cfg = hg.TrainConfig(fanouts=(6, 4, 3), hidden=16, batch_size=96, epochs=1, eta=0.05,
+                         kind=hg.LayerKind.SAGE_MEAN, p_grad=0.9, t_stale=3, seed=5)
+    tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
+    tr.grad_hook = make_allreduce_hook(WORLD)
+    batches = hg.make_batches(ds.train_ids, cfg)
+    ms = []
+    for idx in rank_batch_indices(len(batches), rank, WORLD)[:STEPS]:
+        m = tr.train_iteration(idx, 0, tr.sample(idx, batches[idx]))
+        ms.append([m.hits, m.misses, m.admissions, m.fetched_bytes, m.prune_writes, m.loss])
+    np.save(os.path.join(out_dir, f"r{rank}_metrics.npy"), np.array(ms, dtype=np.float64))
+    np.save(os.path.join(out_dir, f"r{rank}_w.npy"), np.frombuffer(tr.network.checksum_bytes(), np.uint8))
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_two_rank_dp_on_one_gpu(tmp_path):
+    from oracle.dp import dp_serial_run
+    from oracle.step import SAGE, OTrainConfig
+    mp.start_processes(_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True, start_method="spawn")
+    w0 = np.load(tmp_path / "r0_w.npy")
+    w1 = np.load(tmp_path / "r1_w.npy")
+    np.testing.assert_array_equal(w0, w1)
+    ds, g = _data()
+    ocfg = OTrainConfig(fanouts=(6, 4, 3), hidden=16, batch_size=96, epochs=1, eta=0.05, kind=SAGE,
+                        p_grad=0.9, t_stale=3, seed=5)
+    metrics, _ = dp_serial_run(g, ds.features, ds.labels, ds.train_ids, ocfg, ds.num_classes, WORLD, 1)
+    for r in range(WORLD):
+        got = np.load(tmp_path / f"r{r}_metrics.npy")[0]
+        m = metrics[r][0]
+        np.testing.assert_array_equal(got[:5], [m.hits, m.misses, m.admissions, m.fetched_bytes, m.prune_writes])
+        assert abs(got[5] - m.loss) <= 1e-3 * abs(m.loss)
