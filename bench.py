@@ -188,8 +188,8 @@ def main():
         raise SystemExit(f"need {need} batches, epoch has {len(batches)}")
     # rank r takes batch indices world*s + r (iteration number = global batch index)
     mine = [world * s + rank for s in range(args.warmup + 2 * args.steps)]
-    seeds_dev = [torch.as_tensor(batches[i].astype(np.int32), device=dev) for i in mine]
-    labels_dev = [torch.as_tensor(labels[batches[i]].astype(np.int32), device=dev) for i in mine]
+    # inputs of the device-resident steps packed into HBM before timing
+    staged = tr.prestage(mine[: args.warmup + args.steps], [batches[i] for i in mine[: args.warmup + args.steps]])
 
     def barrier():
         if world > 1:
@@ -203,7 +203,7 @@ def main():
         return float(t.item())
 
     for s in range(args.warmup):
-        tr.train_step_device(mine[s], seeds_dev[s], labels_dev[s])
+        tr.train_step_resident(staged[s])
     torch.cuda.synchronize()
 
     # ---- timed region 1: device-resident steps (value) ----
@@ -219,7 +219,7 @@ def main():
     e0.record()
     losses = []
     for s in range(args.warmup, args.warmup + args.steps):
-        losses.append(tr.train_step_device(mine[s], seeds_dev[s], labels_dev[s]))
+        losses.append(tr.train_step_resident(staged[s]))
     e1.record()
     torch.cuda.synchronize()
     prof = _lib.disable_profile()
@@ -259,15 +259,14 @@ def main():
     h2d = d2h = 0
     for s in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
         it = mine[s]
-        sub = tr.sample(it, batches[it])
-        m = tr.train_iteration(it, 0, sub)
+        m = tr.train_step(it, 0, batches[it])
         h2d += batches[it].size * 4 * 2          # seed ids + labels (int32)
         d2h += (1 + tr.cache.counters_vector().numel() + tr.cache.num_layers) * 8
     torch.cuda.synchronize()
     t_e2e = max_over_ranks(time.perf_counter() - t0)
     e2e = {"value": BATCH * world * args.steps / t_e2e, "unit": "seeds/s",
            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-           "api": "Trainer.sample + Trainer.train_iteration (IterMetrics read back every step)"}
+           "api": "Trainer.train_step (host seeds in, IterMetrics read back every step)"}
 
     out = dict(base, value=value, ms_per_step=1e3 * t_dev / args.steps, e2e=e2e, roofline=roofline,
                gpu_launches=int(launches), clocks=clk, per_kernel=per_kernel,

@@ -36,9 +36,11 @@ long long hg_kernel_launches(void);
 
 /* ---- K1+K2 sampler: histgnn/sampler.py:118-163 (_sample_in_neighbors,
  * _build_block), called per layer by sampler.py:166-190 (sample_layered).
- * PCG64 state/inc are the 128-bit halves of
- * default_rng(SeedSequence((seed, batch))) (sampler.py:104-106);
- * *stream_pos_dev = draws consumed before this layer, advanced by sum(deg).
+ * state_dev (u64[6], device): [0..3] = PCG64 state hi/lo, inc hi/lo of
+ * default_rng(SeedSequence((seed, batch))) (sampler.py:104-106); [4] = draws
+ * consumed before this layer (advanced by sum(deg)); [5] = g2l stamp epoch
+ * (start at 1, advanced per layer). Device-resident so a captured CUDA graph
+ * replays with new batches.
  * Outputs: block CSR offsets blk_off[F+1] (start = blk_off[i], end = blk_end[i]),
  * dst_deg[F], col_local[E], src_out = frontier ++ sorted new nodes,
  * counts_dev[0] = E, counts_dev[1] = n_src. g2l (int64[N]) must start as -1;
@@ -46,8 +48,7 @@ long long hg_kernel_launches(void);
 long long hg_sample_layer_scratch_bytes(long long F_max, long long num_nodes);
 int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t* g_col, long long num_nodes,
                     const int32_t* frontier, const int32_t* F_dev, long long F_max, int fanout,
-                    unsigned long long st_hi, unsigned long long st_lo, unsigned long long inc_hi,
-                    unsigned long long inc_lo, unsigned long long* stream_pos_dev, unsigned epoch, int64_t* g2l,
+                    unsigned long long* state_dev, int64_t* g2l,
                     uint32_t* bitmap, int64_t* cand_off, int32_t* blk_off, int32_t* blk_end, int32_t* dst_deg,
                     int32_t* src_flat, int32_t* col_local, int32_t* src_out, int32_t* counts_dev, void* scratch,
                     long long scratch_bytes, cudaStream_t stream);
@@ -63,10 +64,12 @@ int hg_prune_block(const int32_t* n_dst_dev, long long n_dst_max, const int32_t*
                    long long scratch_bytes, cudaStream_t stream);
 
 /* ---- K4 cache lookup: histgnn/cache.py:103-129 (_LayerCache.lookup) via
- * cache.py:269-285 (HistCache.lookup, layer >= 1). t_stale may be +inf. */
+ * cache.py:269-285 (HistCache.lookup, layer >= 1). t_stale may be +inf;
+ * the current iteration is read from it_dev. */
 int hg_cache_lookup(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const int32_t* src_nodes,
-                    long long n_src_max, int32_t* row_of, const int32_t* admit_iter, int32_t* row_owner, int it,
-                    double t_stale, uint8_t* hit_flag, int32_t* hit_row, long long* layer_ctr, cudaStream_t stream);
+                    long long n_src_max, int32_t* row_of, const int32_t* admit_iter, int32_t* row_owner,
+                    const int32_t* it_dev, double t_stale, uint8_t* hit_flag, int32_t* hit_row, long long* layer_ctr,
+                    cudaStream_t stream);
 
 /* ---- K5 feature load: histgnn/trainer.py:326-343 (Trainer._load_input),
  * cache.py:274-284 (feature region), trainer.py:213-228 (FeatureSource.fetch).
@@ -131,12 +134,13 @@ int hg_sgd(float* params, const float* grads, long long n, float eta, cudaStream
  * _count_overwrites cache.py:131-186. Two stages so the host can size the
  * ring table on first use (cache.py:79-91) after reading n_write. */
 long long hg_cache_update_scratch_bytes(long long n_max);
-int hg_cache_rank(int n, int k, const int32_t* live, const int32_t* src_nodes, const double* norms,
-                  const uint8_t* computed_flag, int32_t* row_of, int32_t* row_owner, long long* layer_ctr,
-                  void* scratch, long long scratch_bytes, cudaStream_t stream);
-int hg_cache_write(int n, int k, int cap, int H, int it, double t_stale, int refresh_retained, const int32_t* live,
-                   const float* emb, float* table, int32_t* row_of, int32_t* row_owner, int32_t* admit_iter,
-                   long long* layer_ctr, void* scratch, long long scratch_bytes, cudaStream_t stream);
+int hg_cache_rank(const int32_t* n_dev, int n_max, double p_grad, const int32_t* live, const int32_t* src_nodes,
+                  const double* norms, const uint8_t* computed_flag, int32_t* row_of, int32_t* row_owner,
+                  long long* layer_ctr, void* scratch, long long scratch_bytes, cudaStream_t stream);
+int hg_cache_write(int n_max, int cap, int H, const int32_t* it_dev, double t_stale, int refresh_retained,
+                   const int32_t* live, const float* emb, float* table, int32_t* row_of, int32_t* row_owner,
+                   int32_t* admit_iter, long long* layer_ctr, void* scratch, long long scratch_bytes,
+                   cudaStream_t stream);
 
 /* ---- static feature region: histgnn/cache.py:338-351 (backfill_features) */
 long long hg_degree_order_scratch_bytes(long long n);

@@ -31,11 +31,10 @@ SIGNATURES = {
     "hg_device_sync": (I32, []),
     "hg_kernel_launches": (I64, []),
     "hg_sample_layer_scratch_bytes": (I64, [I64, I64]),
-    "hg_sample_layer": (I32, [P, P, P, I64, P, P, I64, I32, U64, U64, U64, U64, P, U32, P, P, P, P, P,
-                              P, P, P, P, P, P, I64, P]),
+    "hg_sample_layer": (I32, [P, P, P, I64, P, P, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, I64, P]),
     "hg_prune_scratch_bytes": (I64, [I64]),
     "hg_prune_block": (I32, [P, I64, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P]),
-    "hg_cache_lookup": (I32, [P, I64, P, P, I64, P, P, P, I32, F64, P, P, P, P]),
+    "hg_cache_lookup": (I32, [P, I64, P, P, I64, P, P, P, P, F64, P, P, P, P]),
     "hg_load_features": (I32, [P, I64, P, P, P, P, P, I32, I32, P, P, P]),
     "hg_aggregate_fwd": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, P, I32, P]),
     "hg_gemm_rm": (I32, [I32, I32, I64, I64, I64, P, I64, P, I64, F32, P, I64, P]),
@@ -49,8 +48,8 @@ SIGNATURES = {
     "hg_row_norms": (I32, [P, I64, I32, P, P]),
     "hg_sgd": (I32, [P, P, I64, F32, P]),
     "hg_cache_update_scratch_bytes": (I64, [I64]),
-    "hg_cache_rank": (I32, [I32, I32, P, P, P, P, P, P, P, P, I64, P]),
-    "hg_cache_write": (I32, [I32, I32, I32, I32, I32, F64, I32, P, P, P, P, P, P, P, P, I64, P]),
+    "hg_cache_rank": (I32, [P, I32, F64, P, P, P, P, P, P, P, P, I64, P]),
+    "hg_cache_write": (I32, [I32, I32, I32, P, F64, I32, P, P, P, P, P, P, P, P, I64, P]),
     "hg_degree_order_scratch_bytes": (I64, [I64]),
     "hg_feature_region": (I32, [P, P, I64, I64, P, P, P, I64, P]),
     "hg_synth_power_law": (I64, [I64, I32, U64, P, P]),

@@ -35,6 +35,10 @@ _LAYER_IDX = {"hits": CTR_HITS, "misses": CTR_MISSES, "admissions": CTR_ADMISSIO
               "forced_evictions": CTR_FORCED, "staleness_violations": CTR_VIOLATIONS}
 
 
+def _it_dev(it: int, dev) -> torch.Tensor:
+    return torch.tensor([int(it)], dtype=torch.int32, device=dev)
+
+
 @dataclass(frozen=True)
 class CachePolicy:
     """p_grad: admitted fraction per batch (smallest gradient norms first).
@@ -143,36 +147,44 @@ class _LayerCache:
         self.ctr[CTR_HEADER] = 0
 
     # ---- device ops on (live list, src ids) views ----
-    def lookup_dev(self, n_dev, n_max, live, src_nodes, n_src_max, it, hit_flag, hit_row, stream):
+    def lookup_dev(self, n_dev, n_max, live, src_nodes, n_src_max, it_dev, hit_flag, hit_row, stream):
         if self.row_owner_dev is None:
             # nothing admitted yet: every probe misses, no state to invalidate
-            owner = torch.empty(1, dtype=torch.int32, device=self.device)
+            owner = self._dummy_owner()
         else:
             owner = self.row_owner_dev
         _lib.call("hg_cache_lookup", _lib.ptr(n_dev), n_max, _lib.ptr(live), _lib.ptr(src_nodes), n_src_max,
-                  _lib.ptr(self.row_of_dev), _lib.ptr(self.admit_iter_dev), _lib.ptr(owner), int(it),
+                  _lib.ptr(self.row_of_dev), _lib.ptr(self.admit_iter_dev), _lib.ptr(owner), _lib.ptr(it_dev),
                   self._t_stale(), _lib.ptr(hit_flag), _lib.ptr(hit_row), _lib.ptr(self.ctr), stream)
 
-    def update_dev(self, n, live, src_nodes, norms, computed_flag, emb, it, refresh_retained, stream,
-                   scratch=None):
-        """cache.py:188-204 for n live nodes (host-known n)."""
-        if n == 0:
+    def _dummy_owner(self):
+        if getattr(self, "_dummy", None) is None:
+            self._dummy = torch.full((1,), -1, dtype=torch.int32, device=self.device)
+        return self._dummy
+
+    def update_dev(self, n_dev, n_max, live, src_nodes, norms, computed_flag, emb, it_dev, refresh_retained,
+                   stream, allow_alloc=True):
+        """cache.py:188-204 for the n_dev[0] live nodes (n_max host bound).
+        The ring table is allocated on first use (cache.py:79-91), which reads
+        the first write count back to the host (allow_alloc=False forbids it,
+        e.g. while a CUDA graph is being captured)."""
+        if n_max <= 0:
             return
-        k = int(math.floor(self.policy.p_grad * n))
-        sb = _lib.query("hg_cache_update_scratch_bytes", n)
-        if scratch is None or scratch.numel() < sb:
-            scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
-        owner = self.row_owner_dev if self.row_owner_dev is not None else torch.full(
-            (1,), -1, dtype=torch.int32, device=self.device)
-        _lib.call("hg_cache_rank", n, k, _lib.ptr(live), _lib.ptr(src_nodes), _lib.ptr(norms),
-                  _lib.ptr(computed_flag), _lib.ptr(self.row_of_dev), _lib.ptr(owner), _lib.ptr(self.ctr),
-                  _lib.ptr(scratch), sb, stream)
+        sb = _lib.query("hg_cache_update_scratch_bytes", n_max)
+        scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        owner = self.row_owner_dev if self.row_owner_dev is not None else self._dummy_owner()
+        _lib.call("hg_cache_rank", _lib.ptr(n_dev), n_max, float(self.policy.p_grad), _lib.ptr(live),
+                  _lib.ptr(src_nodes), _lib.ptr(norms), _lib.ptr(computed_flag), _lib.ptr(self.row_of_dev),
+                  _lib.ptr(owner), _lib.ptr(self.ctr), _lib.ptr(scratch), sb, stream)
         if self.table is None:
+            if not allow_alloc:
+                raise RuntimeError("cache table must be allocated before graph capture")
             n_write = int(self.ctr[CTR_NWRITE].item())   # first use only: size the ring
             if n_write == 0:
                 return
             self.allocate(n_write)
-        _lib.call("hg_cache_write", n, k, self.capacity, self.dim, int(it), self._t_stale(),
+        row_words = self.dim * (self.table.element_size() // 4)   # rows are copied as 4-byte words
+        _lib.call("hg_cache_write", n_max, self.capacity, row_words, _lib.ptr(it_dev), self._t_stale(),
                   int(bool(refresh_retained)), _lib.ptr(live), _lib.ptr(emb), _lib.ptr(self.table),
                   _lib.ptr(self.row_of_dev), _lib.ptr(self.row_owner_dev), _lib.ptr(self.admit_iter_dev),
                   _lib.ptr(self.ctr), _lib.ptr(scratch), sb, stream)
@@ -252,7 +264,7 @@ class HistCache:
         flag = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
         hrow = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         if n:
-            lc.lookup_dev(n_dev, n, live, src, n, current_iter, flag, hrow, _lib.stream_ptr())
+            lc.lookup_dev(n_dev, n, live, src, n, _it_dev(current_iter, dev), flag, hrow, _lib.stream_ptr())
         f = _np(flag[:n]).astype(bool)
         hit_rows = (_np(lc.table[hrow[:n][flag[:n].bool()].long()]) if f.any() and lc.table is not None
                     else np.empty((0, lc.dim), dtype=self.np_dtype))
@@ -275,10 +287,11 @@ class HistCache:
         n = len(batch_nodes)
         computed = np.isin(batch_nodes, normal_nodes).astype(np.uint8)
         emb = torch.as_tensor(np.asarray(embeddings), device=dev).to(lc.dtype).contiguous()
-        lc.update_dev(n, torch.arange(n, dtype=torch.int32, device=dev),
+        lc.update_dev(torch.tensor([n], dtype=torch.int32, device=dev), n,
+                      torch.arange(n, dtype=torch.int32, device=dev),
                       torch.as_tensor(batch_nodes.astype(np.int32), device=dev),
                       torch.as_tensor(np.asarray(grad_norms, dtype=np.float64), device=dev),
-                      torch.as_tensor(computed, device=dev), emb, current_iter, self.refresh_retained,
+                      torch.as_tensor(computed, device=dev), emb, _it_dev(current_iter, dev), self.refresh_retained,
                       _lib.stream_ptr())
 
     def sweep_staleness(self, current_iter: int | None = None) -> None:

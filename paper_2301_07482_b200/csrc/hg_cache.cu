@@ -34,19 +34,30 @@ struct NormKeyDecomposer {
   }
 };
 
-__global__ void k_norm_keys(int n, const int32_t* __restrict__ live, const int32_t* __restrict__ src_nodes,
-                            const double* __restrict__ norms, NormKey* __restrict__ keys, int32_t* __restrict__ vals) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    keys[i] = NormKey{(unsigned long long)__double_as_longlong(norms[i]), (unsigned)src_nodes[live[i]]};
+// keys for i < n; the tail up to n_max gets sentinels that sort last
+__global__ void k_norm_keys(const int32_t* n_dev, int n_max, double p_grad, const int32_t* __restrict__ live,
+                            const int32_t* __restrict__ src_nodes, const double* __restrict__ norms,
+                            NormKey* __restrict__ keys, int32_t* __restrict__ vals, long long* ctr) {
+  const int n = *n_dev;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr[kCtrK] = (long long)floor(p_grad * (double)n);  // cache.py:190
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_max; i += gridDim.x * blockDim.x) {
+    if (i < n) {
+      keys[i] = NormKey{(unsigned long long)__double_as_longlong(norms[i]), (unsigned)src_nodes[live[i]]};
+    } else {
+      keys[i] = NormKey{~0ull, ~0u};
+    }
     vals[i] = i;
   }
 }
 
-__global__ void k_rank_admit(int n, int k, const NormKey* __restrict__ skeys, const int32_t* __restrict__ svals,
-                             const int32_t* __restrict__ live, const uint8_t* __restrict__ computed_flag,
-                             int32_t* __restrict__ row_of, int32_t* __restrict__ row_owner, uint8_t* __restrict__ wflag,
+__global__ void k_rank_admit(const int32_t* n_dev, const NormKey* __restrict__ skeys,
+                             const int32_t* __restrict__ svals, const int32_t* __restrict__ live,
+                             const uint8_t* __restrict__ computed_flag, int32_t* __restrict__ row_of,
+                             int32_t* __restrict__ row_owner, uint8_t* __restrict__ wflag,
                              uint8_t* __restrict__ retained, long long* ctr) {
   unsigned long long* c = reinterpret_cast<unsigned long long*>(ctr);
+  const int n = *n_dev;
+  const long long k = ctr[kCtrK];
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const int id = (int)skeys[j].id;
     const int i = svals[j];
@@ -89,8 +100,9 @@ __global__ void k_release_writes(const int32_t* __restrict__ wlist, const NormKe
   }
 }
 
-__global__ void k_ring_scan(int cap, int it, double t_stale, int t_inf, int32_t* __restrict__ row_of,
+__global__ void k_ring_scan(int cap, const int32_t* it_dev, double t_stale, int t_inf, int32_t* __restrict__ row_of,
                             int32_t* __restrict__ row_owner, const int32_t* __restrict__ admit_iter, long long* ctr) {
+  const int it = *it_dev;
   const long long nw = ctr[kCtrNWrite];
   const long long header = ctr[kCtrHeader];
   const bool wrap_all = nw >= cap;
@@ -117,7 +129,8 @@ __global__ void k_ring_scan(int cap, int it, double t_stale, int t_inf, int32_t*
 // one warp per written row
 __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* __restrict__ skeys,
                              const int32_t* __restrict__ svals, const int32_t* __restrict__ live,
-                             const float* __restrict__ emb, int H, int cap, int it, float* __restrict__ table,
+                             const float* __restrict__ emb, int H, int cap, const int32_t* it_dev,
+                             float* __restrict__ table,
                              int32_t* __restrict__ row_of, int32_t* __restrict__ row_owner,
                              int32_t* __restrict__ admit_iter, long long* ctr) {
   const long long nw = ctr[kCtrNWrite];
@@ -126,6 +139,7 @@ __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* _
   const long long w0 = wrap_all ? nw - cap : 0;
   const long long neff = nw - w0;
   const int lane = threadIdx.x & 31;
+  const int it = *it_dev;
   const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < neff; w += warps) {
     const int j = wlist[w0 + w];
@@ -159,8 +173,11 @@ __global__ void k_commit(int cap, long long* ctr) {
   ctr[kCtrValid] += neff;
 }
 
-__global__ void k_refresh(int k, const uint8_t* __restrict__ retained, const NormKey* __restrict__ skeys,
-                          const int32_t* __restrict__ row_of, int32_t* __restrict__ admit_iter, int it) {
+__global__ void k_refresh(const long long* ctr, const uint8_t* __restrict__ retained,
+                          const NormKey* __restrict__ skeys, const int32_t* __restrict__ row_of,
+                          int32_t* __restrict__ admit_iter, const int32_t* it_dev) {
+  const long long k = ctr[kCtrK];
+  const int it = *it_dev;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
     if (!retained[j]) continue;
     const int id = (int)skeys[j].id;
@@ -202,14 +219,16 @@ long long hg_cache_update_scratch_bytes(long long n_max) {
 }
 
 // Stage 1 (U1-U3): rank and evict; leaves the write list + n_write on device.
+// n (live nodes) is read from n_dev; n_max sizes the sort (sentinel padding),
+// k = floor(p_grad * n) is computed on the device (cache.py:190).
 // The caller allocates the ring table on first use after reading n_write.
-int hg_cache_rank(int n, int k, const int32_t* live, const int32_t* src_nodes, const double* norms,
-                  const uint8_t* computed_flag, int32_t* row_of, int32_t* row_owner, long long* layer_ctr,
-                  void* scratch, long long scratch_bytes, cudaStream_t stream) {
+int hg_cache_rank(const int32_t* n_dev, int n_max, double p_grad, const int32_t* live, const int32_t* src_nodes,
+                  const double* norms, const uint8_t* computed_flag, int32_t* row_of, int32_t* row_owner,
+                  long long* layer_ctr, void* scratch, long long scratch_bytes, cudaStream_t stream) {
   const char* W = "hg_cache_rank";
-  if (scratch_bytes < hg_cache_update_scratch_bytes(n)) return fail(W, kBadArg, "scratch too small");
-  if (n == 0) return kOk;
-  const long long nn = n + 16;
+  if (scratch_bytes < hg_cache_update_scratch_bytes(n_max)) return fail(W, kBadArg, "scratch too small");
+  if (n_max <= 0) return kOk;
+  const long long nn = n_max + 16;
   char* p = reinterpret_cast<char*>(scratch);
   NormKey* keys_in = reinterpret_cast<NormKey*>(p);
   NormKey* keys_out = keys_in + nn;
@@ -219,28 +238,30 @@ int hg_cache_rank(int n, int k, const int32_t* live, const int32_t* src_nodes, c
   uint8_t* wflag = reinterpret_cast<uint8_t*>(wlist + nn);
   uint8_t* retained = wflag + nn;
   int* part = reinterpret_cast<int*>(retained + nn + 16 - ((uintptr_t)(retained + nn) & 15));
-  void* tmp = part + scan_tiles(n) + 4;
+  void* tmp = part + scan_tiles(n_max) + 4;
   size_t tmp_bytes = (size_t)(scratch_bytes - ((char*)tmp - p));
-  k_norm_keys<<<grid_for(n, 256), 256, 0, stream>>>(n, live, src_nodes, norms, keys_in, vals_in);
+  k_norm_keys<<<grid_for(n_max, 256), 256, 0, stream>>>(n_dev, n_max, p_grad, live, src_nodes, norms, keys_in,
+                                                        vals_in, layer_ctr);
   HG_LAUNCHED(W);
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, vals_out, n,
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, vals_out, n_max,
                                                   NormKeyDecomposer{}, stream);
   if (e != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(e));
-  k_rank_admit<<<grid_for(n, 256), 256, 0, stream>>>(n, k, keys_out, vals_out, live, computed_flag, row_of, row_owner,
-                                                     wflag, retained, layer_ctr);
+  k_rank_admit<<<grid_for(n_max, 256), 256, 0, stream>>>(n_dev, keys_out, vals_out, live, computed_flag, row_of,
+                                                         row_owner, wflag, retained, layer_ctr);
   HG_LAUNCHED(W);
-  return scan_launch<int>(W, FlagU8{wflag}, ConstCount{n}, n, part, EmitCompact{wlist}, StoreNWrite{layer_ctr},
+  return scan_launch<int>(W, FlagU8{wflag}, DevCount{n_dev}, n_max, part, EmitCompact{wlist}, StoreNWrite{layer_ctr},
                           stream);
 }
 
 // Stage 2 (U4-U8): ring write into a table of `cap` rows of H floats.
-int hg_cache_write(int n, int k, int cap, int H, int it, double t_stale, int refresh_retained, const int32_t* live,
-                   const float* emb, float* table, int32_t* row_of, int32_t* row_owner, int32_t* admit_iter,
-                   long long* layer_ctr, void* scratch, long long scratch_bytes, cudaStream_t stream) {
+int hg_cache_write(int n_max, int cap, int H, const int32_t* it_dev, double t_stale, int refresh_retained,
+                   const int32_t* live, const float* emb, float* table, int32_t* row_of, int32_t* row_owner,
+                   int32_t* admit_iter, long long* layer_ctr, void* scratch, long long scratch_bytes,
+                   cudaStream_t stream) {
   const char* W = "hg_cache_write";
-  if (n == 0) return kOk;
+  if (n_max <= 0) return kOk;
   if (cap < 1) return fail(W, kBadArg, "capacity must be >= 1");
-  const long long nn = n + 16;
+  const long long nn = n_max + 16;
   char* p = reinterpret_cast<char*>(scratch);
   NormKey* keys_out = reinterpret_cast<NormKey*>(p) + nn;
   int32_t* vals_out = reinterpret_cast<int32_t*>(keys_out + nn) + nn;
@@ -248,19 +269,19 @@ int hg_cache_write(int n, int k, int cap, int H, int it, double t_stale, int ref
   uint8_t* wflag = reinterpret_cast<uint8_t*>(wlist + nn);
   uint8_t* retained = wflag + nn;
   const int t_inf = isinf(t_stale) ? 1 : 0;
-  const long long nmax = n > cap ? n : cap;
-  k_release_writes<<<grid_for(n, 256), 256, 0, stream>>>(wlist, keys_out, cap, row_of, row_owner, layer_ctr);
+  const long long nmax = n_max > cap ? n_max : cap;
+  k_release_writes<<<grid_for(n_max, 256), 256, 0, stream>>>(wlist, keys_out, cap, row_of, row_owner, layer_ctr);
   HG_LAUNCHED(W);
-  k_ring_scan<<<grid_for(nmax, 256), 256, 0, stream>>>(cap, it, t_stale, t_inf, row_of, row_owner, admit_iter,
+  k_ring_scan<<<grid_for(nmax, 256), 256, 0, stream>>>(cap, it_dev, t_stale, t_inf, row_of, row_owner, admit_iter,
                                                        layer_ctr);
   HG_LAUNCHED(W);
-  k_write_rows<<<grid_for((long long)n * 32, 256, 148 * 16), 256, 0, stream>>>(
-      wlist, keys_out, vals_out, live, emb, H, cap, it, table, row_of, row_owner, admit_iter, layer_ctr);
+  k_write_rows<<<grid_for((long long)n_max * 32, 256, 148 * 16), 256, 0, stream>>>(
+      wlist, keys_out, vals_out, live, emb, H, cap, it_dev, table, row_of, row_owner, admit_iter, layer_ctr);
   HG_LAUNCHED(W);
   k_commit<<<1, 1, 0, stream>>>(cap, layer_ctr);
   HG_LAUNCHED(W);
-  if (refresh_retained && k > 0) {
-    k_refresh<<<grid_for(k, 256), 256, 0, stream>>>(k, retained, keys_out, row_of, admit_iter, it);
+  if (refresh_retained) {
+    k_refresh<<<grid_for(n_max, 256), 256, 0, stream>>>(layer_ctr, retained, keys_out, row_of, admit_iter, it_dev);
     HG_LAUNCHED(W);
   }
   return kOk;

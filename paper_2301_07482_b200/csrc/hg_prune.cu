@@ -51,10 +51,11 @@ struct EmitCompactPos {
 
 __global__ void k_lookup(const int32_t* n_live_dev, const int32_t* __restrict__ live,
                          const int32_t* __restrict__ src_nodes, int32_t* __restrict__ row_of,
-                         const int32_t* __restrict__ admit_iter, int32_t* __restrict__ row_owner, int it,
+                         const int32_t* __restrict__ admit_iter, int32_t* __restrict__ row_owner, const int* it_dev,
                          double t_stale, int t_inf, uint8_t* __restrict__ hit_flag, int32_t* __restrict__ hit_row,
                          long long* ctr) {
   const int n = *n_live_dev;
+  const int it = *it_dev;
   unsigned long long* c = reinterpret_cast<unsigned long long*>(ctr);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int loc = live[i];
@@ -113,14 +114,14 @@ int hg_prune_block(const int32_t* n_dst_dev, long long n_dst_max, const int32_t*
 }
 
 int hg_cache_lookup(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const int32_t* src_nodes,
-                    long long n_src_max, int32_t* row_of, const int32_t* admit_iter, int32_t* row_owner, int it,
-                    double t_stale, uint8_t* hit_flag, int32_t* hit_row, long long* layer_ctr,
+                    long long n_src_max, int32_t* row_of, const int32_t* admit_iter, int32_t* row_owner,
+                    const int32_t* it_dev, double t_stale, uint8_t* hit_flag, int32_t* hit_row, long long* layer_ctr,
                     cudaStream_t stream) {
   const char* W = "hg_cache_lookup";
   HG_CHECK_CUDA(W, cudaMemsetAsync(hit_flag, 0, (size_t)n_src_max, stream));
   const int t_inf = isinf(t_stale) ? 1 : 0;
   k_lookup<<<grid_for(n_live_max, 256), 256, 0, stream>>>(n_live_dev, live, src_nodes, row_of, admit_iter,
-                                                          row_owner, it, t_stale, t_inf, hit_flag, hit_row,
+                                                          row_owner, it_dev, t_stale, t_inf, hit_flag, hit_row,
                                                           layer_ctr);
   HG_LAUNCHED(W);
   return kOk;

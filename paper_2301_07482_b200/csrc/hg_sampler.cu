@@ -108,9 +108,18 @@ struct TotalDegCount {
   }
 };
 
-__global__ void k_stamp(const int32_t* __restrict__ frontier, const int32_t* F_dev, unsigned epoch,
+// device-resident sampler state (u64[6]): PCG64 state hi/lo, inc hi/lo,
+// draws consumed so far in this batch, epoch of the g2l stamps
+struct SampState {
+  unsigned long long st_hi, st_lo, inc_hi, inc_lo;
+  unsigned long long stream_pos;
+  unsigned long long epoch;
+};
+
+__global__ void k_stamp(const int32_t* __restrict__ frontier, const int32_t* F_dev, const SampState* ss,
                         int64_t* __restrict__ g2l, int32_t* __restrict__ src_out) {
   const int F = *F_dev;
+  const unsigned epoch = (unsigned)ss->epoch;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
     int v = frontier[i];
     g2l[v] = (int64_t)(((unsigned long long)epoch << 32) | (unsigned)i);
@@ -162,11 +171,12 @@ __device__ __forceinline__ u128 pcg_jump_c(const JumpTableC& tab, u128 s, unsign
 template <bool kSmallFanout>
 __global__ void __launch_bounds__(kSelThreads) k_select(
     const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end, const int32_t* __restrict__ g_col,
-    const int32_t* __restrict__ frontier, const int32_t* F_dev, int fanout, u128 s0, u128 inc,
-    const unsigned long long* stream_pos, const int64_t* __restrict__ cand_off,
-    const int32_t* __restrict__ blk_off, unsigned epoch, const int64_t* __restrict__ g2l,
+    const int32_t* __restrict__ frontier, const int32_t* F_dev, int fanout, const SampState* ss,
+    const int64_t* __restrict__ cand_off, const int32_t* __restrict__ blk_off, const int64_t* __restrict__ g2l,
     uint32_t* __restrict__ bitmap, int32_t* __restrict__ src_flat) {
   __shared__ JumpTableC tab;
+  const u128 s0{ss->st_hi, ss->st_lo}, inc{ss->inc_hi, ss->inc_lo};
+  const unsigned epoch = (unsigned)ss->epoch;
   for (int t = threadIdx.x; t < 256; t += blockDim.x) {
     (&tab.A[0][0])[t] = (&g_jump.A[0][0])[t];
     (&tab.C[0][0])[t] = mul128(inc, (&g_jump.S[0][0])[t]);
@@ -175,7 +185,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
   const int F = *F_dev;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  const unsigned long long base0 = *stream_pos;
+  const unsigned long long base0 = ss->stream_pos;
   const u128 a32 = tab.A[1][2];            // MULT^32 and its increment term
   const u128 c32 = tab.C[1][2];
   for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < F; row += warps) {
@@ -293,13 +303,14 @@ struct PopWord {
 struct EmitNew {
   uint32_t* bitmap;
   const int32_t* F_dev;
-  unsigned epoch;
+  const SampState* ss;
   int64_t* g2l;
   int32_t* src_out;
   __device__ void operator()(long long w, int excl, int v) const {
     if (!v) return;
     uint32_t bits = bitmap[w];
     const int pos0 = *F_dev + excl;
+    const unsigned epoch = (unsigned)ss->epoch;
     int r = 0;
     while (bits) {
       int b = __ffs(bits) - 1;
@@ -316,18 +327,23 @@ struct EmitNew {
 struct TotalNew {
   const int32_t* F_dev;
   int32_t* counts_dev;
-  unsigned long long* stream_pos;
+  SampState* ss;
   const int64_t* cand_off;
   __device__ void operator()(int t) const {
     const int F = *F_dev;
     counts_dev[1] = F + t;  // n_src of this block = next frontier size
-    *stream_pos += (unsigned long long)cand_off[F];
+    ss->stream_pos += (unsigned long long)cand_off[F];
   }
 };
 
 __global__ void k_relabel(const int32_t* __restrict__ src_flat, const int32_t* counts_dev,
-                          const int64_t* __restrict__ g2l, int32_t* __restrict__ col_local) {
+                          const int64_t* __restrict__ g2l, int32_t* __restrict__ col_local, SampState* ss) {
   const int E = counts_dev[0];
+  // every reader of this layer's epoch has finished (stream order): advance it
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long e = ss->epoch + 1;
+    ss->epoch = (e >= 0xFFFFFFFEull) ? 1ull : e;   // never the 0xFFFFFFFF fill of g2l
+  }
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x)
     col_local[e] = (int32_t)(g2l[src_flat[e]] & 0xffffffffll);
 }
@@ -381,8 +397,7 @@ long long hg_sample_layer_scratch_bytes(long long F_max, long long num_nodes) {
 
 int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t* g_col, long long num_nodes,
                     const int32_t* frontier, const int32_t* F_dev, long long F_max, int fanout,
-                    unsigned long long st_hi, unsigned long long st_lo, unsigned long long inc_hi,
-                    unsigned long long inc_lo, unsigned long long* stream_pos_dev, unsigned epoch, int64_t* g2l,
+                    unsigned long long* state_dev, int64_t* g2l,
                     uint32_t* bitmap, int64_t* cand_off, int32_t* blk_off, int32_t* blk_end, int32_t* dst_deg, int32_t* src_flat,
                     int32_t* col_local, int32_t* src_out, int32_t* counts_dev, void* scratch,
                     long long scratch_bytes, cudaStream_t stream) {
@@ -395,29 +410,29 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   I64x2* part_dc = reinterpret_cast<I64x2*>(scratch);
   int* part_w = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + (scan_tiles(F_max) + 1) * sizeof(I64x2));
 
-  k_stamp<<<grid_for(F_max, 256), 256, 0, stream>>>(frontier, F_dev, epoch, g2l, src_out);
+  SampState* ss = reinterpret_cast<SampState*>(state_dev);
+  k_stamp<<<grid_for(F_max, 256), 256, 0, stream>>>(frontier, F_dev, ss, g2l, src_out);
   HG_LAUNCHED(W);
   DegCount f{g_start, g_end, frontier, fanout};
   st = scan_launch<I64x2>(W, f, DevCount{F_dev}, F_max, part_dc,
                           EmitDegCount{cand_off, blk_off, blk_end, dst_deg, fanout, g_start, g_end, frontier},
                           TotalDegCount{F_dev, cand_off, blk_off, counts_dev}, stream);
   if (st) return st;
-  const u128 s0{st_hi, st_lo}, inc{inc_hi, inc_lo};
   const unsigned sel_grid = grid_for(F_max * 32, kSelThreads, 148 * 16);
   if (fanout <= 32)
-    k_select<true><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, g_col, frontier, F_dev, fanout, s0, inc,
-                                                          stream_pos_dev, cand_off, blk_off, epoch, g2l, bitmap,
+    k_select<true><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, g_col, frontier, F_dev, fanout, ss,
+                                                          cand_off, blk_off, g2l, bitmap,
                                                           src_flat);
   else
-    k_select<false><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, g_col, frontier, F_dev, fanout, s0, inc,
-                                                           stream_pos_dev, cand_off, blk_off, epoch, g2l, bitmap,
+    k_select<false><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, g_col, frontier, F_dev, fanout, ss,
+                                                           cand_off, blk_off, g2l, bitmap,
                                                            src_flat);
   HG_LAUNCHED(W);
   st = scan_launch<int>(W, PopWord{bitmap}, ConstCount{words}, words, part_w,
-                        EmitNew{bitmap, F_dev, epoch, g2l, src_out},
-                        TotalNew{F_dev, counts_dev, stream_pos_dev, cand_off}, stream);
+                        EmitNew{bitmap, F_dev, ss, g2l, src_out},
+                        TotalNew{F_dev, counts_dev, ss, cand_off}, stream);
   if (st) return st;
-  k_relabel<<<grid_for(F_max * (long long)fanout, 256), 256, 0, stream>>>(src_flat, counts_dev, g2l, col_local);
+  k_relabel<<<grid_for(F_max * (long long)fanout, 256), 256, 0, stream>>>(src_flat, counts_dev, g2l, col_local, ss);
   HG_LAUNCHED(W);
   return kOk;
 }

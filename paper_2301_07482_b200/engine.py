@@ -1,0 +1,241 @@
+"""Sync-free, shape-static training step (sample -> prune -> gather -> forward
+-> loss -> backward -> SGD -> cache update), replayed as one CUDA graph.
+
+This is the B200 runtime behind `Trainer.train` / `Trainer.train_step`: the
+same kernels as the API functions (sampler.py, trainer.prune_with_cache,
+nn.py), but every buffer is sized from host upper bounds of the batch
+(layer_bounds: F[l+1] <= F[l] * (1 + fanout)) and every element count is read
+by the kernels from device memory, so a whole iteration issues no host
+synchronisation. The step's inputs live in static device tensors (seeds,
+labels, the batch's PCG64 state, the iteration number) that are refreshed
+from pinned host staging before each launch; after the first eager
+iterations (which size the cache rings, cache.py:79-91) the step is captured
+once with torch.cuda.graph and replayed. The graph is re-captured only when a
+cache table is reallocated (first use / doubling at a sweep, cache.py:93-101).
+Sweeps themselves (every t_stale iterations) run on the host between replays.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .nn import Injection, cross_entropy_dev, layer_backward_dev, layer_forward_dev, sgd_step
+from .sampler import SamplerWorkspace, layer_bounds, pcg_words, sample_blocks_dev
+
+
+@dataclass
+class DevBlock:
+    """A sampled block with upper-bound shapes (counts on the device)."""
+
+    src_nodes: torch.Tensor
+    blk_off: torch.Tensor
+    end: torch.Tensor
+    col: torch.Tensor
+    dst_deg: torch.Tensor
+    src_deg: torch.Tensor
+    n_dst_dev: torch.Tensor
+    n_src_dev: torch.Tensor
+    num_dst: int            # upper bound
+    num_src: int            # upper bound
+    num_edges_built: int    # upper bound
+
+    @property
+    def adj(self):
+        return self
+
+    @property
+    def start(self):
+        return self.blk_off
+
+    @property
+    def col_indices(self):
+        return self.col
+
+
+class StepEngine:
+    def __init__(self, trainer, B: int):
+        self.tr = trainer
+        self.B = int(B)
+        cfg = trainer.cfg
+        g = trainer.graph
+        self.dev = trainer.device
+        self.L = len(cfg.fanouts)
+        self.F, self.E = layer_bounds(self.B, cfg.fanouts, g.num_nodes)
+        self.ws = SamplerWorkspace(g.num_nodes, self.dev)
+        self.seeds = torch.empty(self.B, dtype=torch.int32, device=self.dev)
+        self.labels = torch.empty(self.B, dtype=torch.int32, device=self.dev)
+        self.it = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.F0 = torch.full((1,), self.B, dtype=torch.int32, device=self.dev)
+        self.graph = None
+        self.graph_key = None
+        self.pool = None
+        self.out = None
+        self.capturing = False
+
+    # ------------------------------------------------------------ inputs
+
+    def stage(self, iteration: int, seeds: np.ndarray, labels: np.ndarray, pcg: tuple):
+        """Copy one batch's inputs into the static device tensors (pinned
+        staging buffers from torch's caching host allocator, which keeps each
+        buffer alive until its copy has executed)."""
+        host = torch.from_numpy(self.pack_inputs(iteration, seeds, labels, pcg)).pin_memory()
+        self.stage_device(host.to(self.dev, non_blocking=True))
+
+    def pack_inputs(self, iteration: int, seeds: np.ndarray, labels: np.ndarray, pcg: tuple) -> np.ndarray:
+        """The int32 words `stage` copies (for pre-staging whole runs in HBM)."""
+        words = np.empty(self.B * 2 + 1 + 10, dtype=np.int32)
+        words[: self.B] = seeds
+        words[self.B: 2 * self.B] = labels
+        words[2 * self.B] = iteration
+        words[2 * self.B + 1:] = np.array(pcg_words(*pcg), dtype=np.int64).view(np.int32)
+        return words
+
+    def stage_device(self, words_dev: torch.Tensor):
+        """Device-to-device staging of pre-packed inputs already in HBM."""
+        self.seeds.copy_(words_dev[: self.B])
+        self.labels.copy_(words_dev[self.B: 2 * self.B])
+        self.it.copy_(words_dev[2 * self.B: 2 * self.B + 1])
+        self.ws.state[:5].copy_(words_dev[2 * self.B + 1:].view(torch.int64))
+
+    def launch(self) -> dict:
+        """Run the staged step (graph replay when possible)."""
+        if self._graphable():
+            if self.graph is None or self.graph_key != self._key():
+                self._capture()
+            self.graph.replay()
+            return self.out
+        self.out = self.run()
+        return self.out
+
+    # -------------------------------------------------------------- step
+
+    def run(self) -> dict:
+        """Enqueue one full iteration on the current stream (no host sync)."""
+        tr, cfg, net, cache = self.tr, self.tr.cfg, self.tr.network, self.tr.cache
+        dev, L, B = self.dev, self.L, self.B
+        stream = torch.cuda.current_stream(dev)
+        sp = _lib.stream_ptr(stream)
+        g = tr.graph
+        raw = sample_blocks_dev(g, self.seeds, self.F0, B, cfg.fanouts, self.ws, stream)
+        blocks = []
+        for li in range(L - 1, -1, -1):
+            r = raw[li]
+            blocks.append(DevBlock(r["src"], r["blk_off"], r["blk_end"], r["col"], r["dst_deg"], None, r["F_dev"],
+                                   r["counts"][1:2], r["F_max"], r["Fn_max"], r["E_max"]))
+        for b, blk in enumerate(blocks):
+            blk.src_deg = (torch.zeros(blk.num_src, dtype=torch.int32, device=dev) if b == 0
+                           else blocks[b - 1].dst_deg)
+
+        # ---- prune walk + lookups (trainer.py:166-207) ----
+        counts = torch.empty(2 * L, dtype=torch.int32, device=dev)
+        keep, pos, rows, live = [None] * L, [None] * L, [None] * L, [None] * (L + 1)
+        injected = [None] * L
+        live_dst, inj_flag = None, None
+        sb = _lib.query("hg_prune_scratch_bytes", max(max(b.num_src, b.num_dst) for b in blocks))
+        scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+        for b in range(L - 1, -1, -1):
+            blk = blocks[b]
+            keep[b] = torch.empty(blk.num_dst, dtype=torch.uint8, device=dev)
+            rows[b] = torch.empty(blk.num_dst, dtype=torch.int32, device=dev)
+            pos[b] = torch.empty(blk.num_dst, dtype=torch.int32, device=dev)
+            src_mask = torch.empty(blk.num_src, dtype=torch.uint8, device=dev)
+            live[b] = torch.empty(blk.num_src, dtype=torch.int32, device=dev)
+            _lib.call("hg_prune_block", _lib.ptr(blk.n_dst_dev), blk.num_dst, _lib.ptr(blk.n_src_dev), blk.num_src,
+                      _lib.ptr(live_dst), _lib.ptr(inj_flag), _lib.ptr(blk.blk_off), _lib.ptr(blk.end),
+                      _lib.ptr(blk.col), _lib.ptr(keep[b]), _lib.ptr(rows[b]), _lib.ptr(pos[b]), _lib.ptr(src_mask),
+                      _lib.ptr(live[b]), _lib.ptr(counts[2 * b:2 * b + 2]), _lib.ptr(cache.gctr), _lib.ptr(scratch),
+                      sb, sp)
+            live_dst, inj_flag = src_mask, None
+            if b >= 1:
+                lc = cache._layer(b)
+                hit_flag = torch.empty(blk.num_src, dtype=torch.uint8, device=dev)
+                hit_row = torch.empty(blk.num_src, dtype=torch.int32, device=dev)
+                lc.lookup_dev(counts[2 * b + 1:2 * b + 2], blk.num_src, live[b], blk.src_nodes, blk.num_src, self.it,
+                              hit_flag, hit_row, sp)
+                if lc.table is not None:
+                    inj_flag = hit_flag
+                    injected[b - 1] = Injection(hit_flag, hit_row, lc.table)
+
+        def R_dev(b):
+            return counts[2 * b:2 * b + 1]
+
+        def n_live_dev(b):
+            return counts[2 * b + 1:2 * b + 2]
+
+        # ---- layer-0 input (trainer.py:326-343) ----
+        b0 = blocks[0]
+        h = torch.empty((b0.num_src, tr.feature_dim), dtype=torch.float32, device=dev)
+        region = cache.feature_table if cache.feature_table is not None else tr.features
+        _lib.call("hg_load_features", _lib.ptr(n_live_dev(0)), b0.num_src, _lib.ptr(live[0]), _lib.ptr(b0.src_nodes),
+                  _lib.ptr(cache.feature_row_of_dev), _lib.ptr(region), _lib.ptr(tr.features), tr.feature_dim,
+                  tr._dtype_code, _lib.ptr(h), _lib.ptr(cache.gctr), sp)
+
+        # ---- forward (nn.py:260-297) ----
+        tapes = []
+        for b in range(L):
+            blk = blocks[b]
+            t = layer_forward_dev(net, b, blk, h, rows[b], blk.num_dst, R_dev(b), b < L - 1, injected[b], sp,
+                                  blk.n_dst_dev)
+            tapes.append(t)
+            h = t.h_out
+        d_h, loss = cross_entropy_dev(tapes[-1].h_out, self.labels, B, net.dims[-1], sp)
+
+        # ---- backward (nn.py:300-320) + SGD ----
+        grads = net.new_grads(zero=False)
+        norms = [None] * L
+        for l in range(L - 1, -1, -1):
+            blk = blocks[l]
+            d_prev, nrm = layer_backward_dev(net, l, blk, tapes[l], d_h, grads, l >= 1, keep[l], pos[l], live[l],
+                                             blk.num_src, sp, blk.n_dst_dev, n_live_dev(l))
+            norms[l] = nrm
+            d_h = d_prev
+        if tr.grad_hook is not None:
+            tr.grad_hook(grads)
+        sgd_step(net, grads, cfg.eta)
+
+        # ---- cache admission / ring update (cache.py:188-204) ----
+        for layer in range(1, L):
+            cache._layer(layer).update_dev(n_live_dev(layer), blocks[layer].num_src, live[layer],
+                                           blocks[layer].src_nodes, norms[layer], keep[layer - 1],
+                                           tapes[layer - 1].h_out, self.it, cache.refresh_retained, sp,
+                                           allow_alloc=not self.capturing)
+        return dict(loss=loss, counts=counts, blocks=blocks, live=live, rows=rows, keep=keep, tapes=tapes,
+                    norms=norms, grads=grads, injected=injected)
+
+    # ------------------------------------------------------------ driver
+
+    def _key(self):
+        c = self.tr.cache
+        return tuple(None if lc.table is None else lc.table.data_ptr() for lc in c.layers.values())
+
+    def _graphable(self) -> bool:
+        return (self.tr.use_graphs and self.tr.grad_hook is None
+                and all(lc.table is not None for lc in self.tr.cache.layers.values()))
+
+    def step(self, iteration: int, seeds: np.ndarray, labels: np.ndarray, pcg: tuple) -> dict:
+        """Stage inputs and run one iteration (graph replay when possible)."""
+        self.stage(iteration, seeds, labels, pcg)
+        return self.launch()
+
+    def _capture(self):
+        torch.cuda.synchronize(self.dev)
+        self.graph = torch.cuda.CUDAGraph()
+        if self.pool is None:
+            self.pool = torch.cuda.graph_pool_handle()
+        self.capturing = True
+        try:
+            # capture on a side stream; the staged inputs were copied on the
+            # current stream, which the capture stream waits for
+            side = torch.cuda.Stream(self.dev)
+            side.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(self.graph, pool=self.pool, stream=side):
+                    self.out = self.run()
+            torch.cuda.current_stream(self.dev).wait_stream(side)
+        finally:
+            self.capturing = False
+        self.graph_key = self._key()

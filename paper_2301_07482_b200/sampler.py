@@ -128,23 +128,79 @@ def batch_rng(rng_seed: int, batch_index: int) -> np.random.Generator:
 
 class SamplerWorkspace:
     """Per-sampler O(N) scratch: epoch-stamped global->local map and the
-    self-clearing node bitmap. One workspace serves one stream at a time."""
+    self-clearing node bitmap, plus the device-resident sampler state
+    (u64[6]: PCG64 state hi/lo, inc hi/lo, draws consumed, g2l epoch).
+    One workspace serves one stream at a time."""
 
     def __init__(self, num_nodes: int, device):
         self.num_nodes = int(num_nodes)
         self.device = device
         self.g2l = torch.full((self.num_nodes,), -1, dtype=torch.int64, device=device)
         self.bitmap = torch.zeros(((self.num_nodes + 31) // 32,), dtype=torch.int32, device=device)
-        self.stream_pos = torch.zeros(1, dtype=torch.int64, device=device)
-        self.epoch = 0
+        self.state = torch.zeros(6, dtype=torch.int64, device=device)
+        self.state[5] = 1                       # epoch 0xFFFFFFFF is the g2l fill
         self.lock = threading.Lock()
 
-    def next_epoch(self) -> int:
-        self.epoch += 1
-        if self.epoch >= 0xFFFFFFFE:  # never collide with the -1 fill
-            self.g2l.fill_(-1)
-            self.epoch = 1
-        return self.epoch
+    def set_pcg(self, state: int, inc: int, dst=None):
+        """Stage the PCG64 state of a batch (and zero the draw counter)."""
+        vals = [(state >> 64) & _M64, state & _M64, (inc >> 64) & _M64, inc & _M64, 0]
+        host = torch.tensor([v - (1 << 64) if v >= (1 << 63) else v for v in vals], dtype=torch.int64)
+        (dst if dst is not None else self.state)[:5].copy_(host.pin_memory(), non_blocking=True)
+
+    @property
+    def stream_pos(self):
+        return self.state[4:5]
+
+
+def pcg_words(state: int, inc: int) -> list:
+    """The 5 int64 words hg_sample_layer reads from state_dev[0:5]."""
+    vals = [(state >> 64) & _M64, state & _M64, (inc >> 64) & _M64, inc & _M64, 0]
+    return [v - (1 << 64) if v >= (1 << 63) else v for v in vals]
+
+
+def layer_bounds(B: int, fanouts, num_nodes: int):
+    """Host upper bounds per sampling layer (outermost first): frontier sizes
+    F[0..L] and sampled edges E[0..L-1]."""
+    F, E = [B], []
+    for f in fanouts:
+        e = max(1, F[-1] * f)
+        E.append(e)
+        F.append(min(num_nodes, F[-1] + e))
+    return F, E
+
+
+def sample_blocks_dev(g: Csr2Graph, frontier: torch.Tensor, F0_dev: torch.Tensor, B: int, fanouts,
+                      ws: SamplerWorkspace, stream) -> list:
+    """Launch every sampling layer with host upper bounds and device counts
+    (no host synchronisation). ws.state must hold the batch's PCG64 state.
+    Returns per layer (outermost first): dict of device buffers."""
+    dev = g.start.device
+    N = g.num_nodes
+    sp = _lib.stream_ptr(stream)
+    F_max, F_dev = B, F0_dev
+    raw = []
+    for fanout in fanouts:
+        E_max = max(1, F_max * fanout)
+        Fn_max = min(N, F_max + E_max)
+        cand_off = torch.empty(F_max + 1, dtype=torch.int64, device=dev)
+        blk_off = torch.empty(F_max + 1, dtype=torch.int32, device=dev)
+        blk_end = torch.empty(F_max, dtype=torch.int32, device=dev)
+        dst_deg = torch.empty(F_max, dtype=torch.int32, device=dev)
+        src_flat = torch.empty(E_max, dtype=torch.int32, device=dev)
+        col_local = torch.empty(E_max, dtype=torch.int32, device=dev)
+        src_out = torch.empty(Fn_max, dtype=torch.int32, device=dev)
+        counts = torch.empty(4, dtype=torch.int32, device=dev)
+        sb = _lib.query("hg_sample_layer_scratch_bytes", F_max, N)
+        scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+        _lib.call("hg_sample_layer", _lib.ptr(g.start), _lib.ptr(g.end), _lib.ptr(g.col_indices), N,
+                  _lib.ptr(frontier), _lib.ptr(F_dev), F_max, fanout, _lib.ptr(ws.state), _lib.ptr(ws.g2l),
+                  _lib.ptr(ws.bitmap), _lib.ptr(cand_off), _lib.ptr(blk_off), _lib.ptr(blk_end),
+                  _lib.ptr(dst_deg), _lib.ptr(src_flat), _lib.ptr(col_local), _lib.ptr(src_out),
+                  _lib.ptr(counts), _lib.ptr(scratch), sb, sp)
+        raw.append(dict(F_dev=F_dev, F_max=F_max, E_max=E_max, Fn_max=Fn_max, blk_off=blk_off, blk_end=blk_end,
+                        dst_deg=dst_deg, col=col_local, src=src_out, counts=counts))
+        frontier, F_dev, F_max = src_out, counts[1:2], Fn_max
+    return raw
 
 
 _default_ws: dict = {}
@@ -204,40 +260,17 @@ def sample_layered(g: Csr2Graph, seeds, plan: SamplePlan, rng: np.random.Generat
     dev = g.start.device
     s = stream or torch.cuda.current_stream(dev)
     state, inc = _pcg_state(rng)
-    N = g.num_nodes
     with ws.lock, torch.cuda.stream(s):
-        sp = _lib.stream_ptr(s)
-        ws.stream_pos.zero_()
+        ws.set_pcg(state, inc)
         B = int(seeds.shape[0])
         if seeds_dev is None:
             frontier = torch.from_numpy(seeds.astype(np.int32)).pin_memory().to(dev, non_blocking=True)
         else:
             frontier = seeds_dev
         F_dev = torch.tensor([B], dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
-        F_max = B
-        raw = []
-        for fanout in plan.fanouts:
-            E_max = max(1, F_max * fanout)
-            Fn_max = min(N, F_max + E_max)
-            cand_off = torch.empty(F_max + 1, dtype=torch.int64, device=dev)
-            blk_off = torch.empty(F_max + 1, dtype=torch.int32, device=dev)
-            blk_end = torch.empty(F_max, dtype=torch.int32, device=dev)
-            dst_deg = torch.empty(F_max, dtype=torch.int32, device=dev)
-            src_flat = torch.empty(E_max, dtype=torch.int32, device=dev)
-            col_local = torch.empty(E_max, dtype=torch.int32, device=dev)
-            src_out = torch.empty(Fn_max, dtype=torch.int32, device=dev)
-            counts = torch.zeros(4, dtype=torch.int32, device=dev)
-            sb = _lib.query("hg_sample_layer_scratch_bytes", F_max, N)
-            scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
-            _lib.call("hg_sample_layer", _lib.ptr(g.start), _lib.ptr(g.end), _lib.ptr(g.col_indices), N,
-                      _lib.ptr(frontier), _lib.ptr(F_dev), F_max, fanout,
-                      (state >> 64) & _M64, state & _M64, (inc >> 64) & _M64, inc & _M64,
-                      _lib.ptr(ws.stream_pos), ws.next_epoch(), _lib.ptr(ws.g2l), _lib.ptr(ws.bitmap),
-                      _lib.ptr(cand_off), _lib.ptr(blk_off), _lib.ptr(blk_end), _lib.ptr(dst_deg),
-                      _lib.ptr(src_flat), _lib.ptr(col_local), _lib.ptr(src_out), _lib.ptr(counts),
-                      _lib.ptr(scratch), sb, sp)
-            raw.append((F_dev, blk_off, blk_end, dst_deg, col_local, src_out, counts))
-            frontier, F_dev, F_max = src_out, counts[1:2], Fn_max
+        raw = sample_blocks_dev(g, frontier, F_dev, B, plan.fanouts, ws, s)
+        raw = [(r["F_dev"], r["blk_off"], r["blk_end"], r["dst_deg"], r["col"], r["src"], r["counts"])
+               for r in raw]
         # one host round trip per batch: all block sizes + the draw count
         sizes = torch.cat([torch.stack([r[0][0] for r in raw]).to(torch.int64),
                            torch.stack([r[6][0] for r in raw]).to(torch.int64),

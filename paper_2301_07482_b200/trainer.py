@@ -17,13 +17,15 @@ from __future__ import annotations
 
 import csv
 import math
+import os
 from dataclasses import dataclass, fields
 
 import numpy as np
 import torch
 
 from . import _lib
-from ._state import GCTR_FEATURE_HITS, GCTR_FEATURE_MISSES, LAYER_CTR_LEN, CTR_VALID
+from ._state import GCTR_FEATURE_HITS, GCTR_FEATURE_MISSES, GCTR_PRUNE_WRITES, LAYER_CTR_LEN, CTR_VALID
+from .engine import StepEngine
 from .cache import COUNTER_NAMES, CachePolicy, HistCache
 from .graphs import Csr2Graph, _np, csr2_from_arrays
 from .nn import (Injection, LayerKind, Network, backward, cross_entropy_dev, forward_pass, init_network,
@@ -165,6 +167,7 @@ def prune_with_cache(sub: LayeredSubgraph, cache: HistCache, current_iter: int, 
         blk = sub.layers[b]
         sizes += [blk.num_dst, blk.num_src]
     size_dev = torch.tensor(sizes, dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
+    it_dev = torch.tensor([int(current_iter)], dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
     counts = torch.zeros(2 * L, dtype=torch.int32, device=dev)
     live_dst = None          # NULL = every seed row is live
     inj_flag = None
@@ -191,7 +194,7 @@ def prune_with_cache(sub: LayeredSubgraph, cache: HistCache, current_iter: int, 
             lc = cache._layer(b)
             hit_flag = torch.empty(n_src, dtype=torch.uint8, device=dev)
             hit_row = torch.empty(n_src, dtype=torch.int32, device=dev)
-            lc.lookup_dev(counts[2 * b + 1:2 * b + 2], n_src, lv, blk.src_nodes, n_src, current_iter, hit_flag,
+            lc.lookup_dev(counts[2 * b + 1:2 * b + 2], n_src, lv, blk.src_nodes, n_src, it_dev, hit_flag,
                           hit_row, sp)
             if lc.table is not None:
                 inj_flag = hit_flag
@@ -209,6 +212,22 @@ def prune_with_cache(sub: LayeredSubgraph, cache: HistCache, current_iter: int, 
 
 
 # ----------------------------------------------------------------- trainer
+
+
+class _EngineLast:
+    """Exact-size views of the engine's last step, shaped like the API path's
+    (pruned, tapes, grads, norms) tuple: pruned.layer_live / compute_rows and
+    norms are sliced with the counts read back by train_step."""
+
+    def __init__(self, out, counts):
+        L = len(out["blocks"])
+        self.out = out
+        self.layer_live = [out["live"][b][:counts[2 * b + 1]] for b in range(L)]
+        self.compute_rows = [out["rows"][b][:counts[2 * b]] for b in range(L)]
+        self.norms = [None if out["norms"][l] is None else out["norms"][l][:counts[2 * l + 1]] for l in range(L)]
+
+    def __getitem__(self, i):
+        return (self, self.out["tapes"], self.out["grads"], self.norms)[i]
 
 
 def make_batches(train_ids, cfg: TrainConfig) -> list:
@@ -272,6 +291,8 @@ class Trainer:
         # kernels dereference the host pointer directly over PCIe
         self.probe_nodes = probe_nodes
         self.grad_hook = None   # callable(Grads) run between backward and SGD (data parallel)
+        self.use_graphs = os.environ.get("HG_GRAPHS", "1") != "0"
+        self._engines = {}
 
     # ------------------------------------------------------------ pieces
 
@@ -311,12 +332,75 @@ class Trainer:
         valid = int(sum(host[1 + after.numel():]))
         return self._metrics(iteration, epoch, len(sub.seeds), loss, delta, baseline, valid, sub)
 
-    def train_step_device(self, iteration: int, seeds_dev: torch.Tensor, labels_dev: torch.Tensor):
-        """Device-resident step for throughput runs: seeds/labels already in
-        HBM, loss and counters stay on the device (read them after timing)."""
-        sub = sample_layered(self.graph, None, self.plan, batch_rng(self.cfg.seed, iteration), seeds_dev=seeds_dev)
-        loss_dev, _ = self._step(iteration, sub, labels_dev)
-        return loss_dev
+    # ------------------------------------------- engine path (CUDA graph)
+
+    def _engine(self, B: int) -> StepEngine:
+        eng = self._engines.get(B)
+        if eng is None:
+            eng = self._engines[B] = StepEngine(self, B)
+        return eng
+
+    def _engine_step(self, iteration: int, seeds: np.ndarray):
+        seeds = np.asarray(seeds, dtype=np.int64)
+        eng = self._engine(len(seeds))
+        bg = batch_rng(self.cfg.seed, iteration).bit_generator.state["state"]
+        out = eng.step(iteration, seeds.astype(np.int32), self.labels[seeds].astype(np.int32),
+                       (int(bg["state"]), int(bg["inc"])))
+        return eng, out
+
+    def train_step_device(self, iteration: int, seeds) -> torch.Tensor:
+        """Device-resident step for throughput runs: sample + train one batch
+        (graph replay after warm-up); returns the loss as a device scalar and
+        does not synchronise. Sweeps run on the host every t_stale steps."""
+        eng, out = self._engine_step(iteration, seeds)
+        self.cache.end_iteration(iteration)
+        self._last_engine = (eng, out)
+        return out["loss"]
+
+    def prestage(self, iterations, seeds_list) -> list:
+        """Pack (seeds, labels, PCG64 state, iteration) of several batches
+        into HBM, for runs whose inputs are resident before timing starts."""
+        out = []
+        for it, seeds in zip(iterations, seeds_list):
+            seeds = np.asarray(seeds, dtype=np.int64)
+            eng = self._engine(len(seeds))
+            bg = batch_rng(self.cfg.seed, it).bit_generator.state["state"]
+            words = eng.pack_inputs(it, seeds.astype(np.int32), self.labels[seeds].astype(np.int32),
+                                    (int(bg["state"]), int(bg["inc"])))
+            out.append((it, len(seeds), torch.from_numpy(words).to(self.device)))
+        return out
+
+    def train_step_resident(self, staged) -> torch.Tensor:
+        """One step from prestage()d HBM inputs (no host traffic, no sync)."""
+        it, B, words = staged
+        eng = self._engine(B)
+        eng.stage_device(words)
+        out = eng.launch()
+        self.cache.end_iteration(it)
+        self._last_engine = (eng, out)
+        return out["loss"]
+
+    def train_step(self, iteration: int, epoch: int, seeds) -> IterMetrics:
+        """Sample + train one batch through the engine and read IterMetrics
+        back (trainer.py:362-421 semantics, sampling included)."""
+        cache = self.cache
+        before = cache.counters_vector().clone()
+        eng, out = self._engine_step(iteration, seeds)
+        after = cache.counters_vector()
+        n_src0 = out["blocks"][0].n_src_dev
+        host = torch.cat([out["loss"].view(1), (after - before).double(),
+                          after[CTR_VALID::LAYER_CTR_LEN][:cache.num_layers].double(), n_src0.double(),
+                          out["counts"].double()]).cpu().tolist()
+        nv = after.numel()
+        loss, delta = host[0], [int(x) for x in host[1:1 + nv]]
+        valid = int(sum(host[1 + nv:1 + nv + cache.num_layers]))
+        n_src0 = int(host[1 + nv + cache.num_layers])
+        counts = [int(x) for x in host[2 + nv + cache.num_layers:]]
+        cache.end_iteration(iteration)
+        self._last_engine = (eng, out)
+        self.last = _EngineLast(out, counts)
+        return self._metrics(iteration, epoch, len(seeds), loss, delta, n_src0 * self.row_bytes, valid, None,
+                             prune_writes=delta[cache.num_layers * LAYER_CTR_LEN + GCTR_PRUNE_WRITES])
 
     def _step(self, iteration: int, sub: LayeredSubgraph, labels_dev: torch.Tensor):
         dev = self.device
@@ -359,7 +443,7 @@ class Trainer:
         self.last = (pruned, tapes, grads, norms)
         return loss_dev, baseline
 
-    def _metrics(self, iteration, epoch, num_seeds, loss, delta, baseline, valid, sub):
+    def _metrics(self, iteration, epoch, num_seeds, loss, delta, baseline, valid, sub, prune_writes=None):
         nl = self.cache.num_layers
         tot = dict.fromkeys(COUNTER_NAMES, 0)
         from .cache import _LAYER_IDX
@@ -371,20 +455,21 @@ class Trainer:
         return IterMetrics(
             iteration=iteration, epoch=epoch, num_seeds=num_seeds, loss=float(loss),
             fetched_bytes=fm * self.row_bytes, baseline_bytes=baseline,
-            prune_writes=sum(b.adj.prune_writes for b in sub.layers),
+            prune_writes=(sum(b.adj.prune_writes for b in sub.layers) if prune_writes is None else prune_writes),
             hits=tot["hits"], misses=tot["misses"], admissions=tot["admissions"],
             gradient_evictions=tot["gradient_evictions"], staleness_evictions=tot["staleness_evictions"],
             forced_evictions=tot["forced_evictions"], feature_hits=fh, feature_misses=fm,
             valid_entries=valid, estimation_error=math.nan)
 
     def train(self) -> list:
+        """trainer.py:423-433: every batch of every epoch, in order. Sampling
+        runs inside the captured step (no producer thread is needed: the
+        sampler kernels are part of the same stream / graph)."""
         cfg = self.cfg
         batches = make_batches(self.train_ids, cfg)
         per_epoch = max(1, math.ceil(len(self.train_ids) / cfg.batch_size))
-        with SubgraphProducer(self.graph, batches, self.plan, queue_capacity=2) as producer:
-            for iteration, sub in producer:
-                m = self.train_iteration(iteration, iteration // per_epoch, sub)
-                self.metrics.append(m)
+        for iteration, seeds in enumerate(batches):
+            self.metrics.append(self.train_step(iteration, iteration // per_epoch, seeds))
         return self.metrics
 
 

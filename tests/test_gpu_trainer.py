@@ -147,3 +147,47 @@ def test_fp16_feature_table():
                                  norms_override={l: tr.last[3][l].cpu().numpy() for l in (1, 2)})
         assert m.fetched_bytes == om.fetched_bytes and m.hits == om.hits
         assert abs(m.loss - om.loss) <= 1e-3 * abs(om.loss)
+
+
+@pytest.mark.parametrize("kind", [SAGE, GCN])
+@pytest.mark.parametrize("graphs", [True, False])
+def test_engine_lockstep_with_oracle(kind, graphs):
+    """The sync-free engine (Trainer.train_step, CUDA-graph replay after the
+    cache rings exist) against the oracle in lockstep."""
+    import paper_2301_07482_b200 as hg
+    ds, g = _pl3000()
+    lk, ok = _kinds(kind)
+    common = dict(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=2, eta=0.05, p_grad=0.9, t_stale=5,
+                  seed=3)
+    tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, hg.TrainConfig(kind=lk, **common), ds.num_classes)
+    tr.use_graphs = graphs
+    otr = OTrainer(g, ds.features, ds.labels, ds.train_ids, OTrainConfig(kind=ok, **common), ds.num_classes)
+    batches = hg.make_batches(ds.train_ids, tr.cfg)
+    for it, seeds in enumerate(batches):
+        m = tr.train_step(it, 0, seeds)
+        norms = {l: tr.last[3][l].cpu().numpy() for l in range(1, 3)}
+        om = otr.train_iteration(it, 0, otr.sample(it, seeds), norms_override=norms)
+        for f in INT_FIELDS:
+            assert getattr(m, f) == getattr(om, f), (it, f, getattr(m, f), getattr(om, f))
+        assert abs(m.loss - om.loss) <= 1e-3 * abs(om.loss), (it, m.loss, om.loss)
+        for b in range(3):
+            np.testing.assert_array_equal(tr.last[0].layer_live[b].cpu().numpy(), otr.last[0].layer_live[b])
+            np.testing.assert_array_equal(tr.last[0].compute_rows[b].cpu().numpy(), otr.last[0].compute_rows[b])
+    if graphs:
+        assert any(e.graph is not None for e in tr._engines.values()), "graph was never captured"
+    tr.cache.check_integrity()
+
+
+def test_graph_replay_bitwise_equals_eager_engine():
+    import paper_2301_07482_b200 as hg
+    ds, g = _pl3000()
+    cfg = hg.TrainConfig(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=1, eta=0.05,
+                         kind=hg.LayerKind.SAGE_MEAN, p_grad=0.9, t_stale=5, seed=1)
+    runs = []
+    for graphs in (False, True):
+        tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
+        tr.use_graphs = graphs
+        ms = tr.train()
+        runs.append((hashlib.sha256(tr.network.checksum_bytes()).hexdigest(),
+                     [(m.loss, m.hits, m.admissions, m.fetched_bytes) for m in ms]))
+    assert runs[0] == runs[1]
