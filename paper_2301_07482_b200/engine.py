@@ -87,19 +87,22 @@ class StepEngine:
 
     def pack_inputs(self, iteration: int, seeds: np.ndarray, labels: np.ndarray, pcg: tuple) -> np.ndarray:
         """The int32 words `stage` copies (for pre-staging whole runs in HBM)."""
-        words = np.empty(self.B * 2 + 1 + 10, dtype=np.int32)
-        words[: self.B] = seeds
-        words[self.B: 2 * self.B] = labels
-        words[2 * self.B] = iteration
-        words[2 * self.B + 1:] = np.array(pcg_words(*pcg), dtype=np.int64).view(np.int32)
+        # layout (int32 words): [0:10) PCG64 words (5 x int64, 8-byte aligned),
+        # [10] iteration, [11] pad, [12:12+B) seeds, [12+B:12+2B) labels
+        words = np.empty(12 + 2 * self.B, dtype=np.int32)
+        words[:10] = np.array(pcg_words(*pcg), dtype=np.int64).view(np.int32)
+        words[10] = iteration
+        words[11] = 0
+        words[12: 12 + self.B] = seeds
+        words[12 + self.B:] = labels
         return words
 
     def stage_device(self, words_dev: torch.Tensor):
         """Device-to-device staging of pre-packed inputs already in HBM."""
-        self.seeds.copy_(words_dev[: self.B])
-        self.labels.copy_(words_dev[self.B: 2 * self.B])
-        self.it.copy_(words_dev[2 * self.B: 2 * self.B + 1])
-        self.ws.state[:5].copy_(words_dev[2 * self.B + 1:].view(torch.int64))
+        self.ws.state[:5].copy_(words_dev[:10].view(torch.int64))
+        self.it.copy_(words_dev[10:11])
+        self.seeds.copy_(words_dev[12: 12 + self.B])
+        self.labels.copy_(words_dev[12 + self.B: 12 + 2 * self.B])
 
     def launch(self) -> dict:
         """Run the staged step (graph replay when possible)."""

@@ -432,13 +432,14 @@ class Trainer:
         if self.grad_hook is not None:
             self.grad_hook(grads)          # e.g. NCCL all-reduce of the flat bucket
         sgd_step(net, grads, cfg.eta)
+        it_dev = torch.tensor([int(iteration)], dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
         for layer in range(1, L):
             n_live = pruned.counts[layer][1]
             if n_live == 0:
                 continue
-            cache._layer(layer).update_dev(n_live, pruned.layer_live[layer], sub.layers[layer].src_nodes,
-                                           norms[layer], pruned.keep[layer - 1], tapes[layer - 1].h_out,
-                                           iteration, cache.refresh_retained, sp)
+            cache._layer(layer).update_dev(pruned.n_live_dev(layer), n_live, pruned.layer_live[layer],
+                                           sub.layers[layer].src_nodes, norms[layer], pruned.keep[layer - 1],
+                                           tapes[layer - 1].h_out, it_dev, cache.refresh_retained, sp)
         cache.end_iteration(iteration)
         self.last = (pruned, tapes, grads, norms)
         return loss_dev, baseline
