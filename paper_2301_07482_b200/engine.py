@@ -226,9 +226,11 @@ class StepEngine:
 
     def _capture(self):
         torch.cuda.synchronize(self.dev)
+        # a fresh private memory pool per capture: the previous graph (and its
+        # pool) is released once the new one replaces it
+        self.graph, self.out = None, None
         self.graph = torch.cuda.CUDAGraph()
-        if self.pool is None:
-            self.pool = torch.cuda.graph_pool_handle()
+        self.pool = torch.cuda.graph_pool_handle()
         self.capturing = True
         try:
             # capture on a side stream; the staged inputs were copied on the
