@@ -208,13 +208,16 @@ def main():
 
     # ---- timed region 1: device-resident steps (value) ----
     clocks = ClockSampler(local)
-    # events only around the roofline kernel (2 events per step; negligible)
-    prof_names = ["hg_load_features"]
+    # device-side kernel timers (%globaltimer spans; the step is a CUDA graph,
+    # where host events cannot bracket a single kernel node)
+    timers = torch.zeros(8 * 8, dtype=torch.int64, device=dev)
+    timers.view(8, 8)[:, 0] = -1
+    g_before = tr.cache.gctr.clone()
     barrier()
     torch.cuda.synchronize()
+    _lib.call("hg_set_kernel_timers", _lib.ptr(timers))
     clocks.start()
     launches0 = _lib.load().hg_kernel_launches()
-    _lib.enable_profile(prof_names)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     losses = []
@@ -222,35 +225,38 @@ def main():
         losses.append(tr.train_step_resident(staged[s]))
     e1.record()
     torch.cuda.synchronize()
-    prof = _lib.disable_profile()
+    _lib.call("hg_set_kernel_timers", None)
     launches = _lib.load().hg_kernel_launches() - launches0
     barrier()
     clk = clocks.stop()
     t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
     value = BATCH * world * args.steps / t_dev
+    graph_mode = any(e.graph is not None for e in tr._engines.values())
 
-    # roofline of the feature gather (hg_load_features): algorithmic bytes per launch
+    # roofline of the feature gather (k_load_rows): algorithmic bytes =
+    # live layer-0 rows x (row read + fp32 row write + 3 index reads); the live
+    # rows of the timed steps = delta(feature_hits + feature_misses)
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peak, peak_src = 6551.4, "fallback"
     if os.path.exists(peaks_path):
         peak, peak_src = json.load(open(peaks_path))["hbm_gbs"], "measured"
-    per_kernel = {}
-    for name, recs in prof.items():
-        ms = sum(a.elapsed_time(b) for a, b, _ in recs)
-        per_kernel[name] = {"launches": len(recs), "ms_total": ms}
-    gather = prof["hg_load_features"]
-    g_bytes = 0
-    for _, _, a in gather:
-        n_live, dim, dtype = a[1], a[7], a[8]
-        isz = 2 if dtype == 1 else 4
-        g_bytes += n_live * (dim * isz + dim * 4 + 12)  # row read + fp32 row write + 3 index reads
-    g_time = per_kernel["hg_load_features"]["ms_total"] / 1e3
+    tv = timers.view(8, 8).cpu().tolist()
+    names = ["k_load_rows", "k_aggregate", "k_transpose_agg", "k_select"]
+    per_kernel = {n: {"launches": int(tv[i][3]), "ms_total": tv[i][2] / 1e6,
+                      "share_of_step": (tv[i][2] / 1e9) / t_dev} for i, n in enumerate(names)}
+    g_delta = (tr.cache.gctr - g_before).cpu().tolist()
+    rows = g_delta[0] + g_delta[1]
+    isz = tr.features.element_size()
+    g_bytes = rows * (cfgd["d"] * isz + cfgd["d"] * 4 + 12)
+    g_time = tv[0][2] / 1e9
+    n_launch = max(1, int(tv[0][3]))
     achieved = g_bytes / g_time / 1e9 if g_time > 0 else 0.0
     roofline = {"kernel": "k_load_rows (hg_load_features, feature gather)", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": peak_src, "traffic": None,
-                "bytes_per_launch": g_bytes / max(1, len(gather)),
-                "share_of_step": g_time / (t_dev) if t_dev else None}
+                "bytes_per_launch": g_bytes / n_launch, "avg_launch_us": 1e6 * g_time / n_launch,
+                "timing": "device %globaltimer span per launch, accumulated over the timed region",
+                "share_of_step": g_time / t_dev if t_dev else None}
 
     # ---- timed region 2: end-to-end through the public API (host in, host out) ----
     barrier()
@@ -269,7 +275,7 @@ def main():
            "api": "Trainer.train_step (host seeds in, IterMetrics read back every step)"}
 
     out = dict(base, value=value, ms_per_step=1e3 * t_dev / args.steps, e2e=e2e, roofline=roofline,
-               gpu_launches=int(launches), clocks=clk, per_kernel=per_kernel,
+               gpu_launches=int(launches), clocks=clk, per_kernel=per_kernel, cuda_graph=graph_mode,
                loss_last=float(losses[-1].item()), io_saving_last=None)
     out["io_saving_e2e_last"] = 1.0 - m.fetched_bytes / m.baseline_bytes if m.baseline_bytes else None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

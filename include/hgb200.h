@@ -33,6 +33,10 @@ const char* hg_last_error(void);
 int hg_device_sync(void);
 /* number of hand-written hg kernels launched by this process (library GEMMs excluded) */
 long long hg_kernel_launches(void);
+/* device-side kernel timers for kernels replayed inside CUDA graphs: buf is
+ * u64[8 * 8] (per timer: start=~0, end, total_ns, launches, ...), NULL = off.
+ * Timer 0 = k_load_rows, 1 = k_aggregate, 2 = k_transpose_agg, 3 = k_select. */
+int hg_set_kernel_timers(void* buf);
 
 /* ---- K1+K2 sampler: histgnn/sampler.py:118-163 (_sample_in_neighbors,
  * _build_block), called per layer by sampler.py:166-190 (sample_layered).

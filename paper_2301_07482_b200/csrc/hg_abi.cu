@@ -32,6 +32,14 @@ extern "C" {
 
 int hg_version(void) { return 10000; }  // 1.0.0
 
+// device-side kernel timers (hg::KTimer[kNumTimers]; start fields = ~0), or NULL to disable
+int hg_set_kernel_timers(void* buf) {
+  int st = hg::set_timers_gather(buf);
+  if (!st) st = hg::set_timers_layer(buf);
+  if (!st) st = hg::set_timers_sampler(buf);
+  return st;
+}
+
 // number of hand-written hg kernels launched by this process so far
 long long hg_kernel_launches(void) { return hg::g_launches.load(std::memory_order_relaxed); }
 

@@ -82,9 +82,50 @@ __device__ __forceinline__ uint4 ldg_stream_u4(const uint4* p) {
   return r;
 }
 
+// ---- device-side kernel timers (work inside CUDA graphs, where events can't
+// bracket a single node): span from the first CTA start to the last CTA end
+// (%globaltimer, ns), accumulated per launch by the last CTA to finish.
+struct KTimer {
+  unsigned long long start, end, total_ns, launches, done, pad[3];
+};
+enum TimerId : int { kTLoadRows = 0, kTAggregate = 1, kTTransposeAgg = 2, kTSelect = 3, kNumTimers = 8 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void kt_begin(KTimer* kt) {
+  if (kt && threadIdx.x == 0) atomicMin(&kt->start, gtimer());
+}
+// every thread of the CTA must reach this
+__device__ __forceinline__ void kt_end(KTimer* kt) {
+  if (!kt) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMax(&kt->end, gtimer());
+    __threadfence();
+    const unsigned long long n = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+    if (atomicAdd(&kt->done, 1ull) == n - 1) {
+      __threadfence();
+      const unsigned long long s = atomicAdd(&kt->start, 0ull), e = atomicAdd(&kt->end, 0ull);
+      kt->total_ns += e - s;
+      kt->launches += 1;
+      kt->start = ~0ull;
+      kt->end = 0;
+      kt->done = 0;
+      __threadfence();
+    }
+  }
+}
+
+int set_timers_gather(void* p);
+int set_timers_layer(void* p);
+int set_timers_sampler(void* p);
+
 }  // namespace hg
 
-#define HG_CHECK_CUDA(where, expr)                                         \
+#define HG_CHECK_CUDA(where, expr)                                       \
   do {                                                                     \
     cudaError_t _e = (expr);                                               \
     if (_e != cudaSuccess)                                                 \

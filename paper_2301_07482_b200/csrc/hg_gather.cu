@@ -20,6 +20,14 @@
 namespace hg {
 namespace {
 
+__device__ KTimer* g_kt = nullptr;
+}  // namespace
+int set_timers_gather(void* p) {
+  cudaError_t e = cudaMemcpyToSymbol(g_kt, &p, sizeof(p));
+  return e == cudaSuccess ? kOk : fail("set_timers_gather", kCuda, cudaGetErrorString(e));
+}
+namespace {
+
 constexpr int kRows = 8;        // rows a warp keeps in flight
 constexpr int kMaxT = 4;        // 16-byte vectors per lane per row (rows <= 2 KB)
 
@@ -39,6 +47,8 @@ __global__ void __launch_bounds__(256) k_load_rows(const int32_t* n_live_dev, co
   const int n = *n_live_dev;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
+  KTimer* kt = g_kt ? g_kt + kTLoadRows : nullptr;
+  kt_begin(kt);
   for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g * kRows < n; g += warps) {
     const int i = g * kRows + lane;
     int loc = -1;
@@ -88,6 +98,7 @@ __global__ void __launch_bounds__(256) k_load_rows(const int32_t* n_live_dev, co
       if (valid & ~hits) atomicAdd(gctr + kGCtrFeatureMisses, (unsigned long long)__popc(valid & ~hits));
     }
   }
+  kt_end(kt);
 }
 
 }  // namespace

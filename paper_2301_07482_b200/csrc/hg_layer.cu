@@ -26,6 +26,14 @@
 namespace hg {
 namespace {
 
+__device__ KTimer* g_kt = nullptr;
+}  // namespace
+int set_timers_layer(void* p) {
+  cudaError_t e = cudaMemcpyToSymbol(g_kt, &p, sizeof(p));
+  return e == cudaSuccess ? kOk : fail("set_timers_layer", kCuda, cudaGetErrorString(e));
+}
+namespace {
+
 constexpr int kKindGCN = 0;
 constexpr int kKindSAGE = 1;
 constexpr int kMaxVecPerLane = 4;  // d_in <= 512 floats
@@ -51,6 +59,8 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
   const int nv = d >> 2;
   const int K = kKind == kKindSAGE ? 2 * d : d;
   const int warps = (gridDim.x * blockDim.x) >> 5;
+  KTimer* kt = g_kt ? g_kt + kTAggregate : nullptr;
+  kt_begin(kt);
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < R; i += warps) {
     const int r = rows[i];
     const int e0 = start[r], e1 = end[r];
@@ -108,6 +118,7 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
     }
     if (lane == 0) reinterpret_cast<float4*>(arow + K)[0] = make_float4(1.f, 0.f, 0.f, 0.f);
   }
+  kt_end(kt);
 }
 
 __global__ void k_scatter_rows(const int32_t* R_dev, const int32_t* __restrict__ rows, const float* __restrict__ Z,
@@ -237,6 +248,8 @@ __global__ void __launch_bounds__(256) k_transpose_agg(
   const int nv = d >> 2;
   const int goff = kKind == kKindSAGE ? d : 0;  // neighbour half of [S | G]
   const int warps = (gridDim.x * blockDim.x) >> 5;
+  KTimer* kt = g_kt ? g_kt + kTTransposeAgg : nullptr;
+  kt_begin(kt);
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
     const int c = live[i];
     float4 acc[kMaxVecPerLane];
@@ -293,6 +306,7 @@ __global__ void __launch_bounds__(256) k_transpose_agg(
     sq = warp_sum_fixed(sq);
     if (lane == 0) norms[i] = sqrt(sq);
   }
+  kt_end(kt);
 }
 
 __global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, long long n, float eta) {

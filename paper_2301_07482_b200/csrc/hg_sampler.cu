@@ -25,6 +25,14 @@ __device__ JumpTable g_jump;
 
 namespace {
 
+__device__ KTimer* g_kt = nullptr;
+}  // namespace
+int set_timers_sampler(void* p) {
+  cudaError_t e = cudaMemcpyToSymbol(g_kt, &p, sizeof(p));
+  return e == cudaSuccess ? kOk : fail("set_timers_sampler", kCuda, cudaGetErrorString(e));
+}
+namespace {
+
 struct KeyJ {
   unsigned long long k;
   unsigned j;
@@ -186,6 +194,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const unsigned long long base0 = ss->stream_pos;
+  KTimer* kt = g_kt ? g_kt + kTSelect : nullptr;
+  kt_begin(kt);
   const u128 a32 = tab.A[1][2];            // MULT^32 and its increment term
   const u128 c32 = tab.C[1][2];
   for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < F; row += warps) {
@@ -293,6 +303,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
       }
     }
   }
+  kt_end(kt);
 }
 
 struct PopWord {
