@@ -86,7 +86,7 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
  * _mean_matrix, _layer_forward_ctx). kind 0 = GCN, 1 = SAGE_MEAN. */
 int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
                      const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
-                     const float* h_in, int d, float* A, int ldA, cudaStream_t stream);
+                     const float* h_in, int d, void* A_ts, cudaStream_t stream);
 
 /* ---- K7 dense transform: nn.py:150,156,170-176 (the GEMMs). Row-major. */
 int hg_gemm_rm(int transA, int transB, long long M, long long N, long long K, const float* A, long long lda,
@@ -104,6 +104,22 @@ int hg_tc_linear_dgrad(const int32_t* R_dev, long long R_max, const float* dz, i
 int hg_tc_linear_wgrad(const int32_t* R_dev, long long R_max, const float* A, long long ldA, int K1, const float* dz,
                        int N, float* dP, float* partial, int splits, cudaStream_t stream);
 
+/* ---- K7 on tcgen05 over TS operands (bf16 hi/lo core-matrix tiles in HBM, written by
+ * hg_aggregate_fwd / hg_gather_dz / hg_ts_pack; layout in csrc/hg_ts.cuh). Operand
+ * tiles stream into a 3-stage smem ring with cp.async.bulk; one thread issues
+ * tcgen05.mma; fp32 accumulators in TMEM.
+ *   fwd:   h_out[rows[i]] = relu?(A_ts[i,:K1] . PT_ts^T),  PT_ts = TS(P^T)   nn.py:150,156,289
+ *   dgrad: SG = dz_ts . W_ts^T,  W_ts = TS(P[:K])                           nn.py:171,175-176
+ *   wgrad: dP = A_ts^T . dz_ts over the rows (split-K, fixed-order sum)       nn.py:170,173-174 */
+long long hg_ts_bytes(long long rows, int cols);
+int hg_ts_pack(const float* src, long long ld, int transposed, int rows, int cols, void* dst, cudaStream_t stream);
+int hg_ts_linear_fwd(const int32_t* R_dev, long long R_max, const void* A_ts, int K1, const void* PT_ts, int N,
+                     const int32_t* rows, int relu, float* h_out, cudaStream_t stream);
+int hg_ts_linear_dgrad(const int32_t* R_dev, long long R_max, const void* dz_ts, int N, const void* W_ts, int K,
+                       float* SG, cudaStream_t stream);
+int hg_ts_linear_wgrad(const int32_t* R_dev, long long R_max, const void* A_ts, int K1, const void* dz_ts, int N,
+                       float* dP, float* partial, int splits, cudaStream_t stream);
+
 /* ---- forward epilogue: nn.py:161-162,288-293 (ReLU, h_full[rows], injected rows) */
 int hg_scatter_rows(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* Z, int dout, int relu,
                     float* h_out, cudaStream_t stream);
@@ -116,7 +132,7 @@ int hg_cross_entropy(const float* logits, const int32_t* labels, int B, int C, f
 
 /* ---- K8 backward: nn.py:166-177,300-320 (_layer_backward, backward) */
 int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* d_h, const float* h_out,
-                 int dout, int relu, float* dz, cudaStream_t stream);
+                 int dout, int relu, void* dz_ts, cudaStream_t stream);
 long long hg_csc_scratch_bytes(long long E_max);
 int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t* keep, const int32_t* pos_of,
                  const int32_t* col, long long E_max, long long n_src_max, unsigned* keys_sorted,

@@ -37,7 +37,7 @@ SIGNATURES = {
     "hg_prune_block": (I32, [P, I64, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P]),
     "hg_cache_lookup": (I32, [P, I64, P, P, I64, P, P, P, P, F64, P, P, P, P]),
     "hg_load_features": (I32, [P, I64, P, P, P, P, P, I32, I32, P, P, P]),
-    "hg_aggregate_fwd": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, P, I32, P]),
+    "hg_aggregate_fwd": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, P, P]),
     "hg_gemm_rm": (I32, [I32, I32, I64, I64, I64, P, I64, P, I64, F32, P, I64, P]),
     "hg_scatter_rows": (I32, [P, I64, P, P, I32, I32, P, P]),
     "hg_inject_rows": (I32, [P, I64, P, P, P, I32, P, P]),
@@ -57,6 +57,11 @@ SIGNATURES = {
     "hg_tc_linear_fwd": (I32, [P, I64, P, I64, I32, P, I32, P, I32, P, P]),
     "hg_tc_linear_dgrad": (I32, [P, I64, P, I32, P, I32, P, P]),
     "hg_tc_linear_wgrad": (I32, [P, I64, P, I64, I32, P, I32, P, P, I32, P]),
+    "hg_ts_bytes": (I64, [I64, I32]),
+    "hg_ts_pack": (I32, [P, I64, I32, I32, I32, P, P]),
+    "hg_ts_linear_fwd": (I32, [P, I64, P, I32, P, I32, P, I32, P, P]),
+    "hg_ts_linear_dgrad": (I32, [P, I64, P, I32, P, I32, P, P]),
+    "hg_ts_linear_wgrad": (I32, [P, I64, P, I32, P, I32, P, P, I32, P]),
 }
 
 _lib = None

@@ -22,6 +22,7 @@
 
 #include "hg_scan.cuh"
 #include "hg_state.h"
+#include "hg_ts.cuh"
 
 namespace hg {
 namespace {
@@ -37,6 +38,7 @@ namespace {
 constexpr int kKindGCN = 0;
 constexpr int kKindSAGE = 1;
 constexpr int kMaxVecPerLane = 4;  // d_in <= 512 floats
+constexpr int kMaxRowFloats = 1056; // [self | agg | 1 | pad] <= 2*512 + 32
 
 __device__ __forceinline__ float4 f4_fmadd_rn(float4 acc, float c, float4 x) {
   return make_float4(__fadd_rn(acc.x, __fmul_rn(c, x.x)), __fadd_rn(acc.y, __fmul_rn(c, x.y)),
@@ -53,11 +55,14 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
                                                    const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
-                                                   int d, float* __restrict__ A, int ldA) {
+                                                   int d, uint8_t* __restrict__ A_ts) {
+  __shared__ __align__(16) float s_rows[8][kMaxRowFloats];
   const int R = *R_dev;
   const int lane = threadIdx.x & 31;
   const int nv = d >> 2;
   const int K = kKind == kKindSAGE ? 2 * d : d;
+  const int nK = (K + 1 + 31) / 32;          // TS column chunks of [. | 1 | 0 pad]
+  float* srow = s_rows[threadIdx.x >> 5];
   const int warps = (gridDim.x * blockDim.x) >> 5;
   KTimer* kt = g_kt ? g_kt + kTAggregate : nullptr;
   kt_begin(kt);
@@ -101,23 +106,33 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
         if (v < nv) acc[t] = f4_fmadd_rn(acc[t], w0, reinterpret_cast<const float4*>(h_in + (long long)c0 * d)[v]);
       }
     }
-    float* arow = A + (long long)i * ldA;
+    // assemble [self | agg | 1 | 0...] (SAGE) or [agg | 1 | 0...] (GCN) in smem,
+    // then emit it as bf16 hi/lo TS core-matrix rows (hg_ts.cuh)
     const float4* hs = reinterpret_cast<const float4*>(h_in + (long long)r * d);
 #pragma unroll
     for (int t = 0; t < kMaxVecPerLane; ++t) {
       const int v = lane + 32 * t;
       if (v < nv) {
         if (kKind == kKindSAGE) {
-          reinterpret_cast<float4*>(arow)[v] = hs[v];
-          reinterpret_cast<float4*>(arow + d)[v] = acc[t];
+          reinterpret_cast<float4*>(srow)[v] = hs[v];
+          reinterpret_cast<float4*>(srow + d)[v] = acc[t];
         } else {
           const float ws = gcn_coef(dd, src_deg[r]);
-          reinterpret_cast<float4*>(arow)[v] = f4_fmadd_rn(acc[t], ws, hs[v]);
+          reinterpret_cast<float4*>(srow)[v] = f4_fmadd_rn(acc[t], ws, hs[v]);
         }
       }
     }
-    if (lane == 0) reinterpret_cast<float4*>(arow + K)[0] = make_float4(1.f, 0.f, 0.f, 0.f);
+    for (int c = K + lane; c < nK * 32; c += 32) srow[c] = c == K ? 1.f : 0.f;
+    __syncwarp();
+    for (int g = lane; g < nK * 4; g += 32) ts_store8(A_ts, nK, i, g, srow + g * 8);
+    __syncwarp();
   }
+  // zero the padding rows of the last 128-row tile (the weight-gradient GEMM
+  // reduces over rows, so they must not hold garbage)
+  const int R_pad = (R + kTsRows - 1) / kTsRows * kTsRows;
+  const float zeros[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int i = R + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < R_pad; i += warps)
+    for (int g = lane; g < nK * 4; g += 32) ts_store8(A_ts, nK, i, g, zeros);
   kt_end(kt);
 }
 
@@ -187,16 +202,36 @@ __global__ void __launch_bounds__(1024) k_ce_loss(const double* __restrict__ row
   }
 }
 
-__global__ void k_gather_dz(const int32_t* R_dev, const int32_t* __restrict__ rows, const float* __restrict__ d_h,
-                            const float* __restrict__ h_out, int dout, int relu, float* __restrict__ dz) {
-  const long long n = (long long)(*R_dev) * dout;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(t / dout), j = (int)(t - (long long)i * dout);
-    const long long src = (long long)rows[i] * dout + j;
-    float g = d_h[src];
-    if (relu && !(h_out[src] > 0.f)) g = 0.f;
-    dz[t] = g;
+// dz[i] = d_h[rows[i]] * (h_out[rows[i]] > 0), emitted as TS (hg_ts.cuh): one
+// warp per row, staged through smem; padding rows of the last tile are zeroed.
+__global__ void __launch_bounds__(256) k_gather_dz(const int32_t* R_dev, const int32_t* __restrict__ rows,
+                                                   const float* __restrict__ d_h, const float* __restrict__ h_out,
+                                                   int dout, int relu, uint8_t* __restrict__ dz_ts) {
+  __shared__ __align__(16) float s_rows[8][kMaxRowFloats];
+  const int R = *R_dev;
+  const int lane = threadIdx.x & 31;
+  const int nK = (dout + 31) / 32;
+  float* srow = s_rows[threadIdx.x >> 5];
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int i = w0; i < R; i += warps) {
+    const long long base = (long long)rows[i] * dout;
+    for (int j = lane; j < nK * 32; j += 32) {
+      float g = 0.f;
+      if (j < dout) {
+        g = d_h[base + j];
+        if (relu && !(h_out[base + j] > 0.f)) g = 0.f;
+      }
+      srow[j] = g;
+    }
+    __syncwarp();
+    for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK, i, g, srow + g * 8);
+    __syncwarp();
   }
+  const int R_pad = (R + kTsRows - 1) / kTsRows * kTsRows;
+  const float zeros[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int i = R + w0; i < R_pad; i += warps)
+    for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK, i, g, zeros);
 }
 
 // CSC keys over the block's original edge extents: surviving edges keep their
@@ -338,16 +373,17 @@ extern "C" {
 
 int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
                      const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
-                     const float* h_in, int d, float* A, int ldA, cudaStream_t stream) {
+                     const float* h_in, int d, void* A_ts, cudaStream_t stream) {
   const char* W = "hg_aggregate_fwd";
   if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 512");
-  const int K = kind == kKindSAGE ? 2 * d : d;
-  if (ldA != K + 4) return fail(W, kBadArg, "ldA must be K + 4");
-  const unsigned grid = grid_for(R_max * 32, 256, 148 * 16);
+  // grid covers the compute rows and the zero padding up to the next 128-row tile
+  const long long rows_pad = (R_max + kTsRows - 1) / kTsRows * kTsRows;
+  const unsigned grid = grid_for(rows_pad * 32, 256, 148 * 16);
+  uint8_t* a = static_cast<uint8_t*>(A_ts);
   if (kind == kKindSAGE)
-    k_aggregate<kKindSAGE><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, A, ldA);
+    k_aggregate<kKindSAGE><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a);
   else
-    k_aggregate<kKindGCN><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, A, ldA);
+    k_aggregate<kKindGCN><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a);
   HG_LAUNCHED(W);
   return kOk;
 }
@@ -377,8 +413,11 @@ int hg_cross_entropy(const float* logits, const int32_t* labels, int B, int C, f
 }
 
 int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* d_h, const float* h_out,
-                 int dout, int relu, float* dz, cudaStream_t stream) {
-  k_gather_dz<<<grid_for(R_max * dout, 256), 256, 0, stream>>>(R_dev, rows, d_h, h_out, dout, relu, dz);
+                 int dout, int relu, void* dz_ts, cudaStream_t stream) {
+  if (dout > kMaxRowFloats) return fail("hg_gather_dz", kBadArg, "row too wide");
+  const long long rows_pad = (R_max + kTsRows - 1) / kTsRows * kTsRows;
+  k_gather_dz<<<grid_for(rows_pad * 32, 256, 148 * 16), 256, 0, stream>>>(R_dev, rows, d_h, h_out, dout, relu,
+                                                                         static_cast<uint8_t*>(dz_ts));
   HG_LAUNCHED("hg_gather_dz");
   return kOk;
 }

@@ -32,16 +32,11 @@ from .graphs import _np
 
 KIND_GCN, KIND_SAGE = 0, 1
 
-# Dense transform engine: the tcgen05 kernels (hg_tc_linear_*). "cublas"
-# (fp32 SGEMM) is kept only as a cross-check for tests/diagnostics.
-GEMM_ENGINE = os.environ.get("HG_GEMM", "tcgen05")
-
-
 def _wgrad_splits(R: int, K1: int, n: int) -> int:
-    """Split-K factor for dP = A^T dz: fill ~2 CTAs per SM, >= 8 chunks each."""
+    """Split-K factor for dP = A^T dz: ~1 CTA per SM, >= 8 chunks of 32 rows each."""
     tiles = ((K1 + 127) // 128) * ((n + 255) // 256)
     chunks = max(1, (R + 31) // 32)
-    return max(1, min(2 * 148 // tiles, chunks // 8))
+    return max(1, min(148 // tiles, chunks // 8))
 
 
 class LayerKind(enum.Enum):
@@ -249,28 +244,29 @@ def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch
         raise ValueError(f"h_in has {h_in.shape[0]} rows, frontier needs {blk.num_src}")
     kind = _kind_code(net.kind)
     K = 2 * d_in if kind == KIND_SAGE else d_in
-    ldA = K + 4
-    A = torch.empty((R, ldA), dtype=torch.float32, device=dev)
+    # GEMM operand [self | agg | 1] written by the aggregation directly as TS
+    # (bf16 hi/lo core-matrix tiles, csrc/hg_ts.cuh)
+    A = torch.empty(ts_bytes(R, K + 1), dtype=torch.uint8, device=dev)
     _lib.call("hg_aggregate_fwd", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(blk.adj.start),
               _lib.ptr(blk.adj.end), _lib.ptr(blk.adj.col_indices), _lib.ptr(blk.dst_deg), _lib.ptr(blk.src_deg),
-              _lib.ptr(h_in), d_in, _lib.ptr(A), ldA, stream)
+              _lib.ptr(h_in), d_in, _lib.ptr(A), stream)
+    slab = net.slab(l)
+    PT = torch.empty(ts_bytes(d_out, K + 1), dtype=torch.uint8, device=dev)   # TS(P^T): B of the forward
+    _lib.call("hg_ts_pack", _lib.ptr(slab), d_out, 1, d_out, K + 1, _lib.ptr(PT), stream)
     n_dst = blk.num_dst
     h_out = torch.empty((n_dst, d_out), dtype=torch.float32, device=dev)
-    if GEMM_ENGINE == "tcgen05":
-        # z = [A | 1] . P on tcgen05, ReLU + scatter to h_out[rows] in the epilogue
-        _lib.call("hg_tc_linear_fwd", _lib.ptr(R_dev), R, _lib.ptr(A), ldA, K + 1, _lib.ptr(net.slab(l)), d_out,
-                  _lib.ptr(rows), int(act), _lib.ptr(h_out), stream)
-    else:
-        Z = torch.empty((R, d_out), dtype=torch.float32, device=dev)
-        _lib.call("hg_gemm_rm", 0, 0, R, d_out, K + 1, _lib.ptr(A), ldA, _lib.ptr(net.slab(l)), d_out, 0.0,
-                  _lib.ptr(Z), d_out, stream)
-        _lib.call("hg_scatter_rows", _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(Z), d_out, int(act),
-                  _lib.ptr(h_out), stream)
+    # z = [A | 1] . P on tcgen05, ReLU + scatter to h_out[rows] in the epilogue
+    _lib.call("hg_ts_linear_fwd", _lib.ptr(R_dev), R, _lib.ptr(A), K + 1, _lib.ptr(PT), d_out, _lib.ptr(rows),
+              int(act), _lib.ptr(h_out), stream)
     if inj is not None:
         nd = n_dst_dev if n_dst_dev is not None else _dev_count(n_dst, dev)
         _lib.call("hg_inject_rows", _lib.ptr(nd), n_dst, _lib.ptr(inj.flag),
                   _lib.ptr(inj.row), _lib.ptr(inj.table), d_out, _lib.ptr(h_out), stream)
     return LayerTape(rows, R, R_dev, A, K, act, h_out, inj)
+
+
+def ts_bytes(rows: int, cols: int) -> int:
+    return int(_lib.query("hg_ts_bytes", int(rows), int(cols)))
 
 
 def _rows_tensor(rows, n_dst, dev):
@@ -357,28 +353,21 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
     dev = d_h.device
     d_in_dim, d_out = net.dims[l], net.dims[l + 1]
     R, K = t.R, t.K
-    dz = torch.empty((R, d_out), dtype=torch.float32, device=dev)
+    # dz (ReLU-masked output gradient of the compute rows) as a TS operand
+    dz = torch.empty(ts_bytes(R, d_out), dtype=torch.uint8, device=dev)
     _lib.call("hg_gather_dz", _lib.ptr(t.R_dev), R, _lib.ptr(t.rows), _lib.ptr(d_h), _lib.ptr(t.h_out), d_out,
               int(t.relu), _lib.ptr(dz), stream)
     dP = grads.slab(l)
-    ldA = K + 4
-    if GEMM_ENGINE == "tcgen05":
-        splits = _wgrad_splits(R, K + 1, d_out)
-        part = torch.empty(splits * (K + 1) * d_out, dtype=torch.float32, device=dev)
-        _lib.call("hg_tc_linear_wgrad", _lib.ptr(t.R_dev), R, _lib.ptr(t.A), ldA, K + 1, _lib.ptr(dz), d_out,
-                  _lib.ptr(dP), _lib.ptr(part), splits, stream)
-    else:
-        _lib.call("hg_gemm_rm", 1, 0, K + 1, d_out, R, _lib.ptr(t.A), ldA, _lib.ptr(dz), d_out, 0.0,
-                  _lib.ptr(dP), d_out, stream)
+    splits = _wgrad_splits(R, K + 1, d_out)
+    part = torch.empty(splits * (K + 1) * d_out, dtype=torch.float32, device=dev)
+    _lib.call("hg_ts_linear_wgrad", _lib.ptr(t.R_dev), R, _lib.ptr(t.A), K + 1, _lib.ptr(dz), d_out,
+              _lib.ptr(dP), _lib.ptr(part), splits, stream)
     if not need_input:
         return None, None
     SG = torch.empty((R, K), dtype=torch.float32, device=dev)
-    if GEMM_ENGINE == "tcgen05":
-        _lib.call("hg_tc_linear_dgrad", _lib.ptr(t.R_dev), R, _lib.ptr(dz), d_out, _lib.ptr(net.slab(l)), K,
-                  _lib.ptr(SG), stream)
-    else:
-        _lib.call("hg_gemm_rm", 0, 1, R, K, d_out, _lib.ptr(dz), d_out, _lib.ptr(net.slab(l)), d_out, 0.0,
-                  _lib.ptr(SG), K, stream)
+    W = torch.empty(ts_bytes(K, d_out), dtype=torch.uint8, device=dev)        # TS(P[:K]): B of the dgrad
+    _lib.call("hg_ts_pack", _lib.ptr(net.slab(l)), d_out, 0, K, d_out, _lib.ptr(W), stream)
+    _lib.call("hg_ts_linear_dgrad", _lib.ptr(t.R_dev), R, _lib.ptr(dz), d_out, _lib.ptr(W), K, _lib.ptr(SG), stream)
     if n_dst_dev is None:
         n_dst_dev = _dev_count(blk.num_dst, dev)
     if n_live_dev is None:

@@ -78,3 +78,79 @@ def test_wgrad_splitk_deterministic(R, R_max, K1, N, splits):
     ref = A[:R, :K1].double().T @ dz[:R].double()
     assert rel(outs[0], ref) < 2e-5
     assert torch.equal(outs[0], outs[1])
+
+
+# ---- bulk-copy pipeline over TS operands (the product path) ----
+
+def _ts(lib, X, rows=None):
+    """TS-pack a row-major fp32 matrix (rows beyond `rows` treated as absent)."""
+    r, c = X.shape
+    rows = r if rows is None else rows
+    buf = torch.empty(lib.query("hg_ts_bytes", r, c), dtype=torch.uint8, device="cuda")
+    lib.call("hg_ts_pack", lib.ptr(X), c, 0, rows, c, lib.ptr(buf), lib.stream_ptr())
+    return buf
+
+
+def _ts_T(lib, P):
+    """TS of P^T for a row-major P [K1 x N]."""
+    K1, N = P.shape
+    buf = torch.empty(lib.query("hg_ts_bytes", N, K1), dtype=torch.uint8, device="cuda")
+    lib.call("hg_ts_pack", lib.ptr(P), N, 1, N, K1, lib.ptr(buf), lib.stream_ptr())
+    return buf
+
+
+@pytest.mark.parametrize("R,R_max,K1,N,relu", [(1000, 1000, 201, 256, 1), (777, 1024, 513, 256, 1),
+                                               (130, 200, 513, 47, 0), (1, 128, 33, 8, 0), (4096, 5000, 257, 172, 1)])
+def test_ts_forward_scatter(R, R_max, K1, N, relu):
+    lib = _lib()
+    g = torch.Generator(device="cuda").manual_seed(R + K1)
+    A = torch.randn(R_max, K1, device="cuda", generator=g)
+    P = torch.randn(K1, N, device="cuda", generator=g) * 0.1
+    rows = torch.randperm(R_max, device="cuda", generator=g)[:R].sort().values.to(torch.int32)
+    out = torch.full((R_max, N), float("nan"), device="cuda")
+    R_dev = torch.tensor([R], dtype=torch.int32, device="cuda")
+    lib.call("hg_ts_linear_fwd", lib.ptr(R_dev), R_max, lib.ptr(_ts(lib, A, R)), K1, lib.ptr(_ts_T(lib, P)), N,
+             lib.ptr(rows), relu, lib.ptr(out), lib.stream_ptr())
+    z = A[:R].double() @ P.double()
+    if relu:
+        z = z.clamp_min(0)
+    assert rel(out[rows.long()], z) < 2e-5
+    mask = torch.ones(R_max, dtype=torch.bool, device="cuda")
+    mask[rows.long()] = False
+    assert torch.isnan(out[mask]).all()
+
+
+@pytest.mark.parametrize("R,R_max,N,K", [(1000, 1000, 256, 512), (333, 600, 47, 256), (5, 128, 8, 64),
+                                         (3000, 3000, 256, 200)])
+def test_ts_dgrad(R, R_max, N, K):
+    lib = _lib()
+    g = torch.Generator(device="cuda").manual_seed(R + N)
+    dz = torch.randn(R_max, N, device="cuda", generator=g)
+    P = torch.randn(K + 1, N, device="cuda", generator=g)
+    SG = torch.zeros(R_max, K, device="cuda")
+    R_dev = torch.tensor([R], dtype=torch.int32, device="cuda")
+    lib.call("hg_ts_linear_dgrad", lib.ptr(R_dev), R_max, lib.ptr(_ts(lib, dz, R)), N, lib.ptr(_ts(lib, P[:K].contiguous())),
+             K, lib.ptr(SG), lib.stream_ptr())
+    assert rel(SG[:R], dz[:R].double() @ P[:K].double().T) < 2e-5
+
+
+@pytest.mark.parametrize("R,R_max,K1,N,splits", [(5000, 6000, 201, 256, 16), (300, 300, 513, 256, 4),
+                                                 (50, 64, 257, 47, 3), (70000, 70000, 513, 256, 64),
+                                                 (129, 4000, 201, 8, 7)])
+def test_ts_wgrad_splitk_deterministic(R, R_max, K1, N, splits):
+    lib = _lib()
+    g = torch.Generator(device="cuda").manual_seed(R + K1)
+    A = torch.randn(R_max, K1, device="cuda", generator=g)
+    dz = torch.randn(R_max, N, device="cuda", generator=g) * 1e-3
+    R_dev = torch.tensor([R], dtype=torch.int32, device="cuda")
+    A_ts, dz_ts = _ts(lib, A, R), _ts(lib, dz, R)
+    outs = []
+    for _ in range(2):
+        dP = torch.empty(K1, N, device="cuda")
+        part = torch.empty(splits * K1 * N, device="cuda")
+        lib.call("hg_ts_linear_wgrad", lib.ptr(R_dev), R_max, lib.ptr(A_ts), K1, lib.ptr(dz_ts), N, lib.ptr(dP),
+                 lib.ptr(part), splits, lib.stream_ptr())
+        outs.append(dP.clone())
+    ref = A[:R].double().T @ dz[:R].double()
+    assert rel(outs[0], ref) < 2e-5
+    assert torch.equal(outs[0], outs[1])
