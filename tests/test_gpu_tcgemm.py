@@ -109,8 +109,10 @@ def test_ts_forward_scatter(R, R_max, K1, N, relu):
     rows = torch.randperm(R_max, device="cuda", generator=g)[:R].sort().values.to(torch.int32)
     out = torch.full((R_max, N), float("nan"), device="cuda")
     R_dev = torch.tensor([R], dtype=torch.int32, device="cuda")
-    lib.call("hg_ts_linear_fwd", lib.ptr(R_dev), R_max, lib.ptr(_ts(lib, A, R)), K1, lib.ptr(_ts_T(lib, P)), N,
+    A_ts, PT_ts = _ts(lib, A, R), _ts_T(lib, P)     # keep the buffers alive until the kernel ran
+    lib.call("hg_ts_linear_fwd", lib.ptr(R_dev), R_max, lib.ptr(A_ts), K1, lib.ptr(PT_ts), N,
              lib.ptr(rows), relu, lib.ptr(out), lib.stream_ptr())
+    torch.cuda.synchronize()
     z = A[:R].double() @ P.double()
     if relu:
         z = z.clamp_min(0)
@@ -129,8 +131,11 @@ def test_ts_dgrad(R, R_max, N, K):
     P = torch.randn(K + 1, N, device="cuda", generator=g)
     SG = torch.zeros(R_max, K, device="cuda")
     R_dev = torch.tensor([R], dtype=torch.int32, device="cuda")
-    lib.call("hg_ts_linear_dgrad", lib.ptr(R_dev), R_max, lib.ptr(_ts(lib, dz, R)), N, lib.ptr(_ts(lib, P[:K].contiguous())),
-             K, lib.ptr(SG), lib.stream_ptr())
+    W = P[:K].contiguous()
+    dz_ts, W_ts = _ts(lib, dz, R), _ts(lib, W)
+    lib.call("hg_ts_linear_dgrad", lib.ptr(R_dev), R_max, lib.ptr(dz_ts), N, lib.ptr(W_ts), K, lib.ptr(SG),
+             lib.stream_ptr())
+    torch.cuda.synchronize()
     assert rel(SG[:R], dz[:R].double() @ P[:K].double().T) < 2e-5
 
 
