@@ -105,14 +105,16 @@ int hg_tc_linear_wgrad(const int32_t* R_dev, long long R_max, const float* A, lo
                        int N, float* dP, float* partial, int splits, cudaStream_t stream);
 
 /* ---- K7 on tcgen05 over TS operands (bf16 hi/lo core-matrix tiles in HBM, written by
- * hg_aggregate_fwd / hg_gather_dz / hg_ts_pack; layout in csrc/hg_ts.cuh). Operand
- * tiles stream into a 3-stage smem ring with cp.async.bulk; one thread issues
- * tcgen05.mma; fp32 accumulators in TMEM.
+ * hg_aggregate_fwd / hg_gather_dz / hg_ts_pack; layout in csrc/hg_ts.cuh). Each K-chunk
+ * stage is one 4-D TMA box per operand (cp.async.bulk.tensor) into a 4-stage smem ring;
+ * one thread issues tcgen05.mma; fp32 accumulators in TMEM (csrc/hg_tsgemm.cu).
  *   fwd:   h_out[rows[i]] = relu?(A_ts[i,:K1] . PT_ts^T),  PT_ts = TS(P^T)   nn.py:150,156,289
  *   dgrad: SG = dz_ts . W_ts^T,  W_ts = TS(P[:K])                           nn.py:171,175-176
  *   wgrad: dP = A_ts^T . dz_ts over the rows (split-K, fixed-order sum)       nn.py:170,173-174 */
 long long hg_ts_bytes(long long rows, int cols);
-int hg_ts_pack(const float* src, long long ld, int transposed, int rows, int cols, void* dst, cudaStream_t stream);
+/* pack X[rows x cols] (X(r,c) = transposed ? src[c*ld+r] : src[r*ld+c]) into a TS buffer sized for rows_alloc rows */
+int hg_ts_pack(const float* src, long long ld, int transposed, int rows, int cols, long long rows_alloc, void* dst,
+               cudaStream_t stream);
 int hg_ts_linear_fwd(const int32_t* R_dev, long long R_max, const void* A_ts, int K1, const void* PT_ts, int N,
                      const int32_t* rows, int relu, float* h_out, cudaStream_t stream);
 int hg_ts_linear_dgrad(const int32_t* R_dev, long long R_max, const void* dz_ts, int N, const void* W_ts, int K,

@@ -58,7 +58,7 @@ SIGNATURES = {
     "hg_tc_linear_dgrad": (I32, [P, I64, P, I32, P, I32, P, P]),
     "hg_tc_linear_wgrad": (I32, [P, I64, P, I64, I32, P, I32, P, P, I32, P]),
     "hg_ts_bytes": (I64, [I64, I32]),
-    "hg_ts_pack": (I32, [P, I64, I32, I32, I32, P, P]),
+    "hg_ts_pack": (I32, [P, I64, I32, I32, I32, I64, P, P]),
     "hg_ts_linear_fwd": (I32, [P, I64, P, I32, P, I32, P, I32, P, P]),
     "hg_ts_linear_dgrad": (I32, [P, I64, P, I32, P, I32, P, P]),
     "hg_ts_linear_wgrad": (I32, [P, I64, P, I32, P, I32, P, P, I32, P]),

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
                                                    const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
-                                                   int d, uint8_t* __restrict__ A_ts) {
+                                                   int d, uint8_t* __restrict__ A_ts, long long plane) {
   __shared__ __align__(16) float s_rows[8][kMaxRowFloats];
   const int R = *R_dev;
   const int lane = threadIdx.x & 31;
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
     }
     for (int c = K + lane; c < nK * 32; c += 32) srow[c] = c == K ? 1.f : 0.f;
     __syncwarp();
-    for (int g = lane; g < nK * 4; g += 32) ts_store8(A_ts, nK, i, g, srow + g * 8);
+    for (int g = lane; g < nK * 4; g += 32) ts_store8(A_ts, nK * 4, plane, i, g, srow + g * 8);
     __syncwarp();
   }
   // zero the padding rows of the last 128-row tile (the weight-gradient GEMM
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
   const int R_pad = (R + kTsRows - 1) / kTsRows * kTsRows;
   const float zeros[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   for (int i = R + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < R_pad; i += warps)
-    for (int g = lane; g < nK * 4; g += 32) ts_store8(A_ts, nK, i, g, zeros);
+    for (int g = lane; g < nK * 4; g += 32) ts_store8(A_ts, nK * 4, plane, i, g, zeros);
   kt_end(kt);
 }
 
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(1024) k_ce_loss(const double* __restrict__ row
 // warp per row, staged through smem; padding rows of the last tile are zeroed.
 __global__ void __launch_bounds__(256) k_gather_dz(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const float* __restrict__ d_h, const float* __restrict__ h_out,
-                                                   int dout, int relu, uint8_t* __restrict__ dz_ts) {
+                                                   int dout, int relu, uint8_t* __restrict__ dz_ts, long long plane) {
   __shared__ __align__(16) float s_rows[8][kMaxRowFloats];
   const int R = *R_dev;
   const int lane = threadIdx.x & 31;
@@ -225,13 +225,13 @@ __global__ void __launch_bounds__(256) k_gather_dz(const int32_t* R_dev, const i
       srow[j] = g;
     }
     __syncwarp();
-    for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK, i, g, srow + g * 8);
+    for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK * 4, plane, i, g, srow + g * 8);
     __syncwarp();
   }
   const int R_pad = (R + kTsRows - 1) / kTsRows * kTsRows;
   const float zeros[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   for (int i = R + w0; i < R_pad; i += warps)
-    for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK, i, g, zeros);
+    for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK * 4, plane, i, g, zeros);
 }
 
 // CSC keys over the block's original edge extents: surviving edges keep their
@@ -380,10 +380,13 @@ int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int3
   const long long rows_pad = (R_max + kTsRows - 1) / kTsRows * kTsRows;
   const unsigned grid = grid_for(rows_pad * 32, 256, 148 * 16);
   uint8_t* a = static_cast<uint8_t*>(A_ts);
+  const long long plane = ts_plane_bytes(R_max, (kind == kKindSAGE ? 2 * d : d) + 1);
   if (kind == kKindSAGE)
-    k_aggregate<kKindSAGE><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a);
+    k_aggregate<kKindSAGE><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a,
+                                                     plane);
   else
-    k_aggregate<kKindGCN><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a);
+    k_aggregate<kKindGCN><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a,
+                                                    plane);
   HG_LAUNCHED(W);
   return kOk;
 }
@@ -416,8 +419,8 @@ int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, con
                  int dout, int relu, void* dz_ts, cudaStream_t stream) {
   if (dout > kMaxRowFloats) return fail("hg_gather_dz", kBadArg, "row too wide");
   const long long rows_pad = (R_max + kTsRows - 1) / kTsRows * kTsRows;
-  k_gather_dz<<<grid_for(rows_pad * 32, 256, 148 * 16), 256, 0, stream>>>(R_dev, rows, d_h, h_out, dout, relu,
-                                                                         static_cast<uint8_t*>(dz_ts));
+  k_gather_dz<<<grid_for(rows_pad * 32, 256, 148 * 16), 256, 0, stream>>>(
+      R_dev, rows, d_h, h_out, dout, relu, static_cast<uint8_t*>(dz_ts), ts_plane_bytes(R_max, dout));
   HG_LAUNCHED("hg_gather_dz");
   return kOk;
 }

@@ -21,7 +21,6 @@
 #include <cuda_bf16.h>
 
 #include "hg_common.cuh"
-#include "hg_ts.cuh"
 
 namespace hg {
 namespace {
@@ -347,240 +346,6 @@ int launch(const char* W, GemmShape sh, OpA a, OpB b, Epi e, int splits, cudaStr
 }
 
 
-// ======================================================================
-// Bulk-copy pipeline over TS operands (hg_ts.cuh): the operand tiles are
-// already bf16 hi/lo core matrices in HBM, so a producer thread streams them
-// into a kStages-deep shared-memory ring with cp.async.bulk (completion
-// tracked by mbarrier transaction counts), one thread issues the tcgen05.mma
-// instructions as stages land and releases them with tcgen05.commit, and all
-// four warps drain TMEM in the epilogue. kMN = false: D = A . B^T with both
-// operands K-major (forward, dgrad). kMN = true: D = A^T . B over the stored
-// rows (weight gradient): the same stored tiles are read as MN-major operands.
-// ======================================================================
-constexpr int kStages = 3;
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst_smem)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (true) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return;
-    __nanosleep(64);
-  }
-}
-
-__host__ __device__ constexpr uint32_t make_idesc_major(int M, int N, int a_mn, int b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-struct TsShape {
-  int M, N, K;              // M, K may be replaced by device counts
-  const int32_t* M_dev;
-  const int32_t* K_dev;
-  int a_nK, b_nK;           // column chunks of the stored A / B operands
-  int chunks_per_split;
-};
-
-template <bool kMN, typename Epi>
-__global__ void __launch_bounds__(kThreads, 1) k_ts_gemm(TsShape sh, const uint8_t* __restrict__ A,
-                                                         const uint8_t* __restrict__ B, Epi epi, int N_pad,
-                                                         uint32_t tmem_cols) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
-  __shared__ uint32_t tmem_slot;
-  const int M = sh.M_dev ? *sh.M_dev : sh.M;
-  const int K = sh.K_dev ? *sh.K_dev : sh.K;
-  const int m0 = blockIdx.x * kTM;
-  if (m0 >= M) return;
-  const int n0 = blockIdx.y * N_pad;
-  const int n_valid = min(N_pad, sh.N - n0);
-  const int chunks = (K + kBK - 1) / kBK;
-  const int c_begin = blockIdx.z * sh.chunks_per_split;
-  const int c_end = min(chunks, c_begin + sh.chunks_per_split);
-  const int nc = c_end > c_begin ? c_end - c_begin : 0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // stage layout: [A hi 8K][A lo 8K][B hi][B lo]
-  const int n_rt = (N_pad + kTsRows - 1) / kTsRows;          // K-major B: row tiles per stage
-  const int n_ch = (N_pad + kTsCols - 1) / kTsCols;          // MN-major B: column chunks per stage
-  const uint32_t b_half = kMN ? (uint32_t)n_ch * 4 * 512 : (uint32_t)n_rt * kTsHalf;
-  const uint32_t stage_bytes = 2 * kTsHalf + 2 * b_half;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    mbar_init(&done_bar, 1);
-    fence_mbar_init();
-  }
-  if (warp == 0) tmem_alloc(&tmem_slot, tmem_cols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-
-  if (warp == 0 && lane == 0) {
-    // ---------------- producer: bulk copies into the ring ----------------
-    const int m_tile = blockIdx.x;
-    for (int i = 0; i < nc; ++i) {
-      const int st = i % kStages;
-      if (i >= kStages) mbar_wait_sleep(&empty_bar[st], ((i / kStages) - 1) & 1);
-      uint8_t* base = smem + st * stage_bytes;
-      uint8_t* b_base = base + 2 * kTsHalf;
-      const int c = c_begin + i;
-      if (!kMN) {
-        mbar_expect_tx(&full_bar[st], 2 * kTsHalf + 2 * b_half);
-        const uint8_t* a_src = A + ((long long)m_tile * sh.a_nK + c) * kTsBlock;
-        bulk_g2s(base, a_src, kTsBlock, &full_bar[st]);  // hi + lo contiguous
-        for (int t = 0; t < n_rt; ++t) {
-          const uint8_t* b_src = B + ((long long)(n0 / kTsRows + t) * sh.b_nK + c) * kTsBlock;
-          bulk_g2s(b_base + t * kTsHalf, b_src, kTsHalf, &full_bar[st]);
-          bulk_g2s(b_base + b_half + t * kTsHalf, b_src + kTsHalf, kTsHalf, &full_bar[st]);
-        }
-      } else {
-        // k-chunk c = stored rows 32c..32c+31: row tile rt, row groups g0..g0+3
-        const int rt = c >> 2, g0 = (c & 3) * 4;
-        int a_cc = 0;
-        for (int cc = 0; cc < 4; ++cc)
-          if (m_tile * 4 + cc < sh.a_nK) ++a_cc;
-        const int b_cc = min(n_ch, sh.b_nK - n0 / kTsCols);
-        mbar_expect_tx(&full_bar[st], (uint32_t)(a_cc + b_cc) * 4 * 512 * 2);
-        for (int cc = 0; cc < a_cc; ++cc) {
-          const uint8_t* a_src = A + ((long long)rt * sh.a_nK + m_tile * 4 + cc) * kTsBlock + g0 * 512;
-          for (int g = 0; g < 4; ++g) {
-            bulk_g2s(base + g * 2048 + cc * 512, a_src + g * 512, 512, &full_bar[st]);
-            bulk_g2s(base + kTsHalf + g * 2048 + cc * 512, a_src + kTsHalf + g * 512, 512, &full_bar[st]);
-          }
-        }
-        for (int cc = 0; cc < b_cc; ++cc) {
-          const uint8_t* b_src = B + ((long long)rt * sh.b_nK + n0 / kTsCols + cc) * kTsBlock + g0 * 512;
-          for (int g = 0; g < 4; ++g) {
-            bulk_g2s(b_base + g * (n_ch * 512) + cc * 512, b_src + g * 512, 512, &full_bar[st]);
-            bulk_g2s(b_base + b_half + g * (n_ch * 512) + cc * 512, b_src + kTsHalf + g * 512, 512, &full_bar[st]);
-          }
-        }
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer ----------------
-    const uint32_t idesc = make_idesc_major(kTM, N_pad, kMN ? 1 : 0, kMN ? 1 : 0);
-    for (int i = 0; i < nc; ++i) {
-      const int st = i % kStages;
-      mbar_wait_sleep(&full_bar[st], (i / kStages) & 1);
-      tc_fence_after();
-      const uint32_t sa = smem_u32(smem + st * stage_bytes);
-      const uint32_t sb = sa + 2 * kTsHalf;
-#pragma unroll
-      for (int ks = 0; ks < kBK / 16; ++ks) {
-        uint64_t ah, al, bh, bl;
-        if (!kMN) {
-          const uint32_t ko = ks * 256;
-          ah = make_desc(sa + ko, 128, 512);
-          al = make_desc(sa + kTsHalf + ko, 128, 512);
-          bh = make_desc(sb + ko, 128, 512);
-          bl = make_desc(sb + b_half + ko, 128, 512);
-        } else {
-          // MN-major: SBO = 128 B between 8-element MN groups, LBO = K-group stride
-          ah = make_desc(sa + ks * 4096, 2048, 128);
-          al = make_desc(sa + kTsHalf + ks * 4096, 2048, 128);
-          const uint32_t kg = (uint32_t)n_ch * 512;
-          bh = make_desc(sb + ks * 2 * kg, kg, 128);
-          bl = make_desc(sb + b_half + ks * 2 * kg, kg, 128);
-        }
-        const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
-        mma_bf16(tmem, ah, bh, idesc, acc0);
-        mma_bf16(tmem, ah, bl, idesc, 1u);
-        mma_bf16(tmem, al, bh, idesc, 1u);
-      }
-      mma_commit(&empty_bar[st]);
-    }
-    mma_commit(&done_bar);
-  }
-  __syncwarp();
-  // ---------------- epilogue (all warps) ----------------
-  if (nc > 0) mbar_wait_sleep(&done_bar, 0);
-  tc_fence_after();
-  __syncthreads();   // every stage is consumed; the ring can hold the staging tiles
-  float* stage_f = reinterpret_cast<float*>(smem) + warp * 32 * 33;
-  for (int c0 = 0; c0 < n_valid; c0 += 32) {
-    float acc[32];
-    if (nc > 0) {
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, *reinterpret_cast<float(*)[16]>(acc));
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c0 + 16),
-                *reinterpret_cast<float(*)[16]>(acc + 16));
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) stage_f[lane * 33 + j] = acc[j];
-    __syncwarp();
-    const int col = c0 + lane;
-    for (int r = 0; r < 32; ++r) {
-      const int row = m0 + warp * 32 + r;
-      if (row < M && col < n_valid) epi.store(row, n0 + col, stage_f[r * 33 + lane]);
-    }
-    __syncwarp();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, tmem_cols);
-}
-
-// pack X[rows x cols] (element (r, c) = transposed ? src[c*ld + r] : src[r*ld + c])
-// into TS with zero padding up to 128-row / 32-column boundaries
-__global__ void k_ts_pack(const float* __restrict__ src, long long ld, int transposed, int rows, int cols,
-                          int rows_pad, int nK, uint8_t* __restrict__ dst) {
-  const long long groups = (long long)rows_pad * nK * 4;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < groups;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(t / (nK * 4));
-    const int g = (int)(t - (long long)r * nK * 4);
-    float v[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int c = g * 8 + e;
-      v[e] = (r < rows && c < cols) ? (transposed ? src[(long long)c * ld + r] : src[(long long)r * ld + c]) : 0.f;
-    }
-    ts_store8(dst, nK, r, g, v);
-  }
-}
-
-template <bool kMN, typename Epi>
-int ts_launch(const char* W, TsShape sh, const uint8_t* A, const uint8_t* B, Epi e, int splits, cudaStream_t stream) {
-  const int n_tile = sh.N > 256 ? 256 : pad_n(sh.N);
-  const int n_tiles = (sh.N + n_tile - 1) / n_tile;
-  const int n_rt = (n_tile + kTsRows - 1) / kTsRows;
-  const int n_ch = (n_tile + kTsCols - 1) / kTsCols;
-  const size_t b_half = kMN ? (size_t)n_ch * 4 * 512 : (size_t)n_rt * kTsHalf;
-  const size_t smem = (size_t)kStages * (2 * kTsHalf + 2 * b_half);
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    const int max_smem = kStages * (2 * kTsHalf + 2 * 2 * kTsHalf);
-    cudaError_t err = cudaFuncSetAttribute(k_ts_gemm<kMN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (err != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(err));
-    attr_dev = dev;
-  }
-  dim3 grid((unsigned)((sh.M + kTM - 1) / kTM), (unsigned)n_tiles, (unsigned)splits);
-  k_ts_gemm<kMN, Epi><<<grid, kThreads, smem, stream>>>(sh, A, B, e, n_tile, tmem_cols_for(n_tile));
-  HG_LAUNCHED(W);
-  return kOk;
-}
-
 }  // namespace
 }  // namespace hg
 
@@ -622,53 +387,5 @@ int hg_tc_linear_wgrad(const int32_t* R_dev, long long R_max, const float* A, lo
   return kOk;
 }
 
-
-long long hg_ts_bytes(long long rows, int cols) { return ts_bytes(rows, cols); }
-
-int hg_ts_pack(const float* src, long long ld, int transposed, int rows, int cols, void* dst, cudaStream_t stream) {
-  const int rows_pad = (rows + kTsRows - 1) / kTsRows * kTsRows;
-  const int nK = (cols + kTsCols - 1) / kTsCols;
-  k_ts_pack<<<grid_for((long long)(rows_pad > 0 ? rows_pad : 128) * nK * 4, 256), 256, 0, stream>>>(
-      src, ld, transposed, rows, cols, rows_pad > 0 ? rows_pad : 128, nK, static_cast<uint8_t*>(dst));
-  HG_LAUNCHED("hg_ts_pack");
-  return kOk;
-}
-
-// h_out[rows[i]] = relu?( A_ts[i, :K1] . PT_ts[:, :K1]^T ),  PT_ts = TS of P^T (N x K1)
-int hg_ts_linear_fwd(const int32_t* R_dev, long long R_max, const void* A_ts, int K1, const void* PT_ts, int N,
-                     const int32_t* rows, int relu, float* h_out, cudaStream_t stream) {
-  const int nK = (K1 + kTsCols - 1) / kTsCols;
-  TsShape sh{(int)R_max, N, K1, R_dev, nullptr, nK, nK, nK};
-  return ts_launch<false>("hg_ts_linear_fwd", sh, static_cast<const uint8_t*>(A_ts),
-                          static_cast<const uint8_t*>(PT_ts), EpiScatterRelu{rows, h_out, N, relu}, 1, stream);
-}
-
-// SG[R x K] = dz_ts[R x N] . W_ts[K x N]^T
-int hg_ts_linear_dgrad(const int32_t* R_dev, long long R_max, const void* dz_ts, int N, const void* W_ts, int K,
-                       float* SG, cudaStream_t stream) {
-  const int nK = (N + kTsCols - 1) / kTsCols;
-  TsShape sh{(int)R_max, K, N, R_dev, nullptr, nK, nK, nK};
-  return ts_launch<false>("hg_ts_linear_dgrad", sh, static_cast<const uint8_t*>(dz_ts),
-                          static_cast<const uint8_t*>(W_ts), EpiStore{SG, K}, 1, stream);
-}
-
-// dP[K1 x N] = A_ts[:R, :K1]^T . dz_ts[:R, :N]  (split-K over rows, fixed-order sum)
-int hg_ts_linear_wgrad(const int32_t* R_dev, long long R_max, const void* A_ts, int K1, const void* dz_ts, int N,
-                       float* dP, float* partial, int splits, cudaStream_t stream) {
-  if (splits < 1) splits = 1;
-  const int chunks = (int)((R_max + kBK - 1) / kBK);
-  int per = (chunks + splits - 1) / splits;
-  if (per < 1) per = 1;
-  splits = (chunks + per - 1) / per;
-  if (splits < 1) splits = 1;
-  const long long stride = (long long)K1 * N;
-  TsShape sh{K1, N, (int)R_max, nullptr, R_dev, (K1 + kTsCols - 1) / kTsCols, (N + kTsCols - 1) / kTsCols, per};
-  int st = ts_launch<true>("hg_ts_linear_wgrad", sh, static_cast<const uint8_t*>(A_ts),
-                           static_cast<const uint8_t*>(dz_ts), EpiPartial{partial, N, stride}, splits, stream);
-  if (st) return st;
-  k_splitk_sum<<<grid_for(stride, 256), 256, 0, stream>>>(partial, splits, stride, stride, dP);
-  HG_LAUNCHED("hg_ts_linear_wgrad");
-  return kOk;
-}
 
 }  // extern "C"

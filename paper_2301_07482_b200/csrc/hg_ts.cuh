@@ -1,18 +1,21 @@
 // "TS" (tiled split) operand format shared by the producers of GEMM operands
 // (k_aggregate, k_gather_dz, the per-step weight split) and the tcgen05 GEMM.
 //
-// A logical fp32 matrix X[rows x cols] is stored as bf16 hi/lo halves
-// (x = hi + lo, hi = bf16(x), lo = bf16(x - hi)) in blocks of 128 rows x 32
-// columns. Block (rt, kc) lives at byte offset (rt * nK + kc) * 16 KB and
-// holds [hi 8 KB][lo 8 KB]; inside a half, element (r, k) sits in the UMMA
-// canonical no-swizzle core-matrix layout: 8 rows x 16 B core matrices,
-//   byte = (r / 8) * 512 + (k / 8) * 128 + (r % 8) * 16 + (k % 8) * 2.
-// A block half is therefore directly a K-major tcgen05 operand tile
-// (LBO = 128 B between k-cores, SBO = 512 B between 8-row groups), and each
-// core matrix read "sideways" is an MN-major core matrix for the transposed
-// use (the weight-gradient GEMM), so one stored copy serves both.
-// Rows are padded to a multiple of 128 and columns to a multiple of 32 with
-// zeros by the producers.
+// A logical fp32 matrix X[rows x cols] is stored as two bf16 planes, hi and lo
+// (x = hi + lo, hi = bf16(x), lo = bf16(x - hi)), each in "row-group strip"
+// order: rows are grouped by 8 (G = r / 8), columns by 8 (cg = c / 8), and the
+// 8 x 8 bf16 core matrix (8 rows x 16 B) of (G, cg) is 128 contiguous bytes:
+//   byte(r, c) = ((G * nCG + cg) * 8 + r % 8) * 16 + (c % 8) * 2,
+//   lo plane = hi plane + plane_bytes,  plane_bytes = rows_pad * nCG * 16,
+// with rows padded to a multiple of 128 and columns to a multiple of 32 (zeros).
+// Every tcgen05 operand stage is then ONE 4-D TMA box over
+// (core bytes, cg, G, plane), strides increasing:
+//   K-major  stage (128 rows x 32 cols): box (64, 4, 16, 2) -> smem [plane][G][cg][core]
+//            (SBO = 512 B between row groups, LBO = 128 B between k-cores)
+//   MN-major stage (32 rows x M cols):  box (64, M/8, 4, 2) -> smem [plane][G][cg][core]
+//            (SBO = 128 B between MN groups, LBO = M/8 * 128 B between k-groups)
+// so one stored copy serves the forward / data-gradient GEMMs (K-major) and
+// the weight-gradient GEMM (reads the same cores as MN-major operands).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -21,20 +24,24 @@
 
 namespace hg {
 
-constexpr int kTsRows = 128;
-constexpr int kTsCols = 32;
-constexpr int kTsBlock = 16384;      // bytes per (row tile, col chunk): hi + lo
-constexpr int kTsHalf = 8192;
+constexpr int kTsRows = 128;   // row padding granularity
+constexpr int kTsCols = 32;    // column padding granularity (one K chunk)
 
-__host__ __device__ inline long long ts_bytes(long long rows, int cols) {
-  const long long rt = (rows + kTsRows - 1) / kTsRows;
-  const long long nk = (cols + kTsCols - 1) / kTsCols;
-  return (rt < 1 ? 1 : rt) * (nk < 1 ? 1 : nk) * kTsBlock;
+__host__ __device__ inline long long ts_rows_pad(long long rows) {
+  long long p = (rows + kTsRows - 1) / kTsRows * kTsRows;
+  return p < kTsRows ? kTsRows : p;
 }
+__host__ __device__ inline int ts_ncg(int cols) {
+  int nk = (cols + kTsCols - 1) / kTsCols;
+  return (nk < 1 ? 1 : nk) * 4;
+}
+__host__ __device__ inline long long ts_plane_bytes(long long rows, int cols) {
+  return ts_rows_pad(rows) * ts_ncg(cols) * 16;
+}
+__host__ __device__ inline long long ts_bytes(long long rows, int cols) { return 2 * ts_plane_bytes(rows, cols); }
 
-__device__ __forceinline__ long long ts_off(int r, int c, int nK) {
-  const int rt = r >> 7, rr = r & 127, kc = c >> 5, k = c & 31;
-  return (long long)(rt * nK + kc) * kTsBlock + (rr >> 3) * 512 + (k >> 3) * 128 + (rr & 7) * 16 + (k & 7) * 2;
+__device__ __forceinline__ long long ts_off(int r, int c, int nCG) {
+  return ((long long)(r >> 3) * nCG + (c >> 3)) * 128 + (r & 7) * 16 + (c & 7) * 2;
 }
 
 // pack 8 consecutive fp32 values (one core-matrix row) into hi/lo 16-byte words
@@ -53,13 +60,13 @@ __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
-// store the 8-column group g (cols 8g..8g+7) of row r from fp32 values
-__device__ __forceinline__ void ts_store8(uint8_t* ts, int nK, int r, int g, const float* v8) {
+// store column group g (cols 8g..8g+7) of row r
+__device__ __forceinline__ void ts_store8(uint8_t* ts, int nCG, long long plane, int r, int g, const float* v8) {
   uint4 hi, lo;
   split8(v8, hi, lo);
-  const long long off = ts_off(r, g * 8, nK);
+  const long long off = ts_off(r, g * 8, nCG);
   *reinterpret_cast<uint4*>(ts + off) = hi;
-  *reinterpret_cast<uint4*>(ts + off + kTsHalf) = lo;
+  *reinterpret_cast<uint4*>(ts + plane + off) = lo;
 }
 
 }  // namespace hg

@@ -252,7 +252,7 @@ def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch
               _lib.ptr(h_in), d_in, _lib.ptr(A), stream)
     slab = net.slab(l)
     PT = torch.empty(ts_bytes(d_out, K + 1), dtype=torch.uint8, device=dev)   # TS(P^T): B of the forward
-    _lib.call("hg_ts_pack", _lib.ptr(slab), d_out, 1, d_out, K + 1, _lib.ptr(PT), stream)
+    _lib.call("hg_ts_pack", _lib.ptr(slab), d_out, 1, d_out, K + 1, d_out, _lib.ptr(PT), stream)
     n_dst = blk.num_dst
     h_out = torch.empty((n_dst, d_out), dtype=torch.float32, device=dev)
     # z = [A | 1] . P on tcgen05, ReLU + scatter to h_out[rows] in the epilogue
@@ -366,7 +366,7 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
         return None, None
     SG = torch.empty((R, K), dtype=torch.float32, device=dev)
     W = torch.empty(ts_bytes(K, d_out), dtype=torch.uint8, device=dev)        # TS(P[:K]): B of the dgrad
-    _lib.call("hg_ts_pack", _lib.ptr(net.slab(l)), d_out, 0, K, d_out, _lib.ptr(W), stream)
+    _lib.call("hg_ts_pack", _lib.ptr(net.slab(l)), d_out, 0, K, d_out, K, _lib.ptr(W), stream)
     _lib.call("hg_ts_linear_dgrad", _lib.ptr(t.R_dev), R, _lib.ptr(dz), d_out, _lib.ptr(W), K, _lib.ptr(SG), stream)
     if n_dst_dev is None:
         n_dst_dev = _dev_count(blk.num_dst, dev)

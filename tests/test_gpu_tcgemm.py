@@ -87,7 +87,7 @@ def _ts(lib, X, rows=None):
     r, c = X.shape
     rows = r if rows is None else rows
     buf = torch.empty(lib.query("hg_ts_bytes", r, c), dtype=torch.uint8, device="cuda")
-    lib.call("hg_ts_pack", lib.ptr(X), c, 0, rows, c, lib.ptr(buf), lib.stream_ptr())
+    lib.call("hg_ts_pack", lib.ptr(X), c, 0, rows, c, r, lib.ptr(buf), lib.stream_ptr())
     return buf
 
 
@@ -95,7 +95,7 @@ def _ts_T(lib, P):
     """TS of P^T for a row-major P [K1 x N]."""
     K1, N = P.shape
     buf = torch.empty(lib.query("hg_ts_bytes", N, K1), dtype=torch.uint8, device="cuda")
-    lib.call("hg_ts_pack", lib.ptr(P), N, 1, N, K1, lib.ptr(buf), lib.stream_ptr())
+    lib.call("hg_ts_pack", lib.ptr(P), N, 1, N, K1, N, lib.ptr(buf), lib.stream_ptr())
     return buf
 
 
