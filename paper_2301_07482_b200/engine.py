@@ -17,6 +17,8 @@ Sweeps themselves (every t_stale iterations) run on the host between replays.
 
 from __future__ import annotations
 
+import gc
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -58,7 +60,10 @@ class DevBlock:
 
 class StepEngine:
     def __init__(self, trainer, B: int):
-        self.tr = trainer
+        # weak back-reference: no Trainer <-> engine cycle, so a dropped trainer
+        # (and its graph pool) is freed at once, never by a GC pass that could
+        # run (and cudaFree) in the middle of another capture
+        self.tr = weakref.proxy(trainer)
         self.B = int(B)
         cfg = trainer.cfg
         g = trainer.graph
@@ -225,6 +230,7 @@ class StepEngine:
         return self.launch()
 
     def _capture(self):
+        gc.collect()
         torch.cuda.synchronize(self.dev)
         # a fresh private memory pool per capture: the previous graph (and its
         # pool) is released once the new one replaces it
