@@ -49,11 +49,12 @@ __global__ void __launch_bounds__(256) k_load_rows(const int32_t* n_live_dev, co
   const int warps = (gridDim.x * blockDim.x) >> 5;
   KTimer* kt = g_kt ? g_kt + kTLoadRows : nullptr;
   kt_begin(kt);
-  for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g * kRows < n; g += warps) {
+  // index chain (live -> node id -> region row) of a group, resolved by lanes < kRows
+  auto resolve = [&](int g, int& loc, const TIn*& row, bool& hit) {
     const int i = g * kRows + lane;
-    int loc = -1;
-    const TIn* row = nullptr;
-    bool hit = false;
+    loc = -1;
+    row = nullptr;
+    hit = false;
     if (lane < kRows && i < n) {
       loc = live[i];
       const int id = src_nodes[loc];
@@ -61,6 +62,15 @@ __global__ void __launch_bounds__(256) k_load_rows(const int32_t* n_live_dev, co
       hit = fr >= 0;
       row = hit ? region + (long long)fr * dim : feats + (long long)id * dim;
     }
+  };
+  int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int loc;
+  const TIn* row;
+  bool hit;
+  resolve(g, loc, row, hit);
+  // software pipeline: the next group's index chain is in flight while this
+  // group's row loads complete
+  for (; g * kRows < n; g += warps) {
     const unsigned hits = __ballot_sync(0xffffffffu, hit);
     const unsigned valid = __ballot_sync(0xffffffffu, loc >= 0);
     uint4 val[kRows][kT];
@@ -73,9 +83,11 @@ __global__ void __launch_bounds__(256) k_load_rows(const int32_t* n_live_dev, co
         if (((valid >> r) & 1u) && v < nvec) val[r][t] = ldg_stream_u4(reinterpret_cast<const uint4*>(p) + v);
       }
     }
+    int cur_loc = loc;
+    resolve(g + warps, loc, row, hit);
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {
-      const int lr = __shfl_sync(0xffffffffu, loc, r);
+      const int lr = __shfl_sync(0xffffffffu, cur_loc, r);
       if (!((valid >> r) & 1u)) continue;
       float* dst = out + (long long)lr * dim;
 #pragma unroll
