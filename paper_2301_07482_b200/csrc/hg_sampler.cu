@@ -153,6 +153,17 @@ __device__ __forceinline__ void bitonic_sort32_u64(unsigned long long& k) {
     }
   }
 }
+// ascending bitonic sort of the first `span` lanes (span = 2..32, power of 2);
+// every group of `span` lanes is sorted independently
+__device__ __forceinline__ void bitonic_sort_u64(unsigned long long& k, int span) {
+  const int lane = threadIdx.x & 31;
+  for (int size = 2; size <= span; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const bool ascending = (lane & size) == 0 || size == span;
+      cmpx64(k, stride, ((lane & stride) == 0) == ascending);
+    }
+  }
+}
 __device__ __forceinline__ void bitonic_merge32_u64(unsigned long long& k) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -218,16 +229,27 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
         unsigned long long key = valid ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
         if (c + 32 < deg) s = fma128(a32, s, c32);
         if (c == 0) {
-          bitonic_sort32_u64(key);
+          // sorting network sized to the row (lanes >= deg hold ~0 and stay last)
+          const int span = deg >= 32 ? 32 : (deg > 16 ? 32 : (deg > 8 ? 16 : (deg > 4 ? 8 : (deg > 2 ? 4 : 2))));
+          bitonic_sort_u64(key, span);
           best = key;
           continue;
         }
-        const unsigned long long thr = __shfl_sync(0xffffffffu, best, fanout - 1);
-        if (!__ballot_sync(0xffffffffu, key < thr)) continue;
-        bitonic_sort32_u64(key);
-        const unsigned long long r = __shfl_sync(0xffffffffu, key, 31 - lane);
-        if (r < best) best = r;
-        bitonic_merge32_u64(best);
+        // later chunks: insert only the candidates that beat the current
+        // fanout-th key, one at a time (rank by ballot, shift by shfl_up)
+        unsigned long long thr = __shfl_sync(0xffffffffu, best, fanout - 1);
+        unsigned m = __ballot_sync(0xffffffffu, key < thr);
+        while (m) {
+          const int l = __ffs(m) - 1;
+          const unsigned long long cand = __shfl_sync(0xffffffffu, key, l);
+          const int pos = __popc(__ballot_sync(0xffffffffu, best < cand));
+          const unsigned long long up = __shfl_up_sync(0xffffffffu, best, 1);
+          if (lane == pos) best = cand;
+          else if (lane > pos) best = up;
+          thr = __shfl_sync(0xffffffffu, best, fanout - 1);
+          m &= ~(1u << l);
+          m &= __ballot_sync(0xffffffffu, key < thr);
+        }
       }
       if (lane < count) {
         const int u = g_col[lo + (long long)(best & 2047ull)];
