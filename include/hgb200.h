@@ -154,7 +154,10 @@ int hg_sgd(float* params, const float* grads, long long n, float eta, cudaStream
 /* ---- K10 cache update: histgnn/cache.py:188-204 (_LayerCache.update) via
  * cache.py:289-322 (HistCache.update_cache), with _write/_release/
  * _count_overwrites cache.py:131-186. Two stages so the host can size the
- * ring table on first use (cache.py:79-91) after reading n_write. */
+ * ring table on first use (cache.py:79-91) after reading n_write. In
+ * hg_cache_write, `cap` is the number of ALLOCATED table rows (grid bound);
+ * the logical ring capacity is read from layer_ctr[9] on the device, so the
+ * doublings of cache.py:93-101 need no reallocation while it fits. */
 long long hg_cache_update_scratch_bytes(long long n_max);
 int hg_cache_rank(const int32_t* n_dev, int n_max, double p_grad, const int32_t* live, const int32_t* src_nodes,
                   const double* norms, const uint8_t* computed_flag, int32_t* row_of, int32_t* row_owner,

@@ -67,6 +67,7 @@ class _LayerCache:
         self.device = device
         self.min_capacity = min_capacity
         self.capacity = 0
+        self.rows_alloc = 0
         self.table = None
         self.row_owner_dev = None
         self.row_of_dev = torch.full((num_nodes,), -1, dtype=torch.int32, device=device)
@@ -84,7 +85,13 @@ class _LayerCache:
 
     @property
     def row_owner(self):
-        return None if self.row_owner_dev is None else _np(self.row_owner_dev).astype(np.int64)
+        return (None if self.row_owner_dev is None
+                else _np(self.row_owner_dev[: self.capacity]).astype(np.int64))
+
+    @property
+    def table_view(self):
+        """The logical ring rows [capacity x dim] (the allocation may be larger)."""
+        return None if self.table is None else self.table[: self.capacity]
 
     @property
     def header(self):
@@ -119,10 +126,24 @@ class _LayerCache:
             cap = int(np.clip(cap, self.min_capacity, max(self.num_nodes, 1)))
         return max(1, cap)
 
+    HEADROOM_BYTES = 8 << 30   # ring preallocation budget per layer (growth without reallocation)
+
+    def _rows_for(self, cap: int) -> int:
+        """Rows actually allocated for a logical capacity: up to 4x headroom
+        (never past N or the byte budget) so the doublings of cache.py:93-101
+        only change the device-resident capacity, not the table pointer (a
+        captured CUDA graph stays valid)."""
+        row_bytes = self.dim * torch.tensor([], dtype=self.dtype).element_size()
+        rows = min(max(self.num_nodes, 1), 4 * cap)
+        if rows * row_bytes > self.HEADROOM_BYTES:
+            rows = max(cap, min(rows, self.HEADROOM_BYTES // max(row_bytes, 1)))
+        return max(rows, cap)
+
     def allocate(self, first_admits: int):
         self.capacity = self.first_capacity(first_admits)
-        self.table = torch.zeros((self.capacity, self.dim), dtype=self.dtype, device=self.device)
-        self.row_owner_dev = torch.full((self.capacity,), -1, dtype=torch.int32, device=self.device)
+        self.rows_alloc = self._rows_for(self.capacity)
+        self.table = torch.zeros((self.rows_alloc, self.dim), dtype=self.dtype, device=self.device)
+        self.row_owner_dev = torch.full((self.rows_alloc,), -1, dtype=torch.int32, device=self.device)
         self.ctr[CTR_CAPACITY] = self.capacity
 
     def _grow(self):
@@ -130,11 +151,14 @@ class _LayerCache:
         if self.table is None or self.capacity >= self.num_nodes:
             return
         new_cap = min(self.capacity * 2, max(self.num_nodes, 1))
-        table = torch.zeros((new_cap, self.dim), dtype=self.dtype, device=self.device)
-        table[: self.capacity] = self.table
-        owner = torch.full((new_cap,), -1, dtype=torch.int32, device=self.device)
-        owner[: self.capacity] = self.row_owner_dev
-        self.table, self.row_owner_dev, self.capacity = table, owner, new_cap
+        if new_cap > self.rows_alloc:   # out of headroom: reallocate (a captured graph is re-captured)
+            rows = self._rows_for(new_cap)
+            table = torch.zeros((rows, self.dim), dtype=self.dtype, device=self.device)
+            table[: self.capacity] = self.table[: self.capacity]
+            owner = torch.full((rows,), -1, dtype=torch.int32, device=self.device)
+            owner[: self.capacity] = self.row_owner_dev[: self.capacity]
+            self.table, self.row_owner_dev, self.rows_alloc = table, owner, rows
+        self.capacity = new_cap
         self.ctr[CTR_CAPACITY] = new_cap
 
     def sweep(self):
@@ -184,7 +208,7 @@ class _LayerCache:
                 return
             self.allocate(n_write)
         row_words = self.dim * (self.table.element_size() // 4)   # rows are copied as 4-byte words
-        _lib.call("hg_cache_write", n_max, self.capacity, row_words, _lib.ptr(it_dev), self._t_stale(),
+        _lib.call("hg_cache_write", n_max, self.rows_alloc, row_words, _lib.ptr(it_dev), self._t_stale(),
                   int(bool(refresh_retained)), _lib.ptr(live), _lib.ptr(emb), _lib.ptr(self.table),
                   _lib.ptr(self.row_of_dev), _lib.ptr(self.row_owner_dev), _lib.ptr(self.admit_iter_dev),
                   _lib.ptr(self.ctr), _lib.ptr(scratch), sb, stream)

@@ -86,6 +86,7 @@ struct StoreNWrite {
 
 __global__ void k_release_writes(const int32_t* __restrict__ wlist, const NormKey* __restrict__ skeys, int cap,
                                  int32_t* __restrict__ row_of, int32_t* __restrict__ row_owner, long long* ctr) {
+  cap = (int)ctr[kCtrCapacity];  // logical ring size lives on the device (grows at sweeps)
   const long long nw = ctr[kCtrNWrite];
   const long long w0 = nw >= cap ? nw - cap : 0;
   const long long neff = nw - w0;
@@ -102,6 +103,7 @@ __global__ void k_release_writes(const int32_t* __restrict__ wlist, const NormKe
 
 __global__ void k_ring_scan(int cap, const int32_t* it_dev, double t_stale, int t_inf, int32_t* __restrict__ row_of,
                             int32_t* __restrict__ row_owner, const int32_t* __restrict__ admit_iter, long long* ctr) {
+  cap = (int)ctr[kCtrCapacity];  // logical ring size lives on the device (grows at sweeps)
   const int it = *it_dev;
   const long long nw = ctr[kCtrNWrite];
   const long long header = ctr[kCtrHeader];
@@ -133,6 +135,7 @@ __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* _
                              float* __restrict__ table,
                              int32_t* __restrict__ row_of, int32_t* __restrict__ row_owner,
                              int32_t* __restrict__ admit_iter, long long* ctr) {
+  cap = (int)ctr[kCtrCapacity];  // logical ring size lives on the device (grows at sweeps)
   const long long nw = ctr[kCtrNWrite];
   const long long header = ctr[kCtrHeader];
   const bool wrap_all = nw >= cap;
@@ -163,6 +166,7 @@ __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* _
 }
 
 __global__ void k_commit(int cap, long long* ctr) {
+  cap = (int)ctr[kCtrCapacity];  // logical ring size lives on the device (grows at sweeps)
   const long long nw = ctr[kCtrNWrite];
   const bool wrap_all = nw >= cap;
   const long long neff = wrap_all ? cap : nw;

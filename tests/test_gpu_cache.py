@@ -38,7 +38,7 @@ def test_cache_sequences_match_reference(ci):
         np.testing.assert_array_equal(lc.admit_iter, z[pfx + "admit_iter"], err_msg=f"it {it}")
         if lc.row_owner is not None:
             np.testing.assert_array_equal(lc.row_owner, z[pfx + "row_owner"], err_msg=f"it {it}")
-            np.testing.assert_array_equal(lc.table.cpu().numpy(), z[pfx + "table"], err_msg=f"it {it}")
+            np.testing.assert_array_equal(lc.table_view.cpu().numpy(), z[pfx + "table"], err_msg=f"it {it}")
         np.testing.assert_array_equal([lc.header, lc.capacity, lc.window_admissions, lc.window_forced],
                                       z[pfx + "scalars"], err_msg=f"it {it}")
         c = cache.counters()
