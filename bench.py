@@ -218,6 +218,7 @@ def main():
     _lib.call("hg_set_kernel_timers", _lib.ptr(timers))
     clocks.start()
     launches0 = _lib.load().hg_kernel_launches()
+    caps0 = sum(e.captures for e in tr._engines.values())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     losses = []
@@ -232,6 +233,7 @@ def main():
     t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
     value = BATCH * world * args.steps / t_dev
     graph_mode = any(e.graph is not None for e in tr._engines.values())
+    caps_value = sum(e.captures for e in tr._engines.values()) - caps0
 
     # roofline of the feature gather (k_load_rows): algorithmic bytes =
     # live layer-0 rows x (row read + fp32 row write + 3 index reads); the live
@@ -270,12 +272,14 @@ def main():
         d2h += (1 + tr.cache.counters_vector().numel() + tr.cache.num_layers) * 8
     torch.cuda.synchronize()
     t_e2e = max_over_ranks(time.perf_counter() - t0)
+    caps_e2e = sum(e.captures for e in tr._engines.values()) - caps0 - caps_value
     e2e = {"value": BATCH * world * args.steps / t_e2e, "unit": "seeds/s",
            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
            "api": "Trainer.train_step (host seeds in, IterMetrics read back every step)"}
 
     out = dict(base, value=value, ms_per_step=1e3 * t_dev / args.steps, e2e=e2e, roofline=roofline,
                gpu_launches=int(launches), clocks=clk, per_kernel=per_kernel, cuda_graph=graph_mode,
+               graph_captures_in_timed={"value": caps_value, "e2e": caps_e2e},
                loss_last=float(losses[-1].item()), io_saving_last=None)
     out["io_saving_e2e_last"] = 1.0 - m.fetched_bytes / m.baseline_bytes if m.baseline_bytes else None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

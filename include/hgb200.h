@@ -33,6 +33,8 @@ const char* hg_last_error(void);
 int hg_device_sync(void);
 /* number of hand-written hg kernels launched by this process (library GEMMs excluded) */
 long long hg_kernel_launches(void);
+/* add the n hg kernels of a replayed CUDA graph (counted at its capture) */
+void hg_count_graph_replay(long long n);
 /* device-side kernel timers for kernels replayed inside CUDA graphs: buf is
  * u64[8 * 8] (per timer: start=~0, end, total_ns, launches, ...), NULL = off.
  * Timer 0 = k_load_rows, 1 = k_aggregate, 2 = k_transpose_agg, 3 = k_select. */

@@ -129,15 +129,13 @@ class _LayerCache:
     HEADROOM_BYTES = 8 << 30   # ring preallocation budget per layer (growth without reallocation)
 
     def _rows_for(self, cap: int) -> int:
-        """Rows actually allocated for a logical capacity: up to 4x headroom
-        (never past N or the byte budget) so the doublings of cache.py:93-101
-        only change the device-resident capacity, not the table pointer (a
-        captured CUDA graph stays valid)."""
-        row_bytes = self.dim * torch.tensor([], dtype=self.dtype).element_size()
-        rows = min(max(self.num_nodes, 1), 4 * cap)
-        if rows * row_bytes > self.HEADROOM_BYTES:
-            rows = max(cap, min(rows, self.HEADROOM_BYTES // max(row_bytes, 1)))
-        return max(rows, cap)
+        """Rows actually allocated for a logical capacity: as many as the
+        byte budget allows (never past N, never below 4x cap when N allows),
+        so the doublings of cache.py:93-101 only change the device-resident
+        capacity, not the table pointer (a captured CUDA graph stays valid)."""
+        row_bytes = max(self.dim * torch.tensor([], dtype=self.dtype).element_size(), 1)
+        n = max(self.num_nodes, 1)
+        return max(cap, min(n, max(4 * cap, self.HEADROOM_BYTES // row_bytes)))
 
     def allocate(self, first_admits: int):
         self.capacity = self.first_capacity(first_admits)

@@ -43,6 +43,9 @@ int hg_set_kernel_timers(void* buf) {
 // number of hand-written hg kernels launched by this process so far
 long long hg_kernel_launches(void) { return hg::g_launches.load(std::memory_order_relaxed); }
 
+// a CUDA graph replay re-executes the n hg kernels recorded at its capture
+void hg_count_graph_replay(long long n) { hg::g_launches.fetch_add(n, std::memory_order_relaxed); }
+
 const char* hg_last_error(void) { return hg::g_last_error.c_str(); }
 
 int hg_device_sync(void) {

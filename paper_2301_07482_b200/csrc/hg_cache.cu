@@ -273,7 +273,7 @@ int hg_cache_write(int n_max, int cap, int H, const int32_t* it_dev, double t_st
   uint8_t* wflag = reinterpret_cast<uint8_t*>(wlist + nn);
   uint8_t* retained = wflag + nn;
   const int t_inf = isinf(t_stale) ? 1 : 0;
-  const long long nmax = n_max > cap ? n_max : cap;
+  const long long nmax = n_max;  // rows touched per update <= n_write <= n_max (a wrap needs n_write >= capacity)
   k_release_writes<<<grid_for(n_max, 256), 256, 0, stream>>>(wlist, keys_out, cap, row_of, row_owner, layer_ctr);
   HG_LAUNCHED(W);
   k_ring_scan<<<grid_for(nmax, 256), 256, 0, stream>>>(cap, it_dev, t_stale, t_inf, row_of, row_owner, admit_iter,

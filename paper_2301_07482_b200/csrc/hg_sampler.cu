@@ -142,17 +142,6 @@ __device__ __forceinline__ void cmpx64(unsigned long long& k, int partner_mask, 
   const unsigned long long p = __shfl_xor_sync(0xffffffffu, k, partner_mask);
   if (keep_min ? (p < k) : (k < p)) k = p;
 }
-__device__ __forceinline__ void bitonic_sort32_u64(unsigned long long& k) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const bool ascending = (lane & size) == 0 || size == 32;
-      cmpx64(k, stride, ((lane & stride) == 0) == ascending);
-    }
-  }
-}
 // ascending bitonic sort of the first `span` lanes (span = 2..32, power of 2);
 // every group of `span` lanes is sorted independently
 __device__ __forceinline__ void bitonic_sort_u64(unsigned long long& k, int span) {
@@ -163,11 +152,6 @@ __device__ __forceinline__ void bitonic_sort_u64(unsigned long long& k, int span
       cmpx64(k, stride, ((lane & stride) == 0) == ascending);
     }
   }
-}
-__device__ __forceinline__ void bitonic_merge32_u64(unsigned long long& k) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int stride = 16; stride > 0; stride >>= 1) cmpx64(k, stride, (lane & stride) == 0);
 }
 
 // jump with the per-batch constants C = inc * S precomputed (one 128-bit
@@ -187,18 +171,65 @@ __device__ __forceinline__ u128 pcg_jump_c(const JumpTableC& tab, u128 s, unsign
   return s;
 }
 
+// Warp tasks of k_select: contiguous frontier rows grouped by where their
+// candidate stretch STARTS in the layer's PCG64 stream (tasks of C draws), so
+// tasks are balanced by candidates, not rows (low ids = hubs cluster in the
+// sorted-unique frontier). task_row[t] = first row whose stream offset is
+// >= t*C (a lower bound on cand_off), task_row[T] = F; meta = {T, C}.
+constexpr int kMaxTasks = 1 << 18;
+__global__ void k_task_bounds(const int32_t* F_dev, const int64_t* __restrict__ cand_off, int32_t* __restrict__ task_row,
+                              long long* __restrict__ meta) {
+  const int F = *F_dev;
+  const long long total = cand_off[F];
+  long long C = (total + 148 * 32 - 1) / (148 * 32);       // aim for >= 32 tasks per SM
+  C = C < 64 ? 64 : (C > 512 ? 512 : C);
+  const long long cmin = (total + kMaxTasks - 1) / kMaxTasks;
+  if (C < cmin) C = cmin;
+  const long long T = (total + C - 1) / C;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    meta[0] = T;
+    meta[1] = C;
+    task_row[0] = 0;
+    task_row[T] = F;
+  }
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
+    const long long a = cand_off[j], b = cand_off[j + 1];
+    for (long long t = a / C + 1; t * C <= b && t < T; ++t) task_row[t] = j + 1;
+  }
+}
+
+
+// One warp per task of kRowsPerTask consecutive frontier rows. Consecutive
+// rows draw consecutive stretches of the PCG64 stream, so only a task's first
+// row jumps from the batch state (O(log offset) table steps); each later row
+// advances the lane states by the 1..32 draws left over from the previous row
+// with a single precomputed multiply-add (tables D[d] = jump by d).
 template <bool kSmallFanout>
 __global__ void __launch_bounds__(kSelThreads) k_select(
     const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end, const int32_t* __restrict__ g_col,
     const int32_t* __restrict__ frontier, const int32_t* F_dev, int fanout, const SampState* ss,
     const int64_t* __restrict__ cand_off, const int32_t* __restrict__ blk_off, const int64_t* __restrict__ g2l,
-    uint32_t* __restrict__ bitmap, int32_t* __restrict__ src_flat) {
+    uint32_t* __restrict__ bitmap, int32_t* __restrict__ src_flat, const int32_t* __restrict__ task_row,
+    const long long* __restrict__ task_meta) {
   __shared__ JumpTableC tab;
+  __shared__ u128 dA[33], dC[33];
   const u128 s0{ss->st_hi, ss->st_lo}, inc{ss->inc_hi, ss->inc_lo};
   const unsigned epoch = (unsigned)ss->epoch;
   for (int t = threadIdx.x; t < 256; t += blockDim.x) {
     (&tab.A[0][0])[t] = (&g_jump.A[0][0])[t];
     (&tab.C[0][0])[t] = mul128(inc, (&g_jump.S[0][0])[t]);
+  }
+  __syncthreads();
+  if (threadIdx.x <= 32) {
+    // jump by d = 16*h + l: low nibble first, then the high one
+    const int d = threadIdx.x, l = d & 15, h = d >> 4;
+    u128 a = tab.A[0][l], c = tab.C[0][l];
+    if (h) {
+      c = fma128(tab.A[1][h], c, tab.C[1][h]);
+      a = mul128(tab.A[1][h], a);
+    }
+    dA[d] = a;
+    dC[d] = c;
   }
   __syncthreads();
   const int F = *F_dev;
@@ -209,118 +240,147 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
   kt_begin(kt);
   const u128 a32 = tab.A[1][2];            // MULT^32 and its increment term
   const u128 c32 = tab.C[1][2];
-  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < F; row += warps) {
-    const int v = frontier[row];
-    const long long lo = g_start[v];
-    const long long deg = g_end[v] - lo;
-    const int out0 = blk_off[row];
-    const int count = (int)(deg < fanout ? deg : fanout);
-    if (deg == 0) continue;
-    const unsigned long long k0 = base0 + (unsigned long long)cand_off[row];
-    // lane state: output index k0+lane needs k0+lane+1 steps
-    const u128 first = pcg_jump_c(tab, s0, k0 + (unsigned long long)lane + 1ull);
-    if (kSmallFanout && deg <= 2048) {
-      // fast path: (key53, j) packed into one u64, j < 2^11
-      unsigned long long best = ~0ull;
-      u128 s = first;
-      for (long long c = 0; c < deg; c += 32) {
-        const long long jj = c + lane;
-        const bool valid = jj < deg;
-        unsigned long long key = valid ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
-        if (c + 32 < deg) s = fma128(a32, s, c32);
-        if (c == 0) {
-          // sorting network sized to the row (lanes >= deg hold ~0 and stay last)
-          const int span = deg >= 32 ? 32 : (deg > 16 ? 32 : (deg > 8 ? 16 : (deg > 4 ? 8 : (deg > 2 ? 4 : 2))));
-          bitonic_sort_u64(key, span);
-          best = key;
-          continue;
+  const long long ntask = task_meta[0];
+  for (long long task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < ntask; task += warps) {
+    const int r_begin = task_row[task], r_end = task_row[task + 1];
+    bool have = false;                     // cur = lane state at stream index cur_pos + lane
+    u128 cur{0, 0};
+    unsigned long long cur_pos = 0;
+    for (int r0 = r_begin; r0 < r_end; r0 += 32) {
+      const int nr = r_end - r0 < 32 ? r_end - r0 : 32;
+      // the rows' metadata, fetched by lanes < nr at once
+      long long lo_l = 0, deg_l = 0, off_l = 0;
+      int out_l = 0;
+      if (lane < nr) {
+        const int v = frontier[r0 + lane];
+        lo_l = g_start[v];
+        deg_l = g_end[v] - lo_l;
+        off_l = cand_off[r0 + lane];
+        out_l = blk_off[r0 + lane];
+      }
+      for (int q = 0; q < nr; ++q) {
+        const long long lo = __shfl_sync(0xffffffffu, lo_l, q);
+        const long long deg = __shfl_sync(0xffffffffu, deg_l, q);
+        const int out0 = __shfl_sync(0xffffffffu, out_l, q);
+        const int count = (int)(deg < fanout ? deg : fanout);
+        if (deg == 0) continue;
+        const unsigned long long k0 = base0 + (unsigned long long)__shfl_sync(0xffffffffu, off_l, q);
+        // lane state: output index k0+lane needs k0+lane+1 steps
+        u128 first;
+        if (!have) {
+          first = pcg_jump_c(tab, s0, k0 + (unsigned long long)lane + 1ull);
+        } else {
+          const unsigned long long delta = k0 - cur_pos;
+          first = delta <= 32ull ? fma128(dA[delta], cur, dC[delta]) : pcg_jump_c(tab, cur, delta);
         }
-        // later chunks: insert only the candidates that beat the current
-        // fanout-th key, one at a time (rank by ballot, shift by shfl_up)
-        unsigned long long thr = __shfl_sync(0xffffffffu, best, fanout - 1);
-        unsigned m = __ballot_sync(0xffffffffu, key < thr);
-        while (m) {
-          const int l = __ffs(m) - 1;
-          const unsigned long long cand = __shfl_sync(0xffffffffu, key, l);
-          const int pos = __popc(__ballot_sync(0xffffffffu, best < cand));
-          const unsigned long long up = __shfl_up_sync(0xffffffffu, best, 1);
-          if (lane == pos) best = cand;
-          else if (lane > pos) best = up;
-          thr = __shfl_sync(0xffffffffu, best, fanout - 1);
-          m &= ~(1u << l);
-          m &= __ballot_sync(0xffffffffu, key < thr);
-        }
-      }
-      if (lane < count) {
-        const int u = g_col[lo + (long long)(best & 2047ull)];
-        src_flat[out0 + lane] = u;
-        if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
-      }
-    } else if (kSmallFanout) {
-      unsigned long long bk = ~0ull;
-      unsigned bj = ~0u;
-      u128 s = first;
-      for (long long c = 0; c < deg; c += 32) {
-        const long long jj = c + lane;
-        const bool valid = jj < deg;
-        unsigned long long key = valid ? pcg_key53(s) : ~0ull;
-        unsigned j = valid ? (unsigned)jj : ~0u;
-        if (c + 32 < deg) s = fma128(a32, s, c32);
-        const unsigned long long tk = __shfl_sync(0xffffffffu, bk, fanout - 1);
-        const unsigned tj = __shfl_sync(0xffffffffu, bj, fanout - 1);
-        if (!__ballot_sync(0xffffffffu, valid && kj_less(key, j, tk, tj))) continue;
-        bitonic_sort32(key, j);
-        unsigned long long rk = __shfl_sync(0xffffffffu, key, 31 - lane);
-        unsigned rj = __shfl_sync(0xffffffffu, j, 31 - lane);
-        if (kj_less(rk, rj, bk, bj)) {
-          bk = rk;
-          bj = rj;
-        }
-        bitonic_merge32(bk, bj);
-      }
-      if (lane < count) {
-        const int u = g_col[lo + bj];
-        src_flat[out0 + lane] = u;
-        if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
-      }
-    } else {
-      // generic fanout: repeated warp-min selection (O(count * deg / 32))
-      unsigned long long pk = 0;
-      unsigned pj = 0;
-      bool have_prev = false;
-      for (int r = 0; r < count; ++r) {
-        unsigned long long bk = ~0ull;
-        unsigned bj = ~0u;
-        u128 s = first;
-        for (long long c = 0; c < deg; c += 32) {
-          const long long jj = c + lane;
-          if (jj < deg) {
-            unsigned long long key = pcg_key53(s);
-            unsigned j = (unsigned)jj;
-            bool after = !have_prev || kj_less(pk, pj, key, j);
-            if (after && kj_less(key, j, bk, bj)) {
-              bk = key;
-              bj = j;
+        have = false;
+        if (kSmallFanout && deg <= 2048) {
+          // fast path: (key53, j) packed into one u64, j < 2^11
+          unsigned long long best = ~0ull;
+          u128 s = first;
+          for (long long c = 0; c < deg; c += 32) {
+            const long long jj = c + lane;
+            const bool valid = jj < deg;
+            unsigned long long key = valid ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
+            if (c + 32 < deg) s = fma128(a32, s, c32);
+            if (c == 0) {
+              // sorting network sized to the row (lanes >= deg hold ~0 and stay last)
+              const int span = deg >= 32 ? 32 : (deg > 16 ? 32 : (deg > 8 ? 16 : (deg > 4 ? 8 : (deg > 2 ? 4 : 2))));
+              bitonic_sort_u64(key, span);
+              best = key;
+              continue;
+            }
+            // later chunks: insert only the candidates that beat the current
+            // fanout-th key, one at a time (rank by ballot, shift by shfl_up)
+            unsigned long long thr = __shfl_sync(0xffffffffu, best, fanout - 1);
+            unsigned m = __ballot_sync(0xffffffffu, key < thr);
+            while (m) {
+              const int l = __ffs(m) - 1;
+              const unsigned long long cand = __shfl_sync(0xffffffffu, key, l);
+              const int pos = __popc(__ballot_sync(0xffffffffu, best < cand));
+              const unsigned long long up = __shfl_up_sync(0xffffffffu, best, 1);
+              if (lane == pos) best = cand;
+              else if (lane > pos) best = up;
+              thr = __shfl_sync(0xffffffffu, best, fanout - 1);
+              m &= ~(1u << l);
+              m &= __ballot_sync(0xffffffffu, key < thr);
             }
           }
-          if (c + 32 < deg) s = fma128(a32, s, c32);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-          unsigned oj = __shfl_xor_sync(0xffffffffu, bj, o);
-          if (kj_less(ok, oj, bk, bj)) {
-            bk = ok;
-            bj = oj;
+          cur = s;
+          cur_pos = k0 + 32ull * (unsigned long long)((deg - 1) / 32);
+          have = true;
+          if (lane < count) {
+            const int u = g_col[lo + (long long)(best & 2047ull)];
+            src_flat[out0 + lane] = u;
+            if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
           }
-        }
-        pk = bk;
-        pj = bj;
-        have_prev = true;
-        if (lane == 0) {
-          const int u = g_col[lo + pj];
-          src_flat[out0 + r] = u;
-          if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
+        } else if (kSmallFanout) {
+          unsigned long long bk = ~0ull;
+          unsigned bj = ~0u;
+          u128 s = first;
+          for (long long c = 0; c < deg; c += 32) {
+            const long long jj = c + lane;
+            const bool valid = jj < deg;
+            unsigned long long key = valid ? pcg_key53(s) : ~0ull;
+            unsigned j = valid ? (unsigned)jj : ~0u;
+            if (c + 32 < deg) s = fma128(a32, s, c32);
+            const unsigned long long tk = __shfl_sync(0xffffffffu, bk, fanout - 1);
+            const unsigned tj = __shfl_sync(0xffffffffu, bj, fanout - 1);
+            if (!__ballot_sync(0xffffffffu, valid && kj_less(key, j, tk, tj))) continue;
+            bitonic_sort32(key, j);
+            unsigned long long rk = __shfl_sync(0xffffffffu, key, 31 - lane);
+            unsigned rj = __shfl_sync(0xffffffffu, j, 31 - lane);
+            if (kj_less(rk, rj, bk, bj)) {
+              bk = rk;
+              bj = rj;
+            }
+            bitonic_merge32(bk, bj);
+          }
+          if (lane < count) {
+            const int u = g_col[lo + bj];
+            src_flat[out0 + lane] = u;
+            if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
+          }
+        } else {
+          // generic fanout: repeated warp-min selection (O(count * deg / 32))
+          unsigned long long pk = 0;
+          unsigned pj = 0;
+          bool have_prev = false;
+          for (int r = 0; r < count; ++r) {
+            unsigned long long bk = ~0ull;
+            unsigned bj = ~0u;
+            u128 s = first;
+            for (long long c = 0; c < deg; c += 32) {
+              const long long jj = c + lane;
+              if (jj < deg) {
+                unsigned long long key = pcg_key53(s);
+                unsigned j = (unsigned)jj;
+                bool after = !have_prev || kj_less(pk, pj, key, j);
+                if (after && kj_less(key, j, bk, bj)) {
+                  bk = key;
+                  bj = j;
+                }
+              }
+              if (c + 32 < deg) s = fma128(a32, s, c32);
+            }
+    #pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+              unsigned oj = __shfl_xor_sync(0xffffffffu, bj, o);
+              if (kj_less(ok, oj, bk, bj)) {
+                bk = ok;
+                bj = oj;
+              }
+            }
+            pk = bk;
+            pj = bj;
+            have_prev = true;
+            if (lane == 0) {
+              const int u = g_col[lo + pj];
+              src_flat[out0 + r] = u;
+              if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
+            }
+          }
         }
       }
     }
@@ -425,7 +485,8 @@ extern "C" {
 
 long long hg_sample_layer_scratch_bytes(long long F_max, long long num_nodes) {
   long long words = (num_nodes + 31) / 32;
-  return (scan_tiles(F_max) + 1) * (long long)sizeof(I64x2) + (scan_tiles(words) + 1) * 4 + 256;
+  return (scan_tiles(F_max) + 1) * (long long)sizeof(I64x2) + (scan_tiles(words) + 1) * 4 + 256 +
+         (long long)(kMaxTasks + 2) * 4 + 64;
 }
 
 int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t* g_col, long long num_nodes,
@@ -442,6 +503,9 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   const long long words = (num_nodes + 31) / 32;
   I64x2* part_dc = reinterpret_cast<I64x2*>(scratch);
   int* part_w = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + (scan_tiles(F_max) + 1) * sizeof(I64x2));
+  long long* task_meta = reinterpret_cast<long long*>(part_w + scan_tiles(words) + 2);
+  task_meta = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(task_meta) + 15) & ~uintptr_t(15));
+  int32_t* task_row = reinterpret_cast<int32_t*>(task_meta + 2);
 
   SampState* ss = reinterpret_cast<SampState*>(state_dev);
   k_stamp<<<grid_for(F_max, 256), 256, 0, stream>>>(frontier, F_dev, ss, g2l, src_out);
@@ -451,15 +515,18 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
                           EmitDegCount{cand_off, blk_off, blk_end, dst_deg, fanout, g_start, g_end, frontier},
                           TotalDegCount{F_dev, cand_off, blk_off, counts_dev}, stream);
   if (st) return st;
-  const unsigned sel_grid = grid_for(F_max * 32, kSelThreads, 148 * 16);
+  k_task_bounds<<<grid_for(F_max, 256), 256, 0, stream>>>(F_dev, cand_off, task_row, task_meta);
+  HG_LAUNCHED(W);
+  // enough warps for the largest task count the candidate total can produce
+  const unsigned sel_grid = 148 * 16;
   if (fanout <= 32)
     k_select<true><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, g_col, frontier, F_dev, fanout, ss,
-                                                          cand_off, blk_off, g2l, bitmap,
-                                                          src_flat);
+                                                          cand_off, blk_off, g2l, bitmap, src_flat, task_row,
+                                                          task_meta);
   else
     k_select<false><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, g_col, frontier, F_dev, fanout, ss,
-                                                           cand_off, blk_off, g2l, bitmap,
-                                                           src_flat);
+                                                           cand_off, blk_off, g2l, bitmap, src_flat, task_row,
+                                                           task_meta);
   HG_LAUNCHED(W);
   st = scan_launch<int>(W, PopWord{bitmap}, ConstCount{words}, words, part_w,
                         EmitNew{bitmap, F_dev, ss, g2l, src_out},

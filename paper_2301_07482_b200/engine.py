@@ -75,11 +75,16 @@ class StepEngine:
         self.labels = torch.empty(self.B, dtype=torch.int32, device=self.dev)
         self.it = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.F0 = torch.full((1,), self.B, dtype=torch.int32, device=self.dev)
+        # cache updates of layer l run on a side stream, overlapping the
+        # backward of layers < l (they only read the forward tape and norms[l])
+        self.upd_stream = torch.cuda.Stream(self.dev)
         self.graph = None
         self.graph_key = None
         self.pool = None
         self.out = None
         self.capturing = False
+        self.captures = 0         # graph (re-)captures so far
+        self.graph_launches = 0   # hg kernels recorded in the current graph
 
     # ------------------------------------------------------------ inputs
 
@@ -115,6 +120,7 @@ class StepEngine:
             if self.graph is None or self.graph_key != self._key():
                 self._capture()
             self.graph.replay()
+            _lib.load().hg_count_graph_replay(self.graph_launches)
             return self.out
         self.out = self.run()
         return self.out
@@ -192,25 +198,30 @@ class StepEngine:
             h = t.h_out
         d_h, loss = cross_entropy_dev(tapes[-1].h_out, self.labels, B, net.dims[-1], sp)
 
-        # ---- backward (nn.py:300-320) + SGD ----
+        # ---- backward (nn.py:300-320) + SGD, cache updates (cache.py:188-204) ----
+        # layer l's admission/ring update (l >= 1) is forked onto the update
+        # stream as soon as norms[l] exist; different layers' caches share no
+        # state, and the join below orders them before anything that follows
         grads = net.new_grads(zero=False)
         norms = [None] * L
+        side = self.upd_stream
         for l in range(L - 1, -1, -1):
             blk = blocks[l]
             d_prev, nrm = layer_backward_dev(net, l, blk, tapes[l], d_h, grads, l >= 1, keep[l], pos[l], live[l],
                                              blk.num_src, sp, blk.n_dst_dev, n_live_dev(l))
             norms[l] = nrm
             d_h = d_prev
+            if l >= 1:
+                side.wait_stream(stream)
+                with torch.cuda.stream(side):
+                    cache._layer(l).update_dev(n_live_dev(l), blocks[l].num_src, live[l], blocks[l].src_nodes,
+                                               norms[l], keep[l - 1], tapes[l - 1].h_out, self.it,
+                                               cache.refresh_retained, _lib.stream_ptr(side),
+                                               allow_alloc=not self.capturing)
         if tr.grad_hook is not None:
             tr.grad_hook(grads)
         sgd_step(net, grads, cfg.eta)
-
-        # ---- cache admission / ring update (cache.py:188-204) ----
-        for layer in range(1, L):
-            cache._layer(layer).update_dev(n_live_dev(layer), blocks[layer].num_src, live[layer],
-                                           blocks[layer].src_nodes, norms[layer], keep[layer - 1],
-                                           tapes[layer - 1].h_out, self.it, cache.refresh_retained, sp,
-                                           allow_alloc=not self.capturing)
+        stream.wait_stream(side)
         return dict(loss=loss, counts=counts, blocks=blocks, live=live, rows=rows, keep=keep, tapes=tapes,
                     norms=norms, grads=grads, injected=injected)
 
@@ -238,6 +249,7 @@ class StepEngine:
         self.graph = torch.cuda.CUDAGraph()
         self.pool = torch.cuda.graph_pool_handle()
         self.capturing = True
+        n0 = _lib.load().hg_kernel_launches()
         try:
             # capture on a side stream; the staged inputs were copied on the
             # current stream, which the capture stream waits for
@@ -249,4 +261,8 @@ class StepEngine:
             torch.cuda.current_stream(self.dev).wait_stream(side)
         finally:
             self.capturing = False
+        # capture records the launches without executing them
+        self.graph_launches = _lib.load().hg_kernel_launches() - n0
+        _lib.load().hg_count_graph_replay(-self.graph_launches)
+        self.captures += 1
         self.graph_key = self._key()
