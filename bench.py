@@ -183,11 +183,12 @@ def main():
             grads.flat.div_(world)
         tr.grad_hook = allreduce
     batches = hg.make_batches(train, tcfg)
-    need = (args.warmup + 2 * args.steps) * world
+    n_tl = 10   # extra steps after the timed regions for the phase timeline
+    need = (args.warmup + 2 * args.steps + n_tl) * world
     if need > len(batches):
         raise SystemExit(f"need {need} batches, epoch has {len(batches)}")
     # rank r takes batch indices world*s + r (iteration number = global batch index)
-    mine = [world * s + rank for s in range(args.warmup + 2 * args.steps)]
+    mine = [world * s + rank for s in range(args.warmup + 2 * args.steps + n_tl)]
     # inputs of the device-resident steps packed into HBM before timing
     staged = tr.prestage(mine[: args.warmup + args.steps], [batches[i] for i in mine[: args.warmup + args.steps]])
 
@@ -277,9 +278,22 @@ def main():
            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
            "api": "Trainer.train_step (host seeds in, IterMetrics read back every step)"}
 
+    # ---- phase timeline of the replayed step (after timing; %globaltimer marks) ----
+    eng = tr._engine(BATCH)
+    eng.enable_timeline(True)
+    tl_steps = tr.prestage(mine[-n_tl:], [batches[i] for i in mine[-n_tl:]])
+    acc = {}
+    for st in tl_steps:
+        tr.train_step_resident(st)
+        for k, v in eng.timeline_ms().items():
+            acc[k] = acc.get(k, 0.0) + v / n_tl
+    eng.enable_timeline(False)
+    timeline = {k: round(v, 4) for k, v in acc.items()}
+
     out = dict(base, value=value, ms_per_step=1e3 * t_dev / args.steps, e2e=e2e, roofline=roofline,
                gpu_launches=int(launches), clocks=clk, per_kernel=per_kernel, cuda_graph=graph_mode,
                graph_captures_in_timed={"value": caps_value, "e2e": caps_e2e},
+               timeline_ms=timeline,
                loss_last=float(losses[-1].item()), io_saving_last=None)
     out["io_saving_e2e_last"] = 1.0 - m.fetched_bytes / m.baseline_bytes if m.baseline_bytes else None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -33,6 +33,8 @@ const char* hg_last_error(void);
 int hg_device_sync(void);
 /* number of hand-written hg kernels launched by this process (library GEMMs excluded) */
 long long hg_kernel_launches(void);
+/* step timeline probe: one-thread kernel writing %globaltimer (ns) to *slot */
+int hg_mark_time(unsigned long long* slot, cudaStream_t stream);
 /* add the n hg kernels of a replayed CUDA graph (counted at its capture) */
 void hg_count_graph_replay(long long n);
 /* device-side kernel timers for kernels replayed inside CUDA graphs: buf is

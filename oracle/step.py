@@ -23,7 +23,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from .histcache import OCachePolicy, OHistCache
-from .sampling import OSubgraph, _segment_positions, batch_rng, sample_layered, split_batches
+from .sampling import OBlock, OSubgraph, _segment_positions, batch_rng, sample_layered, split_batches
 
 GCN, SAGE = "gcn", "sage_mean"
 NET_TAG, PERM_TAG = 16807, 1000000007
@@ -459,3 +459,26 @@ def run_plain_loop(graph, features, labels, train_ids, cfg: OTrainConfig, num_cl
         if on_step is not None:
             on_step(idx, net)
     return net, losses
+
+
+def full_graph_blocks(start, end, col, num_nodes, num_layers):
+    """trainer.py:473-482 — whole-graph blocks; block 0's sources carry no
+    in-edges (src_deg = 0), deeper blocks use the in-degree."""
+    ids = np.arange(num_nodes, dtype=np.int64)
+    deg = (np.asarray(end, np.int64) - np.asarray(start, np.int64))
+    zero = np.zeros_like(deg)
+    return [OBlock(ids, ids, np.asarray(start, np.int64), np.asarray(end, np.int64), np.asarray(col, np.int64), deg,
+                   zero if b == 0 else deg) for b in range(num_layers)]
+
+
+def evaluate(net: ONetwork, start, end, col, num_nodes, features, labels, ids):
+    """trainer.py:485-506 — exact full-graph accuracy on `ids`; also returns
+    the logits so tests can separate argmax near-ties."""
+    h = np.asarray(features).astype(net.layers[0].weight.dtype)
+    blocks = full_graph_blocks(start, end, col, num_nodes, net.num_layers)
+    for l, blk in enumerate(blocks):
+        h, _ = layer_forward_ctx(net.kind, net.layers[l], blk, h, np.arange(num_nodes, dtype=np.int64),
+                                 l < net.num_layers - 1)
+    ids = np.asarray(ids, np.int64)
+    pred = h[ids].argmax(axis=1)
+    return float((pred == np.asarray(labels)[ids]).mean()), h

@@ -14,5 +14,6 @@ from .graphs import CooGraph, Csr2Graph, build_csr2, csr2_from_arrays  # noqa: F
 from .nn import LayerKind, backward, cross_entropy, forward_pass, init_network, node_grad_norms, sgd_step  # noqa: F401
 from .sampler import (LayerBlock, LayeredSubgraph, SamplePlan, SubgraphProducer, batch_rng,  # noqa: F401
                       sample_layered, split_batches)
-from .trainer import (IterMetrics, PrunedBatch, TrainConfig, Trainer, io_saving, make_batches,  # noqa: F401
+from .trainer import (IterMetrics, PrunedBatch, TrainConfig, Trainer, evaluate, full_graph_logits, io_saving,  # noqa: F401
+                      make_batches,  # noqa: F401
                       prune_with_cache, run_plain_loop, write_metrics_csv)

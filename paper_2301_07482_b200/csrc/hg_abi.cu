@@ -19,6 +19,12 @@ int fail(const char* where, int code, const std::string& msg) {
 
 static std::atomic<long long> g_launches{0};
 
+__global__ void k_mark_time(unsigned long long* slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+
 int check_launch(const char* where) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
@@ -42,6 +48,12 @@ int hg_set_kernel_timers(void* buf) {
 
 // number of hand-written hg kernels launched by this process so far
 long long hg_kernel_launches(void) { return hg::g_launches.load(std::memory_order_relaxed); }
+
+// step timeline probe: *slot = %globaltimer when the stream reaches this point
+int hg_mark_time(unsigned long long* slot, cudaStream_t stream) {
+  hg::k_mark_time<<<1, 1, 0, stream>>>(slot);
+  return hg::check_launch("hg_mark_time");
+}
 
 // a CUDA graph replay re-executes the n hg kernels recorded at its capture
 void hg_count_graph_replay(long long n) { hg::g_launches.fetch_add(n, std::memory_order_relaxed); }

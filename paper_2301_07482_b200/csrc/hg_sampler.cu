@@ -4,11 +4,15 @@
 // Per layer (frontier F rows, device-side counts):
 //   k_stamp     g2l[frontier[i]] = epoch<<32 | i ; src_out[i] = frontier[i]
 //   scan        (deg, min(deg,fanout)) -> cand_off (PCG stream offsets), blk_off
-//   k_select    one warp per frontier row: jump the PCG64 stream to the row's
-//               first candidate, draw one 53-bit key per candidate in-edge,
-//               keep the `fanout` smallest (key, position) pairs with a
-//               ballot-filtered warp bitonic merge, emit the global sources in
-//               key order and mark non-frontier sources in a node bitmap
+//   k_task_bounds  split the layer's stream into warp tasks of ~C draws
+//               (contiguous rows, balanced by candidates)
+//   k_select    one warp per task: jump the PCG64 stream to the task's first
+//               candidate (later rows: one multiply-add), draw one 53-bit key
+//               per candidate in-edge, keep the `fanout` smallest (key,
+//               position) pairs (warp bitonic network + ballot insertion) and
+//               record the picked edge indices in key order
+//   k_pick      picked edge -> global source id; non-frontier sources are
+//               marked in a node bitmap
 //   bitmap scan sorted-unique "new" nodes fall out of the bitmap in id order:
 //               popcount scan -> src_out[F + rank], g2l[new] = epoch<<32 | F+rank,
 //               the bitmap is cleared as it is consumed
@@ -142,16 +146,27 @@ __device__ __forceinline__ void cmpx64(unsigned long long& k, int partner_mask, 
   const unsigned long long p = __shfl_xor_sync(0xffffffffu, k, partner_mask);
   if (keep_min ? (p < k) : (k < p)) k = p;
 }
-// ascending bitonic sort of the first `span` lanes (span = 2..32, power of 2);
-// every group of `span` lanes is sorted independently
-__device__ __forceinline__ void bitonic_sort_u64(unsigned long long& k, int span) {
+// ascending bitonic sort of every group of kSpan lanes (kSpan = 2..32),
+// fully unrolled: the compare directions are compile-time lane-bit tests
+template <int kSpan>
+__device__ __forceinline__ void bitonic_sort_u64(unsigned long long& k) {
   const int lane = threadIdx.x & 31;
-  for (int size = 2; size <= span; size <<= 1) {
+#pragma unroll
+  for (int size = 2; size <= kSpan; size <<= 1) {
+#pragma unroll
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const bool ascending = (lane & size) == 0 || size == span;
+      const bool ascending = size == kSpan || (lane & size) == 0;
       cmpx64(k, stride, ((lane & stride) == 0) == ascending);
     }
   }
+}
+// sorting network sized to a row of deg candidates (lanes >= deg hold ~0 and stay last)
+__device__ __forceinline__ void sort_first_chunk(unsigned long long& k, long long deg) {
+  if (deg > 16) bitonic_sort_u64<32>(k);
+  else if (deg > 8) bitonic_sort_u64<16>(k);
+  else if (deg > 4) bitonic_sort_u64<8>(k);
+  else if (deg > 2) bitonic_sort_u64<4>(k);
+  else bitonic_sort_u64<2>(k);
 }
 
 // jump with the per-batch constants C = inc * S precomputed (one 128-bit
@@ -204,17 +219,37 @@ __global__ void k_task_bounds(const int32_t* F_dev, const int64_t* __restrict__ 
 // row jumps from the batch state (O(log offset) table steps); each later row
 // advances the lane states by the 1..32 draws left over from the previous row
 // with a single precomputed multiply-add (tables D[d] = jump by d).
+// k_select records each pick as its global edge index, split into the low
+// (src_flat) and high (col_local) 32-bit words; k_pick resolves the column
+// (a random read of the full graph's col) and marks non-frontier sources with
+// full memory-level parallelism, off k_select's per-row critical path.
+__device__ __forceinline__ void put_pick(int32_t* src_flat, int32_t* col_local, int e, long long pos) {
+  src_flat[e] = (int32_t)(unsigned)(pos & 0xffffffffll);
+  col_local[e] = (int32_t)(unsigned)((unsigned long long)pos >> 32);
+}
+
+__global__ void k_pick(const int32_t* __restrict__ g_col, const int32_t* counts_dev, const SampState* ss,
+                       const int64_t* __restrict__ g2l, uint32_t* __restrict__ bitmap, int32_t* __restrict__ src_flat,
+                       const int32_t* __restrict__ col_local) {
+  const int E = counts_dev[0];
+  const unsigned epoch = (unsigned)ss->epoch;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const long long pos = (long long)(((unsigned long long)(unsigned)col_local[e] << 32) | (unsigned)src_flat[e]);
+    const int u = g_col[pos];
+    src_flat[e] = u;
+    if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
+  }
+}
+
 template <bool kSmallFanout>
-__global__ void __launch_bounds__(kSelThreads) k_select(
-    const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end, const int32_t* __restrict__ g_col,
+__global__ void __launch_bounds__(kSelThreads, 4) k_select(
+    const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end,
     const int32_t* __restrict__ frontier, const int32_t* F_dev, int fanout, const SampState* ss,
-    const int64_t* __restrict__ cand_off, const int32_t* __restrict__ blk_off, const int64_t* __restrict__ g2l,
-    uint32_t* __restrict__ bitmap, int32_t* __restrict__ src_flat, const int32_t* __restrict__ task_row,
-    const long long* __restrict__ task_meta) {
+    const int64_t* __restrict__ cand_off, const int32_t* __restrict__ blk_off, int32_t* __restrict__ src_flat,
+    int32_t* __restrict__ col_local, const int32_t* __restrict__ task_row, const long long* __restrict__ task_meta) {
   __shared__ JumpTableC tab;
   __shared__ u128 dA[33], dC[33];
   const u128 s0{ss->st_hi, ss->st_lo}, inc{ss->inc_hi, ss->inc_lo};
-  const unsigned epoch = (unsigned)ss->epoch;
   for (int t = threadIdx.x; t < 256; t += blockDim.x) {
     (&tab.A[0][0])[t] = (&g_jump.A[0][0])[t];
     (&tab.C[0][0])[t] = mul128(inc, (&g_jump.S[0][0])[t]);
@@ -284,9 +319,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
             unsigned long long key = valid ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
             if (c + 32 < deg) s = fma128(a32, s, c32);
             if (c == 0) {
-              // sorting network sized to the row (lanes >= deg hold ~0 and stay last)
-              const int span = deg >= 32 ? 32 : (deg > 16 ? 32 : (deg > 8 ? 16 : (deg > 4 ? 8 : (deg > 2 ? 4 : 2))));
-              bitonic_sort_u64(key, span);
+              sort_first_chunk(key, deg);
               best = key;
               continue;
             }
@@ -309,11 +342,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
           cur = s;
           cur_pos = k0 + 32ull * (unsigned long long)((deg - 1) / 32);
           have = true;
-          if (lane < count) {
-            const int u = g_col[lo + (long long)(best & 2047ull)];
-            src_flat[out0 + lane] = u;
-            if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
-          }
+          if (lane < count) put_pick(src_flat, col_local, out0 + lane, lo + (long long)(best & 2047ull));
         } else if (kSmallFanout) {
           unsigned long long bk = ~0ull;
           unsigned bj = ~0u;
@@ -336,11 +365,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
             }
             bitonic_merge32(bk, bj);
           }
-          if (lane < count) {
-            const int u = g_col[lo + bj];
-            src_flat[out0 + lane] = u;
-            if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
-          }
+          if (lane < count) put_pick(src_flat, col_local, out0 + lane, lo + bj);
         } else {
           // generic fanout: repeated warp-min selection (O(count * deg / 32))
           unsigned long long pk = 0;
@@ -375,11 +400,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(
             pk = bk;
             pj = bj;
             have_prev = true;
-            if (lane == 0) {
-              const int u = g_col[lo + pj];
-              src_flat[out0 + r] = u;
-              if ((unsigned)(g2l[u] >> 32) != epoch) atomicOr(&bitmap[u >> 5], 1u << (u & 31));
-            }
+            if (lane == 0) put_pick(src_flat, col_local, out0 + r, lo + pj);
           }
         }
       }
@@ -520,13 +541,14 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   // enough warps for the largest task count the candidate total can produce
   const unsigned sel_grid = 148 * 16;
   if (fanout <= 32)
-    k_select<true><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, g_col, frontier, F_dev, fanout, ss,
-                                                          cand_off, blk_off, g2l, bitmap, src_flat, task_row,
-                                                          task_meta);
+    k_select<true><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
+                                                          blk_off, src_flat, col_local, task_row, task_meta);
   else
-    k_select<false><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, g_col, frontier, F_dev, fanout, ss,
-                                                           cand_off, blk_off, g2l, bitmap, src_flat, task_row,
-                                                           task_meta);
+    k_select<false><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
+                                                           blk_off, src_flat, col_local, task_row, task_meta);
+  HG_LAUNCHED(W);
+  k_pick<<<grid_for(F_max * (long long)fanout, 256), 256, 0, stream>>>(g_col, counts_dev, ss, g2l, bitmap, src_flat,
+                                                                       col_local);
   HG_LAUNCHED(W);
   st = scan_launch<int>(W, PopWord{bitmap}, ConstCount{words}, words, part_w,
                         EmitNew{bitmap, F_dev, ss, g2l, src_out},

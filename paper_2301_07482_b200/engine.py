@@ -83,6 +83,8 @@ class StepEngine:
         self.pool = None
         self.out = None
         self.capturing = False
+        self.timeline = None      # optional int64[32] %globaltimer marks per step (enable_timeline)
+        self.timeline_names = []
         self.captures = 0         # graph (re-)captures so far
         self.graph_launches = 0   # hg kernels recorded in the current graph
 
@@ -125,6 +127,29 @@ class StepEngine:
         self.out = self.run()
         return self.out
 
+    def enable_timeline(self, on: bool = True):
+        """Record %globaltimer at phase boundaries of every step (a one-thread
+        kernel per mark, on the stream that reaches the boundary); read with
+        timeline_ms(). Changes the captured graph (re-captured on next launch)."""
+        self.timeline = torch.zeros(32, dtype=torch.int64, device=self.dev) if on else None
+        self.timeline_names = []
+        self.graph = None
+
+    def timeline_ms(self) -> dict:
+        """Phase boundary times of the last step, ms after its first mark."""
+        if self.timeline is None:
+            return {}
+        t = self.timeline.cpu().tolist()
+        return {n: (t[i] - t[0]) / 1e6 for i, n in enumerate(self.timeline_names)}
+
+    def _mark(self, name: str, stream):
+        if self.timeline is None:
+            return
+        if name not in self.timeline_names:
+            self.timeline_names.append(name)
+        i = self.timeline_names.index(name)
+        _lib.call("hg_mark_time", self.timeline.data_ptr() + 8 * i, _lib.stream_ptr(stream))
+
     # -------------------------------------------------------------- step
 
     def run(self) -> dict:
@@ -134,6 +159,7 @@ class StepEngine:
         stream = torch.cuda.current_stream(dev)
         sp = _lib.stream_ptr(stream)
         g = tr.graph
+        self._mark("start", stream)
         raw = sample_blocks_dev(g, self.seeds, self.F0, B, cfg.fanouts, self.ws, stream)
         blocks = []
         for li in range(L - 1, -1, -1):
@@ -144,6 +170,7 @@ class StepEngine:
             blk.src_deg = (torch.zeros(blk.num_src, dtype=torch.int32, device=dev) if b == 0
                            else blocks[b - 1].dst_deg)
 
+        self._mark("sampled", stream)
         # ---- prune walk + lookups (trainer.py:166-207) ----
         counts = torch.empty(2 * L, dtype=torch.int32, device=dev)
         keep, pos, rows, live = [None] * L, [None] * L, [None] * L, [None] * (L + 1)
@@ -180,6 +207,7 @@ class StepEngine:
         def n_live_dev(b):
             return counts[2 * b + 1:2 * b + 2]
 
+        self._mark("pruned", stream)
         # ---- layer-0 input (trainer.py:326-343) ----
         b0 = blocks[0]
         h = torch.empty((b0.num_src, tr.feature_dim), dtype=torch.float32, device=dev)
@@ -188,6 +216,7 @@ class StepEngine:
                   _lib.ptr(cache.feature_row_of_dev), _lib.ptr(region), _lib.ptr(tr.features), tr.feature_dim,
                   tr._dtype_code, _lib.ptr(h), _lib.ptr(cache.gctr), sp)
 
+        self._mark("loaded", stream)
         # ---- forward (nn.py:260-297) ----
         tapes = []
         for b in range(L):
@@ -197,6 +226,7 @@ class StepEngine:
             tapes.append(t)
             h = t.h_out
         d_h, loss = cross_entropy_dev(tapes[-1].h_out, self.labels, B, net.dims[-1], sp)
+        self._mark("forward+loss", stream)
 
         # ---- backward (nn.py:300-320) + SGD, cache updates (cache.py:188-204) ----
         # layer l's admission/ring update (l >= 1) is forked onto the update
@@ -211,6 +241,7 @@ class StepEngine:
                                              blk.num_src, sp, blk.n_dst_dev, n_live_dev(l))
             norms[l] = nrm
             d_h = d_prev
+            self._mark(f"backward{l}", stream)
             if l >= 1:
                 side.wait_stream(stream)
                 with torch.cuda.stream(side):
@@ -218,10 +249,13 @@ class StepEngine:
                                                norms[l], keep[l - 1], tapes[l - 1].h_out, self.it,
                                                cache.refresh_retained, _lib.stream_ptr(side),
                                                allow_alloc=not self.capturing)
+                    self._mark(f"cache_update{l} (side)", side)
         if tr.grad_hook is not None:
             tr.grad_hook(grads)
         sgd_step(net, grads, cfg.eta)
+        self._mark("sgd", stream)
         stream.wait_stream(side)
+        self._mark("joined", stream)
         return dict(loss=loss, counts=counts, blocks=blocks, live=live, rows=rows, keep=keep, tapes=tapes,
                     norms=norms, grads=grads, injected=injected)
 
@@ -229,7 +263,8 @@ class StepEngine:
 
     def _key(self):
         c = self.tr.cache
-        return tuple(None if lc.table is None else lc.table.data_ptr() for lc in c.layers.values())
+        return (tuple(None if lc.table is None else lc.table.data_ptr() for lc in c.layers.values()),
+                None if self.timeline is None else self.timeline.data_ptr())
 
     def _graphable(self) -> bool:
         return (self.tr.use_graphs and self.tr.grad_hook is None

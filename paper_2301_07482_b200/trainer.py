@@ -513,3 +513,77 @@ def run_plain_loop(graph, features, labels, train_ids, cfg: TrainConfig, num_cla
         if on_step is not None:
             on_step(idx, network)
     return network, losses
+
+
+# -------------------------------------------------------------- inference
+
+
+def evaluate(network: Network, graph, features, labels, ids, chunk_rows: int | None = None) -> float:
+    """Exact full-graph accuracy on `ids` (trainer.py:485-506): argmax of
+    full_graph_logits over the given node ids."""
+    g = _device_graph(graph)
+    N = int(g.num_nodes)
+    ids = np.asarray(ids, dtype=np.int64)
+    labels = np.asarray(labels, dtype=np.int64)
+    if len(ids) and (ids.min() < 0 or ids.max() >= N):
+        raise ValueError("evaluation ids out of range")
+    h = full_graph_logits(network, g, features, chunk_rows)
+    if len(ids) == 0:
+        return float("nan")
+    pred = h[torch.as_tensor(ids, device=h.device)].argmax(dim=1).cpu().numpy()
+    return float((pred == labels[ids]).mean())
+
+
+def full_graph_logits(network: Network, graph, features, chunk_rows: int | None = None) -> torch.Tensor:
+    """Layer-wise inference over whole-graph blocks (trainer.py:473-482: every
+    node is a dst row, block 0's sources carry no in-edges, deeper blocks use
+    the in-degree), ReLU on every layer but the last; returns the device
+    logits [N x C]. Each layer runs the training kernels (hg_aggregate_fwd ->
+    TS operand -> tcgen05 GEMM with the scatter epilogue) over dst-row chunks
+    of `chunk_rows` rows, so the GEMM operand stays bounded (default ~2 GB)
+    while h stays resident in HBM."""
+    _lib.require_cuda()
+    g = _device_graph(graph)
+    dev = g.start.device
+    N = int(g.num_nodes)
+    if int(g.end.max().item() if N else 0) >= 2 ** 31:
+        raise ValueError("evaluate needs fewer than 2^31 edges (int32 block offsets)")
+    feats = features if isinstance(features, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(features))
+    feats = feats.to(dev)
+    if feats.shape[0] != N:
+        raise ValueError("features must have one row per node")
+    sp = _lib.stream_ptr()
+    d0 = int(feats.shape[1])
+    every = torch.arange(N, dtype=torch.int32, device=dev)
+    # layer-0 input as fp32 rows (the training feature gather, all nodes live)
+    h = torch.empty((N, d0), dtype=torch.float32, device=dev)
+    gctr = torch.zeros(8, dtype=torch.int64, device=dev)
+    _lib.call("hg_load_features", _lib.ptr(_dev_count(N, dev)), N, _lib.ptr(every), _lib.ptr(every), None,
+              _lib.ptr(feats), _lib.ptr(feats), d0, _dtype_code(feats), _lib.ptr(h), _lib.ptr(gctr), sp)
+    start = g.start.to(torch.int32)
+    end = g.end.to(torch.int32)
+    deg = (end - start).contiguous()
+    zero = torch.zeros_like(deg)
+    from .nn import _kind_code, ts_bytes
+    kind = _kind_code(network.kind)
+    L = network.num_layers
+    for l in range(L):
+        d_in, d_out = network.dims[l], network.dims[l + 1]
+        K = 2 * d_in if network.kind == LayerKind.SAGE_MEAN else d_in
+        PT = torch.empty(ts_bytes(d_out, K + 1), dtype=torch.uint8, device=dev)
+        _lib.call("hg_ts_pack", _lib.ptr(network.slab(l)), d_out, 1, d_out, K + 1, d_out, _lib.ptr(PT), sp)
+        per_row = max(1, ts_bytes(1024, K + 1) // 1024)
+        chunk = int(chunk_rows) if chunk_rows else max(128, min(N, (2 << 30) // per_row))
+        A = torch.empty(ts_bytes(min(chunk, max(N, 1)), K + 1), dtype=torch.uint8, device=dev)
+        h_out = torch.empty((N, d_out), dtype=torch.float32, device=dev)
+        for r0 in range(0, N, chunk):
+            R = min(chunk, N - r0)
+            R_dev = _dev_count(R, dev)
+            rows = every[r0:r0 + R]
+            _lib.call("hg_aggregate_fwd", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(start), _lib.ptr(end),
+                      _lib.ptr(g.col_indices), _lib.ptr(deg), _lib.ptr(zero if l == 0 else deg), _lib.ptr(h), d_in,
+                      _lib.ptr(A), sp)
+            _lib.call("hg_ts_linear_fwd", _lib.ptr(R_dev), R, _lib.ptr(A), K + 1, _lib.ptr(PT), d_out, _lib.ptr(rows),
+                      int(l < L - 1), _lib.ptr(h_out), sp)
+        h = h_out
+    return h

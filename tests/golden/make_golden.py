@@ -279,6 +279,33 @@ def gen_trainer():
     np.savez_compressed(os.path.join(HERE, "trainer.npz"), **out)
 
 
+def gen_evaluate():
+    """trainer.py:473-506: full-graph inference of a briefly trained network."""
+    from histgnn.nn import layer_forward
+    from histgnn.trainer import evaluate, full_graph_blocks
+    out = dict(META)
+    ds, g = small_powerlaw()
+    for kind in (LayerKind.SAGE_MEAN, LayerKind.GCN):
+        cfg = TrainConfig(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=1, eta=0.05, kind=kind,
+                          p_grad=0.0, t_stale=0, seed=3)
+        net, _ = run_plain_loop(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
+        k = f"{kind.value}_"
+        for l, lp in enumerate(net.layers):
+            out[k + f"W{l}"] = lp.weight
+            out[k + f"b{l}"] = lp.bias
+            if lp.weight_neigh is not None:
+                out[k + f"Wn{l}"] = lp.weight_neigh
+        h = ds.features.astype(net.dtype)
+        for l, blk in enumerate(full_graph_blocks(g, net.num_layers)):
+            h = layer_forward(net.kind, net.layers[l], blk, h, activation=l < net.num_layers - 1)
+        out[k + "logits"] = h
+        out[k + "acc_val"] = np.array(evaluate(net, g, ds.features, ds.labels, ds.val_ids))
+        out[k + "acc_test"] = np.array(evaluate(net, g, ds.features, ds.labels, ds.test_ids))
+    out["val_ids"] = ds.val_ids
+    out["test_ids"] = ds.test_ids
+    np.savez_compressed(os.path.join(HERE, "evaluate.npz"), **out)
+
+
 def gen_datagen():
     out = dict(META)
     ds = synth_power_law(2000, np.random.default_rng(4), m=4, feature_dim=8, classes=5)
@@ -294,7 +321,7 @@ def gen_datagen():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["datagen", "sampler", "cache", "prune_nn", "trainer", "c1"]
+    which = sys.argv[1:] or ["datagen", "sampler", "cache", "prune_nn", "trainer", "c1", "evaluate"]
     for w in which:
         print("generating", w, flush=True)
         globals()["gen_" + w]()
