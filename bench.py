@@ -78,14 +78,31 @@ class ClockSampler:
         except OSError:
             self.p = None
 
+    def _rows(self):
+        self.f.flush()
+        with open(self.f.name) as fh:
+            return [r.split(",") for r in fh.read().strip().splitlines() if r.strip()]
+
+    def wait_running(self, timeout=10.0):
+        """Block until nvidia-smi has produced a sample; rows up to here are
+        pre-timing and are dropped from the summary."""
+        self.skip = 0
+        if self.p is None:
+            return
+        t0 = time.time()
+        while time.time() - t0 < timeout:
+            n = len(self._rows())
+            if n:
+                self.skip = n
+                return
+            time.sleep(0.02)
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
         self.p.wait()
-        self.f.flush()
-        self.f.seek(0)
-        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        rows = self._rows()[getattr(self, "skip", 0):]
         sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].strip().replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if len(r) > 8 and r[2].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -129,7 +146,7 @@ def cpu_reference(cfg, data, steps, warmup, budget_s=150.0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
@@ -174,8 +191,11 @@ def main():
     from paper_2301_07482_b200.data import csr2_from_edges_device
     graph = csr2_from_edges_device(src, dst, cfgd["n"], dev)
     feats_dev = torch.from_numpy(feats).to(dev)
+    n_tl = 10   # extra steps after the timed regions for the phase timeline
+    need = (args.warmup + 2 * args.steps + n_tl + 1) * world
+    per_epoch = -(-len(train) // BATCH)
     tcfg = hg.TrainConfig(fanouts=FANOUTS, hidden=HIDDEN, batch_size=BATCH, eta=ETA, kind=hg.LayerKind.SAGE_MEAN,
-                          p_grad=P_GRAD, t_stale=T_STALE, seed=0)
+                          p_grad=P_GRAD, t_stale=T_STALE, seed=0, epochs=max(1, -(-need // per_epoch)))
     tr = hg.Trainer(graph, feats_dev, labels, train, tcfg, cfgd["classes"])
     if world > 1:
         def allreduce(grads):
@@ -183,14 +203,14 @@ def main():
             grads.flat.div_(world)
         tr.grad_hook = allreduce
     batches = hg.make_batches(train, tcfg)
-    n_tl = 10   # extra steps after the timed regions for the phase timeline
-    need = (args.warmup + 2 * args.steps + n_tl) * world
     if need > len(batches):
         raise SystemExit(f"need {need} batches, epoch has {len(batches)}")
     # rank r takes batch indices world*s + r (iteration number = global batch index)
-    mine = [world * s + rank for s in range(args.warmup + 2 * args.steps + n_tl)]
+    mine = [world * s + rank for s in range(args.warmup + 2 * args.steps + n_tl + 1)]
     # inputs of the device-resident steps packed into HBM before timing
-    staged = tr.prestage(mine[: args.warmup + args.steps], [batches[i] for i in mine[: args.warmup + args.steps]])
+    # (+1: the last timed step also samples a next batch, like every other one)
+    n_res = args.warmup + args.steps + 1
+    staged = tr.prestage(mine[:n_res], [batches[i] for i in mine[:n_res]])
 
     def barrier():
         if world > 1:
@@ -203,8 +223,11 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    def nxt(i):   # the batch announced for pipelined sampling (staged in HBM)
+        return staged[i + 1] if i + 1 < len(staged) else None
+
     for s in range(args.warmup):
-        tr.train_step_resident(staged[s])
+        tr.train_step_resident(staged[s], nxt(s))
     torch.cuda.synchronize()
 
     # ---- timed region 1: device-resident steps (value) ----
@@ -214,17 +237,18 @@ def main():
     timers = torch.zeros(8 * 8, dtype=torch.int64, device=dev)
     timers.view(8, 8)[:, 0] = -1
     g_before = tr.cache.gctr.clone()
+    clocks.start()
+    clocks.wait_running()
     barrier()
     torch.cuda.synchronize()
     _lib.call("hg_set_kernel_timers", _lib.ptr(timers))
-    clocks.start()
     launches0 = _lib.load().hg_kernel_launches()
     caps0 = sum(e.captures for e in tr._engines.values())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     losses = []
     for s in range(args.warmup, args.warmup + args.steps):
-        losses.append(tr.train_step_resident(staged[s]))
+        losses.append(tr.train_step_resident(staged[s], nxt(s)))
     e1.record()
     torch.cuda.synchronize()
     _lib.call("hg_set_kernel_timers", None)
@@ -268,8 +292,11 @@ def main():
     h2d = d2h = 0
     for s in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
         it = mine[s]
-        m = tr.train_step(it, 0, batches[it])
-        h2d += batches[it].size * 4 * 2          # seed ids + labels (int32)
+        nb = (mine[s + 1], batches[mine[s + 1]])
+        m = tr.train_step(it, 0, batches[it], next_batch=nb)
+        # this step uploads the announced next batch's words (PCG64 state,
+        # iteration, seed ids, labels), or its own when none was announced
+        h2d += (12 + 2 * BATCH) * 4
         d2h += (1 + tr.cache.counters_vector().numel() + tr.cache.num_layers) * 8
     torch.cuda.synchronize()
     t_e2e = max_over_ranks(time.perf_counter() - t0)
@@ -281,10 +308,10 @@ def main():
     # ---- phase timeline of the replayed step (after timing; %globaltimer marks) ----
     eng = tr._engine(BATCH)
     eng.enable_timeline(True)
-    tl_steps = tr.prestage(mine[-n_tl:], [batches[i] for i in mine[-n_tl:]])
+    tl_steps = tr.prestage(mine[-(n_tl + 1):], [batches[i] for i in mine[-(n_tl + 1):]])
     acc = {}
-    for st in tl_steps:
-        tr.train_step_resident(st)
+    for i in range(n_tl):   # every step samples the next one (the last staged batch is lookahead only)
+        tr.train_step_resident(tl_steps[i], tl_steps[i + 1])
         for k, v in eng.timeline_ms().items():
             acc[k] = acc.get(k, 0.0) + v / n_tl
     eng.enable_timeline(False)

@@ -15,7 +15,10 @@
 //   U7  header update; U8 optional refresh of retained timestamps
 // Norms are non-negative, so their IEEE bit patterns order like the values.
 #include "hgb200.h"
+#include <cub/device/device_merge_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
+#include <cstdlib>
+#include <cstring>
 
 #include "hg_scan.cuh"
 #include "hg_state.h"
@@ -27,6 +30,22 @@ struct NormKey {
   unsigned long long norm;
   unsigned id;
 };
+
+struct NormKeyLess {
+  __device__ bool operator()(const NormKey& a, const NormKey& b) const {
+    return a.norm < b.norm || (a.norm == b.norm && a.id < b.id);
+  }
+};
+
+// rank sort: "merge" (block sort + merge passes; default) or "radix" (96-bit LSD)
+inline bool use_radix_sort() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("HG_CACHE_SORT");
+    v = (e && std::strcmp(e, "radix") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
 
 struct NormKeyDecomposer {
   __host__ __device__ ::cuda::std::tuple<unsigned long long&, unsigned&> operator()(NormKey& k) const {
@@ -214,9 +233,12 @@ using namespace hg;
 extern "C" {
 
 long long hg_cache_update_scratch_bytes(long long n_max) {
-  size_t tmp = 0;
+  size_t tmp = 0, tmp2 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const NormKey*)nullptr, (NormKey*)nullptr, (const int32_t*)nullptr,
                                   (int32_t*)nullptr, (int)(n_max > 0 ? n_max : 1), NormKeyDecomposer{});
+  cub::DeviceMergeSort::SortPairs(nullptr, tmp2, (NormKey*)nullptr, (int32_t*)nullptr, (int)(n_max > 0 ? n_max : 1),
+                                  NormKeyLess{});
+  if (tmp2 > tmp) tmp = tmp2;
   const long long n = n_max + 16;
   // keys_in, keys_out (16 B), vals_in, vals_out, wlist (4 B), wflag, retained (1 B), scan partials
   return n * 16 * 2 + n * 4 * 3 + n * 2 + (scan_tiles(n_max) + 1) * 4 + (long long)tmp + 2048;
@@ -244,11 +266,16 @@ int hg_cache_rank(const int32_t* n_dev, int n_max, double p_grad, const int32_t*
   int* part = reinterpret_cast<int*>(retained + nn + 16 - ((uintptr_t)(retained + nn) & 15));
   void* tmp = part + scan_tiles(n_max) + 4;
   size_t tmp_bytes = (size_t)(scratch_bytes - ((char*)tmp - p));
-  k_norm_keys<<<grid_for(n_max, 256), 256, 0, stream>>>(n_dev, n_max, p_grad, live, src_nodes, norms, keys_in,
-                                                        vals_in, layer_ctr);
+  const bool radix = use_radix_sort();
+  // the merge sort is in place: keys go straight to keys_out / vals_out
+  k_norm_keys<<<grid_for(n_max, 256), 256, 0, stream>>>(n_dev, n_max, p_grad, live, src_nodes, norms,
+                                                        radix ? keys_in : keys_out, radix ? vals_in : vals_out,
+                                                        layer_ctr);
   HG_LAUNCHED(W);
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, vals_out, n_max,
-                                                  NormKeyDecomposer{}, stream);
+  cudaError_t e = radix ? cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, vals_out, n_max,
+                                                          NormKeyDecomposer{}, stream)
+                        : cub::DeviceMergeSort::SortPairs(tmp, tmp_bytes, keys_out, vals_out, n_max, NormKeyLess{},
+                                                          stream);
   if (e != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(e));
   k_rank_admit<<<grid_for(n_max, 256), 256, 0, stream>>>(n_dev, keys_out, vals_out, live, computed_flag, row_of,
                                                          row_owner, wflag, retained, layer_ctr);

@@ -1,5 +1,6 @@
 """Sync-free, shape-static training step (sample -> prune -> gather -> forward
--> loss -> backward -> SGD -> cache update), replayed as one CUDA graph.
+-> loss -> backward -> SGD -> cache update), replayed as CUDA graphs, with the
+sampler software-pipelined one batch ahead.
 
 This is the B200 runtime behind `Trainer.train` / `Trainer.train_step`: the
 same kernels as the API functions (sampler.py, trainer.prune_with_cache,
@@ -11,8 +12,17 @@ labels, the batch's PCG64 state, the iteration number) that are refreshed
 from pinned host staging before each launch; after the first eager
 iterations (which size the cache rings, cache.py:79-91) the step is captured
 once with torch.cuda.graph and replayed. The graph is re-captured only when a
-cache table is reallocated (first use / doubling at a sweep, cache.py:93-101).
-Sweeps themselves (every t_stale iterations) run on the host between replays.
+cache table is reallocated (growth past the preallocated headroom,
+cache.py:93-101). Sweeps themselves (every t_stale iterations) run on the host
+between replays.
+
+Pipelining: sampling depends only on the graph, the seeds and the batch's
+PCG64 state, never on the weights or the cache, so when the caller names the
+next batch the step also samples it, on a side stream, into the other of two
+preallocated sample slots, concurrently with the training of the current
+batch (two graph variants, one per slot parity). A batch's training reads the
+slot filled by the previous step; a mismatch (no lookahead, or a different
+batch than announced) falls back to sampling it first.
 """
 
 from __future__ import annotations
@@ -26,7 +36,7 @@ import torch
 
 from . import _lib
 from .nn import Injection, cross_entropy_dev, layer_backward_dev, layer_forward_dev, sgd_step
-from .sampler import SamplerWorkspace, layer_bounds, pcg_words, sample_blocks_dev
+from .sampler import SamplerWorkspace, SampleSlot, layer_bounds, pcg_words, sample_blocks_dev
 
 
 @dataclass
@@ -58,10 +68,14 @@ class DevBlock:
         return self.col
 
 
+class _Graph:
+    __slots__ = ("graph", "pool", "out", "key", "launches")
+
+
 class StepEngine:
     def __init__(self, trainer, B: int):
         # weak back-reference: no Trainer <-> engine cycle, so a dropped trainer
-        # (and its graph pool) is freed at once, never by a GC pass that could
+        # (and its graph pools) is freed at once, never by a GC pass that could
         # run (and cudaFree) in the middle of another capture
         self.tr = weakref.proxy(trainer)
         self.B = int(B)
@@ -71,34 +85,35 @@ class StepEngine:
         self.L = len(cfg.fanouts)
         self.F, self.E = layer_bounds(self.B, cfg.fanouts, g.num_nodes)
         self.ws = SamplerWorkspace(g.num_nodes, self.dev)
-        self.seeds = torch.empty(self.B, dtype=torch.int32, device=self.dev)
-        self.labels = torch.empty(self.B, dtype=torch.int32, device=self.dev)
-        self.it = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.seeds = torch.empty(self.B, dtype=torch.int32, device=self.dev)    # sampler input
+        self.labels = torch.empty(self.B, dtype=torch.int32, device=self.dev)   # training input
+        self.it = torch.zeros(1, dtype=torch.int32, device=self.dev)            # training iteration
         self.F0 = torch.full((1,), self.B, dtype=torch.int32, device=self.dev)
-        # cache updates of layer l run on a side stream, overlapping the
+        self.slots = [SampleSlot(g, self.B, cfg.fanouts), SampleSlot(g, self.B, cfg.fanouts)]
+        self.slot_words = [None, None]   # staged input words of the batch each slot holds
+        self.cur = 0                     # slot of the next batch to train
+        # block 0's sources carry no in-edges (src_deg = 0): one persistent zero vector
+        self.zero_deg = torch.zeros(self.slots[0].layers[-1]["Fn_max"], dtype=torch.int32, device=self.dev)
+        self.samp_stream = torch.cuda.Stream(self.dev)
+        # cache updates of layer l run on side stream l, overlapping the
         # backward of layers < l (they only read the forward tape and norms[l])
-        self.upd_stream = torch.cuda.Stream(self.dev)
-        self.graph = None
-        self.graph_key = None
-        self.pool = None
+        self.upd_streams = {l: torch.cuda.Stream(self.dev) for l in range(1, self.L)}
+        self.graphs = {}          # (slot, lookahead) -> _Graph
         self.out = None
         self.capturing = False
         self.timeline = None      # optional int64[32] %globaltimer marks per step (enable_timeline)
         self.timeline_names = []
         self.captures = 0         # graph (re-)captures so far
-        self.graph_launches = 0   # hg kernels recorded in the current graph
+
+    @property
+    def graph(self):
+        """Any captured graph (None before the first capture)."""
+        return next(iter(self.graphs.values())).graph if self.graphs else None
 
     # ------------------------------------------------------------ inputs
 
-    def stage(self, iteration: int, seeds: np.ndarray, labels: np.ndarray, pcg: tuple):
-        """Copy one batch's inputs into the static device tensors (pinned
-        staging buffers from torch's caching host allocator, which keeps each
-        buffer alive until its copy has executed)."""
-        host = torch.from_numpy(self.pack_inputs(iteration, seeds, labels, pcg)).pin_memory()
-        self.stage_device(host.to(self.dev, non_blocking=True))
-
     def pack_inputs(self, iteration: int, seeds: np.ndarray, labels: np.ndarray, pcg: tuple) -> np.ndarray:
-        """The int32 words `stage` copies (for pre-staging whole runs in HBM)."""
+        """One batch's input words (host), as staged in HBM."""
         # layout (int32 words): [0:10) PCG64 words (5 x int64, 8-byte aligned),
         # [10] iteration, [11] pad, [12:12+B) seeds, [12+B:12+2B) labels
         words = np.empty(12 + 2 * self.B, dtype=np.int32)
@@ -109,31 +124,64 @@ class StepEngine:
         words[12 + self.B:] = labels
         return words
 
-    def stage_device(self, words_dev: torch.Tensor):
-        """Device-to-device staging of pre-packed inputs already in HBM."""
+    def upload(self, words: np.ndarray) -> torch.Tensor:
+        """Host words -> HBM (pinned staging from torch's caching host
+        allocator, which keeps the buffer alive until its copy has run)."""
+        return torch.from_numpy(words).pin_memory().to(self.dev, non_blocking=True)
+
+    def _stage_sample(self, words_dev: torch.Tensor):
         self.ws.state[:5].copy_(words_dev[:10].view(torch.int64))
-        self.it.copy_(words_dev[10:11])
         self.seeds.copy_(words_dev[12: 12 + self.B])
+
+    def _stage_train(self, words_dev: torch.Tensor):
+        self.it.copy_(words_dev[10:11])
         self.labels.copy_(words_dev[12 + self.B: 12 + 2 * self.B])
 
-    def launch(self) -> dict:
-        """Run the staged step (graph replay when possible)."""
+    def holds(self, words_dev: torch.Tensor) -> bool:
+        """True if the next slot already holds this batch (sampled ahead)."""
+        w = self.slot_words[self.cur]
+        return w is not None and w is words_dev
+
+    def step_words(self, words_dev: torch.Tensor, next_words: torch.Tensor | None = None) -> dict:
+        """Train the batch whose input words are `words_dev`; when
+        `next_words` is given, also sample that batch ahead (pipelined)."""
+        s = self.cur
+        if not self.holds(words_dev):
+            # prologue / unannounced batch: sample it first, on this stream
+            self._stage_sample(words_dev)
+            sample_blocks_dev(self.tr.graph, self.seeds, self.F0, self.B, self.tr.cfg.fanouts, self.ws,
+                              torch.cuda.current_stream(self.dev), self.slots[s])
+        self._stage_train(words_dev)
+        ahead = next_words is not None
+        if ahead:
+            self._stage_sample(next_words)
+        out = self._launch(s, ahead)
+        self.slot_words[s] = None
+        if ahead:
+            self.slot_words[1 - s] = next_words
+            self.cur = 1 - s
+        return out
+
+    def _launch(self, s: int, ahead: bool) -> dict:
         if self._graphable():
-            if self.graph is None or self.graph_key != self._key():
-                self._capture()
-            self.graph.replay()
-            _lib.load().hg_count_graph_replay(self.graph_launches)
+            gk = (s, ahead)
+            g = self.graphs.get(gk)
+            if g is None or g.key != self._key():
+                g = self._capture(s, ahead)
+            g.graph.replay()
+            _lib.load().hg_count_graph_replay(g.launches)
+            self.out = g.out
             return self.out
-        self.out = self.run()
+        self.out = self.run(s, ahead)
         return self.out
 
     def enable_timeline(self, on: bool = True):
         """Record %globaltimer at phase boundaries of every step (a one-thread
         kernel per mark, on the stream that reaches the boundary); read with
-        timeline_ms(). Changes the captured graph (re-captured on next launch)."""
+        timeline_ms(). Changes the captured graphs (re-captured on next launch)."""
         self.timeline = torch.zeros(32, dtype=torch.int64, device=self.dev) if on else None
         self.timeline_names = []
-        self.graph = None
+        self.graphs = {}
 
     def timeline_ms(self) -> dict:
         """Phase boundary times of the last step, ms after its first mark."""
@@ -152,25 +200,36 @@ class StepEngine:
 
     # -------------------------------------------------------------- step
 
-    def run(self) -> dict:
-        """Enqueue one full iteration on the current stream (no host sync)."""
+    def _blocks(self, s: int) -> list:
+        """DevBlocks (innermost first) over the buffers of sample slot s."""
+        layers = self.slots[s].layers
+        blocks = []
+        for li in range(self.L - 1, -1, -1):
+            r = layers[li]
+            F_dev = self.F0 if li == 0 else layers[li - 1]["counts"][1:2]
+            blocks.append(DevBlock(r["src"], r["blk_off"], r["blk_end"], r["col"], r["dst_deg"], None, F_dev,
+                                   r["counts"][1:2], r["F_max"], r["Fn_max"], r["E_max"]))
+        for b, blk in enumerate(blocks):
+            blk.src_deg = self.zero_deg if b == 0 else blocks[b - 1].dst_deg
+        return blocks
+
+    def run(self, s: int, ahead: bool) -> dict:
+        """Enqueue one full iteration on the current stream (no host sync):
+        train the batch in slot s; if `ahead`, sample the staged next batch
+        into slot 1-s on the sampler stream meanwhile."""
         tr, cfg, net, cache = self.tr, self.tr.cfg, self.tr.network, self.tr.cache
         dev, L, B = self.dev, self.L, self.B
         stream = torch.cuda.current_stream(dev)
         sp = _lib.stream_ptr(stream)
-        g = tr.graph
         self._mark("start", stream)
-        raw = sample_blocks_dev(g, self.seeds, self.F0, B, cfg.fanouts, self.ws, stream)
-        blocks = []
-        for li in range(L - 1, -1, -1):
-            r = raw[li]
-            blocks.append(DevBlock(r["src"], r["blk_off"], r["blk_end"], r["col"], r["dst_deg"], None, r["F_dev"],
-                                   r["counts"][1:2], r["F_max"], r["Fn_max"], r["E_max"]))
-        for b, blk in enumerate(blocks):
-            blk.src_deg = (torch.zeros(blk.num_src, dtype=torch.int32, device=dev) if b == 0
-                           else blocks[b - 1].dst_deg)
+        if ahead:
+            samp = self.samp_stream
+            samp.wait_stream(stream)
+            with torch.cuda.stream(samp):
+                sample_blocks_dev(tr.graph, self.seeds, self.F0, B, cfg.fanouts, self.ws, samp, self.slots[1 - s])
+                self._mark("next_sampled (side)", samp)
+        blocks = self._blocks(s)
 
-        self._mark("sampled", stream)
         # ---- prune walk + lookups (trainer.py:166-207) ----
         counts = torch.empty(2 * L, dtype=torch.int32, device=dev)
         keep, pos, rows, live = [None] * L, [None] * L, [None] * L, [None] * (L + 1)
@@ -229,12 +288,11 @@ class StepEngine:
         self._mark("forward+loss", stream)
 
         # ---- backward (nn.py:300-320) + SGD, cache updates (cache.py:188-204) ----
-        # layer l's admission/ring update (l >= 1) is forked onto the update
+        # layer l's admission/ring update (l >= 1) is forked onto its own
         # stream as soon as norms[l] exist; different layers' caches share no
-        # state, and the join below orders them before anything that follows
+        # state, and the joins below order them before anything that follows
         grads = net.new_grads(zero=False)
         norms = [None] * L
-        side = self.upd_stream
         for l in range(L - 1, -1, -1):
             blk = blocks[l]
             d_prev, nrm = layer_backward_dev(net, l, blk, tapes[l], d_h, grads, l >= 1, keep[l], pos[l], live[l],
@@ -243,6 +301,7 @@ class StepEngine:
             d_h = d_prev
             self._mark(f"backward{l}", stream)
             if l >= 1:
+                side = self.upd_streams[l]
                 side.wait_stream(stream)
                 with torch.cuda.stream(side):
                     cache._layer(l).update_dev(n_live_dev(l), blocks[l].num_src, live[l], blocks[l].src_nodes,
@@ -254,7 +313,10 @@ class StepEngine:
             tr.grad_hook(grads)
         sgd_step(net, grads, cfg.eta)
         self._mark("sgd", stream)
-        stream.wait_stream(side)
+        for side in self.upd_streams.values():
+            stream.wait_stream(side)
+        if ahead:
+            stream.wait_stream(self.samp_stream)
         self._mark("joined", stream)
         return dict(loss=loss, counts=counts, blocks=blocks, live=live, rows=rows, keep=keep, tapes=tapes,
                     norms=norms, grads=grads, injected=injected)
@@ -270,19 +332,15 @@ class StepEngine:
         return (self.tr.use_graphs and self.tr.grad_hook is None
                 and all(lc.table is not None for lc in self.tr.cache.layers.values()))
 
-    def step(self, iteration: int, seeds: np.ndarray, labels: np.ndarray, pcg: tuple) -> dict:
-        """Stage inputs and run one iteration (graph replay when possible)."""
-        self.stage(iteration, seeds, labels, pcg)
-        return self.launch()
-
-    def _capture(self):
+    def _capture(self, s: int, ahead: bool) -> _Graph:
         gc.collect()
         torch.cuda.synchronize(self.dev)
-        # a fresh private memory pool per capture: the previous graph (and its
-        # pool) is released once the new one replaces it
-        self.graph, self.out = None, None
-        self.graph = torch.cuda.CUDAGraph()
-        self.pool = torch.cuda.graph_pool_handle()
+        # a fresh private memory pool per capture: a replaced graph (and its
+        # pool) is released when it is dropped here
+        self.graphs.pop((s, ahead), None)
+        g = _Graph()
+        g.graph = torch.cuda.CUDAGraph()
+        g.pool = torch.cuda.graph_pool_handle()
         self.capturing = True
         n0 = _lib.load().hg_kernel_launches()
         try:
@@ -291,13 +349,15 @@ class StepEngine:
             side = torch.cuda.Stream(self.dev)
             side.wait_stream(torch.cuda.current_stream(self.dev))
             with torch.cuda.stream(side):
-                with torch.cuda.graph(self.graph, pool=self.pool, stream=side):
-                    self.out = self.run()
+                with torch.cuda.graph(g.graph, pool=g.pool, stream=side):
+                    g.out = self.run(s, ahead)
             torch.cuda.current_stream(self.dev).wait_stream(side)
         finally:
             self.capturing = False
         # capture records the launches without executing them
-        self.graph_launches = _lib.load().hg_kernel_launches() - n0
-        _lib.load().hg_count_graph_replay(-self.graph_launches)
+        g.launches = _lib.load().hg_kernel_launches() - n0
+        _lib.load().hg_count_graph_replay(-g.launches)
         self.captures += 1
-        self.graph_key = self._key()
+        g.key = self._key()
+        self.graphs[(s, ahead)] = g
+        return g

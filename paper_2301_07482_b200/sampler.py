@@ -169,37 +169,57 @@ def layer_bounds(B: int, fanouts, num_nodes: int):
     return F, E
 
 
+class SampleSlot:
+    """Preallocated outputs of one batch's layered sampling (upper-bound
+    shapes, device counts): lets a sampled batch outlive the CUDA graph that
+    produced it (the engine samples batch i+1 while it trains batch i)."""
+
+    def __init__(self, g: Csr2Graph, B: int, fanouts):
+        dev = g.start.device
+        N = g.num_nodes
+        self.layers = []
+        F_max = B
+        for fanout in fanouts:
+            E_max = max(1, F_max * fanout)
+            Fn_max = min(N, F_max + E_max)
+            sb = _lib.query("hg_sample_layer_scratch_bytes", F_max, N)
+            self.layers.append(dict(
+                F_max=F_max, E_max=E_max, Fn_max=Fn_max, fanout=fanout,
+                cand_off=torch.empty(F_max + 1, dtype=torch.int64, device=dev),
+                blk_off=torch.empty(F_max + 1, dtype=torch.int32, device=dev),
+                blk_end=torch.empty(F_max, dtype=torch.int32, device=dev),
+                dst_deg=torch.empty(F_max, dtype=torch.int32, device=dev),
+                src_flat=torch.empty(E_max, dtype=torch.int32, device=dev),
+                col=torch.empty(E_max, dtype=torch.int32, device=dev),
+                src=torch.empty(Fn_max, dtype=torch.int32, device=dev),
+                counts=torch.empty(4, dtype=torch.int32, device=dev),
+                scratch=torch.empty(sb, dtype=torch.uint8, device=dev), sb=sb))
+            F_max = Fn_max
+        self.key = None     # which batch the slot currently holds (set by the engine)
+
+
 def sample_blocks_dev(g: Csr2Graph, frontier: torch.Tensor, F0_dev: torch.Tensor, B: int, fanouts,
-                      ws: SamplerWorkspace, stream) -> list:
+                      ws: SamplerWorkspace, stream, slot: SampleSlot | None = None) -> list:
     """Launch every sampling layer with host upper bounds and device counts
     (no host synchronisation). ws.state must hold the batch's PCG64 state.
-    Returns per layer (outermost first): dict of device buffers."""
-    dev = g.start.device
+    Returns per layer (outermost first): dict of device buffers (the slot's
+    preallocated ones when `slot` is given)."""
     N = g.num_nodes
     sp = _lib.stream_ptr(stream)
-    F_max, F_dev = B, F0_dev
+    if slot is None:
+        slot = SampleSlot(g, B, fanouts)
+    F_dev = F0_dev
     raw = []
-    for fanout in fanouts:
-        E_max = max(1, F_max * fanout)
-        Fn_max = min(N, F_max + E_max)
-        cand_off = torch.empty(F_max + 1, dtype=torch.int64, device=dev)
-        blk_off = torch.empty(F_max + 1, dtype=torch.int32, device=dev)
-        blk_end = torch.empty(F_max, dtype=torch.int32, device=dev)
-        dst_deg = torch.empty(F_max, dtype=torch.int32, device=dev)
-        src_flat = torch.empty(E_max, dtype=torch.int32, device=dev)
-        col_local = torch.empty(E_max, dtype=torch.int32, device=dev)
-        src_out = torch.empty(Fn_max, dtype=torch.int32, device=dev)
-        counts = torch.empty(4, dtype=torch.int32, device=dev)
-        sb = _lib.query("hg_sample_layer_scratch_bytes", F_max, N)
-        scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+    for L in slot.layers:
         _lib.call("hg_sample_layer", _lib.ptr(g.start), _lib.ptr(g.end), _lib.ptr(g.col_indices), N,
-                  _lib.ptr(frontier), _lib.ptr(F_dev), F_max, fanout, _lib.ptr(ws.state), _lib.ptr(ws.g2l),
-                  _lib.ptr(ws.bitmap), _lib.ptr(cand_off), _lib.ptr(blk_off), _lib.ptr(blk_end),
-                  _lib.ptr(dst_deg), _lib.ptr(src_flat), _lib.ptr(col_local), _lib.ptr(src_out),
-                  _lib.ptr(counts), _lib.ptr(scratch), sb, sp)
-        raw.append(dict(F_dev=F_dev, F_max=F_max, E_max=E_max, Fn_max=Fn_max, blk_off=blk_off, blk_end=blk_end,
-                        dst_deg=dst_deg, col=col_local, src=src_out, counts=counts))
-        frontier, F_dev, F_max = src_out, counts[1:2], Fn_max
+                  _lib.ptr(frontier), _lib.ptr(F_dev), L["F_max"], L["fanout"], _lib.ptr(ws.state),
+                  _lib.ptr(ws.g2l), _lib.ptr(ws.bitmap), _lib.ptr(L["cand_off"]), _lib.ptr(L["blk_off"]),
+                  _lib.ptr(L["blk_end"]), _lib.ptr(L["dst_deg"]), _lib.ptr(L["src_flat"]), _lib.ptr(L["col"]),
+                  _lib.ptr(L["src"]), _lib.ptr(L["counts"]), _lib.ptr(L["scratch"]), L["sb"], sp)
+        raw.append(dict(F_dev=F_dev, F_max=L["F_max"], E_max=L["E_max"], Fn_max=L["Fn_max"],
+                        blk_off=L["blk_off"], blk_end=L["blk_end"], dst_deg=L["dst_deg"], col=L["col"],
+                        src=L["src"], counts=L["counts"]))
+        frontier, F_dev = L["src"], L["counts"][1:2]
     return raw
 
 

@@ -293,6 +293,7 @@ class Trainer:
         self.grad_hook = None   # callable(Grads) run between backward and SGD (data parallel)
         self.use_graphs = os.environ.get("HG_GRAPHS", "1") != "0"
         self._engines = {}
+        self._ahead = None     # (key, device words) of the batch announced by the last step
 
     # ------------------------------------------------------------ pieces
 
@@ -340,19 +341,37 @@ class Trainer:
             eng = self._engines[B] = StepEngine(self, B)
         return eng
 
-    def _engine_step(self, iteration: int, seeds: np.ndarray):
+    def _words(self, eng: StepEngine, iteration: int, seeds: np.ndarray) -> np.ndarray:
+        bg = batch_rng(self.cfg.seed, iteration).bit_generator.state["state"]
+        return eng.pack_inputs(iteration, seeds.astype(np.int32), self.labels[seeds].astype(np.int32),
+                               (int(bg["state"]), int(bg["inc"])))
+
+    def _engine_step(self, iteration: int, seeds, next_batch=None):
+        """Run one engine step; `next_batch=(iteration, seeds)` announces the
+        following batch so the step samples it ahead (pipelined)."""
         seeds = np.asarray(seeds, dtype=np.int64)
         eng = self._engine(len(seeds))
-        bg = batch_rng(self.cfg.seed, iteration).bit_generator.state["state"]
-        out = eng.step(iteration, seeds.astype(np.int32), self.labels[seeds].astype(np.int32),
-                       (int(bg["state"]), int(bg["inc"])))
+        key = (len(seeds), int(iteration), hash(seeds.tobytes()))
+        if self._ahead is not None and self._ahead[0] == key:
+            words = self._ahead[1]          # uploaded (and sampled) by the previous step
+        else:
+            words = eng.upload(self._words(eng, iteration, seeds))
+        self._ahead = None
+        nxt = None
+        if next_batch is not None:
+            nit, nseeds = next_batch
+            nseeds = np.asarray(nseeds, dtype=np.int64)
+            if len(nseeds) == len(seeds):   # same engine (batch size): pipeline it
+                nxt = eng.upload(self._words(eng, nit, nseeds))
+                self._ahead = ((len(nseeds), int(nit), hash(nseeds.tobytes())), nxt)
+        out = eng.step_words(words, nxt)
         return eng, out
 
-    def train_step_device(self, iteration: int, seeds) -> torch.Tensor:
+    def train_step_device(self, iteration: int, seeds, next_batch=None) -> torch.Tensor:
         """Device-resident step for throughput runs: sample + train one batch
         (graph replay after warm-up); returns the loss as a device scalar and
         does not synchronise. Sweeps run on the host every t_stale steps."""
-        eng, out = self._engine_step(iteration, seeds)
+        eng, out = self._engine_step(iteration, seeds, next_batch)
         self.cache.end_iteration(iteration)
         self._last_engine = (eng, out)
         return out["loss"]
@@ -364,28 +383,27 @@ class Trainer:
         for it, seeds in zip(iterations, seeds_list):
             seeds = np.asarray(seeds, dtype=np.int64)
             eng = self._engine(len(seeds))
-            bg = batch_rng(self.cfg.seed, it).bit_generator.state["state"]
-            words = eng.pack_inputs(it, seeds.astype(np.int32), self.labels[seeds].astype(np.int32),
-                                    (int(bg["state"]), int(bg["inc"])))
-            out.append((it, len(seeds), torch.from_numpy(words).to(self.device)))
+            out.append((it, len(seeds), torch.from_numpy(self._words(eng, it, seeds)).to(self.device)))
         return out
 
-    def train_step_resident(self, staged) -> torch.Tensor:
-        """One step from prestage()d HBM inputs (no host traffic, no sync)."""
+    def train_step_resident(self, staged, next_staged=None) -> torch.Tensor:
+        """One step from prestage()d HBM inputs (no host traffic, no sync);
+        `next_staged` is sampled ahead when given."""
         it, B, words = staged
         eng = self._engine(B)
-        eng.stage_device(words)
-        out = eng.launch()
+        nxt = next_staged[2] if next_staged is not None and next_staged[1] == B else None
+        out = eng.step_words(words, nxt)
         self.cache.end_iteration(it)
         self._last_engine = (eng, out)
         return out["loss"]
 
-    def train_step(self, iteration: int, epoch: int, seeds) -> IterMetrics:
+    def train_step(self, iteration: int, epoch: int, seeds, next_batch=None) -> IterMetrics:
         """Sample + train one batch through the engine and read IterMetrics
-        back (trainer.py:362-421 semantics, sampling included)."""
+        back (trainer.py:362-421 semantics, sampling included).
+        `next_batch=(iteration, seeds)` lets the step sample that batch ahead."""
         cache = self.cache
         before = cache.counters_vector().clone()
-        eng, out = self._engine_step(iteration, seeds)
+        eng, out = self._engine_step(iteration, seeds, next_batch)
         after = cache.counters_vector()
         n_src0 = out["blocks"][0].n_src_dev
         host = torch.cat([out["loss"].view(1), (after - before).double(),
@@ -463,14 +481,16 @@ class Trainer:
             valid_entries=valid, estimation_error=math.nan)
 
     def train(self) -> list:
-        """trainer.py:423-433: every batch of every epoch, in order. Sampling
-        runs inside the captured step (no producer thread is needed: the
-        sampler kernels are part of the same stream / graph)."""
+        """trainer.py:423-433: every batch of every epoch, in order. The
+        producer thread's run-ahead (sampler.py:193-263) becomes the engine's
+        pipelined sampler: each step samples the next batch on a side stream
+        while it trains the current one."""
         cfg = self.cfg
         batches = make_batches(self.train_ids, cfg)
         per_epoch = max(1, math.ceil(len(self.train_ids) / cfg.batch_size))
         for iteration, seeds in enumerate(batches):
-            self.metrics.append(self.train_step(iteration, iteration // per_epoch, seeds))
+            nxt = (iteration + 1, batches[iteration + 1]) if iteration + 1 < len(batches) else None
+            self.metrics.append(self.train_step(iteration, iteration // per_epoch, seeds, next_batch=nxt))
         return self.metrics
 
 

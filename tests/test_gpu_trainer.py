@@ -151,9 +151,11 @@ def test_fp16_feature_table():
 
 @pytest.mark.parametrize("kind", [SAGE, GCN])
 @pytest.mark.parametrize("graphs", [True, False])
-def test_engine_lockstep_with_oracle(kind, graphs):
+@pytest.mark.parametrize("ahead", [True, False])
+def test_engine_lockstep_with_oracle(kind, graphs, ahead):
     """The sync-free engine (Trainer.train_step, CUDA-graph replay after the
-    cache rings exist) against the oracle in lockstep."""
+    cache rings exist; with `ahead` the next batch is sampled during the
+    current step) against the oracle in lockstep."""
     import paper_2301_07482_b200 as hg
     ds, g = _pl3000()
     lk, ok = _kinds(kind)
@@ -164,7 +166,8 @@ def test_engine_lockstep_with_oracle(kind, graphs):
     otr = OTrainer(g, ds.features, ds.labels, ds.train_ids, OTrainConfig(kind=ok, **common), ds.num_classes)
     batches = hg.make_batches(ds.train_ids, tr.cfg)
     for it, seeds in enumerate(batches):
-        m = tr.train_step(it, 0, seeds)
+        nxt = (it + 1, batches[it + 1]) if ahead and it + 1 < len(batches) else None
+        m = tr.train_step(it, 0, seeds, next_batch=nxt)
         norms = {l: tr.last[3][l].cpu().numpy() for l in range(1, 3)}
         om = otr.train_iteration(it, 0, otr.sample(it, seeds), norms_override=norms)
         for f in INT_FIELDS:
@@ -176,6 +179,32 @@ def test_engine_lockstep_with_oracle(kind, graphs):
     if graphs:
         assert any(e.graph is not None for e in tr._engines.values()), "graph was never captured"
     tr.cache.check_integrity()
+
+
+def test_pipelined_sampling_bitwise_equals_sequential():
+    """Sampling batch i+1 during step i (two slots, side stream) changes
+    nothing: weights, losses and cache decisions are bitwise identical to
+    the unpipelined engine, including an announced batch that is then not
+    used (the engine resamples) and a batch-size change at the epoch end."""
+    import paper_2301_07482_b200 as hg
+    ds, g = _pl3000()
+    cfg = hg.TrainConfig(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=2, eta=0.05,
+                         kind=hg.LayerKind.SAGE_MEAN, p_grad=0.9, t_stale=5, seed=2)
+    batches = hg.make_batches(ds.train_ids, cfg)
+    runs = []
+    for mode in ("seq", "ahead", "ahead_wrong"):
+        tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
+        ms = []
+        for it, seeds in enumerate(batches):
+            nxt = None
+            if mode != "seq" and it + 1 < len(batches):
+                nxt = (it + 1, batches[it + 1])
+                if mode == "ahead_wrong" and it % 7 == 3:
+                    nxt = (it + 2, batches[(it + 2) % len(batches)])   # announced, then not used
+            ms.append(tr.train_step(it, 0, seeds, next_batch=nxt))
+        runs.append((hashlib.sha256(tr.network.checksum_bytes()).hexdigest(),
+                     [(m.loss, m.hits, m.admissions, m.fetched_bytes, m.prune_writes) for m in ms]))
+    assert runs[0] == runs[1] == runs[2]
 
 
 def test_graph_replay_bitwise_equals_eager_engine():
