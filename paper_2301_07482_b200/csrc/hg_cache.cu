@@ -1,8 +1,10 @@
 // K10: historical-cache admission / eviction / ring scatter-update for one
 // layer, bit-exact with histgnn/cache.py:131-204 (oracle: oracle/histcache.py).
 //
-//   U1  keys (norm fp64 bits, node id) for the live nodes; one stable radix sort
-//       ranks them "norm ascending, ties by id" (cache.py:191)
+//   U1  keys (norm fp64 bits, node id) for the live nodes; one device sort
+//       (merge sort, or 96-bit LSD radix at large n) ranks them "norm
+//       ascending, ties by id" (cache.py:191); ids are unique, so the order is
+//       total and independent of the algorithm
 //   U2  rank j >= k (k = floor(p_grad * n)): gradient eviction of cached nodes;
 //       rank j < k: admitted; admitted & computed -> write flag
 //   U3  compaction of write flags in rank order -> write list, n_write
@@ -37,14 +39,19 @@ struct NormKeyLess {
   }
 };
 
-// rank sort: "merge" (block sort + merge passes; default) or "radix" (96-bit LSD)
-inline bool use_radix_sort() {
-  static int v = -1;
-  if (v < 0) {
+// rank sort: CUB merge sort (block sort + merge-path passes) up to kMergeMaxN
+// live nodes, CUB 96-bit LSD radix sort above (12 onesweep passes, better at
+// large n). HG_CACHE_SORT=radix|merge overrides (A/B measurements).
+constexpr long long kMergeMaxN = 1 << 20;
+enum SortMode { kSortMerge = 1, kSortRadix = 2 };
+inline int sort_mode(long long n_max) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = std::getenv("HG_CACHE_SORT");
-    v = (e && std::strcmp(e, "radix") == 0) ? 1 : 0;
+    v = !e ? -1 : (std::strcmp(e, "radix") == 0 ? kSortRadix : (std::strcmp(e, "merge") == 0 ? kSortMerge : -1));
   }
-  return v == 1;
+  if (v >= 0) return v;
+  return n_max <= kMergeMaxN ? kSortMerge : kSortRadix;
 }
 
 struct NormKeyDecomposer {
@@ -266,7 +273,7 @@ int hg_cache_rank(const int32_t* n_dev, int n_max, double p_grad, const int32_t*
   int* part = reinterpret_cast<int*>(retained + nn + 16 - ((uintptr_t)(retained + nn) & 15));
   void* tmp = part + scan_tiles(n_max) + 4;
   size_t tmp_bytes = (size_t)(scratch_bytes - ((char*)tmp - p));
-  const bool radix = use_radix_sort();
+  const bool radix = sort_mode(n_max) == kSortRadix;
   // the merge sort is in place: keys go straight to keys_out / vals_out
   k_norm_keys<<<grid_for(n_max, 256), 256, 0, stream>>>(n_dev, n_max, p_grad, live, src_nodes, norms,
                                                         radix ? keys_in : keys_out, radix ? vals_in : vals_out,

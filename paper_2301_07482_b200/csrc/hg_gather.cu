@@ -13,6 +13,8 @@
 // are issued before any store (memory-level parallelism per warp = kRows rows).
 #include "hgb200.h"
 #include <cuda_fp16.h>
+#include <cstdlib>
+#include <cstring>
 
 #include "hg_common.cuh"
 #include "hg_state.h"
@@ -113,6 +115,119 @@ __global__ void __launch_bounds__(256) k_load_rows(const int32_t* n_live_dev, co
   kt_end(kt);
 }
 
+// ---------------------------------------------------------------------------
+// fp32 sources: the gather is a pure row copy, done by the TMA engine.
+// Each warp streams groups of R rows (lane r < R owns row r of the group):
+// cp.async.bulk global -> smem (one bulk copy per row, completion counted in
+// bytes on the stage's mbarrier), then cp.async.bulk smem -> global into the
+// row's frontier position. kS stages per warp keep kS-1 groups of loads in
+// flight while earlier groups drain, without holding any row in registers.
+constexpr int kBulkWarps = 2;
+constexpr int kBulkStages = 3;
+constexpr int kBulkSmem = 80 * 1024;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(b)));
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done)
+                 : "r"(su32(b)), "r"(parity)
+                 : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(b))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(su32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kBulkWarps * 32) k_load_rows_bulk(
+    const int32_t* n_live_dev, const int32_t* __restrict__ live, const int32_t* __restrict__ src_nodes,
+    const int32_t* __restrict__ feature_row_of, const char* __restrict__ region, const char* __restrict__ feats,
+    int row_bytes, int rows_per_group, float* __restrict__ out, unsigned long long* __restrict__ gctr) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int R = rows_per_group;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * kBulkStages;
+  unsigned char* buf = smem + 128 + (size_t)warp * kBulkStages * R * row_bytes;
+  if (lane == 0) {
+    for (int s = 0; s < kBulkStages; ++s) bar_init(&bars[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  KTimer* kt = g_kt ? g_kt + kTLoadRows : nullptr;
+  kt_begin(kt);
+  const int n = *n_live_dev;
+  const int ngroups = (n + R - 1) / R;
+  const int W = gridDim.x * kBulkWarps;
+  const int gw = blockIdx.x * kBulkWarps + warp;
+  const int mine = gw < ngroups ? (ngroups - gw + W - 1) / W : 0;
+  unsigned hits = 0, valid_rows = 0;
+  auto issue = [&](int it) {
+    const int s = it % kBulkStages;
+    const int i = (gw + it * W) * R + lane;
+    const bool valid = lane < R && i < n;
+    const char* src = nullptr;
+    bool hit = false;
+    if (valid) {
+      const int id = src_nodes[live[i]];
+      const int fr = feature_row_of ? feature_row_of[id] : -1;
+      hit = fr >= 0;
+      src = hit ? region + (long long)fr * row_bytes : feats + (long long)id * row_bytes;
+    }
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    hits += __popc(__ballot_sync(0xffffffffu, hit));
+    valid_rows += __popc(vm);
+    if (lane == 0) bar_expect_tx(&bars[s], (uint32_t)__popc(vm) * (uint32_t)row_bytes);
+    if (valid) bulk_load(buf + ((size_t)s * R + lane) * row_bytes, src, (uint32_t)row_bytes, &bars[s]);
+  };
+  for (int p = 0; p < kBulkStages - 1 && p < mine; ++p) issue(p);
+  for (int it = 0; it < mine; ++it) {
+    const int s = it % kBulkStages;
+    bar_wait(&bars[s], (uint32_t)((it / kBulkStages) & 1));
+    const int i = (gw + it * W) * R + lane;
+    if (lane < R && i < n)
+      bulk_store(reinterpret_cast<char*>(out) + (long long)live[i] * row_bytes, buf + ((size_t)s * R + lane) * row_bytes,
+                 (uint32_t)row_bytes);
+    const int nx = it + kBulkStages - 1;
+    if (nx < mine) {
+      bulk_wait_read1();  // the stage nx reuses was last stored from two groups ago
+      issue(nx);
+    }
+  }
+  bulk_wait_all();
+  if (lane == 0) {
+    if (hits) atomicAdd(gctr + kGCtrFeatureHits, (unsigned long long)hits);
+    if (valid_rows - hits) atomicAdd(gctr + kGCtrFeatureMisses, (unsigned long long)(valid_rows - hits));
+  }
+  kt_end(kt);
+}
+
+// HG_GATHER=bulk selects the TMA gather (faster alone; the register gather
+// shares SMs better with the concurrently running sampler)
+inline bool use_bulk_gather() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("HG_GATHER");
+    v = (e && std::strcmp(e, "bulk") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 }  // namespace
 }  // namespace hg
 
@@ -130,8 +245,30 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
   if ((reinterpret_cast<uintptr_t>(feats) | reinterpret_cast<uintptr_t>(h_out)) & 15)
     return fail(W, kBadArg, "feature / output pointers must be 16-byte aligned");
   if (dim * isz > 16 * 32 * kMaxT) return fail(W, kBadArg, "feature rows above 2 KB are not supported");
-  const unsigned grid = grid_for((n_live_max + kRows - 1) / kRows * 32, 256, 148 * 8);
   auto* g = reinterpret_cast<unsigned long long*>(global_ctr);
+  if (dtype == 0 && use_bulk_gather()) {
+    const int row_bytes = dim * 4;
+    int R = (kBulkSmem - 128) / (kBulkWarps * kBulkStages * row_bytes);
+    if (R > 32) R = 32;
+    if (R >= 1) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_load_rows_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+        attr = true;
+      }
+      const long long groups = (n_live_max + R - 1) / R;
+      long long blocks = (groups + kBulkWarps - 1) / kBulkWarps;
+      if (blocks > 148 * 2) blocks = 148 * 2;
+      if (blocks < 1) blocks = 1;
+      const size_t smem = 128 + (size_t)kBulkWarps * kBulkStages * R * row_bytes;
+      k_load_rows_bulk<<<(unsigned)blocks, kBulkWarps * 32, smem, stream>>>(
+          n_live_dev, live, src_nodes, feature_row_of, static_cast<const char*>(region),
+          static_cast<const char*>(feats), row_bytes, R, h_out, g);
+      HG_LAUNCHED(W);
+      return kOk;
+    }
+  }
+  const unsigned grid = grid_for((n_live_max + kRows - 1) / kRows * 32, 256, 148 * 8);
   const int T = (dim * isz / 16 + 31) / 32;
 #define HG_LOAD(TT, KT)                                                                                     \
   k_load_rows<TT, KT><<<grid, 256, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,               \

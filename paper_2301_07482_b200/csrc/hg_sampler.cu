@@ -20,6 +20,7 @@
 // No O(N) memset per call: g2l entries are epoch-stamped, the bitmap is
 // self-clearing.
 #include "hgb200.h"
+#include <cstdlib>
 #include "hg_pcg.cuh"
 #include "hg_scan.cuh"
 
@@ -538,8 +539,15 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   if (st) return st;
   k_task_bounds<<<grid_for(F_max, 256), 256, 0, stream>>>(F_dev, cand_off, task_row, task_meta);
   HG_LAUNCHED(W);
-  // enough warps for the largest task count the candidate total can produce
-  const unsigned sel_grid = 148 * 16;
+  // persistent warps over the tasks; HG_SEL_BLOCKS caps the grid (leaves SMs
+  // to the training stream that runs concurrently with the pipelined sampler)
+  static long long sel_cap = -1;
+  if (sel_cap < 0) {
+    const char* e = std::getenv("HG_SEL_BLOCKS");
+    sel_cap = e ? std::atoll(e) : 148 * 2;   // 2 CTAs (16 warps) per SM measured best
+    if (sel_cap < 1) sel_cap = 148 * 2;
+  }
+  const unsigned sel_grid = (unsigned)sel_cap;
   if (fanout <= 32)
     k_select<true><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
                                                           blk_off, src_flat, col_local, task_row, task_meta);

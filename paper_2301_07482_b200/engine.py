@@ -35,7 +35,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .nn import Injection, cross_entropy_dev, layer_backward_dev, layer_forward_dev, sgd_step
+from .nn import (Injection, build_csc, cross_entropy_dev, layer_backward_dev, layer_forward_dev,
+                 pack_dgrad_weights, sgd_step)
 from .sampler import SamplerWorkspace, SampleSlot, layer_bounds, pcg_words, sample_blocks_dev
 
 
@@ -95,6 +96,11 @@ class StepEngine:
         # block 0's sources carry no in-edges (src_deg = 0): one persistent zero vector
         self.zero_deg = torch.zeros(self.slots[0].layers[-1]["Fn_max"], dtype=torch.int32, device=self.dev)
         self.samp_stream = torch.cuda.Stream(self.dev)
+        # backward inputs that depend only on the pruned blocks / the weights
+        # (transposed CSC, TS-packed dgrad weights) are built on prep_stream
+        # during the forward; weight-gradient GEMMs run on wgrad_stream
+        self.prep_stream = torch.cuda.Stream(self.dev)
+        self.wgrad_stream = torch.cuda.Stream(self.dev)
         # cache updates of layer l run on side stream l, overlapping the
         # backward of layers < l (they only read the forward tape and norms[l])
         self.upd_streams = {l: torch.cuda.Stream(self.dev) for l in range(1, self.L)}
@@ -267,6 +273,15 @@ class StepEngine:
             return counts[2 * b + 1:2 * b + 2]
 
         self._mark("pruned", stream)
+        # ---- off-critical-path backward prep (overlaps the forward) ----
+        prep = self.prep_stream
+        prep.wait_stream(stream)
+        cscs, w_ts = [None] * L, [None] * L
+        with torch.cuda.stream(prep):
+            psp = _lib.stream_ptr(prep)
+            for l in range(1, L):
+                cscs[l] = build_csc(blocks[l], keep[l], pos[l], blocks[l].n_dst_dev, psp)
+                w_ts[l] = pack_dgrad_weights(net, l, psp)
         # ---- layer-0 input (trainer.py:326-343) ----
         b0 = blocks[0]
         h = torch.empty((b0.num_src, tr.feature_dim), dtype=torch.float32, device=dev)
@@ -293,10 +308,13 @@ class StepEngine:
         # state, and the joins below order them before anything that follows
         grads = net.new_grads(zero=False)
         norms = [None] * L
+        keepalive = []
+        stream.wait_stream(prep)
         for l in range(L - 1, -1, -1):
             blk = blocks[l]
             d_prev, nrm = layer_backward_dev(net, l, blk, tapes[l], d_h, grads, l >= 1, keep[l], pos[l], live[l],
-                                             blk.num_src, sp, blk.n_dst_dev, n_live_dev(l))
+                                             blk.num_src, sp, blk.n_dst_dev, n_live_dev(l), csc=cscs[l],
+                                             W_ts=w_ts[l], wgrad_stream=self.wgrad_stream, keepalive=keepalive)
             norms[l] = nrm
             d_h = d_prev
             self._mark(f"backward{l}", stream)
@@ -309,6 +327,7 @@ class StepEngine:
                                                cache.refresh_retained, _lib.stream_ptr(side),
                                                allow_alloc=not self.capturing)
                     self._mark(f"cache_update{l} (side)", side)
+        stream.wait_stream(self.wgrad_stream)
         if tr.grad_hook is not None:
             tr.grad_hook(grads)
         sgd_step(net, grads, cfg.eta)
@@ -319,7 +338,7 @@ class StepEngine:
             stream.wait_stream(self.samp_stream)
         self._mark("joined", stream)
         return dict(loss=loss, counts=counts, blocks=blocks, live=live, rows=rows, keep=keep, tapes=tapes,
-                    norms=norms, grads=grads, injected=injected)
+                    norms=norms, grads=grads, injected=injected, keepalive=(keepalive, cscs, w_ts))
 
     # ------------------------------------------------------------ driver
 

@@ -346,10 +346,27 @@ def build_csc(blk, keep: torch.Tensor, pos_of: torch.Tensor, n_dst_dev, stream, 
     return BlockCsc(vals, seg_lo, seg_hi)
 
 
+def pack_dgrad_weights(net: Network, l: int, stream) -> torch.Tensor:
+    """TS(P[:K]) of layer l: the B operand of the input-gradient GEMM."""
+    d_in, d_out = net.dims[l], net.dims[l + 1]
+    K = 2 * d_in if _kind_code(net.kind) == KIND_SAGE else d_in
+    W = torch.empty(ts_bytes(K, d_out), dtype=torch.uint8, device=net.flat.device)
+    _lib.call("hg_ts_pack", _lib.ptr(net.slab(l)), d_out, 0, K, d_out, K, _lib.ptr(W), stream)
+    return W
+
+
 def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tensor, grads: Grads,
-                       need_input: bool, keep, pos_of, live, n_live, stream, n_dst_dev=None, n_live_dev=None):
+                       need_input: bool, keep, pos_of, live, n_live, stream, n_dst_dev=None, n_live_dev=None,
+                       csc: BlockCsc | None = None, W_ts: torch.Tensor | None = None, wgrad_stream=None,
+                       keepalive: list | None = None):
     """Writes dP into grads; returns (d_in [n_src, d_in] with rows valid on
-    `live`, fp64 norms aligned with `live`) or (None, None)."""
+    `live`, fp64 norms aligned with `live`) or (None, None).
+
+    Engine options: `csc` / `W_ts` prebuilt off the critical path (they
+    depend only on the pruned block / the weights), and `wgrad_stream`: the
+    weight-gradient GEMM forks onto it (only SGD waits for it) while the
+    input-gradient chain continues; buffers it reads are appended to
+    `keepalive`, which the caller holds until the streams are joined."""
     dev = d_h.device
     d_in_dim, d_out = net.dims[l], net.dims[l + 1]
     R, K = t.R, t.K
@@ -359,20 +376,34 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
               int(t.relu), _lib.ptr(dz), stream)
     dP = grads.slab(l)
     splits = _wgrad_splits(R, K + 1, d_out)
-    part = torch.empty(splits * (K + 1) * d_out, dtype=torch.float32, device=dev)
-    _lib.call("hg_ts_linear_wgrad", _lib.ptr(t.R_dev), R, _lib.ptr(t.A), K + 1, _lib.ptr(dz), d_out,
-              _lib.ptr(dP), _lib.ptr(part), splits, stream)
+
+    def wgrad(sp):
+        part = torch.empty(splits * (K + 1) * d_out, dtype=torch.float32, device=dev)
+        _lib.call("hg_ts_linear_wgrad", _lib.ptr(t.R_dev), R, _lib.ptr(t.A), K + 1, _lib.ptr(dz), d_out,
+                  _lib.ptr(dP), _lib.ptr(part), splits, sp)
+        return part
+
+    if wgrad_stream is not None:
+        cur = torch.cuda.current_stream(dev)
+        wgrad_stream.wait_stream(cur)
+        with torch.cuda.stream(wgrad_stream):
+            part = wgrad(_lib.stream_ptr(wgrad_stream))
+        if keepalive is not None:
+            keepalive.extend([dz, part])
+    else:
+        wgrad(stream)
     if not need_input:
         return None, None
     SG = torch.empty((R, K), dtype=torch.float32, device=dev)
-    W = torch.empty(ts_bytes(K, d_out), dtype=torch.uint8, device=dev)        # TS(P[:K]): B of the dgrad
-    _lib.call("hg_ts_pack", _lib.ptr(net.slab(l)), d_out, 0, K, d_out, K, _lib.ptr(W), stream)
-    _lib.call("hg_ts_linear_dgrad", _lib.ptr(t.R_dev), R, _lib.ptr(dz), d_out, _lib.ptr(W), K, _lib.ptr(SG), stream)
+    if W_ts is None:
+        W_ts = pack_dgrad_weights(net, l, stream)
+    _lib.call("hg_ts_linear_dgrad", _lib.ptr(t.R_dev), R, _lib.ptr(dz), d_out, _lib.ptr(W_ts), K, _lib.ptr(SG), stream)
     if n_dst_dev is None:
         n_dst_dev = _dev_count(blk.num_dst, dev)
     if n_live_dev is None:
         n_live_dev = _dev_count(n_live, dev)
-    csc = build_csc(blk, keep, pos_of, n_dst_dev, stream)
+    if csc is None:
+        csc = build_csc(blk, keep, pos_of, n_dst_dev, stream)
     d_in = torch.empty((blk.num_src, d_in_dim), dtype=torch.float32, device=dev)
     norms = torch.empty(max(n_live, 1), dtype=torch.float64, device=dev)
     _lib.call("hg_transpose_agg", _kind_code(net.kind), _lib.ptr(n_live_dev), n_live, _lib.ptr(live),

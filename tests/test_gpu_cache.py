@@ -80,3 +80,36 @@ def test_oversized_batch_keeps_trailing_writes():
     assert sorted(hits) == [1, 2] and list(miss) == [0]
     assert cache.valid_entries() == 2
     cache.check_integrity()
+
+
+@pytest.mark.parametrize("n,ties", [(3000, 7), (50_000, 50), (200_000, 1000), (1_100_000, 3000)])
+def test_large_updates_with_ties_match_oracle(n, ties):
+    """Admission ranking at batch sizes where the device sort switches
+    strategy (merge sort up to 2^20 live nodes, LSD radix above), with heavy
+    exact norm ties (ties break by node id, cache.py:191): three iterations of
+    lookup + update + sweep, bit-exact against the oracle."""
+    import paper_2301_07482_b200 as hg
+    from oracle.histcache import OCachePolicy, OHistCache
+    N, H = 2 * n, 4
+    rng = np.random.default_rng(n)
+    pol = (0.8, 2.0, None)
+    cache = hg.HistCache(N, [H], hg.CachePolicy(*pol))
+    ocache = OHistCache(N, [H], OCachePolicy(*pol))
+    for it in range(3):
+        batch = rng.choice(N, size=n, replace=False).astype(np.int64)
+        hits, rows, miss = cache.lookup(1, batch, it)
+        oh, orows, om = ocache.lookup(1, batch, it)
+        np.testing.assert_array_equal(hits, oh)
+        np.testing.assert_array_equal(miss, om)
+        np.testing.assert_array_equal(np.asarray(rows), np.asarray(orows))
+        emb = rng.standard_normal((n, H)).astype(np.float32)
+        norms = rng.integers(0, ties, size=n).astype(np.float64) * 0.125   # exact duplicates
+        cache.update_cache(1, batch, miss, emb, norms, it)
+        ocache.update_cache(1, batch, om, emb, norms, it)
+        cache.end_iteration(it)
+        ocache.end_iteration(it)
+        lc, oc = cache.layers[1], ocache.layers[1]
+        np.testing.assert_array_equal(lc.row_of, oc.row_of)
+        np.testing.assert_array_equal(lc.admit_iter, oc.admit_iter)
+        np.testing.assert_array_equal(lc.table_view.cpu().numpy(), oc.table)
+        assert cache.counters() == ocache.counters()
