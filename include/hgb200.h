@@ -82,9 +82,12 @@ int hg_cache_lookup(const int32_t* n_live_dev, long long n_live_max, const int32
 /* ---- K5 feature load: histgnn/trainer.py:326-343 (Trainer._load_input),
  * cache.py:274-284 (feature region), trainer.py:213-228 (FeatureSource.fetch).
  * feats may be a UVA pointer to pinned host memory. dtype 0 = fp32, 1 = fp16. */
+long long hg_load_features_scratch_bytes(long long n_live_max);
+/* scratch may be NULL (register gather); with it, fp32 rows are copied by TMA bulk copies */
 int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const int32_t* src_nodes,
                      const int32_t* feature_row_of, const void* region, const void* feats, int dim, int dtype,
-                     float* h_out, long long* global_ctr, cudaStream_t stream);
+                     float* h_out, long long* global_ctr, void* scratch, long long scratch_bytes,
+                     cudaStream_t stream);
 
 /* ---- K6 block aggregation: histgnn/nn.py:101-128,142-156 (_gcn_matrix,
  * _mean_matrix, _layer_forward_ctx). kind 0 = GCN, 1 = SAGE_MEAN. */

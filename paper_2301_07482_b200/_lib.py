@@ -38,7 +38,8 @@ SIGNATURES = {
     "hg_prune_scratch_bytes": (I64, [I64]),
     "hg_prune_block": (I32, [P, I64, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P]),
     "hg_cache_lookup": (I32, [P, I64, P, P, I64, P, P, P, P, F64, P, P, P, P]),
-    "hg_load_features": (I32, [P, I64, P, P, P, P, P, I32, I32, P, P, P]),
+    "hg_load_features_scratch_bytes": (I64, [I64]),
+    "hg_load_features": (I32, [P, I64, P, P, P, P, P, I32, I32, P, P, P, I64, P]),
     "hg_aggregate_fwd": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, P, P]),
     "hg_gemm_rm": (I32, [I32, I32, I64, I64, I64, P, I64, P, I64, F32, P, I64, P]),
     "hg_scatter_rows": (I32, [P, I64, P, P, I32, I32, P, P]),

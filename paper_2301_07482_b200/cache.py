@@ -185,7 +185,7 @@ class _LayerCache:
         return self._dummy
 
     def update_dev(self, n_dev, n_max, live, src_nodes, norms, computed_flag, emb, it_dev, refresh_retained,
-                   stream, allow_alloc=True):
+                   stream, allow_alloc=True, mark=None):
         """cache.py:188-204 for the n_dev[0] live nodes (n_max host bound).
         The ring table is allocated on first use (cache.py:79-91), which reads
         the first write count back to the host (allow_alloc=False forbids it,
@@ -198,6 +198,8 @@ class _LayerCache:
         _lib.call("hg_cache_rank", _lib.ptr(n_dev), n_max, float(self.policy.p_grad), _lib.ptr(live),
                   _lib.ptr(src_nodes), _lib.ptr(norms), _lib.ptr(computed_flag), _lib.ptr(self.row_of_dev),
                   _lib.ptr(owner), _lib.ptr(self.ctr), _lib.ptr(scratch), sb, stream)
+        if mark is not None:
+            mark("ranked")
         if self.table is None:
             if not allow_alloc:
                 raise RuntimeError("cache table must be allocated before graph capture")

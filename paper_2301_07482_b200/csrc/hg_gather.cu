@@ -38,7 +38,7 @@ constexpr int kMaxT = 4;        // 16-byte vectors per lane per row (rows <= 2 K
 // issues its 16-byte loads for all kRows rows before the first store, so each
 // warp has up to kRows * kMaxT independent 128-bit loads in flight.
 template <typename TIn, int kT>
-__global__ void __launch_bounds__(256) k_load_rows(const int32_t* n_live_dev, const int32_t* __restrict__ live,
+__global__ void __launch_bounds__(256, 4) k_load_rows(const int32_t* n_live_dev, const int32_t* __restrict__ live,
                                                    const int32_t* __restrict__ src_nodes,
                                                    const int32_t* __restrict__ feature_row_of,
                                                    const TIn* __restrict__ region, const TIn* __restrict__ feats,
@@ -123,8 +123,8 @@ __global__ void __launch_bounds__(256) k_load_rows(const int32_t* n_live_dev, co
 // row's frontier position. kS stages per warp keep kS-1 groups of loads in
 // flight while earlier groups drain, without holding any row in registers.
 constexpr int kBulkWarps = 2;
-constexpr int kBulkStages = 3;
-constexpr int kBulkSmem = 80 * 1024;
+constexpr int kBulkStages = 4;
+constexpr int kBulkSmem = 110 * 1024;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(uint64_t* b) {
@@ -155,10 +155,34 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t 
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// index chain (live -> node id -> region row) resolved for every live row at
+// once, fully parallel and coalesced, so the copy kernel's issue loop has no
+// dependent loads: src_ptr[i] = source row address; hit / miss counters
+__global__ void __launch_bounds__(256) k_row_src(const int32_t* n_live_dev, const int32_t* __restrict__ live,
+                                                 const int32_t* __restrict__ src_nodes,
+                                                 const int32_t* __restrict__ feature_row_of,
+                                                 const char* __restrict__ region, const char* __restrict__ feats,
+                                                 int row_bytes, const char** __restrict__ src_ptr,
+                                                 unsigned long long* __restrict__ gctr) {
+  const int n = *n_live_dev;
+  unsigned long long* c = gctr;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i - (int)(threadIdx.x & 31) < n; i += gridDim.x * blockDim.x) {
+    const bool valid = i < n;
+    bool hit = false;
+    if (valid) {
+      const int id = src_nodes[live[i]];
+      const int fr = feature_row_of ? feature_row_of[id] : -1;
+      hit = fr >= 0;
+      src_ptr[i] = hit ? region + (long long)fr * row_bytes : feats + (long long)id * row_bytes;
+    }
+    warp_count_add(c + kGCtrFeatureHits, hit);
+    warp_count_add(c + kGCtrFeatureMisses, valid && !hit);
+  }
+}
+
 __global__ void __launch_bounds__(kBulkWarps * 32) k_load_rows_bulk(
-    const int32_t* n_live_dev, const int32_t* __restrict__ live, const int32_t* __restrict__ src_nodes,
-    const int32_t* __restrict__ feature_row_of, const char* __restrict__ region, const char* __restrict__ feats,
-    int row_bytes, int rows_per_group, float* __restrict__ out, unsigned long long* __restrict__ gctr) {
+    const int32_t* n_live_dev, const int32_t* __restrict__ live, const char* const* __restrict__ src_ptr,
+    int row_bytes, int rows_per_group, float* __restrict__ out) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int R = rows_per_group;
@@ -176,24 +200,13 @@ __global__ void __launch_bounds__(kBulkWarps * 32) k_load_rows_bulk(
   const int W = gridDim.x * kBulkWarps;
   const int gw = blockIdx.x * kBulkWarps + warp;
   const int mine = gw < ngroups ? (ngroups - gw + W - 1) / W : 0;
-  unsigned hits = 0, valid_rows = 0;
   auto issue = [&](int it) {
     const int s = it % kBulkStages;
     const int i = (gw + it * W) * R + lane;
     const bool valid = lane < R && i < n;
-    const char* src = nullptr;
-    bool hit = false;
-    if (valid) {
-      const int id = src_nodes[live[i]];
-      const int fr = feature_row_of ? feature_row_of[id] : -1;
-      hit = fr >= 0;
-      src = hit ? region + (long long)fr * row_bytes : feats + (long long)id * row_bytes;
-    }
     const unsigned vm = __ballot_sync(0xffffffffu, valid);
-    hits += __popc(__ballot_sync(0xffffffffu, hit));
-    valid_rows += __popc(vm);
     if (lane == 0) bar_expect_tx(&bars[s], (uint32_t)__popc(vm) * (uint32_t)row_bytes);
-    if (valid) bulk_load(buf + ((size_t)s * R + lane) * row_bytes, src, (uint32_t)row_bytes, &bars[s]);
+    if (valid) bulk_load(buf + ((size_t)s * R + lane) * row_bytes, src_ptr[i], (uint32_t)row_bytes, &bars[s]);
   };
   for (int p = 0; p < kBulkStages - 1 && p < mine; ++p) issue(p);
   for (int it = 0; it < mine; ++it) {
@@ -210,15 +223,13 @@ __global__ void __launch_bounds__(kBulkWarps * 32) k_load_rows_bulk(
     }
   }
   bulk_wait_all();
-  if (lane == 0) {
-    if (hits) atomicAdd(gctr + kGCtrFeatureHits, (unsigned long long)hits);
-    if (valid_rows - hits) atomicAdd(gctr + kGCtrFeatureMisses, (unsigned long long)(valid_rows - hits));
-  }
   kt_end(kt);
 }
 
-// HG_GATHER=bulk selects the TMA gather (faster alone; the register gather
-// shares SMs better with the concurrently running sampler)
+// HG_GATHER=bulk selects the TMA copy path (given a workspace). Measured on
+// C2 (400-byte rows): the bulk copies are TMA-issue bound (~67 us for 312K
+// rows) and the index pre-pass adds ~16 us, so the register gather (~82 us)
+// stays the default.
 inline bool use_bulk_gather() {
   static int v = -1;
   if (v < 0) {
@@ -235,22 +246,35 @@ using namespace hg;
 
 extern "C" {
 
+long long hg_load_features_scratch_bytes(long long n_live_max) { return (n_live_max + 2) * 8 + 256; }
+
 // dtype: 0 = fp32, 1 = fp16. dim * itemsize must be a multiple of 16 bytes.
+// With a workspace (scratch, hg_load_features_scratch_bytes), fp32 rows are
+// copied by the TMA engine (k_row_src + k_load_rows_bulk); otherwise, or for
+// fp16 (converted on the fly), by the register gather k_load_rows.
 int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const int32_t* src_nodes,
                      const int32_t* feature_row_of, const void* region, const void* feats, int dim, int dtype,
-                     float* h_out, long long* global_ctr, cudaStream_t stream) {
+                     float* h_out, long long* global_ctr, void* scratch, long long scratch_bytes,
+                     cudaStream_t stream) {
   const char* W = "hg_load_features";
   const int isz = dtype == 1 ? 2 : 4;
   if ((dim * isz) % 16) return fail(W, kBadArg, "feature row bytes must be a multiple of 16");
   if ((reinterpret_cast<uintptr_t>(feats) | reinterpret_cast<uintptr_t>(h_out)) & 15)
     return fail(W, kBadArg, "feature / output pointers must be 16-byte aligned");
   if (dim * isz > 16 * 32 * kMaxT) return fail(W, kBadArg, "feature rows above 2 KB are not supported");
+  if (scratch && scratch_bytes < hg_load_features_scratch_bytes(n_live_max))
+    return fail(W, kBadArg, "scratch too small");
   auto* g = reinterpret_cast<unsigned long long*>(global_ctr);
-  if (dtype == 0 && use_bulk_gather()) {
+  if (dtype == 0 && scratch && use_bulk_gather()) {
     const int row_bytes = dim * 4;
     int R = (kBulkSmem - 128) / (kBulkWarps * kBulkStages * row_bytes);
     if (R > 32) R = 32;
     if (R >= 1) {
+      const char** src_ptr = reinterpret_cast<const char**>((reinterpret_cast<uintptr_t>(scratch) + 15) & ~uintptr_t(15));
+      k_row_src<<<grid_for(n_live_max, 256), 256, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,
+                                                               static_cast<const char*>(region),
+                                                               static_cast<const char*>(feats), row_bytes, src_ptr, g);
+      HG_LAUNCHED(W);
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(k_load_rows_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
@@ -261,9 +285,8 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
       if (blocks > 148 * 2) blocks = 148 * 2;
       if (blocks < 1) blocks = 1;
       const size_t smem = 128 + (size_t)kBulkWarps * kBulkStages * R * row_bytes;
-      k_load_rows_bulk<<<(unsigned)blocks, kBulkWarps * 32, smem, stream>>>(
-          n_live_dev, live, src_nodes, feature_row_of, static_cast<const char*>(region),
-          static_cast<const char*>(feats), row_bytes, R, h_out, g);
+      k_load_rows_bulk<<<(unsigned)blocks, kBulkWarps * 32, smem, stream>>>(n_live_dev, live, src_ptr, row_bytes, R,
+                                                                              h_out);
       HG_LAUNCHED(W);
       return kOk;
     }

@@ -36,7 +36,7 @@ import torch
 
 from . import _lib
 from .nn import (Injection, build_csc, cross_entropy_dev, layer_backward_dev, layer_forward_dev,
-                 pack_dgrad_weights, sgd_step)
+                 load_features_dev, pack_dgrad_weights, sgd_step)
 from .sampler import SamplerWorkspace, SampleSlot, layer_bounds, pcg_words, sample_blocks_dev
 
 
@@ -286,9 +286,8 @@ class StepEngine:
         b0 = blocks[0]
         h = torch.empty((b0.num_src, tr.feature_dim), dtype=torch.float32, device=dev)
         region = cache.feature_table if cache.feature_table is not None else tr.features
-        _lib.call("hg_load_features", _lib.ptr(n_live_dev(0)), b0.num_src, _lib.ptr(live[0]), _lib.ptr(b0.src_nodes),
-                  _lib.ptr(cache.feature_row_of_dev), _lib.ptr(region), _lib.ptr(tr.features), tr.feature_dim,
-                  tr._dtype_code, _lib.ptr(h), _lib.ptr(cache.gctr), sp)
+        load_features_dev(n_live_dev(0), b0.num_src, live[0], b0.src_nodes, cache.feature_row_of_dev, region,
+                          tr.features, tr.feature_dim, tr._dtype_code, h, cache.gctr, sp)
 
         self._mark("loaded", stream)
         # ---- forward (nn.py:260-297) ----
@@ -325,7 +324,9 @@ class StepEngine:
                     cache._layer(l).update_dev(n_live_dev(l), blocks[l].num_src, live[l], blocks[l].src_nodes,
                                                norms[l], keep[l - 1], tapes[l - 1].h_out, self.it,
                                                cache.refresh_retained, _lib.stream_ptr(side),
-                                               allow_alloc=not self.capturing)
+                                               allow_alloc=not self.capturing,
+                                               mark=lambda what, l=l, side=side: self._mark(f"cache{l}_{what} (side)",
+                                                                                            side))
                     self._mark(f"cache_update{l} (side)", side)
         stream.wait_stream(self.wgrad_stream)
         if tr.grad_hook is not None:

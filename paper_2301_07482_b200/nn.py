@@ -230,6 +230,17 @@ class Injection:
     locals_dev: torch.Tensor | None = None
 
 
+def load_features_dev(n_live_dev, n_max: int, live, src_nodes, feature_row_of, region, feats, dim: int,
+                      dtype_code: int, out: torch.Tensor, gctr, stream) -> None:
+    """Layer-0 input rows (trainer.py:326-343) through hg_load_features with
+    a workspace (the TMA copy path for fp32 features)."""
+    sb = int(_lib.query("hg_load_features_scratch_bytes", max(int(n_max), 1)))
+    scratch = torch.empty(sb, dtype=torch.uint8, device=out.device)
+    _lib.call("hg_load_features", _lib.ptr(n_live_dev), n_max, _lib.ptr(live), _lib.ptr(src_nodes),
+              _lib.ptr(feature_row_of), _lib.ptr(region), _lib.ptr(feats), dim, dtype_code, _lib.ptr(out),
+              _lib.ptr(gctr), _lib.ptr(scratch), sb, stream)
+
+
 def _dev_count(n: int, dev) -> torch.Tensor:
     return torch.tensor([n], dtype=torch.int32, device=dev)
 

@@ -29,7 +29,7 @@ from .engine import StepEngine
 from .cache import COUNTER_NAMES, CachePolicy, HistCache
 from .graphs import Csr2Graph, _np, csr2_from_arrays
 from .nn import (Injection, LayerKind, Network, backward, cross_entropy_dev, forward_pass, init_network,
-                 layer_backward_dev, layer_forward_dev, sgd_step, _dev_count)
+                 layer_backward_dev, layer_forward_dev, load_features_dev, sgd_step, _dev_count)
 from .sampler import LayeredSubgraph, SamplePlan, SubgraphProducer, batch_rng, sample_layered, split_batches
 
 _NET_TAG = 16807
@@ -309,10 +309,9 @@ class Trainer:
         h = torch.empty((b0.num_src, self.feature_dim), dtype=torch.float32, device=dev)
         n_live0 = pruned.counts[0][1]
         region = self.cache.feature_table if self.cache.feature_table is not None else self.features
-        _lib.call("hg_load_features", _lib.ptr(pruned.n_live_dev(0)), n_live0, _lib.ptr(pruned.layer_live[0]),
-                  _lib.ptr(b0.src_nodes), _lib.ptr(self.cache.feature_row_of_dev), _lib.ptr(region),
-                  _lib.ptr(self.features), self.feature_dim, self._dtype_code, _lib.ptr(h),
-                  _lib.ptr(self.cache.gctr), sp)
+        load_features_dev(pruned.n_live_dev(0), n_live0, pruned.layer_live[0], b0.src_nodes,
+                          self.cache.feature_row_of_dev, region, self.features, self.feature_dim, self._dtype_code, h,
+                          self.cache.gctr, sp)
         return h, b0.num_src * self.row_bytes
 
     # --------------------------------------------------------- main loop
@@ -521,9 +520,8 @@ def run_plain_loop(graph, features, labels, train_ids, cfg: TrainConfig, num_cla
         b0 = sub.layers[0]
         h = torch.empty((b0.num_src, d), dtype=torch.float32, device=dev)
         live = torch.arange(b0.num_src, dtype=torch.int32, device=dev)
-        _lib.call("hg_load_features", _lib.ptr(_dev_count(b0.num_src, dev)), b0.num_src, _lib.ptr(live),
-                  _lib.ptr(b0.src_nodes), None, _lib.ptr(feats), _lib.ptr(feats), d, _dtype_code(feats),
-                  _lib.ptr(h), _lib.ptr(gctr), sp)
+        load_features_dev(_dev_count(b0.num_src, dev), b0.num_src, live, b0.src_nodes, None, feats, feats, d,
+                          _dtype_code(feats), h, gctr, sp)
         tape = forward_pass(network, sub.layers, h)
         labels_dev = torch.as_tensor(labels[seeds].astype(np.int32), device=dev)
         d_logits, loss = cross_entropy_dev(tape.logits.contiguous(), labels_dev, len(seeds), ncls, sp)
@@ -578,8 +576,7 @@ def full_graph_logits(network: Network, graph, features, chunk_rows: int | None 
     # layer-0 input as fp32 rows (the training feature gather, all nodes live)
     h = torch.empty((N, d0), dtype=torch.float32, device=dev)
     gctr = torch.zeros(8, dtype=torch.int64, device=dev)
-    _lib.call("hg_load_features", _lib.ptr(_dev_count(N, dev)), N, _lib.ptr(every), _lib.ptr(every), None,
-              _lib.ptr(feats), _lib.ptr(feats), d0, _dtype_code(feats), _lib.ptr(h), _lib.ptr(gctr), sp)
+    load_features_dev(_dev_count(N, dev), N, every, every, None, feats, feats, d0, _dtype_code(feats), h, gctr, sp)
     start = g.start.to(torch.int32)
     end = g.end.to(torch.int32)
     deg = (end - start).contiguous()

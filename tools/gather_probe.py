@@ -18,13 +18,14 @@ cnt = torch.tensor([n_live], dtype=torch.int32, device=dev)
 gctr = torch.zeros(8, dtype=torch.int64, device=dev)
 sp = _lib.stream_ptr()
 cudart = ctypes.CDLL("libcudart.so")
+ws = torch.empty(int(_lib.query("hg_load_features_scratch_bytes", n_src)), dtype=torch.uint8, device=dev)
 
 
 def run(dim, out_ptr, tag):
     feats = torch.randn(N, dim, device=dev)
     for _ in range(3):
         _lib.call("hg_load_features", _lib.ptr(cnt), n_src, _lib.ptr(live), _lib.ptr(src_nodes), None,
-                  _lib.ptr(feats), _lib.ptr(feats), dim, 0, out_ptr, _lib.ptr(gctr), sp)
+                  _lib.ptr(feats), _lib.ptr(feats), dim, 0, out_ptr, _lib.ptr(gctr), _lib.ptr(ws), ws.numel(), sp)
     torch.cuda.synchronize()
     print(tag, "done", flush=True)
 
