@@ -264,7 +264,7 @@ def main():
     # live layer-0 rows x (row read + fp32 row write + 3 index reads); the live
     # rows of the timed steps = delta(feature_hits + feature_misses)
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    peak, peak_src = 6551.4, "fallback"
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md: MEASURED_PEAKS.json absent)"
     if os.path.exists(peaks_path):
         peak, peak_src = json.load(open(peaks_path))["hbm_gbs"], "measured"
     tv = timers.view(8, 8).cpu().tolist()

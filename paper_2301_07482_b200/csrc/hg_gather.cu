@@ -8,9 +8,8 @@
 // matrix at their local frontier position. Non-live rows are not touched
 // (no kernel ever reads them).
 //
-// A warp owns groups of kRows rows; consecutive lanes read consecutive 16 B of
-// a row (coalesced 128-bit loads, no L1 allocation), and all loads of the group
-// are issued before any store (memory-level parallelism per warp = kRows rows).
+// Persistent warps copy batches of 32 rows as a flat stream of 128-bit
+// vectors (see k_load_rows); the bulk-copy (TMA engine) variant is opt-in.
 #include "hgb200.h"
 #include <cuda_fp16.h>
 #include <cstdlib>
@@ -30,83 +29,86 @@ int set_timers_gather(void* p) {
 }
 namespace {
 
-constexpr int kRows = 8;        // rows a warp keeps in flight
-constexpr int kMaxT = 4;        // 16-byte vectors per lane per row (rows <= 2 KB)
+constexpr int kWarps = 8;       // warps per CTA (256 threads)
 
-// One warp per group of kRows live rows. Lanes < kRows resolve the index chain
-// (live -> node id -> region row) for the whole group at once, then every lane
-// issues its 16-byte loads for all kRows rows before the first store, so each
-// warp has up to kRows * kMaxT independent 128-bit loads in flight.
-template <typename TIn, int kT>
-__global__ void __launch_bounds__(256, 4) k_load_rows(const int32_t* n_live_dev, const int32_t* __restrict__ live,
-                                                   const int32_t* __restrict__ src_nodes,
-                                                   const int32_t* __restrict__ feature_row_of,
-                                                   const TIn* __restrict__ region, const TIn* __restrict__ feats,
-                                                   int dim, float* __restrict__ out,
-                                                   unsigned long long* __restrict__ gctr) {
+// Persistent warps; a warp owns batches of 32 live rows (lane r resolves row
+// r's index chain live -> node id -> region row, 3 dependent loads). The rows
+// of a batch are copied as one flat stream of (row, 16-byte vector) pairs
+// spread over all 32 lanes, kU independent 128-bit loads per lane in flight
+// (8 for fp32, 6 for fp16 whose conversion needs registers),
+// so narrow rows (e.g. 100 fp32 = 25 vectors) keep every lane busy. The next
+// batch's index chain advances one dependent step per chunk of the current
+// batch, hiding its latency behind the row loads.
+template <typename TIn, int kU>
+__global__ void __launch_bounds__(kWarps * 32, 4) k_load_rows(const int32_t* n_live_dev, const int32_t* __restrict__ live,
+                                                           const int32_t* __restrict__ src_nodes,
+                                                           const int32_t* __restrict__ feature_row_of,
+                                                           const TIn* __restrict__ region,
+                                                           const TIn* __restrict__ feats, int dim,
+                                                           float* __restrict__ out,
+                                                           unsigned long long* __restrict__ gctr) {
   constexpr int kPerVec = 16 / sizeof(TIn);  // elements per 16-byte vector
+  __shared__ const TIn* s_row[kWarps][32];
+  __shared__ int s_loc[kWarps][32];
   const int nvec = dim / kPerVec;
   const int n = *n_live_dev;
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int W = (gridDim.x * blockDim.x) >> 5;
   KTimer* kt = g_kt ? g_kt + kTLoadRows : nullptr;
   kt_begin(kt);
-  // index chain (live -> node id -> region row) of a group, resolved by lanes < kRows
-  auto resolve = [&](int g, int& loc, const TIn*& row, bool& hit) {
-    const int i = g * kRows + lane;
-    loc = -1;
-    row = nullptr;
-    hit = false;
-    if (lane < kRows && i < n) {
-      loc = live[i];
-      const int id = src_nodes[loc];
-      const int fr = feature_row_of ? feature_row_of[id] : -1;
-      hit = fr >= 0;
-      row = hit ? region + (long long)fr * dim : feats + (long long)id * dim;
-    }
-  };
-  int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int loc;
-  const TIn* row;
-  bool hit;
-  resolve(g, loc, row, hit);
-  // software pipeline: the next group's index chain is in flight while this
-  // group's row loads complete
-  for (; g * kRows < n; g += warps) {
-    const unsigned hits = __ballot_sync(0xffffffffu, hit);
-    const unsigned valid = __ballot_sync(0xffffffffu, loc >= 0);
-    uint4 val[kRows][kT];
+  int b = blockIdx.x * kWarps + wib;
+  // index chain of this warp's first batch
+  int i = b * 32 + lane;
+  bool ok = i < n;
+  int loc = ok ? live[i] : 0;
+  int id = ok ? src_nodes[loc] : 0;
+  int fr = ok && feature_row_of ? feature_row_of[id] : -1;
+  for (; b * 32 < n; b += W) {
+    __syncwarp();
+    s_row[wib][lane] = fr >= 0 ? region + (long long)fr * dim : feats + (long long)id * dim;
+    s_loc[wib][lane] = loc;
+    const unsigned valid = __ballot_sync(0xffffffffu, ok);
+    const unsigned hits = __ballot_sync(0xffffffffu, ok && fr >= 0);
+    __syncwarp();
+    const int vtotal = __popc(valid) * nvec;  // valid rows are a prefix of the batch
+    // next batch: the chain advances one dependent load per chunk
+    i = (b + W) * 32 + lane;
+    ok = i < n;
+    int stage = 0;
+    for (int c0 = 0; c0 < vtotal; c0 += 32 * kU) {
+      uint4 val[kU];
+      int dst[kU];
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const TIn* p = reinterpret_cast<const TIn*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(row), r));
-#pragma unroll
-      for (int t = 0; t < kT; ++t) {
-        const int v = lane + 32 * t;
-        if (((valid >> r) & 1u) && v < nvec) val[r][t] = ldg_stream_u4(reinterpret_cast<const uint4*>(p) + v);
+      for (int t = 0; t < kU; ++t) {
+        const int k = c0 + t * 32 + lane;
+        dst[t] = -1;
+        if (k < vtotal) {
+          const int r = k / nvec, v = k - r * nvec;
+          val[t] = ldg_stream_u4(reinterpret_cast<const uint4*>(s_row[wib][r]) + v);
+          dst[t] = s_loc[wib][r] * nvec + v;   // output vector index (in input vectors)
+        }
       }
-    }
-    int cur_loc = loc;
-    resolve(g + warps, loc, row, hit);
+      if (stage == 0) loc = ok ? live[i] : 0;
+      else if (stage == 1) id = ok ? src_nodes[loc] : 0;
+      else if (stage == 2) fr = ok && feature_row_of ? feature_row_of[id] : -1;
+      ++stage;
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const int lr = __shfl_sync(0xffffffffu, cur_loc, r);
-      if (!((valid >> r) & 1u)) continue;
-      float* dst = out + (long long)lr * dim;
-#pragma unroll
-      for (int t = 0; t < kT; ++t) {
-        const int v = lane + 32 * t;
-        if (v >= nvec) continue;
+      for (int t = 0; t < kU; ++t) {
+        if (dst[t] < 0) continue;
         if (sizeof(TIn) == 4) {
-          reinterpret_cast<uint4*>(dst)[v] = val[r][t];
+          reinterpret_cast<uint4*>(out)[dst[t]] = val[t];
         } else {
-          const __half2* h = reinterpret_cast<const __half2*>(&val[r][t]);
-          float2 a = __half22float2(h[0]), b = __half22float2(h[1]);
+          const __half2* h = reinterpret_cast<const __half2*>(&val[t]);
+          float2 a = __half22float2(h[0]), bb = __half22float2(h[1]);
           float2 c = __half22float2(h[2]), d = __half22float2(h[3]);
-          reinterpret_cast<float4*>(dst)[2 * v] = make_float4(a.x, a.y, b.x, b.y);
-          reinterpret_cast<float4*>(dst)[2 * v + 1] = make_float4(c.x, c.y, d.x, d.y);
+          reinterpret_cast<float4*>(out)[2 * (long long)dst[t]] = make_float4(a.x, a.y, bb.x, bb.y);
+          reinterpret_cast<float4*>(out)[2 * (long long)dst[t] + 1] = make_float4(c.x, c.y, d.x, d.y);
         }
       }
     }
+    if (stage <= 0) loc = ok ? live[i] : 0;
+    if (stage <= 1) id = ok ? src_nodes[loc] : 0;
+    if (stage <= 2) fr = ok && feature_row_of ? feature_row_of[id] : -1;
     if (lane == 0) {
       if (hits) atomicAdd(gctr + kGCtrFeatureHits, (unsigned long long)__popc(hits));
       if (valid & ~hits) atomicAdd(gctr + kGCtrFeatureMisses, (unsigned long long)__popc(valid & ~hits));
@@ -261,7 +263,7 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
   if ((dim * isz) % 16) return fail(W, kBadArg, "feature row bytes must be a multiple of 16");
   if ((reinterpret_cast<uintptr_t>(feats) | reinterpret_cast<uintptr_t>(h_out)) & 15)
     return fail(W, kBadArg, "feature / output pointers must be 16-byte aligned");
-  if (dim * isz > 16 * 32 * kMaxT) return fail(W, kBadArg, "feature rows above 2 KB are not supported");
+  if ((long long)dim * isz / 16 * 32 >= (1ll << 31)) return fail(W, kBadArg, "feature rows too wide");
   if (scratch && scratch_bytes < hg_load_features_scratch_bytes(n_live_max))
     return fail(W, kBadArg, "scratch too small");
   auto* g = reinterpret_cast<unsigned long long*>(global_ctr);
@@ -291,17 +293,13 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
       return kOk;
     }
   }
-  const unsigned grid = grid_for((n_live_max + kRows - 1) / kRows * 32, 256, 148 * 8);
-  const int T = (dim * isz / 16 + 31) / 32;
-#define HG_LOAD(TT, KT)                                                                                     \
-  k_load_rows<TT, KT><<<grid, 256, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,               \
-                                                static_cast<const TT*>(region), static_cast<const TT*>(feats), \
-                                                dim, h_out, g)
-  if (dtype == 1) {
-    if (T == 1) HG_LOAD(__half, 1); else if (T == 2) HG_LOAD(__half, 2); else HG_LOAD(__half, 4);
-  } else {
-    if (T == 1) HG_LOAD(float, 1); else if (T == 2) HG_LOAD(float, 2); else HG_LOAD(float, 4);
-  }
+  // persistent: one wave of 4 CTAs per SM (or fewer when the batch is small)
+  const unsigned grid = grid_for((n_live_max + 31) / 32, kWarps, 148 * 4);
+#define HG_LOAD(TT, U)                                                                                            \
+  k_load_rows<TT, U><<<grid, kWarps * 32, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,                \
+                                                    static_cast<const TT*>(region), static_cast<const TT*>(feats), \
+                                                    dim, h_out, g)
+  if (dtype == 1) HG_LOAD(__half, 6); else HG_LOAD(float, 8);
 #undef HG_LOAD
   HG_LAUNCHED(W);
   return kOk;
