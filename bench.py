@@ -39,6 +39,9 @@ CONFIGS = {
     "c2": dict(workload="ogbn-products-shape synthetic power-law (2.4M nodes, 62.4M edges, 100-d fp32), "
                         "3-layer GraphSAGE hidden 256, fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
                n=2_400_000, m=13, d=100, classes=47),
+    "c3": dict(workload="ogbn-papers100M-shape synthetic power-law (111M nodes, 1.55B edges, 128-d fp16), "
+                        "3-layer GraphSAGE hidden 256, fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
+               n=111_000_000, m=7, d=128, classes=172, fp16=True, capacity=6_000_000, max_capacity=24_000_000),
     "c1": dict(workload="synthetic power-law 100K nodes / 2M edges, 128-d fp32, 3-layer GraphSAGE hidden 256, "
                         "fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
                n=100_000, m=10, d=128, classes=8),
@@ -47,15 +50,29 @@ FANOUTS, HIDDEN, BATCH, P_GRAD, T_STALE, ETA = (15, 10, 5), 256, 1024, 0.9, 20, 
 
 
 def make_data(cfg, seed=0):
-    """Native power-law graph (C++) + numpy N(0,1) features; identical for both arms."""
+    """Native power-law graph (C++) + numpy N(0,1) features; identical for both arms.
+    At the papers100M shape the features (28 GB fp16) are drawn on the device
+    instead (feats = None here, see device_features)."""
     from paper_2301_07482_b200.data import synth_edges
     src, dst = synth_edges(cfg["n"], cfg["m"], seed)
     rng = np.random.default_rng(seed)
-    feats = rng.standard_normal((cfg["n"], cfg["d"]), dtype=np.float32)
+    feats = None if cfg.get("fp16") else rng.standard_normal((cfg["n"], cfg["d"]), dtype=np.float32)
     labels = rng.integers(0, cfg["classes"], size=cfg["n"])
     perm = rng.permutation(cfg["n"])
     train = np.sort(perm[: int(0.6 * cfg["n"])])
     return src, dst, feats, labels, train
+
+
+def device_features(cfg, dev, seed=0, chunk=1 << 22):
+    """N(0,1) feature table drawn on the device in row chunks, stored fp16."""
+    import torch
+    out = torch.empty((cfg["n"], cfg["d"]), dtype=torch.float16, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    for a in range(0, cfg["n"], chunk):
+        b = min(cfg["n"], a + chunk)
+        out[a:b] = torch.randn((b - a, cfg["d"]), generator=gen, device=dev)
+    return out
 
 
 class ClockSampler:
@@ -190,12 +207,14 @@ def main():
     src, dst, feats, labels, train = data
     from paper_2301_07482_b200.data import csr2_from_edges_device
     graph = csr2_from_edges_device(src, dst, cfgd["n"], dev)
-    feats_dev = torch.from_numpy(feats).to(dev)
+    feats_dev = device_features(cfgd, dev) if feats is None else torch.from_numpy(feats).to(dev)
+    del src, dst
     n_tl = 10   # extra steps after the timed regions for the phase timeline
     need = (args.warmup + 2 * args.steps + n_tl + 1) * world
     per_epoch = -(-len(train) // BATCH)
     tcfg = hg.TrainConfig(fanouts=FANOUTS, hidden=HIDDEN, batch_size=BATCH, eta=ETA, kind=hg.LayerKind.SAGE_MEAN,
-                          p_grad=P_GRAD, t_stale=T_STALE, seed=0, epochs=max(1, -(-need // per_epoch)))
+                          p_grad=P_GRAD, t_stale=T_STALE, seed=0, epochs=max(1, -(-need // per_epoch)),
+                          capacity=cfgd.get("capacity"), max_capacity=cfgd.get("max_capacity"))
     tr = hg.Trainer(graph, feats_dev, labels, train, tcfg, cfgd["classes"])
     if world > 1:
         def allreduce(grads):
@@ -203,6 +222,7 @@ def main():
             grads.flat.div_(world)
         tr.grad_hook = allreduce
     batches = hg.make_batches(train, tcfg)
+    mem_setup = torch.cuda.memory_allocated(dev)
     if need > len(batches):
         raise SystemExit(f"need {need} batches, epoch has {len(batches)}")
     # rank r takes batch indices world*s + r (iteration number = global batch index)
@@ -323,7 +343,19 @@ def main():
                timeline_ms=timeline,
                loss_last=float(losses[-1].item()), io_saving_last=None)
     out["io_saving_e2e_last"] = 1.0 - m.fetched_bytes / m.baseline_bytes if m.baseline_bytes else None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    out["hbm_gb"] = {"allocated_after_setup": round(mem_setup / 1e9, 2),
+                     "peak": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2)}
+    if cfgd.get("capacity"):
+        config["cache_capacity_rows_per_layer"] = [cfgd["capacity"], cfgd["max_capacity"]]
+    if cfgd.get("fp16"):
+        out["dtype"] = "fp32 (fp16 feature table, converted in the gather)"
+        config["l2"] = "inputs > L2 (28 GB features + 6 GB graph resident, random rows)"
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfgd.get("fp16"):
+        out["cpu_baseline"] = {"value": None, "unit": "seeds/s", "cores": len(os.sched_getaffinity(0)),
+                               "kind": "port", "sample": "not run at the papers100M shape (the numpy port needs "
+                               "the 28 GB table and 12 GB graph in host RAM, minutes per iteration); "
+                               "see the C2 line for the CPU comparison"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_reference(cfgd, data, steps=3, warmup=1, budget_s=args.cpu_budget)
         out["cpu_baseline"] = {"value": r["value"], "unit": "seeds/s", "cores": r["cores"], "kind": "port",
                                "sample": r["sample"]}

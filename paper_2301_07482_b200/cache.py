@@ -43,11 +43,15 @@ def _it_dev(it: int, dev) -> torch.Tensor:
 class CachePolicy:
     """p_grad: admitted fraction per batch (smallest gradient norms first).
     t_stale: max age of a served entry in iterations; math.inf disables aging.
-    capacity: rows per layer table; None sizes each table on first use."""
+    capacity: rows per layer table; None sizes each table on first use.
+    max_capacity: growth limit (extension, not in the reference: None = N as in
+    cache.py:93-101); bounds HBM use at the papers100M shape, where doubling to
+    N rows of 1 KB would need 113 GB per layer."""
 
     p_grad: float
     t_stale: float
     capacity: int | None = None
+    max_capacity: int | None = None
 
     def __post_init__(self):
         if not 0.0 <= self.p_grad <= 1.0:
@@ -56,6 +60,8 @@ class CachePolicy:
             raise ValueError(f"t_stale must be >= 0 or inf, got {self.t_stale}")
         if self.capacity is not None and self.capacity < 1:
             raise ValueError("capacity must be >= 1 when given")
+        if self.max_capacity is not None and self.max_capacity < 1:
+            raise ValueError("max_capacity must be >= 1 when given")
 
 
 class _LayerCache:
@@ -146,9 +152,12 @@ class _LayerCache:
 
     def _grow(self):
         """cache.py:93-101 — double (up to N), rows kept in place."""
-        if self.table is None or self.capacity >= self.num_nodes:
+        limit = max(self.num_nodes, 1)
+        if self.policy.max_capacity is not None:
+            limit = min(limit, self.policy.max_capacity)
+        if self.table is None or self.capacity >= limit:
             return
-        new_cap = min(self.capacity * 2, max(self.num_nodes, 1))
+        new_cap = min(self.capacity * 2, limit)
         if new_cap > self.rows_alloc:   # out of headroom: reallocate (a captured graph is re-captured)
             rows = self._rows_for(new_cap)
             table = torch.zeros((rows, self.dim), dtype=self.dtype, device=self.device)

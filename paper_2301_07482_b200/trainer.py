@@ -63,6 +63,7 @@ class TrainConfig:
     dtype: type = np.float32
     # B200 additions (not in the reference): where the raw feature table lives
     feature_placement: str = "hbm"      # "hbm" | "host" (pinned, read through UVA)
+    max_capacity: int | None = None     # cache growth limit (see CachePolicy)
 
     def __post_init__(self):
         if len(self.fanouts) == 0 or any(f < 1 for f in self.fanouts):
@@ -277,7 +278,7 @@ class Trainer:
         depth = len(cfg.fanouts)
         dims = [self.feature_dim] + [cfg.hidden] * (depth - 1) + [self.num_classes]
         self.network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, self.device)
-        policy = CachePolicy(cfg.p_grad, cfg.t_stale, cfg.capacity)
+        policy = CachePolicy(cfg.p_grad, cfg.t_stale, cfg.capacity, cfg.max_capacity)
         feature_rows = self.graph.num_nodes // 10 if cfg.feature_rows is None else cfg.feature_rows
         self.cache = HistCache(self.graph.num_nodes, [cfg.hidden] * (depth - 1), policy, feature_rows=feature_rows,
                                refresh_retained=cfg.refresh_retained, dtype=cfg.dtype, device=self.device)
