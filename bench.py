@@ -63,15 +63,19 @@ def make_data(cfg, seed=0):
     return src, dst, feats, labels, train
 
 
-def device_features(cfg, dev, seed=0, chunk=1 << 22):
-    """N(0,1) feature table drawn on the device in row chunks, stored fp16."""
+def device_features(cfg, dev, seed=0, lo=0, hi=None, chunk=1 << 22):
+    """Rows [lo, hi) of the N(0,1) feature table, drawn on the device in row
+    chunks (chunk c from its own seeded generator, so every rank's shard is
+    the same slice of one table whatever the rank count), stored fp16."""
     import torch
-    out = torch.empty((cfg["n"], cfg["d"]), dtype=torch.float16, device=dev)
+    hi = cfg["n"] if hi is None else hi
+    out = torch.empty((hi - lo, cfg["d"]), dtype=torch.float16, device=dev)
     gen = torch.Generator(device=dev)
-    gen.manual_seed(seed)
-    for a in range(0, cfg["n"], chunk):
-        b = min(cfg["n"], a + chunk)
-        out[a:b] = torch.randn((b - a, cfg["d"]), generator=gen, device=dev)
+    for c in range(lo // chunk, -(-hi // chunk)):
+        a, b = c * chunk, min(cfg["n"], (c + 1) * chunk)
+        gen.manual_seed(seed * 1_000_003 + c)
+        x = torch.randn((b - a, cfg["d"]), generator=gen, device=dev)
+        out[max(a, lo) - lo:min(b, hi) - lo] = x[max(a, lo) - a:min(b, hi) - a]
     return out
 
 
@@ -169,6 +173,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--replicate-features", action="store_true",
+                    help="N>1: full feature table on every GPU instead of owner-range shards over NVLink")
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -198,16 +204,36 @@ def main():
     import paper_2301_07482_b200 as hg
     from paper_2301_07482_b200 import _lib
 
+    # HG_BENCH_ONE_GPU=1: every rank on cuda:0 over gloo (exercises the
+    # multi-rank path, IPC shards included, on a 1-GPU box; not a scaling run)
+    one_gpu = os.environ.get("HG_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     data = make_data(cfgd)
     src, dst, feats, labels, train = data
     from paper_2301_07482_b200.data import csr2_from_edges_device
     graph = csr2_from_edges_device(src, dst, cfgd["n"], dev)
-    feats_dev = device_features(cfgd, dev) if feats is None else torch.from_numpy(feats).to(dev)
+    sharded = world > 1 and not args.replicate_features
+    if sharded:
+        # this rank's owner range only (comms.py:329-337); peers mapped over NVLink
+        from paper_2301_07482_b200.distributed import owner_ranges
+        bnd = owner_ranges(cfgd["n"], world)
+        lo, hi = int(bnd[rank]), int(bnd[rank + 1])
+        local_rows = device_features(cfgd, dev, lo=lo, hi=hi) if feats is None else feats[lo:hi]
+        feats_dev = hg.ShardedFeatures.from_process_group(local_rows, cfgd["n"], rank, world, dev)
+        del local_rows
+    else:
+        feats_dev = device_features(cfgd, dev) if feats is None else torch.from_numpy(feats).to(dev)
+    config["features"] = (f"sharded {world}-way by owner range, remote rows read over NVLink (CUDA IPC)"
+                          if sharded else "replicated in HBM")
     del src, dst
     n_tl = 10   # extra steps after the timed regions for the phase timeline
     need = (args.warmup + 2 * args.steps + n_tl + 1) * world
@@ -217,10 +243,8 @@ def main():
                           capacity=cfgd.get("capacity"), max_capacity=cfgd.get("max_capacity"))
     tr = hg.Trainer(graph, feats_dev, labels, train, tcfg, cfgd["classes"])
     if world > 1:
-        def allreduce(grads):
-            dist.all_reduce(grads.flat)
-            grads.flat.div_(world)
-        tr.grad_hook = allreduce
+        from paper_2301_07482_b200.distributed import make_allreduce_hook
+        tr.grad_hook = make_allreduce_hook(world)   # NCCL: captured in the step's CUDA graph
     batches = hg.make_batches(train, tcfg)
     mem_setup = torch.cuda.memory_allocated(dev)
     if need > len(batches):
@@ -292,6 +316,7 @@ def main():
     per_kernel = {n: {"launches": int(tv[i][3]), "ms_total": tv[i][2] / 1e6,
                       "share_of_step": (tv[i][2] / 1e9) / t_dev} for i, n in enumerate(names)}
     g_delta = (tr.cache.gctr - g_before).cpu().tolist()
+    remote_rows = g_delta[3]
     rows = g_delta[0] + g_delta[1]
     isz = tr.features.element_size()
     g_bytes = rows * (cfgd["d"] * isz + cfgd["d"] * 4 + 12)
@@ -337,7 +362,10 @@ def main():
     eng.enable_timeline(False)
     timeline = {k: round(v, 4) for k, v in acc.items()}
 
-    out = dict(base, value=value, ms_per_step=1e3 * t_dev / args.steps, e2e=e2e, roofline=roofline,
+    row_b = cfgd["d"] * tr.features.element_size()
+    nvlink = {"remote_rows_per_step": remote_rows / args.steps, "bytes_per_step": remote_rows * row_b / args.steps,
+              "share_of_gathered_rows": remote_rows / max(1, g_delta[0] + g_delta[1])}
+    out = dict(base, value=value, nvlink_gather=nvlink, ms_per_step=1e3 * t_dev / args.steps, e2e=e2e, roofline=roofline,
                gpu_launches=int(launches), clocks=clk, per_kernel=per_kernel, cuda_graph=graph_mode,
                graph_captures_in_timed={"value": caps_value, "e2e": caps_e2e},
                timeline_ms=timeline,
@@ -361,6 +389,11 @@ def main():
                                "sample": r["sample"]}
     if rank == 0:
         print(json.dumps(out))
+    if sharded:
+        torch.cuda.synchronize()
+        barrier()
+        del tr
+        feats_dev.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 

@@ -89,6 +89,25 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
                      float* h_out, long long* global_ctr, void* scratch, long long scratch_bytes,
                      cudaStream_t stream);
 
+/* Sharded feature table: miss rows of node id are read from
+ * shard o with bounds[o] <= id < bounds[o+1] at shard_ptrs[o] + (id - bounds[o])
+ * * dim; shard_ptrs (device array [P], P <= 16) may hold CUDA-IPC mappings of
+ * peer GPUs' shards (one-sided NVLink reads). Partition as
+ * comms.py:329-337 (partition_features). Rows from shards != local_shard are
+ * counted in global_ctr[3]. */
+int hg_load_features_sharded(const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
+                             const int32_t* src_nodes, const int32_t* feature_row_of, const void* region,
+                             const void* const* shard_ptrs, const long long* shard_bounds, int num_shards,
+                             int local_shard, int dim, int dtype, float* h_out, long long* global_ctr,
+                             cudaStream_t stream);
+/* shard allocation and CUDA IPC export/open/close of peer shards */
+int hg_device_alloc(long long bytes, void** out);
+int hg_device_free(void* p);
+long long hg_ipc_handle_bytes(void);
+int hg_ipc_export(void* p, void* handle_out);
+int hg_ipc_open(const void* handle, void** out);
+int hg_ipc_close(void* p);
+
 /* ---- K6 block aggregation: histgnn/nn.py:101-128,142-156 (_gcn_matrix,
  * _mean_matrix, _layer_forward_ctx). kind 0 = GCN, 1 = SAGE_MEAN. */
 int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,

@@ -12,6 +12,7 @@ from . import _lib  # noqa: F401
 from .cache import CachePolicy, HistCache  # noqa: F401
 from .graphs import CooGraph, Csr2Graph, build_csr2, csr2_from_arrays  # noqa: F401
 from .nn import LayerKind, backward, cross_entropy, forward_pass, init_network, node_grad_norms, sgd_step  # noqa: F401
+from .sharding import ShardedFeatures  # noqa: F401
 from .sampler import (LayerBlock, LayeredSubgraph, SamplePlan, SubgraphProducer, batch_rng,  # noqa: F401
                       sample_layered, split_batches)
 from .trainer import (IterMetrics, PrunedBatch, TrainConfig, Trainer, evaluate, full_graph_logits, io_saving,  # noqa: F401

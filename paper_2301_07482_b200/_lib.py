@@ -40,6 +40,13 @@ SIGNATURES = {
     "hg_cache_lookup": (I32, [P, I64, P, P, I64, P, P, P, P, F64, P, P, P, P]),
     "hg_load_features_scratch_bytes": (I64, [I64]),
     "hg_load_features": (I32, [P, I64, P, P, P, P, P, I32, I32, P, P, P, I64, P]),
+    "hg_load_features_sharded": (I32, [P, I64, P, P, P, P, P, P, I32, I32, I32, I32, P, P, P]),
+    "hg_device_alloc": (I32, [I64, P]),
+    "hg_device_free": (I32, [P]),
+    "hg_ipc_handle_bytes": (I64, []),
+    "hg_ipc_export": (I32, [P, P]),
+    "hg_ipc_open": (I32, [P, P]),
+    "hg_ipc_close": (I32, [P]),
     "hg_aggregate_fwd": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, P, P]),
     "hg_gemm_rm": (I32, [I32, I32, I64, I64, I64, P, I64, P, I64, F32, P, I64, P]),
     "hg_scatter_rows": (I32, [P, I64, P, P, I32, I32, P, P]),

@@ -359,7 +359,8 @@ class HistCache:
         scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
         _lib.call("hg_feature_region", _lib.ptr(start), _lib.ptr(end), n, k, _lib.ptr(chosen),
                   _lib.ptr(self.feature_row_of_dev), _lib.ptr(scratch), sb, _lib.stream_ptr())
-        feats = features if isinstance(features, torch.Tensor) else torch.as_tensor(np.asarray(features))
+        feats = (features if isinstance(features, torch.Tensor) or hasattr(features, "index_select")
+                 else torch.as_tensor(np.asarray(features)))
         self.feature_dim = int(feats.shape[1])
         if feats.device.type == "cuda":
             self.feature_table = feats.index_select(0, chosen[:k].long()).contiguous()

@@ -39,17 +39,36 @@ constexpr int kWarps = 8;       // warps per CTA (256 threads)
 // so narrow rows (e.g. 100 fp32 = 25 vectors) keep every lane busy. The next
 // batch's index chain advances one dependent step per chunk of the current
 // batch, hiding its latency behind the row loads.
-template <typename TIn, int kU>
+// Sharded source: the miss rows live in P owner shards, shard o
+// holding nodes [bounds[o], bounds[o+1]) (histgnn/comms.py:329-337 contiguous
+// partition); shard pointers may be peer-GPU memory mapped over NVLink (CUDA
+// IPC), so a miss is a one-sided P2P read by the loading GPU.
+struct Shards {
+  const void* const* ptr;     // device array [P]
+  const long long* bounds;    // device array [P + 1]
+  int P;
+  int local;                  // index of this GPU's own shard (remote-row accounting)
+};
+constexpr int kMaxShards = 16;
+
+template <typename TIn, int kU, bool kShard>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_load_rows(const int32_t* n_live_dev, const int32_t* __restrict__ live,
                                                            const int32_t* __restrict__ src_nodes,
                                                            const int32_t* __restrict__ feature_row_of,
                                                            const TIn* __restrict__ region,
                                                            const TIn* __restrict__ feats, int dim,
                                                            float* __restrict__ out,
-                                                           unsigned long long* __restrict__ gctr) {
+                                                           unsigned long long* __restrict__ gctr, Shards sh) {
   constexpr int kPerVec = 16 / sizeof(TIn);  // elements per 16-byte vector
   __shared__ const TIn* s_row[kWarps][32];
   __shared__ int s_loc[kWarps][32];
+  __shared__ const TIn* s_shard[kMaxShards];
+  __shared__ long long s_bound[kMaxShards + 1];
+  if (kShard) {
+    if (threadIdx.x < sh.P) s_shard[threadIdx.x] = static_cast<const TIn*>(sh.ptr[threadIdx.x]);
+    if (threadIdx.x <= sh.P) s_bound[threadIdx.x] = sh.bounds[threadIdx.x];
+    __syncthreads();
+  }
   const int nvec = dim / kPerVec;
   const int n = *n_live_dev;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -65,10 +84,23 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_load_rows(const int32_t* n_l
   int fr = ok && feature_row_of ? feature_row_of[id] : -1;
   for (; b * 32 < n; b += W) {
     __syncwarp();
-    s_row[wib][lane] = fr >= 0 ? region + (long long)fr * dim : feats + (long long)id * dim;
+    bool remote = false;
+    if (kShard) {
+      const TIn* src = region + (long long)fr * dim;
+      if (fr < 0) {
+        int o = 0;
+        while (o + 1 < sh.P && id >= s_bound[o + 1]) ++o;
+        src = s_shard[o] + (long long)(id - s_bound[o]) * dim;
+        remote = ok && o != sh.local;
+      }
+      s_row[wib][lane] = src;
+    } else {
+      s_row[wib][lane] = fr >= 0 ? region + (long long)fr * dim : feats + (long long)id * dim;
+    }
     s_loc[wib][lane] = loc;
     const unsigned valid = __ballot_sync(0xffffffffu, ok);
     const unsigned hits = __ballot_sync(0xffffffffu, ok && fr >= 0);
+    const unsigned remotes = kShard ? __ballot_sync(0xffffffffu, remote) : 0u;
     __syncwarp();
     const int vtotal = __popc(valid) * nvec;  // valid rows are a prefix of the batch
     // next batch: the chain advances one dependent load per chunk
@@ -112,6 +144,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_load_rows(const int32_t* n_l
     if (lane == 0) {
       if (hits) atomicAdd(gctr + kGCtrFeatureHits, (unsigned long long)__popc(hits));
       if (valid & ~hits) atomicAdd(gctr + kGCtrFeatureMisses, (unsigned long long)__popc(valid & ~hits));
+      if (remotes) atomicAdd(gctr + kGCtrRemoteRows, (unsigned long long)__popc(remotes));
     }
   }
   kt_end(kt);
@@ -296,13 +329,77 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
   // persistent: one wave of 4 CTAs per SM (or fewer when the batch is small)
   const unsigned grid = grid_for((n_live_max + 31) / 32, kWarps, 148 * 4);
 #define HG_LOAD(TT, U)                                                                                            \
-  k_load_rows<TT, U><<<grid, kWarps * 32, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,                \
+  k_load_rows<TT, U, false><<<grid, kWarps * 32, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,         \
                                                     static_cast<const TT*>(region), static_cast<const TT*>(feats), \
-                                                    dim, h_out, g)
+                                                    dim, h_out, g, Shards{nullptr, nullptr, 0, 0})
   if (dtype == 1) HG_LOAD(__half, 6); else HG_LOAD(float, 8);
 #undef HG_LOAD
   HG_LAUNCHED(W);
   return kOk;
+}
+
+// Sharded feature table: misses are read from shard o = owner(id) at
+// shard_ptrs[o] + (id - bounds[o]) * dim (peer HBM over NVLink when the
+// pointer is an IPC mapping of another GPU's shard). Region hits are local.
+int hg_load_features_sharded(const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
+                             const int32_t* src_nodes, const int32_t* feature_row_of, const void* region,
+                             const void* const* shard_ptrs, const long long* shard_bounds, int num_shards,
+                             int local_shard, int dim, int dtype, float* h_out, long long* global_ctr,
+                             cudaStream_t stream) {
+  const char* W = "hg_load_features_sharded";
+  const int isz = dtype == 1 ? 2 : 4;
+  if ((dim * isz) % 16) return fail(W, kBadArg, "feature row bytes must be a multiple of 16");
+  if (num_shards < 1 || num_shards > kMaxShards) return fail(W, kBadArg, "num_shards must be in [1, 16]");
+  if (!shard_ptrs || !shard_bounds) return fail(W, kBadArg, "shard tables must be given");
+  if (reinterpret_cast<uintptr_t>(h_out) & 15) return fail(W, kBadArg, "output must be 16-byte aligned");
+  auto* g = reinterpret_cast<unsigned long long*>(global_ctr);
+  const unsigned grid = grid_for((n_live_max + 31) / 32, kWarps, 148 * 4);
+  const Shards sh{shard_ptrs, shard_bounds, num_shards, local_shard};
+  if (dtype == 1)
+    k_load_rows<__half, 6, true><<<grid, kWarps * 32, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,
+                                                                  static_cast<const __half*>(region), nullptr, dim,
+                                                                  h_out, g, sh);
+  else
+    k_load_rows<float, 8, true><<<grid, kWarps * 32, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,
+                                                                 static_cast<const float*>(region), nullptr, dim,
+                                                                 h_out, g, sh);
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+// ---- shard memory + CUDA IPC (one-sided NVLink access to peer shards) ----
+int hg_device_alloc(long long bytes, void** out) {
+  if (!out || bytes < 1) return fail("hg_device_alloc", kBadArg, "bad arguments");
+  cudaError_t e = cudaMalloc(out, (size_t)bytes);
+  return e == cudaSuccess ? kOk : fail("hg_device_alloc", kCuda, cudaGetErrorString(e));
+}
+
+int hg_device_free(void* p) {
+  cudaError_t e = cudaFree(p);
+  return e == cudaSuccess ? kOk : fail("hg_device_free", kCuda, cudaGetErrorString(e));
+}
+
+long long hg_ipc_handle_bytes(void) { return (long long)sizeof(cudaIpcMemHandle_t); }
+
+// handle_out: hg_ipc_handle_bytes() bytes; p must be the base of a cudaMalloc allocation
+int hg_ipc_export(void* p, void* handle_out) {
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) return fail("hg_ipc_export", kCuda, cudaGetErrorString(e));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return kOk;
+}
+
+int hg_ipc_open(const void* handle, void** out) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? kOk : fail("hg_ipc_open", kCuda, cudaGetErrorString(e));
+}
+
+int hg_ipc_close(void* p) {
+  cudaError_t e = cudaIpcCloseMemHandle(p);
+  return e == cudaSuccess ? kOk : fail("hg_ipc_close", kCuda, cudaGetErrorString(e));
 }
 
 }  // extern "C"

@@ -28,6 +28,7 @@ enum GlobalCtr : int {
   kGCtrFeatureHits = 0,
   kGCtrFeatureMisses = 1,
   kGCtrPruneWrites = 2,
+  kGCtrRemoteRows = 3,       // feature rows read from a peer GPU's shard
   kGlobalCtrLen = 8,
 };
 

@@ -46,4 +46,8 @@ def make_allreduce_hook(world: int, group=None):
         dist.all_reduce(flat, group=group)
         flat.div_(world)
 
+    # NCCL collectives are stream-ordered device work and can be captured in
+    # the step's CUDA graph (engine.StepEngine); gloo's host-side all-reduce
+    # cannot, so a gloo hook keeps the step eager
+    hook.graph_safe = dist.get_backend(group) == "nccl"
     return hook

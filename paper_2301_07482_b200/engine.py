@@ -349,7 +349,8 @@ class StepEngine:
                 None if self.timeline is None else self.timeline.data_ptr())
 
     def _graphable(self) -> bool:
-        return (self.tr.use_graphs and self.tr.grad_hook is None
+        hook = self.tr.grad_hook
+        return (self.tr.use_graphs and (hook is None or getattr(hook, "graph_safe", False))
                 and all(lc.table is not None for lc in self.tr.cache.layers.values()))
 
     def _capture(self, s: int, ahead: bool) -> _Graph:

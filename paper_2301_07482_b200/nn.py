@@ -234,6 +234,10 @@ def load_features_dev(n_live_dev, n_max: int, live, src_nodes, feature_row_of, r
                       dtype_code: int, out: torch.Tensor, gctr, stream) -> None:
     """Layer-0 input rows (trainer.py:326-343) through hg_load_features with
     a workspace (the TMA copy path for fp32 features)."""
+    if hasattr(feats, "load_rows"):   # sharding.ShardedFeatures (peer shards over NVLink)
+        feats.load_rows(n_live_dev, n_max, live, src_nodes, feature_row_of,
+                        region if feature_row_of is not None else None, out, gctr, stream)
+        return
     sb = int(_lib.query("hg_load_features_scratch_bytes", max(int(n_max), 1)))
     scratch = torch.empty(sb, dtype=torch.uint8, device=out.device)
     _lib.call("hg_load_features", _lib.ptr(n_live_dev), n_max, _lib.ptr(live), _lib.ptr(src_nodes),

@@ -30,6 +30,7 @@ from .cache import COUNTER_NAMES, CachePolicy, HistCache
 from .graphs import Csr2Graph, _np, csr2_from_arrays
 from .nn import (Injection, LayerKind, Network, backward, cross_entropy_dev, forward_pass, init_network,
                  layer_backward_dev, layer_forward_dev, load_features_dev, sgd_step, _dev_count)
+from .sharding import ShardedFeatures
 from .sampler import LayeredSubgraph, SamplePlan, SubgraphProducer, batch_rng, sample_layered, split_batches
 
 _NET_TAG = 16807
@@ -248,6 +249,8 @@ def _device_graph(graph) -> Csr2Graph:
 
 
 def _dtype_code(t: torch.Tensor) -> int:
+    if isinstance(t, ShardedFeatures):
+        return t.dtype_code
     if t.dtype == torch.float16:
         return 1
     if t.dtype == torch.float32:
@@ -264,11 +267,15 @@ class Trainer:
         self.labels = np.asarray(labels, dtype=np.int64)
         self.train_ids = np.asarray(train_ids, dtype=np.int64)
         self.num_classes = int(num_classes or self.labels.max() + 1)
-        if isinstance(features, torch.Tensor):
+        if isinstance(features, ShardedFeatures):
+            feats = features        # owner-range shards, peers mapped over NVLink (sharding.py)
+        elif isinstance(features, torch.Tensor):
             feats = features
         else:
             feats = torch.from_numpy(np.ascontiguousarray(features))
-        if cfg.feature_placement == "hbm":
+        if isinstance(feats, ShardedFeatures):
+            pass
+        elif cfg.feature_placement == "hbm":
             feats = feats.to(self.device)
         elif feats.device.type != "cpu" or not feats.is_pinned():
             feats = feats.cpu().pin_memory()

@@ -68,3 +68,40 @@ def test_two_rank_dp_on_one_gpu(tmp_path):
         m = metrics[r][0]
         np.testing.assert_array_equal(got[:5], [m.hits, m.misses, m.admissions, m.fetched_bytes, m.prune_writes])
         assert abs(got[5] - m.loss) <= 1e-3 * abs(m.loss)
+
+
+def _nccl_worker(rank, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    import paper_2301_07482_b200 as hg
+    from paper_2301_07482_b200.distributed import make_allreduce_hook
+    ds, g = _data()
+    cfg = hg.TrainConfig(fanouts=(6, 4, 3), hidden=16, batch_size=96, epochs=1, eta=0.05,
+                         kind=hg.LayerKind.SAGE_MEAN, p_grad=0.9, t_stale=3, seed=5)
+    out = []
+    for hooked in (False, True):
+        tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
+        if hooked:
+            tr.grad_hook = make_allreduce_hook(1)
+            assert tr.grad_hook.graph_safe
+        batches = hg.make_batches(ds.train_ids, cfg)
+        losses = [tr.train_step(i, 0, batches[i], next_batch=(i + 1, batches[i + 1])).loss for i in range(8)]
+        caps = sum(e.captures for e in tr._engines.values())
+        out.append((losses, caps, np.frombuffer(tr.network.checksum_bytes(), np.uint8)))
+    np.save(os.path.join(out_dir, "losses.npy"), np.array([o[0] for o in out]))
+    np.save(os.path.join(out_dir, "caps.npy"), np.array([o[1] for o in out]))
+    np.save(os.path.join(out_dir, "w.npy"), np.stack([o[2] for o in out]))
+    dist.destroy_process_group()
+
+
+def test_nccl_allreduce_is_captured_in_the_step_graph(tmp_path):
+    """A single-rank NCCL group: the all-reduce hook is recorded inside the
+    step's CUDA graph (the N>1 bench path) and changes nothing numerically."""
+    mp.start_processes(_nccl_worker, args=(_free_port(), str(tmp_path)), nprocs=1, join=True, start_method="spawn")
+    caps = np.load(tmp_path / "caps.npy")
+    assert caps[1] >= 1, "the hooked trainer never captured a CUDA graph"
+    losses = np.load(tmp_path / "losses.npy")
+    np.testing.assert_array_equal(losses[0], losses[1])
+    w = np.load(tmp_path / "w.npy")
+    np.testing.assert_array_equal(w[0], w[1])
