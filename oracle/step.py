@@ -22,10 +22,11 @@ from dataclasses import dataclass, field, fields
 import numpy as np
 import scipy.sparse as sp
 
+from . import gat as ogat
 from .histcache import OCachePolicy, OHistCache
 from .sampling import OBlock, OSubgraph, _segment_positions, batch_rng, sample_layered, split_batches
 
-GCN, SAGE = "gcn", "sage_mean"
+GCN, SAGE, GAT = "gcn", "sage_mean", "gat"
 NET_TAG, PERM_TAG = 16807, 1000000007
 
 
@@ -62,9 +63,15 @@ class ONetwork:
         return b"".join(np.ascontiguousarray(a).tobytes() for l in self.layers for a in l.arrays())
 
 
-def init_network(kind, dims, rng, dtype=np.float32):
-    """nn.py:73-85 — Glorot-uniform, self weight drawn before neighbour weight."""
+def init_network(kind, dims, rng, dtype=np.float32, heads=4):
+    """nn.py:73-85 — Glorot-uniform, self weight drawn before neighbour weight.
+    GAT (no reference, oracle/gat.py): `heads` on hidden layers, 1 on the last."""
     out = []
+    if kind == GAT:
+        L = len(dims) - 1
+        for l, (fi, fo) in enumerate(zip(dims[:-1], dims[1:])):
+            out.append(ogat.init_layer(rng, fi, fo, heads if l < L - 1 else 1, dtype))
+        return ONetwork(kind, out)
     for fi, fo in zip(dims[:-1], dims[1:]):
         lim = np.sqrt(6.0 / (fi + fo))
         w = rng.uniform(-lim, lim, size=(fi, fo)).astype(dtype)
@@ -209,6 +216,8 @@ def _agg_operator(kind, blk, rows, dtype):
 def layer_forward_ctx(kind, p: OLayer, blk, h_in, rows, act):
     if h_in.shape[0] != blk.num_src:
         raise ValueError(f"h_in has {h_in.shape[0]} rows, frontier needs {blk.num_src}")
+    if kind == GAT:
+        return ogat.layer_forward(p, blk, h_in, rows, act)
     A = _agg_operator(kind, blk, rows, h_in.dtype)
     agg = A @ h_in
     if kind == GCN:
@@ -225,6 +234,8 @@ def layer_forward_ctx(kind, p: OLayer, blk, h_in, rows, act):
 
 
 def layer_backward(kind, p: OLayer, t: OTape, d_out, need_input=True):
+    if kind == GAT:
+        return ogat.layer_backward(p, t, d_out, need_input)
     dz = d_out if t.relu is None else np.where(t.relu, d_out, 0)
     db = dz.sum(axis=0)
     if kind == GCN:
@@ -307,8 +318,11 @@ def sgd_step(net: ONetwork, grads, eta):
     for p, g in zip(net.layers, grads):
         p.weight -= e * g.weight
         p.bias -= e * g.bias
-        if p.weight_neigh is not None:
+        if getattr(p, "weight_neigh", None) is not None:
             p.weight_neigh -= e * g.weight_neigh
+        if net.kind == GAT:
+            p.att_src -= e * g.att_src
+            p.att_dst -= e * g.att_dst
 
 
 # ----------------------------------------------------------------- trainer
@@ -329,6 +343,7 @@ class OTrainConfig:
     refresh_retained: bool = False
     seed: int = 0
     dtype: type = np.float32
+    heads: int = 4          # GAT hidden-layer heads (oracle/gat.py)
 
 
 @dataclass
@@ -376,7 +391,7 @@ class OTrainer:
         self.num_classes = int(num_classes or self.labels.max() + 1)
         depth = len(cfg.fanouts)
         dims = [features.shape[1]] + [cfg.hidden] * (depth - 1) + [self.num_classes]
-        self.network = init_network(cfg.kind, dims, network_rng(cfg.seed), cfg.dtype)
+        self.network = init_network(cfg.kind, dims, network_rng(cfg.seed), cfg.dtype, cfg.heads)
         frows = self.num_nodes // 10 if cfg.feature_rows is None else cfg.feature_rows
         self.cache = OHistCache(self.num_nodes, [cfg.hidden] * (depth - 1),
                                 OCachePolicy(cfg.p_grad, cfg.t_stale, cfg.capacity),
@@ -446,7 +461,7 @@ def run_plain_loop(graph, features, labels, train_ids, cfg: OTrainConfig, num_cl
     ncls = int(num_classes or labels.max() + 1)
     depth = len(cfg.fanouts)
     dims = [features.shape[1]] + [cfg.hidden] * (depth - 1) + [ncls]
-    net = init_network(cfg.kind, dims, network_rng(cfg.seed), cfg.dtype)
+    net = init_network(cfg.kind, dims, network_rng(cfg.seed), cfg.dtype, cfg.heads)
     losses = []
     for idx, seeds in enumerate(make_batches(np.asarray(train_ids, np.int64), cfg)):
         sub = sample_layered(start, end, col, len(start), seeds, cfg.fanouts, batch_rng(cfg.seed, idx))
