@@ -1,0 +1,485 @@
+// GAT block layer (BASELINE config 5). The reference has no
+// GAT (histgnn/nn.py:28-30); the layer is defined by the CPU restatement in
+// oracle/gat.py (dense + finite-difference pinned) and these kernels follow
+// it step for step:
+//   z = h_in[live] @ W                      tcgen05 GEMM (hg_ts_linear_fwd, rows = live)
+//   el/er = per-head <z, a_src> / <z, a_dst> k_gat_scores (warp per live row)
+//   softmax over surviving in-edges + self  k_gat_aggregate (warp per compute row,
+//     + bias, ReLU, scatter to h_out[rows])   two passes: max, then exp-sum + weighted sum)
+//   backward, per compute row i:            k_gat_bwd_dst: gz (ReLU-masked grad),
+//                                             c_i = sum_j a_ij da_ij, der_i = sum_j ds_ij
+//   backward, per live source j (CSC):      k_gat_bwd_src: dz_j = sum_i a_ij gz_i
+//                                             + del_j a_src (+ der_j a_dst if j computes),
+//                                             emitted as a TS operand for the dgrad / wgrad GEMMs
+//   parameter vectors (a_src, a_dst, bias): k_gat_param_partial + k_gat_param_sum
+//                                             (fixed-order two-level column sums)
+//   d_in rows + fp64 node-gradient norms:   k_gat_scatter_norms
+// No atomics on floats anywhere: every run is bit-identical.
+#include "hgb200.h"
+
+#include "hg_common.cuh"
+#include "hg_ts.cuh"
+
+namespace hg {
+namespace {
+
+constexpr int kMaxH = 8;
+constexpr float kSlope = 0.2f;
+
+__device__ __forceinline__ float leaky(float x) { return x > 0.f ? x : kSlope * x; }
+__device__ __forceinline__ float leaky_d(float x) { return x > 0.f ? 1.f : kSlope; }
+
+// per-head warp sums of per-lane partials (fixed shuffle tree)
+template <int kH>
+__device__ __forceinline__ void warp_sum_heads(float (&p)[kH]) {
+#pragma unroll
+  for (int h = 0; h < kH; ++h) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p[h] += __shfl_xor_sync(0xffffffffu, p[h], o);
+  }
+}
+
+// el[j*H + h] = <z[j, hF:(h+1)F], a_src[hF:(h+1)F]>, er likewise with a_dst
+template <int kT>
+__global__ void __launch_bounds__(256) k_gat_scores(const int32_t* n_dev, const int32_t* __restrict__ live,
+                                                    const float* __restrict__ z, int HF, int H, int F,
+                                                    const float* __restrict__ a_src, const float* __restrict__ a_dst,
+                                                    float* __restrict__ el, float* __restrict__ er) {
+  const int n = *n_dev;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const int j = live[i];
+    float pl[kMaxH], pr[kMaxH];
+#pragma unroll
+    for (int h = 0; h < kMaxH; ++h) pl[h] = pr[h] = 0.f;
+#pragma unroll
+    for (int t = 0; t < kT; ++t) {
+      const int c = lane + 32 * t;
+      if (c < HF) {
+        const float x = z[(long long)j * HF + c];
+        const int h = c / F;
+#pragma unroll
+        for (int q = 0; q < kMaxH; ++q)
+          if (q == h) {
+            pl[q] = __fmaf_rn(x, a_src[c], pl[q]);
+            pr[q] = __fmaf_rn(x, a_dst[c], pr[q]);
+          }
+      }
+    }
+    warp_sum_heads<kMaxH>(pl);
+    warp_sum_heads<kMaxH>(pr);
+#pragma unroll
+    for (int q = 0; q < kMaxH; ++q)
+      if (lane == q && q < H) {
+        el[(long long)j * H + q] = pl[q];
+        er[(long long)j * H + q] = pr[q];
+      }
+  }
+}
+
+// value of head h held by lane h of `v` (lanes < H hold one head each)
+__device__ __forceinline__ float head_val(float v, int h) { return __shfl_sync(0xffffffffu, v, h); }
+
+template <int kT>
+__global__ void __launch_bounds__(256) k_gat_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
+                                                       const int32_t* __restrict__ start, const int32_t* __restrict__ end,
+                                                       const int32_t* __restrict__ col, const float* __restrict__ z,
+                                                       const float* __restrict__ el, const float* __restrict__ er,
+                                                       int HF, int H, int F, const float* __restrict__ bias, int relu,
+                                                       float* __restrict__ h_out, float* __restrict__ mx,
+                                                       float* __restrict__ ssum) {
+  const int R = *R_dev;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += warps) {
+    const int i = rows[r];
+    const int e0 = start[i], e1 = end[i];
+    const float eri = lane < H ? er[(long long)i * H + lane] : 0.f;
+    // pass 1: per-head max of the attention logits (edges, then the self loop)
+    float m = -INFINITY;
+    for (int e = e0; e <= e1; ++e) {
+      const int j = e < e1 ? col[e] : i;
+      if (lane < H) m = fmaxf(m, leaky(el[(long long)j * H + lane] + eri));
+    }
+    // pass 2: exp-weights, their sum and the weighted sum of z rows
+    float s = 0.f;
+    float acc[kT];
+#pragma unroll
+    for (int t = 0; t < kT; ++t) acc[t] = 0.f;
+    for (int e = e0; e <= e1; ++e) {
+      const int j = e < e1 ? col[e] : i;
+      const float w = lane < H ? expf(leaky(el[(long long)j * H + lane] + eri) - m) : 0.f;
+      s += w;
+      const float* zj = z + (long long)j * HF;
+#pragma unroll
+      for (int t = 0; t < kT; ++t) {
+        const int c = lane + 32 * t;
+        const float wh = head_val(w, c < HF ? c / F : 0);
+        if (c < HF) acc[t] = __fmaf_rn(wh, zj[c], acc[t]);
+      }
+    }
+    float* out = h_out + (long long)i * HF;
+#pragma unroll
+    for (int t = 0; t < kT; ++t) {
+      const int c = lane + 32 * t;
+      const float sh = head_val(s, c < HF ? c / F : 0);
+      if (c < HF) {
+        float v = acc[t] / sh + bias[c];
+        if (relu) v = v > 0.f ? v : 0.f;
+        out[c] = v;
+      }
+    }
+    if (lane < H) {
+      mx[(long long)r * H + lane] = m;
+      ssum[(long long)r * H + lane] = s;
+    }
+  }
+}
+
+// backward, warp per compute row r (i = rows[r]):
+//   gz = dL/dout masked by ReLU; c[r][h] = sum_j a_ij da_ij; der[r][h] = sum_j ds_ij
+template <int kT>
+__global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const int32_t* __restrict__ rows,
+                                                     const int32_t* __restrict__ start, const int32_t* __restrict__ end,
+                                                     const int32_t* __restrict__ col, const float* __restrict__ z,
+                                                     const float* __restrict__ el, const float* __restrict__ er,
+                                                     const float* __restrict__ mx, const float* __restrict__ ssum,
+                                                     const float* __restrict__ d_h, const float* __restrict__ h_out,
+                                                     int relu, int HF, int H, int F, float* __restrict__ gz,
+                                                     float* __restrict__ cc, float* __restrict__ der) {
+  const int R = *R_dev;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += warps) {
+    const int i = rows[r];
+    float g[kT];
+#pragma unroll
+    for (int t = 0; t < kT; ++t) {
+      const int c = lane + 32 * t;
+      g[t] = 0.f;
+      if (c < HF) {
+        const long long o = (long long)i * HF + c;
+        g[t] = d_h[o];
+        if (relu && !(h_out[o] > 0.f)) g[t] = 0.f;
+        gz[(long long)r * HF + c] = g[t];
+      }
+    }
+    const int e0 = start[i], e1 = end[i];
+    const float eri = lane < H ? er[(long long)i * H + lane] : 0.f;
+    const float mi = lane < H ? mx[(long long)r * H + lane] : 0.f;
+    const float si = lane < H ? ssum[(long long)r * H + lane] : 1.f;
+    float ci = 0.f, deri = 0.f;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int e = e0; e <= e1; ++e) {
+        const int j = e < e1 ? col[e] : i;
+        const float* zj = z + (long long)j * HF;
+        float p[kMaxH];
+#pragma unroll
+        for (int q = 0; q < kMaxH; ++q) p[q] = 0.f;
+#pragma unroll
+        for (int t = 0; t < kT; ++t) {
+          const int c = lane + 32 * t;
+          if (c < HF) {
+            const int h = c / F;
+            const float v = g[t] * zj[c];
+#pragma unroll
+            for (int q = 0; q < kMaxH; ++q)
+              if (q == h) p[q] += v;
+          }
+        }
+        warp_sum_heads<kMaxH>(p);
+        float da = 0.f;
+#pragma unroll
+        for (int q = 0; q < kMaxH; ++q)
+          if (lane == q) da = p[q];
+        if (lane < H) {
+          const float pre = el[(long long)j * H + lane] + eri;
+          const float a = expf(leaky(pre) - mi) / si;
+          if (pass == 0) ci += a * da;
+          else deri += a * (da - ci) * leaky_d(pre);
+        }
+      }
+    }
+    if (lane < H) {
+      cc[(long long)r * H + lane] = ci;
+      der[(long long)r * H + lane] = deri;
+    }
+  }
+}
+
+// backward, warp per live source j (CSC of the surviving edges; csc_pos[p]
+// = compute position of the edge's dst row): dz_j and del_j. dz is emitted as
+// TS row k (compact over the live list) for the dgrad / wgrad GEMMs.
+template <int kT>
+__global__ void __launch_bounds__(256) k_gat_bwd_src(
+    const int32_t* n_dev, const int32_t* __restrict__ live, const int32_t* __restrict__ seg_lo,
+    const int32_t* __restrict__ seg_hi, const unsigned* __restrict__ csc_pos, const int32_t* __restrict__ rows,
+    const int32_t* n_dst_dev, const int32_t* __restrict__ pos_of, const float* __restrict__ z,
+    const float* __restrict__ el, const float* __restrict__ er, const float* __restrict__ mx,
+    const float* __restrict__ ssum, const float* __restrict__ gz, const float* __restrict__ cc,
+    const float* __restrict__ der, const float* __restrict__ a_src, const float* __restrict__ a_dst, int HF, int H,
+    int F, uint8_t* __restrict__ dz_ts, long long plane, float* __restrict__ del) {
+  __shared__ __align__(16) float s_rows[8][kT * 32];
+  const int n = *n_dev;
+  const int n_dst = *n_dst_dev;
+  const int lane = threadIdx.x & 31;
+  const int nK = (HF + 31) / 32;
+  float* srow = s_rows[threadIdx.x >> 5];
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int k = w0; k < n; k += warps) {
+    const int j = live[k];
+    const float* zj = z + (long long)j * HF;
+    float zr[kT], acc[kT];
+#pragma unroll
+    for (int t = 0; t < kT; ++t) {
+      const int c = lane + 32 * t;
+      zr[t] = c < HF ? zj[c] : 0.f;
+      acc[t] = 0.f;
+    }
+    const float elj = lane < H ? el[(long long)j * H + lane] : 0.f;
+    float dl = 0.f;
+    const int self = j < n_dst ? pos_of[j] : -1;
+    const int p0 = seg_lo[j], p1 = seg_hi[j];
+    // CSC edges (ascending dst row), then the self loop
+    for (int p = p0; p <= p1; ++p) {
+      int pos;
+      if (p < p1) pos = (int)csc_pos[p];
+      else if (self >= 0) pos = self;
+      else break;
+      const int i = rows[pos];
+      const float* gi = gz + (long long)pos * HF;
+      float gv[kT];
+      float q8[kMaxH];
+#pragma unroll
+      for (int q = 0; q < kMaxH; ++q) q8[q] = 0.f;
+#pragma unroll
+      for (int t = 0; t < kT; ++t) {
+        const int c = lane + 32 * t;
+        gv[t] = c < HF ? gi[c] : 0.f;
+        if (c < HF) {
+          const int h = c / F;
+          const float v = gv[t] * zr[t];
+#pragma unroll
+          for (int q = 0; q < kMaxH; ++q)
+            if (q == h) q8[q] += v;
+        }
+      }
+      warp_sum_heads<kMaxH>(q8);
+      float da = 0.f;
+#pragma unroll
+      for (int q = 0; q < kMaxH; ++q)
+        if (lane == q) da = q8[q];
+      float a = 0.f;
+      if (lane < H) {
+        const float pre = elj + er[(long long)i * H + lane];
+        a = expf(leaky(pre) - mx[(long long)pos * H + lane]) / ssum[(long long)pos * H + lane];
+        dl += a * (da - cc[(long long)pos * H + lane]) * leaky_d(pre);
+      }
+#pragma unroll
+      for (int t = 0; t < kT; ++t) {
+        const int c = lane + 32 * t;
+        const float ah = head_val(a, c < HF ? c / F : 0);
+        if (c < HF) acc[t] = __fmaf_rn(ah, gv[t], acc[t]);
+      }
+    }
+    const float dr = (self >= 0 && lane < H) ? der[(long long)self * H + lane] : 0.f;
+#pragma unroll
+    for (int t = 0; t < kT; ++t) {
+      const int c = lane + 32 * t;
+      const int h = c < HF ? c / F : 0;
+      const float dlh = head_val(dl, h);
+      const float drh = head_val(dr, h);
+      float v = 0.f;
+      if (c < HF) {
+        v = __fmaf_rn(dlh, a_src[c], acc[t]);
+        if (self >= 0) v = __fmaf_rn(drh, a_dst[c], v);
+      }
+      srow[c] = v;   // zero padding up to the 32-column chunk
+    }
+    if (lane < H) del[(long long)k * H + lane] = dl;
+    __syncwarp();
+    for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK * 4, plane, k, g, srow + g * 8);
+    __syncwarp();
+  }
+  // zero the padding rows of the last 128-row tile (the weight-gradient GEMM reduces over rows)
+  const int n_pad = (n + kTsRows - 1) / kTsRows * kTsRows;
+  const float zeros[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int k = n + w0; k < n_pad; k += warps)
+    for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK * 4, plane, k, g, zeros);
+}
+
+constexpr int kParamBlocks = 148;
+
+// partial[b][0..HF) = sum over block b's compute rows of gz      (bias)
+// partial[b][HF..2HF) = sum over its compute rows of der[h] z     (a_dst)
+// partial[b][2HF..3HF) = sum over its live rows of del[h] z      (a_src)
+// rows split into kParamBlocks contiguous ranges by the device counts: a
+// fixed summation order independent of the launch
+__global__ void k_gat_param_partial(const int32_t* R_dev, const int32_t* __restrict__ rows,
+                                    const float* __restrict__ gz, const float* __restrict__ der,
+                                    const int32_t* n_dev, const int32_t* __restrict__ live,
+                                    const float* __restrict__ del, const float* __restrict__ z, int HF, int H, int F,
+                                    float* __restrict__ partial) {
+  const int R = *R_dev, n = *n_dev;
+  const int b = blockIdx.x;
+  for (int c = threadIdx.x; c < HF; c += blockDim.x) {
+    const int h = c / F;
+    float sb = 0.f, sd = 0.f, ss = 0.f;
+    const int r0 = (int)((long long)R * b / kParamBlocks), r1 = (int)((long long)R * (b + 1) / kParamBlocks);
+    for (int r = r0; r < r1; ++r) {
+      sb += gz[(long long)r * HF + c];
+      sd = __fmaf_rn(der[(long long)r * H + h], z[(long long)rows[r] * HF + c], sd);
+    }
+    const int k0 = (int)((long long)n * b / kParamBlocks), k1 = (int)((long long)n * (b + 1) / kParamBlocks);
+    for (int k = k0; k < k1; ++k) ss = __fmaf_rn(del[(long long)k * H + h], z[(long long)live[k] * HF + c], ss);
+    float* pb = partial + (long long)b * 3 * HF;
+    pb[c] = sb;
+    pb[HF + c] = sd;
+    pb[2 * HF + c] = ss;
+  }
+}
+
+// slab rows: d_in = a_src, d_in + 1 = a_dst, d_in + 2 = bias (each HF wide)
+__global__ void k_gat_param_sum(const float* __restrict__ partial, int HF, float* __restrict__ d_att_src,
+                                float* __restrict__ d_att_dst, float* __restrict__ d_bias) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < 3 * HF; c += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < kParamBlocks; ++b) s += partial[(long long)b * 3 * HF + c];
+    if (c < HF) d_bias[c] = s;
+    else if (c < 2 * HF) d_att_dst[c - HF] = s;
+    else d_att_src[c - 2 * HF] = s;
+  }
+}
+
+// d_in[live[k]] = SG[k]; norms[k] = ||SG[k]|| (fp64, fixed-order warp tree)
+__global__ void k_gat_scatter_norms(const int32_t* n_dev, const int32_t* __restrict__ live,
+                                    const float* __restrict__ SG, int d, float* __restrict__ d_in,
+                                    double* __restrict__ norms) {
+  const int n = *n_dev;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n; k += warps) {
+    const float* s = SG + (long long)k * d;
+    float* o = d_in + (long long)live[k] * d;
+    double sq = 0.0;
+    for (int c = lane; c < d; c += 32) {
+      const float v = s[c];
+      o[c] = v;
+      sq += (double)v * v;
+    }
+    sq = warp_sum_fixed(sq);
+    if (lane == 0) norms[k] = sqrt(sq);
+  }
+}
+
+inline int cols_per_lane(int HF) {
+  const int t = (HF + 31) / 32;
+  return t <= 1 ? 1 : t <= 2 ? 2 : t <= 4 ? 4 : t <= 8 ? 8 : t <= 16 ? 16 : -1;
+}
+
+}  // namespace
+}  // namespace hg
+
+using namespace hg;
+
+#define HG_GAT_DISPATCH(T, CALL)                \
+  switch (T) {                                  \
+    case 1: { constexpr int kT = 1; CALL; } break;  \
+    case 2: { constexpr int kT = 2; CALL; } break;  \
+    case 4: { constexpr int kT = 4; CALL; } break;  \
+    case 8: { constexpr int kT = 8; CALL; } break;  \
+    default: { constexpr int kT = 16; CALL; } break; \
+  }
+
+static int gat_check(const char* W, int HF, int H) {
+  if (H < 1 || H > kMaxH) return fail(W, kBadArg, "heads must be in [1, 8]");
+  if (HF % H) return fail(W, kBadArg, "d_out must be a multiple of heads");
+  if (cols_per_lane(HF) < 0) return fail(W, kBadArg, "d_out must be <= 512");
+  return kOk;
+}
+
+extern "C" {
+
+int hg_gat_scores(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const float* z, int HF, int H,
+                  const float* att_src, const float* att_dst, float* el, float* er, cudaStream_t stream) {
+  const char* W = "hg_gat_scores";
+  if (int st = gat_check(W, HF, H)) return st;
+  const unsigned grid = grid_for(n_live_max * 32, 256, 148 * 16);
+  HG_GAT_DISPATCH(cols_per_lane(HF), (k_gat_scores<kT><<<grid, 256, 0, stream>>>(n_live_dev, live, z, HF, H, HF / H,
+                                                                                  att_src, att_dst, el, er)));
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+int hg_gat_aggregate(const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
+                     const int32_t* end, const int32_t* col, const float* z, const float* el, const float* er, int HF,
+                     int H, const float* bias, int relu, float* h_out, float* mx, float* ssum, cudaStream_t stream) {
+  const char* W = "hg_gat_aggregate";
+  if (int st = gat_check(W, HF, H)) return st;
+  const unsigned grid = grid_for(R_max * 32, 256, 148 * 16);
+  HG_GAT_DISPATCH(cols_per_lane(HF),
+                  (k_gat_aggregate<kT><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, z, el, er, HF, H,
+                                                                  HF / H, bias, relu, h_out, mx, ssum)));
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+int hg_gat_bwd_dst(const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
+                   const int32_t* end, const int32_t* col, const float* z, const float* el, const float* er,
+                   const float* mx, const float* ssum, const float* d_h, const float* h_out, int relu, int HF, int H,
+                   float* gz, float* cc, float* der, cudaStream_t stream) {
+  const char* W = "hg_gat_bwd_dst";
+  if (int st = gat_check(W, HF, H)) return st;
+  const unsigned grid = grid_for(R_max * 32, 256, 148 * 16);
+  HG_GAT_DISPATCH(cols_per_lane(HF),
+                  (k_gat_bwd_dst<kT><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, z, el, er, mx, ssum, d_h,
+                                                                h_out, relu, HF, H, HF / H, gz, cc, der)));
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+int hg_gat_bwd_src(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const int32_t* seg_lo,
+                   const int32_t* seg_hi, const unsigned* csc_pos, const int32_t* rows, const int32_t* n_dst_dev,
+                   const int32_t* pos_of, const float* z, const float* el, const float* er, const float* mx,
+                   const float* ssum, const float* gz, const float* cc, const float* der, const float* att_src,
+                   const float* att_dst, int HF, int H, void* dz_ts, float* del, cudaStream_t stream) {
+  const char* W = "hg_gat_bwd_src";
+  if (int st = gat_check(W, HF, H)) return st;
+  const long long rows_pad = (n_live_max + kTsRows - 1) / kTsRows * kTsRows;
+  const unsigned grid = grid_for(rows_pad * 32, 256, 148 * 16);
+  const long long plane = ts_plane_bytes(n_live_max, HF);
+  HG_GAT_DISPATCH(cols_per_lane(HF),
+                  (k_gat_bwd_src<kT><<<grid, 256, 0, stream>>>(n_live_dev, live, seg_lo, seg_hi, csc_pos, rows,
+                                                                n_dst_dev, pos_of, z, el, er, mx, ssum, gz, cc, der,
+                                                                att_src, att_dst, HF, H, HF / H,
+                                                                static_cast<uint8_t*>(dz_ts), plane, del)));
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+long long hg_gat_param_scratch_bytes(int HF) { return (long long)kParamBlocks * 3 * HF * 4; }
+
+int hg_gat_param_grads(const int32_t* R_dev, const int32_t* rows, const float* gz, const float* der,
+                       const int32_t* n_live_dev, const int32_t* live, const float* del, const float* z, int HF, int H,
+                       float* partial, float* d_att_src, float* d_att_dst, float* d_bias, cudaStream_t stream) {
+  const char* W = "hg_gat_param_grads";
+  if (int st = gat_check(W, HF, H)) return st;
+  k_gat_param_partial<<<kParamBlocks, 256, 0, stream>>>(R_dev, rows, gz, der, n_live_dev, live, del, z, HF, H,
+                                                         HF / H, partial);
+  HG_LAUNCHED(W);
+  k_gat_param_sum<<<grid_for(3LL * HF, 256), 256, 0, stream>>>(partial, HF, d_att_src, d_att_dst, d_bias);
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+int hg_gat_scatter_norms(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const float* SG, int d,
+                         float* d_in, double* norms, cudaStream_t stream) {
+  k_gat_scatter_norms<<<grid_for(n_live_max * 32, 256, 148 * 16), 256, 0, stream>>>(n_live_dev, live, SG, d, d_in,
+                                                                                    norms);
+  HG_LAUNCHED("hg_gat_scatter_norms");
+  return kOk;
+}
+
+}  // extern "C"

@@ -35,7 +35,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .nn import (Injection, build_csc, cross_entropy_dev, layer_backward_dev, layer_forward_dev,
+from .nn import (Injection, LayerKind, build_csc, cross_entropy_dev, layer_backward_dev, layer_forward_dev,
                  load_features_dev, pack_dgrad_weights, sgd_step)
 from .sampler import SamplerWorkspace, SampleSlot, layer_bounds, pcg_words, sample_blocks_dev
 
@@ -279,9 +279,11 @@ class StepEngine:
         cscs, w_ts = [None] * L, [None] * L
         with torch.cuda.stream(prep):
             psp = _lib.stream_ptr(prep)
-            for l in range(1, L):
+            gat = net.kind is LayerKind.GAT   # GAT needs the transposed edges at every layer (dz for dW)
+            for l in range(0 if gat else 1, L):
                 cscs[l] = build_csc(blocks[l], keep[l], pos[l], blocks[l].n_dst_dev, psp)
-                w_ts[l] = pack_dgrad_weights(net, l, psp)
+                if not gat:
+                    w_ts[l] = pack_dgrad_weights(net, l, psp)
         # ---- layer-0 input (trainer.py:326-343) ----
         b0 = blocks[0]
         h = torch.empty((b0.num_src, tr.feature_dim), dtype=torch.float32, device=dev)
@@ -295,7 +297,7 @@ class StepEngine:
         for b in range(L):
             blk = blocks[b]
             t = layer_forward_dev(net, b, blk, h, rows[b], blk.num_dst, R_dev(b), b < L - 1, injected[b], sp,
-                                  blk.n_dst_dev)
+                                  blk.n_dst_dev, live=live[b], n_live=blk.num_src, n_live_dev=n_live_dev(b))
             tapes.append(t)
             h = t.h_out
         d_h, loss = cross_entropy_dev(tapes[-1].h_out, self.labels, B, net.dims[-1], sp)

@@ -42,10 +42,21 @@ def _wgrad_splits(R: int, K1: int, n: int) -> int:
 class LayerKind(enum.Enum):
     GCN = "gcn"
     SAGE_MEAN = "sage_mean"
+    GAT = "gat"        # not in the reference (nn.py:28-30); defined by oracle/gat.py
 
 
 def _kind_code(kind: LayerKind) -> int:
     return KIND_SAGE if kind is LayerKind.SAGE_MEAN else KIND_GCN
+
+
+def _slab_k(kind: LayerKind, fi: int) -> int:
+    """Rows above the bias row of a layer slab: SAGE [W_self; W_neigh],
+    GCN [W], GAT [W; a_src; a_dst]."""
+    if kind is LayerKind.SAGE_MEAN:
+        return 2 * fi
+    if kind is LayerKind.GAT:
+        return fi + 2
+    return fi
 
 
 @dataclass
@@ -55,11 +66,15 @@ class LayerParams:
     weight: torch.Tensor
     bias: torch.Tensor
     weight_neigh: torch.Tensor | None = None
+    att_src: torch.Tensor | None = None      # GAT only
+    att_dst: torch.Tensor | None = None
 
     def named_arrays(self):
         pairs = [("weight", self.weight), ("bias", self.bias)]
         if self.weight_neigh is not None:
             pairs.append(("weight_neigh", self.weight_neigh))
+        if self.att_src is not None:
+            pairs += [("att_src", self.att_src), ("att_dst", self.att_dst)]
         return pairs
 
     def numpy(self):
@@ -69,10 +84,12 @@ class LayerParams:
 def _slab_views(flat: torch.Tensor, kind: LayerKind, dims, offsets):
     out = []
     for l, (fi, fo) in enumerate(zip(dims[:-1], dims[1:])):
-        K = 2 * fi if kind is LayerKind.SAGE_MEAN else fi
+        K = _slab_k(kind, fi)
         slab = flat[offsets[l]:offsets[l] + (K + 1) * fo].view(K + 1, fo)
         if kind is LayerKind.SAGE_MEAN:
             out.append(LayerParams(slab[:fi], slab[K], slab[fi:K]))
+        elif kind is LayerKind.GAT:
+            out.append(LayerParams(slab[:fi], slab[K], None, slab[fi], slab[fi + 1]))
         else:
             out.append(LayerParams(slab[:fi], slab[K], None))
     return out
@@ -81,7 +98,7 @@ def _slab_views(flat: torch.Tensor, kind: LayerKind, dims, offsets):
 def _offsets(kind, dims):
     offs, o = [], 0
     for fi, fo in zip(dims[:-1], dims[1:]):
-        K = 2 * fi if kind is LayerKind.SAGE_MEAN else fi
+        K = _slab_k(kind, fi)
         offs.append(o)
         o += (K + 1) * fo
     return offs, o
@@ -94,10 +111,13 @@ class Network:
     flat: torch.Tensor                       # all parameters, fp32, device
     offsets: list
     layers: list = field(default_factory=list)
+    heads: list | None = None                # GAT heads per layer (hidden H, output 1)
 
     def __post_init__(self):
         if not self.layers:
             self.layers = _slab_views(self.flat, self.kind, self.dims, self.offsets)
+        if self.heads is None:
+            self.heads = [1] * (len(self.dims) - 1)
 
     @property
     def num_layers(self) -> int:
@@ -109,7 +129,7 @@ class Network:
 
     def slab(self, l: int) -> torch.Tensor:
         fi, fo = self.dims[l], self.dims[l + 1]
-        K = 2 * fi if self.kind is LayerKind.SAGE_MEAN else fi
+        K = _slab_k(self.kind, fi)
         return self.flat[self.offsets[l]:self.offsets[l] + (K + 1) * fo].view(K + 1, fo)
 
     def checksum_bytes(self) -> bytes:
@@ -138,44 +158,60 @@ class Grads:
 
     def slab(self, l):
         fi, fo = self.net.dims[l], self.net.dims[l + 1]
-        K = 2 * fi if self.net.kind is LayerKind.SAGE_MEAN else fi
+        K = _slab_k(self.net.kind, fi)
         return self.flat[self.net.offsets[l]:self.net.offsets[l] + (K + 1) * fo].view(K + 1, fo)
 
 
-def init_network(kind: LayerKind, dims, rng: np.random.Generator, dtype=np.float32, device=None) -> Network:
-    """Glorot-uniform weights, zero biases (nn.py:73-85); host RNG, then upload."""
+def init_network(kind: LayerKind, dims, rng: np.random.Generator, dtype=np.float32, device=None,
+                 heads: int = 4) -> Network:
+    """Glorot-uniform weights, zero biases (nn.py:73-85); host RNG, then upload.
+    GAT (oracle/gat.py init_layer): per layer W, then a_src, a_dst ~
+    U(+-sqrt(6/(F+1))); `heads` on hidden layers, 1 on the output layer."""
     _lib.require_cuda()
     if np.dtype(dtype) != np.float32:
         raise ValueError("the device network computes in fp32")
     dims = [int(d) for d in dims]
+    L = len(dims) - 1
+    hl = [heads if l < L - 1 else 1 for l in range(L)] if kind is LayerKind.GAT else [1] * L
     offs, total = _offsets(kind, dims)
     host = np.zeros(total, dtype=np.float32)
     for l, (fi, fo) in enumerate(zip(dims[:-1], dims[1:])):
         s = np.sqrt(6.0 / (fi + fo))
         w = rng.uniform(-s, s, size=(fi, fo)).astype(np.float32)
-        K = 2 * fi if kind is LayerKind.SAGE_MEAN else fi
+        K = _slab_k(kind, fi)
         slab = host[offs[l]:offs[l] + (K + 1) * fo].reshape(K + 1, fo)
         slab[:fi] = w
         if kind is LayerKind.SAGE_MEAN:
             slab[fi:K] = rng.uniform(-s, s, size=(fi, fo)).astype(np.float32)
+        elif kind is LayerKind.GAT:
+            if fo % hl[l]:
+                raise ValueError(f"layer {l}: d_out {fo} not divisible by {hl[l]} heads")
+            la = np.sqrt(6.0 / (fo // hl[l] + 1))
+            slab[fi] = rng.uniform(-la, la, size=fo).astype(np.float32)
+            slab[fi + 1] = rng.uniform(-la, la, size=fo).astype(np.float32)
     flat = torch.from_numpy(host).to(torch.device(device or "cuda"))
-    return Network(kind, dims, flat, offs)
+    return Network(kind, dims, flat, offs, heads=hl)
 
 
-def network_from_numpy(kind: LayerKind, layers, device=None) -> Network:
-    """Pack reference-style per-layer arrays (weight, bias, weight_neigh)."""
+def network_from_numpy(kind: LayerKind, layers, device=None, heads=None) -> Network:
+    """Pack reference-style per-layer arrays (weight, bias, weight_neigh /
+    att_src, att_dst)."""
     dims = [layers[0]["weight"].shape[0]] + [p["weight"].shape[1] for p in layers]
     offs, total = _offsets(kind, dims)
     host = np.zeros(total, dtype=np.float32)
     for l, p in enumerate(layers):
         fi, fo = p["weight"].shape
-        K = 2 * fi if kind is LayerKind.SAGE_MEAN else fi
+        K = _slab_k(kind, fi)
         slab = host[offs[l]:offs[l] + (K + 1) * fo].reshape(K + 1, fo)
         slab[:fi] = p["weight"]
         slab[K] = p["bias"]
         if kind is LayerKind.SAGE_MEAN:
             slab[fi:K] = p["weight_neigh"]
-    return Network(kind, dims, torch.from_numpy(host).to(torch.device(device or "cuda")), offs)
+        elif kind is LayerKind.GAT:
+            slab[fi] = p["att_src"]
+            slab[fi + 1] = p["att_dst"]
+    return Network(kind, dims, torch.from_numpy(host).to(torch.device(device or "cuda")), offs,
+                   heads=None if heads is None else list(heads))
 
 
 # ---------------------------------------------------------------- tapes
@@ -249,9 +285,138 @@ def _dev_count(n: int, dev) -> torch.Tensor:
     return torch.tensor([n], dtype=torch.int32, device=dev)
 
 
+@dataclass
+class GatTape(LayerTape):
+    """GAT forward state kept for the backward (oracle/gat.py GATTape)."""
+    z: torch.Tensor = None         # [n_src, HF] (rows of `live` valid)
+    el: torch.Tensor = None        # [n_src, H]
+    er: torch.Tensor = None
+    mx: torch.Tensor = None        # [R, H] per-row logit max
+    ssum: torch.Tensor = None      # [R, H] per-row exp sums
+    live: torch.Tensor = None
+    n_live: int = 0
+    n_live_dev: torch.Tensor = None
+    heads: int = 1
+
+
+def _att_rows(slab: torch.Tensor, d_in: int):
+    """(a_src, a_dst, bias) rows of a GAT slab [W; a_src; a_dst; bias]."""
+    return slab[d_in], slab[d_in + 1], slab[d_in + 2]
+
+
+def gat_layer_forward_dev(net: Network, l: int, blk, h_in, rows, R, R_dev, act, inj, stream, n_dst_dev,
+                          live, n_live, n_live_dev) -> GatTape:
+    """GAT block layer (oracle/gat.py layer_forward) on the device:
+    z[live] = h_in[live] W on tcgen05, per-head scores, then the attention
+    softmax + aggregation over the surviving edges and the self loop."""
+    dev = h_in.device
+    d_in, HF, H = net.dims[l], net.dims[l + 1], net.heads[l]
+    if live is None:
+        live = torch.arange(blk.num_src, dtype=torch.int32, device=dev)
+        n_live, n_live_dev = blk.num_src, _dev_count(blk.num_src, dev)
+    A = torch.empty(ts_bytes(n_live, d_in), dtype=torch.uint8, device=dev)
+    _lib.call("hg_gather_dz", _lib.ptr(n_live_dev), n_live, _lib.ptr(live), _lib.ptr(h_in), None, d_in, 0,
+              _lib.ptr(A), stream)
+    slab = net.slab(l)
+    PT = torch.empty(ts_bytes(HF, d_in), dtype=torch.uint8, device=dev)      # TS(W^T)
+    _lib.call("hg_ts_pack", _lib.ptr(slab), HF, 1, HF, d_in, HF, _lib.ptr(PT), stream)
+    z = torch.empty((blk.num_src, HF), dtype=torch.float32, device=dev)
+    _lib.call("hg_ts_linear_fwd", _lib.ptr(n_live_dev), n_live, _lib.ptr(A), d_in, _lib.ptr(PT), HF, _lib.ptr(live),
+              0, _lib.ptr(z), stream)
+    a_src, a_dst, bias = _att_rows(slab, d_in)
+    el = torch.empty((blk.num_src, H), dtype=torch.float32, device=dev)
+    er = torch.empty((blk.num_src, H), dtype=torch.float32, device=dev)
+    _lib.call("hg_gat_scores", _lib.ptr(n_live_dev), n_live, _lib.ptr(live), _lib.ptr(z), HF, H, _lib.ptr(a_src),
+              _lib.ptr(a_dst), _lib.ptr(el), _lib.ptr(er), stream)
+    n_dst = blk.num_dst
+    h_out = torch.empty((n_dst, HF), dtype=torch.float32, device=dev)
+    mx = torch.empty((max(R, 1), H), dtype=torch.float32, device=dev)
+    ssum = torch.empty((max(R, 1), H), dtype=torch.float32, device=dev)
+    _lib.call("hg_gat_aggregate", _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(blk.adj.start), _lib.ptr(blk.adj.end),
+              _lib.ptr(blk.adj.col_indices), _lib.ptr(z), _lib.ptr(el), _lib.ptr(er), HF, H, _lib.ptr(bias), int(act),
+              _lib.ptr(h_out), _lib.ptr(mx), _lib.ptr(ssum), stream)
+    if inj is not None:
+        nd = n_dst_dev if n_dst_dev is not None else _dev_count(n_dst, dev)
+        _lib.call("hg_inject_rows", _lib.ptr(nd), n_dst, _lib.ptr(inj.flag),
+                  _lib.ptr(inj.row), _lib.ptr(inj.table), HF, _lib.ptr(h_out), stream)
+    return GatTape(rows, R, R_dev, A, d_in, act, h_out, inj, z=z, el=el, er=er, mx=mx, ssum=ssum, live=live,
+                   n_live=n_live, n_live_dev=n_live_dev, heads=H)
+
+
+def gat_layer_backward_dev(net: Network, l: int, blk, t: GatTape, d_h, grads, need_input, keep, pos_of, stream,
+                           n_dst_dev=None, csc=None, wgrad_stream=None, keepalive=None):
+    """oracle/gat.py layer_backward on the device. Writes the layer's slab of
+    `grads`; returns (d_in [n_src, d_in] valid on the live rows, fp64 norms
+    aligned with the live list) or (None, None)."""
+    dev = d_h.device
+    d_in, HF, H = net.dims[l], net.dims[l + 1], t.heads
+    R, n_live = t.R, t.n_live
+    if n_dst_dev is None:
+        n_dst_dev = _dev_count(blk.num_dst, dev)
+    gz = torch.empty((max(R, 1), HF), dtype=torch.float32, device=dev)
+    cc = torch.empty((max(R, 1), H), dtype=torch.float32, device=dev)
+    der = torch.empty((max(R, 1), H), dtype=torch.float32, device=dev)
+    _lib.call("hg_gat_bwd_dst", _lib.ptr(t.R_dev), R, _lib.ptr(t.rows), _lib.ptr(blk.adj.start), _lib.ptr(blk.adj.end),
+              _lib.ptr(blk.adj.col_indices), _lib.ptr(t.z), _lib.ptr(t.el), _lib.ptr(t.er), _lib.ptr(t.mx),
+              _lib.ptr(t.ssum), _lib.ptr(d_h), _lib.ptr(t.h_out), int(t.relu), HF, H, _lib.ptr(gz), _lib.ptr(cc),
+              _lib.ptr(der), stream)
+    if csc is None:
+        csc = build_csc(blk, keep, pos_of, n_dst_dev, stream)
+    slab = net.slab(l)
+    a_src, a_dst, _ = _att_rows(slab, d_in)
+    dz = torch.empty(ts_bytes(n_live, HF), dtype=torch.uint8, device=dev)
+    dl = torch.empty((max(n_live, 1), H), dtype=torch.float32, device=dev)
+    _lib.call("hg_gat_bwd_src", _lib.ptr(t.n_live_dev), n_live, _lib.ptr(t.live), _lib.ptr(csc.seg_lo),
+              _lib.ptr(csc.seg_hi), _lib.ptr(csc.vals), _lib.ptr(t.rows), _lib.ptr(n_dst_dev), _lib.ptr(pos_of),
+              _lib.ptr(t.z), _lib.ptr(t.el), _lib.ptr(t.er), _lib.ptr(t.mx), _lib.ptr(t.ssum), _lib.ptr(gz),
+              _lib.ptr(cc), _lib.ptr(der), _lib.ptr(a_src), _lib.ptr(a_dst), HF, H, _lib.ptr(dz), _lib.ptr(dl), stream)
+    t.bwd = (gz, cc, der, dl)     # kept for inspection (tools/gat_diag.py)
+    gslab = grads.slab(l)
+    g_src, g_dst, g_bias = _att_rows(gslab, d_in)
+    part = torch.empty(int(_lib.query("hg_gat_param_scratch_bytes", HF)) // 4, dtype=torch.float32, device=dev)
+    _lib.call("hg_gat_param_grads", _lib.ptr(t.R_dev), _lib.ptr(t.rows), _lib.ptr(gz), _lib.ptr(der),
+              _lib.ptr(t.n_live_dev), _lib.ptr(t.live), _lib.ptr(dl), _lib.ptr(t.z), HF, H, _lib.ptr(part),
+              _lib.ptr(g_src), _lib.ptr(g_dst), _lib.ptr(g_bias), stream)
+    splits = _wgrad_splits(n_live, d_in, HF)
+
+    def wgrad(sp):
+        wp = torch.empty(splits * d_in * HF, dtype=torch.float32, device=dev)
+        _lib.call("hg_ts_linear_wgrad", _lib.ptr(t.n_live_dev), n_live, _lib.ptr(t.A), d_in, _lib.ptr(dz), HF,
+                  _lib.ptr(gslab), _lib.ptr(wp), splits, sp)
+        return wp
+
+    if wgrad_stream is not None:
+        cur = torch.cuda.current_stream(dev)
+        wgrad_stream.wait_stream(cur)
+        with torch.cuda.stream(wgrad_stream):
+            wp = wgrad(_lib.stream_ptr(wgrad_stream))
+        if keepalive is not None:
+            keepalive.extend([dz, wp, part, gz, cc, der, dl])
+    else:
+        wgrad(stream)
+    if not need_input:
+        return None, None
+    W_ts = pack_dgrad_weights(net, l, stream)
+    SG = torch.empty((max(n_live, 1), d_in), dtype=torch.float32, device=dev)
+    _lib.call("hg_ts_linear_dgrad", _lib.ptr(t.n_live_dev), n_live, _lib.ptr(dz), HF, _lib.ptr(W_ts), d_in,
+              _lib.ptr(SG), stream)
+    d_full = torch.empty((blk.num_src, d_in), dtype=torch.float32, device=dev)
+    norms = torch.empty(max(n_live, 1), dtype=torch.float64, device=dev)
+    _lib.call("hg_gat_scatter_norms", _lib.ptr(t.n_live_dev), n_live, _lib.ptr(t.live), _lib.ptr(SG), d_in,
+              _lib.ptr(d_full), _lib.ptr(norms), stream)
+    if keepalive is not None:
+        keepalive.extend([W_ts, SG])
+    return d_full, norms[:n_live]
+
+
 def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch.Tensor, R: int,
                       R_dev: torch.Tensor, act: bool, inj: Injection | None, stream,
-                      n_dst_dev: torch.Tensor | None = None) -> LayerTape:
+                      n_dst_dev: torch.Tensor | None = None, live=None, n_live=None, n_live_dev=None) -> LayerTape:
+    if net.kind is LayerKind.GAT:
+        if h_in.shape[0] != blk.num_src:
+            raise ValueError(f"h_in has {h_in.shape[0]} rows, frontier needs {blk.num_src}")
+        return gat_layer_forward_dev(net, l, blk, h_in, rows, R, R_dev, act, inj, stream, n_dst_dev, live, n_live,
+                                     n_live_dev)
     dev = h_in.device
     d_in = net.dims[l]
     d_out = net.dims[l + 1]
@@ -362,9 +527,10 @@ def build_csc(blk, keep: torch.Tensor, pos_of: torch.Tensor, n_dst_dev, stream, 
 
 
 def pack_dgrad_weights(net: Network, l: int, stream) -> torch.Tensor:
-    """TS(P[:K]) of layer l: the B operand of the input-gradient GEMM."""
+    """TS(P[:K]) of layer l: the B operand of the input-gradient GEMM
+    (GAT: the W rows only)."""
     d_in, d_out = net.dims[l], net.dims[l + 1]
-    K = 2 * d_in if _kind_code(net.kind) == KIND_SAGE else d_in
+    K = 2 * d_in if _kind_code(net.kind) == KIND_SAGE and net.kind is not LayerKind.GAT else d_in
     W = torch.empty(ts_bytes(K, d_out), dtype=torch.uint8, device=net.flat.device)
     _lib.call("hg_ts_pack", _lib.ptr(net.slab(l)), d_out, 0, K, d_out, K, _lib.ptr(W), stream)
     return W
@@ -382,6 +548,9 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
     weight-gradient GEMM forks onto it (only SGD waits for it) while the
     input-gradient chain continues; buffers it reads are appended to
     `keepalive`, which the caller holds until the streams are joined."""
+    if net.kind is LayerKind.GAT:
+        return gat_layer_backward_dev(net, l, blk, t, d_h, grads, need_input, keep, pos_of, stream, n_dst_dev,
+                                      csc, wgrad_stream, keepalive)
     dev = d_h.device
     d_in_dim, d_out = net.dims[l], net.dims[l + 1]
     R, K = t.R, t.K

@@ -65,6 +65,7 @@ class TrainConfig:
     # B200 additions (not in the reference): where the raw feature table lives
     feature_placement: str = "hbm"      # "hbm" | "host" (pinned, read through UVA)
     max_capacity: int | None = None     # cache growth limit (see CachePolicy)
+    heads: int = 4                      # GAT hidden-layer heads (LayerKind.GAT, oracle/gat.py)
 
     def __post_init__(self):
         if len(self.fanouts) == 0 or any(f < 1 for f in self.fanouts):
@@ -284,7 +285,7 @@ class Trainer:
         self.row_bytes = self.feature_dim * feats.element_size()
         depth = len(cfg.fanouts)
         dims = [self.feature_dim] + [cfg.hidden] * (depth - 1) + [self.num_classes]
-        self.network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, self.device)
+        self.network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, self.device, heads=cfg.heads)
         policy = CachePolicy(cfg.p_grad, cfg.t_stale, cfg.capacity, cfg.max_capacity)
         feature_rows = self.graph.num_nodes // 10 if cfg.feature_rows is None else cfg.feature_rows
         self.cache = HistCache(self.graph.num_nodes, [cfg.hidden] * (depth - 1), policy, feature_rows=feature_rows,
@@ -440,7 +441,8 @@ class Trainer:
         for b in range(L):
             R, _ = pruned.counts[b]
             t = layer_forward_dev(net, b, sub.layers[b], h, pruned.compute_rows[b], R, pruned.R_dev(b),
-                                  b < L - 1, pruned.injected[b], sp, pruned.n_dst_dev(b))
+                                  b < L - 1, pruned.injected[b], sp, pruned.n_dst_dev(b), live=pruned.layer_live[b],
+                                  n_live=pruned.counts[b][1], n_live_dev=pruned.n_live_dev(b))
             tapes.append(t)
             h = t.h_out
         B = int(sub.seeds.shape[0])
@@ -518,7 +520,7 @@ def run_plain_loop(graph, features, labels, train_ids, cfg: TrainConfig, num_cla
     d = int(feats.shape[1])
     depth = len(cfg.fanouts)
     dims = [d] + [cfg.hidden] * (depth - 1) + [ncls]
-    network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, dev)
+    network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, dev, heads=cfg.heads)
     plan = SamplePlan(cfg.fanouts, cfg.batch_size, cfg.seed)
     losses = []
     gctr = torch.zeros(8, dtype=torch.int64, device=dev)
@@ -589,9 +591,19 @@ def full_graph_logits(network: Network, graph, features, chunk_rows: int | None 
     end = g.end.to(torch.int32)
     deg = (end - start).contiguous()
     zero = torch.zeros_like(deg)
-    from .nn import _kind_code, ts_bytes
+    from .nn import _kind_code, gat_layer_forward_dev, ts_bytes
     kind = _kind_code(network.kind)
     L = network.num_layers
+    if network.kind is LayerKind.GAT:
+        # whole-graph blocks: every node a dst row, sources = all nodes
+        class _Full:
+            num_src = num_dst = N
+            adj = type("A", (), {"start": start, "end": end, "col_indices": g.col_indices})()
+        cnt = _dev_count(N, dev)
+        for l in range(L):
+            t = gat_layer_forward_dev(network, l, _Full, h, every, N, cnt, l < L - 1, None, sp, cnt, every, N, cnt)
+            h = t.h_out
+        return h
     for l in range(L):
         d_in, d_out = network.dims[l], network.dims[l + 1]
         K = 2 * d_in if network.kind == LayerKind.SAGE_MEAN else d_in
