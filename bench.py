@@ -42,6 +42,10 @@ CONFIGS = {
     "c3": dict(workload="ogbn-papers100M-shape synthetic power-law (111M nodes, 1.55B edges, 128-d fp16), "
                         "3-layer GraphSAGE hidden 256, fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
                n=111_000_000, m=7, d=128, classes=172, fp16=True, capacity=6_000_000, max_capacity=24_000_000),
+    "c5": dict(workload="ogbn-papers100M-shape synthetic power-law (111M nodes, 1.55B edges, 128-d fp16), "
+                        "3-layer GAT (4 heads, hidden 256), fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
+               n=111_000_000, m=7, d=128, classes=172, fp16=True, capacity=6_000_000, max_capacity=24_000_000,
+               kind="gat"),
     "c1": dict(workload="synthetic power-law 100K nodes / 2M edges, 128-d fp32, 3-layer GraphSAGE hidden 256, "
                         "fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
                n=100_000, m=10, d=128, classes=8),
@@ -238,7 +242,8 @@ def main():
     n_tl = 10   # extra steps after the timed regions for the phase timeline
     need = (args.warmup + 2 * args.steps + n_tl + 1) * world
     per_epoch = -(-len(train) // BATCH)
-    tcfg = hg.TrainConfig(fanouts=FANOUTS, hidden=HIDDEN, batch_size=BATCH, eta=ETA, kind=hg.LayerKind.SAGE_MEAN,
+    kind = hg.LayerKind.GAT if cfgd.get("kind") == "gat" else hg.LayerKind.SAGE_MEAN
+    tcfg = hg.TrainConfig(fanouts=FANOUTS, hidden=HIDDEN, batch_size=BATCH, eta=ETA, kind=kind, heads=4,
                           p_grad=P_GRAD, t_stale=T_STALE, seed=0, epochs=max(1, -(-need // per_epoch)),
                           capacity=cfgd.get("capacity"), max_capacity=cfgd.get("max_capacity"))
     tr = hg.Trainer(graph, feats_dev, labels, train, tcfg, cfgd["classes"])

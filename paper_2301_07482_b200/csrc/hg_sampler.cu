@@ -544,8 +544,11 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   static long long sel_cap = -1;
   if (sel_cap < 0) {
     const char* e = std::getenv("HG_SEL_BLOCKS");
-    sel_cap = e ? std::atoll(e) : 148 * 2;   // 2 CTAs (16 warps) per SM measured best
-    if (sel_cap < 1) sel_cap = 148 * 2;
+    // 4 CTAs (32 warps) per SM: the selection is latency-bound per row, so
+    // more rows in flight help (C2: k_select 81 -> 59 ms / 200 steps; C3
+    // step 1.29 -> 1.23 ms); 6/SM gains little more (profiles/r01/notes)
+    sel_cap = e ? std::atoll(e) : 148 * 4;
+    if (sel_cap < 1) sel_cap = 148 * 4;
   }
   const unsigned sel_grid = (unsigned)sel_cap;
   if (fanout <= 32)
