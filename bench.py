@@ -328,9 +328,18 @@ def main():
     g_time = tv[0][2] / 1e9
     n_launch = max(1, int(tv[0][3]))
     achieved = g_bytes / g_time / 1e9 if g_time > 0 else 0.0
+    # DRAM traffic of one warm k_load_rows launch from the committed ncu
+    # --set full capture of this config (profiles/r01/traffic.json)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+    tkey = "c3" if args.config in ("c3", "c5") else args.config
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath)).get(tkey)
+        if tj:
+            traffic, traffic_src = tj["traffic_bytes"], tj["capture"]
     roofline = {"kernel": "k_load_rows (hg_load_features, feature gather)", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "peak_source": peak_src, "traffic": None,
+                "peak_source": peak_src, "traffic": traffic, "traffic_source": traffic_src,
                 "bytes_per_launch": g_bytes / n_launch, "avg_launch_us": 1e6 * g_time / n_launch,
                 "timing": "device %globaltimer span per launch, accumulated over the timed region",
                 "share_of_step": g_time / t_dev if t_dev else None}
