@@ -39,49 +39,75 @@ __device__ __forceinline__ void warp_sum_heads(float (&p)[kH]) {
   }
 }
 
+// Column -> head map. kH > 0: compile-time (H == 1, or HF == 32 kT with kT a
+// multiple of H, so lane column slot t always belongs to head t / (kT / kH));
+// kH == 0: generic (runtime c / F, kMaxH select chain).
+template <int kT, int kH>
+struct Heads {
+  static constexpr int N = kH > 0 ? kH : kMaxH;
+  __device__ __forceinline__ static int of(int t, int c, int F) {
+    if constexpr (kH == 1) return 0;
+    else if constexpr (kH > 1) return t / (kT / kH);
+    else return c / F;
+  }
+  __device__ __forceinline__ static void add(float (&p)[N], int t, int c, int F, float v) {
+    if constexpr (kH > 0) {
+      p[of(t, c, F)] += v;
+    } else {
+      const int h = c / F;
+#pragma unroll
+      for (int q = 0; q < kMaxH; ++q)
+        if (q == h) p[q] += v;
+    }
+  }
+  // lane q (< H) receives the value of head q
+  __device__ __forceinline__ static float pick(const float (&p)[N], int lane) {
+    float r = 0.f;
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+      if (lane == q) r = p[q];
+    return r;
+  }
+};
+
 // el[j*H + h] = <z[j, hF:(h+1)F], a_src[hF:(h+1)F]>, er likewise with a_dst
-template <int kT>
+template <int kT, int kH>
 __global__ void __launch_bounds__(256) k_gat_scores(const int32_t* n_dev, const int32_t* __restrict__ live,
                                                     const float* __restrict__ z, int HF, int H, int F,
                                                     const float* __restrict__ a_src, const float* __restrict__ a_dst,
                                                     float* __restrict__ el, float* __restrict__ er) {
+  using HM = Heads<kT, kH>;
   const int n = *n_dev;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
     const int j = live[i];
-    float pl[kMaxH], pr[kMaxH];
+    float pl[HM::N], pr[HM::N];
 #pragma unroll
-    for (int h = 0; h < kMaxH; ++h) pl[h] = pr[h] = 0.f;
+    for (int h = 0; h < HM::N; ++h) pl[h] = pr[h] = 0.f;
 #pragma unroll
     for (int t = 0; t < kT; ++t) {
       const int c = lane + 32 * t;
       if (c < HF) {
         const float x = z[(long long)j * HF + c];
-        const int h = c / F;
-#pragma unroll
-        for (int q = 0; q < kMaxH; ++q)
-          if (q == h) {
-            pl[q] = __fmaf_rn(x, a_src[c], pl[q]);
-            pr[q] = __fmaf_rn(x, a_dst[c], pr[q]);
-          }
+        HM::add(pl, t, c, F, x * a_src[c]);
+        HM::add(pr, t, c, F, x * a_dst[c]);
       }
     }
-    warp_sum_heads<kMaxH>(pl);
-    warp_sum_heads<kMaxH>(pr);
-#pragma unroll
-    for (int q = 0; q < kMaxH; ++q)
-      if (lane == q && q < H) {
-        el[(long long)j * H + q] = pl[q];
-        er[(long long)j * H + q] = pr[q];
-      }
+    warp_sum_heads<HM::N>(pl);
+    warp_sum_heads<HM::N>(pr);
+    const float vl = HM::pick(pl, lane), vr = HM::pick(pr, lane);
+    if (lane < H) {
+      el[(long long)j * H + lane] = vl;
+      er[(long long)j * H + lane] = vr;
+    }
   }
 }
 
 // value of head h held by lane h of `v` (lanes < H hold one head each)
 __device__ __forceinline__ float head_val(float v, int h) { return __shfl_sync(0xffffffffu, v, h); }
 
-template <int kT>
+template <int kT, int kH>
 __global__ void __launch_bounds__(256) k_gat_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                        const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                        const int32_t* __restrict__ col, const float* __restrict__ z,
@@ -115,7 +141,7 @@ __global__ void __launch_bounds__(256) k_gat_aggregate(const int32_t* R_dev, con
 #pragma unroll
       for (int t = 0; t < kT; ++t) {
         const int c = lane + 32 * t;
-        const float wh = head_val(w, c < HF ? c / F : 0);
+        const float wh = head_val(w, c < HF ? Heads<kT, kH>::of(t, c, F) : 0);
         if (c < HF) acc[t] = __fmaf_rn(wh, zj[c], acc[t]);
       }
     }
@@ -123,7 +149,7 @@ __global__ void __launch_bounds__(256) k_gat_aggregate(const int32_t* R_dev, con
 #pragma unroll
     for (int t = 0; t < kT; ++t) {
       const int c = lane + 32 * t;
-      const float sh = head_val(s, c < HF ? c / F : 0);
+      const float sh = head_val(s, c < HF ? Heads<kT, kH>::of(t, c, F) : 0);
       if (c < HF) {
         float v = acc[t] / sh + bias[c];
         if (relu) v = v > 0.f ? v : 0.f;
@@ -139,7 +165,7 @@ __global__ void __launch_bounds__(256) k_gat_aggregate(const int32_t* R_dev, con
 
 // backward, warp per compute row r (i = rows[r]):
 //   gz = dL/dout masked by ReLU; c[r][h] = sum_j a_ij da_ij; der[r][h] = sum_j ds_ij
-template <int kT>
+template <int kT, int kH>
 __global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                      const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                      const int32_t* __restrict__ col, const float* __restrict__ z,
@@ -174,25 +200,17 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const
       for (int e = e0; e <= e1; ++e) {
         const int j = e < e1 ? col[e] : i;
         const float* zj = z + (long long)j * HF;
-        float p[kMaxH];
+        using HM = Heads<kT, kH>;
+        float p[HM::N];
 #pragma unroll
-        for (int q = 0; q < kMaxH; ++q) p[q] = 0.f;
+        for (int q = 0; q < HM::N; ++q) p[q] = 0.f;
 #pragma unroll
         for (int t = 0; t < kT; ++t) {
           const int c = lane + 32 * t;
-          if (c < HF) {
-            const int h = c / F;
-            const float v = g[t] * zj[c];
-#pragma unroll
-            for (int q = 0; q < kMaxH; ++q)
-              if (q == h) p[q] += v;
-          }
+          if (c < HF) HM::add(p, t, c, F, g[t] * zj[c]);
         }
-        warp_sum_heads<kMaxH>(p);
-        float da = 0.f;
-#pragma unroll
-        for (int q = 0; q < kMaxH; ++q)
-          if (lane == q) da = p[q];
+        warp_sum_heads<HM::N>(p);
+        const float da = HM::pick(p, lane);
         if (lane < H) {
           const float pre = el[(long long)j * H + lane] + eri;
           const float a = expf(leaky(pre) - mi) / si;
@@ -211,7 +229,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const
 // backward, warp per live source j (CSC of the surviving edges; csc_pos[p]
 // = compute position of the edge's dst row): dz_j and del_j. dz is emitted as
 // TS row k (compact over the live list) for the dgrad / wgrad GEMMs.
-template <int kT>
+template <int kT, int kH>
 __global__ void __launch_bounds__(256) k_gat_bwd_src(
     const int32_t* n_dev, const int32_t* __restrict__ live, const int32_t* __restrict__ seg_lo,
     const int32_t* __restrict__ seg_hi, const unsigned* __restrict__ csc_pos, const int32_t* __restrict__ rows,
@@ -250,27 +268,19 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(
       else break;
       const int i = rows[pos];
       const float* gi = gz + (long long)pos * HF;
+      using HM = Heads<kT, kH>;
       float gv[kT];
-      float q8[kMaxH];
+      float q8[HM::N];
 #pragma unroll
-      for (int q = 0; q < kMaxH; ++q) q8[q] = 0.f;
+      for (int q = 0; q < HM::N; ++q) q8[q] = 0.f;
 #pragma unroll
       for (int t = 0; t < kT; ++t) {
         const int c = lane + 32 * t;
         gv[t] = c < HF ? gi[c] : 0.f;
-        if (c < HF) {
-          const int h = c / F;
-          const float v = gv[t] * zr[t];
-#pragma unroll
-          for (int q = 0; q < kMaxH; ++q)
-            if (q == h) q8[q] += v;
-        }
+        if (c < HF) HM::add(q8, t, c, F, gv[t] * zr[t]);
       }
-      warp_sum_heads<kMaxH>(q8);
-      float da = 0.f;
-#pragma unroll
-      for (int q = 0; q < kMaxH; ++q)
-        if (lane == q) da = q8[q];
+      warp_sum_heads<HM::N>(q8);
+      const float da = HM::pick(q8, lane);
       float a = 0.f;
       if (lane < H) {
         const float pre = elj + er[(long long)i * H + lane];
@@ -280,7 +290,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(
 #pragma unroll
       for (int t = 0; t < kT; ++t) {
         const int c = lane + 32 * t;
-        const float ah = head_val(a, c < HF ? c / F : 0);
+        const float ah = head_val(a, c < HF ? Heads<kT, kH>::of(t, c, F) : 0);
         if (c < HF) acc[t] = __fmaf_rn(ah, gv[t], acc[t]);
       }
     }
@@ -288,7 +298,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(
 #pragma unroll
     for (int t = 0; t < kT; ++t) {
       const int c = lane + 32 * t;
-      const int h = c < HF ? c / F : 0;
+      const int h = c < HF ? Heads<kT, kH>::of(t, c, F) : 0;
       const float dlh = head_val(dl, h);
       const float drh = head_val(dr, h);
       float v = 0.f;
@@ -384,14 +394,32 @@ inline int cols_per_lane(int HF) {
 
 using namespace hg;
 
-#define HG_GAT_DISPATCH(T, CALL)                \
-  switch (T) {                                  \
-    case 1: { constexpr int kT = 1; CALL; } break;  \
-    case 2: { constexpr int kT = 2; CALL; } break;  \
-    case 4: { constexpr int kT = 4; CALL; } break;  \
-    case 8: { constexpr int kT = 8; CALL; } break;  \
-    default: { constexpr int kT = 16; CALL; } break; \
+// (kT, kH) dispatch: kH = H when the column -> head map is static (H == 1,
+// or HF == 32 kT with kT % H == 0), else the generic kH = 0 variant
+#define HG_GAT_T(T, KH, CALL)                            \
+  switch (T) {                                          \
+    case 1: { constexpr int kT = 1; constexpr int kH = (KH) <= 1 ? (KH) : 0; CALL; } break;   \
+    case 2: { constexpr int kT = 2; constexpr int kH = (KH) <= 2 ? (KH) : 0; CALL; } break;   \
+    case 4: { constexpr int kT = 4; constexpr int kH = (KH) <= 4 ? (KH) : 0; CALL; } break;   \
+    case 8: { constexpr int kT = 8; constexpr int kH = (KH); CALL; } break;                    \
+    default: { constexpr int kT = 16; constexpr int kH = (KH); CALL; } break;                 \
   }
+#define HG_GAT_DISPATCH(HF_, H_, CALL)                                             \
+  {                                                                                \
+    const int T_ = cols_per_lane(HF_);                                             \
+    const int kh_ = static_head_map(HF_, H_, T_);                                  \
+    if (kh_ == 1) HG_GAT_T(T_, 1, CALL)                                            \
+    else if (kh_ == 2) HG_GAT_T(T_, 2, CALL)                                       \
+    else if (kh_ == 4) HG_GAT_T(T_, 4, CALL)                                       \
+    else if (kh_ == 8) HG_GAT_T(T_, 8, CALL)                                       \
+    else HG_GAT_T(T_, 0, CALL)                                                     \
+  }
+
+inline int static_head_map(int HF, int H, int T) {
+  if (H == 1) return 1;
+  if (HF == 32 * T && T % H == 0 && (H == 2 || H == 4 || H == 8)) return H;
+  return 0;
+}
 
 static int gat_check(const char* W, int HF, int H) {
   if (H < 1 || H > kMaxH) return fail(W, kBadArg, "heads must be in [1, 8]");
@@ -407,7 +435,7 @@ int hg_gat_scores(const int32_t* n_live_dev, long long n_live_max, const int32_t
   const char* W = "hg_gat_scores";
   if (int st = gat_check(W, HF, H)) return st;
   const unsigned grid = grid_for(n_live_max * 32, 256, 148 * 16);
-  HG_GAT_DISPATCH(cols_per_lane(HF), (k_gat_scores<kT><<<grid, 256, 0, stream>>>(n_live_dev, live, z, HF, H, HF / H,
+  HG_GAT_DISPATCH(HF, H, (k_gat_scores<kT, kH><<<grid, 256, 0, stream>>>(n_live_dev, live, z, HF, H, HF / H,
                                                                                   att_src, att_dst, el, er)));
   HG_LAUNCHED(W);
   return kOk;
@@ -419,8 +447,8 @@ int hg_gat_aggregate(const int32_t* R_dev, long long R_max, const int32_t* rows,
   const char* W = "hg_gat_aggregate";
   if (int st = gat_check(W, HF, H)) return st;
   const unsigned grid = grid_for(R_max * 32, 256, 148 * 16);
-  HG_GAT_DISPATCH(cols_per_lane(HF),
-                  (k_gat_aggregate<kT><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, z, el, er, HF, H,
+  HG_GAT_DISPATCH(HF, H,
+                  (k_gat_aggregate<kT, kH><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, z, el, er, HF, H,
                                                                   HF / H, bias, relu, h_out, mx, ssum)));
   HG_LAUNCHED(W);
   return kOk;
@@ -433,8 +461,8 @@ int hg_gat_bwd_dst(const int32_t* R_dev, long long R_max, const int32_t* rows, c
   const char* W = "hg_gat_bwd_dst";
   if (int st = gat_check(W, HF, H)) return st;
   const unsigned grid = grid_for(R_max * 32, 256, 148 * 16);
-  HG_GAT_DISPATCH(cols_per_lane(HF),
-                  (k_gat_bwd_dst<kT><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, z, el, er, mx, ssum, d_h,
+  HG_GAT_DISPATCH(HF, H,
+                  (k_gat_bwd_dst<kT, kH><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, z, el, er, mx, ssum, d_h,
                                                                 h_out, relu, HF, H, HF / H, gz, cc, der)));
   HG_LAUNCHED(W);
   return kOk;
@@ -450,8 +478,8 @@ int hg_gat_bwd_src(const int32_t* n_live_dev, long long n_live_max, const int32_
   const long long rows_pad = (n_live_max + kTsRows - 1) / kTsRows * kTsRows;
   const unsigned grid = grid_for(rows_pad * 32, 256, 148 * 16);
   const long long plane = ts_plane_bytes(n_live_max, HF);
-  HG_GAT_DISPATCH(cols_per_lane(HF),
-                  (k_gat_bwd_src<kT><<<grid, 256, 0, stream>>>(n_live_dev, live, seg_lo, seg_hi, csc_pos, rows,
+  HG_GAT_DISPATCH(HF, H,
+                  (k_gat_bwd_src<kT, kH><<<grid, 256, 0, stream>>>(n_live_dev, live, seg_lo, seg_hi, csc_pos, rows,
                                                                 n_dst_dev, pos_of, z, el, er, mx, ssum, gz, cc, der,
                                                                 att_src, att_dst, HF, H, HF / H,
                                                                 static_cast<uint8_t*>(dz_ts), plane, del)));
