@@ -68,6 +68,32 @@ struct Heads {
       if (lane == q) r = p[q];
     return r;
   }
+  // warp sums of the per-lane head partials p, delivered to lane h (< H) for
+  // head h. kH = 2^m: reduce-scatter (m halving exchanges, then 5 - m xor
+  // steps on one value: kH - 1 + 5 - m shuffles) + one gather shuffle,
+  // instead of kH full reductions; fixed order, so bit-reproducible.
+  __device__ __forceinline__ static float sum_to_lanes(float (&p)[N], int lane) {
+    if constexpr (kH == 2 || kH == 4 || kH == 8) {
+      constexpr int m = kH == 2 ? 1 : (kH == 4 ? 2 : 3);
+#pragma unroll
+      for (int s = 0, half = kH / 2; s < m; ++s, half >>= 1) {
+        const int o = 16 >> s;
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+          const float send = up ? p[i] : p[i + half];
+          const float keep = up ? p[i + half] : p[i];
+          p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+#pragma unroll
+      for (int o = 16 >> m; o > 0; o >>= 1) p[0] += __shfl_xor_sync(0xffffffffu, p[0], o);
+      return __shfl_sync(0xffffffffu, p[0], (lane & (kH - 1)) << (5 - m));
+    } else {
+      warp_sum_heads<N>(p);
+      return pick(p, lane);
+    }
+  }
 };
 
 // el[j*H + h] = <z[j, hF:(h+1)F], a_src[hF:(h+1)F]>, er likewise with a_dst
@@ -94,9 +120,8 @@ __global__ void __launch_bounds__(256) k_gat_scores(const int32_t* n_dev, const 
         HM::add(pr, t, c, F, x * a_dst[c]);
       }
     }
-    warp_sum_heads<HM::N>(pl);
-    warp_sum_heads<HM::N>(pr);
-    const float vl = HM::pick(pl, lane), vr = HM::pick(pr, lane);
+    const float vl = HM::sum_to_lanes(pl, lane);
+    const float vr = HM::sum_to_lanes(pr, lane);
     if (lane < H) {
       el[(long long)j * H + lane] = vl;
       er[(long long)j * H + lane] = vr;
@@ -174,8 +199,9 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const
                                                      const float* __restrict__ d_h, const float* __restrict__ h_out,
                                                      int relu, int HF, int H, int F, float* __restrict__ gz,
                                                      float* __restrict__ cc, float* __restrict__ der) {
+  __shared__ float s_da[8][32][kMaxH], s_a[8][32][kMaxH], s_sl[8][32][kMaxH];
   const int R = *R_dev;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += warps) {
     const int i = rows[r];
@@ -196,8 +222,20 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const
     const float mi = lane < H ? mx[(long long)r * H + lane] : 0.f;
     const float si = lane < H ? ssum[(long long)r * H + lane] : 1.f;
     float ci = 0.f, deri = 0.f;
+    // rows of up to 32 edges (incl. the self loop; every sampled block, whose
+    // degrees are bounded by the fanout) keep (da, a, slope) of each edge in
+    // shared memory for the second pass instead of recomputing it
+    const bool cached = e1 - e0 + 1 <= 32;
     for (int pass = 0; pass < 2; ++pass) {
       for (int e = e0; e <= e1; ++e) {
+        const int ei = e - e0;
+        if (pass == 1 && cached) {
+          if (lane < H) {
+            const float da = s_da[wib][ei][lane], a = s_a[wib][ei][lane];
+            deri += a * (da - ci) * s_sl[wib][ei][lane];
+          }
+          continue;
+        }
         const int j = e < e1 ? col[e] : i;
         const float* zj = z + (long long)j * HF;
         using HM = Heads<kT, kH>;
@@ -209,15 +247,23 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const
           const int c = lane + 32 * t;
           if (c < HF) HM::add(p, t, c, F, g[t] * zj[c]);
         }
-        warp_sum_heads<HM::N>(p);
-        const float da = HM::pick(p, lane);
+        const float da = HM::sum_to_lanes(p, lane);
         if (lane < H) {
           const float pre = el[(long long)j * H + lane] + eri;
           const float a = expf(leaky(pre) - mi) / si;
-          if (pass == 0) ci += a * da;
-          else deri += a * (da - ci) * leaky_d(pre);
+          if (pass == 0) {
+            ci += a * da;
+            if (cached) {
+              s_da[wib][ei][lane] = da;
+              s_a[wib][ei][lane] = a;
+              s_sl[wib][ei][lane] = leaky_d(pre);
+            }
+          } else {
+            deri += a * (da - ci) * leaky_d(pre);
+          }
         }
       }
+      __syncwarp();
     }
     if (lane < H) {
       cc[(long long)r * H + lane] = ci;
@@ -279,8 +325,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(
         gv[t] = c < HF ? gi[c] : 0.f;
         if (c < HF) HM::add(q8, t, c, F, gv[t] * zr[t]);
       }
-      warp_sum_heads<HM::N>(q8);
-      const float da = HM::pick(q8, lane);
+      const float da = HM::sum_to_lanes(q8, lane);
       float a = 0.f;
       if (lane < H) {
         const float pre = elj + er[(long long)i * H + lane];
@@ -320,34 +365,53 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(
     for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK * 4, plane, k, g, zeros);
 }
 
-constexpr int kParamBlocks = 148;
+constexpr int kParamBlocks = 148 * 8;
+constexpr int kParamGroups = 4;       // row groups per block (blockDim = kParamGroups * kParamCols)
+constexpr int kParamCols = 256;
 
 // partial[b][0..HF) = sum over block b's compute rows of gz      (bias)
 // partial[b][HF..2HF) = sum over its compute rows of der[h] z     (a_dst)
 // partial[b][2HF..3HF) = sum over its live rows of del[h] z      (a_src)
-// rows split into kParamBlocks contiguous ranges by the device counts: a
-// fixed summation order independent of the launch
-__global__ void k_gat_param_partial(const int32_t* R_dev, const int32_t* __restrict__ rows,
-                                    const float* __restrict__ gz, const float* __restrict__ der,
-                                    const int32_t* n_dev, const int32_t* __restrict__ live,
-                                    const float* __restrict__ del, const float* __restrict__ z, int HF, int H, int F,
-                                    float* __restrict__ partial) {
+// Rows are split into kParamBlocks contiguous ranges by the device counts;
+// inside a block, row group g takes rows g, g+4, ... and the groups are
+// combined in order: a fixed summation order independent of the launch.
+__global__ void __launch_bounds__(kParamGroups * kParamCols) k_gat_param_partial(
+    const int32_t* R_dev, const int32_t* __restrict__ rows, const float* __restrict__ gz,
+    const float* __restrict__ der, const int32_t* n_dev, const int32_t* __restrict__ live,
+    const float* __restrict__ del, const float* __restrict__ z, int HF, int H, int F, float* __restrict__ partial) {
+  __shared__ float red[kParamGroups][3][kParamCols];
   const int R = *R_dev, n = *n_dev;
   const int b = blockIdx.x;
-  for (int c = threadIdx.x; c < HF; c += blockDim.x) {
-    const int h = c / F;
+  const int grp = threadIdx.x / kParamCols, col = threadIdx.x % kParamCols;
+  const int r0 = (int)((long long)R * b / kParamBlocks), r1 = (int)((long long)R * (b + 1) / kParamBlocks);
+  const int k0 = (int)((long long)n * b / kParamBlocks), k1 = (int)((long long)n * (b + 1) / kParamBlocks);
+  for (int c0 = 0; c0 < HF; c0 += kParamCols) {
+    const int c = c0 + col;
     float sb = 0.f, sd = 0.f, ss = 0.f;
-    const int r0 = (int)((long long)R * b / kParamBlocks), r1 = (int)((long long)R * (b + 1) / kParamBlocks);
-    for (int r = r0; r < r1; ++r) {
-      sb += gz[(long long)r * HF + c];
-      sd = __fmaf_rn(der[(long long)r * H + h], z[(long long)rows[r] * HF + c], sd);
+    if (c < HF) {
+      const int h = c / F;
+      for (int r = r0 + grp; r < r1; r += kParamGroups) {
+        sb += gz[(long long)r * HF + c];
+        sd = __fmaf_rn(der[(long long)r * H + h], z[(long long)rows[r] * HF + c], sd);
+      }
+      for (int k = k0 + grp; k < k1; k += kParamGroups)
+        ss = __fmaf_rn(del[(long long)k * H + h], z[(long long)live[k] * HF + c], ss);
     }
-    const int k0 = (int)((long long)n * b / kParamBlocks), k1 = (int)((long long)n * (b + 1) / kParamBlocks);
-    for (int k = k0; k < k1; ++k) ss = __fmaf_rn(del[(long long)k * H + h], z[(long long)live[k] * HF + c], ss);
-    float* pb = partial + (long long)b * 3 * HF;
-    pb[c] = sb;
-    pb[HF + c] = sd;
-    pb[2 * HF + c] = ss;
+    red[grp][0][col] = sb;
+    red[grp][1][col] = sd;
+    red[grp][2][col] = ss;
+    __syncthreads();
+    if (grp == 0 && c < HF) {
+      float* pb = partial + (long long)b * 3 * HF;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        float v = red[0][q][col];
+#pragma unroll
+        for (int g = 1; g < kParamGroups; ++g) v += red[g][q][col];
+        pb[q * HF + c] = v;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -494,7 +558,7 @@ int hg_gat_param_grads(const int32_t* R_dev, const int32_t* rows, const float* g
                        float* partial, float* d_att_src, float* d_att_dst, float* d_bias, cudaStream_t stream) {
   const char* W = "hg_gat_param_grads";
   if (int st = gat_check(W, HF, H)) return st;
-  k_gat_param_partial<<<kParamBlocks, 256, 0, stream>>>(R_dev, rows, gz, der, n_live_dev, live, del, z, HF, H,
+  k_gat_param_partial<<<kParamBlocks, kParamGroups * kParamCols, 0, stream>>>(R_dev, rows, gz, der, n_live_dev, live, del, z, HF, H,
                                                          HF / H, partial);
   HG_LAUNCHED(W);
   k_gat_param_sum<<<grid_for(3LL * HF, 256), 256, 0, stream>>>(partial, HF, d_att_src, d_att_dst, d_bias);
