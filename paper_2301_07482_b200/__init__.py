@@ -15,6 +15,6 @@ from .nn import LayerKind, backward, cross_entropy, forward_pass, init_network, 
 from .sharding import ShardedFeatures  # noqa: F401
 from .sampler import (LayerBlock, LayeredSubgraph, SamplePlan, SubgraphProducer, batch_rng,  # noqa: F401
                       sample_layered, split_batches)
-from .trainer import (IterMetrics, PrunedBatch, TrainConfig, Trainer, evaluate, full_graph_logits, io_saving,  # noqa: F401
+from .trainer import (EmbeddingLog, IterMetrics, cosine_rows, epoch_mean_estimation_error, PrunedBatch, TrainConfig, Trainer, evaluate, full_graph_logits, io_saving,  # noqa: F401
                       make_batches,  # noqa: F401
                       prune_with_cache, run_plain_loop, write_metrics_csv)

@@ -338,7 +338,8 @@ int launch(const char* W, GemmShape sh, OpA a, OpB b, Epi e, int splits, cudaStr
     if (err != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(err));
     attr_dev = dev;
   }
-  dim3 grid((unsigned)((sh.M + kTM - 1) / kTM), (unsigned)n_tiles, (unsigned)splits);
+  const long long mt = (sh.M + kTM - 1) / kTM;   // R_max == 0 still launches one (exiting) CTA
+  dim3 grid((unsigned)(mt > 0 ? mt : 1), (unsigned)(n_tiles > 0 ? n_tiles : 1), (unsigned)splits);
   if (grid.x == 0) return kOk;
   k_tcgemm<OpA, OpB, Epi><<<grid, kThreads, smem, stream>>>(sh, a, b, e, n_tile, tmem_cols_for(n_tile));
   HG_LAUNCHED(W);

@@ -343,7 +343,10 @@ int launch(const char* W, const CUtensorMap& a, const CUtensorMap& b, Shape sh, 
     if (err != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(err));
     attr_dev = dev;
   }
-  dim3 grid((unsigned)((sh.M + kTM - 1) / kTM), (unsigned)n_tiles, (unsigned)splits);
+  // an empty row range (R_max == 0: everything pruned or injected) still
+  // launches one CTA, which exits at once (m0 >= M)
+  const long long mt = (sh.M + kTM - 1) / kTM;
+  dim3 grid((unsigned)(mt > 0 ? mt : 1), (unsigned)(n_tiles > 0 ? n_tiles : 1), (unsigned)splits);
   k_tsgemm<kMN, Epi><<<grid, kThreads, smem, stream>>>(a, b, sh, e, n_tile, tmem_cols_for(n_tile));
   HG_LAUNCHED(W);
   return kOk;

@@ -74,8 +74,8 @@ class TrainConfig:
             raise ValueError("batch_size, epochs and hidden must be >= 1")
         if not math.isfinite(self.eta):
             raise ValueError("eta must be finite")
-        if self.probe_every:
-            raise ValueError("estimation probes are out of scope for the device trainer (probe_every=0)")
+        if self.probe_every < 0:
+            raise ValueError("probe_every must be >= 0")
         if self.feature_placement not in ("hbm", "host"):
             raise ValueError("feature_placement must be 'hbm' or 'host'")
 
@@ -117,6 +117,51 @@ def io_saving(metrics) -> float:
     if base == 0:
         return 0.0
     return 1.0 - sum(m.fetched_bytes for m in metrics) / base
+
+
+def epoch_mean_estimation_error(metrics, epoch: int) -> float:
+    """trainer.py:126-132: mean probe error of an epoch (nan-free), or nan."""
+    vals = [m.estimation_error for m in metrics if m.epoch == epoch and not math.isnan(m.estimation_error)]
+    return float(np.mean(vals)) if vals else math.nan
+
+
+# ------------------------------------------------------------ drift probes
+# (trainer.py:231-272; host-side bookkeeping of device-computed embeddings)
+
+
+def cosine_rows(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Row-wise cosine; rows where either side has zero norm come back nan."""
+    na = np.linalg.norm(a, axis=1)
+    nb = np.linalg.norm(b, axis=1)
+    ok = (na > 0) & (nb > 0)
+    out = np.full(len(a), np.nan)
+    out[ok] = np.einsum("ij,ij->i", a[ok], b[ok]) / (na[ok] * nb[ok])
+    return out
+
+
+class EmbeddingLog:
+    """Exact-embedding snapshots of a tracked node set keyed by iteration
+    (trainer.py:244-272)."""
+
+    def __init__(self):
+        self.records: dict = {}
+
+    def record(self, iteration: int, ids, rows) -> None:
+        self.records[iteration] = (np.asarray(ids, dtype=np.int64).copy(), np.asarray(rows).copy())
+
+    def similarity(self, t: int, s: int) -> float:
+        if s < 0 or t - s < 0:
+            raise ValueError(f"need 0 <= s <= t, got t={t} s={s}")
+        if t not in self.records or t - s not in self.records:
+            raise ValueError(f"no snapshot for iterations {t} and {t - s}")
+        ids_a, rows_a = self.records[t]
+        ids_b, rows_b = self.records[t - s]
+        common, ia, ib = np.intersect1d(ids_a, ids_b, return_indices=True)
+        if len(common) == 0:
+            return math.nan
+        cos = cosine_rows(rows_a[ia], rows_b[ib])
+        cos = cos[~np.isnan(cos)]
+        return float(cos.mean()) if len(cos) else math.nan
 
 
 # ------------------------------------------------------ cache-aware pruning
@@ -298,7 +343,9 @@ class Trainer:
         self._dtype_code = _dtype_code(self.features)
         # host placement: pinned (cudaHostAlloc) memory is UVA-mapped, so the
         # kernels dereference the host pointer directly over PCIe
-        self.probe_nodes = probe_nodes
+        self.probe_nodes = None if probe_nodes is None else np.asarray(probe_nodes, dtype=np.int64)
+        self.embedding_log = EmbeddingLog() if cfg.probe_every > 0 else None
+        self._probe_record = None
         self.grad_hook = None   # callable(Grads) run between backward and SGD (data parallel)
         self.use_graphs = os.environ.get("HG_GRAPHS", "1") != "0"
         self._engines = {}
@@ -327,19 +374,48 @@ class Trainer:
 
     def train_iteration(self, iteration: int, epoch: int, sub: LayeredSubgraph, probe: bool = False) -> IterMetrics:
         """trainer.py:362-421. Returns IterMetrics (one device->host read)."""
-        if probe:
-            raise ValueError("estimation probes are out of scope for the device trainer")
         dev = self.device
         cache = self.cache
         before = cache.counters_vector().clone()
         labels_dev = torch.from_numpy(self.labels[sub.seeds].astype(np.int32)).pin_memory().to(dev, non_blocking=True)
-        loss_dev, baseline = self._step(iteration, sub, labels_dev)
+        exact_sub = sub.copy() if probe else None      # before pruning mutates the CSR2 ends
+        self._probe_err = None
+        loss_dev, baseline = self._step(iteration, sub, labels_dev, exact_sub=exact_sub)
         after = cache.counters_vector()
         host = torch.cat([loss_dev.view(1), (after - before).double(), after[CTR_VALID::LAYER_CTR_LEN]
                           [:cache.num_layers].double()]).cpu().tolist()
         loss, delta = host[0], [int(x) for x in host[1:1 + after.numel()]]
         valid = int(sum(host[1 + after.numel():]))
-        return self._metrics(iteration, epoch, len(sub.seeds), loss, delta, baseline, valid, sub)
+        m = self._metrics(iteration, epoch, len(sub.seeds), loss, delta, baseline, valid, sub)
+        if probe:
+            m.estimation_error = float(self._probe_err.item())
+            if self.embedding_log is not None and self._probe_record is not None:
+                self.embedding_log.record(iteration, *self._probe_record)
+        return m
+
+    def _estimation_probe(self, exact_sub: LayeredSubgraph, mixed_logits: torch.Tensor, stream) -> torch.Tensor:
+        """trainer.py:345-358: relative error of the mixed (cache-pruned)
+        logits against an exact recompute of the unpruned subgraph at the
+        current weights (device scalar, fp64). Records the exact layer
+        `probe_layer` embeddings of the tracked probe nodes."""
+        dev = self.device
+        b0 = exact_sub.layers[0]
+        n0 = b0.num_src
+        h = torch.empty((n0, self.feature_dim), dtype=torch.float32, device=dev)
+        every = torch.arange(n0, dtype=torch.int32, device=dev)
+        scratch_ctr = torch.zeros(8, dtype=torch.int64, device=dev)   # not the trainer's I/O counters
+        load_features_dev(_dev_count(n0, dev), n0, every, b0.src_nodes, None, self.features, self.features,
+                          self.feature_dim, self._dtype_code, h, scratch_ctr, _lib.stream_ptr(stream))
+        exact = forward_pass(self.network, exact_sub.layers, h)
+        diff = torch.linalg.vector_norm((mixed_logits - exact.logits).double())
+        base = torch.linalg.vector_norm(exact.logits.double())
+        self._probe_record = None
+        li = self.cfg.probe_layer
+        if self.probe_nodes is not None and 1 <= li <= exact_sub.num_layers:
+            frontier = exact_sub.layers[li - 1].dst_nodes.long()
+            present = torch.isin(frontier, torch.as_tensor(self.probe_nodes, device=dev))
+            self._probe_record = (frontier[present].cpu().numpy(), exact.h_layers[li - 1][present].cpu().numpy())
+        return diff / torch.clamp(base, min=1e-30)
 
     # ------------------------------------------- engine path (CUDA graph)
 
@@ -428,7 +504,7 @@ class Trainer:
         return self._metrics(iteration, epoch, len(seeds), loss, delta, n_src0 * self.row_bytes, valid, None,
                              prune_writes=delta[cache.num_layers * LAYER_CTR_LEN + GCTR_PRUNE_WRITES])
 
-    def _step(self, iteration: int, sub: LayeredSubgraph, labels_dev: torch.Tensor):
+    def _step(self, iteration: int, sub: LayeredSubgraph, labels_dev: torch.Tensor, exact_sub=None):
         dev = self.device
         stream = torch.cuda.current_stream(dev)
         sp = _lib.stream_ptr(stream)
@@ -447,6 +523,8 @@ class Trainer:
             h = t.h_out
         B = int(sub.seeds.shape[0])
         d_h, loss_dev = cross_entropy_dev(tapes[-1].h_out, labels_dev, B, net.dims[-1], sp)
+        if exact_sub is not None:       # probe between the forward and the SGD step (trainer.py:376-381)
+            self._probe_err = self._estimation_probe(exact_sub, tapes[-1].h_out, stream)
         grads = net.new_grads(zero=False)
         norms = [None] * L
         for l in range(L - 1, -1, -1):
@@ -497,8 +575,21 @@ class Trainer:
         cfg = self.cfg
         batches = make_batches(self.train_ids, cfg)
         per_epoch = max(1, math.ceil(len(self.train_ids) / cfg.batch_size))
+        pe = cfg.probe_every
+
+        def probing(it):
+            return pe > 0 and it % pe == 0
+
         for iteration, seeds in enumerate(batches):
-            nxt = (iteration + 1, batches[iteration + 1]) if iteration + 1 < len(batches) else None
+            if probing(iteration):
+                # probe iterations run the eager API path (the exact recompute
+                # sits between the forward and the SGD step)
+                m = self.train_iteration(iteration, iteration // per_epoch, self.sample(iteration, seeds), probe=True)
+                self.metrics.append(m)
+                continue
+            nxt = None
+            if iteration + 1 < len(batches) and not probing(iteration + 1):
+                nxt = (iteration + 1, batches[iteration + 1])
             self.metrics.append(self.train_step(iteration, iteration // per_epoch, seeds, next_batch=nxt))
         return self.metrics
 
