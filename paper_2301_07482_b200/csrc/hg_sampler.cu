@@ -193,8 +193,29 @@ __device__ __forceinline__ u128 pcg_jump_c(const JumpTableC& tab, u128 s, unsign
 // sorted-unique frontier). task_row[t] = first row whose stream offset is
 // >= t*C (a lower bound on cand_off), task_row[T] = F; meta = {T, C}.
 constexpr int kMaxTasks = 1 << 18;
+
+// Hub rows (more than kHuge candidates, fanout <= 32) are split into
+// segments of kSegC candidates, one warp each (k_select_huge: exact top-fanout
+// of the segment by (key53, j)), then merged per row (k_merge_huge). The
+// top-fanout of a row is contained in the union of its segments' top-fanout,
+// so the result is exact; without the split one warp walks a 56K-candidate
+// hub alone (papers100M shape) and sets the layer's duration.
+constexpr long long kHuge = 4096;
+constexpr int kSegC = 2048;
+constexpr int kMaxSegs = 1 << 16;     // per layer; hubs beyond stay on the warp path
+struct HugeState {
+  int* ctr;             // [0] accepted hub rows, [1] segments claimed
+  int32_t* rows;        // [F_max] accepted hub rows
+  int32_t* base;        // [F_max] first segment of each accepted hub
+  uint8_t* flag;        // [F_max] 1 = row handled by the hub path
+  int32_t* seg_row;     // [kMaxSegs] row of each segment (-1 unused)
+  int32_t* seg_s;       // [kMaxSegs] segment index within its row
+  unsigned long long* seg_key;   // [kMaxSegs * 32] key53 of the segment's picks
+  int32_t* seg_j;       // [kMaxSegs * 32] row-global candidate position
+};
+
 __global__ void k_task_bounds(const int32_t* F_dev, const int64_t* __restrict__ cand_off, int32_t* __restrict__ task_row,
-                              long long* __restrict__ meta) {
+                              long long* __restrict__ meta, int fanout, HugeState hs) {
   const int F = *F_dev;
   const long long total = cand_off[F];
   long long C = (total + 148 * 32 - 1) / (148 * 32);       // aim for >= 32 tasks per SM
@@ -211,6 +232,24 @@ __global__ void k_task_bounds(const int32_t* F_dev, const int64_t* __restrict__ 
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
     const long long a = cand_off[j], b = cand_off[j + 1];
     for (long long t = a / C + 1; t * C <= b && t < T; ++t) task_row[t] = j + 1;
+    uint8_t huge = 0;
+    if (fanout <= 32 && b - a > kHuge) {
+      const int nseg = (int)((b - a + kSegC - 1) / kSegC);
+      const int base = atomicAdd(&hs.ctr[1], nseg);
+      if (base + nseg <= kMaxSegs) {
+        huge = 1;
+        const int i = atomicAdd(&hs.ctr[0], 1);
+        hs.rows[i] = j;
+        hs.base[i] = base;
+        for (int q = 0; q < nseg; ++q) {
+          hs.seg_row[base + q] = j;
+          hs.seg_s[base + q] = q;
+        }
+      } else {
+        for (int q = base; q < kMaxSegs && q < base + nseg; ++q) hs.seg_row[q] = -1;
+      }
+    }
+    hs.flag[j] = huge;
   }
 }
 
@@ -247,7 +286,8 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select(
     const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end,
     const int32_t* __restrict__ frontier, const int32_t* F_dev, int fanout, const SampState* ss,
     const int64_t* __restrict__ cand_off, const int32_t* __restrict__ blk_off, int32_t* __restrict__ src_flat,
-    int32_t* __restrict__ col_local, const int32_t* __restrict__ task_row, const long long* __restrict__ task_meta) {
+    int32_t* __restrict__ col_local, const int32_t* __restrict__ task_row, const long long* __restrict__ task_meta,
+    const uint8_t* __restrict__ huge_flag) {
   __shared__ JumpTableC tab;
   __shared__ u128 dA[33], dC[33];
   const u128 s0{ss->st_hi, ss->st_lo}, inc{ss->inc_hi, ss->inc_lo};
@@ -293,6 +333,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select(
         deg_l = g_end[v] - lo_l;
         off_l = cand_off[r0 + lane];
         out_l = blk_off[r0 + lane];
+        if (huge_flag && huge_flag[r0 + lane]) deg_l = 0;   // selected by k_select_huge / k_merge_huge
       }
       for (int q = 0; q < nr; ++q) {
         const long long lo = __shfl_sync(0xffffffffu, lo_l, q);
@@ -410,6 +451,101 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select(
   kt_end(kt);
 }
 
+// one warp per hub segment: exact top-fanout (packed key53 << 11 | j_local)
+// of kSegC consecutive candidates, written as (key53, row-global j)
+__global__ void __launch_bounds__(kSelThreads, 4) k_select_huge(
+    const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end, const int32_t* __restrict__ frontier,
+    int fanout, const SampState* ss, const int64_t* __restrict__ cand_off, HugeState hs) {
+  __shared__ JumpTableC tab;
+  const u128 s0{ss->st_hi, ss->st_lo}, inc{ss->inc_hi, ss->inc_lo};
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) {
+    (&tab.A[0][0])[t] = (&g_jump.A[0][0])[t];
+    (&tab.C[0][0])[t] = mul128(inc, (&g_jump.S[0][0])[t]);
+  }
+  __syncthreads();
+  const int nseg = min(hs.ctr[1], kMaxSegs);
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const u128 a32 = tab.A[1][2];
+  const u128 c32 = tab.C[1][2];
+  for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < nseg; g += warps) {
+    const int row = hs.seg_row[g];
+    if (row < 0) continue;
+    const int sidx = hs.seg_s[g];
+    const int v = frontier[row];
+    const long long deg = g_end[v] - g_start[v];
+    const long long j0 = (long long)sidx * kSegC;
+    const long long len = deg - j0 < kSegC ? deg - j0 : kSegC;
+    const unsigned long long k0 = ss->stream_pos + (unsigned long long)cand_off[row] + (unsigned long long)j0;
+    u128 s = pcg_jump_c(tab, s0, k0 + (unsigned long long)lane + 1ull);
+    unsigned long long best = ~0ull;
+    for (long long c = 0; c < len; c += 32) {
+      const long long jj = c + lane;
+      const bool valid = jj < len;
+      unsigned long long key = valid ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
+      if (c + 32 < len) s = fma128(a32, s, c32);
+      if (c == 0) {
+        sort_first_chunk(key, len);
+        best = key;
+        continue;
+      }
+      unsigned long long thr = __shfl_sync(0xffffffffu, best, fanout - 1);
+      unsigned m = __ballot_sync(0xffffffffu, key < thr);
+      while (m) {
+        const int l = __ffs(m) - 1;
+        const unsigned long long cand = __shfl_sync(0xffffffffu, key, l);
+        const int pos = __popc(__ballot_sync(0xffffffffu, best < cand));
+        const unsigned long long up = __shfl_up_sync(0xffffffffu, best, 1);
+        if (lane == pos) best = cand;
+        else if (lane > pos) best = up;
+        thr = __shfl_sync(0xffffffffu, best, fanout - 1);
+        m &= ~(1u << l);
+        m &= __ballot_sync(0xffffffffu, key < thr);
+      }
+    }
+    const int cnt = (int)(len < fanout ? len : fanout);
+    hs.seg_key[(long long)g * 32 + lane] = lane < cnt ? (best >> 11) : ~0ull;
+    hs.seg_j[(long long)g * 32 + lane] = lane < cnt ? (int32_t)(j0 + (long long)(best & 2047ull)) : 0x7fffffff;
+  }
+}
+
+// one warp per accepted hub row: top-fanout by (key53, j) over its segments'
+// picks, emitted in key order like every other row
+__global__ void __launch_bounds__(256) k_merge_huge(const int64_t* __restrict__ g_start,
+                                                    const int32_t* __restrict__ frontier, int fanout,
+                                                    const int64_t* __restrict__ cand_off,
+                                                    const int32_t* __restrict__ blk_off, int32_t* __restrict__ src_flat,
+                                                    int32_t* __restrict__ col_local, HugeState hs) {
+  const int nh = hs.ctr[0];
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nh; i += warps) {
+    const int row = hs.rows[i];
+    const int base = hs.base[i];
+    const long long deg = cand_off[row + 1] - cand_off[row];
+    const int nseg = (int)((deg + kSegC - 1) / kSegC);
+    unsigned long long bk = ~0ull;
+    unsigned bj = ~0u;
+    for (int g = base; g < base + nseg; ++g) {
+      unsigned long long key = hs.seg_key[(long long)g * 32 + lane];
+      unsigned j = (unsigned)hs.seg_j[(long long)g * 32 + lane];
+      if (lane >= fanout) {
+        key = ~0ull;
+        j = ~0u;
+      }
+      bitonic_sort32(key, j);
+      unsigned long long rk = __shfl_sync(0xffffffffu, key, 31 - lane);
+      unsigned rj = __shfl_sync(0xffffffffu, j, 31 - lane);
+      if (kj_less(rk, rj, bk, bj)) {
+        bk = rk;
+        bj = rj;
+      }
+      bitonic_merge32(bk, bj);
+    }
+    if (lane < fanout) put_pick(src_flat, col_local, blk_off[row] + lane, g_start[frontier[row]] + (long long)bj);
+  }
+}
+
 struct PopWord {
   const uint32_t* bitmap;
   __device__ int operator()(long long i) const { return __popc(bitmap[i]); }
@@ -503,12 +639,16 @@ int ensure_jump_table() {
 
 using namespace hg;
 
+static long long huge_scratch_bytes(long long F_max) {
+  return 64 + (F_max + 16) * 9 + (long long)kMaxSegs * (4 + 4 + 32 * 8 + 32 * 4) + 256;
+}
+
 extern "C" {
 
 long long hg_sample_layer_scratch_bytes(long long F_max, long long num_nodes) {
   long long words = (num_nodes + 31) / 32;
   return (scan_tiles(F_max) + 1) * (long long)sizeof(I64x2) + (scan_tiles(words) + 1) * 4 + 256 +
-         (long long)(kMaxTasks + 2) * 4 + 64;
+         (long long)(kMaxTasks + 2) * 4 + 64 + huge_scratch_bytes(F_max);
 }
 
 int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t* g_col, long long num_nodes,
@@ -528,6 +668,18 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   long long* task_meta = reinterpret_cast<long long*>(part_w + scan_tiles(words) + 2);
   task_meta = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(task_meta) + 15) & ~uintptr_t(15));
   int32_t* task_row = reinterpret_cast<int32_t*>(task_meta + 2);
+  // hub-row state after the task table (16-byte aligned pieces)
+  char* hp = reinterpret_cast<char*>(task_row + kMaxTasks + 2);
+  hp = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(hp) + 15) & ~uintptr_t(15));
+  HugeState hs;
+  hs.ctr = reinterpret_cast<int*>(hp);
+  hs.seg_key = reinterpret_cast<unsigned long long*>(hp + 64);
+  hs.seg_j = reinterpret_cast<int32_t*>(hs.seg_key + (long long)kMaxSegs * 32);
+  hs.seg_row = hs.seg_j + (long long)kMaxSegs * 32;
+  hs.seg_s = hs.seg_row + kMaxSegs;
+  hs.rows = hs.seg_s + kMaxSegs;
+  hs.base = hs.rows + (F_max + 16);
+  hs.flag = reinterpret_cast<uint8_t*>(hs.base + (F_max + 16));
 
   SampState* ss = reinterpret_cast<SampState*>(state_dev);
   k_stamp<<<grid_for(F_max, 256), 256, 0, stream>>>(frontier, F_dev, ss, g2l, src_out);
@@ -537,7 +689,8 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
                           EmitDegCount{cand_off, blk_off, blk_end, dst_deg, fanout, g_start, g_end, frontier},
                           TotalDegCount{F_dev, cand_off, blk_off, counts_dev}, stream);
   if (st) return st;
-  k_task_bounds<<<grid_for(F_max, 256), 256, 0, stream>>>(F_dev, cand_off, task_row, task_meta);
+  HG_CHECK_CUDA(W, cudaMemsetAsync(hs.ctr, 0, 8, stream));
+  k_task_bounds<<<grid_for(F_max, 256), 256, 0, stream>>>(F_dev, cand_off, task_row, task_meta, fanout, hs);
   HG_LAUNCHED(W);
   // persistent warps over the tasks; HG_SEL_BLOCKS caps the grid (leaves SMs
   // to the training stream that runs concurrently with the pipelined sampler)
@@ -551,13 +704,19 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
     if (sel_cap < 1) sel_cap = 148 * 4;
   }
   const unsigned sel_grid = (unsigned)sel_cap;
-  if (fanout <= 32)
+  if (fanout <= 32) {
     k_select<true><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
-                                                          blk_off, src_flat, col_local, task_row, task_meta);
-  else
+                                                          blk_off, src_flat, col_local, task_row, task_meta, hs.flag);
+    HG_LAUNCHED(W);
+    k_select_huge<<<148 * 4, kSelThreads, 0, stream>>>(g_start, g_end, frontier, fanout, ss, cand_off, hs);
+    HG_LAUNCHED(W);
+    k_merge_huge<<<148, 256, 0, stream>>>(g_start, frontier, fanout, cand_off, blk_off, src_flat, col_local, hs);
+    HG_LAUNCHED(W);
+  } else {
     k_select<false><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
-                                                           blk_off, src_flat, col_local, task_row, task_meta);
-  HG_LAUNCHED(W);
+                                                           blk_off, src_flat, col_local, task_row, task_meta, nullptr);
+    HG_LAUNCHED(W);
+  }
   k_pick<<<grid_for(F_max * (long long)fanout, 256), 256, 0, stream>>>(g_col, counts_dev, ss, g2l, bitmap, src_flat,
                                                                        col_local);
   HG_LAUNCHED(W);

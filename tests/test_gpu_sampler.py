@@ -149,3 +149,28 @@ def test_producer_matches_sequential():
     assert [i for i, _ in got] == list(range(5))
     for (_, a), b in zip(got, seq):
         assert_sub_equal(_np_blocks(a), _np_blocks(b))
+
+
+@pytest.mark.parametrize("fanouts", [(5, 3), (15, 10), (32,)])
+def test_hub_rows_split_across_warps_vs_oracle(fanouts):
+    """Rows with more than 4096 candidates take the segmented hub path
+    (k_select_huge + k_merge_huge): several hubs of 4097 .. 30000 in-edges
+    (multi-edges and ties included) must sample bit-exactly like the oracle."""
+    hg = _hg()
+    rng = np.random.default_rng(77)
+    n = 40000
+    hubs = [0, 1, 2, 3, 7]
+    degs = [4097, 6000, 12345, 30000, 8192]
+    src = [rng.integers(0, n, d) for d in degs]
+    dst = [np.full(d, h) for h, d in zip(hubs, degs)]
+    # background edges so the second layer has ordinary rows too
+    bs, bd = rng.integers(0, n, 60000), rng.integers(0, n, 60000)
+    s, e, c = csr2_from_edges(np.concatenate(src + [bs]), np.concatenate(dst + [bd]), n)
+    g = hg.csr2_from_arrays(s, e, c)
+    for idx in range(3):
+        seeds = np.concatenate([hubs, rng.choice(np.arange(10, n), size=59, replace=False)])
+        want = osample(s, e, c, n, seeds, fanouts, obatch_rng(9, idx))
+        got = hg.sample_layered(g, seeds, hg.SamplePlan(fanouts, len(seeds), 9), hg.batch_rng(9, idx))
+        assert_sub_equal(_np_blocks(got), [
+            {"dst": b.dst_nodes, "src": b.src_nodes, "start": b.start, "end": b.end, "col": b.col,
+             "dst_deg": b.dst_deg, "src_deg": b.src_deg} for b in want.layers])
