@@ -352,17 +352,19 @@ def main():
     for s in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
         it = mine[s]
         nb = (mine[s + 1], batches[mine[s + 1]])
-        m = tr.train_step(it, 0, batches[it], next_batch=nb)
+        m = tr.train_step(it, 0, batches[it], next_batch=nb, sync=False)
         # this step uploads the announced next batch's words (PCG64 state,
         # iteration, seed ids, labels), or its own when none was announced
         h2d += (12 + 2 * BATCH) * 4
         d2h += (1 + tr.cache.counters_vector().numel() + tr.cache.num_layers) * 8
     torch.cuda.synchronize()
     t_e2e = max_over_ranks(time.perf_counter() - t0)
+    m = m.result()
     caps_e2e = sum(e.captures for e in tr._engines.values()) - caps0 - caps_value
     e2e = {"value": BATCH * world * args.steps / t_e2e, "unit": "seeds/s",
            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-           "api": "Trainer.train_step (host seeds in, IterMetrics read back every step)"}
+           "api": "Trainer.train_step (host seeds in via pinned staging, IterMetrics counters copied to pinned "
+                  "host memory every step, sync=False: the host enqueues step s+1 while step s runs)"}
 
     # ---- phase timeline of the replayed step (after timing; %globaltimer marks) ----
     eng = tr._engine(BATCH)

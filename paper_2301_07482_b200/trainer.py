@@ -278,6 +278,29 @@ class _EngineLast:
         return (self, self.out["tapes"], self.out["grads"], self.norms)[i]
 
 
+class PendingMetrics:
+    """IterMetrics of a `Trainer.train_step(..., sync=False)` step whose
+    counters are still in flight (device -> pinned host copy)."""
+
+    def __init__(self, trainer, host_buf, event, iteration, epoch, num_seeds, nv):
+        self._tr, self._buf, self._ev = trainer, host_buf, event
+        self._args = (iteration, epoch, num_seeds, nv)
+        self._m = None
+
+    def result(self) -> IterMetrics:
+        if self._m is None:
+            self._ev.synchronize()
+            it, ep, ns, nv = self._args
+            self._m = self._tr._finish_pending(self._buf.tolist(), it, ep, ns, nv)
+            self._buf = None
+        return self._m
+
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self.result(), name)
+
+
 def make_batches(train_ids, cfg: TrainConfig) -> list:
     out = []
     for epoch in range(cfg.epochs):
@@ -481,18 +504,31 @@ class Trainer:
         self._last_engine = (eng, out)
         return out["loss"]
 
-    def train_step(self, iteration: int, epoch: int, seeds, next_batch=None) -> IterMetrics:
+    def train_step(self, iteration: int, epoch: int, seeds, next_batch=None, sync: bool = True):
         """Sample + train one batch through the engine and read IterMetrics
         back (trainer.py:362-421 semantics, sampling included).
-        `next_batch=(iteration, seeds)` lets the step sample that batch ahead."""
+        `next_batch=(iteration, seeds)` lets the step sample that batch ahead.
+        sync=False: the metrics are copied device -> pinned host memory
+        asynchronously and a PendingMetrics is returned (IterMetrics on
+        `.result()` or on first attribute access), so the host can enqueue
+        the next step while this one runs."""
         cache = self.cache
         before = cache.counters_vector().clone()
         eng, out = self._engine_step(iteration, seeds, next_batch)
         after = cache.counters_vector()
         n_src0 = out["blocks"][0].n_src_dev
-        host = torch.cat([out["loss"].view(1), (after - before).double(),
-                          after[CTR_VALID::LAYER_CTR_LEN][:cache.num_layers].double(), n_src0.double(),
-                          out["counts"].double()]).cpu().tolist()
+        dev_buf = torch.cat([out["loss"].view(1), (after - before).double(),
+                             after[CTR_VALID::LAYER_CTR_LEN][:cache.num_layers].double(), n_src0.double(),
+                             out["counts"].double()])
+        if not sync:
+            host_buf = torch.empty(dev_buf.shape, dtype=dev_buf.dtype, pin_memory=True)
+            host_buf.copy_(dev_buf, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            cache.end_iteration(iteration)
+            self._last_engine = (eng, out)
+            return PendingMetrics(self, host_buf, ev, iteration, epoch, len(seeds), after.numel())
+        host = dev_buf.cpu().tolist()
         nv = after.numel()
         loss, delta = host[0], [int(x) for x in host[1:1 + nv]]
         valid = int(sum(host[1 + nv:1 + nv + cache.num_layers]))
@@ -502,6 +538,14 @@ class Trainer:
         self._last_engine = (eng, out)
         self.last = _EngineLast(out, counts)
         return self._metrics(iteration, epoch, len(seeds), loss, delta, n_src0 * self.row_bytes, valid, None,
+                             prune_writes=delta[cache.num_layers * LAYER_CTR_LEN + GCTR_PRUNE_WRITES])
+
+    def _finish_pending(self, host, iteration, epoch, num_seeds, nv):
+        cache = self.cache
+        loss, delta = host[0], [int(x) for x in host[1:1 + nv]]
+        valid = int(sum(host[1 + nv:1 + nv + cache.num_layers]))
+        n_src0 = int(host[1 + nv + cache.num_layers])
+        return self._metrics(iteration, epoch, num_seeds, loss, delta, n_src0 * self.row_bytes, valid, None,
                              prune_writes=delta[cache.num_layers * LAYER_CTR_LEN + GCTR_PRUNE_WRITES])
 
     def _step(self, iteration: int, sub: LayeredSubgraph, labels_dev: torch.Tensor, exact_sub=None):

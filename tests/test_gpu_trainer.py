@@ -220,3 +220,20 @@ def test_graph_replay_bitwise_equals_eager_engine():
         runs.append((hashlib.sha256(tr.network.checksum_bytes()).hexdigest(),
                      [(m.loss, m.hits, m.admissions, m.fetched_bytes) for m in ms]))
     assert runs[0] == runs[1]
+
+
+def test_async_metrics_equal_sync_metrics():
+    """train_step(sync=False) returns PendingMetrics that resolve to the same
+    IterMetrics as the synchronous call (same run, bitwise)."""
+    import paper_2301_07482_b200 as hg
+    ds, g = _pl3000()
+    cfg = hg.TrainConfig(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=1, eta=0.05,
+                         kind=hg.LayerKind.SAGE_MEAN, p_grad=0.9, t_stale=5, seed=4)
+    batches = hg.make_batches(ds.train_ids, cfg)[:16]
+    runs = []
+    for sync in (True, False):
+        tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
+        ms = [tr.train_step(i, 0, s, next_batch=(i + 1, batches[i + 1]) if i + 1 < len(batches) else None,
+                            sync=sync) for i, s in enumerate(batches)]
+        runs.append([m if sync else m.result() for m in ms])
+    assert runs[0] == runs[1]
