@@ -1,6 +1,7 @@
 // Library-wide entry points: version, last error, launch checking.
 #include "hgb200.h"
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -23,6 +24,15 @@ __global__ void k_mark_time(unsigned long long* slot) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   *slot = t;
+}
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("HG_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 int check_launch(const char* where) {

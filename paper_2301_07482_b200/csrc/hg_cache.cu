@@ -64,6 +64,7 @@ struct NormKeyDecomposer {
 __global__ void k_norm_keys(const int32_t* n_dev, int n_max, double p_grad, const int32_t* __restrict__ live,
                             const int32_t* __restrict__ src_nodes, const double* __restrict__ norms,
                             NormKey* __restrict__ keys, int32_t* __restrict__ vals, long long* ctr) {
+  pdl_wait();
   const int n = *n_dev;
   if (blockIdx.x == 0 && threadIdx.x == 0) ctr[kCtrK] = (long long)floor(p_grad * (double)n);  // cache.py:190
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_max; i += gridDim.x * blockDim.x) {
@@ -81,6 +82,7 @@ __global__ void k_rank_admit(const int32_t* n_dev, const NormKey* __restrict__ s
                              const uint8_t* __restrict__ computed_flag, int32_t* __restrict__ row_of,
                              int32_t* __restrict__ row_owner, uint8_t* __restrict__ wflag,
                              uint8_t* __restrict__ retained, long long* ctr) {
+  pdl_wait();
   unsigned long long* c = reinterpret_cast<unsigned long long*>(ctr);
   const int n = *n_dev;
   const long long k = ctr[kCtrK];
@@ -112,6 +114,7 @@ struct StoreNWrite {
 
 __global__ void k_release_writes(const int32_t* __restrict__ wlist, const NormKey* __restrict__ skeys, int cap,
                                  int32_t* __restrict__ row_of, int32_t* __restrict__ row_owner, long long* ctr) {
+  pdl_wait();
   cap = (int)ctr[kCtrCapacity];  // logical ring size lives on the device (grows at sweeps)
   const long long nw = ctr[kCtrNWrite];
   const long long w0 = nw >= cap ? nw - cap : 0;
@@ -129,6 +132,7 @@ __global__ void k_release_writes(const int32_t* __restrict__ wlist, const NormKe
 
 __global__ void k_ring_scan(int cap, const int32_t* it_dev, double t_stale, int t_inf, int32_t* __restrict__ row_of,
                             int32_t* __restrict__ row_owner, const int32_t* __restrict__ admit_iter, long long* ctr) {
+  pdl_wait();
   cap = (int)ctr[kCtrCapacity];  // logical ring size lives on the device (grows at sweeps)
   const int it = *it_dev;
   const long long nw = ctr[kCtrNWrite];
@@ -161,6 +165,7 @@ __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* _
                              float* __restrict__ table,
                              int32_t* __restrict__ row_of, int32_t* __restrict__ row_owner,
                              int32_t* __restrict__ admit_iter, long long* ctr) {
+  pdl_wait();
   cap = (int)ctr[kCtrCapacity];  // logical ring size lives on the device (grows at sweeps)
   const long long nw = ctr[kCtrNWrite];
   const long long header = ctr[kCtrHeader];
@@ -192,6 +197,7 @@ __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* _
 }
 
 __global__ void k_commit(int cap, long long* ctr) {
+  pdl_wait();
   cap = (int)ctr[kCtrCapacity];  // logical ring size lives on the device (grows at sweeps)
   const long long nw = ctr[kCtrNWrite];
   const bool wrap_all = nw >= cap;
@@ -206,6 +212,7 @@ __global__ void k_commit(int cap, long long* ctr) {
 __global__ void k_refresh(const long long* ctr, const uint8_t* __restrict__ retained,
                           const NormKey* __restrict__ skeys, const int32_t* __restrict__ row_of,
                           int32_t* __restrict__ admit_iter, const int32_t* it_dev) {
+  pdl_wait();
   const long long k = ctr[kCtrK];
   const int it = *it_dev;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
@@ -217,6 +224,7 @@ __global__ void k_refresh(const long long* ctr, const uint8_t* __restrict__ reta
 
 __global__ void k_iota_deg(long long n, const int64_t* __restrict__ start, const int64_t* __restrict__ end,
                            long long* __restrict__ deg, int32_t* __restrict__ ids) {
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     deg[i] = end[i] - start[i];
     ids[i] = (int32_t)i;
@@ -224,6 +232,7 @@ __global__ void k_iota_deg(long long n, const int64_t* __restrict__ start, const
 }
 __global__ void k_region_rows(long long k, const int32_t* __restrict__ sorted_ids, int32_t* __restrict__ chosen,
                               int32_t* __restrict__ feature_row_of) {
+  pdl_wait();
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < k; p += (long long)gridDim.x * blockDim.x) {
     const int id = sorted_ids[p];
     const int row = (int)(k - 1 - p);  // max-degree node last (cache.py:348)
@@ -275,17 +284,17 @@ int hg_cache_rank(const int32_t* n_dev, int n_max, double p_grad, const int32_t*
   size_t tmp_bytes = (size_t)(scratch_bytes - ((char*)tmp - p));
   const bool radix = sort_mode(n_max) == kSortRadix;
   // the merge sort is in place: keys go straight to keys_out / vals_out
-  k_norm_keys<<<grid_for(n_max, 256), 256, 0, stream>>>(n_dev, n_max, p_grad, live, src_nodes, norms,
+  { const cudaError_t _pe = hg::launch_pdl(k_norm_keys, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev, n_max, p_grad, live, src_nodes, norms,
                                                         radix ? keys_in : keys_out, radix ? vals_in : vals_out,
-                                                        layer_ctr);
+                                                        layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   cudaError_t e = radix ? cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, vals_out, n_max,
                                                           NormKeyDecomposer{}, stream)
                         : cub::DeviceMergeSort::SortPairs(tmp, tmp_bytes, keys_out, vals_out, n_max, NormKeyLess{},
                                                           stream);
   if (e != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(e));
-  k_rank_admit<<<grid_for(n_max, 256), 256, 0, stream>>>(n_dev, keys_out, vals_out, live, computed_flag, row_of,
-                                                         row_owner, wflag, retained, layer_ctr);
+  { const cudaError_t _pe = hg::launch_pdl(k_rank_admit, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev, keys_out, vals_out, live, computed_flag, row_of,
+                                                         row_owner, wflag, retained, layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return scan_launch<int>(W, FlagU8{wflag}, DevCount{n_dev}, n_max, part, EmitCompact{wlist}, StoreNWrite{layer_ctr},
                           stream);
@@ -308,18 +317,18 @@ int hg_cache_write(int n_max, int cap, int H, const int32_t* it_dev, double t_st
   uint8_t* retained = wflag + nn;
   const int t_inf = isinf(t_stale) ? 1 : 0;
   const long long nmax = n_max;  // rows touched per update <= n_write <= n_max (a wrap needs n_write >= capacity)
-  k_release_writes<<<grid_for(n_max, 256), 256, 0, stream>>>(wlist, keys_out, cap, row_of, row_owner, layer_ctr);
+  { const cudaError_t _pe = hg::launch_pdl(k_release_writes, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, wlist, keys_out, cap, row_of, row_owner, layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
-  k_ring_scan<<<grid_for(nmax, 256), 256, 0, stream>>>(cap, it_dev, t_stale, t_inf, row_of, row_owner, admit_iter,
-                                                       layer_ctr);
+  { const cudaError_t _pe = hg::launch_pdl(k_ring_scan, dim3(grid_for(nmax, 256)), dim3(256), 0, stream, cap, it_dev, t_stale, t_inf, row_of, row_owner, admit_iter,
+                                                       layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
-  k_write_rows<<<grid_for((long long)n_max * 32, 256, 148 * 16), 256, 0, stream>>>(
-      wlist, keys_out, vals_out, live, emb, H, cap, it_dev, table, row_of, row_owner, admit_iter, layer_ctr);
+  { const cudaError_t _pe = hg::launch_pdl(k_write_rows, dim3(grid_for((long long)n_max * 32, 256, 148 * 16)), dim3(256), 0, stream, 
+      wlist, keys_out, vals_out, live, emb, H, cap, it_dev, table, row_of, row_owner, admit_iter, layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
-  k_commit<<<1, 1, 0, stream>>>(cap, layer_ctr);
+  { const cudaError_t _pe = hg::launch_pdl(k_commit, dim3(1), dim3(1), 0, stream, cap, layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   if (refresh_retained) {
-    k_refresh<<<grid_for(n_max, 256), 256, 0, stream>>>(layer_ctr, retained, keys_out, row_of, admit_iter, it_dev);
+    { const cudaError_t _pe = hg::launch_pdl(k_refresh, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, layer_ctr, retained, keys_out, row_of, admit_iter, it_dev); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
     HG_LAUNCHED(W);
   }
   return kOk;
@@ -347,12 +356,12 @@ int hg_feature_region(const int64_t* g_start, const int64_t* g_end, long long n,
   int32_t* ids_out = ids + n + 16;
   void* tmp = ids_out + n + 16;
   size_t tmp_bytes = (size_t)(scratch_bytes - ((char*)tmp - p));
-  k_iota_deg<<<grid_for(n, 256), 256, 0, stream>>>(n, g_start, g_end, deg, ids);
+  { const cudaError_t _pe = hg::launch_pdl(k_iota_deg, dim3(grid_for(n, 256)), dim3(256), 0, stream, n, g_start, g_end, deg, ids); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   cudaError_t e =
       cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, deg, deg_out, ids, ids_out, (int)n, 0, 64, stream);
   if (e != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(e));
-  k_region_rows<<<grid_for(k, 256), 256, 0, stream>>>(k, ids_out, chosen, feature_row_of);
+  { const cudaError_t _pe = hg::launch_pdl(k_region_rows, dim3(grid_for(k, 256)), dim3(256), 0, stream, k, ids_out, chosen, feature_row_of); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }

@@ -119,6 +119,35 @@ __device__ __forceinline__ void kt_end(KTimer* kt) {
   }
 }
 
+// Programmatic dependent launch (PDL): kernels launched with launch_pdl may
+// be scheduled while their predecessor in the stream is still finishing (its
+// launch latency overlaps the predecessor's tail); they call pdl_wait() first,
+// which blocks until the predecessor grid has completed and its writes are
+// visible, so stream semantics are unchanged. A no-op for normal launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();   // HG_PDL=0 disables (A/B)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args... args) {
+  if (!pdl_enabled()) {
+    kernel<<<grid, block, smem, stream>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 int set_timers_gather(void* p);
 int set_timers_layer(void* p);
 int set_timers_sampler(void* p);

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
                                                    int d, uint8_t* __restrict__ A_ts, long long plane) {
+  pdl_wait();
   __shared__ __align__(16) float s_rows[8][kMaxRowFloats];
   const int R = *R_dev;
   const int lane = threadIdx.x & 31;
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
 
 __global__ void k_scatter_rows(const int32_t* R_dev, const int32_t* __restrict__ rows, const float* __restrict__ Z,
                                int dout, int relu, float* __restrict__ h_out) {
+  pdl_wait();
   const long long n = (long long)(*R_dev) * dout;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(t / dout), j = (int)(t - (long long)i * dout);
@@ -149,6 +151,7 @@ __global__ void k_scatter_rows(const int32_t* R_dev, const int32_t* __restrict__
 
 __global__ void k_inject(const int32_t* n_dev, const uint8_t* __restrict__ flag, const int32_t* __restrict__ hit_row,
                          const float* __restrict__ table, int dim, float* __restrict__ h_out) {
+  pdl_wait();
   const int n = *n_dev;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -163,6 +166,7 @@ __global__ void k_inject(const int32_t* n_dev, const uint8_t* __restrict__ flag,
 // one warp per seed row; fp64 throughout like the reference
 __global__ void k_ce_rows(const float* __restrict__ logits, const int32_t* __restrict__ labels, int B, int C,
                           float* __restrict__ dlogits, double* __restrict__ row_logp) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < B; i += warps) {
@@ -189,6 +193,7 @@ __global__ void k_ce_rows(const float* __restrict__ logits, const int32_t* __res
 }
 
 __global__ void __launch_bounds__(1024) k_ce_loss(const double* __restrict__ row_logp, int B, double* loss) {
+  pdl_wait();
   __shared__ double part[32];
   double s = 0.0;
   for (int i = threadIdx.x; i < B; i += blockDim.x) s += row_logp[i];
@@ -207,6 +212,7 @@ __global__ void __launch_bounds__(1024) k_ce_loss(const double* __restrict__ row
 __global__ void __launch_bounds__(256) k_gather_dz(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const float* __restrict__ d_h, const float* __restrict__ h_out,
                                                    int dout, int relu, uint8_t* __restrict__ dz_ts, long long plane) {
+  pdl_wait();
   __shared__ __align__(16) float s_rows[8][kMaxRowFloats];
   const int R = *R_dev;
   const int lane = threadIdx.x & 31;
@@ -240,6 +246,7 @@ __global__ void k_csc_keys(const int32_t* n_dst_dev, const int32_t* __restrict__
                            const uint8_t* __restrict__ keep, const int32_t* __restrict__ pos_of,
                            const int32_t* __restrict__ col, long long E_max, unsigned sentinel,
                            unsigned* __restrict__ keys, unsigned* __restrict__ vals) {
+  pdl_wait();
   const int n = *n_dst_dev;
   const long long E = blk_off[n];
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -260,6 +267,7 @@ __global__ void k_csc_keys(const int32_t* n_dst_dev, const int32_t* __restrict__
 
 __global__ void k_csc_segments(const unsigned* __restrict__ keys, long long E_max, unsigned sentinel,
                                int32_t* __restrict__ seg_lo, int32_t* __restrict__ seg_hi) {
+  pdl_wait();
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < E_max;
        p += (long long)gridDim.x * blockDim.x) {
     const unsigned k = keys[p];
@@ -277,6 +285,7 @@ __global__ void __launch_bounds__(256) k_transpose_agg(
     const int32_t* __restrict__ start, const int32_t* __restrict__ end, const int32_t* __restrict__ dst_deg,
     const int32_t* __restrict__ src_deg, const int32_t* n_dst_dev, const int32_t* __restrict__ pos_of,
     const float* __restrict__ SG, int ldSG, int d, float* __restrict__ d_in, double* __restrict__ norms) {
+  pdl_wait();
   const int n = *n_live_dev;
   const int n_dst = *n_dst_dev;
   const int lane = threadIdx.x & 31;
@@ -345,12 +354,14 @@ __global__ void __launch_bounds__(256) k_transpose_agg(
 }
 
 __global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, long long n, float eta) {
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = __fsub_rn(p[i], __fmul_rn(eta, g[i]));
 }
 
 // row norms of arbitrary fp32 rows (API node_grad_norms)
 __global__ void k_row_norms(const float* __restrict__ x, long long n, int d, double* __restrict__ out) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
@@ -382,25 +393,25 @@ int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int3
   uint8_t* a = static_cast<uint8_t*>(A_ts);
   const long long plane = ts_plane_bytes(R_max, (kind == kKindSAGE ? 2 * d : d) + 1);
   if (kind == kKindSAGE)
-    k_aggregate<kKindSAGE><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a,
-                                                     plane);
+    { const cudaError_t _pe = hg::launch_pdl(k_aggregate<kKindSAGE>, dim3(grid), dim3(256), 0, stream, R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a,
+                                                     plane); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   else
-    k_aggregate<kKindGCN><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a,
-                                                    plane);
+    { const cudaError_t _pe = hg::launch_pdl(k_aggregate<kKindGCN>, dim3(grid), dim3(256), 0, stream, R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a,
+                                                    plane); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }
 
 int hg_scatter_rows(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* Z, int dout, int relu,
                     float* h_out, cudaStream_t stream) {
-  k_scatter_rows<<<grid_for(R_max * dout, 256), 256, 0, stream>>>(R_dev, rows, Z, dout, relu, h_out);
+  { const cudaError_t _pe = hg::launch_pdl(k_scatter_rows, dim3(grid_for(R_max * dout, 256)), dim3(256), 0, stream, R_dev, rows, Z, dout, relu, h_out); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_scatter_rows");
   return kOk;
 }
 
 int hg_inject_rows(const int32_t* n_dev, long long n_max, const uint8_t* flag, const int32_t* hit_row,
                    const float* table, int dim, float* h_out, cudaStream_t stream) {
-  k_inject<<<grid_for(n_max * 32, 256, 148 * 16), 256, 0, stream>>>(n_dev, flag, hit_row, table, dim, h_out);
+  { const cudaError_t _pe = hg::launch_pdl(k_inject, dim3(grid_for(n_max * 32, 256, 148 * 16)), dim3(256), 0, stream, n_dev, flag, hit_row, table, dim, h_out); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_inject_rows");
   return kOk;
 }
@@ -408,9 +419,9 @@ int hg_inject_rows(const int32_t* n_dev, long long n_max, const uint8_t* flag, c
 int hg_cross_entropy(const float* logits, const int32_t* labels, int B, int C, float* dlogits, double* row_logp,
                      double* loss, cudaStream_t stream) {
   if (B < 1 || C < 1) return fail("hg_cross_entropy", kBadArg, "empty logits");
-  k_ce_rows<<<grid_for((long long)B * 32, 256, 148 * 16), 256, 0, stream>>>(logits, labels, B, C, dlogits, row_logp);
+  { const cudaError_t _pe = hg::launch_pdl(k_ce_rows, dim3(grid_for((long long)B * 32, 256, 148 * 16)), dim3(256), 0, stream, logits, labels, B, C, dlogits, row_logp); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_cross_entropy");
-  k_ce_loss<<<1, 1024, 0, stream>>>(row_logp, B, loss);
+  { const cudaError_t _pe = hg::launch_pdl(k_ce_loss, dim3(1), dim3(1024), 0, stream, row_logp, B, loss); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_cross_entropy");
   return kOk;
 }
@@ -419,8 +430,8 @@ int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, con
                  int dout, int relu, void* dz_ts, cudaStream_t stream) {
   if (dout > kMaxRowFloats) return fail("hg_gather_dz", kBadArg, "row too wide");
   const long long rows_pad = (R_max + kTsRows - 1) / kTsRows * kTsRows;
-  k_gather_dz<<<grid_for(rows_pad * 32, 256, 148 * 16), 256, 0, stream>>>(
-      R_dev, rows, d_h, h_out, dout, relu, static_cast<uint8_t*>(dz_ts), ts_plane_bytes(R_max, dout));
+  { const cudaError_t _pe = hg::launch_pdl(k_gather_dz, dim3(grid_for(rows_pad * 32, 256, 148 * 16)), dim3(256), 0, stream, 
+      R_dev, rows, d_h, h_out, dout, relu, static_cast<uint8_t*>(dz_ts), ts_plane_bytes(R_max, dout)); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_gather_dz");
   return kOk;
 }
@@ -451,13 +462,13 @@ int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t
   HG_CHECK_CUDA(W, cudaMemsetAsync(seg_lo, 0, (size_t)n_src_max * 4, stream));
   HG_CHECK_CUDA(W, cudaMemsetAsync(seg_hi, 0, (size_t)n_src_max * 4, stream));
   if (E_max == 0) return kOk;
-  k_csc_keys<<<grid_for(E_max, 256), 256, 0, stream>>>(n_dst_dev, blk_off, keep, pos_of, col, E_max, sentinel,
-                                                       keys_in, vals_in);
+  { const cudaError_t _pe = hg::launch_pdl(k_csc_keys, dim3(grid_for(E_max, 256)), dim3(256), 0, stream, n_dst_dev, blk_off, keep, pos_of, col, E_max, sentinel,
+                                                       keys_in, vals_in); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_sorted, vals_in, vals_sorted,
                                                   (int)E_max, 0, bits, stream);
   if (e != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(e));
-  k_csc_segments<<<grid_for(E_max, 256), 256, 0, stream>>>(keys_sorted, E_max, sentinel, seg_lo, seg_hi);
+  { const cudaError_t _pe = hg::launch_pdl(k_csc_segments, dim3(grid_for(E_max, 256)), dim3(256), 0, stream, keys_sorted, E_max, sentinel, seg_lo, seg_hi); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }
@@ -471,25 +482,25 @@ int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, 
   if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 512");
   const unsigned grid = grid_for(n_live_max * 32, 256, 148 * 16);
   if (kind == kKindSAGE)
-    k_transpose_agg<kKindSAGE><<<grid, 256, 0, stream>>>(n_live_dev, live, seg_lo, seg_hi, vals_sorted, rows, start,
+    { const cudaError_t _pe = hg::launch_pdl(k_transpose_agg<kKindSAGE>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, seg_lo, seg_hi, vals_sorted, rows, start,
                                                          end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d,
-                                                         d_in, norms);
+                                                         d_in, norms); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   else
-    k_transpose_agg<kKindGCN><<<grid, 256, 0, stream>>>(n_live_dev, live, seg_lo, seg_hi, vals_sorted, rows, start,
+    { const cudaError_t _pe = hg::launch_pdl(k_transpose_agg<kKindGCN>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, seg_lo, seg_hi, vals_sorted, rows, start,
                                                         end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d, d_in,
-                                                        norms);
+                                                        norms); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }
 
 int hg_sgd(float* params, const float* grads, long long n, float eta, cudaStream_t stream) {
-  k_sgd<<<grid_for(n, 256), 256, 0, stream>>>(params, grads, n, eta);
+  { const cudaError_t _pe = hg::launch_pdl(k_sgd, dim3(grid_for(n, 256)), dim3(256), 0, stream, params, grads, n, eta); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_sgd");
   return kOk;
 }
 
 int hg_row_norms(const float* x, long long n, int d, double* out, cudaStream_t stream) {
-  k_row_norms<<<grid_for(n * 32, 256, 148 * 16), 256, 0, stream>>>(x, n, d, out);
+  { const cudaError_t _pe = hg::launch_pdl(k_row_norms, dim3(grid_for(n * 32, 256, 148 * 16)), dim3(256), 0, stream, x, n, d, out); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_row_norms");
   return kOk;
 }

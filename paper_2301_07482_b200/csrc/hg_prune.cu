@@ -25,6 +25,7 @@ __global__ void k_prune_rows(const int32_t* n_dst_dev, const uint8_t* __restrict
                              int32_t* __restrict__ end, const int32_t* __restrict__ col,
                              uint8_t* __restrict__ keep, uint8_t* __restrict__ src_mask,
                              unsigned long long* prune_writes) {
+  pdl_wait();
   const int n = *n_dst_dev;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     const bool k = (!live_dst || live_dst[r]) && !(inj_dst && inj_dst[r]);
@@ -54,6 +55,7 @@ __global__ void k_lookup(const int32_t* n_live_dev, const int32_t* __restrict__ 
                          const int32_t* __restrict__ admit_iter, int32_t* __restrict__ row_owner, const int* it_dev,
                          double t_stale, int t_inf, uint8_t* __restrict__ hit_flag, int32_t* __restrict__ hit_row,
                          long long* ctr) {
+  pdl_wait();
   const int n = *n_live_dev;
   const int it = *it_dev;
   unsigned long long* c = reinterpret_cast<unsigned long long*>(ctr);
@@ -100,9 +102,9 @@ int hg_prune_block(const int32_t* n_dst_dev, long long n_dst_max, const int32_t*
   if (scratch_bytes < hg_prune_scratch_bytes(n_src_max > n_dst_max ? n_src_max : n_dst_max))
     return fail(W, kBadArg, "scratch too small");
   HG_CHECK_CUDA(W, cudaMemsetAsync(src_mask, 0, (size_t)n_src_max, stream));
-  k_prune_rows<<<grid_for(n_dst_max, 256), 256, 0, stream>>>(
+  { const cudaError_t _pe = hg::launch_pdl(k_prune_rows, dim3(grid_for(n_dst_max, 256)), dim3(256), 0, stream, 
       n_dst_dev, live_dst, inj_dst, start, end, col, keep, src_mask,
-      reinterpret_cast<unsigned long long*>(global_ctr + kGCtrPruneWrites));
+      reinterpret_cast<unsigned long long*>(global_ctr + kGCtrPruneWrites)); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   int* part = reinterpret_cast<int*>(scratch);
   int st = scan_launch<int>(W, FlagU8{keep}, DevCount{n_dst_dev}, n_dst_max, part,
@@ -120,9 +122,9 @@ int hg_cache_lookup(const int32_t* n_live_dev, long long n_live_max, const int32
   const char* W = "hg_cache_lookup";
   HG_CHECK_CUDA(W, cudaMemsetAsync(hit_flag, 0, (size_t)n_src_max, stream));
   const int t_inf = isinf(t_stale) ? 1 : 0;
-  k_lookup<<<grid_for(n_live_max, 256), 256, 0, stream>>>(n_live_dev, live, src_nodes, row_of, admit_iter,
+  { const cudaError_t _pe = hg::launch_pdl(k_lookup, dim3(grid_for(n_live_max, 256)), dim3(256), 0, stream, n_live_dev, live, src_nodes, row_of, admit_iter,
                                                           row_owner, it_dev, t_stale, t_inf, hit_flag, hit_row,
-                                                          layer_ctr);
+                                                          layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }

@@ -131,6 +131,7 @@ struct SampState {
 
 __global__ void k_stamp(const int32_t* __restrict__ frontier, const int32_t* F_dev, const SampState* ss,
                         int64_t* __restrict__ g2l, int32_t* __restrict__ src_out) {
+  pdl_wait();
   const int F = *F_dev;
   const unsigned epoch = (unsigned)ss->epoch;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
@@ -216,6 +217,7 @@ struct HugeState {
 
 __global__ void k_task_bounds(const int32_t* F_dev, const int64_t* __restrict__ cand_off, int32_t* __restrict__ task_row,
                               long long* __restrict__ meta, int fanout, HugeState hs) {
+  pdl_wait();
   const int F = *F_dev;
   const long long total = cand_off[F];
   long long C = (total + 148 * 32 - 1) / (148 * 32);       // aim for >= 32 tasks per SM
@@ -271,6 +273,7 @@ __device__ __forceinline__ void put_pick(int32_t* src_flat, int32_t* col_local, 
 __global__ void k_pick(const int32_t* __restrict__ g_col, const int32_t* counts_dev, const SampState* ss,
                        const int64_t* __restrict__ g2l, uint32_t* __restrict__ bitmap, int32_t* __restrict__ src_flat,
                        const int32_t* __restrict__ col_local) {
+  pdl_wait();
   const int E = counts_dev[0];
   const unsigned epoch = (unsigned)ss->epoch;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
@@ -288,6 +291,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select(
     const int64_t* __restrict__ cand_off, const int32_t* __restrict__ blk_off, int32_t* __restrict__ src_flat,
     int32_t* __restrict__ col_local, const int32_t* __restrict__ task_row, const long long* __restrict__ task_meta,
     const uint8_t* __restrict__ huge_flag) {
+  pdl_wait();
   __shared__ JumpTableC tab;
   __shared__ u128 dA[33], dC[33];
   const u128 s0{ss->st_hi, ss->st_lo}, inc{ss->inc_hi, ss->inc_lo};
@@ -456,6 +460,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select(
 __global__ void __launch_bounds__(kSelThreads, 4) k_select_huge(
     const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end, const int32_t* __restrict__ frontier,
     int fanout, const SampState* ss, const int64_t* __restrict__ cand_off, HugeState hs) {
+  pdl_wait();
   __shared__ JumpTableC tab;
   const u128 s0{ss->st_hi, ss->st_lo}, inc{ss->inc_hi, ss->inc_lo};
   for (int t = threadIdx.x; t < 256; t += blockDim.x) {
@@ -516,6 +521,7 @@ __global__ void __launch_bounds__(256) k_merge_huge(const int64_t* __restrict__ 
                                                     const int64_t* __restrict__ cand_off,
                                                     const int32_t* __restrict__ blk_off, int32_t* __restrict__ src_flat,
                                                     int32_t* __restrict__ col_local, HugeState hs) {
+  pdl_wait();
   const int nh = hs.ctr[0];
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -589,6 +595,7 @@ struct TotalNew {
 
 __global__ void k_relabel(const int32_t* __restrict__ src_flat, const int32_t* counts_dev,
                           const int64_t* __restrict__ g2l, int32_t* __restrict__ col_local, SampState* ss) {
+  pdl_wait();
   const int E = counts_dev[0];
   // every reader of this layer's epoch has finished (stream order): advance it
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -682,7 +689,7 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   hs.flag = reinterpret_cast<uint8_t*>(hs.base + (F_max + 16));
 
   SampState* ss = reinterpret_cast<SampState*>(state_dev);
-  k_stamp<<<grid_for(F_max, 256), 256, 0, stream>>>(frontier, F_dev, ss, g2l, src_out);
+  { const cudaError_t _pe = hg::launch_pdl(k_stamp, dim3(grid_for(F_max, 256)), dim3(256), 0, stream, frontier, F_dev, ss, g2l, src_out); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   DegCount f{g_start, g_end, frontier, fanout};
   st = scan_launch<I64x2>(W, f, DevCount{F_dev}, F_max, part_dc,
@@ -690,7 +697,7 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
                           TotalDegCount{F_dev, cand_off, blk_off, counts_dev}, stream);
   if (st) return st;
   HG_CHECK_CUDA(W, cudaMemsetAsync(hs.ctr, 0, 8, stream));
-  k_task_bounds<<<grid_for(F_max, 256), 256, 0, stream>>>(F_dev, cand_off, task_row, task_meta, fanout, hs);
+  { const cudaError_t _pe = hg::launch_pdl(k_task_bounds, dim3(grid_for(F_max, 256)), dim3(256), 0, stream, F_dev, cand_off, task_row, task_meta, fanout, hs); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   // persistent warps over the tasks; HG_SEL_BLOCKS caps the grid (leaves SMs
   // to the training stream that runs concurrently with the pipelined sampler)
@@ -705,26 +712,26 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   }
   const unsigned sel_grid = (unsigned)sel_cap;
   if (fanout <= 32) {
-    k_select<true><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
-                                                          blk_off, src_flat, col_local, task_row, task_meta, hs.flag);
+    { const cudaError_t _pe = hg::launch_pdl(k_select<true>, dim3(sel_grid), dim3(kSelThreads), 0, stream, g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
+                                                          blk_off, src_flat, col_local, task_row, task_meta, hs.flag); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
     HG_LAUNCHED(W);
-    k_select_huge<<<148 * 4, kSelThreads, 0, stream>>>(g_start, g_end, frontier, fanout, ss, cand_off, hs);
+    { const cudaError_t _pe = hg::launch_pdl(k_select_huge, dim3(148 * 4), dim3(kSelThreads), 0, stream, g_start, g_end, frontier, fanout, ss, cand_off, hs); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
     HG_LAUNCHED(W);
-    k_merge_huge<<<148, 256, 0, stream>>>(g_start, frontier, fanout, cand_off, blk_off, src_flat, col_local, hs);
+    { const cudaError_t _pe = hg::launch_pdl(k_merge_huge, dim3(148), dim3(256), 0, stream, g_start, frontier, fanout, cand_off, blk_off, src_flat, col_local, hs); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
     HG_LAUNCHED(W);
   } else {
-    k_select<false><<<sel_grid, kSelThreads, 0, stream>>>(g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
-                                                           blk_off, src_flat, col_local, task_row, task_meta, nullptr);
+    { const cudaError_t _pe = hg::launch_pdl(k_select<false>, dim3(sel_grid), dim3(kSelThreads), 0, stream, g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
+                                                           blk_off, src_flat, col_local, task_row, task_meta, nullptr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
     HG_LAUNCHED(W);
   }
-  k_pick<<<grid_for(F_max * (long long)fanout, 256), 256, 0, stream>>>(g_col, counts_dev, ss, g2l, bitmap, src_flat,
-                                                                       col_local);
+  { const cudaError_t _pe = hg::launch_pdl(k_pick, dim3(grid_for(F_max * (long long)fanout, 256)), dim3(256), 0, stream, g_col, counts_dev, ss, g2l, bitmap, src_flat,
+                                                                       col_local); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   st = scan_launch<int>(W, PopWord{bitmap}, ConstCount{words}, words, part_w,
                         EmitNew{bitmap, F_dev, ss, g2l, src_out},
                         TotalNew{F_dev, counts_dev, ss, cand_off}, stream);
   if (st) return st;
-  k_relabel<<<grid_for(F_max * (long long)fanout, 256), 256, 0, stream>>>(src_flat, counts_dev, g2l, col_local, ss);
+  { const cudaError_t _pe = hg::launch_pdl(k_relabel, dim3(grid_for(F_max * (long long)fanout, 256)), dim3(256), 0, stream, src_flat, counts_dev, g2l, col_local, ss); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }

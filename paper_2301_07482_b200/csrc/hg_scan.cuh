@@ -85,6 +85,7 @@ __device__ __forceinline__ T block_exclusive(T v, T* block_total) {
 
 template <typename T, typename F, typename NC>
 __global__ void __launch_bounds__(kScanThreads) k_tile_reduce(F f, NC nc, T* partials) {
+  pdl_wait();
   const long long n = nc.get();
   const long long base = (long long)blockIdx.x * kScanTile;
   T acc = zero_of<T>();
@@ -103,6 +104,7 @@ template <typename T>
 __global__ void __launch_bounds__(1024) k_scan_partials(T* partials, int tiles) {
   __shared__ T wt[32];
   __shared__ T carry_s;
+  pdl_wait();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x == 0) carry_s = zero_of<T>();
   __syncthreads();
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(1024) k_scan_partials(T* partials, int tiles) 
 template <typename T, typename F, typename NC, typename Emit, typename Total>
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(F f, NC nc, const T* partials, Emit emit,
                                                             Total total) {
+  pdl_wait();
   const long long n = nc.get();
   const long long base = (long long)blockIdx.x * kScanTile;
   if (n == 0) {
@@ -175,11 +178,13 @@ int scan_launch(const char* where, F f, NC nc, long long n_max, T* partials, Emi
                 cudaStream_t s) {
   long long tiles = scan_tiles(n_max);
   if (tiles < 1) tiles = 1;
-  k_tile_reduce<T, F, NC><<<(unsigned)tiles, kScanThreads, 0, s>>>(f, nc, partials);
+  HG_CHECK_CUDA(where, launch_pdl(k_tile_reduce<T, F, NC>, dim3((unsigned)tiles), dim3(kScanThreads), 0, s, f, nc,
+                                   partials));
   HG_LAUNCHED(where);
-  k_scan_partials<T><<<1, 1024, 0, s>>>(partials, (int)tiles);
+  HG_CHECK_CUDA(where, launch_pdl(k_scan_partials<T>, dim3(1), dim3(1024), 0, s, partials, (int)tiles));
   HG_LAUNCHED(where);
-  k_tile_scan<T, F, NC, Emit, Total><<<(unsigned)tiles, kScanThreads, 0, s>>>(f, nc, partials, emit, total);
+  HG_CHECK_CUDA(where, launch_pdl(k_tile_scan<T, F, NC, Emit, Total>, dim3((unsigned)tiles), dim3(kScanThreads), 0, s,
+                                   f, nc, (const T*)partials, emit, total));
   HG_LAUNCHED(where);
   return kOk;
 }

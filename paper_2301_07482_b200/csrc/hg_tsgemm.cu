@@ -144,6 +144,7 @@ template <bool kMN, typename Epi>
 __global__ void __launch_bounds__(kThreads, 1) k_tsgemm(const __grid_constant__ CUtensorMap tmA,
                                                         const __grid_constant__ CUtensorMap tmB, Shape sh, Epi epi,
                                                         int N_pad, uint32_t tmem_cols) {
+  pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
   __shared__ uint32_t tmem_slot;
@@ -259,6 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tsgemm(const __grid_constant__ 
 
 __global__ void k_splitk_sum(const float* __restrict__ part, int splits, long long n, long long stride,
                              float* __restrict__ out) {
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     float s = part[i];
     for (int z = 1; z < splits; ++z) s = __fadd_rn(s, part[z * stride + i]);
@@ -270,6 +272,7 @@ __global__ void k_splitk_sum(const float* __restrict__ part, int splits, long lo
 // sized for rows_alloc rows; zero padding up to the 128-row / 32-column boundaries
 __global__ void k_ts_pack(const float* __restrict__ src, long long ld, int transposed, int rows, int cols,
                           int rows_pad, int nCG, long long plane, uint8_t* __restrict__ dst) {
+  pdl_wait();
   const long long groups = (long long)rows_pad * nCG;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < groups;
        t += (long long)gridDim.x * blockDim.x) {
@@ -347,7 +350,7 @@ int launch(const char* W, const CUtensorMap& a, const CUtensorMap& b, Shape sh, 
   // launches one CTA, which exits at once (m0 >= M)
   const long long mt = (sh.M + kTM - 1) / kTM;
   dim3 grid((unsigned)(mt > 0 ? mt : 1), (unsigned)(n_tiles > 0 ? n_tiles : 1), (unsigned)splits);
-  k_tsgemm<kMN, Epi><<<grid, kThreads, smem, stream>>>(a, b, sh, e, n_tile, tmem_cols_for(n_tile));
+  { const cudaError_t _pe = hg::launch_pdl(k_tsgemm<kMN, Epi>, dim3(grid), dim3(kThreads), smem, stream, a, b, sh, e, n_tile, tmem_cols_for(n_tile)); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }
@@ -367,9 +370,9 @@ int hg_ts_pack(const float* src, long long ld, int transposed, int rows, int col
                cudaStream_t stream) {
   const long long rows_pad = ts_rows_pad(rows_alloc);
   const int nCG = ts_ncg(cols);
-  k_ts_pack<<<grid_for(rows_pad * nCG, 256), 256, 0, stream>>>(src, ld, transposed, rows, cols, (int)rows_pad, nCG,
+  { const cudaError_t _pe = hg::launch_pdl(k_ts_pack, dim3(grid_for(rows_pad * nCG, 256)), dim3(256), 0, stream, src, ld, transposed, rows, cols, (int)rows_pad, nCG,
                                                                ts_plane_bytes(rows_alloc, cols),
-                                                               static_cast<uint8_t*>(dst));
+                                                               static_cast<uint8_t*>(dst)); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_ts_pack");
   return kOk;
 }
@@ -419,7 +422,7 @@ int hg_ts_linear_wgrad(const int32_t* R_dev, long long R_max, const void* A_ts, 
   Shape sh{K1, N, (int)R_max, nullptr, R_dev, per};
   st = launch<true>(W, a, b, sh, EpiPartial{partial, N, stride}, nt, splits, stream);
   if (st) return st;
-  k_splitk_sum<<<grid_for(stride, 256), 256, 0, stream>>>(partial, splits, stride, stride, dP);
+  { const cudaError_t _pe = hg::launch_pdl(k_splitk_sum, dim3(grid_for(stride, 256)), dim3(256), 0, stream, partial, splits, stride, stride, dP); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }
