@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(256) k_gat_scores(const int32_t* n_dev, const 
                                                     const float* __restrict__ z, int HF, int H, int F,
                                                     const float* __restrict__ a_src, const float* __restrict__ a_dst,
                                                     float* __restrict__ el, float* __restrict__ er) {
+  pdl_wait();
   using HM = Heads<kT, kH>;
   const int n = *n_dev;
   const int lane = threadIdx.x & 31;
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(256) k_gat_aggregate(const int32_t* R_dev, con
                                                        int HF, int H, int F, const float* __restrict__ bias, int relu,
                                                        float* __restrict__ h_out, float* __restrict__ mx,
                                                        float* __restrict__ ssum) {
+  pdl_wait();
   const int R = *R_dev;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -199,6 +201,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const
                                                      const float* __restrict__ d_h, const float* __restrict__ h_out,
                                                      int relu, int HF, int H, int F, float* __restrict__ gz,
                                                      float* __restrict__ cc, float* __restrict__ der) {
+  pdl_wait();
   __shared__ float s_da[8][32][kMaxH], s_a[8][32][kMaxH], s_sl[8][32][kMaxH];
   const int R = *R_dev;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(
     const float* __restrict__ ssum, const float* __restrict__ gz, const float* __restrict__ cc,
     const float* __restrict__ der, const float* __restrict__ a_src, const float* __restrict__ a_dst, int HF, int H,
     int F, uint8_t* __restrict__ dz_ts, long long plane, float* __restrict__ del) {
+  pdl_wait();
   __shared__ __align__(16) float s_rows[8][kT * 32];
   const int n = *n_dev;
   const int n_dst = *n_dst_dev;
@@ -379,6 +383,7 @@ __global__ void __launch_bounds__(kParamGroups * kParamCols) k_gat_param_partial
     const int32_t* R_dev, const int32_t* __restrict__ rows, const float* __restrict__ gz,
     const float* __restrict__ der, const int32_t* n_dev, const int32_t* __restrict__ live,
     const float* __restrict__ del, const float* __restrict__ z, int HF, int H, int F, float* __restrict__ partial) {
+  pdl_wait();
   __shared__ float red[kParamGroups][3][kParamCols];
   const int R = *R_dev, n = *n_dev;
   const int b = blockIdx.x;
@@ -418,6 +423,7 @@ __global__ void __launch_bounds__(kParamGroups * kParamCols) k_gat_param_partial
 // slab rows: d_in = a_src, d_in + 1 = a_dst, d_in + 2 = bias (each HF wide)
 __global__ void k_gat_param_sum(const float* __restrict__ partial, int HF, float* __restrict__ d_att_src,
                                 float* __restrict__ d_att_dst, float* __restrict__ d_bias) {
+  pdl_wait();
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < 3 * HF; c += gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int b = 0; b < kParamBlocks; ++b) s += partial[(long long)b * 3 * HF + c];
@@ -431,6 +437,7 @@ __global__ void k_gat_param_sum(const float* __restrict__ partial, int HF, float
 __global__ void k_gat_scatter_norms(const int32_t* n_dev, const int32_t* __restrict__ live,
                                     const float* __restrict__ SG, int d, float* __restrict__ d_in,
                                     double* __restrict__ norms) {
+  pdl_wait();
   const int n = *n_dev;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -499,7 +506,7 @@ int hg_gat_scores(const int32_t* n_live_dev, long long n_live_max, const int32_t
   const char* W = "hg_gat_scores";
   if (int st = gat_check(W, HF, H)) return st;
   const unsigned grid = grid_for(n_live_max * 32, 256, 148 * 16);
-  HG_GAT_DISPATCH(HF, H, (k_gat_scores<kT, kH><<<grid, 256, 0, stream>>>(n_live_dev, live, z, HF, H, HF / H,
+  HG_GAT_DISPATCH(HF, H, ((void)hg::launch_pdl(k_gat_scores<kT, kH>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, z, HF, H, HF / H,
                                                                                   att_src, att_dst, el, er)));
   HG_LAUNCHED(W);
   return kOk;
@@ -512,7 +519,7 @@ int hg_gat_aggregate(const int32_t* R_dev, long long R_max, const int32_t* rows,
   if (int st = gat_check(W, HF, H)) return st;
   const unsigned grid = grid_for(R_max * 32, 256, 148 * 16);
   HG_GAT_DISPATCH(HF, H,
-                  (k_gat_aggregate<kT, kH><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, z, el, er, HF, H,
+                  ((void)hg::launch_pdl(k_gat_aggregate<kT, kH>, dim3(grid), dim3(256), 0, stream, R_dev, rows, start, end, col, z, el, er, HF, H,
                                                                   HF / H, bias, relu, h_out, mx, ssum)));
   HG_LAUNCHED(W);
   return kOk;
@@ -526,7 +533,7 @@ int hg_gat_bwd_dst(const int32_t* R_dev, long long R_max, const int32_t* rows, c
   if (int st = gat_check(W, HF, H)) return st;
   const unsigned grid = grid_for(R_max * 32, 256, 148 * 16);
   HG_GAT_DISPATCH(HF, H,
-                  (k_gat_bwd_dst<kT, kH><<<grid, 256, 0, stream>>>(R_dev, rows, start, end, col, z, el, er, mx, ssum, d_h,
+                  ((void)hg::launch_pdl(k_gat_bwd_dst<kT, kH>, dim3(grid), dim3(256), 0, stream, R_dev, rows, start, end, col, z, el, er, mx, ssum, d_h,
                                                                 h_out, relu, HF, H, HF / H, gz, cc, der)));
   HG_LAUNCHED(W);
   return kOk;
@@ -543,7 +550,7 @@ int hg_gat_bwd_src(const int32_t* n_live_dev, long long n_live_max, const int32_
   const unsigned grid = grid_for(rows_pad * 32, 256, 148 * 16);
   const long long plane = ts_plane_bytes(n_live_max, HF);
   HG_GAT_DISPATCH(HF, H,
-                  (k_gat_bwd_src<kT, kH><<<grid, 256, 0, stream>>>(n_live_dev, live, seg_lo, seg_hi, csc_pos, rows,
+                  ((void)hg::launch_pdl(k_gat_bwd_src<kT, kH>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, seg_lo, seg_hi, csc_pos, rows,
                                                                 n_dst_dev, pos_of, z, el, er, mx, ssum, gz, cc, der,
                                                                 att_src, att_dst, HF, H, HF / H,
                                                                 static_cast<uint8_t*>(dz_ts), plane, del)));
@@ -558,18 +565,18 @@ int hg_gat_param_grads(const int32_t* R_dev, const int32_t* rows, const float* g
                        float* partial, float* d_att_src, float* d_att_dst, float* d_bias, cudaStream_t stream) {
   const char* W = "hg_gat_param_grads";
   if (int st = gat_check(W, HF, H)) return st;
-  k_gat_param_partial<<<kParamBlocks, kParamGroups * kParamCols, 0, stream>>>(R_dev, rows, gz, der, n_live_dev, live, del, z, HF, H,
-                                                         HF / H, partial);
+  { const cudaError_t _pe = hg::launch_pdl(k_gat_param_partial, dim3(kParamBlocks), dim3(kParamGroups * kParamCols), 0, stream, R_dev, rows, gz, der, n_live_dev, live, del, z, HF, H,
+                                                         HF / H, partial); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
-  k_gat_param_sum<<<grid_for(3LL * HF, 256), 256, 0, stream>>>(partial, HF, d_att_src, d_att_dst, d_bias);
+  { const cudaError_t _pe = hg::launch_pdl(k_gat_param_sum, dim3(grid_for(3LL * HF, 256)), dim3(256), 0, stream, partial, HF, d_att_src, d_att_dst, d_bias); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }
 
 int hg_gat_scatter_norms(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const float* SG, int d,
                          float* d_in, double* norms, cudaStream_t stream) {
-  k_gat_scatter_norms<<<grid_for(n_live_max * 32, 256, 148 * 16), 256, 0, stream>>>(n_live_dev, live, SG, d, d_in,
-                                                                                    norms);
+  { const cudaError_t _pe = hg::launch_pdl(k_gat_scatter_norms, dim3(grid_for(n_live_max * 32, 256, 148 * 16)), dim3(256), 0, stream, n_live_dev, live, SG, d, d_in,
+                                                                                    norms); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_gat_scatter_norms");
   return kOk;
 }

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_load_rows(const int32_t* n_l
                                                            const TIn* __restrict__ feats, int dim,
                                                            float* __restrict__ out,
                                                            unsigned long long* __restrict__ gctr, Shards sh) {
+  pdl_wait();
   constexpr int kPerVec = 16 / sizeof(TIn);  // elements per 16-byte vector
   __shared__ const TIn* s_row[kWarps][32];
   __shared__ int s_loc[kWarps][32];
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(256) k_row_src(const int32_t* n_live_dev, cons
                                                  const char* __restrict__ region, const char* __restrict__ feats,
                                                  int row_bytes, const char** __restrict__ src_ptr,
                                                  unsigned long long* __restrict__ gctr) {
+  pdl_wait();
   const int n = *n_live_dev;
   unsigned long long* c = gctr;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i - (int)(threadIdx.x & 31) < n; i += gridDim.x * blockDim.x) {
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(256) k_row_src(const int32_t* n_live_dev, cons
 __global__ void __launch_bounds__(kBulkWarps * 32) k_load_rows_bulk(
     const int32_t* n_live_dev, const int32_t* __restrict__ live, const char* const* __restrict__ src_ptr,
     int row_bytes, int rows_per_group, float* __restrict__ out) {
+  pdl_wait();
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int R = rows_per_group;
@@ -329,9 +332,9 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
   // persistent: one wave of 4 CTAs per SM (or fewer when the batch is small)
   const unsigned grid = grid_for((n_live_max + 31) / 32, kWarps, 148 * 4);
 #define HG_LOAD(TT, U)                                                                                            \
-  k_load_rows<TT, U, false><<<grid, kWarps * 32, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,         \
-                                                    static_cast<const TT*>(region), static_cast<const TT*>(feats), \
-                                                    dim, h_out, g, Shards{nullptr, nullptr, 0, 0})
+  (void)hg::launch_pdl(k_load_rows<TT, U, false>, dim3(grid), dim3(kWarps * 32), 0, stream, n_live_dev, live,   \
+                       src_nodes, feature_row_of, static_cast<const TT*>(region), static_cast<const TT*>(feats),  \
+                       dim, h_out, g, Shards{nullptr, nullptr, 0, 0})
   if (dtype == 1) HG_LOAD(__half, 6); else HG_LOAD(float, 8);
 #undef HG_LOAD
   HG_LAUNCHED(W);
@@ -356,13 +359,13 @@ int hg_load_features_sharded(const int32_t* n_live_dev, long long n_live_max, co
   const unsigned grid = grid_for((n_live_max + 31) / 32, kWarps, 148 * 4);
   const Shards sh{shard_ptrs, shard_bounds, num_shards, local_shard};
   if (dtype == 1)
-    k_load_rows<__half, 6, true><<<grid, kWarps * 32, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,
+    { const cudaError_t _pe = hg::launch_pdl(k_load_rows<__half, 6, true>, dim3(grid), dim3(kWarps * 32), 0, stream, n_live_dev, live, src_nodes, feature_row_of,
                                                                   static_cast<const __half*>(region), nullptr, dim,
-                                                                  h_out, g, sh);
+                                                                  h_out, g, sh); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   else
-    k_load_rows<float, 8, true><<<grid, kWarps * 32, 0, stream>>>(n_live_dev, live, src_nodes, feature_row_of,
+    { const cudaError_t _pe = hg::launch_pdl(k_load_rows<float, 8, true>, dim3(grid), dim3(kWarps * 32), 0, stream, n_live_dev, live, src_nodes, feature_row_of,
                                                                  static_cast<const float*>(region), nullptr, dim,
-                                                                 h_out, g, sh);
+                                                                 h_out, g, sh); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }
