@@ -53,6 +53,7 @@ int hg_set_kernel_timers(void* buf) {
   int st = hg::set_timers_gather(buf);
   if (!st) st = hg::set_timers_layer(buf);
   if (!st) st = hg::set_timers_sampler(buf);
+  if (!st) st = hg::set_timers_gemm(buf);
   return st;
 }
 

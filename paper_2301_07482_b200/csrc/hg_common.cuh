@@ -88,7 +88,8 @@ __device__ __forceinline__ uint4 ldg_stream_u4(const uint4* p) {
 struct KTimer {
   unsigned long long start, end, total_ns, launches, done, pad[3];
 };
-enum TimerId : int { kTLoadRows = 0, kTAggregate = 1, kTTransposeAgg = 2, kTSelect = 3, kNumTimers = 8 };
+enum TimerId : int { kTLoadRows = 0, kTAggregate = 1, kTTransposeAgg = 2, kTSelect = 3, kTGemmFwd = 4, kTGemmBwd = 5,
+                     kNumTimers = 8 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -151,6 +152,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 int set_timers_gather(void* p);
 int set_timers_layer(void* p);
 int set_timers_sampler(void* p);
+int set_timers_gemm(void* p);
 
 }  // namespace hg
 
