@@ -226,18 +226,33 @@ def main():
     from paper_2301_07482_b200.data import csr2_from_edges_device
     graph = csr2_from_edges_device(src, dst, cfgd["n"], dev)
     sharded = world > 1 and not args.replicate_features
+    shard_note = None
     if sharded:
         # this rank's owner range only (comms.py:329-337); peers mapped over NVLink
         from paper_2301_07482_b200.distributed import owner_ranges
         bnd = owner_ranges(cfgd["n"], world)
         lo, hi = int(bnd[rank]), int(bnd[rank + 1])
         local_rows = device_features(cfgd, dev, lo=lo, hi=hi) if feats is None else feats[lo:hi]
-        feats_dev = hg.ShardedFeatures.from_process_group(local_rows, cfgd["n"], rank, world, dev)
+        feats_dev, err = None, ""
+        try:
+            feats_dev = hg.ShardedFeatures.from_process_group(local_rows, cfgd["n"], rank, world, dev)
+        except Exception as e:   # e.g. no peer access between these GPUs
+            err = f"{type(e).__name__}: {e}"
+        ok = torch.tensor([0 if feats_dev is None else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            # every rank falls back together to full local tables (never mixes layouts)
+            if feats_dev is not None:
+                torch.cuda.synchronize()
+                dist.barrier()
+                feats_dev.close()
+            sharded, shard_note = False, f"IPC sharding unavailable ({err or 'on a peer rank'}); replicated"
+            feats_dev = device_features(cfgd, dev) if feats is None else torch.from_numpy(feats).to(dev)
         del local_rows
     else:
         feats_dev = device_features(cfgd, dev) if feats is None else torch.from_numpy(feats).to(dev)
     config["features"] = (f"sharded {world}-way by owner range, remote rows read over NVLink (CUDA IPC)"
-                          if sharded else "replicated in HBM")
+                          if sharded else (shard_note or "replicated in HBM"))
     del src, dst
     n_tl = 10   # extra steps after the timed regions for the phase timeline
     need = (args.warmup + 2 * args.steps + n_tl + 1) * world
