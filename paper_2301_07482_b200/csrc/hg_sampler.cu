@@ -539,7 +539,14 @@ __global__ void __launch_bounds__(256) k_merge_huge(const int64_t* __restrict__ 
         key = ~0ull;
         j = ~0u;
       }
-      bitonic_sort32(key, j);
+      // a segment's picks are sorted: skip it when its best does not beat
+      // the current fanout-th pick (nothing of it can enter the top-fanout)
+      const unsigned long long k0 = __shfl_sync(0xffffffffu, key, 0);
+      const unsigned j0 = __shfl_sync(0xffffffffu, j, 0);
+      const unsigned long long tk = __shfl_sync(0xffffffffu, bk, fanout - 1);
+      const unsigned tj = __shfl_sync(0xffffffffu, bj, fanout - 1);
+      if (!kj_less(k0, j0, tk, tj)) continue;
+      // (already ascending across lanes: k_select_huge stores its sorted picks)
       unsigned long long rk = __shfl_sync(0xffffffffu, key, 31 - lane);
       unsigned rj = __shfl_sync(0xffffffffu, j, 31 - lane);
       if (kj_less(rk, rj, bk, bj)) {
