@@ -287,8 +287,10 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    no_ahead = os.environ.get("HG_NO_LOOKAHEAD") == "1"   # diagnostic: sample each batch in its own step
+
     def nxt(i):   # the batch announced for pipelined sampling (staged in HBM)
-        return staged[i + 1] if i + 1 < len(staged) else None
+        return staged[i + 1] if i + 1 < len(staged) and not no_ahead else None
 
     for s in range(args.warmup):
         tr.train_step_resident(staged[s], nxt(s))
@@ -387,7 +389,7 @@ def main():
     tl_steps = tr.prestage(mine[-(n_tl + 1):], [batches[i] for i in mine[-(n_tl + 1):]])
     acc = {}
     for i in range(n_tl):   # every step samples the next one (the last staged batch is lookahead only)
-        tr.train_step_resident(tl_steps[i], tl_steps[i + 1])
+        tr.train_step_resident(tl_steps[i], None if no_ahead else tl_steps[i + 1])
         for k, v in eng.timeline_ms().items():
             acc[k] = acc.get(k, 0.0) + v / n_tl
     eng.enable_timeline(False)
