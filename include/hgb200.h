@@ -154,8 +154,10 @@ int hg_ts_linear_wgrad(const int32_t* R_dev, long long R_max, const void* A_ts, 
  *   scores:    el[j,h] = <z_j,h , a_src,h>, er[j,h] = <z_j,h , a_dst,h> over the live rows
  *   aggregate: h_out[rows[r]] = relu?(sum_j softmax_j(leaky(el_j + er_i)) z_j + bias) over the
  *              surviving in-edges of i = rows[r] plus the self loop; mx / ssum [R x H] kept
- *   bwd_dst:   gz [R x HF] (ReLU-masked), cc = sum_j a da, der = sum_j ds        [R x H]
- *   bwd_src:   dz_j (TS, compact over live) = sum_i a_ij gz_i + del_j a_src (+ der_j a_dst), del [n_live x H]
+ *   bwd_dst:   gz [R x HF] (ReLU-masked), cc = sum_j a da, der = sum_j ds        [R x H],
+ *              per-CTA partials of d bias = sum gz and d a_dst = sum der z_i
+ *   bwd_src:   dz_j (TS, compact over live) = sum_i a_ij gz_i + del_j a_src (+ der_j a_dst), del [n_live x H],
+ *              per-CTA partials of d a_src = sum del z_j
  *   param_grads: d a_src, d a_dst, d bias (fixed-order column sums)
  *   scatter_norms: d_in[live[k]] = SG[k], fp64 norms (nn.py:346-349)
  * HF = d_out <= 512, H <= 8 heads, HF % H == 0. */
@@ -167,16 +169,16 @@ int hg_gat_aggregate(const int32_t* R_dev, long long R_max, const int32_t* rows,
 int hg_gat_bwd_dst(const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
                    const int32_t* end, const int32_t* col, const float* z, const float* el, const float* er,
                    const float* mx, const float* ssum, const float* d_h, const float* h_out, int relu, int HF, int H,
-                   float* gz, float* cc, float* der, cudaStream_t stream);
+                   float* gz, float* cc, float* der, float* part, cudaStream_t stream);
 int hg_gat_bwd_src(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const int32_t* seg_lo,
                    const int32_t* seg_hi, const unsigned* csc_pos, const int32_t* rows, const int32_t* n_dst_dev,
                    const int32_t* pos_of, const float* z, const float* el, const float* er, const float* mx,
                    const float* ssum, const float* gz, const float* cc, const float* der, const float* att_src,
-                   const float* att_dst, int HF, int H, void* dz_ts, float* del, cudaStream_t stream);
+                   const float* att_dst, int HF, int H, void* dz_ts, float* del, float* part, cudaStream_t stream);
 long long hg_gat_param_scratch_bytes(int HF);
-int hg_gat_param_grads(const int32_t* R_dev, const int32_t* rows, const float* gz, const float* der,
-                       const int32_t* n_live_dev, const int32_t* live, const float* del, const float* z, int HF, int H,
-                       float* partial, float* d_att_src, float* d_att_dst, float* d_bias, cudaStream_t stream);
+/* part buffers of bwd_dst ([grid][2][HF]: bias, a_dst) and bwd_src ([grid][HF]: a_src), summed in a fixed order */
+int hg_gat_param_grads(long long R_max, long long n_live_max, int HF, const float* part_dst, const float* part_src,
+                       float* d_att_src, float* d_att_dst, float* d_bias, cudaStream_t stream);
 int hg_gat_scatter_norms(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const float* SG, int d,
                          float* d_in, double* norms, cudaStream_t stream);
 

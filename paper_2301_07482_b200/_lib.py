@@ -49,10 +49,10 @@ SIGNATURES = {
     "hg_ipc_close": (I32, [P]),
     "hg_gat_scores": (I32, [P, I64, P, P, I32, I32, P, P, P, P, P]),
     "hg_gat_aggregate": (I32, [P, I64, P, P, P, P, P, P, P, I32, I32, P, I32, P, P, P, P]),
-    "hg_gat_bwd_dst": (I32, [P, I64, P, P, P, P, P, P, P, P, P, P, P, I32, I32, I32, P, P, P, P]),
-    "hg_gat_bwd_src": (I32, [P, I64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P]),
+    "hg_gat_bwd_dst": (I32, [P, I64, P, P, P, P, P, P, P, P, P, P, P, I32, I32, I32, P, P, P, P, P]),
+    "hg_gat_bwd_src": (I32, [P, I64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P, P]),
     "hg_gat_param_scratch_bytes": (I64, [I32]),
-    "hg_gat_param_grads": (I32, [P, P, P, P, P, P, P, P, I32, I32, P, P, P, P, P]),
+    "hg_gat_param_grads": (I32, [I64, I64, I32, P, P, P, P, P, P]),
     "hg_gat_scatter_norms": (I32, [P, I64, P, P, I32, P, P, P]),
     "hg_aggregate_fwd": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, P, P]),
     "hg_gemm_rm": (I32, [I32, I32, I64, I64, I64, P, I64, P, I64, F32, P, I64, P]),

@@ -11,8 +11,8 @@
 //   backward, per live source j (CSC):      k_gat_bwd_src: dz_j = sum_i a_ij gz_i
 //                                             + del_j a_src (+ der_j a_dst if j computes),
 //                                             emitted as a TS operand for the dgrad / wgrad GEMMs
-//   parameter vectors (a_src, a_dst, bias): k_gat_param_partial + k_gat_param_sum
-//                                             (fixed-order two-level column sums)
+//   parameter vectors (a_src, a_dst, bias): per-CTA column partials accumulated by the two
+//                                             backward kernels, k_gat_param_sum (fixed order)
 //   d_in rows + fp64 node-gradient norms:   k_gat_scatter_norms
 // No atomics on floats anywhere: every run is bit-identical.
 #include "hgb200.h"
@@ -190,6 +190,23 @@ __global__ void __launch_bounds__(256) k_gat_aggregate(const int32_t* R_dev, con
   }
 }
 
+// Sum per-warp column partials v[kT] (lane owns columns lane + 32 t) over the
+// 8 warps of the CTA in warp order and store them at out[c] (c < HF).
+template <int kT>
+__device__ __forceinline__ void block_colsum_store(float (&v)[kT], float (*red)[kT * 32], int HF, float* out) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < kT; ++t) red[wib][lane + 32 * t] = v[t];
+  __syncthreads();
+  for (int c = threadIdx.x; c < HF; c += blockDim.x) {
+    float sacc = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sacc += red[w][c];
+    out[c] = sacc;
+  }
+  __syncthreads();
+}
+
 // backward, warp per compute row r (i = rows[r]):
 //   gz = dL/dout masked by ReLU; c[r][h] = sum_j a_ij da_ij; der[r][h] = sum_j ds_ij
 template <int kT, int kH>
@@ -200,12 +217,18 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const
                                                      const float* __restrict__ mx, const float* __restrict__ ssum,
                                                      const float* __restrict__ d_h, const float* __restrict__ h_out,
                                                      int relu, int HF, int H, int F, float* __restrict__ gz,
-                                                     float* __restrict__ cc, float* __restrict__ der) {
+                                                     float* __restrict__ cc, float* __restrict__ der,
+                                                     float* __restrict__ part) {
   pdl_wait();
   __shared__ float s_da[8][32][kMaxH], s_a[8][32][kMaxH], s_sl[8][32][kMaxH];
+  __shared__ float s_red[8][kT * 32];
   const int R = *R_dev;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int warps = (gridDim.x * blockDim.x) >> 5;
+  // this warp's share of d bias = sum gz and d a_dst = sum der[h] z_i (rows in grid-stride order)
+  float pb[kT], pd[kT];
+#pragma unroll
+  for (int t = 0; t < kT; ++t) pb[t] = pd[t] = 0.f;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += warps) {
     const int i = rows[r];
     float g[kT];
@@ -272,7 +295,20 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const
       cc[(long long)r * H + lane] = ci;
       der[(long long)r * H + lane] = deri;
     }
+    const float* zi = z + (long long)i * HF;
+#pragma unroll
+    for (int t = 0; t < kT; ++t) {
+      const int c = lane + 32 * t;
+      const float dh = head_val(deri, c < HF ? Heads<kT, kH>::of(t, c, F) : 0);
+      if (c < HF) {
+        pb[t] += g[t];
+        pd[t] = __fmaf_rn(dh, zi[c], pd[t]);
+      }
+    }
   }
+  float* pbk = part + (long long)blockIdx.x * 2 * HF;
+  block_colsum_store<kT>(pb, s_red, HF, pbk);
+  block_colsum_store<kT>(pd, s_red, HF, pbk + HF);
 }
 
 // backward, warp per live source j (CSC of the surviving edges; csc_pos[p]
@@ -286,9 +322,13 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(
     const float* __restrict__ el, const float* __restrict__ er, const float* __restrict__ mx,
     const float* __restrict__ ssum, const float* __restrict__ gz, const float* __restrict__ cc,
     const float* __restrict__ der, const float* __restrict__ a_src, const float* __restrict__ a_dst, int HF, int H,
-    int F, uint8_t* __restrict__ dz_ts, long long plane, float* __restrict__ del) {
+    int F, uint8_t* __restrict__ dz_ts, long long plane, float* __restrict__ del, float* __restrict__ part) {
   pdl_wait();
   __shared__ __align__(16) float s_rows[8][kT * 32];
+  __shared__ float s_red[8][kT * 32];
+  float ps[kT];   // this warp's share of d a_src = sum del[h] z_j
+#pragma unroll
+  for (int t = 0; t < kT; ++t) ps[t] = 0.f;
   const int n = *n_dev;
   const int n_dst = *n_dst_dev;
   const int lane = threadIdx.x & 31;
@@ -354,6 +394,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(
       if (c < HF) {
         v = __fmaf_rn(dlh, a_src[c], acc[t]);
         if (self >= 0) v = __fmaf_rn(drh, a_dst[c], v);
+        ps[t] = __fmaf_rn(dlh, zr[t], ps[t]);
       }
       srow[c] = v;   // zero padding up to the 32-column chunk
     }
@@ -367,69 +408,31 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(
   const float zeros[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   for (int k = n + w0; k < n_pad; k += warps)
     for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK * 4, plane, k, g, zeros);
+  block_colsum_store<kT>(ps, s_red, HF, part + (long long)blockIdx.x * HF);
 }
 
-constexpr int kParamBlocks = 148 * 8;
-constexpr int kParamGroups = 4;       // row groups per block (blockDim = kParamGroups * kParamCols)
-constexpr int kParamCols = 256;
+constexpr int kGatMaxBlocks = 148 * 16;   // grid cap of the backward kernels (grid_for)
 
-// partial[b][0..HF) = sum over block b's compute rows of gz      (bias)
-// partial[b][HF..2HF) = sum over its compute rows of der[h] z     (a_dst)
-// partial[b][2HF..3HF) = sum over its live rows of del[h] z      (a_src)
-// Rows are split into kParamBlocks contiguous ranges by the device counts;
-// inside a block, row group g takes rows g, g+4, ... and the groups are
-// combined in order: a fixed summation order independent of the launch.
-__global__ void __launch_bounds__(kParamGroups * kParamCols) k_gat_param_partial(
-    const int32_t* R_dev, const int32_t* __restrict__ rows, const float* __restrict__ gz,
-    const float* __restrict__ der, const int32_t* n_dev, const int32_t* __restrict__ live,
-    const float* __restrict__ del, const float* __restrict__ z, int HF, int H, int F, float* __restrict__ partial) {
+// d bias / d a_dst / d a_src: one warp per (vector, column) sums the
+// per-CTA partials of the backward kernels in a fixed order (lane-strided
+// runs, then a fixed shuffle tree), so every run gives the same bits.
+__global__ void k_gat_param_sum(const float* __restrict__ part_dst, int nb_dst, const float* __restrict__ part_src,
+                                int nb_src, int HF, float* __restrict__ d_att_src, float* __restrict__ d_att_dst,
+                                float* __restrict__ d_bias) {
   pdl_wait();
-  __shared__ float red[kParamGroups][3][kParamCols];
-  const int R = *R_dev, n = *n_dev;
-  const int b = blockIdx.x;
-  const int grp = threadIdx.x / kParamCols, col = threadIdx.x % kParamCols;
-  const int r0 = (int)((long long)R * b / kParamBlocks), r1 = (int)((long long)R * (b + 1) / kParamBlocks);
-  const int k0 = (int)((long long)n * b / kParamBlocks), k1 = (int)((long long)n * (b + 1) / kParamBlocks);
-  for (int c0 = 0; c0 < HF; c0 += kParamCols) {
-    const int c = c0 + col;
-    float sb = 0.f, sd = 0.f, ss = 0.f;
-    if (c < HF) {
-      const int h = c / F;
-      for (int r = r0 + grp; r < r1; r += kParamGroups) {
-        sb += gz[(long long)r * HF + c];
-        sd = __fmaf_rn(der[(long long)r * H + h], z[(long long)rows[r] * HF + c], sd);
-      }
-      for (int k = k0 + grp; k < k1; k += kParamGroups)
-        ss = __fmaf_rn(del[(long long)k * H + h], z[(long long)live[k] * HF + c], ss);
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < 3 * HF; w += warps) {
+    const int q = w / HF, c = w - q * HF;
+    float sacc = 0.f;
+    if (q < 2) {
+      for (int b = lane; b < nb_dst; b += 32) sacc += part_dst[(long long)b * 2 * HF + q * HF + c];
+    } else {
+      for (int b = lane; b < nb_src; b += 32) sacc += part_src[(long long)b * HF + c];
     }
-    red[grp][0][col] = sb;
-    red[grp][1][col] = sd;
-    red[grp][2][col] = ss;
-    __syncthreads();
-    if (grp == 0 && c < HF) {
-      float* pb = partial + (long long)b * 3 * HF;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        float v = red[0][q][col];
-#pragma unroll
-        for (int g = 1; g < kParamGroups; ++g) v += red[g][q][col];
-        pb[q * HF + c] = v;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// slab rows: d_in = a_src, d_in + 1 = a_dst, d_in + 2 = bias (each HF wide)
-__global__ void k_gat_param_sum(const float* __restrict__ partial, int HF, float* __restrict__ d_att_src,
-                                float* __restrict__ d_att_dst, float* __restrict__ d_bias) {
-  pdl_wait();
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < 3 * HF; c += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int b = 0; b < kParamBlocks; ++b) s += partial[(long long)b * 3 * HF + c];
-    if (c < HF) d_bias[c] = s;
-    else if (c < 2 * HF) d_att_dst[c - HF] = s;
-    else d_att_src[c - 2 * HF] = s;
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0) (q == 0 ? d_bias : (q == 1 ? d_att_dst : d_att_src))[c] = sacc;
   }
 }
 
@@ -528,13 +531,13 @@ int hg_gat_aggregate(const int32_t* R_dev, long long R_max, const int32_t* rows,
 int hg_gat_bwd_dst(const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
                    const int32_t* end, const int32_t* col, const float* z, const float* el, const float* er,
                    const float* mx, const float* ssum, const float* d_h, const float* h_out, int relu, int HF, int H,
-                   float* gz, float* cc, float* der, cudaStream_t stream) {
+                   float* gz, float* cc, float* der, float* part, cudaStream_t stream) {
   const char* W = "hg_gat_bwd_dst";
   if (int st = gat_check(W, HF, H)) return st;
   const unsigned grid = grid_for(R_max * 32, 256, 148 * 16);
   HG_GAT_DISPATCH(HF, H,
                   ((void)hg::launch_pdl(k_gat_bwd_dst<kT, kH>, dim3(grid), dim3(256), 0, stream, R_dev, rows, start, end, col, z, el, er, mx, ssum, d_h,
-                                                                h_out, relu, HF, H, HF / H, gz, cc, der)));
+                                                                h_out, relu, HF, H, HF / H, gz, cc, der, part)));
   HG_LAUNCHED(W);
   return kOk;
 }
@@ -543,7 +546,7 @@ int hg_gat_bwd_src(const int32_t* n_live_dev, long long n_live_max, const int32_
                    const int32_t* seg_hi, const unsigned* csc_pos, const int32_t* rows, const int32_t* n_dst_dev,
                    const int32_t* pos_of, const float* z, const float* el, const float* er, const float* mx,
                    const float* ssum, const float* gz, const float* cc, const float* der, const float* att_src,
-                   const float* att_dst, int HF, int H, void* dz_ts, float* del, cudaStream_t stream) {
+                   const float* att_dst, int HF, int H, void* dz_ts, float* del, float* part, cudaStream_t stream) {
   const char* W = "hg_gat_bwd_src";
   if (int st = gat_check(W, HF, H)) return st;
   const long long rows_pad = (n_live_max + kTsRows - 1) / kTsRows * kTsRows;
@@ -553,22 +556,25 @@ int hg_gat_bwd_src(const int32_t* n_live_dev, long long n_live_max, const int32_
                   ((void)hg::launch_pdl(k_gat_bwd_src<kT, kH>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, seg_lo, seg_hi, csc_pos, rows,
                                                                 n_dst_dev, pos_of, z, el, er, mx, ssum, gz, cc, der,
                                                                 att_src, att_dst, HF, H, HF / H,
-                                                                static_cast<uint8_t*>(dz_ts), plane, del)));
+                                                                static_cast<uint8_t*>(dz_ts), plane, del, part)));
   HG_LAUNCHED(W);
   return kOk;
 }
 
-long long hg_gat_param_scratch_bytes(int HF) { return (long long)kParamBlocks * 3 * HF * 4; }
+// partial buffers of the backward kernels: [kGatMaxBlocks][2][HF] (dst) then
+// [kGatMaxBlocks][HF] (src)
+long long hg_gat_param_scratch_bytes(int HF) { return (long long)kGatMaxBlocks * 3 * HF * 4; }
 
-int hg_gat_param_grads(const int32_t* R_dev, const int32_t* rows, const float* gz, const float* der,
-                       const int32_t* n_live_dev, const int32_t* live, const float* del, const float* z, int HF, int H,
-                       float* partial, float* d_att_src, float* d_att_dst, float* d_bias, cudaStream_t stream) {
+int hg_gat_param_grads(long long R_max, long long n_live_max, int HF, const float* part_dst, const float* part_src,
+                       float* d_att_src, float* d_att_dst, float* d_bias, cudaStream_t stream) {
   const char* W = "hg_gat_param_grads";
-  if (int st = gat_check(W, HF, H)) return st;
-  { const cudaError_t _pe = hg::launch_pdl(k_gat_param_partial, dim3(kParamBlocks), dim3(kParamGroups * kParamCols), 0, stream, R_dev, rows, gz, der, n_live_dev, live, del, z, HF, H,
-                                                         HF / H, partial); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
-  HG_LAUNCHED(W);
-  { const cudaError_t _pe = hg::launch_pdl(k_gat_param_sum, dim3(grid_for(3LL * HF, 256)), dim3(256), 0, stream, partial, HF, d_att_src, d_att_dst, d_bias); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  // the grids hg_gat_bwd_dst / hg_gat_bwd_src used (every CTA wrote its partial)
+  const int nb_dst = (int)grid_for(R_max * 32, 256, 148 * 16);
+  const long long rows_pad = (n_live_max + kTsRows - 1) / kTsRows * kTsRows;
+  const int nb_src = (int)grid_for(rows_pad * 32, 256, 148 * 16);
+  { const cudaError_t _pe = hg::launch_pdl(k_gat_param_sum, dim3(grid_for(3LL * HF * 32, 256)), dim3(256), 0, stream,
+                                           part_dst, nb_dst, part_src, nb_src, HF, d_att_src, d_att_dst, d_bias);
+    if (_pe != cudaSuccess) return hg::fail(W, hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   return kOk;
 }

@@ -356,10 +356,12 @@ def gat_layer_backward_dev(net: Network, l: int, blk, t: GatTape, d_h, grads, ne
     gz = torch.empty((max(R, 1), HF), dtype=torch.float32, device=dev)
     cc = torch.empty((max(R, 1), H), dtype=torch.float32, device=dev)
     der = torch.empty((max(R, 1), H), dtype=torch.float32, device=dev)
+    part = torch.empty(int(_lib.query("hg_gat_param_scratch_bytes", HF)) // 4, dtype=torch.float32, device=dev)
+    part_dst, part_src = part[: 2 * (part.numel() // 3)], part[2 * (part.numel() // 3):]
     _lib.call("hg_gat_bwd_dst", _lib.ptr(t.R_dev), R, _lib.ptr(t.rows), _lib.ptr(blk.adj.start), _lib.ptr(blk.adj.end),
               _lib.ptr(blk.adj.col_indices), _lib.ptr(t.z), _lib.ptr(t.el), _lib.ptr(t.er), _lib.ptr(t.mx),
               _lib.ptr(t.ssum), _lib.ptr(d_h), _lib.ptr(t.h_out), int(t.relu), HF, H, _lib.ptr(gz), _lib.ptr(cc),
-              _lib.ptr(der), stream)
+              _lib.ptr(der), _lib.ptr(part_dst), stream)
     if csc is None:
         csc = build_csc(blk, keep, pos_of, n_dst_dev, stream)
     slab = net.slab(l)
@@ -369,14 +371,13 @@ def gat_layer_backward_dev(net: Network, l: int, blk, t: GatTape, d_h, grads, ne
     _lib.call("hg_gat_bwd_src", _lib.ptr(t.n_live_dev), n_live, _lib.ptr(t.live), _lib.ptr(csc.seg_lo),
               _lib.ptr(csc.seg_hi), _lib.ptr(csc.vals), _lib.ptr(t.rows), _lib.ptr(n_dst_dev), _lib.ptr(pos_of),
               _lib.ptr(t.z), _lib.ptr(t.el), _lib.ptr(t.er), _lib.ptr(t.mx), _lib.ptr(t.ssum), _lib.ptr(gz),
-              _lib.ptr(cc), _lib.ptr(der), _lib.ptr(a_src), _lib.ptr(a_dst), HF, H, _lib.ptr(dz), _lib.ptr(dl), stream)
+              _lib.ptr(cc), _lib.ptr(der), _lib.ptr(a_src), _lib.ptr(a_dst), HF, H, _lib.ptr(dz), _lib.ptr(dl),
+              _lib.ptr(part_src), stream)
     t.bwd = (gz, cc, der, dl)     # kept for inspection (tools/gat_diag.py)
     gslab = grads.slab(l)
     g_src, g_dst, g_bias = _att_rows(gslab, d_in)
-    part = torch.empty(int(_lib.query("hg_gat_param_scratch_bytes", HF)) // 4, dtype=torch.float32, device=dev)
-    _lib.call("hg_gat_param_grads", _lib.ptr(t.R_dev), _lib.ptr(t.rows), _lib.ptr(gz), _lib.ptr(der),
-              _lib.ptr(t.n_live_dev), _lib.ptr(t.live), _lib.ptr(dl), _lib.ptr(t.z), HF, H, _lib.ptr(part),
-              _lib.ptr(g_src), _lib.ptr(g_dst), _lib.ptr(g_bias), stream)
+    _lib.call("hg_gat_param_grads", R, n_live, HF, _lib.ptr(part_dst), _lib.ptr(part_src), _lib.ptr(g_src),
+              _lib.ptr(g_dst), _lib.ptr(g_bias), stream)
     splits = _wgrad_splits(n_live, d_in, HF)
 
     def wgrad(sp):
