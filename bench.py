@@ -83,6 +83,27 @@ def device_features(cfg, dev, seed=0, lo=0, hi=None, chunk=1 << 22):
     return out
 
 
+def aggregate_bytes(out, tr):
+    """Algorithmic bytes of one step's k_aggregate launches (SAGE / GCN):
+    per block b, U = live input rows, R = compute rows, E = their surviving
+    edges: U.d.4 (input rows) + R.K1.4 (TS operand, bf16 hi + lo) + 4E (col)
+    + 8R (offsets)."""
+    import torch
+    if tr.network.kind.value == "gat":
+        return None
+    counts = out["counts"].cpu().tolist()
+    total = 0
+    for b, blk in enumerate(out["blocks"]):
+        R, U = counts[2 * b], counts[2 * b + 1]
+        rows = out["rows"][b][:R].long()
+        E = int((blk.end.long()[rows] - blk.blk_off.long()[rows]).sum().item()) if R else 0
+        d = tr.network.dims[b]
+        K1 = (2 * d if tr.network.kind.value == "sage_mean" else d) + 1
+        K1 = (K1 + 31) // 32 * 32
+        total += U * d * 4 + R * K1 * 4 + 4 * E + 8 * R
+    return total
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -388,8 +409,10 @@ def main():
     eng.enable_timeline(True)
     tl_steps = tr.prestage(mine[-(n_tl + 1):], [batches[i] for i in mine[-(n_tl + 1):]])
     acc = {}
+    agg_bytes = []
     for i in range(n_tl):   # every step samples the next one (the last staged batch is lookahead only)
         tr.train_step_resident(tl_steps[i], None if no_ahead else tl_steps[i + 1])
+        agg_bytes.append(aggregate_bytes(eng.out, tr))
         for k, v in eng.timeline_ms().items():
             acc[k] = acc.get(k, 0.0) + v / n_tl
     eng.enable_timeline(False)
@@ -398,7 +421,18 @@ def main():
     row_b = cfgd["d"] * tr.features.element_size()
     nvlink = {"remote_rows_per_step": remote_rows / args.steps, "bytes_per_step": remote_rows * row_b / args.steps,
               "share_of_gathered_rows": remote_rows / max(1, g_delta[0] + g_delta[1])}
-    out = dict(base, value=value, nvlink_gather=nvlink, ms_per_step=1e3 * t_dev / args.steps, e2e=e2e, roofline=roofline,
+    # SAGE neighbour aggregation (k_aggregate, all layers): algorithmic bytes
+    # per step from the counts of the post-timing steps (SURVEY 8(d):
+    # U.d.4 + R.(K+1).4 + 4E + 8R per layer) over its timed per-step duration
+    agg_roof = None
+    if per_kernel["k_aggregate"]["launches"] and agg_bytes and agg_bytes[0] is not None:
+        t_step = per_kernel["k_aggregate"]["ms_total"] / 1e3 / args.steps
+        b_step = float(np.mean(agg_bytes))
+        agg_roof = {"kernel": "k_aggregate (hg_aggregate_fwd, all layers)", "bound": "hbm",
+                    "achieved": b_step / t_step / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": b_step / t_step / 1e9 / peak, "bytes_per_step": b_step,
+                    "bytes_source": f"counts of the {n_tl} post-timing steps"}
+    out = dict(base, value=value, nvlink_gather=nvlink, aggregate_roofline=agg_roof, ms_per_step=1e3 * t_dev / args.steps, e2e=e2e, roofline=roofline,
                gpu_launches=int(launches), clocks=clk, per_kernel=per_kernel, cuda_graph=graph_mode,
                graph_captures_in_timed={"value": caps_value, "e2e": caps_e2e},
                timeline_ms=timeline,
