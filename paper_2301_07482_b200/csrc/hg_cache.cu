@@ -42,16 +42,289 @@ struct NormKeyLess {
 // rank sort: CUB merge sort (block sort + merge-path passes) up to kMergeMaxN
 // live nodes, CUB 96-bit LSD radix sort above (12 onesweep passes, better at
 // large n). HG_CACHE_SORT=radix|merge overrides (A/B measurements).
-constexpr long long kMergeMaxN = 1 << 20;
-enum SortMode { kSortMerge = 1, kSortRadix = 2 };
+enum SortMode { kSortMerge = 1, kSortRadix = 2, kSortBucket = 3 };
 inline int sort_mode(long long n_max) {
   static int v = -2;
   if (v == -2) {
     const char* e = std::getenv("HG_CACHE_SORT");
-    v = !e ? -1 : (std::strcmp(e, "radix") == 0 ? kSortRadix : (std::strcmp(e, "merge") == 0 ? kSortMerge : -1));
+    v = !e ? -1
+           : (std::strcmp(e, "radix") == 0 ? kSortRadix
+                                           : (std::strcmp(e, "merge") == 0 ? kSortMerge
+                                                                           : (std::strcmp(e, "bucket") == 0 ? kSortBucket : -1)));
   }
   if (v >= 0) return v;
-  return n_max <= kMergeMaxN ? kSortMerge : kSortRadix;
+  return kSortBucket;
+}
+
+// ---------------------------------------------------------------------------
+// Bucket sort of the (norm bits, id) keys (kSortBucket, the default).
+// fp64 norms are >= 0, so their bit patterns order like the values. The
+// occupied bit range [lo, hi] is cut into kNB buckets by (bits - lo) >> shift
+// (monotone; equal norms share a bucket), items are scattered to their
+// buckets, and every bucket is sorted by (norm, id) on chip. Keys are
+// distinct (ids are), so the result is the unique sorted order: identical to
+// the CUB merge / radix sorts, in 6 launches instead of ~19, O(n) work.
+// Buckets above kBucketCap items (e.g. masses of equal norms) are sorted by
+// one CTA each with a chunk sort + global merge passes (k_bs_big).
+constexpr int kNB = 4096;
+constexpr int kBucketCap = 2048;
+
+struct BucketState {            // device scratch
+  unsigned long long lo, hi;    // min / max norm bits over the n live keys
+  int n_big;                    // buckets above kBucketCap
+  int pad;
+};
+
+__device__ __forceinline__ int bucket_of(unsigned long long bits, unsigned long long lo, int shift) {
+  const unsigned long long b = (bits - lo) >> shift;
+  return b < (unsigned long long)kNB ? (int)b : kNB - 1;
+}
+__device__ __forceinline__ int bucket_shift(unsigned long long lo, unsigned long long hi) {
+  const unsigned long long r = hi - lo;
+  const int bits = r ? 64 - __clzll((long long)r) : 0;
+  return bits > 12 ? bits - 12 : 0;
+}
+__device__ __forceinline__ bool key_less(unsigned long long an, unsigned ai, unsigned long long bn, unsigned bi) {
+  return an < bn || (an == bn && ai < bi);
+}
+
+__global__ void k_bs_hist(const int32_t* n_dev, const NormKey* __restrict__ keys, const BucketState* st,
+                          int* __restrict__ count) {
+  pdl_wait();
+  __shared__ int h[kNB];
+  for (int b = threadIdx.x; b < kNB; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int n = *n_dev;
+  const unsigned long long lo = st->lo;
+  const int shift = bucket_shift(lo, st->hi);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&h[bucket_of(keys[i].norm, lo, shift)], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kNB; b += blockDim.x)
+    if (h[b]) atomicAdd(&count[b], h[b]);
+}
+
+// exclusive offsets of the kNB bucket counts (one CTA), cursors, big-bucket list
+__global__ void __launch_bounds__(1024) k_bs_scan(const int* __restrict__ count, int* __restrict__ off,
+                                                  int* __restrict__ cursor, int* __restrict__ big, BucketState* st) {
+  pdl_wait();
+  __shared__ int part[1024];
+  __shared__ int nbig;
+  constexpr int kPer = kNB / 1024;
+  int v[kPer], s = 0;
+  if (threadIdx.x == 0) nbig = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    v[q] = count[threadIdx.x * kPer + q];
+    s += v[q];
+  }
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {
+    const int t = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
+    __syncthreads();
+    part[threadIdx.x] += t;
+    __syncthreads();
+  }
+  int run = part[threadIdx.x] - s;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int b = threadIdx.x * kPer + q;
+    off[b] = run;
+    cursor[b] = run;
+    if (v[q] > kBucketCap) big[atomicAdd(&nbig, 1)] = b;
+    run += v[q];
+  }
+  if (threadIdx.x == 1023) off[kNB] = run;
+  __syncthreads();
+  if (threadIdx.x == 0) st->n_big = nbig;
+}
+
+__global__ void k_bs_scatter(const int32_t* n_dev, const NormKey* __restrict__ keys, const BucketState* st,
+                             int* __restrict__ cursor, NormKey* __restrict__ tkeys, int32_t* __restrict__ tvals) {
+  pdl_wait();
+  const int n = *n_dev;
+  const unsigned long long lo = st->lo;
+  const int shift = bucket_shift(lo, st->hi);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const NormKey k = keys[i];
+    const int pos = atomicAdd(&cursor[bucket_of(k.norm, lo, shift)], 1);
+    tkeys[pos] = k;
+    tvals[pos] = i;
+  }
+}
+
+// in-smem bitonic sort of m (power of 2) (norm, id, val) items
+__device__ __forceinline__ void smem_bitonic(unsigned long long* sn, unsigned* si, int* sv, int m) {
+  for (int size = 2; size <= m; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (m >> 1); t += blockDim.x) {
+        const int a = 2 * t - (t & (stride - 1));
+        const int b = a + stride;
+        const bool up = (a & size) == 0;
+        if (key_less(sn[b], si[b], sn[a], si[a]) == up) {
+          const unsigned long long tn = sn[a];
+          const unsigned ti = si[a];
+          const int tv = sv[a];
+          sn[a] = sn[b]; si[a] = si[b]; sv[a] = sv[b];
+          sn[b] = tn; si[b] = ti; sv[b] = tv;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// one CTA per bucket of <= kBucketCap items: sort in shared memory, write back
+__global__ void __launch_bounds__(256) k_bs_small(const int* __restrict__ off, const NormKey* __restrict__ tkeys,
+                                                  const int32_t* __restrict__ tvals, NormKey* __restrict__ okeys,
+                                                  int32_t* __restrict__ ovals) {
+  pdl_wait();
+  __shared__ unsigned long long sn[kBucketCap];
+  __shared__ unsigned si[kBucketCap];
+  __shared__ int sv[kBucketCap];
+  for (int b = blockIdx.x; b < kNB; b += gridDim.x) {
+    const int o = off[b], cnt = off[b + 1] - o;
+    if (cnt == 0 || cnt > kBucketCap) continue;   // uniform per CTA
+    if (cnt == 1) {
+      if (threadIdx.x == 0) {
+        okeys[o] = tkeys[o];
+        ovals[o] = tvals[o];
+      }
+      continue;
+    }
+    int m = 2;
+    while (m < cnt) m <<= 1;
+    for (int t = threadIdx.x; t < m; t += blockDim.x) {
+      if (t < cnt) {
+        sn[t] = tkeys[o + t].norm;
+        si[t] = tkeys[o + t].id;
+        sv[t] = tvals[o + t];
+      } else {
+        sn[t] = ~0ull;
+        si[t] = ~0u;
+        sv[t] = -1;
+      }
+    }
+    __syncthreads();
+    smem_bitonic(sn, si, sv, m);
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      okeys[o + t] = NormKey{sn[t], si[t]};
+      ovals[o + t] = sv[t];
+    }
+    __syncthreads();
+  }
+}
+
+// merge path: number of items taken from A among the first d of merge(A, B)
+__device__ __forceinline__ int merge_split(const NormKey* A, int na, const NormKey* B, int nb, int d) {
+  int lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    // take A[mid] before B[d-1-mid] ?
+    if (key_less(A[mid].norm, A[mid].id, B[d - 1 - mid].norm, B[d - 1 - mid].id)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// big buckets (> kBucketCap items): one CTA each; chunk sort in shared memory,
+// then bottom-up merge passes between tkeys/tvals and the b2 buffers
+__global__ void __launch_bounds__(256) k_bs_big(const int* __restrict__ off, const int* __restrict__ big,
+                                                const BucketState* st, NormKey* __restrict__ tkeys,
+                                                int32_t* __restrict__ tvals, NormKey* __restrict__ k2,
+                                                int32_t* __restrict__ v2, NormKey* __restrict__ okeys,
+                                                int32_t* __restrict__ ovals) {
+  pdl_wait();
+  __shared__ unsigned long long sn[kBucketCap];
+  __shared__ unsigned si[kBucketCap];
+  __shared__ int sv[kBucketCap];
+  const int nbig = st->n_big;
+  for (int q = blockIdx.x; q < nbig; q += gridDim.x) {
+    const int b = big[q];
+    const int o = off[b], cnt = off[b + 1] - o;
+    // 1. sorted chunks of kBucketCap
+    for (int c0 = 0; c0 < cnt; c0 += kBucketCap) {
+      const int len = cnt - c0 < kBucketCap ? cnt - c0 : kBucketCap;
+      for (int t = threadIdx.x; t < kBucketCap; t += blockDim.x) {
+        if (t < len) {
+          sn[t] = tkeys[o + c0 + t].norm;
+          si[t] = tkeys[o + c0 + t].id;
+          sv[t] = tvals[o + c0 + t];
+        } else {
+          sn[t] = ~0ull;
+          si[t] = ~0u;
+          sv[t] = -1;
+        }
+      }
+      __syncthreads();
+      smem_bitonic(sn, si, sv, kBucketCap);
+      for (int t = threadIdx.x; t < len; t += blockDim.x) {
+        tkeys[o + c0 + t] = NormKey{sn[t], si[t]};
+        tvals[o + c0 + t] = sv[t];
+      }
+      __syncthreads();
+    }
+    // 2. merge passes: runs of width w -> 2w, ping-pong between t* and *2
+    NormKey* sk = tkeys + o;
+    int32_t* svv = tvals + o;
+    NormKey* dk = k2 + o;
+    int32_t* dvv = v2 + o;
+    for (int w = kBucketCap; w < cnt; w <<= 1) {
+      for (int p0 = 0; p0 < cnt; p0 += 2 * w) {
+        const int na = cnt - p0 < w ? cnt - p0 : w;
+        const int nb = cnt - p0 - na < w ? (cnt - p0 - na > 0 ? cnt - p0 - na : 0) : w;
+        const NormKey* A = sk + p0;
+        const NormKey* B = A + na;
+        const int tot = na + nb;
+        const int per = (tot + blockDim.x - 1) / blockDim.x;
+        const int d0 = threadIdx.x * per < tot ? threadIdx.x * per : tot;
+        const int d1 = d0 + per < tot ? d0 + per : tot;
+        int ia = merge_split(A, na, B, nb, d0), ib = d0 - ia;
+        for (int d = d0; d < d1; ++d) {
+          const bool takeA = ib >= nb || (ia < na && key_less(A[ia].norm, A[ia].id, B[ib].norm, B[ib].id));
+          if (takeA) {
+            dk[p0 + d] = A[ia];
+            dvv[p0 + d] = svv[p0 + ia];
+            ++ia;
+          } else {
+            dk[p0 + d] = B[ib];
+            dvv[p0 + d] = svv[p0 + na + ib];
+            ++ib;
+          }
+        }
+      }
+      __syncthreads();
+      NormKey* tk = sk; sk = dk; dk = tk;
+      int32_t* tv = svv; svv = dvv; dvv = tv;
+    }
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      okeys[o + t] = sk[t];
+      ovals[o + t] = svv[t];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_bs_minmax(const int32_t* n_dev, const NormKey* __restrict__ keys, BucketState* st) {
+  pdl_wait();
+  const int n = *n_dev;
+  unsigned long long mn = ~0ull, mx = 0ull;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long v = keys[i].norm;
+    mn = v < mn ? v : mn;
+    mx = v > mx ? v : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o), c = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = c > mx ? c : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&st->lo, mn);
+    atomicMax(&st->hi, mx);
+  }
 }
 
 struct NormKeyDecomposer {
@@ -256,8 +529,10 @@ long long hg_cache_update_scratch_bytes(long long n_max) {
                                   NormKeyLess{});
   if (tmp2 > tmp) tmp = tmp2;
   const long long n = n_max + 16;
-  // keys_in, keys_out (16 B), vals_in, vals_out, wlist (4 B), wflag, retained (1 B), scan partials
-  return n * 16 * 2 + n * 4 * 3 + n * 2 + (scan_tiles(n_max) + 1) * 4 + (long long)tmp + 2048;
+  // keys_in, keys_out (16 B), vals_in, vals_out, wlist (4 B), wflag, retained (1 B), scan partials,
+  // bucket sort: second key/val buffers + state + count/off/cursor/big
+  return n * 16 * 2 + n * 4 * 3 + n * 2 + (scan_tiles(n_max) + 1) * 4 + (long long)tmp + 2048 + n * 20 + 64 +
+         4LL * (4 * kNB + 16);
 }
 
 // Stage 1 (U1-U3): rank and evict; leaves the write list + n_write on device.
@@ -282,7 +557,49 @@ int hg_cache_rank(const int32_t* n_dev, int n_max, double p_grad, const int32_t*
   int* part = reinterpret_cast<int*>(retained + nn + 16 - ((uintptr_t)(retained + nn) & 15));
   void* tmp = part + scan_tiles(n_max) + 4;
   size_t tmp_bytes = (size_t)(scratch_bytes - ((char*)tmp - p));
-  const bool radix = sort_mode(n_max) == kSortRadix;
+  const int mode = sort_mode(n_max);
+  if (mode == kSortBucket) {
+    // bucket buffers live after the CUB temp area
+    const size_t need = (size_t)nn * 20 + 64 + 4 * (4 * kNB + 16);
+    const uintptr_t end = reinterpret_cast<uintptr_t>(tmp) + tmp_bytes;
+    char* bp = reinterpret_cast<char*>((end - need - 16) & ~uintptr_t(15));   // 16-byte aligned tail region
+    NormKey* k2 = reinterpret_cast<NormKey*>(bp);
+    int32_t* v2 = reinterpret_cast<int32_t*>(k2 + nn);
+    BucketState* bst = reinterpret_cast<BucketState*>((reinterpret_cast<uintptr_t>(v2 + nn) + 15) & ~uintptr_t(15));
+    int* count = reinterpret_cast<int*>(bst + 1);
+    int* off = count + kNB;
+    int* cursor = off + kNB + 1;
+    int* big = cursor + kNB;
+    HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->lo, 0xFF, 8, stream));
+    HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->hi, 0x00, 8, stream));
+    HG_CHECK_CUDA(W, cudaMemsetAsync(count, 0, 4 * kNB, stream));
+    const unsigned g = grid_for(n_max, 256, 148 * 4);
+#define HG_L(K, G, B, ...)                                                                   \
+  {                                                                                          \
+    const cudaError_t _pe = hg::launch_pdl(K, dim3(G), dim3(B), 0, stream, __VA_ARGS__);     \
+    if (_pe != cudaSuccess) return hg::fail(W, hg::kCuda, cudaGetErrorString(_pe));          \
+    HG_LAUNCHED(W);                                                                          \
+  }
+    // keys -> k2 / v2; bucketed -> keys_in / vals_in; sorted -> keys_out / vals_out (read by hg_cache_write)
+    HG_L(k_norm_keys, grid_for(n_max, 256), 256, n_dev, n_max, p_grad, live, src_nodes, norms, k2, v2, layer_ctr);
+    HG_L(k_bs_minmax, g, 256, n_dev, (const NormKey*)k2, bst);
+    HG_L(k_bs_hist, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, count);
+    HG_L(k_bs_scan, 1, 1024, (const int*)count, off, cursor, big, bst);
+    HG_L(k_bs_scatter, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, cursor, keys_in, vals_in);
+    HG_L(k_bs_small, 148 * 8, 256, (const int*)off, (const NormKey*)keys_in, (const int32_t*)vals_in, keys_out,
+         vals_out);
+    HG_L(k_bs_big, 64, 256, (const int*)off, (const int*)big, (const BucketState*)bst, keys_in, vals_in, k2, v2,
+         keys_out, vals_out);
+#undef HG_L
+    { const cudaError_t _pe = hg::launch_pdl(k_rank_admit, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev,
+                                             (const NormKey*)keys_out, (const int32_t*)vals_out, live, computed_flag,
+                                             row_of, row_owner, wflag, retained, layer_ctr);
+      if (_pe != cudaSuccess) return hg::fail(W, hg::kCuda, cudaGetErrorString(_pe)); }
+    HG_LAUNCHED(W);
+    return scan_launch<int>(W, FlagU8{wflag}, DevCount{n_dev}, n_max, part, EmitCompact{wlist},
+                            StoreNWrite{layer_ctr}, stream);
+  }
+  const bool radix = mode == kSortRadix;
   // the merge sort is in place: keys go straight to keys_out / vals_out
   { const cudaError_t _pe = hg::launch_pdl(k_norm_keys, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev, n_max, p_grad, live, src_nodes, norms,
                                                         radix ? keys_in : keys_out, radix ? vals_in : vals_out,
