@@ -50,6 +50,36 @@ struct EmitCompactPos {
   }
 };
 
+// both compactions of a block in one scan: (keep[i] for i < n_dst, src_mask[i])
+struct KeepSrcFlags {
+  const uint8_t* keep;
+  const uint8_t* src_mask;
+  const int32_t* n_dst_dev;
+  __device__ I64x2 operator()(long long i) const {
+    return {(i < *n_dst_dev && keep[i]) ? 1ll : 0ll, src_mask[i] ? 1ll : 0ll};
+  }
+};
+struct EmitKeepSrc {
+  int32_t* compute_rows;
+  int32_t* pos_of;
+  int32_t* live_src;
+  const int32_t* n_dst_dev;
+  __device__ void operator()(long long i, I64x2 excl, I64x2 v) const {
+    if (i < *n_dst_dev) {
+      if (v.a) compute_rows[excl.a] = (int32_t)i;
+      pos_of[i] = v.a ? (int32_t)excl.a : -1;
+    }
+    if (v.b) live_src[excl.b] = (int32_t)i;
+  }
+};
+struct StoreKeepSrcTotals {
+  int32_t* counts;
+  __device__ void operator()(I64x2 t) const {
+    counts[0] = (int32_t)t.a;
+    counts[1] = (int32_t)t.b;
+  }
+};
+
 __global__ void k_lookup(const int32_t* n_live_dev, const int32_t* __restrict__ live,
                          const int32_t* __restrict__ src_nodes, int32_t* __restrict__ row_of,
                          const int32_t* __restrict__ admit_iter, int32_t* __restrict__ row_owner, const int* it_dev,
@@ -90,7 +120,7 @@ using namespace hg;
 
 extern "C" {
 
-long long hg_prune_scratch_bytes(long long n_src_max) { return (scan_tiles(n_src_max) + 1) * 4 + 256; }
+long long hg_prune_scratch_bytes(long long n_src_max) { return (scan_tiles(n_src_max) + 1) * 16 + 256; }
 
 // Prune block b and (optionally) probe the layer-b cache. See hgb200.h.
 int hg_prune_block(const int32_t* n_dst_dev, long long n_dst_max, const int32_t* n_src_dev, long long n_src_max,
@@ -106,13 +136,12 @@ int hg_prune_block(const int32_t* n_dst_dev, long long n_dst_max, const int32_t*
       n_dst_dev, live_dst, inj_dst, start, end, col, keep, src_mask,
       reinterpret_cast<unsigned long long*>(global_ctr + kGCtrPruneWrites)); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
-  int* part = reinterpret_cast<int*>(scratch);
-  int st = scan_launch<int>(W, FlagU8{keep}, DevCount{n_dst_dev}, n_dst_max, part,
-                            EmitCompactPos{compute_rows, pos_of}, StoreTotalI32{counts_dev + 0}, stream);
-  if (st) return st;
-  st = scan_launch<int>(W, FlagU8{src_mask}, DevCount{n_src_dev}, n_src_max, part,
-                        EmitCompactPos{live_src, nullptr}, StoreTotalI32{counts_dev + 1}, stream);
-  return st;
+  // compute rows (compact keep) and layer_live (compact src_mask) in one pass
+  // over the block's sources (dst rows are a prefix of them)
+  I64x2* part = reinterpret_cast<I64x2*>(scratch);
+  return scan_launch<I64x2>(W, KeepSrcFlags{keep, src_mask, n_dst_dev}, DevCount{n_src_dev}, n_src_max, part,
+                            EmitKeepSrc{compute_rows, pos_of, live_src, n_dst_dev}, StoreKeepSrcTotals{counts_dev},
+                            stream);
 }
 
 int hg_cache_lookup(const int32_t* n_live_dev, long long n_live_max, const int32_t* live, const int32_t* src_nodes,

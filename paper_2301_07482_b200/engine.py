@@ -265,6 +265,7 @@ class StepEngine:
                 if lc.table is not None:
                     inj_flag = hit_flag
                     injected[b - 1] = Injection(hit_flag, hit_row, lc.table)
+            self._mark(f"pruned{b}", stream)
 
         def R_dev(b):
             return counts[2 * b:2 * b + 1]
@@ -300,6 +301,7 @@ class StepEngine:
                                   blk.n_dst_dev, live=live[b], n_live=blk.num_src, n_live_dev=n_live_dev(b))
             tapes.append(t)
             h = t.h_out
+            self._mark(f"forward{b}", stream)
         d_h, loss = cross_entropy_dev(tapes[-1].h_out, self.labels, B, net.dims[-1], sp)
         self._mark("forward+loss", stream)
 
