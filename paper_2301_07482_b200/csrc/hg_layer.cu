@@ -152,14 +152,44 @@ __global__ void k_scatter_rows(const int32_t* R_dev, const int32_t* __restrict__
 __global__ void k_inject(const int32_t* n_dev, const uint8_t* __restrict__ flag, const int32_t* __restrict__ hit_row,
                          const float* __restrict__ table, int dim, float* __restrict__ h_out) {
   pdl_wait();
+  // a warp takes 32 rows at once (flags / cache rows read lane-parallel), then
+  // copies the injected ones with 128-bit accesses, two rows in flight
   const int n = *n_dev;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
-    if (!flag[r]) continue;
-    const float* src = table + (long long)hit_row[r] * dim;
-    float* dst = h_out + (long long)r * dim;
-    for (int j = lane; j < dim; j += 32) dst[j] = src[j];
+  const bool vec = (dim & 3) == 0;
+  const int nv = vec ? dim >> 2 : dim;
+  for (int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < n; r0 += warps * 32) {
+    const int r = r0 + lane;
+    const bool f = r < n && flag[r];
+    const int hr = f ? hit_row[r] : 0;
+    unsigned m = __ballot_sync(0xffffffffu, f);
+    while (m) {
+      const int q0 = __ffs(m) - 1;
+      m &= m - 1;
+      const int q1 = m ? __ffs(m) - 1 : -1;
+      if (q1 >= 0) m &= m - 1;
+      const int h0 = __shfl_sync(0xffffffffu, hr, q0);
+      const int h1 = __shfl_sync(0xffffffffu, hr, q1 < 0 ? q0 : q1);
+      if (vec) {
+        const float4* s0 = reinterpret_cast<const float4*>(table + (long long)h0 * dim);
+        const float4* s1 = reinterpret_cast<const float4*>(table + (long long)h1 * dim);
+        float4* d0 = reinterpret_cast<float4*>(h_out + (long long)(r0 + q0) * dim);
+        float4* d1 = reinterpret_cast<float4*>(h_out + (long long)(r0 + (q1 < 0 ? q0 : q1)) * dim);
+        for (int j = lane; j < nv; j += 32) {
+          const float4 a = s0[j];
+          float4 b;
+          if (q1 >= 0) b = s1[j];
+          d0[j] = a;
+          if (q1 >= 0) d1[j] = b;
+        }
+      } else {
+        for (int j = lane; j < nv; j += 32) {
+          h_out[(long long)(r0 + q0) * dim + j] = table[(long long)h0 * dim + j];
+          if (q1 >= 0) h_out[(long long)(r0 + q1) * dim + j] = table[(long long)h1 * dim + j];
+        }
+      }
+    }
   }
 }
 
