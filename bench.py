@@ -355,7 +355,8 @@ def main():
     if os.path.exists(peaks_path):
         peak, peak_src = json.load(open(peaks_path))["hbm_gbs"], "measured"
     tv = timers.view(8, 8).cpu().tolist()
-    names = ["k_load_rows", "k_aggregate", "k_transpose_agg", "k_select", "k_tsgemm (forward)", "k_tsgemm (dgrad)"]
+    names = ["k_load_rows", "k_aggregate", "k_transpose_agg", "k_select", "k_tsgemm (forward)", "k_tsgemm (dgrad)",
+             "k_tsgemm (wgrad, split-K)"]
     per_kernel = {n: {"launches": int(tv[i][3]), "ms_total": tv[i][2] / 1e6,
                       "share_of_step": (tv[i][2] / 1e9) / t_dev} for i, n in enumerate(names)}
     g_delta = (tr.cache.gctr - g_before).cpu().tolist()

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tsgemm(const __grid_constant__ 
   const int M = sh.M_dev ? *sh.M_dev : sh.M;
   const int K = sh.K_dev ? *sh.K_dev : sh.K;
   const int m0 = blockIdx.x * kTM;
-  KTimer* kt = (g_kt && !kMN) ? g_kt + (Epi::kFwd ? kTGemmFwd : kTGemmBwd) : nullptr;
+  KTimer* kt = g_kt ? g_kt + (kMN ? kTGemmWgrad : (Epi::kFwd ? kTGemmFwd : kTGemmBwd)) : nullptr;
   kt_begin(kt);
   if (m0 >= M) {
     kt_end(kt);
