@@ -127,3 +127,19 @@ def test_ipc_shards_two_processes(tmp_path):
         w = np.load(tmp_path / f"r{r}_w.npy")
         np.testing.assert_array_equal(w[0], w[1])
     np.testing.assert_array_equal(np.load(tmp_path / "r0_w.npy"), np.load(tmp_path / "r1_w.npy"))
+
+
+@pytest.mark.parametrize("kind", ["gcn", "gat"])
+def test_virtual_shards_engine_other_layer_kinds(kind):
+    """Sharded features under the CUDA-graph engine (pipelined sampling) for
+    GCN and GAT: bitwise the same run as with the plain table."""
+    import paper_2301_07482_b200 as hg
+    ds, g = _data()
+    k = hg.LayerKind.GCN if kind == "gcn" else hg.LayerKind.GAT
+    runs = []
+    for feats in (ds.features, hg.ShardedFeatures.virtual(ds.features, 4)):
+        tr = hg.Trainer(g, feats, ds.labels, ds.train_ids, _cfg(hg, kind=k, heads=2), ds.num_classes)
+        b = hg.make_batches(ds.train_ids, tr.cfg)[:10]
+        ms = [tr.train_step(i, 0, s, next_batch=(i + 1, b[i + 1]) if i + 1 < len(b) else None) for i, s in enumerate(b)]
+        runs.append(([(m.loss, m.hits, m.admissions, m.feature_hits) for m in ms], tr.network.checksum_bytes()))
+    assert runs[0] == runs[1]
