@@ -46,6 +46,10 @@ CONFIGS = {
                         "3-layer GAT (4 heads, hidden 256), fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
                n=111_000_000, m=7, d=128, classes=172, fp16=True, capacity=6_000_000, max_capacity=24_000_000,
                kind="gat"),
+    "c4s": dict(workload="MAG240M-shape slice for one GPU: synthetic power-law (40M nodes, 280M edges, 768-d fp16, "
+                         "61 GB), 3-layer GraphSAGE hidden 256, fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
+                n=40_000_000, m=4, d=768, classes=153, fp16=True, capacity=6_000_000, max_capacity=12_000_000,
+                feature_rows_frac=0.01),
     "c1": dict(workload="synthetic power-law 100K nodes / 2M edges, 128-d fp32, 3-layer GraphSAGE hidden 256, "
                         "fanout 15,10,5, batch 1024, cache p_grad 0.9 t_stale 20",
                n=100_000, m=10, d=128, classes=8),
@@ -281,7 +285,9 @@ def main():
     kind = hg.LayerKind.GAT if cfgd.get("kind") == "gat" else hg.LayerKind.SAGE_MEAN
     tcfg = hg.TrainConfig(fanouts=FANOUTS, hidden=HIDDEN, batch_size=BATCH, eta=ETA, kind=kind, heads=4,
                           p_grad=P_GRAD, t_stale=T_STALE, seed=0, epochs=max(1, -(-need // per_epoch)),
-                          capacity=cfgd.get("capacity"), max_capacity=cfgd.get("max_capacity"))
+                          capacity=cfgd.get("capacity"), max_capacity=cfgd.get("max_capacity"),
+                          feature_rows=(int(cfgd["n"] * cfgd["feature_rows_frac"]) if "feature_rows_frac" in cfgd
+                                        else None))
     tr = hg.Trainer(graph, feats_dev, labels, train, tcfg, cfgd["classes"])
     if world > 1:
         from paper_2301_07482_b200.distributed import make_allreduce_hook
@@ -445,12 +451,12 @@ def main():
         config["cache_capacity_rows_per_layer"] = [cfgd["capacity"], cfgd["max_capacity"]]
     if cfgd.get("fp16"):
         out["dtype"] = "fp32 (fp16 feature table, converted in the gather)"
-        config["l2"] = "inputs > L2 (28 GB features + 6 GB graph resident, random rows)"
+        config["l2"] = f"inputs > L2 ({cfgd['n'] * cfgd['d'] * 2 / 1e9:.0f} GB features resident, random rows)"
     if rank == 0 and world == 1 and not args.no_cpu_baseline and cfgd.get("fp16"):
         out["cpu_baseline"] = {"value": None, "unit": "seeds/s", "cores": len(os.sched_getaffinity(0)),
-                               "kind": "port", "sample": "not run at the papers100M shape (the numpy port needs "
-                               "the 28 GB table and 12 GB graph in host RAM, minutes per iteration); "
-                               "see the C2 line for the CPU comparison"}
+                               "kind": "port", "sample": "not run at this shape (the numpy port needs the full "
+                               f"{cfgd['n'] * cfgd['d'] * 2 / 1e9:.0f} GB feature table and the graph in host "
+                               "RAM, minutes per iteration); see the C2 line for the CPU comparison"}
     elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_reference(cfgd, data, steps=3, warmup=1, budget_s=args.cpu_budget)
         out["cpu_baseline"] = {"value": r["value"], "unit": "seeds/s", "cores": r["cores"], "kind": "port",

@@ -37,8 +37,8 @@ namespace {
 
 constexpr int kKindGCN = 0;
 constexpr int kKindSAGE = 1;
-constexpr int kMaxVecPerLane = 4;  // d_in <= 512 floats
-constexpr int kMaxRowFloats = 1056; // [self | agg | 1 | pad] <= 2*512 + 32
+constexpr int kMaxVecPerLane = 8;  // d_in <= 1024 floats (kT = float4 per lane, templated)
+constexpr int kMaxRowFloats = 1056; // k_gather_dz staging: d_out <= 1056
 
 __device__ __forceinline__ float4 f4_fmadd_rn(float4 acc, float c, float4 x) {
   return make_float4(__fadd_rn(acc.x, __fmul_rn(c, x.x)), __fadd_rn(acc.y, __fmul_rn(c, x.y)),
@@ -49,21 +49,23 @@ __device__ __forceinline__ float gcn_coef(int dd, int sd) {
   return (float)(1.0 / sqrt(((double)dd + 1.0) * ((double)sd + 1.0)));
 }
 
-// one warp per compute row
-template <int kKind>
+// one warp per compute row; kT = float4 vectors per lane (d <= 128 kT); the
+// [self | agg | 1 | pad] row is staged in dynamic shared memory (row_floats
+// per warp) before it is emitted as TS core rows
+template <int kKind, int kT>
 __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
-                                                   int d, uint8_t* __restrict__ A_ts, long long plane) {
+                                                   int d, uint8_t* __restrict__ A_ts, long long plane, int row_floats) {
   pdl_wait();
-  __shared__ __align__(16) float s_rows[8][kMaxRowFloats];
+  extern __shared__ __align__(16) float agg_smem[];
   const int R = *R_dev;
   const int lane = threadIdx.x & 31;
   const int nv = d >> 2;
   const int K = kKind == kKindSAGE ? 2 * d : d;
   const int nK = (K + 1 + 31) / 32;          // TS column chunks of [. | 1 | 0 pad]
-  float* srow = s_rows[threadIdx.x >> 5];
+  float* srow = agg_smem + (size_t)(threadIdx.x >> 5) * row_floats;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   KTimer* kt = g_kt ? g_kt + kTAggregate : nullptr;
   kt_begin(kt);
@@ -71,9 +73,9 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
     const int r = rows[i];
     const int e0 = start[r], e1 = end[r];
     const int cnt = e1 - e0;
-    float4 acc[kMaxVecPerLane];
+    float4 acc[kT];
 #pragma unroll
-    for (int t = 0; t < kMaxVecPerLane; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int t = 0; t < kT; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     float cs = 0.f;
     if (kKind == kKindSAGE) cs = cnt > 0 ? (float)(1.0 / (double)cnt) : 0.f;
     const int dd = kKind == kKindGCN ? dst_deg[r] : 0;
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
         w[q] = kKind == kKindSAGE ? cs : gcn_coef(dd, src_deg[c[q]]);
       }
 #pragma unroll
-      for (int t = 0; t < kMaxVecPerLane; ++t) {
+      for (int t = 0; t < kT; ++t) {
         const int v = lane + 32 * t;
         if (v < nv) {
           float4 x[4];
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
       const int c0 = col[e];
       const float w0 = kKind == kKindSAGE ? cs : gcn_coef(dd, src_deg[c0]);
 #pragma unroll
-      for (int t = 0; t < kMaxVecPerLane; ++t) {
+      for (int t = 0; t < kT; ++t) {
         const int v = lane + 32 * t;
         if (v < nv) acc[t] = f4_fmadd_rn(acc[t], w0, reinterpret_cast<const float4*>(h_in + (long long)c0 * d)[v]);
       }
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const i
     // then emit it as bf16 hi/lo TS core-matrix rows (hg_ts.cuh)
     const float4* hs = reinterpret_cast<const float4*>(h_in + (long long)r * d);
 #pragma unroll
-    for (int t = 0; t < kMaxVecPerLane; ++t) {
+    for (int t = 0; t < kT; ++t) {
       const int v = lane + 32 * t;
       if (v < nv) {
         if (kKind == kKindSAGE) {
@@ -308,7 +310,7 @@ __global__ void k_csc_segments(const unsigned* __restrict__ keys, long long E_ma
 }
 
 // d_in rows for the live sources of block l + their fp64 norms (one warp per source)
-template <int kKind>
+template <int kKind, int kT>
 __global__ void __launch_bounds__(256) k_transpose_agg(
     const int32_t* n_live_dev, const int32_t* __restrict__ live, const int32_t* __restrict__ seg_lo,
     const int32_t* __restrict__ seg_hi, const unsigned* __restrict__ srt_vals, const int32_t* __restrict__ rows,
@@ -326,9 +328,9 @@ __global__ void __launch_bounds__(256) k_transpose_agg(
   kt_begin(kt);
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
     const int c = live[i];
-    float4 acc[kMaxVecPerLane];
+    float4 acc[kT];
 #pragma unroll
-    for (int t = 0; t < kMaxVecPerLane; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int t = 0; t < kT; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int p0 = seg_lo[c], p1 = seg_hi[c];
     const int sd = kKind == kKindGCN ? src_deg[c] : 0;
     for (int p = p0; p < p1; ++p) {
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(256) k_transpose_agg(
       }
       const float4* g = reinterpret_cast<const float4*>(SG + (long long)pos * ldSG + goff);
 #pragma unroll
-      for (int t = 0; t < kMaxVecPerLane; ++t) {
+      for (int t = 0; t < kT; ++t) {
         const int v = lane + 32 * t;
         if (v < nv) acc[t] = f4_fmadd_rn(acc[t], w, g[v]);
       }
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(256) k_transpose_agg(
       const float4* s = reinterpret_cast<const float4*>(SG + (long long)self * ldSG);
       const float ws = kKind == kKindSAGE ? 1.f : gcn_coef(dst_deg[c], sd);
 #pragma unroll
-      for (int t = 0; t < kMaxVecPerLane; ++t) {
+      for (int t = 0; t < kT; ++t) {
         const int v = lane + 32 * t;
         if (v < nv) {
           if (kKind == kKindSAGE) {
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(256) k_transpose_agg(
     double sq = 0.0;
     float4* out = reinterpret_cast<float4*>(d_in + (long long)c * d);
 #pragma unroll
-    for (int t = 0; t < kMaxVecPerLane; ++t) {
+    for (int t = 0; t < kT; ++t) {
       const int v = lane + 32 * t;
       if (v < nv) {
         out[v] = acc[t];
@@ -416,18 +418,37 @@ int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int3
                      const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
                      const float* h_in, int d, void* A_ts, cudaStream_t stream) {
   const char* W = "hg_aggregate_fwd";
-  if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 512");
+  if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 1024");
   // grid covers the compute rows and the zero padding up to the next 128-row tile
   const long long rows_pad = (R_max + kTsRows - 1) / kTsRows * kTsRows;
   const unsigned grid = grid_for(rows_pad * 32, 256, 148 * 16);
   uint8_t* a = static_cast<uint8_t*>(A_ts);
-  const long long plane = ts_plane_bytes(R_max, (kind == kKindSAGE ? 2 * d : d) + 1);
-  if (kind == kKindSAGE)
-    { const cudaError_t _pe = hg::launch_pdl(k_aggregate<kKindSAGE>, dim3(grid), dim3(256), 0, stream, R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a,
-                                                     plane); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
-  else
-    { const cudaError_t _pe = hg::launch_pdl(k_aggregate<kKindGCN>, dim3(grid), dim3(256), 0, stream, R_dev, rows, start, end, col, dst_deg, src_deg, h_in, d, a,
-                                                    plane); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  const int K1 = (kind == kKindSAGE ? 2 * d : d) + 1;
+  const long long plane = ts_plane_bytes(R_max, K1);
+  const int row_floats = (K1 + 31) / 32 * 32;
+  const size_t smem = (size_t)8 * row_floats * 4;
+  const int vpl = (d / 4 + 31) / 32;
+  cudaError_t pe = cudaSuccess;
+#define HG_AGG(KIND, T)                                                                                           \
+  {                                                                                                              \
+    if (smem > 48 * 1024) {                                                                                      \
+      pe = cudaFuncSetAttribute(k_aggregate<KIND, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+      if (pe != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(pe));                                      \
+    }                                                                                                            \
+    pe = hg::launch_pdl(k_aggregate<KIND, T>, dim3(grid), dim3(256), smem, stream, R_dev, rows, start, end, col,  \
+                        dst_deg, src_deg, h_in, d, a, plane, row_floats);                                        \
+  }
+#define HG_AGG_T(KIND)                                                                                            \
+  if (vpl <= 1) HG_AGG(KIND, 1) else if (vpl <= 2) HG_AGG(KIND, 2) else if (vpl <= 4) HG_AGG(KIND, 4)           \
+  else HG_AGG(KIND, 8)
+  if (kind == kKindSAGE) {
+    HG_AGG_T(kKindSAGE)
+  } else {
+    HG_AGG_T(kKindGCN)
+  }
+#undef HG_AGG_T
+#undef HG_AGG
+  if (pe != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(pe));
   HG_LAUNCHED(W);
   return kOk;
 }
@@ -509,16 +530,24 @@ int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, 
                      const int32_t* n_dst_dev, const int32_t* pos_of, const float* SG, int ldSG, int d,
                      float* d_in, double* norms, cudaStream_t stream) {
   const char* W = "hg_transpose_agg";
-  if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 512");
+  if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 1024");
   const unsigned grid = grid_for(n_live_max * 32, 256, 148 * 16);
-  if (kind == kKindSAGE)
-    { const cudaError_t _pe = hg::launch_pdl(k_transpose_agg<kKindSAGE>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, seg_lo, seg_hi, vals_sorted, rows, start,
-                                                         end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d,
-                                                         d_in, norms); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
-  else
-    { const cudaError_t _pe = hg::launch_pdl(k_transpose_agg<kKindGCN>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, seg_lo, seg_hi, vals_sorted, rows, start,
-                                                        end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d, d_in,
-                                                        norms); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  const int vpl = (d / 4 + 31) / 32;
+  cudaError_t pe = cudaSuccess;
+#define HG_TA(KIND, T)                                                                                            \
+  pe = hg::launch_pdl(k_transpose_agg<KIND, T>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, seg_lo, seg_hi,  \
+                      vals_sorted, rows, start, end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d, d_in, norms)
+#define HG_TA_T(KIND)                                                                                             \
+  if (vpl <= 1) HG_TA(KIND, 1); else if (vpl <= 2) HG_TA(KIND, 2); else if (vpl <= 4) HG_TA(KIND, 4);           \
+  else HG_TA(KIND, 8);
+  if (kind == kKindSAGE) {
+    HG_TA_T(kKindSAGE)
+  } else {
+    HG_TA_T(kKindGCN)
+  }
+#undef HG_TA_T
+#undef HG_TA
+  if (pe != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(pe));
   HG_LAUNCHED(W);
   return kOk;
 }
