@@ -35,7 +35,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .nn import (Injection, LayerKind, build_csc, cross_entropy_dev, layer_backward_dev, layer_forward_dev,
+from .nn import (Injection, LayerKind, build_csc, cross_entropy_dev, inject_rows_dev, layer_backward_dev,
+                 layer_forward_dev,
                  load_features_dev, pack_dgrad_weights, sgd_step)
 from .sampler import SamplerWorkspace, SampleSlot, layer_bounds, pcg_words, sample_blocks_dev
 
@@ -101,6 +102,7 @@ class StepEngine:
         # during the forward; weight-gradient GEMMs run on wgrad_stream
         self.prep_stream = torch.cuda.Stream(self.dev)
         self.wgrad_stream = torch.cuda.Stream(self.dev)
+        self.inj_stream = torch.cuda.Stream(self.dev)      # cache-hit row injection (forward)
         # cache updates of layer l run on side stream l, overlapping the
         # backward of layers < l (they only read the forward tape and norms[l])
         self.upd_streams = {l: torch.cuda.Stream(self.dev) for l in range(1, self.L)}
@@ -274,6 +276,22 @@ class StepEngine:
             return counts[2 * b + 1:2 * b + 2]
 
         self._mark("pruned", stream)
+        # injected (cache-hit) rows of every layer output depend only on the
+        # prune walk: write them on a side stream while the layers compute
+        # (SAGE / GCN; the main stream joins before the next layer reads them)
+        h_outs = [None] * L
+        inj_stream = None
+        if net.kind is not LayerKind.GAT and any(x is not None for x in injected):
+            # outputs allocated on the main stream (it owns and frees them; the
+            # side stream is joined before any main-stream use after it)
+            h_outs = [torch.empty((blocks[b].num_dst, net.dims[b + 1]), dtype=torch.float32, device=dev)
+                      for b in range(L)]
+            inj_stream = self.inj_stream
+            inj_stream.wait_stream(stream)
+            isp = _lib.stream_ptr(inj_stream)
+            for b in range(L):
+                if injected[b] is not None:
+                    inject_rows_dev(injected[b], h_outs[b], blocks[b].num_dst, blocks[b].n_dst_dev, isp)
         # ---- off-critical-path backward prep (overlaps the forward) ----
         prep = self.prep_stream
         prep.wait_stream(stream)
@@ -297,8 +315,11 @@ class StepEngine:
         tapes = []
         for b in range(L):
             blk = blocks[b]
+            if b == 1 and inj_stream is not None:
+                stream.wait_stream(inj_stream)      # layer 1 reads layer 0's injected rows
             t = layer_forward_dev(net, b, blk, h, rows[b], blk.num_dst, R_dev(b), b < L - 1, injected[b], sp,
-                                  blk.n_dst_dev, live=live[b], n_live=blk.num_src, n_live_dev=n_live_dev(b))
+                                  blk.n_dst_dev, live=live[b], n_live=blk.num_src, n_live_dev=n_live_dev(b),
+                                  h_out=h_outs[b], injected_already=inj_stream is not None)
             tapes.append(t)
             h = t.h_out
             self._mark(f"forward{b}", stream)

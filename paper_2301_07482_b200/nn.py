@@ -410,9 +410,18 @@ def gat_layer_backward_dev(net: Network, l: int, blk, t: GatTape, d_h, grads, ne
     return d_full, norms[:n_live]
 
 
+def inject_rows_dev(inj: Injection, h_out: torch.Tensor, n_dst: int, n_dst_dev, stream) -> None:
+    """h_out[r] = table[row[r]] for the injected rows (nn.py:290-293)."""
+    _lib.call("hg_inject_rows", _lib.ptr(n_dst_dev), n_dst, _lib.ptr(inj.flag), _lib.ptr(inj.row),
+              _lib.ptr(inj.table), int(h_out.shape[1]), _lib.ptr(h_out), stream)
+
+
 def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch.Tensor, R: int,
                       R_dev: torch.Tensor, act: bool, inj: Injection | None, stream,
-                      n_dst_dev: torch.Tensor | None = None, live=None, n_live=None, n_live_dev=None) -> LayerTape:
+                      n_dst_dev: torch.Tensor | None = None, live=None, n_live=None, n_live_dev=None,
+                      h_out: torch.Tensor | None = None, injected_already: bool = False) -> LayerTape:
+    """h_out / injected_already: the engine preallocates the output and writes
+    the injected rows on a side stream (they do not depend on the layer)."""
     if net.kind is LayerKind.GAT:
         if h_in.shape[0] != blk.num_src:
             raise ValueError(f"h_in has {h_in.shape[0]} rows, frontier needs {blk.num_src}")
@@ -435,14 +444,14 @@ def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch
     PT = torch.empty(ts_bytes(d_out, K + 1), dtype=torch.uint8, device=dev)   # TS(P^T): B of the forward
     _lib.call("hg_ts_pack", _lib.ptr(slab), d_out, 1, d_out, K + 1, d_out, _lib.ptr(PT), stream)
     n_dst = blk.num_dst
-    h_out = torch.empty((n_dst, d_out), dtype=torch.float32, device=dev)
+    if h_out is None:
+        h_out = torch.empty((n_dst, d_out), dtype=torch.float32, device=dev)
     # z = [A | 1] . P on tcgen05, ReLU + scatter to h_out[rows] in the epilogue
     _lib.call("hg_ts_linear_fwd", _lib.ptr(R_dev), R, _lib.ptr(A), K + 1, _lib.ptr(PT), d_out, _lib.ptr(rows),
               int(act), _lib.ptr(h_out), stream)
-    if inj is not None:
+    if inj is not None and not injected_already:
         nd = n_dst_dev if n_dst_dev is not None else _dev_count(n_dst, dev)
-        _lib.call("hg_inject_rows", _lib.ptr(nd), n_dst, _lib.ptr(inj.flag),
-                  _lib.ptr(inj.row), _lib.ptr(inj.table), d_out, _lib.ptr(h_out), stream)
+        inject_rows_dev(inj, h_out, n_dst, nd, stream)
     return LayerTape(rows, R, R_dev, A, K, act, h_out, inj)
 
 
