@@ -37,7 +37,7 @@ import torch
 from . import _lib
 from .nn import (Injection, LayerKind, build_csc, cross_entropy_dev, inject_rows_dev, layer_backward_dev,
                  layer_forward_dev,
-                 load_features_dev, pack_dgrad_weights, sgd_step)
+                 load_features_dev, pack_dgrad_weights, pack_forward_weights, sgd_step, ts_bytes)
 from .sampler import SamplerWorkspace, SampleSlot, layer_bounds, pcg_words, sample_blocks_dev
 
 
@@ -236,6 +236,20 @@ class StepEngine:
             with torch.cuda.stream(samp):
                 sample_blocks_dev(tr.graph, self.seeds, self.F0, B, cfg.fanouts, self.ws, samp, self.slots[1 - s])
                 self._mark("next_sampled (side)", samp)
+        # forward weight operands (depend only on the weights): packed on the
+        # injection stream concurrently with the prune walk
+        PTs = [None] * L
+        packed = None
+        if net.kind is not LayerKind.GAT:
+            # buffers owned by the main stream (allocated here), filled on the side stream
+            PTs = [torch.empty(ts_bytes(net.dims[b + 1], (2 * net.dims[b] if net.kind is LayerKind.SAGE_MEAN
+                                                         else net.dims[b]) + 1), dtype=torch.uint8, device=dev)
+                   for b in range(L)]
+            self.inj_stream.wait_stream(stream)
+            for b in range(L):
+                pack_forward_weights(net, b, _lib.stream_ptr(self.inj_stream), out=PTs[b])
+            packed = torch.cuda.Event()
+            packed.record(self.inj_stream)
         blocks = self._blocks(s)
 
         # ---- prune walk + lookups (trainer.py:166-207) ----
@@ -287,7 +301,7 @@ class StepEngine:
             h_outs = [torch.empty((blocks[b].num_dst, net.dims[b + 1]), dtype=torch.float32, device=dev)
                       for b in range(L)]
             inj_stream = self.inj_stream
-            inj_stream.wait_stream(stream)
+            inj_stream.wait_stream(stream)              # after the prune walk's lookups
             isp = _lib.stream_ptr(inj_stream)
             for b in range(L):
                 if injected[b] is not None:
@@ -315,11 +329,13 @@ class StepEngine:
         tapes = []
         for b in range(L):
             blk = blocks[b]
+            if b == 0 and packed is not None:
+                stream.wait_event(packed)               # forward weight operands
             if b == 1 and inj_stream is not None:
-                stream.wait_stream(inj_stream)      # layer 1 reads layer 0's injected rows
+                stream.wait_stream(inj_stream)          # layer 1 reads layer 0's injected rows
             t = layer_forward_dev(net, b, blk, h, rows[b], blk.num_dst, R_dev(b), b < L - 1, injected[b], sp,
                                   blk.n_dst_dev, live=live[b], n_live=blk.num_src, n_live_dev=n_live_dev(b),
-                                  h_out=h_outs[b], injected_already=inj_stream is not None)
+                                  h_out=h_outs[b], injected_already=inj_stream is not None, PT=PTs[b])
             tapes.append(t)
             h = t.h_out
             self._mark(f"forward{b}", stream)
@@ -353,6 +369,8 @@ class StepEngine:
                                                mark=lambda what, l=l, side=side: self._mark(f"cache{l}_{what} (side)",
                                                                                             side))
                     self._mark(f"cache_update{l} (side)", side)
+        if packed is not None:
+            stream.wait_stream(self.inj_stream)      # only when work was enqueued there (graph capture)
         stream.wait_stream(self.wgrad_stream)
         if tr.grad_hook is not None:
             tr.grad_hook(grads)

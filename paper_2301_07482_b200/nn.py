@@ -419,9 +419,11 @@ def inject_rows_dev(inj: Injection, h_out: torch.Tensor, n_dst: int, n_dst_dev, 
 def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch.Tensor, R: int,
                       R_dev: torch.Tensor, act: bool, inj: Injection | None, stream,
                       n_dst_dev: torch.Tensor | None = None, live=None, n_live=None, n_live_dev=None,
-                      h_out: torch.Tensor | None = None, injected_already: bool = False) -> LayerTape:
+                      h_out: torch.Tensor | None = None, injected_already: bool = False,
+                      PT: torch.Tensor | None = None) -> LayerTape:
     """h_out / injected_already: the engine preallocates the output and writes
-    the injected rows on a side stream (they do not depend on the layer)."""
+    the injected rows on a side stream (they do not depend on the layer);
+    PT: the forward weight operand packed ahead (pack_forward_weights)."""
     if net.kind is LayerKind.GAT:
         if h_in.shape[0] != blk.num_src:
             raise ValueError(f"h_in has {h_in.shape[0]} rows, frontier needs {blk.num_src}")
@@ -440,9 +442,8 @@ def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch
     _lib.call("hg_aggregate_fwd", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(blk.adj.start),
               _lib.ptr(blk.adj.end), _lib.ptr(blk.adj.col_indices), _lib.ptr(blk.dst_deg), _lib.ptr(blk.src_deg),
               _lib.ptr(h_in), d_in, _lib.ptr(A), stream)
-    slab = net.slab(l)
-    PT = torch.empty(ts_bytes(d_out, K + 1), dtype=torch.uint8, device=dev)   # TS(P^T): B of the forward
-    _lib.call("hg_ts_pack", _lib.ptr(slab), d_out, 1, d_out, K + 1, d_out, _lib.ptr(PT), stream)
+    if PT is None:
+        PT = pack_forward_weights(net, l, stream)
     n_dst = blk.num_dst
     if h_out is None:
         h_out = torch.empty((n_dst, d_out), dtype=torch.float32, device=dev)
@@ -534,6 +535,15 @@ def build_csc(blk, keep: torch.Tensor, pos_of: torch.Tensor, n_dst_dev, stream, 
               _lib.ptr(blk.adj.col_indices), E, n_src, _lib.ptr(keys), _lib.ptr(vals), _lib.ptr(seg_lo),
               _lib.ptr(seg_hi), _lib.ptr(scratch), sb, stream)
     return BlockCsc(vals, seg_lo, seg_hi)
+
+
+def pack_forward_weights(net: Network, l: int, stream, out: torch.Tensor | None = None) -> torch.Tensor:
+    """TS(P^T) of layer l (SAGE / GCN): the B operand of the forward GEMM."""
+    d_in, d_out = net.dims[l], net.dims[l + 1]
+    K = 2 * d_in if _kind_code(net.kind) == KIND_SAGE else d_in
+    PT = out if out is not None else torch.empty(ts_bytes(d_out, K + 1), dtype=torch.uint8, device=net.flat.device)
+    _lib.call("hg_ts_pack", _lib.ptr(net.slab(l)), d_out, 1, d_out, K + 1, d_out, _lib.ptr(PT), stream)
+    return PT
 
 
 def pack_dgrad_weights(net: Network, l: int, stream) -> torch.Tensor:
