@@ -313,10 +313,16 @@ class StepEngine:
         with torch.cuda.stream(prep):
             psp = _lib.stream_ptr(prep)
             gat = net.kind is LayerKind.GAT   # GAT needs the transposed edges at every layer (dz for dW)
-            for l in range(0 if gat else 1, L):
+            # outermost layer first: the backward consumes them in that order,
+            # each layer waits only for its own transposed edges / weights
+            prep_done = [None] * L
+            for l in range(L - 1, (-1 if gat else 0), -1):
                 cscs[l] = build_csc(blocks[l], keep[l], pos[l], blocks[l].n_dst_dev, psp)
                 if not gat:
                     w_ts[l] = pack_dgrad_weights(net, l, psp)
+                prep_done[l] = torch.cuda.Event()
+                prep_done[l].record(prep)
+            self._mark("backward_prep (side)", prep)
         # ---- layer-0 input (trainer.py:326-343) ----
         b0 = blocks[0]
         h = torch.empty((b0.num_src, tr.feature_dim), dtype=torch.float32, device=dev)
@@ -349,9 +355,10 @@ class StepEngine:
         grads = net.new_grads(zero=False)
         norms = [None] * L
         keepalive = []
-        stream.wait_stream(prep)
         for l in range(L - 1, -1, -1):
             blk = blocks[l]
+            if prep_done[l] is not None:
+                stream.wait_event(prep_done[l])
             d_prev, nrm = layer_backward_dev(net, l, blk, tapes[l], d_h, grads, l >= 1, keep[l], pos[l], live[l],
                                              blk.num_src, sp, blk.n_dst_dev, n_live_dev(l), csc=cscs[l],
                                              W_ts=w_ts[l], wgrad_stream=self.wgrad_stream, keepalive=keepalive)
@@ -369,6 +376,7 @@ class StepEngine:
                                                mark=lambda what, l=l, side=side: self._mark(f"cache{l}_{what} (side)",
                                                                                             side))
                     self._mark(f"cache_update{l} (side)", side)
+        stream.wait_stream(prep)
         if packed is not None:
             stream.wait_stream(self.inj_stream)      # only when work was enqueued there (graph capture)
         stream.wait_stream(self.wgrad_stream)
