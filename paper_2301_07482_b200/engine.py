@@ -290,22 +290,6 @@ class StepEngine:
             return counts[2 * b + 1:2 * b + 2]
 
         self._mark("pruned", stream)
-        # injected (cache-hit) rows of every layer output depend only on the
-        # prune walk: write them on a side stream while the layers compute
-        # (SAGE / GCN; the main stream joins before the next layer reads them)
-        h_outs = [None] * L
-        inj_stream = None
-        if net.kind is not LayerKind.GAT and any(x is not None for x in injected):
-            # outputs allocated on the main stream (it owns and frees them; the
-            # side stream is joined before any main-stream use after it)
-            h_outs = [torch.empty((blocks[b].num_dst, net.dims[b + 1]), dtype=torch.float32, device=dev)
-                      for b in range(L)]
-            inj_stream = self.inj_stream
-            inj_stream.wait_stream(stream)              # after the prune walk's lookups
-            isp = _lib.stream_ptr(inj_stream)
-            for b in range(L):
-                if injected[b] is not None:
-                    inject_rows_dev(injected[b], h_outs[b], blocks[b].num_dst, blocks[b].n_dst_dev, isp)
         # ---- off-critical-path backward prep (overlaps the forward) ----
         prep = self.prep_stream
         prep.wait_stream(stream)
@@ -331,6 +315,23 @@ class StepEngine:
                           tr.features, tr.feature_dim, tr._dtype_code, h, cache.gctr, sp)
 
         self._mark("loaded", stream)
+        # injected (cache-hit) rows of every layer output depend only on the
+        # prune walk: written on a side stream while the layers compute, issued
+        # after the feature gather so that the gather runs without HBM contention
+        # (SAGE / GCN; the main stream joins before the next layer reads them)
+        h_outs = [None] * L
+        inj_stream = None
+        if net.kind is not LayerKind.GAT and any(x is not None for x in injected):
+            # outputs allocated on the main stream (it owns and frees them; the
+            # side stream is joined before any main-stream use after it)
+            h_outs = [torch.empty((blocks[b].num_dst, net.dims[b + 1]), dtype=torch.float32, device=dev)
+                      for b in range(L)]
+            inj_stream = self.inj_stream
+            inj_stream.wait_stream(stream)              # after the lookups and the feature gather
+            isp = _lib.stream_ptr(inj_stream)
+            for b in range(L):
+                if injected[b] is not None:
+                    inject_rows_dev(injected[b], h_outs[b], blocks[b].num_dst, blocks[b].n_dst_dev, isp)
         # ---- forward (nn.py:260-297) ----
         tapes = []
         for b in range(L):
