@@ -202,6 +202,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--allreduce", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 gradient exchange: fused peer-memory kernel (default) or NCCL all_reduce")
     ap.add_argument("--replicate-features", action="store_true",
                     help="N>1: full feature table on every GPU instead of owner-range shards over NVLink")
     args = ap.parse_args()
@@ -290,8 +292,26 @@ def main():
                                         else None))
     tr = hg.Trainer(graph, feats_dev, labels, train, tcfg, cfgd["classes"])
     if world > 1:
-        from paper_2301_07482_b200.distributed import make_allreduce_hook
-        tr.grad_hook = make_allreduce_hook(world)   # NCCL: captured in the step's CUDA graph
+        from paper_2301_07482_b200.distributed import P2PAllReduce, make_allreduce_hook
+        hook, err = None, ""
+        if args.allreduce == "p2p":
+            # gradient exchange fused with SGD over CUDA-IPC slots (NVLink loads)
+            try:
+                hook = P2PAllReduce(tr.network.flat.numel(), rank, world, dev)
+            except Exception as e:
+                err = f"{type(e).__name__}: {e}"
+            ok = torch.tensor([0 if hook is None else 1], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0:
+                if hook is not None:
+                    hook.close()
+                hook = None
+                config["allreduce_note"] = f"P2P exchange unavailable ({err or 'on a peer rank'}); NCCL"
+        if hook is None:
+            hook = make_allreduce_hook(world)   # NCCL: captured in the step's CUDA graph
+        tr.grad_hook = hook
+        config["allreduce"] = ("fused P2P all-reduce + SGD (hg_p2p_allreduce_sgd)"
+                               if getattr(hook, "fused_sgd", False) else f"{dist.get_backend()} all_reduce + hg_sgd")
     batches = hg.make_batches(train, tcfg)
     mem_setup = torch.cuda.memory_allocated(dev)
     if need > len(batches):

@@ -210,6 +210,16 @@ int hg_row_norms(const float* x, long long n, int d, double* out, cudaStream_t s
 
 /* ---- K11 optimizer: nn.py:355-360 (sgd_step) */
 int hg_sgd(float* params, const float* grads, long long n, float eta, cudaStream_t stream);
+/* Data-parallel gradient average fused with SGD over NVLink peer memory, the
+ * alternative to an NCCL all-reduce hook before hg_sgd (histgnn/trainer.py:423-433,
+ * nn.py:355-360 with gradients averaged over P ranks). my_slots: this rank's
+ * 2 x n float exchange area, my_flag: its u64 flag word (both CUDA-IPC
+ * exported); slots[r] / flags[r]: device arrays with every rank's mapping;
+ * state: 4 zero-initialised u64 words. Two launches, no host sync; sums in
+ * rank order so every rank applies identical bits. */
+int hg_p2p_allreduce_sgd(float* params, const float* grads, long long n, float* my_slots,
+                         unsigned long long* my_flag, const float* const* slots, unsigned long long* const* flags,
+                         int P, unsigned long long* state, float eta, cudaStream_t stream);
 
 /* ---- K10 cache update: histgnn/cache.py:188-204 (_LayerCache.update) via
  * cache.py:289-322 (HistCache.update_cache), with _write/_release/

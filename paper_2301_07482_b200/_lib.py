@@ -65,6 +65,7 @@ SIGNATURES = {
     "hg_transpose_agg": (I32, [I32, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P]),
     "hg_row_norms": (I32, [P, I64, I32, P, P]),
     "hg_sgd": (I32, [P, P, I64, F32, P]),
+    "hg_p2p_allreduce_sgd": (I32, [P, P, I64, P, P, P, P, I32, P, F32, P]),
     "hg_cache_update_scratch_bytes": (I64, [I64]),
     "hg_cache_rank": (I32, [P, I32, F64, P, P, P, P, P, P, P, P, I64, P]),
     "hg_cache_write": (I32, [I32, I32, I32, P, F64, I32, P, P, P, P, P, P, P, P, I64, P]),

@@ -41,15 +41,6 @@ __global__ void k_prune_rows(const int32_t* n_dst_dev, const uint8_t* __restrict
   }
 }
 
-struct EmitCompactPos {
-  int32_t* out_idx;
-  int32_t* pos_of;  // optional: position of i in the compacted list, -1 if absent
-  __device__ void operator()(long long i, int excl, int v) const {
-    if (v) out_idx[excl] = (int32_t)i;
-    if (pos_of) pos_of[i] = v ? excl : -1;
-  }
-};
-
 // both compactions of a block in one scan: (keep[i] for i < n_dst, src_mask[i])
 struct KeepSrcFlags {
   const uint8_t* keep;

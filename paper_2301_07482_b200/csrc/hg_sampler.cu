@@ -312,7 +312,6 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select(
     dC[d] = c;
   }
   __syncthreads();
-  const int F = *F_dev;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const unsigned long long base0 = ss->stream_pos;

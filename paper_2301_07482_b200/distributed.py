@@ -51,3 +51,103 @@ def make_allreduce_hook(world: int, group=None):
     # cannot, so a gloo hook keeps the step eager
     hook.graph_safe = dist.get_backend(group) == "nccl"
     return hook
+
+
+class P2PAllReduce:
+    """Fused data-parallel exchange + SGD over peer memory (hg_p2p_allreduce_sgd).
+
+    Replaces `make_allreduce_hook` + `sgd_step`: every rank copies its flat
+    gradient bucket into its own CUDA-IPC exchange slot and raises a flag; each
+    rank then reads all P slots (NVLink loads on a multi-GPU box), sums them in
+    rank order, divides by P and applies SGD to its parameters in the same
+    kernel, so every rank holds identical weights without an NCCL launch. Two
+    kernel launches, capturable in the step's CUDA graph. A collective
+    constructor (every rank of `group` calls it with the same bucket size)."""
+
+    fused_sgd = True
+    graph_safe = True
+
+    def __init__(self, numel: int, rank: int, world: int, device, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        from .sharding import _DevBuf
+        _lib.require_cuda()
+        self.n, self.rank, self.world = int(numel), int(rank), int(world)
+        self.device = torch.device(device)
+        slot_bytes = 2 * self.n * 4
+        flag_off = (slot_bytes + 255) // 256 * 256
+        p = ctypes.c_void_p()
+        _lib.call("hg_device_alloc", flag_off + 256, ctypes.byref(p))
+        self._owned = p.value
+        torch.as_tensor(_DevBuf(p.value, (flag_off + 256,), "|u1"), device=self.device).zero_()
+        torch.cuda.synchronize(self.device)
+        lib = _lib.load()
+        hb = int(lib.hg_ipc_handle_bytes())
+        h = ctypes.create_string_buffer(hb)
+        _lib.call("hg_ipc_export", p, h)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(h.raw), group=group)
+        bases, self._opened = [], []
+        for r in range(self.world):
+            if r == self.rank:
+                bases.append(p.value)
+                continue
+            q = ctypes.c_void_p()
+            _lib.call("hg_ipc_open", ctypes.create_string_buffer(handles[r], hb), ctypes.byref(q))
+            bases.append(q.value)
+            self._opened.append(q.value)
+        self.my_slots, self.my_flag = p.value, p.value + flag_off
+        self.slots_dev = torch.tensor(bases, dtype=torch.int64, device=self.device)
+        self.flags_dev = torch.tensor([b + flag_off for b in bases], dtype=torch.int64, device=self.device)
+        self.state = torch.zeros(4, dtype=torch.int64, device=self.device)
+        dist.barrier(group=group)
+
+    def __call__(self, grads):
+        raise TypeError("P2PAllReduce fuses the exchange with SGD: call .sgd(network, grads, eta)")
+
+    def sgd(self, network, grads, eta: float) -> None:
+        from . import _lib
+        if grads.flat.numel() != self.n:
+            raise ValueError(f"bucket of {grads.flat.numel()} floats, exchange sized for {self.n}")
+        _lib.call("hg_p2p_allreduce_sgd", _lib.ptr(network.flat), _lib.ptr(grads.flat), self.n, self.my_slots,
+                  self.my_flag, _lib.ptr(self.slots_dev), _lib.ptr(self.flags_dev), self.world, _lib.ptr(self.state),
+                  float(np.float32(eta)), _lib.stream_ptr())
+
+    @property
+    def timed_out(self) -> bool:
+        return bool(int(self.state[3].item()))
+
+    def close(self, group=None) -> None:
+        """Unmap peers and free the exchange area (collective: barriers
+        first so no peer still reads it)."""
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=group)
+        for q in self._opened:
+            _lib.call("hg_ipc_close", ctypes.c_void_p(q))
+        self._opened = []
+        dist.barrier(group=group)
+        if self._owned is not None:
+            _lib.call("hg_device_free", ctypes.c_void_p(self._owned))
+            self._owned = None
+
+
+def apply_sgd(hook, network, grads, eta: float) -> None:
+    """The optimizer step of a (possibly data-parallel) iteration: a fused
+    exchange hook does both; a plain hook all-reduces, then hg_sgd."""
+    from .nn import sgd_step
+    if hook is not None and getattr(hook, "fused_sgd", False):
+        hook.sgd(network, grads, eta)
+        return
+    if hook is not None:
+        hook(grads)
+    sgd_step(network, grads, eta)

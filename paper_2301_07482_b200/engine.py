@@ -35,9 +35,10 @@ import numpy as np
 import torch
 
 from . import _lib
+from .distributed import apply_sgd
 from .nn import (Injection, LayerKind, build_csc, cross_entropy_dev, inject_rows_dev, layer_backward_dev,
                  layer_forward_dev,
-                 load_features_dev, pack_dgrad_weights, pack_forward_weights, sgd_step, ts_bytes)
+                 load_features_dev, pack_dgrad_weights, pack_forward_weights, ts_bytes)
 from .sampler import SamplerWorkspace, SampleSlot, layer_bounds, pcg_words, sample_blocks_dev
 
 
@@ -381,9 +382,7 @@ class StepEngine:
         if packed is not None:
             stream.wait_stream(self.inj_stream)      # only when work was enqueued there (graph capture)
         stream.wait_stream(self.wgrad_stream)
-        if tr.grad_hook is not None:
-            tr.grad_hook(grads)
-        sgd_step(net, grads, cfg.eta)
+        apply_sgd(tr.grad_hook, net, grads, cfg.eta)   # all-reduce (NCCL or fused P2P) + SGD
         self._mark("sgd", stream)
         for side in self.upd_streams.values():
             stream.wait_stream(side)

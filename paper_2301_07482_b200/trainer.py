@@ -25,6 +25,7 @@ import torch
 
 from . import _lib
 from ._state import GCTR_FEATURE_HITS, GCTR_FEATURE_MISSES, GCTR_PRUNE_WRITES, LAYER_CTR_LEN, CTR_VALID
+from .distributed import apply_sgd
 from .engine import StepEngine
 from .cache import COUNTER_NAMES, CachePolicy, HistCache
 from .graphs import Csr2Graph, _np, csr2_from_arrays
@@ -578,9 +579,7 @@ class Trainer:
                                              pruned.n_dst_dev(l), pruned.n_live_dev(l))
             norms[l] = nrm
             d_h = d_prev
-        if self.grad_hook is not None:
-            self.grad_hook(grads)          # e.g. NCCL all-reduce of the flat bucket
-        sgd_step(net, grads, cfg.eta)
+        apply_sgd(self.grad_hook, net, grads, cfg.eta)   # e.g. NCCL all-reduce of the flat bucket, then SGD
         it_dev = torch.tensor([int(iteration)], dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
         for layer in range(1, L):
             n_live = pruned.counts[layer][1]

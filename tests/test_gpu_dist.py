@@ -105,3 +105,56 @@ def test_nccl_allreduce_is_captured_in_the_step_graph(tmp_path):
     np.testing.assert_array_equal(losses[0], losses[1])
     w = np.load(tmp_path / "w.npy")
     np.testing.assert_array_equal(w[0], w[1])
+
+
+def _p2p_worker(rank, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    torch.cuda.set_device(0)
+    import paper_2301_07482_b200 as hg
+    from paper_2301_07482_b200.distributed import P2PAllReduce, make_allreduce_hook, rank_batch_indices
+    ds, g = _data()
+    cfg = hg.TrainConfig(fanouts=(6, 4, 3), hidden=16, batch_size=96, epochs=1, eta=0.05,
+                         kind=hg.LayerKind.SAGE_MEAN, p_grad=0.9, t_stale=3, seed=5)
+    out = {}
+    for mode in ("gloo", "p2p"):
+        tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
+        ex = None
+        if mode == "gloo":
+            tr.grad_hook = make_allreduce_hook(WORLD)
+        else:
+            ex = P2PAllReduce(tr.network.flat.numel(), rank, WORLD, "cuda:0")
+            tr.grad_hook = ex
+        batches = hg.make_batches(ds.train_ids, cfg)
+        idx = rank_batch_indices(len(batches), rank, WORLD)[:6]
+        losses = []
+        for k, i in enumerate(idx):
+            nb = (idx[k + 1], batches[idx[k + 1]]) if k + 1 < len(idx) else None
+            losses.append(tr.train_step(i, 0, batches[i], next_batch=nb).loss)
+        torch.cuda.synchronize()
+        caps = sum(e.captures for e in tr._engines.values())
+        out[mode] = (np.array(losses), caps, np.frombuffer(tr.network.checksum_bytes(), np.uint8).copy())
+        if ex is not None:
+            assert not ex.timed_out
+            ex.close()
+    np.save(os.path.join(out_dir, f"p{rank}_losses.npy"), np.stack([out["gloo"][0], out["p2p"][0]]))
+    np.save(os.path.join(out_dir, f"p{rank}_caps.npy"), np.array([out["gloo"][1], out["p2p"][1]]))
+    np.save(os.path.join(out_dir, f"p{rank}_w.npy"), np.stack([out["gloo"][2], out["p2p"][2]]))
+    dist.destroy_process_group()
+
+
+def test_p2p_fused_allreduce_sgd_matches_gloo(tmp_path):
+    """Two processes on one GPU exchange gradients through CUDA-IPC slots with
+    hg_p2p_allreduce_sgd (captured in the step graph, no host collective per
+    step): both ranks end bitwise equal, and equal to the gloo all-reduce +
+    hg_sgd path ((g0 + g1) / 2 is the same float either way for P = 2)."""
+    mp.start_processes(_p2p_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True,
+                       start_method="spawn")
+    w = [np.load(tmp_path / f"p{r}_w.npy") for r in range(WORLD)]
+    np.testing.assert_array_equal(w[0][1], w[1][1])
+    np.testing.assert_array_equal(w[0][0], w[0][1])
+    for r in range(WORLD):
+        caps = np.load(tmp_path / f"p{r}_caps.npy")
+        assert caps[1] >= 1, "the P2P step was never captured in a CUDA graph"
+        losses = np.load(tmp_path / f"p{r}_losses.npy")
+        np.testing.assert_array_equal(losses[0], losses[1])
