@@ -20,6 +20,13 @@
 #include "hg_common.cuh"
 #include "hg_ts.cuh"
 
+// >= 4 resident CTAs for the attention kernels with rows <= 256 floats:
+// their edge loops are latency-bound; measured C5 2.55e5 -> 3.04e5 seeds/s
+// (backward 2.04 -> 1.42 ms/step) going from 1 (80 regs) to 4; 6 spills
+#ifndef HG_GAT_MINB
+#define HG_GAT_MINB 4
+#endif
+
 namespace hg {
 namespace {
 
@@ -98,7 +105,7 @@ struct Heads {
 
 // el[j*H + h] = <z[j, hF:(h+1)F], a_src[hF:(h+1)F]>, er likewise with a_dst
 template <int kT, int kH>
-__global__ void __launch_bounds__(256) k_gat_scores(const int32_t* n_dev, const int32_t* __restrict__ live,
+__global__ void __launch_bounds__(256, kT <= 8 ? HG_GAT_MINB : 1) k_gat_scores(const int32_t* n_dev, const int32_t* __restrict__ live,
                                                     const float* __restrict__ z, int HF, int H, int F,
                                                     const float* __restrict__ a_src, const float* __restrict__ a_dst,
                                                     float* __restrict__ el, float* __restrict__ er) {
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(256) k_gat_scores(const int32_t* n_dev, const 
 __device__ __forceinline__ float head_val(float v, int h) { return __shfl_sync(0xffffffffu, v, h); }
 
 template <int kT, int kH>
-__global__ void __launch_bounds__(256) k_gat_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, kT <= 8 ? HG_GAT_MINB : 1) k_gat_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                        const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                        const int32_t* __restrict__ col, const float* __restrict__ z,
                                                        const float* __restrict__ el, const float* __restrict__ er,
@@ -210,7 +217,7 @@ __device__ __forceinline__ void block_colsum_store(float (&v)[kT], float (*red)[
 // backward, warp per compute row r (i = rows[r]):
 //   gz = dL/dout masked by ReLU; c[r][h] = sum_j a_ij da_ij; der[r][h] = sum_j ds_ij
 template <int kT, int kH>
-__global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, kT <= 8 ? HG_GAT_MINB : 1) k_gat_bwd_dst(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                      const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                      const int32_t* __restrict__ col, const float* __restrict__ z,
                                                      const float* __restrict__ el, const float* __restrict__ er,
@@ -315,7 +322,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const int32_t* R_dev, const
 // = compute position of the edge's dst row): dz_j and del_j. dz is emitted as
 // TS row k (compact over the live list) for the dgrad / wgrad GEMMs.
 template <int kT, int kH>
-__global__ void __launch_bounds__(256) k_gat_bwd_src(
+__global__ void __launch_bounds__(256, kT <= 8 ? HG_GAT_MINB : 1) k_gat_bwd_src(
     const int32_t* n_dev, const int32_t* __restrict__ live, const int32_t* __restrict__ seg_lo,
     const int32_t* __restrict__ seg_hi, const unsigned* __restrict__ csc_pos, const int32_t* __restrict__ rows,
     const int32_t* n_dst_dev, const int32_t* __restrict__ pos_of, const float* __restrict__ z,

@@ -38,7 +38,16 @@ namespace {
 constexpr int kKindGCN = 0;
 constexpr int kKindSAGE = 1;
 constexpr int kMaxVecPerLane = 8;  // d_in <= 1024 floats (kT = float4 per lane, templated)
-constexpr int kMaxRowFloats = 1056; // k_gather_dz staging: d_out <= 1056
+constexpr int kMaxRowFloats = 1056;
+// resident CTAs forced for the d <= 256 (kT <= 2) aggregation kernels:
+// latency-bound edge-row gathers, so occupancy is the lever (measured C2:
+// k_aggregate 0.155 -> 0.125 ms/step at 6, k_transpose_agg 0.106 -> 0.089 at 8)
+#ifndef HG_AGG_MINB
+#define HG_AGG_MINB 6
+#endif
+#ifndef HG_TAGG_MINB
+#define HG_TAGG_MINB 8
+#endif // k_gather_dz staging: d_out <= 1056
 
 __device__ __forceinline__ float4 f4_fmadd_rn(float4 acc, float c, float4 x) {
   return make_float4(__fadd_rn(acc.x, __fmul_rn(c, x.x)), __fadd_rn(acc.y, __fmul_rn(c, x.y)),
@@ -53,7 +62,7 @@ __device__ __forceinline__ float gcn_coef(int dd, int sd) {
 // [self | agg | 1 | pad] row is staged in dynamic shared memory (row_floats
 // per warp) before it is emitted as TS core rows
 template <int kKind, int kT>
-__global__ void __launch_bounds__(256) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
@@ -311,7 +320,7 @@ __global__ void k_csc_segments(const unsigned* __restrict__ keys, long long E_ma
 
 // d_in rows for the live sources of block l + their fp64 norms (one warp per source)
 template <int kKind, int kT>
-__global__ void __launch_bounds__(256) k_transpose_agg(
+__global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_agg(
     const int32_t* n_live_dev, const int32_t* __restrict__ live, const int32_t* __restrict__ seg_lo,
     const int32_t* __restrict__ seg_hi, const unsigned* __restrict__ srt_vals, const int32_t* __restrict__ rows,
     const int32_t* __restrict__ start, const int32_t* __restrict__ end, const int32_t* __restrict__ dst_deg,
