@@ -369,7 +369,10 @@ def main():
     barrier()
     clk = clocks.stop()
     t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
-    value = BATCH * world * args.steps / t_dev
+    # seeds actually trained (an epoch's last batch can be short); the same
+    # on every rank pattern-wise, so scale rank 0's by the world size
+    seeds_value = world * sum(len(batches[mine[s]]) for s in range(args.warmup, args.warmup + args.steps))
+    value = seeds_value / t_dev
     graph_mode = any(e.graph is not None for e in tr._engines.values())
     caps_value = sum(e.captures for e in tr._engines.values()) - caps0
 
@@ -426,7 +429,8 @@ def main():
     t_e2e = max_over_ranks(time.perf_counter() - t0)
     m = m.result()
     caps_e2e = sum(e.captures for e in tr._engines.values()) - caps0 - caps_value
-    e2e = {"value": BATCH * world * args.steps / t_e2e, "unit": "seeds/s",
+    seeds_e2e = world * sum(len(batches[mine[s]]) for s in range(args.warmup + args.steps, args.warmup + 2 * args.steps))
+    e2e = {"value": seeds_e2e / t_e2e, "unit": "seeds/s",
            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
            "api": "Trainer.train_step (host seeds in via pinned staging, IterMetrics counters copied to pinned "
                   "host memory every step, sync=False: the host enqueues step s+1 while step s runs)"}
@@ -469,6 +473,14 @@ def main():
                      "peak": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2)}
     if cfgd.get("capacity"):
         config["cache_capacity_rows_per_layer"] = [cfgd["capacity"], cfgd["max_capacity"]]
+    feat_bytes = cfgd["n"] * cfgd["d"] * tr.features.element_size()
+    if feat_bytes < 2 * 126e6:
+        # small graphs (C1) stay L2-resident across steps; no flush is done,
+        # so this is a parity-size configuration, not a bench line
+        config["l2"] = (f"inputs fit in L2 ({feat_bytes / 1e6:.0f} MB features), not flushed: "
+                        "parity-size config, not a bench line")
+    elif not cfgd.get("fp16"):
+        config["l2"] = f"inputs > L2 ({feat_bytes / 1e9:.1f} GB features resident, random rows)"
     if cfgd.get("fp16"):
         out["dtype"] = "fp32 (fp16 feature table, converted in the gather)"
         config["l2"] = f"inputs > L2 ({cfgd['n'] * cfgd['d'] * 2 / 1e9:.0f} GB features resident, random rows)"
