@@ -488,17 +488,21 @@ inline uint32_t tmem_cols_for(int n) {
   return c;
 }
 
-// HG_GEMM_PERSISTENT=1 selects the persistent warp-specialised kernel for
-// fwd / dgrad. Measured in-situ on C2 (kernel timers, 300 steps): forward
-// 36.3 vs 34.1 us per launch, dgrad 24.0 vs 23.4 us — the one-tile kernel
-// stays the default (profiles/r01/notes).
-inline bool use_persistent_gemm() {
-  static int v = -1;
-  if (v < 0) {
+// fwd / dgrad kernel choice by the row bound M: the persistent
+// warp-specialised kernel (epilogue of tile i overlapping the MMAs of tile
+// i+1) for tall GEMMs, the one-tile kernel otherwise. Measured in-situ
+// (kernel timers): C2/C3 SAGE (M <= ~200K rows) one-tile 34 vs 36 us per
+// forward launch, C3 forward total 0.152 vs 0.178 ms/step; C5 GAT layer 0
+// (z over ~530K live sources) 0.63 -> 0.50 ms/step of forward GEMMs, +5 %
+// end to end. HG_GEMM_PERSISTENT=0/1 forces one or the other.
+constexpr long long kPersistentMinRows = 256 * 1024;
+inline bool use_persistent_gemm(long long M) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = std::getenv("HG_GEMM_PERSISTENT");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && e[0] == '1') ? 1 : (e && e[0] == '0') ? 0 : -1;
   }
-  return v == 1;
+  return v == 1 || (v == -1 && M >= kPersistentMinRows);
 }
 
 template <typename Epi>
@@ -529,7 +533,7 @@ int launch_persistent(const char* W, const CUtensorMap& a, const CUtensorMap& b,
 template <bool kMN, typename Epi>
 int launch(const char* W, const CUtensorMap& a, const CUtensorMap& b, Shape sh, Epi e, int n_tile, int splits,
            cudaStream_t stream) {
-  if (!kMN && splits == 1 && use_persistent_gemm()) return launch_persistent(W, a, b, sh, e, n_tile, stream);
+  if (!kMN && splits == 1 && use_persistent_gemm(sh.M)) return launch_persistent(W, a, b, sh, e, n_tile, stream);
   const int n_tiles = (sh.N + n_tile - 1) / n_tile;
   const size_t smem = (size_t)kStages * (2 * 8192 + 2 * (size_t)n_tile * 64);
   static int attr_dev = -1;

@@ -100,7 +100,9 @@ def _ts_T(lib, P):
 
 
 @pytest.mark.parametrize("R,R_max,K1,N,relu", [(1000, 1000, 201, 256, 1), (777, 1024, 513, 256, 1),
-                                               (130, 200, 513, 47, 0), (1, 128, 33, 8, 0), (4096, 5000, 257, 172, 1)])
+                                               (130, 200, 513, 47, 0), (1, 128, 33, 8, 0), (4096, 5000, 257, 172, 1),
+                                               # row bounds >= 256K select the persistent kernel
+                                               (300000, 330000, 129, 256, 1), (1000, 300000, 201, 256, 0)])
 def test_ts_forward_scatter(R, R_max, K1, N, relu):
     lib = _lib()
     g = torch.Generator(device="cuda").manual_seed(R + K1)
@@ -123,7 +125,7 @@ def test_ts_forward_scatter(R, R_max, K1, N, relu):
 
 
 @pytest.mark.parametrize("R,R_max,N,K", [(1000, 1000, 256, 512), (333, 600, 47, 256), (5, 128, 8, 64),
-                                         (3000, 3000, 256, 200)])
+                                         (3000, 3000, 256, 200), (280000, 300000, 256, 128)])
 def test_ts_dgrad(R, R_max, N, K):
     lib = _lib()
     g = torch.Generator(device="cuda").manual_seed(R + N)
