@@ -37,6 +37,11 @@ long long hg_kernel_launches(void);
 int hg_mark_time(unsigned long long* slot, cudaStream_t stream);
 /* add the n hg kernels of a replayed CUDA graph (counted at its capture) */
 void hg_count_graph_replay(long long n);
+/* instantiate a captured cudaGraph_t with per-node priorities
+ * (cudaGraphInstantiateFlagUseNodePriority), launch it, destroy it */
+int hg_graph_instantiate(void* graph, void** exec_out);
+int hg_graph_launch(void* exec, cudaStream_t stream);
+int hg_graph_exec_destroy(void* exec);
 /* device-side kernel timers for kernels replayed inside CUDA graphs: buf is
  * u64[8 * 8] (per timer: start=~0, end, total_ns, launches, ...), NULL = off.
  * Timer 0 = k_load_rows, 1 = k_aggregate, 2 = k_transpose_agg, 3 = k_select. */

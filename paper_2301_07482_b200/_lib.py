@@ -31,6 +31,9 @@ SIGNATURES = {
     "hg_device_sync": (I32, []),
     "hg_kernel_launches": (I64, []),
     "hg_count_graph_replay": (None, [I64]),
+    "hg_graph_instantiate": (I32, [P, P]),
+    "hg_graph_launch": (I32, [P, P]),
+    "hg_graph_exec_destroy": (I32, [P]),
     "hg_mark_time": (I32, [P, P]),
     "hg_set_kernel_timers": (I32, [P]),
     "hg_sample_layer_scratch_bytes": (I64, [I64, I64]),

@@ -35,6 +35,15 @@ bool pdl_enabled() {
   return v == 1;
 }
 
+bool node_prio_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("HG_NODE_PRIO");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int check_launch(const char* where) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
@@ -68,6 +77,29 @@ int hg_mark_time(unsigned long long* slot, cudaStream_t stream) {
 
 // a CUDA graph replay re-executes the n hg kernels recorded at its capture
 void hg_count_graph_replay(long long n) { hg::g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// executable graph honouring per-node priorities (HG_NODE_PRIO=1 path of
+// engine.StepEngine: the cache-update and training streams outrank the
+// lookahead sampler inside one replay)
+int hg_graph_instantiate(void* graph, void** exec_out) {
+  if (!graph || !exec_out) return hg::fail("hg_graph_instantiate", hg::kBadArg, "null graph");
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t e = cudaGraphInstantiateWithFlags(&ex, static_cast<cudaGraph_t>(graph),
+                                                cudaGraphInstantiateFlagUseNodePriority);
+  if (e != cudaSuccess) return hg::fail("hg_graph_instantiate", hg::kCuda, cudaGetErrorString(e));
+  *exec_out = ex;
+  return hg::kOk;
+}
+
+int hg_graph_launch(void* exec, cudaStream_t stream) {
+  cudaError_t e = cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), stream);
+  return e == cudaSuccess ? hg::kOk : hg::fail("hg_graph_launch", hg::kCuda, cudaGetErrorString(e));
+}
+
+int hg_graph_exec_destroy(void* exec) {
+  cudaError_t e = cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec));
+  return e == cudaSuccess ? hg::kOk : hg::fail("hg_graph_exec_destroy", hg::kCuda, cudaGetErrorString(e));
+}
 
 const char* hg_last_error(void) { return hg::g_last_error.c_str(); }
 

@@ -128,6 +128,7 @@ __device__ __forceinline__ void kt_end(KTimer* kt) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 bool pdl_enabled();   // HG_PDL=0 disables (A/B)
+bool node_prio_enabled();   // HG_NODE_PRIO=1: kernel nodes carry their stream's priority
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
@@ -141,11 +142,21 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (node_prio_enabled()) {
+    // recorded on the kernel node at capture; honoured by graphs instantiated
+    // with cudaGraphInstantiateFlagUseNodePriority (hg_graph_instantiate)
+    int prio = 0;
+    if (cudaStreamGetPriority(stream, &prio) == cudaSuccess) {
+      attr[1].id = cudaLaunchAttributePriority;
+      attr[1].val.priority = prio;
+      cfg.numAttrs = 2;
+    }
+  }
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 

@@ -27,7 +27,9 @@ batch than announced) falls back to sampling it first.
 
 from __future__ import annotations
 
+import ctypes
 import gc
+import os
 import weakref
 from dataclasses import dataclass
 
@@ -71,8 +73,13 @@ class DevBlock:
         return self.col
 
 
+# HG_NODE_PRIO=1: streams get priorities (cache updates > training > lookahead
+# sampler) and the captured step is instantiated with per-node priorities
+_NODE_PRIO = os.environ.get("HG_NODE_PRIO") == "1"
+
+
 class _Graph:
-    __slots__ = ("graph", "pool", "out", "key", "launches")
+    __slots__ = ("graph", "pool", "out", "key", "launches", "exec", "__weakref__")
 
 
 class StepEngine:
@@ -97,16 +104,18 @@ class StepEngine:
         self.cur = 0                     # slot of the next batch to train
         # block 0's sources carry no in-edges (src_deg = 0): one persistent zero vector
         self.zero_deg = torch.zeros(self.slots[0].layers[-1]["Fn_max"], dtype=torch.int32, device=self.dev)
-        self.samp_stream = torch.cuda.Stream(self.dev)
+        pr = (lambda p: dict(priority=p)) if _NODE_PRIO else (lambda p: {})
+        self._prio = pr
+        self.samp_stream = torch.cuda.Stream(self.dev, **pr(0))
         # backward inputs that depend only on the pruned blocks / the weights
         # (transposed CSC, TS-packed dgrad weights) are built on prep_stream
         # during the forward; weight-gradient GEMMs run on wgrad_stream
-        self.prep_stream = torch.cuda.Stream(self.dev)
-        self.wgrad_stream = torch.cuda.Stream(self.dev)
-        self.inj_stream = torch.cuda.Stream(self.dev)      # cache-hit row injection (forward)
+        self.prep_stream = torch.cuda.Stream(self.dev, **pr(-1))
+        self.wgrad_stream = torch.cuda.Stream(self.dev, **pr(-1))
+        self.inj_stream = torch.cuda.Stream(self.dev, **pr(-1))      # cache-hit row injection (forward)
         # cache updates of layer l run on side stream l, overlapping the
         # backward of layers < l (they only read the forward tape and norms[l])
-        self.upd_streams = {l: torch.cuda.Stream(self.dev) for l in range(1, self.L)}
+        self.upd_streams = {l: torch.cuda.Stream(self.dev, **pr(-2)) for l in range(1, self.L)}
         self.graphs = {}          # (slot, lookahead) -> _Graph
         self.out = None
         self.capturing = False
@@ -177,7 +186,10 @@ class StepEngine:
             g = self.graphs.get(gk)
             if g is None or g.key != self._key():
                 g = self._capture(s, ahead)
-            g.graph.replay()
+            if g.exec is not None:
+                _lib.call("hg_graph_launch", g.exec, _lib.stream_ptr())
+            else:
+                g.graph.replay()
             _lib.load().hg_count_graph_replay(g.launches)
             self.out = g.out
             return self.out
@@ -411,14 +423,15 @@ class StepEngine:
         # pool) is released when it is dropped here
         self.graphs.pop((s, ahead), None)
         g = _Graph()
-        g.graph = torch.cuda.CUDAGraph()
+        g.exec = None
+        g.graph = torch.cuda.CUDAGraph(keep_graph=True) if _NODE_PRIO else torch.cuda.CUDAGraph()
         g.pool = torch.cuda.graph_pool_handle()
         self.capturing = True
         n0 = _lib.load().hg_kernel_launches()
         try:
             # capture on a side stream; the staged inputs were copied on the
             # current stream, which the capture stream waits for
-            side = torch.cuda.Stream(self.dev)
+            side = torch.cuda.Stream(self.dev, **self._prio(-1))
             side.wait_stream(torch.cuda.current_stream(self.dev))
             with torch.cuda.stream(side):
                 with torch.cuda.graph(g.graph, pool=g.pool, stream=side):
@@ -426,6 +439,11 @@ class StepEngine:
             torch.cuda.current_stream(self.dev).wait_stream(side)
         finally:
             self.capturing = False
+        if _NODE_PRIO:
+            ex = ctypes.c_void_p()
+            _lib.call("hg_graph_instantiate", ctypes.c_void_p(g.graph.raw_cuda_graph()), ctypes.byref(ex))
+            g.exec = ex.value
+            weakref.finalize(g, _lib.call, "hg_graph_exec_destroy", ctypes.c_void_p(ex.value))
         # capture records the launches without executing them
         g.launches = _lib.load().hg_kernel_launches() - n0
         _lib.load().hg_count_graph_replay(-g.launches)
