@@ -11,4 +11,4 @@ for c in c3 c5 c4s; do
   timeout 900 python bench.py --config $c --no-cpu-baseline > $O/bench_$c.log 2>&1; tail -1 $O/bench_$c.log > $O/bench_$c.json
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.log 2>&1; tail -1 $O/bench_ref.log > $O/bench_ref.json
-bash tools/profile.sh c2 k_load_rows k_aggregate
+[ "${SKIP_PROFILE:-0}" = 1 ] || bash tools/profile.sh c2 k_load_rows k_aggregate
