@@ -121,19 +121,22 @@ __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0
 }
 
 // ---------------------------------------------------------------- epilogues
-// Epilogues store acc at key(i) + n. With kHoist the key is computed once per
-// tile row by the lane owning the row and broadcast with a shuffle (dgrad /
-// wgrad: -25 % / -13 % GEMM time at C2); the forward scatter reads rows[i]
-// per store instead (L1 broadcast hits; hoisting it was 0.51 -> 0.60 ms/step
-// of forward GEMMs at C5).
+// Epilogues store acc at expand(key(i)) + n. The key is computed once per
+// tile row by the lane that owns the row and shuffled to the storing lanes,
+// so the store loop carries no index loads. Key widths are what measured
+// best (C2/C5, kernel timers): the forward scatter shuffles the 32-bit
+// rows[i] (forward GEMMs 0.51 -> 0.45 ms/step at C5), dgrad / wgrad shuffle
+// the 64-bit row offset (-25 % / -13 % vs per-store arithmetic; a 32-bit
+// key there was slower than either).
 struct EpiScatterRelu {  // h_out[rows[i]][n] = act(acc)
   static constexpr bool kFwd = true;
-  static constexpr bool kHoist = false;
+  using Key = int;
   const int32_t* rows;
   float* out;
   int ldo;
   int relu;
-  __device__ __forceinline__ long long key(int i) const { return (long long)rows[i] * ldo; }
+  __device__ __forceinline__ Key key(int i) const { return rows[i]; }
+  __device__ __forceinline__ long long expand(Key k) const { return (long long)k * ldo; }
   __device__ __forceinline__ void store(long long k, int n, float x) const {
     if (relu) x = x > 0.f ? x : 0.f;
     out[k + n] = x;
@@ -141,19 +144,21 @@ struct EpiScatterRelu {  // h_out[rows[i]][n] = act(acc)
 };
 struct EpiStore {
   static constexpr bool kFwd = false;
-  static constexpr bool kHoist = true;
+  using Key = long long;
   float* out;
   long long ldo;
-  __device__ __forceinline__ long long key(int i) const { return (long long)i * ldo; }
+  __device__ __forceinline__ Key key(int i) const { return (long long)i * ldo; }
+  __device__ __forceinline__ long long expand(Key k) const { return k; }
   __device__ __forceinline__ void store(long long k, int n, float x) const { out[k + n] = x; }
 };
 struct EpiPartial {      // part[z][i][n] = acc
   static constexpr bool kFwd = false;
-  static constexpr bool kHoist = true;
+  using Key = long long;
   float* part;
   long long ldo;
   long long stride;
-  __device__ __forceinline__ long long key(int i) const { return (long long)blockIdx.z * stride + (long long)i * ldo; }
+  __device__ __forceinline__ Key key(int i) const { return (long long)blockIdx.z * stride + (long long)i * ldo; }
+  __device__ __forceinline__ long long expand(Key k) const { return k; }
   __device__ __forceinline__ void store(long long k, int n, float x) const { part[k + n] = x; }
 };
 
@@ -263,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tsgemm(const __grid_constant__ 
   tc_fence_after();
   __syncthreads();
   float* stage_f = reinterpret_cast<float*>(smem) + warp * 32 * 33;
-  const long long my_key = (Epi::kHoist && m0 + warp * 32 + lane < M) ? epi.key(m0 + warp * 32 + lane) : 0;
+  const typename Epi::Key my_key = (m0 + warp * 32 + lane < M) ? epi.key(m0 + warp * 32 + lane) : 0;
   for (int c0 = 0; c0 < n_valid; c0 += 32) {
     float acc[32];
     if (nc > 0) {
@@ -279,12 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tsgemm(const __grid_constant__ 
     const int col = c0 + lane;
     for (int r = 0; r < 32; ++r) {
       const int row = m0 + warp * 32 + r;
-      if constexpr (Epi::kHoist) {
-        const long long k = __shfl_sync(0xffffffffu, my_key, r);
-        if (row < M && col < n_valid) epi.store(k, n0 + col, stage_f[r * 33 + lane]);
-      } else {
-        if (row < M && col < n_valid) epi.store(epi.key(row), n0 + col, stage_f[r * 33 + lane]);
-      }
+      const long long k = epi.expand(__shfl_sync(0xffffffffu, my_key, r));
+      if (row < M && col < n_valid) epi.store(k, n0 + col, stage_f[r * 33 + lane]);
     }
     __syncwarp();
   }
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tsgemm_p(const __grid_constant
       const int buf = lt & 1;
       const int m0 = (t / n_tiles) * kTM, n0 = (t % n_tiles) * N_pad;
       const int n_valid = min(N_pad, sh.N - n0);
-      const long long my_key = (Epi::kHoist && m0 + q * 32 + lane < M) ? epi.key(m0 + q * 32 + lane) : 0;
+      const typename Epi::Key my_key = (m0 + q * 32 + lane < M) ? epi.key(m0 + q * 32 + lane) : 0;
       mbar_wait(&acc_full[buf], (lt >> 1) & 1);
       tc_fence_after();
       for (int c0 = 0; c0 < n_valid; c0 += 32) {
@@ -415,12 +416,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tsgemm_p(const __grid_constant
         const int col = c0 + lane;
         for (int r = 0; r < 32; ++r) {
           const int row = m0 + q * 32 + r;
-          if constexpr (Epi::kHoist) {
-            const long long k = __shfl_sync(0xffffffffu, my_key, r);
-            if (row < M && col < n_valid) epi.store(k, n0 + col, stage_f[r * 33 + lane]);
-          } else {
-            if (row < M && col < n_valid) epi.store(epi.key(row), n0 + col, stage_f[r * 33 + lane]);
-          }
+          const long long k = epi.expand(__shfl_sync(0xffffffffu, my_key, r));
+          if (row < M && col < n_valid) epi.store(k, n0 + col, stage_f[r * 33 + lane]);
         }
         __syncwarp();
       }
