@@ -656,7 +656,8 @@ int hg_ts_linear_dgrad(const int32_t* R_dev, long long R_max, const void* dz_ts,
   if (!st) st = make_map(W, &b, W_ts, K, N, 4, nt / 8);
   if (st) return st;
   Shape sh{(int)R_max, K, N, R_dev, nullptr, (N + kBK - 1) / kBK};
-  return launch<false>(W, a, b, sh, EpiStore{SG, K, false}   // scalar rows measured 0.034 vs 0.036 ms/step (C2), nt, 1, stream);
+  // dgrad keeps scalar row stores: measured 0.034 vs 0.036 ms/step (C2)
+  return launch<false>(W, a, b, sh, EpiStore{SG, K, false}, nt, 1, stream);
 }
 
 // dP[K1 x N] = A[:R, :K1]^T . dz[:R, :N]  (split-K over the rows, fixed-order sum)
