@@ -4,9 +4,9 @@ Names and semantics follow the reference: `LayerKind` (nn.py:28-30),
 `LayerParams`/`Network` (:33-70), `init_network` (:73-85, host RNG so weights
 are bit-identical), `forward_pass` (:260-297), `backward` (:300-320),
 `cross_entropy` (:326-343), `node_grad_norms` (:346-349), `sgd_step`
-(:355-360). The work is done by hg_aggregate_fwd / hg_gemm_rm /
-hg_scatter_rows / hg_inject_rows / hg_gather_dz / hg_build_csc /
-hg_transpose_agg / hg_cross_entropy / hg_sgd.
+(:355-360). The work is done by hg_aggregate_fwd / hg_ts_linear_{fwd,dgrad,
+wgrad} (tcgen05) / hg_inject_rows / hg_gather_dz / hg_build_csc /
+hg_transpose_agg / hg_gat_* / hg_cross_entropy / hg_sgd.
 
 Parameters of all layers live in ONE flat fp32 device buffer (one gradient
 bucket for the data-parallel all-reduce); layer l occupies a
