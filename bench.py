@@ -20,6 +20,7 @@ own cache replica; gradients are all-reduced (NCCL) before SGD; weak scaling.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -342,6 +343,12 @@ def main():
     for s in range(args.warmup):
         tr.train_step_resident(staged[s], nxt(s))
     torch.cuda.synchronize()
+    # setup objects (graph, tables, captured graphs) move to the permanent GC
+    # generation, so a cyclic-GC pass inside the timed steps scans only the
+    # per-step garbage (a full pass over the setup heap stalled the host for
+    # tens of ms in some e2e runs)
+    gc.collect()
+    gc.freeze()
 
     # ---- timed region 1: device-resident steps (value) ----
     clocks = ClockSampler(local)
