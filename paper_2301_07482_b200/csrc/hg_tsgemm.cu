@@ -542,14 +542,13 @@ inline uint32_t tmem_cols_for(int n) {
   return c;
 }
 
-// fwd / dgrad kernel choice by the row bound M: the persistent
-// warp-specialised kernel (epilogue of tile i overlapping the MMAs of tile
-// i+1) for tall GEMMs, the one-tile kernel otherwise. Measured in-situ
-// (kernel timers): C2/C3 SAGE (M <= ~200K rows) one-tile 34 vs 36 us per
-// forward launch, C3 forward total 0.152 vs 0.178 ms/step; C5 GAT layer 0
-// (z over ~530K live sources) 0.63 -> 0.50 ms/step of forward GEMMs, +5 %
-// end to end. HG_GEMM_PERSISTENT=0/1 forces one or the other.
-constexpr long long kPersistentMinRows = 256 * 1024;
+// fwd / dgrad use the persistent warp-specialised kernel (epilogue of tile i
+// overlapping the MMAs of tile i+1). Before the epilogue rework the one-tile
+// kernel was faster below ~256K rows (C3 forward 0.152 vs 0.178 ms/step);
+// with the vector epilogue the persistent kernel wins at every measured
+// shape: C2 1.080 -> 1.105e6, C3 0.99 -> 1.02e6 seeds/s, C5 layer 0
+// 0.63 -> 0.30 ms/step of forward GEMMs. HG_GEMM_PERSISTENT=0/1 forces.
+constexpr long long kPersistentMinRows = 0;
 inline bool use_persistent_gemm(long long M) {
   static int v = -2;
   if (v == -2) {
