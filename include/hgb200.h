@@ -119,22 +119,6 @@ int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int3
                      const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
                      const float* h_in, int d, void* A_ts, cudaStream_t stream);
 
-/* ---- K7 dense transform: nn.py:150,156,170-176 (the GEMMs). Row-major. */
-int hg_gemm_rm(int transA, int transB, long long M, long long N, long long K, const float* A, long long lda,
-               const float* B, long long ldb, float beta, float* C, long long ldc, cudaStream_t stream);
-
-/* ---- K7 on tcgen05 (3 x bf16 split, fp32 accumulate in TMEM; hg_tcgemm.cu) ----
- * forward: h_out[rows[i]] = relu?( A[i, :K1] . P )           nn.py:150,156,161-162,289
- * dgrad:   SG = dz . P[:K]^T                                   nn.py:171,175-176
- * wgrad:   dP = A[:, :K1]^T . dz  (split-K, fixed-order sum)   nn.py:170,173-174
- * R (rows) may live on the device (R_dev), R_max sizes the grid. */
-int hg_tc_linear_fwd(const int32_t* R_dev, long long R_max, const float* A, long long ldA, int K1, const float* P,
-                     int N, const int32_t* rows, int relu, float* h_out, cudaStream_t stream);
-int hg_tc_linear_dgrad(const int32_t* R_dev, long long R_max, const float* dz, int N, const float* P, int K,
-                       float* SG, cudaStream_t stream);
-int hg_tc_linear_wgrad(const int32_t* R_dev, long long R_max, const float* A, long long ldA, int K1, const float* dz,
-                       int N, float* dP, float* partial, int splits, cudaStream_t stream);
-
 /* ---- K7 on tcgen05 over TS operands (bf16 hi/lo core-matrix tiles in HBM, written by
  * hg_aggregate_fwd / hg_gather_dz / hg_ts_pack; layout in csrc/hg_ts.cuh). Each K-chunk
  * stage is one 4-D TMA box per operand (cp.async.bulk.tensor) into a 4-stage smem ring;
@@ -242,16 +226,25 @@ int hg_cache_write(int n_max, int cap, int H, const int32_t* it_dev, double t_st
                    int32_t* admit_iter, long long* layer_ctr, void* scratch, long long scratch_bytes,
                    cudaStream_t stream);
 
+/* ---- end-of-window sweep: histgnn/cache.py:206-211 (_LayerCache.sweep) on the
+ * device: double the capacity (up to `limit`, rows already allocated) when the
+ * window's forced overwrites exceed 1% of its admissions, then reset the window
+ * counters and the ring header. No host read. */
+int hg_cache_sweep(long long* layer_ctr, long long limit, cudaStream_t stream);
+
 /* ---- static feature region: histgnn/cache.py:338-351 (backfill_features) */
 long long hg_degree_order_scratch_bytes(long long n);
 int hg_feature_region(const int64_t* g_start, const int64_t* g_end, long long n, long long k, int32_t* chosen,
                       int32_t* feature_row_of, void* scratch, long long scratch_bytes, cudaStream_t stream);
 
-/* ---- native synthetic data: the histgnn/data.py:243-270 process (preferential
- * attachment, both edge directions) with its own PRNG, for the benchmark
- * shapes the reference generator cannot reach. Host function; writes
- * 2*m*(n-m) edges into host int32 arrays; returns the edge count or -1. */
-long long hg_synth_power_law(long long n, int m, unsigned long long seed, int32_t* src_out, int32_t* dst_out);
+/* ---- native synthetic data: histgnn/data.py:243-270 (synth_power_law),
+ * bit-identical to the reference for the same numpy Generator. pcg[6] in/out
+ * is the Generator's PCG64 state (state hi/lo, inc hi/lo, has_uint32,
+ * uinteger); it is advanced exactly as `rng.integers(len(pool))` would, so
+ * numpy continues the stream for features, labels and the split. Host
+ * function; writes 2*m*(n-m) edges into host int32 arrays; returns the edge
+ * count or -1 for invalid (n, m). */
+long long hg_synth_power_law(long long n, int m, unsigned long long* pcg, int32_t* src_out, int32_t* dst_out);
 
 #ifdef __cplusplus
 }

@@ -58,7 +58,6 @@ SIGNATURES = {
     "hg_gat_param_grads": (I32, [I64, I64, I32, P, P, P, P, P, P]),
     "hg_gat_scatter_norms": (I32, [P, I64, P, P, I32, P, P, P]),
     "hg_aggregate_fwd": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, P, P]),
-    "hg_gemm_rm": (I32, [I32, I32, I64, I64, I64, P, I64, P, I64, F32, P, I64, P]),
     "hg_scatter_rows": (I32, [P, I64, P, P, I32, I32, P, P]),
     "hg_inject_rows": (I32, [P, I64, P, P, P, I32, P, P]),
     "hg_cross_entropy": (I32, [P, P, I32, I32, P, P, P, P]),
@@ -72,12 +71,10 @@ SIGNATURES = {
     "hg_cache_update_scratch_bytes": (I64, [I64]),
     "hg_cache_rank": (I32, [P, I32, F64, P, P, P, P, P, P, P, P, I64, P]),
     "hg_cache_write": (I32, [I32, I32, I32, P, F64, I32, P, P, P, P, P, P, P, P, I64, P]),
+    "hg_cache_sweep": (I32, [P, I64, P]),
     "hg_degree_order_scratch_bytes": (I64, [I64]),
     "hg_feature_region": (I32, [P, P, I64, I64, P, P, P, I64, P]),
-    "hg_synth_power_law": (I64, [I64, I32, U64, P, P]),
-    "hg_tc_linear_fwd": (I32, [P, I64, P, I64, I32, P, I32, P, I32, P, P]),
-    "hg_tc_linear_dgrad": (I32, [P, I64, P, I32, P, I32, P, P]),
-    "hg_tc_linear_wgrad": (I32, [P, I64, P, I64, I32, P, I32, P, P, I32, P]),
+    "hg_synth_power_law": (I64, [I64, I32, P, P, P]),
     "hg_ts_bytes": (I64, [I64, I32]),
     "hg_ts_pack": (I32, [P, I64, I32, I32, I32, I64, P, P]),
     "hg_ts_linear_fwd": (I32, [P, I64, P, I32, P, I32, P, I32, P, P]),

@@ -62,6 +62,8 @@ class CachePolicy:
             raise ValueError("capacity must be >= 1 when given")
         if self.max_capacity is not None and self.max_capacity < 1:
             raise ValueError("max_capacity must be >= 1 when given")
+        if self.capacity is not None and self.max_capacity is not None and self.capacity > self.max_capacity:
+            raise ValueError(f"capacity {self.capacity} exceeds max_capacity {self.max_capacity}")
 
 
 class _LayerCache:
@@ -72,13 +74,33 @@ class _LayerCache:
         self.dtype = dtype
         self.device = device
         self.min_capacity = min_capacity
-        self.capacity = 0
+        self._capacity = 0
+        self._cap_on_device = False   # True once sweeps may grow the capacity on the device
         self.rows_alloc = 0
         self.table = None
         self.row_owner_dev = None
         self.row_of_dev = torch.full((num_nodes,), -1, dtype=torch.int32, device=device)
         self.admit_iter_dev = torch.zeros(num_nodes, dtype=torch.int32, device=device)
         self.ctr = torch.zeros(LAYER_CTR_LEN, dtype=torch.int64, device=device)
+
+    @property
+    def capacity(self) -> int:
+        """Logical ring size (cache.py:79-101). Device-resident once sweeps run
+        on the device (then reading it synchronises)."""
+        if self._cap_on_device:
+            self._capacity = int(self.ctr[CTR_CAPACITY].item())
+        return self._capacity
+
+    @capacity.setter
+    def capacity(self, v: int):
+        self._capacity = int(v)
+
+    def limit(self) -> int:
+        """Growth limit: N (cache.py:93-101), or the policy's max_capacity."""
+        limit = max(self.num_nodes, 1)
+        if self.policy.max_capacity is not None:
+            limit = min(limit, self.policy.max_capacity)
+        return limit
 
     # ---- reference-visible state (numpy views) ----
     @property
@@ -130,6 +152,8 @@ class _LayerCache:
             window = max(1, int(p.t_stale))
             cap = 2 * max(1, first_admits) * window
             cap = int(np.clip(cap, self.min_capacity, max(self.num_nodes, 1)))
+        if p.max_capacity is not None:
+            cap = min(cap, p.max_capacity)
         return max(1, cap)
 
     HEADROOM_BYTES = 8 << 30   # ring preallocation budget per layer (growth without reallocation)
@@ -138,10 +162,10 @@ class _LayerCache:
         """Rows actually allocated for a logical capacity: as many as the
         byte budget allows (never past N, never below 4x cap when N allows),
         so the doublings of cache.py:93-101 only change the device-resident
-        capacity, not the table pointer (a captured CUDA graph stays valid)."""
+        capacity, not the table pointer (a captured CUDA graph stays valid).
+        Never past the growth limit (max_capacity bounds HBM use)."""
         row_bytes = max(self.dim * torch.tensor([], dtype=self.dtype).element_size(), 1)
-        n = max(self.num_nodes, 1)
-        return max(cap, min(n, max(4 * cap, self.HEADROOM_BYTES // row_bytes)))
+        return max(cap, min(self.limit(), max(4 * cap, self.HEADROOM_BYTES // row_bytes)))
 
     def allocate(self, first_admits: int):
         self.capacity = self.first_capacity(first_admits)
@@ -152,9 +176,7 @@ class _LayerCache:
 
     def _grow(self):
         """cache.py:93-101 — double (up to N), rows kept in place."""
-        limit = max(self.num_nodes, 1)
-        if self.policy.max_capacity is not None:
-            limit = min(limit, self.policy.max_capacity)
+        limit = self.limit()
         if self.table is None or self.capacity >= limit:
             return
         new_cap = min(self.capacity * 2, limit)
@@ -168,8 +190,16 @@ class _LayerCache:
         self.capacity = new_cap
         self.ctr[CTR_CAPACITY] = new_cap
 
-    def sweep(self):
-        """cache.py:206-211 (one host read of the window counters)."""
+    def sweep(self, stream=None):
+        """cache.py:206-211. When the preallocated rows already reach the
+        growth limit, no doubling can need a reallocation: the whole sweep
+        (grow test, capacity doubling, window/header reset) runs as one device
+        kernel, with no host read. Otherwise one host read of the window
+        counters decides the growth on the host."""
+        if self.table is not None and self.rows_alloc >= self.limit():
+            self._cap_on_device = True
+            _lib.call("hg_cache_sweep", _lib.ptr(self.ctr), self.limit(), _lib.stream_ptr(stream))
+            return
         wa, wf = self.ctr[CTR_WIN_ADMIT:CTR_WIN_FORCED + 1].cpu().tolist()
         if wa and wf > 0.01 * wa:
             self._grow()

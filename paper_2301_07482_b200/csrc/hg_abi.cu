@@ -3,6 +3,8 @@
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <string>
 
 #include "hg_common.cuh"
@@ -27,21 +29,36 @@ __global__ void k_mark_time(unsigned long long* slot) {
 }
 
 bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {
     const char* e = std::getenv("HG_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+    return !(e && e[0] == '0');
+  }();
+  return v;
 }
 
 bool node_prio_enabled() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {
     const char* e = std::getenv("HG_NODE_PRIO");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+const char* env_knob(const char* name) { return std::getenv(name); }
+
+int ensure_smem_attr(const void* kernel, int bytes, const char* where) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(where, kCuda, cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(kernel, dev, bytes);
+  if (done.count(key)) return kOk;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return fail(where, kCuda, cudaGetErrorString(e));
+  done.insert(key);
+  return kOk;
 }
 
 int check_launch(const char* where) {

@@ -44,14 +44,13 @@ struct NormKeyLess {
 // large n). HG_CACHE_SORT=radix|merge overrides (A/B measurements).
 enum SortMode { kSortMerge = 1, kSortRadix = 2, kSortBucket = 3 };
 inline int sort_mode(long long n_max) {
-  static int v = -2;
-  if (v == -2) {
+  static const int v = [] {
     const char* e = std::getenv("HG_CACHE_SORT");
-    v = !e ? -1
-           : (std::strcmp(e, "radix") == 0 ? kSortRadix
-                                           : (std::strcmp(e, "merge") == 0 ? kSortMerge
-                                                                           : (std::strcmp(e, "bucket") == 0 ? kSortBucket : -1)));
-  }
+    return !e ? -1
+              : (std::strcmp(e, "radix") == 0 ? kSortRadix
+                                              : (std::strcmp(e, "merge") == 0 ? kSortMerge
+                                                                              : (std::strcmp(e, "bucket") == 0 ? kSortBucket : -1)));
+  }();
   if (v >= 0) return v;
   return kSortBucket;
 }
@@ -514,6 +513,17 @@ __global__ void k_region_rows(long long k, const int32_t* __restrict__ sorted_id
   }
 }
 
+__global__ void k_sweep(long long* ctr, long long limit) {
+  pdl_wait();
+  const long long wa = ctr[kCtrWindowAdmissions], wf = ctr[kCtrWindowForced];
+  long long cap = ctr[kCtrCapacity];
+  if (wa != 0 && (double)wf > 0.01 * (double)wa && cap < limit) cap = cap * 2 < limit ? cap * 2 : limit;
+  ctr[kCtrCapacity] = cap;
+  ctr[kCtrWindowAdmissions] = 0;
+  ctr[kCtrWindowForced] = 0;
+  ctr[kCtrHeader] = 0;
+}
+
 }  // namespace
 }  // namespace hg
 
@@ -648,6 +658,19 @@ int hg_cache_write(int n_max, int cap, int H, const int32_t* it_dev, double t_st
     { const cudaError_t _pe = hg::launch_pdl(k_refresh, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, layer_ctr, retained, keys_out, row_of, admit_iter, it_dev); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
     HG_LAUNCHED(W);
   }
+  return kOk;
+}
+
+// cache.py:206-211 (_LayerCache.sweep) on the device: grow when the window's
+// forced overwrites exceed 1% of its admissions (doubling, up to `limit`
+// rows, which the caller guarantees are allocated), reset the window
+// counters and the ring header. The comparison is the reference's
+// `forced > 0.01 * admissions` in float64 (exact for counts < 2^53).
+int hg_cache_sweep(long long* layer_ctr, long long limit, cudaStream_t stream) {
+  if (limit < 1) return fail("hg_cache_sweep", kBadArg, "limit must be >= 1");
+  { const cudaError_t _pe = hg::launch_pdl(k_sweep, dim3(1), dim3(1), 0, stream, layer_ctr, limit);
+    if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  HG_LAUNCHED("hg_cache_sweep");
   return kOk;
 }
 

@@ -128,6 +128,11 @@ __device__ __forceinline__ void kt_end(KTimer* kt) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 bool pdl_enabled();   // HG_PDL=0 disables (A/B)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device);
+// thread-safe (a mutex-guarded set), no process-global "done" flag
+int ensure_smem_attr(const void* kernel, int bytes, const char* where);
+// read an environment knob once (thread-safe static initialisation)
+const char* env_knob(const char* name);
 bool node_prio_enabled();   // HG_NODE_PRIO=1: kernel nodes carry their stream's priority
 
 template <typename... KArgs, typename... Args>

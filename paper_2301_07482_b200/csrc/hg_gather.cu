@@ -269,12 +269,11 @@ __global__ void __launch_bounds__(kBulkWarps * 32) k_load_rows_bulk(
 // rows) and the index pre-pass adds ~16 us, so the register gather (~82 us)
 // stays the default.
 inline bool use_bulk_gather() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {
     const char* e = std::getenv("HG_GATHER");
-    v = (e && std::strcmp(e, "bulk") == 0) ? 1 : 0;
-  }
-  return v == 1;
+    return e && std::strcmp(e, "bulk") == 0;
+  }();
+  return v;
 }
 
 }  // namespace
@@ -313,11 +312,8 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
                                                                static_cast<const char*>(region),
                                                                static_cast<const char*>(feats), row_bytes, src_ptr, g);
       HG_LAUNCHED(W);
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k_load_rows_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
-        attr = true;
-      }
+      const int sa = ensure_smem_attr((const void*)k_load_rows_bulk, kBulkSmem, W);
+      if (sa) return sa;
       const long long groups = (n_live_max + R - 1) / R;
       long long blocks = (groups + kBulkWarps - 1) / kBulkWarps;
       if (blocks > 148 * 2) blocks = 148 * 2;

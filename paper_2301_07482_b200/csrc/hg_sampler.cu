@@ -21,6 +21,7 @@
 // self-clearing.
 #include "hgb200.h"
 #include <cstdlib>
+#include <mutex>
 #include "hg_pcg.cuh"
 #include "hg_scan.cuh"
 
@@ -615,10 +616,14 @@ __global__ void k_relabel(const int32_t* __restrict__ src_flat, const int32_t* c
 }  // namespace
 
 int ensure_jump_table() {
-  static int done_dev = -1;
+  // once per device (the __constant__ table is per-device module state);
+  // a mutex-guarded device mask keeps concurrent callers thread-safe
+  static std::mutex mu;
+  static unsigned long long done_mask = 0;
   int dev = 0;
   HG_CHECK_CUDA("jump_table", cudaGetDevice(&dev));
-  if (done_dev == dev) return kOk;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done_mask >> (dev & 63) & 1ull) return kOk;
   JumpTable* h = new JumpTable;
   const unsigned __int128 mult = ((unsigned __int128)kMultHi << 64) | kMultLo;
   unsigned __int128 base = mult;  // MULT^(16^w)
@@ -644,7 +649,7 @@ int ensure_jump_table() {
   cudaError_t e = cudaMemcpyToSymbol(g_jump, h, sizeof(JumpTable));
   delete h;
   if (e != cudaSuccess) return fail("jump_table", kCuda, cudaGetErrorString(e));
-  done_dev = dev;
+  done_mask |= 1ull << (dev & 63);
   return kOk;
 }
 
@@ -707,15 +712,14 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   HG_LAUNCHED(W);
   // persistent warps over the tasks; HG_SEL_BLOCKS caps the grid (leaves SMs
   // to the training stream that runs concurrently with the pipelined sampler)
-  static long long sel_cap = -1;
-  if (sel_cap < 0) {
+  // 4 CTAs (32 warps) per SM: the selection is latency-bound per row, so
+  // more rows in flight help (C2: k_select 81 -> 59 ms / 200 steps; C3
+  // step 1.29 -> 1.23 ms); 6/SM gains little more (profiles/r01/notes)
+  static const long long sel_cap = [] {
     const char* e = std::getenv("HG_SEL_BLOCKS");
-    // 4 CTAs (32 warps) per SM: the selection is latency-bound per row, so
-    // more rows in flight help (C2: k_select 81 -> 59 ms / 200 steps; C3
-    // step 1.29 -> 1.23 ms); 6/SM gains little more (profiles/r01/notes)
-    sel_cap = e ? std::atoll(e) : 148 * 4;
-    if (sel_cap < 1) sel_cap = 148 * 4;
-  }
+    const long long v = e ? std::atoll(e) : 148 * 4;
+    return v < 1 ? 148ll * 4 : v;
+  }();
   const unsigned sel_grid = (unsigned)sel_cap;
   if (fanout <= 32) {
     { const cudaError_t _pe = hg::launch_pdl(k_select<true>, dim3(sel_grid), dim3(kSelThreads), 0, stream, g_start, g_end, frontier, F_dev, fanout, ss, cand_off,

@@ -547,30 +547,18 @@ inline uint32_t tmem_cols_for(int n) {
 // kernel was faster below ~256K rows (C3 forward 0.152 vs 0.178 ms/step);
 // with the vector epilogue the persistent kernel wins at every measured
 // shape: C2 1.080 -> 1.105e6, C3 0.99 -> 1.02e6 seeds/s, C5 layer 0
-// 0.63 -> 0.30 ms/step of forward GEMMs. HG_GEMM_PERSISTENT=0/1 forces.
-constexpr long long kPersistentMinRows = 0;
-inline bool use_persistent_gemm(long long M) {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = std::getenv("HG_GEMM_PERSISTENT");
-    v = (e && e[0] == '1') ? 1 : (e && e[0] == '0') ? 0 : -1;
-  }
-  return v == 1 || (v == -1 && M >= kPersistentMinRows);
-}
+// 0.63 -> 0.30 ms/step of forward GEMMs. The one-tile kernel k_tsgemm serves
+// the split-K weight gradients only.
 
 template <typename Epi>
 int launch_persistent(const char* W, const CUtensorMap& a, const CUtensorMap& b, Shape sh, Epi e, int n_tile,
                       cudaStream_t stream) {
   const int n_tiles = (sh.N + n_tile - 1) / n_tile;
   const size_t smem = (size_t)kStages * (2 * 8192 + 2 * (size_t)n_tile * 64) + 4 * 32 * 33 * 4;
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
+  {
     const int max_smem = kStages * (2 * 8192 + 2 * 256 * 64) + 4 * 32 * 33 * 4;
-    cudaError_t err = cudaFuncSetAttribute(k_tsgemm_p<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (err != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(err));
-    attr_dev = dev;
+    const int sa = ensure_smem_attr((const void*)k_tsgemm_p<Epi>, max_smem, W);
+    if (sa) return sa;
   }
   const long long tiles = ((sh.M + kTM - 1) / kTM) * (long long)n_tiles;
   const unsigned grid = (unsigned)(tiles < 1 ? 1 : (tiles < 148 ? tiles : 148));
@@ -586,17 +574,17 @@ int launch_persistent(const char* W, const CUtensorMap& a, const CUtensorMap& b,
 template <bool kMN, typename Epi>
 int launch(const char* W, const CUtensorMap& a, const CUtensorMap& b, Shape sh, Epi e, int n_tile, int splits,
            cudaStream_t stream) {
-  if (!kMN && splits == 1 && use_persistent_gemm(sh.M)) return launch_persistent(W, a, b, sh, e, n_tile, stream);
+  if constexpr (!kMN) {
+    // row-major products (forward / dgrad): persistent kernel, one K pass
+    if (splits != 1) return fail(W, kBadArg, "split-K is for the weight gradient only");
+    return launch_persistent(W, a, b, sh, e, n_tile, stream);
+  }
   const int n_tiles = (sh.N + n_tile - 1) / n_tile;
   const size_t smem = (size_t)kStages * (2 * 8192 + 2 * (size_t)n_tile * 64);
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
+  {
     const int max_smem = kStages * (2 * 8192 + 2 * 256 * 64);
-    cudaError_t err = cudaFuncSetAttribute(k_tsgemm<kMN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (err != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(err));
-    attr_dev = dev;
+    const int sa = ensure_smem_attr((const void*)k_tsgemm<kMN, Epi>, max_smem, W);
+    if (sa) return sa;
   }
   // an empty row range (R_max == 0: everything pruned or injected) still
   // launches one CTA, which exits at once (m0 >= M)

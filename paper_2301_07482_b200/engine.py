@@ -82,6 +82,38 @@ class _Graph:
     __slots__ = ("graph", "pool", "out", "key", "launches", "exec", "__weakref__")
 
 
+class PinnedRing:
+    """Reusable pinned host buffers for the per-step host<->device copies (no
+    pinned allocation per step). Slot i is handed out again only after the
+    copy last issued from it has completed (its event) and after its current
+    holder, if any, has been released (`owner._release()` reads it out)."""
+
+    def __init__(self, depth: int, numel: int, dtype):
+        self.bufs = [torch.empty(numel, dtype=dtype, pin_memory=True) for _ in range(depth)]
+        self.events = [None] * depth
+        self.owners = [None] * depth
+        self.i = 0
+
+    def acquire(self, owner=None):
+        i = self.i
+        self.i = (i + 1) % len(self.bufs)
+        prev = self.owners[i]
+        if prev is not None:
+            o = prev()
+            if o is not None:
+                o._release()
+        if self.events[i] is not None:
+            self.events[i].synchronize()
+        self.owners[i] = None if owner is None else weakref.ref(owner)
+        return i, self.bufs[i]
+
+    def issued(self, i: int, stream=None):
+        ev = self.events[i] or torch.cuda.Event()
+        ev.record(stream)
+        self.events[i] = ev
+        return ev
+
+
 class StepEngine:
     def __init__(self, trainer, B: int):
         # weak back-reference: no Trainer <-> engine cycle, so a dropped trainer
@@ -122,6 +154,7 @@ class StepEngine:
         self.timeline = None      # optional int64[32] %globaltimer marks per step (enable_timeline)
         self.timeline_names = []
         self.captures = 0         # graph (re-)captures so far
+        self.up_ring = PinnedRing(4, 12 + 2 * self.B, torch.int32)   # input words, host -> HBM
 
     @property
     def graph(self):
@@ -143,9 +176,13 @@ class StepEngine:
         return words
 
     def upload(self, words: np.ndarray) -> torch.Tensor:
-        """Host words -> HBM (pinned staging from torch's caching host
-        allocator, which keeps the buffer alive until its copy has run)."""
-        return torch.from_numpy(words).pin_memory().to(self.dev, non_blocking=True)
+        """Host words -> HBM through a reused pinned staging slot."""
+        i, buf = self.up_ring.acquire()
+        buf.numpy()[:] = words
+        dev = torch.empty(buf.shape, dtype=buf.dtype, device=self.dev)
+        dev.copy_(buf, non_blocking=True)
+        self.up_ring.issued(i)
+        return dev
 
     def _stage_sample(self, words_dev: torch.Tensor):
         self.ws.state[:5].copy_(words_dev[:10].view(torch.int64))

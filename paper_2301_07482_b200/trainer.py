@@ -288,12 +288,16 @@ class PendingMetrics:
         self._args = (iteration, epoch, num_seeds, nv)
         self._m = None
 
-    def result(self) -> IterMetrics:
+    def _release(self):
+        """Read the counters out of the (reused) pinned slot."""
         if self._m is None:
             self._ev.synchronize()
             it, ep, ns, nv = self._args
             self._m = self._tr._finish_pending(self._buf.tolist(), it, ep, ns, nv)
             self._buf = None
+
+    def result(self) -> IterMetrics:
+        self._release()
         return self._m
 
     def __getattr__(self, name):
@@ -522,13 +526,14 @@ class Trainer:
                              after[CTR_VALID::LAYER_CTR_LEN][:cache.num_layers].double(), n_src0.double(),
                              out["counts"].double()])
         if not sync:
-            host_buf = torch.empty(dev_buf.shape, dtype=dev_buf.dtype, pin_memory=True)
+            ring = self._metrics_ring(eng, dev_buf.numel())
+            pm = PendingMetrics(self, None, None, iteration, epoch, len(seeds), after.numel())
+            i, host_buf = ring.acquire(pm)
             host_buf.copy_(dev_buf, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record()
+            pm._buf, pm._ev = host_buf, ring.issued(i)
             cache.end_iteration(iteration)
             self._last_engine = (eng, out)
-            return PendingMetrics(self, host_buf, ev, iteration, epoch, len(seeds), after.numel())
+            return pm
         host = dev_buf.cpu().tolist()
         nv = after.numel()
         loss, delta = host[0], [int(x) for x in host[1:1 + nv]]
@@ -540,6 +545,13 @@ class Trainer:
         self.last = _EngineLast(out, counts)
         return self._metrics(iteration, epoch, len(seeds), loss, delta, n_src0 * self.row_bytes, valid, None,
                              prune_writes=delta[cache.num_layers * LAYER_CTR_LEN + GCTR_PRUNE_WRITES])
+
+    def _metrics_ring(self, eng, numel: int):
+        ring = getattr(eng, "metrics_ring", None)
+        if ring is None or ring.bufs[0].numel() != numel:
+            from .engine import PinnedRing
+            ring = eng.metrics_ring = PinnedRing(8, numel, torch.float64)
+        return ring
 
     def _finish_pending(self, host, iteration, epoch, num_seeds, nv):
         cache = self.cache

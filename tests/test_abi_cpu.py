@@ -18,7 +18,7 @@ def header_symbols():
 def test_header_declares_the_path():
     syms = header_symbols()
     for s in ("hg_sample_layer", "hg_prune_block", "hg_cache_lookup", "hg_load_features", "hg_aggregate_fwd",
-              "hg_transpose_agg", "hg_cache_rank", "hg_cache_write", "hg_gemm_rm"):
+              "hg_transpose_agg", "hg_cache_rank", "hg_cache_write"):
         assert s in syms
 
 
