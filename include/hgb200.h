@@ -204,8 +204,10 @@ int hg_sgd(float* params, const float* grads, long long n, float eta, cudaStream
  * nn.py:355-360 with gradients averaged over P ranks). my_slots: this rank's
  * 2 x n float exchange area, my_flag: its u64 flag word (both CUDA-IPC
  * exported); slots[r] / flags[r]: device arrays with every rank's mapping;
- * state: 4 zero-initialised u64 words. Two launches, no host sync; sums in
- * rank order so every rank applies identical bits. */
+ * state: 8 u64 words, zero except [4] = peer-wait timeout in ns (0 = 120 s);
+ * a peer that misses it sets state[3] and the update is skipped (no trap; the
+ * host checks state[3]). Two launches, no host sync; sums in rank order so
+ * every rank applies identical bits. */
 int hg_p2p_allreduce_sgd(float* params, const float* grads, long long n, float* my_slots,
                          unsigned long long* my_flag, const float* const* slots, unsigned long long* const* flags,
                          int P, unsigned long long* state, float eta, cudaStream_t stream);

@@ -34,8 +34,10 @@ def average_grads(grad_sets):
     return out
 
 
-def dp_serial_run(graph, features, labels, train_ids, cfg, num_classes, world, steps):
-    """Returns ([per-rank metrics lists], final network of rank 0)."""
+def dp_serial_run(graph, features, labels, train_ids, cfg, num_classes, world, steps, norms_for=None):
+    """Returns ([per-rank metrics lists], final network of rank 0).
+    norms_for(rank, step) -> {layer: fp64 norms} feeds each worker's cache
+    admission with externally computed norms (lockstep, SURVEY §8(c) Mode B)."""
     workers = [OTrainer(graph, features, labels, train_ids, cfg, num_classes) for _ in range(world)]
     batches = make_batches(train_ids, cfg)
     metrics = [[] for _ in range(world)]
@@ -72,7 +74,8 @@ def dp_serial_run(graph, features, labels, train_ids, cfg, num_classes, world, s
                     g.weight_neigh[...] = m.weight_neigh
 
         for r, w in enumerate(workers):
-            metrics[r].append(w.train_iteration(subs[r][0], 0, subs[r][1], grad_hook=apply_mean))
+            nrm = None if norms_for is None else norms_for(r, s)
+            metrics[r].append(w.train_iteration(subs[r][0], 0, subs[r][1], norms_override=nrm, grad_hook=apply_mean))
     return metrics, workers[0].network
 
 

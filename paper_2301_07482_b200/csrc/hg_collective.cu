@@ -12,7 +12,9 @@
 // last CTA of k_p2p_reduce_sgd advances, so it counts exchange steps and is
 // the same on every rank at a step. Slot (epoch & 1) is rewritten at epoch + 2
 // only after every rank passed the epoch + 1 barrier, i.e. finished reading it.
-// The wait times out (trap) instead of hanging if a peer never arrives.
+// The wait times out instead of hanging if a peer never arrives: the kernel
+// records the timeout in the state word, skips the update and exits (the
+// context stays usable); the host reads the word and raises.
 #include "hgb200.h"
 
 #include "hg_common.cuh"
@@ -20,7 +22,7 @@
 namespace hg {
 namespace {
 
-constexpr unsigned long long kP2PTimeoutNs = 120ull * 1000000000ull;
+constexpr unsigned long long kP2PTimeoutNs = 120ull * 1000000000ull;   // default when state[4] == 0
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -36,7 +38,8 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// st: [0] stage arrivals, [1] reduce arrivals, [2] completed exchanges, [3] timeout
+// st: [0] stage arrivals, [1] reduce arrivals, [2] completed exchanges,
+//     [3] timeout flag (sticky), [4] timeout in ns (0 = kP2PTimeoutNs)
 __global__ void k_p2p_stage(const float* __restrict__ grads, long long n, float* __restrict__ my_slots,
                             unsigned long long* my_flag, unsigned long long* st) {
   pdl_wait();
@@ -59,20 +62,26 @@ __global__ void k_p2p_reduce_sgd(float* __restrict__ params, long long n, const 
                                  unsigned long long* const* __restrict__ flags, int P, float eta,
                                  unsigned long long* st) {
   pdl_wait();
+  __shared__ int s_abort;
   const unsigned long long epoch = st[2] + 1ull;
   if (threadIdx.x == 0) {
+    const unsigned long long limit = st[4] ? st[4] : kP2PTimeoutNs;
     const unsigned long long t0 = globaltimer_ns();
-    for (int r = 0; r < P; ++r) {
+    int abort = ld_acquire_sys(st + 3) != 0ull;   // an earlier exchange already failed
+    for (int r = 0; r < P && !abort; ++r) {
       while (ld_acquire_sys(flags[r]) < epoch) {
-        if (globaltimer_ns() - t0 > kP2PTimeoutNs) {   // a peer never arrived: fail loudly, never hang the GPU
+        if (globaltimer_ns() - t0 > limit) {   // a peer never arrived: record it, never hang the GPU
           atomicExch(st + 3, 1ull);
-          __trap();
+          abort = 1;
+          break;
         }
         __nanosleep(128);
       }
     }
+    s_abort = abort;
   }
   __syncthreads();
+  if (s_abort) return;   // parameters untouched; the host sees state[3] and raises
   const long long off = (long long)(epoch & 1ull) * n;
   const float inv = 1.0f / (float)P;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -99,7 +108,8 @@ extern "C" {
 // one data-parallel step: average this rank's grads with the P-1 peers' over
 // the IPC-mapped slots and apply SGD; slots[r] = rank r's 2 x n float slot
 // area, flags[r] = rank r's flag word (device arrays of P pointers);
-// state = 4 zero-initialised u64 words owned by this rank
+// state = 8 u64 words owned by this rank, zero-initialised except [4] (the
+// peer-wait timeout in ns, 0 = 120 s); state[3] != 0 after a timed-out wait
 int hg_p2p_allreduce_sgd(float* params, const float* grads, long long n, float* my_slots,
                          unsigned long long* my_flag, const float* const* slots, unsigned long long* const* flags,
                          int P, unsigned long long* state, float eta, cudaStream_t stream) {

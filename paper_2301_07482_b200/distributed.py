@@ -67,7 +67,7 @@ class P2PAllReduce:
     fused_sgd = True
     graph_safe = True
 
-    def __init__(self, numel: int, rank: int, world: int, device, group=None):
+    def __init__(self, numel: int, rank: int, world: int, device, group=None, timeout_s: float = 120.0):
         import ctypes
 
         import torch
@@ -103,7 +103,8 @@ class P2PAllReduce:
         self.my_slots, self.my_flag = p.value, p.value + flag_off
         self.slots_dev = torch.tensor(bases, dtype=torch.int64, device=self.device)
         self.flags_dev = torch.tensor([b + flag_off for b in bases], dtype=torch.int64, device=self.device)
-        self.state = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self.state = torch.zeros(8, dtype=torch.int64, device=self.device)
+        self.state[4] = int(timeout_s * 1e9)     # peer-wait limit (hg_collective.cu)
         dist.barrier(group=group)
 
     def __call__(self, grads):
@@ -120,6 +121,12 @@ class P2PAllReduce:
     @property
     def timed_out(self) -> bool:
         return bool(int(self.state[3].item()))
+
+    def check(self) -> None:
+        """Raise if a peer missed an exchange (the kernel skipped the update)."""
+        if self.timed_out:
+            raise RuntimeError("P2P gradient exchange timed out waiting for a peer rank; parameters were not "
+                               "updated from that step on")
 
     def close(self, group=None) -> None:
         """Unmap peers and free the exchange area (collective: barriers

@@ -356,6 +356,14 @@ class Trainer:
         self.features = feats
         self.feature_dim = int(feats.shape[1])
         self.row_bytes = self.feature_dim * feats.element_size()
+        # the gather / aggregation kernels move rows as 16-byte vectors and
+        # stage at most 1024 floats per row (hg_layer.cu, hg_gather.cu); the
+        # reference takes any width, so say so here rather than deep in a launch
+        if self.row_bytes % 16 or self.feature_dim > 1024:
+            raise ValueError(f"feature rows must be a multiple of 16 bytes and at most 1024 wide "
+                             f"(got {self.feature_dim} x {feats.element_size()} B); zero-pad the feature table")
+        if cfg.hidden % 4 or cfg.hidden > 1024:
+            raise ValueError(f"hidden must be a multiple of 4 and at most 1024 (got {cfg.hidden})")
         depth = len(cfg.fanouts)
         dims = [self.feature_dim] + [cfg.hidden] * (depth - 1) + [self.num_classes]
         self.network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, self.device, heads=cfg.heads)

@@ -129,12 +129,17 @@ def gen_c1():
     res["subgraphs"] = subs
     tr = Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
     mets = []
-    for it in range(6):
+    for it in range(20):
         sub = sample_layered(g, batches[it], plan, batch_rng(cfg.seed, it))
         m = tr.train_iteration(it, 0, sub)
         mets.append({k: (float(v) if isinstance(v, float) else int(v)) for k, v in m.__dict__.items()
                      if k != "estimation_error"})
     res["trainer_sage_0.9_20"] = mets
+    res["trainer_sage_0.9_20_weights"] = {
+        f"W{l}": {"fro": float(np.linalg.norm(lp.weight.astype(np.float64))),
+                  "sum": float(lp.weight.astype(np.float64).sum()),
+                  "first": [float(x) for x in lp.weight.reshape(-1)[:16]]}
+        for l, lp in enumerate(tr.network.layers)}
     with open(os.path.join(HERE, "c1.json"), "w") as fh:
         json.dump(res, fh, indent=1)
 
@@ -276,6 +281,9 @@ def gen_trainer():
         net, losses = run_plain_loop(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
         out[f"{kind.value}_plain_sha"] = np.array(hashlib.sha256(net.checksum_bytes()).hexdigest())
         out[f"{kind.value}_plain_loss"] = np.array(losses)
+        for l, lp in enumerate(net.layers):
+            out[f"{kind.value}_plain_W{l}"] = lp.weight
+            out[f"{kind.value}_plain_b{l}"] = lp.bias
     np.savez_compressed(os.path.join(HERE, "trainer.npz"), **out)
 
 

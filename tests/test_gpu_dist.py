@@ -1,7 +1,8 @@
 """Data-parallel GPU path with two ranks sharing one B200 (gloo carries the
 CUDA-tensor all-reduce because NCCL refuses duplicate GPUs): both ranks end
-with bitwise-identical weights, and step 0 (no cache history yet) matches the
-serial DP oracle's loss within 1e-3 and its integer metrics exactly."""
+with bitwise-identical weights, and every step matches the serial DP oracle
+(oracle/dp.py) in lockstep (its cache admission fed each rank's GPU norms):
+integer metrics exact, loss within 1e-3, final weights within 1e-3."""
 
 import os
 import socket
@@ -14,7 +15,7 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-WORLD, STEPS = 2, 4
+WORLD, STEPS = 2, 6
 
 
 def _data():
@@ -35,13 +36,22 @@ def _worker(rank, port, out_dir):
     tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes)
     tr.grad_hook = make_allreduce_hook(WORLD)
     batches = hg.make_batches(ds.train_ids, cfg)
-    ms = []
-    for idx in rank_batch_indices(len(batches), rank, WORLD)[:STEPS]:
+    ms, norms = [], {}
+    for s, idx in enumerate(rank_batch_indices(len(batches), rank, WORLD)[:STEPS]):
         m = tr.train_iteration(idx, 0, tr.sample(idx, batches[idx]))
-        ms.append([m.hits, m.misses, m.admissions, m.fetched_bytes, m.prune_writes, m.loss])
+        ms.append([getattr(m, f) for f in FIELDS] + [m.loss])
+        for l in (1, 2):
+            norms[f"s{s}_l{l}"] = tr.last[3][l].cpu().numpy()
     np.save(os.path.join(out_dir, f"r{rank}_metrics.npy"), np.array(ms, dtype=np.float64))
+    np.savez(os.path.join(out_dir, f"r{rank}_norms.npz"), **norms)
+    np.save(os.path.join(out_dir, f"r{rank}_W.npy"), np.concatenate([tr.network.layers[l].weight.cpu().numpy().ravel()
+                                                                    for l in range(3)]))
     np.save(os.path.join(out_dir, f"r{rank}_w.npy"), np.frombuffer(tr.network.checksum_bytes(), np.uint8))
     dist.destroy_process_group()
+
+
+FIELDS = ["fetched_bytes", "baseline_bytes", "prune_writes", "hits", "misses", "admissions", "gradient_evictions",
+          "staleness_evictions", "forced_evictions", "feature_hits", "feature_misses", "valid_entries"]
 
 
 def _free_port():
@@ -62,12 +72,19 @@ def test_two_rank_dp_on_one_gpu(tmp_path):
     ds, g = _data()
     ocfg = OTrainConfig(fanouts=(6, 4, 3), hidden=16, batch_size=96, epochs=1, eta=0.05, kind=SAGE,
                         p_grad=0.9, t_stale=3, seed=5)
-    metrics, _ = dp_serial_run(g, ds.features, ds.labels, ds.train_ids, ocfg, ds.num_classes, WORLD, 1)
+    nz = [dict(np.load(tmp_path / f"r{r}_norms.npz")) for r in range(WORLD)]
+    metrics, onet = dp_serial_run(g, ds.features, ds.labels, ds.train_ids, ocfg, ds.num_classes, WORLD, STEPS,
+                                  norms_for=lambda r, s: {l: nz[r][f"s{s}_l{l}"] for l in (1, 2)})
     for r in range(WORLD):
-        got = np.load(tmp_path / f"r{r}_metrics.npy")[0]
-        m = metrics[r][0]
-        np.testing.assert_array_equal(got[:5], [m.hits, m.misses, m.admissions, m.fetched_bytes, m.prune_writes])
-        assert abs(got[5] - m.loss) <= 1e-3 * abs(m.loss)
+        got = np.load(tmp_path / f"r{r}_metrics.npy")
+        for s in range(STEPS):
+            m = metrics[r][s]
+            np.testing.assert_array_equal(got[s, :len(FIELDS)], [getattr(m, f) for f in FIELDS],
+                                          err_msg=f"rank {r} step {s}")
+            assert abs(got[s, -1] - m.loss) <= 1e-3 * abs(m.loss), (r, s)
+    W = np.load(tmp_path / "r0_W.npy")
+    oW = np.concatenate([onet.layers[l].weight.ravel() for l in range(3)])
+    assert np.linalg.norm(W - oW) <= 1e-3 * np.linalg.norm(oW)
 
 
 def _nccl_worker(rank, port, out_dir):
@@ -158,3 +175,42 @@ def test_p2p_fused_allreduce_sgd_matches_gloo(tmp_path):
         assert caps[1] >= 1, "the P2P step was never captured in a CUDA graph"
         losses = np.load(tmp_path / f"p{r}_losses.npy")
         np.testing.assert_array_equal(losses[0], losses[1])
+
+
+def _timeout_worker(rank, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    torch.cuda.set_device(0)
+    import paper_2301_07482_b200 as hg
+    from paper_2301_07482_b200.distributed import P2PAllReduce
+    ds, g = _data()
+    cfg = hg.TrainConfig(fanouts=(6, 4, 3), hidden=16, batch_size=96, epochs=1, eta=0.05,
+                         kind=hg.LayerKind.SAGE_MEAN, p_grad=0.9, t_stale=3, seed=5)
+    net = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes).network
+    ex = P2PAllReduce(net.flat.numel(), rank, WORLD, "cuda:0", timeout_s=0.5)
+    if rank == 0:           # rank 1 never joins this exchange
+        before = net.flat.clone()
+        grads = net.new_grads(zero=True)
+        ex.sgd(net, grads, 0.05)
+        torch.cuda.synchronize()
+        np.save(os.path.join(out_dir, "timeout.npy"),
+                np.array([ex.timed_out, bool(torch.equal(before, net.flat))]))
+        try:
+            ex.check()
+            raised = False
+        except RuntimeError:
+            raised = True
+        np.save(os.path.join(out_dir, "raised.npy"), np.array([raised]))
+        torch.zeros(1, device="cuda").add_(1)      # the context is still usable
+        torch.cuda.synchronize()
+    ex.close()
+    dist.destroy_process_group()
+
+
+def test_p2p_exchange_timeout_is_reported_not_trapped(tmp_path):
+    mp.start_processes(_timeout_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True,
+                       start_method="spawn")
+    flags = np.load(tmp_path / "timeout.npy")
+    assert flags[0], "the missing peer was not detected"
+    assert flags[1], "parameters changed although the exchange failed"
+    assert np.load(tmp_path / "raised.npy")[0]
