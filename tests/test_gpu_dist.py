@@ -15,7 +15,7 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-WORLD, STEPS = 2, 6
+WORLD, STEPS = 2, 5
 
 
 def _data():
