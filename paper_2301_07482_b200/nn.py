@@ -81,17 +81,44 @@ class LayerParams:
         return {k: _np(v) for k, v in self.named_arrays()}
 
 
-def _slab_views(flat: torch.Tensor, kind: LayerKind, dims, offsets):
+def _slab_views(flat: torch.Tensor, kind: LayerKind, dims, offsets, in_dim=None):
+    """Reference-shaped views of every layer slab. `dims` are the storage
+    widths; layer 0's input may be stored zero-padded (in_dim = the logical
+    feature width): its weight views then take the first in_dim rows of each
+    [fi_pad]-row block, so the padded rows are invisible (and stay zero: their
+    gradients are products with zero feature columns)."""
     out = []
     for l, (fi, fo) in enumerate(zip(dims[:-1], dims[1:])):
         K = _slab_k(kind, fi)
+        fl = in_dim if (l == 0 and in_dim is not None) else fi
         slab = flat[offsets[l]:offsets[l] + (K + 1) * fo].view(K + 1, fo)
         if kind is LayerKind.SAGE_MEAN:
-            out.append(LayerParams(slab[:fi], slab[K], slab[fi:K]))
+            out.append(LayerParams(slab[:fl], slab[K], slab[fi:fi + fl]))
         elif kind is LayerKind.GAT:
-            out.append(LayerParams(slab[:fi], slab[K], None, slab[fi], slab[fi + 1]))
+            out.append(LayerParams(slab[:fl], slab[K], None, slab[fi], slab[fi + 1]))
         else:
-            out.append(LayerParams(slab[:fi], slab[K], None))
+            out.append(LayerParams(slab[:fl], slab[K], None))
+    return out
+
+
+def pad_width(d: int, itemsize: int = 4) -> int:
+    """Row width the kernels need: rows move as 16-byte vectors."""
+    m = max(1, 16 // itemsize)
+    return -(-int(d) // m) * m
+
+
+def pad_columns(x, width: int):
+    """Zero-pad the columns of a 2-d host array / device tensor to `width`
+    (returned unchanged when already that wide)."""
+    if x.shape[1] == width:
+        return x
+    if isinstance(x, torch.Tensor):
+        out = torch.zeros((x.shape[0], width), dtype=x.dtype, device=x.device)
+        out[:, :x.shape[1]] = x
+        return out
+    x = np.asarray(x)
+    out = np.zeros((x.shape[0], width), dtype=x.dtype)
+    out[:, :x.shape[1]] = x
     return out
 
 
@@ -112,16 +139,22 @@ class Network:
     offsets: list
     layers: list = field(default_factory=list)
     heads: list | None = None                # GAT heads per layer (hidden H, output 1)
+    in_dim: int | None = None                # logical layer-0 input width when dims[0] is padded
 
     def __post_init__(self):
         if not self.layers:
-            self.layers = _slab_views(self.flat, self.kind, self.dims, self.offsets)
+            self.layers = _slab_views(self.flat, self.kind, self.dims, self.offsets, self.in_dim)
         if self.heads is None:
             self.heads = [1] * (len(self.dims) - 1)
 
     @property
     def num_layers(self) -> int:
         return len(self.dims) - 1
+
+    @property
+    def logical_dims(self) -> list:
+        """Reference layer widths (dims[0] unpadded)."""
+        return [self.in_dim if self.in_dim is not None else self.dims[0]] + list(self.dims[1:])
 
     @property
     def dtype(self):
@@ -148,7 +181,7 @@ class Grads:
 
     @property
     def layers(self):
-        return _slab_views(self.flat, self.net.kind, self.net.dims, self.net.offsets)
+        return _slab_views(self.flat, self.net.kind, self.net.dims, self.net.offsets, self.net.in_dim)
 
     def __getitem__(self, l):
         return self.layers[l]
@@ -163,7 +196,7 @@ class Grads:
 
 
 def init_network(kind: LayerKind, dims, rng: np.random.Generator, dtype=np.float32, device=None,
-                 heads: int = 4) -> Network:
+                 heads: int = 4, in_pad: int | None = None) -> Network:
     """Glorot-uniform weights, zero biases (nn.py:73-85); host RNG, then upload.
     GAT (oracle/gat.py init_layer): per layer W, then a_src, a_dst ~
     U(+-sqrt(6/(F+1))); `heads` on hidden layers, 1 on the output layer."""
@@ -173,45 +206,53 @@ def init_network(kind: LayerKind, dims, rng: np.random.Generator, dtype=np.float
     dims = [int(d) for d in dims]
     L = len(dims) - 1
     hl = [heads if l < L - 1 else 1 for l in range(L)] if kind is LayerKind.GAT else [1] * L
-    offs, total = _offsets(kind, dims)
+    sdims = [int(in_pad) if in_pad else dims[0]] + dims[1:]   # storage widths
+    if sdims[0] < dims[0]:
+        raise ValueError("in_pad must be >= the input width")
+    offs, total = _offsets(kind, sdims)
     host = np.zeros(total, dtype=np.float32)
     for l, (fi, fo) in enumerate(zip(dims[:-1], dims[1:])):
+        fs = sdims[l]
         s = np.sqrt(6.0 / (fi + fo))
         w = rng.uniform(-s, s, size=(fi, fo)).astype(np.float32)
-        K = _slab_k(kind, fi)
+        K = _slab_k(kind, fs)
         slab = host[offs[l]:offs[l] + (K + 1) * fo].reshape(K + 1, fo)
         slab[:fi] = w
         if kind is LayerKind.SAGE_MEAN:
-            slab[fi:K] = rng.uniform(-s, s, size=(fi, fo)).astype(np.float32)
+            slab[fs:fs + fi] = rng.uniform(-s, s, size=(fi, fo)).astype(np.float32)
         elif kind is LayerKind.GAT:
             if fo % hl[l]:
                 raise ValueError(f"layer {l}: d_out {fo} not divisible by {hl[l]} heads")
             la = np.sqrt(6.0 / (fo // hl[l] + 1))
-            slab[fi] = rng.uniform(-la, la, size=fo).astype(np.float32)
-            slab[fi + 1] = rng.uniform(-la, la, size=fo).astype(np.float32)
+            slab[fs] = rng.uniform(-la, la, size=fo).astype(np.float32)
+            slab[fs + 1] = rng.uniform(-la, la, size=fo).astype(np.float32)
     flat = torch.from_numpy(host).to(torch.device(device or "cuda"))
-    return Network(kind, dims, flat, offs, heads=hl)
+    return Network(kind, sdims, flat, offs, heads=hl, in_dim=dims[0] if sdims[0] != dims[0] else None)
 
 
-def network_from_numpy(kind: LayerKind, layers, device=None, heads=None) -> Network:
+def network_from_numpy(kind: LayerKind, layers, device=None, heads=None, in_pad: int | None = None) -> Network:
     """Pack reference-style per-layer arrays (weight, bias, weight_neigh /
-    att_src, att_dst)."""
+    att_src, att_dst); in_pad stores layer 0's input zero-padded (pad_width)."""
     dims = [layers[0]["weight"].shape[0]] + [p["weight"].shape[1] for p in layers]
-    offs, total = _offsets(kind, dims)
+    if in_pad is None:
+        in_pad = pad_width(dims[0])
+    sdims = [int(in_pad)] + dims[1:]
+    offs, total = _offsets(kind, sdims)
     host = np.zeros(total, dtype=np.float32)
     for l, p in enumerate(layers):
         fi, fo = p["weight"].shape
-        K = _slab_k(kind, fi)
+        fs = sdims[l]
+        K = _slab_k(kind, fs)
         slab = host[offs[l]:offs[l] + (K + 1) * fo].reshape(K + 1, fo)
         slab[:fi] = p["weight"]
         slab[K] = p["bias"]
         if kind is LayerKind.SAGE_MEAN:
-            slab[fi:K] = p["weight_neigh"]
+            slab[fs:fs + fi] = p["weight_neigh"]
         elif kind is LayerKind.GAT:
-            slab[fi] = p["att_src"]
-            slab[fi + 1] = p["att_dst"]
-    return Network(kind, dims, torch.from_numpy(host).to(torch.device(device or "cuda")), offs,
-                   heads=None if heads is None else list(heads))
+            slab[fs] = p["att_src"]
+            slab[fs + 1] = p["att_dst"]
+    return Network(kind, sdims, torch.from_numpy(host).to(torch.device(device or "cuda")), offs,
+                   heads=None if heads is None else list(heads), in_dim=dims[0] if sdims[0] != dims[0] else None)
 
 
 # ---------------------------------------------------------------- tapes
@@ -494,7 +535,7 @@ def forward_pass(network: Network, blocks, h_input, compute_rows=None, injected=
     dev = network.flat.device
     stream = _lib.stream_ptr()
     h = h_input if isinstance(h_input, torch.Tensor) else torch.as_tensor(np.asarray(h_input, np.float32))
-    h = h.to(dev, torch.float32).contiguous()
+    h = pad_columns(h.to(dev, torch.float32), network.dims[0]).contiguous()
     ents, hs = [], []
     h_prev = h
     for l, blk in enumerate(blocks):
@@ -647,6 +688,8 @@ def backward(network: Network, blocks, tape: BatchTape, d_logits, need_input: bo
         live = torch.arange(blk.num_src, dtype=torch.int32, device=dev)
         d_prev, _ = layer_backward_dev(network, l, blk, t, d_h, grads, want, keep, pos, live, blk.num_src, stream)
         d_h = d_prev
+    if d_h is not None and network.in_dim is not None:
+        d_h = d_h[:, :network.in_dim]
     return grads, node_grads, d_h
 
 

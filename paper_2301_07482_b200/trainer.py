@@ -29,7 +29,8 @@ from .distributed import apply_sgd
 from .engine import StepEngine
 from .cache import COUNTER_NAMES, CachePolicy, HistCache
 from .graphs import Csr2Graph, _np, csr2_from_arrays
-from .nn import (Injection, LayerKind, Network, backward, cross_entropy_dev, forward_pass, init_network,
+from .nn import (Injection, LayerKind, Network, backward, cross_entropy_dev, forward_pass, init_network, pad_columns,
+                 pad_width,
                  layer_backward_dev, layer_forward_dev, load_features_dev, sgd_step, _dev_count)
 from .sharding import ShardedFeatures
 from .sampler import LayeredSubgraph, SamplePlan, SubgraphProducer, batch_rng, sample_layered, split_batches
@@ -347,6 +348,20 @@ class Trainer:
             feats = features
         else:
             feats = torch.from_numpy(np.ascontiguousarray(features))
+        # the gather / aggregation kernels move rows as 16-byte vectors (at
+        # most 1024 floats): a feature width that is not a multiple of 16
+        # bytes is stored zero-padded (layer 0's weights get matching zero
+        # rows, invisible through the reference-shaped views, nn._slab_views)
+        self.in_dim = int(feats.shape[1])
+        d_pad = pad_width(self.in_dim, feats.element_size())
+        if d_pad > 1024:
+            raise ValueError(f"feature width {self.in_dim} exceeds the kernels' 1024-float row limit")
+        if cfg.hidden % 4 or cfg.hidden > 1024:
+            raise ValueError(f"hidden must be a multiple of 4 and at most 1024 (got {cfg.hidden})")
+        if d_pad != self.in_dim:
+            if isinstance(feats, ShardedFeatures):
+                raise ValueError("sharded feature tables need rows of a multiple of 16 bytes")
+            feats = pad_columns(feats, d_pad)
         if isinstance(feats, ShardedFeatures):
             pass
         elif cfg.feature_placement == "hbm":
@@ -354,19 +369,12 @@ class Trainer:
         elif feats.device.type != "cpu" or not feats.is_pinned():
             feats = feats.cpu().pin_memory()
         self.features = feats
-        self.feature_dim = int(feats.shape[1])
-        self.row_bytes = self.feature_dim * feats.element_size()
-        # the gather / aggregation kernels move rows as 16-byte vectors and
-        # stage at most 1024 floats per row (hg_layer.cu, hg_gather.cu); the
-        # reference takes any width, so say so here rather than deep in a launch
-        if self.row_bytes % 16 or self.feature_dim > 1024:
-            raise ValueError(f"feature rows must be a multiple of 16 bytes and at most 1024 wide "
-                             f"(got {self.feature_dim} x {feats.element_size()} B); zero-pad the feature table")
-        if cfg.hidden % 4 or cfg.hidden > 1024:
-            raise ValueError(f"hidden must be a multiple of 4 and at most 1024 (got {cfg.hidden})")
+        self.feature_dim = d_pad                                  # storage width of every layer-0 row
+        self.row_bytes = self.in_dim * feats.element_size()       # the reference's I/O accounting unit
         depth = len(cfg.fanouts)
-        dims = [self.feature_dim] + [cfg.hidden] * (depth - 1) + [self.num_classes]
-        self.network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, self.device, heads=cfg.heads)
+        dims = [self.in_dim] + [cfg.hidden] * (depth - 1) + [self.num_classes]
+        self.network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, self.device, heads=cfg.heads,
+                                    in_pad=self.feature_dim)
         policy = CachePolicy(cfg.p_grad, cfg.t_stale, cfg.capacity, cfg.max_capacity)
         feature_rows = self.graph.num_nodes // 10 if cfg.feature_rows is None else cfg.feature_rows
         self.cache = HistCache(self.graph.num_nodes, [cfg.hidden] * (depth - 1), policy, feature_rows=feature_rows,
@@ -670,11 +678,12 @@ def run_plain_loop(graph, features, labels, train_ids, cfg: TrainConfig, num_cla
     train_ids = np.asarray(train_ids, dtype=np.int64)
     ncls = int(num_classes or labels.max() + 1)
     feats = features if isinstance(features, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(features))
-    feats = feats.to(dev)
-    d = int(feats.shape[1])
+    d_in = int(feats.shape[1])
+    d = pad_width(d_in, feats.element_size())
+    feats = pad_columns(feats.to(dev), d)
     depth = len(cfg.fanouts)
-    dims = [d] + [cfg.hidden] * (depth - 1) + [ncls]
-    network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, dev, heads=cfg.heads)
+    dims = [d_in] + [cfg.hidden] * (depth - 1) + [ncls]
+    network = init_network(cfg.kind, dims, _network_rng(cfg.seed), cfg.dtype, dev, heads=cfg.heads, in_pad=d)
     plan = SamplePlan(cfg.fanouts, cfg.batch_size, cfg.seed)
     losses = []
     gctr = torch.zeros(8, dtype=torch.int64, device=dev)
@@ -731,7 +740,7 @@ def full_graph_logits(network: Network, graph, features, chunk_rows: int | None 
     if int(g.end.max().item() if N else 0) >= 2 ** 31:
         raise ValueError("evaluate needs fewer than 2^31 edges (int32 block offsets)")
     feats = features if isinstance(features, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(features))
-    feats = feats.to(dev)
+    feats = pad_columns(feats.to(dev), network.dims[0])
     if feats.shape[0] != N:
         raise ValueError("features must have one row per node")
     sp = _lib.stream_ptr()

@@ -262,3 +262,37 @@ def test_wide_feature_rows_lockstep(kind, dim):
     w = tr.network.layers[0].weight.cpu().numpy()
     ow = otr.network.layers[0].weight
     assert np.linalg.norm(w - ow) <= 1e-3 * np.linalg.norm(ow)
+
+
+@pytest.mark.parametrize("kind,dim,fp16", [(SAGE, 3, False), (GCN, 6, False), (SAGE, 12, True)])
+def test_unaligned_feature_width_lockstep(kind, dim, fp16):
+    """Feature widths that are not a multiple of 16 bytes (the reference takes
+    any width; its own tests use 3- and 4-d features): stored zero-padded on
+    the device, reference-shaped weights, results as the oracle's."""
+    import paper_2301_07482_b200 as hg
+    ds = power_law_dataset(1200, np.random.default_rng(9), m=3, feature_dim=dim)
+    feats = ds.features.astype(np.float16) if fp16 else ds.features
+    g = csr2_from_edges(ds.src, ds.dst, ds.num_nodes)
+    lk, ok = _kinds(kind)
+    common = dict(fanouts=(5, 4, 3), hidden=16, batch_size=64, epochs=1, eta=0.05, p_grad=0.9, t_stale=3, seed=2)
+    tr = hg.Trainer(g, feats, ds.labels, ds.train_ids, hg.TrainConfig(kind=lk, **common), ds.num_classes)
+    otr = OTrainer(g, feats, ds.labels, ds.train_ids, OTrainConfig(kind=ok, **common), ds.num_classes)
+    assert tuple(tr.network.layers[0].weight.shape) == (dim, 16)
+    for it, seeds in enumerate(hg.make_batches(ds.train_ids, tr.cfg)[:6]):
+        m = tr.train_iteration(it, 0, tr.sample(it, seeds))
+        norms = {l: tr.last[3][l].cpu().numpy() for l in range(1, 3)}
+        om = otr.train_iteration(it, 0, otr.sample(it, seeds), norms_override=norms)
+        for f in INT_FIELDS:
+            assert getattr(m, f) == getattr(om, f), (it, f, getattr(m, f), getattr(om, f))
+        assert abs(m.loss - om.loss) <= 1e-3 * abs(om.loss), (it, m.loss, om.loss)
+    for l in range(3):
+        w = tr.network.layers[l].weight.cpu().numpy()
+        ow = otr.network.layers[l].weight
+        assert w.shape == ow.shape
+        assert np.linalg.norm(w - ow) <= 1e-3 * np.linalg.norm(ow)
+    # the padded weight rows stayed exactly zero
+    slab = tr.network.slab(0).cpu().numpy()
+    fs = tr.network.dims[0]
+    assert not slab[dim:fs].any()
+    if kind == SAGE:
+        assert not slab[fs + dim:2 * fs].any()
