@@ -293,6 +293,11 @@ class HistCache:
         return len(self.layers)
 
     @property
+    def feature_table_dev(self):
+        """The device feature region [k x d] (None before backfill)."""
+        return self.feature_table
+
+    @property
     def feature_row_of(self):
         return _np(self.feature_row_of_dev).astype(np.int64)
 
@@ -316,7 +321,8 @@ class HistCache:
             self.gctr[GCTR_FEATURE_HITS] += nh
             self.gctr[GCTR_FEATURE_MISSES] += len(ids) - nh
             okn = _np(ok)
-            vals = (_np(self.feature_table[rows[ok].long()]) if self.feature_table is not None and nh
+            ft = self.feature_table_dev
+            vals = (_np(ft[rows[ok].long()]) if ft is not None and nh
                     else np.empty((0, self.feature_dim or 0)))
             return ids[okn], vals, ids[~okn]
         lc = self._layer(layer)

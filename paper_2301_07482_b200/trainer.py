@@ -132,38 +132,50 @@ def epoch_mean_estimation_error(metrics, epoch: int) -> float:
 
 
 def cosine_rows(a: np.ndarray, b: np.ndarray) -> np.ndarray:
-    """Row-wise cosine; rows where either side has zero norm come back nan."""
-    na = np.linalg.norm(a, axis=1)
-    nb = np.linalg.norm(b, axis=1)
-    ok = (na > 0) & (nb > 0)
-    out = np.full(len(a), np.nan)
-    out[ok] = np.einsum("ij,ij->i", a[ok], b[ok]) / (na[ok] * nb[ok])
-    return out
+    """Per-row cosine of two equally shaped matrices (trainer.py:234-241);
+    nan where either row is all zeros."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    denom = np.sqrt((a * a).sum(axis=1) * (b * b).sum(axis=1))
+    with np.errstate(invalid="ignore", divide="ignore"):
+        cos = (a * b).sum(axis=1) / denom
+    cos[denom == 0] = np.nan
+    return cos
 
 
 class EmbeddingLog:
     """Exact-embedding snapshots of a tracked node set keyed by iteration
-    (trainer.py:244-272)."""
+    (trainer.py:244-272): `similarity(t, s)` is the mean cosine between the
+    snapshots of iterations t and t - s over the nodes both contain,
+    all-zero rows left out (nan when nothing is left)."""
 
     def __init__(self):
         self.records: dict = {}
 
     def record(self, iteration: int, ids, rows) -> None:
-        self.records[iteration] = (np.asarray(ids, dtype=np.int64).copy(), np.asarray(rows).copy())
+        self.records[iteration] = (np.array(ids, dtype=np.int64), np.array(rows))
 
     def similarity(self, t: int, s: int) -> float:
-        if s < 0 or t - s < 0:
+        older = t - s
+        if s < 0 or older < 0:
             raise ValueError(f"need 0 <= s <= t, got t={t} s={s}")
-        if t not in self.records or t - s not in self.records:
-            raise ValueError(f"no snapshot for iterations {t} and {t - s}")
-        ids_a, rows_a = self.records[t]
-        ids_b, rows_b = self.records[t - s]
-        common, ia, ib = np.intersect1d(ids_a, ids_b, return_indices=True)
-        if len(common) == 0:
+        missing = [i for i in (t, older) if i not in self.records]
+        if missing:
+            raise ValueError(f"no snapshot for iterations {t} and {older}")
+        (ids_t, rows_t), (ids_o, rows_o) = self.records[t], self.records[older]
+        order_o = np.argsort(ids_o, kind="stable")
+        pos = np.searchsorted(ids_o, ids_t, sorter=order_o)
+        pos = np.minimum(pos, max(len(ids_o) - 1, 0))
+        both = (len(ids_o) > 0) & (ids_o[order_o[pos]] == ids_t) if len(ids_o) else np.zeros(len(ids_t), bool)
+        if not both.any():
             return math.nan
-        cos = cosine_rows(rows_a[ia], rows_b[ib])
-        cos = cos[~np.isnan(cos)]
-        return float(cos.mean()) if len(cos) else math.nan
+        # first occurrence per common id (ids within a snapshot are unique)
+        keep_t = np.flatnonzero(both)
+        _, first = np.unique(ids_t[keep_t], return_index=True)
+        keep_t = keep_t[first]
+        cos = cosine_rows(rows_t[keep_t], rows_o[order_o[pos[keep_t]]])
+        cos = cos[np.isfinite(cos)]
+        return float(cos.mean()) if cos.size else math.nan
 
 
 # ------------------------------------------------------ cache-aware pruning

@@ -55,3 +55,35 @@ def test_product_fails_loudly_without_gpu():
     from paper_2301_07482_b200._lib import HgError
     with pytest.raises(HgError):
         hg.build_csr2(hg.CooGraph([0, 1], [1, 2], 3))
+
+
+def test_integration_stub_binds_the_header_signature():
+    """The binding stub INTEGRATION.md shows a maintainer is executable and
+    its argtypes equal the package's table (and so the header's arity)."""
+    import ctypes
+    import types
+    from paper_2301_07482_b200 import _lib
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    blocks = re.findall(r"```python\n(.*?)```", text, re.S)
+    stub = [b for b in blocks if "hg_sample_layer.argtypes" in b]
+    assert len(stub) == 1
+
+    class FakeLib:
+        def __init__(self, *_):
+            self.fns = {}
+
+        def __getattr__(self, name):
+            return self.__dict__["fns"].setdefault(name, types.SimpleNamespace())
+
+    ns = {}
+    real = ctypes.CDLL
+    ctypes.CDLL = FakeLib
+    try:
+        exec(compile(stub[0], "INTEGRATION.md", "exec"), ns)
+    finally:
+        ctypes.CDLL = real
+    for name in ("hg_sample_layer", "hg_sample_layer_scratch_bytes"):
+        got = getattr(ns["_lib"], name)
+        res, args = _lib.SIGNATURES[name]
+        assert got.argtypes == args, name
+        assert got.restype == res, name

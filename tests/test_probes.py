@@ -80,3 +80,31 @@ def test_trainer_fills_embedding_log_for_probe_nodes():
     assert len(tr.embedding_log.records) > 0
     t = max(tr.embedding_log.records)
     assert tr.embedding_log.similarity(t, 0) == pytest.approx(1.0)
+
+
+def test_similarity_edge_cases_against_a_set_restatement():
+    """Random snapshots (empty, disjoint, zero rows) against a dictionary
+    restatement of trainer.py:253-272."""
+    rng = np.random.default_rng(0)
+
+    def slow(log, t, s):
+        a, b = dict(zip(*map(list, log.records[t]))), dict(zip(*map(list, log.records[t - s])))
+        cos = []
+        for k in sorted(set(a) & set(b)):
+            x, y = np.asarray(a[k], float), np.asarray(b[k], float)
+            nx, ny = np.linalg.norm(x), np.linalg.norm(y)
+            if nx > 0 and ny > 0:
+                cos.append(float(x @ y) / (nx * ny))
+        return float(np.mean(cos)) if cos else math.nan
+
+    for _ in range(200):
+        log = EmbeddingLog()
+        for it in range(4):
+            n = int(rng.integers(0, 8))
+            rows = rng.standard_normal((n, 3))
+            rows[rng.random(n) < 0.2] = 0.0
+            log.record(it, rng.choice(12, size=n, replace=False), rows)
+        for t in range(4):
+            for s in range(t + 1):
+                got, want = log.similarity(t, s), slow(log, t, s)
+                assert (math.isnan(got) and math.isnan(want)) or got == pytest.approx(want, abs=1e-12)
