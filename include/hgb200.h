@@ -234,6 +234,51 @@ int hg_cache_write(int n_max, int cap, int H, const int32_t* it_dev, double t_st
  * counters and the ring header. No host read. */
 int hg_cache_sweep(long long* layer_ctr, long long limit, cudaStream_t stream);
 
+/* ---- owner-sharded cache (semantics: oracle/shardcache.py;
+ * kernels: csrc/hg_shard_cache.cu). Node v is owned by o with
+ * bounds[o] <= v < bounds[o+1] (comms.py:329-337); an owner's row_of /
+ * admit_iter are indexed by v - bounds[o], its row_owner holds global ids.
+ * Request area (the requesting rank's IPC-mapped memory): per rank position j
+ * req_id, req_act, req_src and, for writes, the row req_emb[j]; header
+ * int64[8]: [0] n, [1] k, [2] iteration, [3] expired count.
+ *
+ * hg_cache_request_reset: start of a step (hdr = {0, 0, *it_dev, 0}).
+ * hg_cache_lookup_sharded: cache.py:103-129 as a pure read of every owner's
+ *   state (pointer tables of P entries, peer mappings over CUDA IPC); hit rows
+ *   copied to staging[loc] (hit_row[loc] = loc), expired ids appended to
+ *   exp_ids (not invalidated: the owners apply them at commit).
+ * hg_cache_request: cache.py:188-191's admission rank of one batch as actions
+ *   (0 evict-if-held, 1 write, 2 retained) in rank order; touches no state.
+ * hg_cache_invalidate / hg_cache_apply: owner side of the commit: all ranks'
+ *   expiries (cache.py:106-115), then one rank's request restricted to owned
+ *   ids (cache.py:131-204) and that batch's end_iteration sweep (:206-211,
+ *   :330-334). cap_fixed = ceil(capacity / P) or -1; n_owned / limit bound
+ *   the first-use sizing and growth (cache.py:79-101).
+ * hg_peer_signal / hg_peer_wait: device barrier over IPC-mapped u64 flags;
+ *   state u64[4] = {epoch, timeout flag (sticky), timeout ns (0 = 120 s)}. */
+int hg_cache_request_reset(long long* req_hdr, const int32_t* it_dev, cudaStream_t stream);
+int hg_cache_lookup_sharded(const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
+                            const int32_t* src_nodes, long long n_src_max, int P, const long long* bounds,
+                            const int32_t* const* row_of, const int32_t* const* admit_iter, const float* const* tables,
+                            int row_words, const int32_t* it_dev, double t_stale, uint8_t* hit_flag, int32_t* hit_row,
+                            float* staging, int32_t* exp_ids, long long* req_hdr, long long* layer_ctr,
+                            cudaStream_t stream);
+int hg_cache_request(const int32_t* n_dev, int n_max, double p_grad, const int32_t* live, const int32_t* src_nodes,
+                     const double* norms, const uint8_t* computed_flag, const float* emb, int row_words,
+                     int32_t* req_id, uint8_t* req_act, int32_t* req_src, float* req_emb, long long* req_hdr,
+                     void* scratch, long long scratch_bytes, cudaStream_t stream);
+long long hg_cache_apply_scratch_bytes(long long n_max);
+int hg_cache_invalidate(int P, const int32_t* const* exp_ids, const long long* const* req_hdrs, long long n_max,
+                        long long lo, long long hi, int32_t* row_of, int32_t* row_owner, long long* layer_ctr,
+                        cudaStream_t stream);
+int hg_cache_apply(const long long* req_hdr, const int32_t* req_id, const uint8_t* req_act, const float* req_emb,
+                   long long n_max, int row_words, long long lo, long long hi, double t_stale, int refresh_retained,
+                   long long cap_fixed, long long n_owned, long long limit, float* table, int32_t* row_of,
+                   int32_t* row_owner, int32_t* admit_iter, long long* layer_ctr, void* scratch,
+                   long long scratch_bytes, cudaStream_t stream);
+int hg_peer_signal(unsigned long long* my_flag, unsigned long long* state, cudaStream_t stream);
+int hg_peer_wait(unsigned long long* const* flags, int P, unsigned long long* state, cudaStream_t stream);
+
 /* ---- static feature region: histgnn/cache.py:338-351 (backfill_features) */
 long long hg_degree_order_scratch_bytes(long long n);
 int hg_feature_region(const int64_t* g_start, const int64_t* g_end, long long n, long long k, int32_t* chosen,

@@ -46,8 +46,13 @@ class OCachePolicy:
 
 
 class _Ring:
-    def __init__(self, n, dim, policy, dtype, min_capacity=64):
+    """n = id space (row_of is indexed by global id); n_cap = the node count
+    the capacity rule clips to and growth stops at (cache.py:79-101): the
+    whole graph, or an owner's range in the sharded cache (oracle/shardcache.py)."""
+
+    def __init__(self, n, dim, policy, dtype, min_capacity=64, n_cap=None):
         self.n, self.dim, self.policy, self.dtype = n, dim, policy, dtype
+        self.n_cap = n if n_cap is None else n_cap
         self.min_capacity = min_capacity
         self.capacity, self.header = 0, 0
         self.table = None
@@ -67,18 +72,18 @@ class _Ring:
         if p.capacity is not None:
             cap = p.capacity
         elif self._inf:
-            cap = self.n
+            cap = self.n_cap
         else:
             cap = 2 * max(1, first_admits) * max(1, int(p.t_stale))
-            cap = int(min(max(cap, self.min_capacity), max(self.n, 1)))
+            cap = int(min(max(cap, self.min_capacity), max(self.n_cap, 1)))
         self.capacity = max(1, cap)
         self.table = np.zeros((self.capacity, self.dim), self.dtype)
         self.row_owner = np.full(self.capacity, -1, np.int64)
 
     def grow(self):
-        if self.table is None or self.capacity >= self.n:
+        if self.table is None or self.capacity >= self.n_cap:
             return
-        cap = min(2 * self.capacity, max(self.n, 1))
+        cap = min(2 * self.capacity, max(self.n_cap, 1))
         t = np.zeros((cap, self.dim), self.dtype)
         t[:self.capacity] = self.table
         o = np.full(cap, -1, np.int64)
@@ -165,6 +170,45 @@ class _Ring:
         self.write(nodes[wpos], emb[wpos], it)
         if refresh_retained:
             kept = nodes[admitted & ~computed]
+            kept = kept[self.row_of[kept] >= 0]
+            self.admit_iter[kept] = it
+
+    # ---- split form for the owner-sharded cache (oracle/shardcache.py) ----
+    def peek(self, ids, it):
+        """Pure-read lookup: (fresh mask, rows of the fresh ids in input
+        order, expired mask). No state or counter changes."""
+        r = self.row_of[ids]
+        ok = r >= 0
+        expired = np.zeros(len(ids), bool)
+        if not self._inf:
+            expired = ok & (it - self.admit_iter[ids] > self.policy.t_stale)
+            ok = ok & ~expired
+        vals = (self.table[r[ok]].copy() if self.table is not None and ok.any()
+                else np.empty((0, self.dim), self.dtype))
+        return ok, vals, expired
+
+    def invalidate(self, ids):
+        """Apply expiries found by pure-read lookups (counted once per entry
+        still held, as the eager lookup of cache.py:106-115 counts them)."""
+        if self.table is not None and len(ids):
+            self.counters["staleness_evictions"] += self._drop(np.unique(np.asarray(ids, np.int64)))
+
+    def apply(self, nodes, computed, emb, norms, it, refresh_retained, owned):
+        """update() with the batch-wide admission rank, applied only to the
+        `owned` members (an owner's share of a peer's request)."""
+        n = len(nodes)
+        k = int(math.floor(self.policy.p_grad * n))
+        rank = np.lexsort((nodes, norms))
+        admitted = np.zeros(n, bool)
+        admitted[rank[:k]] = True
+        losers = ~admitted & owned & (self.row_of[nodes] >= 0)
+        if losers.any():
+            self.counters["gradient_evictions"] += self._drop(nodes[losers])
+        top = rank[:k]
+        wpos = top[computed[top] & owned[top]]
+        self.write(nodes[wpos], emb[wpos], it)
+        if refresh_retained:
+            kept = nodes[admitted & ~computed & owned]
             kept = kept[self.row_of[kept] >= 0]
             self.admit_iter[kept] = it
 

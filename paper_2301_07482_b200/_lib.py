@@ -72,6 +72,14 @@ SIGNATURES = {
     "hg_cache_rank": (I32, [P, I32, F64, P, P, P, P, P, P, P, P, I64, P]),
     "hg_cache_write": (I32, [I32, I32, I32, P, F64, I32, P, P, P, P, P, P, P, P, I64, P]),
     "hg_cache_sweep": (I32, [P, I64, P]),
+    "hg_cache_request_reset": (I32, [P, P, P]),
+    "hg_cache_lookup_sharded": (I32, [P, I64, P, P, I64, I32, P, P, P, P, I32, P, F64, P, P, P, P, P, P, P]),
+    "hg_cache_request": (I32, [P, I32, F64, P, P, P, P, P, I32, P, P, P, P, P, P, I64, P]),
+    "hg_cache_apply_scratch_bytes": (I64, [I64]),
+    "hg_cache_invalidate": (I32, [I32, P, P, I64, I64, I64, P, P, P, P]),
+    "hg_cache_apply": (I32, [P, P, P, P, I64, I32, I64, I64, F64, I32, I64, I64, I64, P, P, P, P, P, P, I64, P]),
+    "hg_peer_signal": (I32, [P, P, P]),
+    "hg_peer_wait": (I32, [P, I32, P, P]),
     "hg_degree_order_scratch_bytes": (I64, [I64]),
     "hg_feature_region": (I32, [P, P, I64, I64, P, P, P, I64, P]),
     "hg_synth_power_law": (I64, [I64, I32, P, P, P]),

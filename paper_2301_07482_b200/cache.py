@@ -288,6 +288,15 @@ class HistCache:
         self.feature_row_of_dev = torch.full((num_nodes,), -1, dtype=torch.int32, device=self.device)
         self.gctr = torch.zeros(GLOBAL_CTR_LEN, dtype=torch.int64, device=self.device)
 
+    sharded = False
+
+    def begin_step(self, it_dev, stream) -> None:
+        """Data-parallel hook before a step's lookups (the owner-sharded cache
+        waits for its peers' commits there); a process-local cache has none."""
+
+    def commit(self, stream) -> None:
+        """Data-parallel hook after a step's updates; nothing to do here."""
+
     @property
     def num_layers(self) -> int:
         return len(self.layers)

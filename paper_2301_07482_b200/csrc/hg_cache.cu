@@ -335,10 +335,10 @@ struct NormKeyDecomposer {
 // keys for i < n; the tail up to n_max gets sentinels that sort last
 __global__ void k_norm_keys(const int32_t* n_dev, int n_max, double p_grad, const int32_t* __restrict__ live,
                             const int32_t* __restrict__ src_nodes, const double* __restrict__ norms,
-                            NormKey* __restrict__ keys, int32_t* __restrict__ vals, long long* ctr) {
+                            NormKey* __restrict__ keys, int32_t* __restrict__ vals, long long* k_out) {
   pdl_wait();
   const int n = *n_dev;
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctr[kCtrK] = (long long)floor(p_grad * (double)n);  // cache.py:190
+  if (blockIdx.x == 0 && threadIdx.x == 0) *k_out = (long long)floor(p_grad * (double)n);  // cache.py:190
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_max; i += gridDim.x * blockDim.x) {
     if (i < n) {
       keys[i] = NormKey{(unsigned long long)__double_as_longlong(norms[i]), (unsigned)src_nodes[live[i]]};
@@ -376,6 +376,48 @@ __global__ void k_rank_admit(const int32_t* n_dev, const NormKey* __restrict__ s
     retained[j] = admitted && !computed;
     warp_count_add(c + kCtrGradientEvictions, evicted);
     if (evicted) atomicAdd(c + kCtrValid, (unsigned long long)-1ll);
+  }
+}
+
+// sharded cache (hg_shard_cache.cu): the batch-wide admission rank as
+// per-position actions for the owners, in admit-rank order; no cache state
+// is touched here. act 0 = not admitted (owner evicts it if held),
+// 1 = admitted & computed (ring write), 2 = admitted & injected (retained).
+// The rows to be written are staged at req_emb[j] (this rank's IPC-mapped
+// request area: the owners read them from there, never from the tape). One
+// warp per 32 positions: lane-parallel actions, then the warp copies the
+// write rows with 16-byte vectors.
+__global__ void k_request(const int32_t* n_dev, const NormKey* __restrict__ skeys, const int32_t* __restrict__ svals,
+                          const int32_t* __restrict__ live, const uint8_t* __restrict__ computed_flag,
+                          const float* __restrict__ emb, int row_words, int32_t* __restrict__ req_id,
+                          uint8_t* __restrict__ req_act, int32_t* __restrict__ req_src, float* __restrict__ req_emb,
+                          long long* hdr) {
+  pdl_wait();
+  const int n = *n_dev;
+  const long long k = hdr[1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) hdr[0] = n;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int nv = row_words >> 2;
+  for (int j0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; j0 < n; j0 += warps * 32) {
+    const int j = j0 + lane;
+    int loc = 0, act = 0;
+    if (j < n) {
+      loc = live[svals[j]];
+      act = j >= k ? 0 : (computed_flag[loc] ? 1 : 2);
+      req_id[j] = (int32_t)skeys[j].id;
+      req_src[j] = loc;
+      req_act[j] = (uint8_t)act;
+    }
+    unsigned m = __ballot_sync(0xffffffffu, act == 1);
+    while (m) {
+      const int q = __ffs(m) - 1;
+      m &= m - 1;
+      const int ql = __shfl_sync(0xffffffffu, loc, q);
+      const uint4* s = reinterpret_cast<const uint4*>(emb + (long long)ql * row_words);
+      uint4* d = reinterpret_cast<uint4*>(req_emb + (long long)(j0 + q) * row_words);
+      for (int x = lane; x < nv; x += 32) d[x] = s[x];
+    }
   }
 }
 
@@ -545,6 +587,80 @@ long long hg_cache_update_scratch_bytes(long long n_max) {
          4LL * (4 * kNB + 16);
 }
 
+}  // extern "C"
+
+namespace hg {
+namespace {
+struct RankBufs {
+  NormKey *keys_in, *keys_out;
+  int32_t *vals_in, *vals_out, *wlist;
+  uint8_t *wflag, *retained;
+  int* part;
+  void* tmp;
+  size_t tmp_bytes;
+};
+
+RankBufs carve(void* scratch, long long scratch_bytes, long long n_max) {
+  RankBufs b;
+  const long long nn = n_max + 16;
+  char* p = reinterpret_cast<char*>(scratch);
+  b.keys_in = reinterpret_cast<NormKey*>(p);
+  b.keys_out = b.keys_in + nn;
+  b.vals_in = reinterpret_cast<int32_t*>(b.keys_out + nn);
+  b.vals_out = b.vals_in + nn;
+  b.wlist = b.vals_out + nn;
+  b.wflag = reinterpret_cast<uint8_t*>(b.wlist + nn);
+  b.retained = b.wflag + nn;
+  b.part = reinterpret_cast<int*>(b.retained + nn + 16 - ((uintptr_t)(b.retained + nn) & 15));
+  b.tmp = b.part + scan_tiles(n_max) + 4;
+  b.tmp_bytes = (size_t)(scratch_bytes - ((char*)b.tmp - p));
+  return b;
+}
+
+// U1: (norm bits, id) keys of the n live nodes sorted into keys_out /
+// vals_out by the bucket sort (6 launches); *k_out = floor(p_grad * n)
+int bucket_rank(const char* W, const int32_t* n_dev, int n_max, double p_grad, const int32_t* live,
+                const int32_t* src_nodes, const double* norms, long long* k_out, const RankBufs& rb,
+                cudaStream_t stream) {
+  const long long nn = n_max + 16;
+  const size_t need = (size_t)nn * 20 + 64 + 4 * (4 * kNB + 16);
+  const uintptr_t end = reinterpret_cast<uintptr_t>(rb.tmp) + rb.tmp_bytes;
+  char* bp = reinterpret_cast<char*>((end - need - 16) & ~uintptr_t(15));   // 16-byte aligned tail region
+  NormKey* k2 = reinterpret_cast<NormKey*>(bp);
+  int32_t* v2 = reinterpret_cast<int32_t*>(k2 + nn);
+  BucketState* bst = reinterpret_cast<BucketState*>((reinterpret_cast<uintptr_t>(v2 + nn) + 15) & ~uintptr_t(15));
+  int* count = reinterpret_cast<int*>(bst + 1);
+  int* off = count + kNB;
+  int* cursor = off + kNB + 1;
+  int* big = cursor + kNB;
+  HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->lo, 0xFF, 8, stream));
+  HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->hi, 0x00, 8, stream));
+  HG_CHECK_CUDA(W, cudaMemsetAsync(count, 0, 4 * kNB, stream));
+  const unsigned g = grid_for(n_max, 256, 148 * 4);
+#define HG_L(K, G, B, ...)                                                                   \
+  {                                                                                          \
+    const cudaError_t _pe = hg::launch_pdl(K, dim3(G), dim3(B), 0, stream, __VA_ARGS__);     \
+    if (_pe != cudaSuccess) return hg::fail(W, hg::kCuda, cudaGetErrorString(_pe));          \
+    HG_LAUNCHED(W);                                                                          \
+  }
+  // keys -> k2 / v2; bucketed -> keys_in / vals_in; sorted -> keys_out / vals_out
+  HG_L(k_norm_keys, grid_for(n_max, 256), 256, n_dev, n_max, p_grad, live, src_nodes, norms, k2, v2, k_out);
+  HG_L(k_bs_minmax, g, 256, n_dev, (const NormKey*)k2, bst);
+  HG_L(k_bs_hist, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, count);
+  HG_L(k_bs_scan, 1, 1024, (const int*)count, off, cursor, big, bst);
+  HG_L(k_bs_scatter, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, cursor, rb.keys_in, rb.vals_in);
+  HG_L(k_bs_small, 148 * 8, 256, (const int*)off, (const NormKey*)rb.keys_in, (const int32_t*)rb.vals_in,
+       rb.keys_out, rb.vals_out);
+  HG_L(k_bs_big, 64, 256, (const int*)off, (const int*)big, (const BucketState*)bst, rb.keys_in, rb.vals_in, k2, v2,
+       rb.keys_out, rb.vals_out);
+#undef HG_L
+  return kOk;
+}
+}  // namespace
+}  // namespace hg
+
+extern "C" {
+
 // Stage 1 (U1-U3): rank and evict; leaves the write list + n_write on device.
 // n (live nodes) is read from n_dev; n_max sizes the sort (sentinel padding),
 // k = floor(p_grad * n) is computed on the device (cache.py:190).
@@ -555,76 +671,54 @@ int hg_cache_rank(const int32_t* n_dev, int n_max, double p_grad, const int32_t*
   const char* W = "hg_cache_rank";
   if (scratch_bytes < hg_cache_update_scratch_bytes(n_max)) return fail(W, kBadArg, "scratch too small");
   if (n_max <= 0) return kOk;
-  const long long nn = n_max + 16;
-  char* p = reinterpret_cast<char*>(scratch);
-  NormKey* keys_in = reinterpret_cast<NormKey*>(p);
-  NormKey* keys_out = keys_in + nn;
-  int32_t* vals_in = reinterpret_cast<int32_t*>(keys_out + nn);
-  int32_t* vals_out = vals_in + nn;
-  int32_t* wlist = vals_out + nn;
-  uint8_t* wflag = reinterpret_cast<uint8_t*>(wlist + nn);
-  uint8_t* retained = wflag + nn;
-  int* part = reinterpret_cast<int*>(retained + nn + 16 - ((uintptr_t)(retained + nn) & 15));
-  void* tmp = part + scan_tiles(n_max) + 4;
-  size_t tmp_bytes = (size_t)(scratch_bytes - ((char*)tmp - p));
+  const RankBufs rb = carve(scratch, scratch_bytes, n_max);
   const int mode = sort_mode(n_max);
   if (mode == kSortBucket) {
-    // bucket buffers live after the CUB temp area
-    const size_t need = (size_t)nn * 20 + 64 + 4 * (4 * kNB + 16);
-    const uintptr_t end = reinterpret_cast<uintptr_t>(tmp) + tmp_bytes;
-    char* bp = reinterpret_cast<char*>((end - need - 16) & ~uintptr_t(15));   // 16-byte aligned tail region
-    NormKey* k2 = reinterpret_cast<NormKey*>(bp);
-    int32_t* v2 = reinterpret_cast<int32_t*>(k2 + nn);
-    BucketState* bst = reinterpret_cast<BucketState*>((reinterpret_cast<uintptr_t>(v2 + nn) + 15) & ~uintptr_t(15));
-    int* count = reinterpret_cast<int*>(bst + 1);
-    int* off = count + kNB;
-    int* cursor = off + kNB + 1;
-    int* big = cursor + kNB;
-    HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->lo, 0xFF, 8, stream));
-    HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->hi, 0x00, 8, stream));
-    HG_CHECK_CUDA(W, cudaMemsetAsync(count, 0, 4 * kNB, stream));
-    const unsigned g = grid_for(n_max, 256, 148 * 4);
-#define HG_L(K, G, B, ...)                                                                   \
-  {                                                                                          \
-    const cudaError_t _pe = hg::launch_pdl(K, dim3(G), dim3(B), 0, stream, __VA_ARGS__);     \
-    if (_pe != cudaSuccess) return hg::fail(W, hg::kCuda, cudaGetErrorString(_pe));          \
-    HG_LAUNCHED(W);                                                                          \
-  }
-    // keys -> k2 / v2; bucketed -> keys_in / vals_in; sorted -> keys_out / vals_out (read by hg_cache_write)
-    HG_L(k_norm_keys, grid_for(n_max, 256), 256, n_dev, n_max, p_grad, live, src_nodes, norms, k2, v2, layer_ctr);
-    HG_L(k_bs_minmax, g, 256, n_dev, (const NormKey*)k2, bst);
-    HG_L(k_bs_hist, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, count);
-    HG_L(k_bs_scan, 1, 1024, (const int*)count, off, cursor, big, bst);
-    HG_L(k_bs_scatter, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, cursor, keys_in, vals_in);
-    HG_L(k_bs_small, 148 * 8, 256, (const int*)off, (const NormKey*)keys_in, (const int32_t*)vals_in, keys_out,
-         vals_out);
-    HG_L(k_bs_big, 64, 256, (const int*)off, (const int*)big, (const BucketState*)bst, keys_in, vals_in, k2, v2,
-         keys_out, vals_out);
-#undef HG_L
-    { const cudaError_t _pe = hg::launch_pdl(k_rank_admit, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev,
-                                             (const NormKey*)keys_out, (const int32_t*)vals_out, live, computed_flag,
-                                             row_of, row_owner, wflag, retained, layer_ctr);
-      if (_pe != cudaSuccess) return hg::fail(W, hg::kCuda, cudaGetErrorString(_pe)); }
+    const int s = bucket_rank(W, n_dev, n_max, p_grad, live, src_nodes, norms, layer_ctr + kCtrK, rb, stream);
+    if (s) return s;
+  } else {
+    const bool radix = mode == kSortRadix;
+    // the merge sort is in place: keys go straight to keys_out / vals_out
+    HG_CHECK_CUDA(W, hg::launch_pdl(k_norm_keys, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev, n_max,
+                                    p_grad, live, src_nodes, norms, radix ? rb.keys_in : rb.keys_out,
+                                    radix ? rb.vals_in : rb.vals_out, layer_ctr + kCtrK));
     HG_LAUNCHED(W);
-    return scan_launch<int>(W, FlagU8{wflag}, DevCount{n_dev}, n_max, part, EmitCompact{wlist},
-                            StoreNWrite{layer_ctr}, stream);
+    size_t tb = rb.tmp_bytes;
+    cudaError_t e = radix ? cub::DeviceRadixSort::SortPairs(rb.tmp, tb, rb.keys_in, rb.keys_out, rb.vals_in,
+                                                            rb.vals_out, n_max, NormKeyDecomposer{}, stream)
+                          : cub::DeviceMergeSort::SortPairs(rb.tmp, tb, rb.keys_out, rb.vals_out, n_max,
+                                                            NormKeyLess{}, stream);
+    if (e != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(e));
   }
-  const bool radix = mode == kSortRadix;
-  // the merge sort is in place: keys go straight to keys_out / vals_out
-  { const cudaError_t _pe = hg::launch_pdl(k_norm_keys, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev, n_max, p_grad, live, src_nodes, norms,
-                                                        radix ? keys_in : keys_out, radix ? vals_in : vals_out,
-                                                        layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  HG_CHECK_CUDA(W, hg::launch_pdl(k_rank_admit, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev,
+                                  (const NormKey*)rb.keys_out, (const int32_t*)rb.vals_out, live, computed_flag,
+                                  row_of, row_owner, rb.wflag, rb.retained, layer_ctr));
   HG_LAUNCHED(W);
-  cudaError_t e = radix ? cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, vals_out, n_max,
-                                                          NormKeyDecomposer{}, stream)
-                        : cub::DeviceMergeSort::SortPairs(tmp, tmp_bytes, keys_out, vals_out, n_max, NormKeyLess{},
-                                                          stream);
-  if (e != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(e));
-  { const cudaError_t _pe = hg::launch_pdl(k_rank_admit, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev, keys_out, vals_out, live, computed_flag, row_of,
-                                                         row_owner, wflag, retained, layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  return scan_launch<int>(W, FlagU8{rb.wflag}, DevCount{n_dev}, n_max, rb.part, EmitCompact{rb.wlist},
+                          StoreNWrite{layer_ctr}, stream);
+}
+
+// Sharded cache, rank side (hg_shard_cache.cu): the same admission rank,
+// published as (req_id, req_act, req_src, req_emb rows of the writes) in
+// rank order with the header [0] n, [1] k (hdr[2] = it, hdr[3] = expiries:
+// set by the reset / lookup side); the owners apply it. Scratch:
+// hg_cache_update_scratch_bytes.
+int hg_cache_request(const int32_t* n_dev, int n_max, double p_grad, const int32_t* live, const int32_t* src_nodes,
+                     const double* norms, const uint8_t* computed_flag, const float* emb, int row_words,
+                     int32_t* req_id, uint8_t* req_act, int32_t* req_src, float* req_emb, long long* req_hdr,
+                     void* scratch, long long scratch_bytes, cudaStream_t stream) {
+  const char* W = "hg_cache_request";
+  if (scratch_bytes < hg_cache_update_scratch_bytes(n_max)) return fail(W, kBadArg, "scratch too small");
+  if (row_words < 4 || (row_words & 3)) return fail(W, kBadArg, "rows must be a multiple of 4 words");
+  if (n_max <= 0) return kOk;
+  const RankBufs rb = carve(scratch, scratch_bytes, n_max);
+  const int s = bucket_rank(W, n_dev, n_max, p_grad, live, src_nodes, norms, req_hdr + 1, rb, stream);
+  if (s) return s;
+  HG_CHECK_CUDA(W, hg::launch_pdl(k_request, dim3(grid_for((long long)n_max * 32, 256, 148 * 16)), dim3(256), 0,
+                                  stream, n_dev, (const NormKey*)rb.keys_out, (const int32_t*)rb.vals_out, live,
+                                  computed_flag, emb, row_words, req_id, req_act, req_src, req_emb, req_hdr));
   HG_LAUNCHED(W);
-  return scan_launch<int>(W, FlagU8{wflag}, DevCount{n_dev}, n_max, part, EmitCompact{wlist}, StoreNWrite{layer_ctr},
-                          stream);
+  return kOk;
 }
 
 // Stage 2 (U4-U8): ring write into a table of `cap` rows of H floats.

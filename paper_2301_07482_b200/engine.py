@@ -301,6 +301,7 @@ class StepEngine:
             packed = torch.cuda.Event()
             packed.record(self.inj_stream)
         blocks = self._blocks(s)
+        cache.begin_step(self.it, sp)     # owner-sharded cache: peers' previous commits first
 
         # ---- prune walk + lookups (trainer.py:166-207) ----
         counts = torch.empty(2 * L, dtype=torch.int32, device=dev)
@@ -435,6 +436,8 @@ class StepEngine:
         self._mark("sgd", stream)
         for side in self.upd_streams.values():
             stream.wait_stream(side)
+        cache.commit(sp)                  # owner-sharded cache: every rank's requests, in batch order
+        self._mark("cache_committed", stream)
         if ahead:
             stream.wait_stream(self.samp_stream)
         self._mark("joined", stream)

@@ -68,6 +68,9 @@ class TrainConfig:
     feature_placement: str = "hbm"      # "hbm" | "host" (pinned, read through UVA)
     max_capacity: int | None = None     # cache growth limit (see CachePolicy)
     heads: int = 4                      # GAT hidden-layer heads (LayerKind.GAT, oracle/gat.py)
+    # data parallel: "local" = one cache per rank; "owner" = one cache sharded
+    # by node owner over the torch.distributed group (shardcache.py)
+    cache_sharding: str = "local"
 
     def __post_init__(self):
         if len(self.fanouts) == 0 or any(f < 1 for f in self.fanouts):
@@ -80,6 +83,8 @@ class TrainConfig:
             raise ValueError("probe_every must be >= 0")
         if self.feature_placement not in ("hbm", "host"):
             raise ValueError("feature_placement must be 'hbm' or 'host'")
+        if self.cache_sharding not in ("local", "owner"):
+            raise ValueError("cache_sharding must be 'local' or 'owner'")
 
 
 @dataclass
@@ -389,8 +394,22 @@ class Trainer:
                                     in_pad=self.feature_dim)
         policy = CachePolicy(cfg.p_grad, cfg.t_stale, cfg.capacity, cfg.max_capacity)
         feature_rows = self.graph.num_nodes // 10 if cfg.feature_rows is None else cfg.feature_rows
-        self.cache = HistCache(self.graph.num_nodes, [cfg.hidden] * (depth - 1), policy, feature_rows=feature_rows,
-                               refresh_retained=cfg.refresh_retained, dtype=cfg.dtype, device=self.device)
+        if cfg.cache_sharding == "owner":
+            import torch.distributed as dist
+            from .sampler import layer_bounds
+            from .shardcache import ShardedHistCache
+            if not dist.is_initialized():
+                raise ValueError("cache_sharding='owner' needs an initialised torch.distributed process group")
+            F, _ = layer_bounds(cfg.batch_size, cfg.fanouts, self.graph.num_nodes)
+            n_req = [F[depth - l] for l in range(1, depth)]     # sources of block l bound its live set
+            self.cache = ShardedHistCache(self.graph.num_nodes, [cfg.hidden] * (depth - 1), policy, n_req,
+                                          dist.get_rank(), dist.get_world_size(), feature_rows=feature_rows,
+                                          refresh_retained=cfg.refresh_retained, dtype=cfg.dtype,
+                                          device=self.device)
+        else:
+            self.cache = HistCache(self.graph.num_nodes, [cfg.hidden] * (depth - 1), policy,
+                                   feature_rows=feature_rows, refresh_retained=cfg.refresh_retained, dtype=cfg.dtype,
+                                   device=self.device)
         if feature_rows > 0:
             self.cache.backfill_features(self.features, graph=self.graph)
         self.plan = SamplePlan(cfg.fanouts, cfg.batch_size, cfg.seed)
@@ -594,6 +613,8 @@ class Trainer:
         stream = torch.cuda.current_stream(dev)
         sp = _lib.stream_ptr(stream)
         net, cache, cfg = self.network, self.cache, self.cfg
+        it_dev = torch.tensor([int(iteration)], dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
+        cache.begin_step(it_dev, sp)
         pruned = prune_with_cache(sub, cache, iteration, stream)
         h0, baseline = self._load_input(pruned, iteration, stream)
         L = sub.num_layers
@@ -620,7 +641,6 @@ class Trainer:
             norms[l] = nrm
             d_h = d_prev
         apply_sgd(self.grad_hook, net, grads, cfg.eta)   # e.g. NCCL all-reduce of the flat bucket, then SGD
-        it_dev = torch.tensor([int(iteration)], dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
         for layer in range(1, L):
             n_live = pruned.counts[layer][1]
             if n_live == 0:
@@ -628,6 +648,7 @@ class Trainer:
             cache._layer(layer).update_dev(pruned.n_live_dev(layer), n_live, pruned.layer_live[layer],
                                            sub.layers[layer].src_nodes, norms[layer], pruned.keep[layer - 1],
                                            tapes[layer - 1].h_out, it_dev, cache.refresh_retained, sp)
+        cache.commit(sp)                 # owner-sharded cache: apply every rank's requests (no-op otherwise)
         cache.end_iteration(iteration)
         self.last = (pruned, tapes, grads, norms)
         return loss_dev, baseline
