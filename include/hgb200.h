@@ -104,8 +104,12 @@ int hg_load_features_sharded(const int32_t* n_live_dev, long long n_live_max, co
                              const int32_t* src_nodes, const int32_t* feature_row_of, const void* region,
                              const void* const* shard_ptrs, const long long* shard_bounds, int num_shards,
                              int local_shard, int dim, int dtype, float* h_out, long long* global_ctr,
-                             cudaStream_t stream);
-/* shard allocation and CUDA IPC export/open/close of peer shards */
+                             long long* owner_rows, cudaStream_t stream);
+/* owner_rows (int64[P] or NULL): rows read from each owner's shard, the
+ * transfer sizes of comms.py:326-337 (requests_for_batch) taken from the real
+ * reads; the accounting of comms.py:283-323 is derived from them on the host
+ * (distributed.transfer_accounting).
+ * shard allocation and CUDA IPC export/open/close of peer shards */
 int hg_device_alloc(long long bytes, void** out);
 int hg_device_free(void* p);
 long long hg_ipc_handle_bytes(void);
@@ -278,6 +282,21 @@ int hg_cache_apply(const long long* req_hdr, const int32_t* req_id, const uint8_
                    long long scratch_bytes, cudaStream_t stream);
 int hg_peer_signal(unsigned long long* my_flag, unsigned long long* state, cudaStream_t stream);
 int hg_peer_wait(unsigned long long* const* flags, int P, unsigned long long* state, cudaStream_t stream);
+
+/* ---- dataset ingest, host side (csrc/hg_ingest.cu):
+ * multi-threaded parsers of the reference's text formats over a read-only
+ * mapping of the file. Call once with out / src / dst = NULL to count, then
+ * with arrays of *count entries. On bad input *err = kind (1 not an integer,
+ * 2 negative, 3 out of range, 4 wrong field count) and *err_line = the first
+ * offending line (1-based); the caller words the message like the reference.
+ * hg_parse_int_lines: histgnn/data.py:109-129 (_read_int_lines); upper < 0 =
+ *   unbounded; *err_val = the offending value.
+ * hg_parse_edge_list: histgnn/graphs.py:186-218 (read_edge_list): "src dst"
+ *   lines, '#' comments; ids parsed into int32 (device id width). */
+int hg_parse_int_lines(const char* path, long long upper, int64_t* out, long long* count, int* err,
+                       long long* err_line, long long* err_val, int nthreads);
+int hg_parse_edge_list(const char* path, int32_t* src, int32_t* dst, long long* count, long long* max_src,
+                       long long* max_dst, int* err, long long* err_line, int nthreads);
 
 /* ---- static feature region: histgnn/cache.py:338-351 (backfill_features) */
 long long hg_degree_order_scratch_bytes(long long n);

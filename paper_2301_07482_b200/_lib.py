@@ -23,6 +23,7 @@ I64 = ctypes.c_longlong
 U64 = ctypes.c_ulonglong
 F64 = ctypes.c_double
 F32 = ctypes.c_float
+S = ctypes.c_char_p
 
 # name -> (restype, argtypes); mirrors include/hgb200.h
 SIGNATURES = {
@@ -43,7 +44,7 @@ SIGNATURES = {
     "hg_cache_lookup": (I32, [P, I64, P, P, I64, P, P, P, P, F64, P, P, P, P]),
     "hg_load_features_scratch_bytes": (I64, [I64]),
     "hg_load_features": (I32, [P, I64, P, P, P, P, P, I32, I32, P, P, P, I64, P]),
-    "hg_load_features_sharded": (I32, [P, I64, P, P, P, P, P, P, I32, I32, I32, I32, P, P, P]),
+    "hg_load_features_sharded": (I32, [P, I64, P, P, P, P, P, P, I32, I32, I32, I32, P, P, P, P]),
     "hg_device_alloc": (I32, [I64, P]),
     "hg_device_free": (I32, [P]),
     "hg_ipc_handle_bytes": (I64, []),
@@ -83,6 +84,8 @@ SIGNATURES = {
     "hg_degree_order_scratch_bytes": (I64, [I64]),
     "hg_feature_region": (I32, [P, P, I64, I64, P, P, P, I64, P]),
     "hg_synth_power_law": (I64, [I64, I32, P, P, P]),
+    "hg_parse_int_lines": (I32, [S, I64, P, P, P, P, P, I32]),
+    "hg_parse_edge_list": (I32, [S, P, P, P, P, P, P, P, I32]),
     "hg_ts_bytes": (I64, [I64, I32]),
     "hg_ts_pack": (I32, [P, I64, I32, I32, I32, I64, P, P]),
     "hg_ts_linear_fwd": (I32, [P, I64, P, I32, P, I32, P, I32, P, P]),

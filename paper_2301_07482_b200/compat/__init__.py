@@ -14,9 +14,10 @@ subpackage converts at the boundary:
   histgnn.cache    -> compat.cache    (the device HistCache, numpy views)
   histgnn.nn       -> compat.nn       (reference-shaped LayerParams / Network)
   histgnn.trainer  -> compat.trainer  (prune_with_cache / Trainer on the GPU)
+  histgnn.data     -> compat.data     (dataset format; native multi-threaded parsers)
 
 A reference user (or the reference's own test-suite, `tools/
 run_reference_tests.py`) changes only the import line.
 """
 
-from . import cache, graphs, nn, sampler, trainer  # noqa: F401
+from . import cache, data, graphs, nn, sampler, trainer  # noqa: F401

@@ -48,6 +48,7 @@ struct Shards {
   const long long* bounds;    // device array [P + 1]
   int P;
   int local;                  // index of this GPU's own shard (remote-row accounting)
+  unsigned long long* owner_rows;   // [P] rows read per owner shard (NULL = not counted)
 };
 constexpr int kMaxShards = 16;
 
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_load_rows(const int32_t* n_l
   for (; b * 32 < n; b += W) {
     __syncwarp();
     bool remote = false;
+    int own = -1;
     if (kShard) {
       const TIn* src = region + (long long)fr * dim;
       if (fr < 0) {
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_load_rows(const int32_t* n_l
         while (o + 1 < sh.P && id >= s_bound[o + 1]) ++o;
         src = s_shard[o] + (long long)(id - s_bound[o]) * dim;
         remote = ok && o != sh.local;
+        own = ok ? o : -1;
       }
       s_row[wib][lane] = src;
     } else {
@@ -146,6 +149,12 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_load_rows(const int32_t* n_l
       if (hits) atomicAdd(gctr + kGCtrFeatureHits, (unsigned long long)__popc(hits));
       if (valid & ~hits) atomicAdd(gctr + kGCtrFeatureMisses, (unsigned long long)__popc(valid & ~hits));
       if (remotes) atomicAdd(gctr + kGCtrRemoteRows, (unsigned long long)__popc(remotes));
+    }
+    if (kShard && sh.owner_rows) {   // per-owner transfer sizes (comms.py:326-337 requests_for_batch)
+      for (int o = 0; o < sh.P; ++o) {
+        const unsigned m = __ballot_sync(0xffffffffu, own == o);
+        if (lane == 0 && m) atomicAdd(sh.owner_rows + o, (unsigned long long)__popc(m));
+      }
     }
   }
   kt_end(kt);
@@ -330,7 +339,7 @@ int hg_load_features(const int32_t* n_live_dev, long long n_live_max, const int3
 #define HG_LOAD(TT, U)                                                                                            \
   (void)hg::launch_pdl(k_load_rows<TT, U, false>, dim3(grid), dim3(kWarps * 32), 0, stream, n_live_dev, live,   \
                        src_nodes, feature_row_of, static_cast<const TT*>(region), static_cast<const TT*>(feats),  \
-                       dim, h_out, g, Shards{nullptr, nullptr, 0, 0})
+                       dim, h_out, g, Shards{nullptr, nullptr, 0, 0, nullptr})
   if (dtype == 1) HG_LOAD(__half, 6); else HG_LOAD(float, 8);
 #undef HG_LOAD
   HG_LAUNCHED(W);
@@ -344,7 +353,7 @@ int hg_load_features_sharded(const int32_t* n_live_dev, long long n_live_max, co
                              const int32_t* src_nodes, const int32_t* feature_row_of, const void* region,
                              const void* const* shard_ptrs, const long long* shard_bounds, int num_shards,
                              int local_shard, int dim, int dtype, float* h_out, long long* global_ctr,
-                             cudaStream_t stream) {
+                             long long* owner_rows, cudaStream_t stream) {
   const char* W = "hg_load_features_sharded";
   const int isz = dtype == 1 ? 2 : 4;
   if ((dim * isz) % 16) return fail(W, kBadArg, "feature row bytes must be a multiple of 16");
@@ -353,7 +362,8 @@ int hg_load_features_sharded(const int32_t* n_live_dev, long long n_live_max, co
   if (reinterpret_cast<uintptr_t>(h_out) & 15) return fail(W, kBadArg, "output must be 16-byte aligned");
   auto* g = reinterpret_cast<unsigned long long*>(global_ctr);
   const unsigned grid = grid_for((n_live_max + 31) / 32, kWarps, 148 * 4);
-  const Shards sh{shard_ptrs, shard_bounds, num_shards, local_shard};
+  const Shards sh{shard_ptrs, shard_bounds, num_shards, local_shard,
+                  reinterpret_cast<unsigned long long*>(owner_rows)};
   if (dtype == 1)
     { const cudaError_t _pe = hg::launch_pdl(k_load_rows<__half, 6, true>, dim3(grid), dim3(kWarps * 32), 0, stream, n_live_dev, live, src_nodes, feature_row_of,
                                                                   static_cast<const __half*>(region), nullptr, dim,

@@ -158,3 +158,26 @@ def apply_sgd(hook, network, grads, eta: float) -> None:
     if hook is not None:
         hook(grads)
     sgd_step(network, grads, eta)
+
+
+INDEX_BYTES_PER_ID = 8     # histgnn/comms.py:26 (two-sided: the requester ships its id list)
+
+
+def transfer_accounting(owner_rows, rank: int, row_bytes: int) -> dict:
+    """The feature-fetch accounting of histgnn/comms.py:283-323 (simulate_fetch)
+    computed from the rows this rank really read from each owner's shard
+    (ShardedFeatures.owner_rows deltas): one transfer per remote owner with
+    rows (requests_for_batch / merge_transfers, comms.py:187-194,326-337),
+    payload = rows x row_bytes; one-sided reads move only the payload, the
+    two-sided protocol adds the id list (8 B per id) and one synchronisation
+    per transfer. Round scheduling / completion time model a PCIe switch tree
+    and are not applicable to NVSwitch."""
+    rows = [int(x) for x in (owner_rows.tolist() if hasattr(owner_rows, "tolist") else owner_rows)]
+    transfers = [(o, rank, n) for o, n in enumerate(rows) if o != rank and n > 0]
+    payload = sum(n for _, _, n in transfers) * int(row_bytes)
+    index = sum(n for _, _, n in transfers) * INDEX_BYTES_PER_ID
+    return {"transfers": [{"src": s, "dst": d, "num_ids": n} for s, d, n in transfers],
+            "one_sided": {"payload_bytes": payload, "index_bytes": 0, "sync_events": 0, "total_bytes": payload},
+            "two_sided": {"payload_bytes": payload, "index_bytes": index, "sync_events": len(transfers),
+                          "total_bytes": payload + index},
+            "local_rows": rows[rank] if 0 <= rank < len(rows) else 0}

@@ -62,6 +62,9 @@ class ShardedFeatures:
         self._owned = owned          # hg_device_alloc pointer of the local shard (IPC mode)
         self._opened = list(opened)  # IPC mappings of peer shards
         self.local_rows = None       # tensor view of this rank's own shard
+        # rows read per owner shard (cumulative; the real transfer sizes behind
+        # distributed.transfer_accounting, comms.py:283-337)
+        self.owner_rows = torch.zeros(self.num_shards, dtype=torch.int64, device=self.device)
 
     # ---- tensor-like surface used by Trainer / cache.backfill_features ----
     @property
@@ -141,11 +144,13 @@ class ShardedFeatures:
             self._owned = None
 
     # ---- row access ----
-    def load_rows(self, n_live_dev, n_max: int, live, src_nodes, feature_row_of, region, out, gctr, stream):
+    def load_rows(self, n_live_dev, n_max: int, live, src_nodes, feature_row_of, region, out, gctr, stream,
+                  count: bool = True):
         """hg_load_features_sharded: out[live[i]] = fp32(row of src_nodes[live[i]])."""
         _lib.call("hg_load_features_sharded", _lib.ptr(n_live_dev), int(n_max), _lib.ptr(live), _lib.ptr(src_nodes),
                   _lib.ptr(feature_row_of), _lib.ptr(region), _lib.ptr(self.ptrs_dev), _lib.ptr(self.bounds_dev),
-                  self.num_shards, self.local_shard, self.dim, self.dtype_code, _lib.ptr(out), _lib.ptr(gctr), stream)
+                  self.num_shards, self.local_shard, self.dim, self.dtype_code, _lib.ptr(out), _lib.ptr(gctr),
+                  _lib.ptr(self.owner_rows) if count else None, stream)
 
     def index_select(self, dim: int, ids: torch.Tensor, chunk: int = 1 << 22) -> torch.Tensor:
         """rows[ids] in the table's dtype (device), read through the shards
@@ -163,6 +168,6 @@ class ShardedFeatures:
             tmp = torch.empty((n, self.dim), dtype=torch.float32, device=self.device)
             live = torch.arange(n, dtype=torch.int32, device=self.device)
             cnt = torch.tensor([n], dtype=torch.int32, device=self.device)
-            self.load_rows(cnt, n, live, ids[a:b].contiguous(), None, None, tmp, gctr, sp)
+            self.load_rows(cnt, n, live, ids[a:b].contiguous(), None, None, tmp, gctr, sp, count=False)
             out[a:b] = tmp.to(self.dtype)      # fp16 -> fp32 -> fp16 is exact
         return out

@@ -314,6 +314,33 @@ def gen_evaluate():
     np.savez_compressed(os.path.join(HERE, "evaluate.npz"), **out)
 
 
+def gen_probes():
+    """trainer.py:231-272,345-358: estimation-error and drift probes of a
+    cache-everything run (p_grad 1, t_stale inf): every admission decision is
+    independent of the gradient norms, so a free-running GPU trainer follows
+    the same integer trajectory and its probes are comparable value for value."""
+    out = dict(META)
+    ds, g = small_powerlaw()
+    for kind in (LayerKind.SAGE_MEAN, LayerKind.GCN):
+        cfg = TrainConfig(fanouts=(4, 4), hidden=16, batch_size=64, epochs=2, eta=0.1, kind=kind, p_grad=1.0,
+                          t_stale=math.inf, probe_every=1, seed=3)
+        tr = Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes,
+                     probe_nodes=np.arange(0, ds.features.shape[0], 7))
+        ms = tr.train()
+        k = f"{kind.value}_"
+        names = [f for f in ms[0].__dict__ if f not in ("loss", "estimation_error")]
+        out[k + "ints"] = np.array([[getattr(m, f) for f in names] for m in ms], np.int64)
+        out[k + "loss"] = np.array([m.loss for m in ms])
+        out[k + "est"] = np.array([m.estimation_error for m in ms])
+        its = sorted(tr.embedding_log.records)
+        pairs = [(t, s) for t in its[-3:] for s in (0, 1, 5, 20) if t - s in tr.embedding_log.records]
+        out[k + "sim_pairs"] = np.array(pairs, np.int64)
+        out[k + "sim"] = np.array([tr.embedding_log.similarity(t, s) for t, s in pairs])
+        out[k + "log_ids_last"] = tr.embedding_log.records[its[-1]][0]
+    out["int_names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "probes.npz"), **out)
+
+
 def gen_datagen():
     out = dict(META)
     ds = synth_power_law(2000, np.random.default_rng(4), m=4, feature_dim=8, classes=5)
@@ -329,7 +356,7 @@ def gen_datagen():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["datagen", "sampler", "cache", "prune_nn", "trainer", "c1", "evaluate"]
+    which = sys.argv[1:] or ["datagen", "sampler", "cache", "prune_nn", "trainer", "c1", "evaluate", "probes"]
     for w in which:
         print("generating", w, flush=True)
         globals()["gen_" + w]()

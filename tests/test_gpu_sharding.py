@@ -143,3 +143,63 @@ def test_virtual_shards_engine_other_layer_kinds(kind):
         ms = [tr.train_step(i, 0, s, next_batch=(i + 1, b[i + 1]) if i + 1 < len(b) else None) for i, s in enumerate(b)]
         runs.append(([(m.loss, m.hits, m.admissions, m.feature_hits) for m in ms], tr.network.checksum_bytes()))
     assert runs[0] == runs[1]
+
+
+@pytest.mark.parametrize("P", [3, 8])
+def test_owner_row_counters_give_the_reference_transfer_accounting(P):
+    """Per-owner rows read by the sharded gather == requests_for_batch of the
+    iteration's fetched ids (comms.py:326-349, restated in oracle/comms.py),
+    and the one-/two-sided byte accounting (comms.py:283-323) follows."""
+    import paper_2301_07482_b200 as hg
+    from oracle.comms import fetch_bytes, merge_transfers, partition_features, requests_for_batch
+    from paper_2301_07482_b200.distributed import transfer_accounting
+    ds, g = _data()
+    sf = hg.ShardedFeatures.virtual(ds.features, P)
+    tr = hg.Trainer(g, sf, ds.labels, ds.train_ids, _cfg(hg), ds.num_classes)
+    batches = hg.make_batches(ds.train_ids, tr.cfg)
+    owner = partition_features(ds.num_nodes, P)
+    region = tr.cache.feature_row_of >= 0
+    for i in range(5):
+        before = sf.owner_rows.clone()
+        sub = tr.sample(i, batches[i])
+        m = tr.train_iteration(i, 0, sub)
+        pruned = tr.last[0]
+        ids = sub.layers[0].src_nodes[pruned.layer_live[0]].cpu().numpy().astype(np.int64)
+        fetched = ids[~region[ids]]
+        assert len(fetched) == m.feature_misses
+        counts = (sf.owner_rows - before).cpu().numpy()
+        np.testing.assert_array_equal(counts, np.bincount(owner[fetched], minlength=P))
+        acc = transfer_accounting(counts, sf.local_shard, tr.row_bytes)
+        want = merge_transfers(requests_for_batch(owner, fetched, sf.local_shard))
+        assert [(t["src"], t["dst"], t["num_ids"]) for t in acc["transfers"]] == want
+        assert acc["two_sided"] == fetch_bytes(want, True, tr.row_bytes)
+        assert acc["one_sided"]["payload_bytes"] + acc["local_rows"] * tr.row_bytes == m.fetched_bytes
+
+
+def test_ingest_device_matches_in_memory_training(tmp_path):
+    """A dataset written in the reference's directory format and ingested
+    into the device layout (native parsers, CSR2 on the GPU, features
+    streamed to HBM / pinned host / fp16) trains exactly like the same
+    dataset built in memory."""
+    import torch
+    import paper_2301_07482_b200 as hg
+    from paper_2301_07482_b200.compat.data import Dataset, save_dataset
+    from paper_2301_07482_b200.compat.graphs import CooGraph
+    from paper_2301_07482_b200.ingest import ingest_device
+    ds, g = _data()
+    save_dataset(tmp_path, Dataset(CooGraph(ds.src, ds.dst, ds.num_nodes), ds.features, ds.labels, ds.train_ids,
+                                   ds.val_ids, ds.test_ids))
+    tr0, m0 = _run(hg, g, ds.features, ds)
+    for placement, dtype in (("hbm", torch.float32), ("host", torch.float32), ("hbm", torch.float16)):
+        dd = ingest_device(tmp_path, placement=placement, dtype=dtype)
+        assert torch.equal(dd.graph.col_indices.cpu(), torch.as_tensor(g[2]).to(torch.int32))
+        np.testing.assert_array_equal(dd.graph.end.cpu().numpy(), g[1])
+        want = torch.from_numpy(ds.features).to(dtype)
+        assert torch.equal(dd.features.cpu(), want)
+        if dtype == torch.float32:
+            tr = hg.Trainer(dd.graph, dd.features, dd.labels, dd.train_ids, _cfg(hg, feature_placement=placement),
+                            dd.num_classes)
+            batches = hg.make_batches(dd.train_ids, tr.cfg)
+            m1 = [tr.train_iteration(i, 0, tr.sample(i, batches[i])) for i in range(6)]
+            assert [a == b for a, b in zip(m0, m1)] == [True] * 6
+            assert tr.network.checksum_bytes() == tr0.network.checksum_bytes()

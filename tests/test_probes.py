@@ -108,3 +108,39 @@ def test_similarity_edge_cases_against_a_set_restatement():
             for s in range(t + 1):
                 got, want = log.similarity(t, s), slow(log, t, s)
                 assert (math.isnan(got) and math.isnan(want)) or got == pytest.approx(want, abs=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["sage_mean", "gcn"])
+def test_probes_match_reference_golden(kind):
+    """Free-running GPU trainer vs the reference's own probe values
+    (tests/golden/probes.npz, make_golden.py gen_probes): a cache-everything
+    run (p_grad 1, t_stale inf) whose admissions never depend on the norms,
+    so the integer trajectory is identical and the estimation errors
+    (trainer.py:345-358) and drift similarities (trainer.py:253-272) agree
+    value for value within fp32 tolerance."""
+    import os
+    import paper_2301_07482_b200 as hg
+    from oracle.datagen import csr2_from_edges, power_law_dataset
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "probes.npz"))
+    ds = power_law_dataset(3000, np.random.default_rng(0), m=4, feature_dim=16)
+    g = csr2_from_edges(ds.src, ds.dst, ds.num_nodes)
+    lk = {"sage_mean": hg.LayerKind.SAGE_MEAN, "gcn": hg.LayerKind.GCN}[kind]
+    cfg = hg.TrainConfig(fanouts=(4, 4), hidden=16, batch_size=64, epochs=2, eta=0.1, kind=lk, p_grad=1.0,
+                         t_stale=math.inf, probe_every=1, seed=3)
+    tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, cfg, ds.num_classes,
+                    probe_nodes=np.arange(0, ds.num_nodes, 7))
+    ms = tr.train()
+    names = list(z["int_names"])
+    np.testing.assert_array_equal(np.array([[getattr(m, f) for f in names] for m in ms], np.int64),
+                                  z[f"{kind}_ints"])
+    np.testing.assert_allclose([m.loss for m in ms], z[f"{kind}_loss"], rtol=1e-3)
+    est = np.array([m.estimation_error for m in ms])
+    want = z[f"{kind}_est"]
+    assert est[0] == 0.0 and want[0] == 0.0
+    np.testing.assert_allclose(est, want, rtol=1e-3, atol=1e-6)
+    pairs = z[f"{kind}_sim_pairs"]
+    sim = np.array([tr.embedding_log.similarity(int(t), int(s)) for t, s in pairs])
+    np.testing.assert_allclose(sim, z[f"{kind}_sim"], rtol=1e-4, atol=1e-6, equal_nan=True)
+    last = max(tr.embedding_log.records)
+    np.testing.assert_array_equal(tr.embedding_log.records[last][0], z[f"{kind}_log_ids_last"])

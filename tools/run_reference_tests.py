@@ -8,10 +8,10 @@ the drop-in, changing only the import lines.
 `stage` copies the selected reference test modules into
 `baseline/_ref/reference_tests/` (git-ignored, travels to the GPU box with
 the installed reference) and rewrites every `from histgnn.<m> import ...`
-with m in {graphs, sampler, cache, nn, trainer}: the names the drop-in's
+with m in {graphs, sampler, cache, nn, trainer, data}: the names the drop-in's
 reference-typed facade (`paper_2301_07482_b200.compat.<m>`) provides come
 from it, anything else (e.g. `normalize_adjacency`, the layer-math
-functions) stays on the reference. Data generators (`histgnn.data`), the
+functions, the synthetic generators) stays on the reference. The
 communication simulator and SGC stay on the reference untouched: they are
 test inputs / out-of-scope subsystems.
 
@@ -31,8 +31,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF_TESTS = "/root/reference/pkg/tests"
 REF_PKG = os.path.join(ROOT, "baseline", "_ref")
 OUT = os.path.join(REF_PKG, "reference_tests")
-MODULES = ("test_sampler.py", "test_cache.py", "test_trainer.py", "test_graphs.py", "test_acceptance.py")
-FACADE = ("graphs", "sampler", "cache", "nn", "trainer")
+MODULES = ("test_sampler.py", "test_cache.py", "test_trainer.py", "test_graphs.py", "test_data.py",
+           "test_acceptance.py")
+FACADE = ("graphs", "sampler", "cache", "nn", "trainer", "data")
 
 # node-id fragment -> reason (kept out of the run; everything else must pass)
 DESELECT = {
