@@ -46,6 +46,13 @@ int hg_graph_exec_destroy(void* exec);
  * u64[8 * 8] (per timer: start=~0, end, total_ns, launches, ...), NULL = off.
  * Timer 0 = k_load_rows, 1 = k_aggregate, 2 = k_transpose_agg, 3 = k_select. */
 int hg_set_kernel_timers(void* buf);
+/* IterMetrics row of one step (trainer.py:86-104,407-421), written on the
+ * device at the end of the step: out = [*loss, vecs[...] - prev (prev := now),
+ * vecs[l][valid_idx] for the nvec-1 layer vectors, *n_src0, counts[0..n)];
+ * vecs / lens: device arrays of the counter vectors (layers, then global). */
+int hg_metrics_row(const long long* const* vecs, const int* lens, int nvec, long long* prev, const double* loss,
+                   const int32_t* n_src0, const int32_t* counts, int ncounts, int valid_idx, double* out,
+                   cudaStream_t stream);
 
 /* ---- K1+K2 sampler: histgnn/sampler.py:118-163 (_sample_in_neighbors,
  * _build_block), called per layer by sampler.py:166-190 (sample_layered).
@@ -122,6 +129,21 @@ int hg_ipc_close(void* p);
 int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
                      const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
                      const float* h_in, int d, void* A_ts, cudaStream_t stream);
+/* K5 fused into K6 (layer 0): hg_resolve_feature_rows writes rowp[live[i]]
+ * = the address of live source i's feature row (static region row, table row
+ * or owner-shard row over NVLink; shard_ptrs NULL = unsharded `feats`) with
+ * hg_load_features' accounting; hg_aggregate_fwd_rows aggregates layer 0
+ * reading those rows in place (dtype 0 fp32 / 1 fp16, d = padded width), so
+ * no fp32 copy of the input frontier is materialised. Bit-identical to
+ * hg_load_features + hg_aggregate_fwd. */
+int hg_resolve_feature_rows(const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
+                            const int32_t* src_nodes, const int32_t* feature_row_of, const void* region,
+                            const void* feats, const void* const* shard_ptrs, const long long* shard_bounds,
+                            int num_shards, int local_shard, int dim, int dtype, unsigned long long* rowp,
+                            long long* global_ctr, long long* owner_rows, cudaStream_t stream);
+int hg_aggregate_fwd_rows(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
+                          const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
+                          const unsigned long long* rowp, int dtype, int d, void* A_ts, cudaStream_t stream);
 
 /* ---- K7 on tcgen05 over TS operands (bf16 hi/lo core-matrix tiles in HBM, written by
  * hg_aggregate_fwd / hg_gather_dz / hg_ts_pack; layout in csrc/hg_ts.cuh). Each K-chunk
@@ -194,11 +216,13 @@ int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t
                  unsigned* vals_sorted, int32_t* seg_lo, int32_t* seg_hi, void* scratch, long long scratch_bytes,
                  cudaStream_t stream);
 /* K8 + K9 fused: transposed aggregation + nn.py:346-349 (node_grad_norms) */
+/* need_row (uint8 per source row, may be NULL): rows with 0 get their fp64
+ * norm only, no gradient row (the next layer does not compute them) */
 int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
                      const int32_t* seg_lo, const int32_t* seg_hi, const unsigned* vals_sorted, const int32_t* rows,
                      const int32_t* start, const int32_t* end, const int32_t* dst_deg, const int32_t* src_deg,
                      const int32_t* n_dst_dev, const int32_t* pos_of, const float* SG, int ldSG, int d,
-                     float* d_in, double* norms, cudaStream_t stream);
+                     float* d_in, double* norms, const uint8_t* need_row, cudaStream_t stream);
 int hg_row_norms(const float* x, long long n, int d, double* out, cudaStream_t stream);
 
 /* ---- K11 optimizer: nn.py:355-360 (sgd_step) */

@@ -287,6 +287,7 @@ class HistCache:
         self.feature_table = None              # device tensor [k, d] (features dtype)
         self.feature_row_of_dev = torch.full((num_nodes,), -1, dtype=torch.int32, device=self.device)
         self.gctr = torch.zeros(GLOBAL_CTR_LEN, dtype=torch.int64, device=self.device)
+        self._ops = 0      # numpy-API calls that moved counters (engine metric snapshots re-sync on change)
 
     sharded = False
 
@@ -322,6 +323,7 @@ class HistCache:
         expired entries are invalidated and reported as misses."""
         ids = np.asarray(ids, dtype=np.int64)
         dev = self.device
+        self._ops += 1
         if layer == 0:
             idx = torch.as_tensor(ids, device=dev)
             rows = self.feature_row_of_dev[idx]
@@ -354,6 +356,7 @@ class HistCache:
         """Admission/eviction for one layer after a finished iteration (cache.py:289-322)."""
         batch_nodes = np.asarray(batch_nodes, dtype=np.int64)
         normal_nodes = np.asarray(normal_nodes, dtype=np.int64)
+        self._ops += 1
         if len(batch_nodes) == 0:
             return
         if embeddings.shape[0] != len(batch_nodes):

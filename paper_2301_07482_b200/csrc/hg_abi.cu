@@ -28,6 +28,29 @@ __global__ void k_mark_time(unsigned long long* slot) {
   *slot = t;
 }
 
+// one step's IterMetrics source row (trainer.py:86-104,407-421) written by
+// the device at the end of the step: [loss, counter deltas since the previous
+// row (prev updated in place), per-layer valid entries, n_src of block 0,
+// the prune counts]; the host reads it with one async copy
+__global__ void k_metrics_row(const long long* const* __restrict__ vecs, const int* __restrict__ lens, int nvec,
+                              long long* __restrict__ prev, const double* loss, const int32_t* n_src0,
+                              const int32_t* __restrict__ counts, int ncounts, int valid_idx, double* __restrict__ out) {
+  int nv = 0;
+  for (int v = 0; v < nvec; ++v) nv += lens[v];
+  if (threadIdx.x == 0) out[0] = *loss;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    int v = 0, o = i;
+    while (o >= lens[v]) o -= lens[v++];
+    const long long cur = vecs[v][o];
+    out[1 + i] = (double)(cur - prev[i]);
+    prev[i] = cur;
+  }
+  const int nl = nvec - 1;   // every vector but the last (global) is a layer
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) out[1 + nv + l] = (double)vecs[l][valid_idx];
+  if (threadIdx.x == 0) out[1 + nv + nl] = (double)*n_src0;
+  for (int c = threadIdx.x; c < ncounts; c += blockDim.x) out[2 + nv + nl + c] = (double)counts[c];
+}
+
 bool pdl_enabled() {
   static const bool v = [] {
     const char* e = std::getenv("HG_PDL");
@@ -90,6 +113,14 @@ long long hg_kernel_launches(void) { return hg::g_launches.load(std::memory_orde
 int hg_mark_time(unsigned long long* slot, cudaStream_t stream) {
   hg::k_mark_time<<<1, 1, 0, stream>>>(slot);
   return hg::check_launch("hg_mark_time");
+}
+
+int hg_metrics_row(const long long* const* vecs, const int* lens, int nvec, long long* prev, const double* loss,
+                   const int32_t* n_src0, const int32_t* counts, int ncounts, int valid_idx, double* out,
+                   cudaStream_t stream) {
+  if (nvec < 1) return hg::fail("hg_metrics_row", hg::kBadArg, "no counter vectors");
+  hg::k_metrics_row<<<1, 64, 0, stream>>>(vecs, lens, nvec, prev, loss, n_src0, counts, ncounts, valid_idx, out);
+  return hg::check_launch("hg_metrics_row");
 }
 
 // a CUDA graph replay re-executes the n hg kernels recorded at its capture

@@ -89,7 +89,7 @@ struct KTimer {
   unsigned long long start, end, total_ns, launches, done, pad[3];
 };
 enum TimerId : int { kTLoadRows = 0, kTAggregate = 1, kTTransposeAgg = 2, kTSelect = 3, kTGemmFwd = 4, kTGemmBwd = 5, kTGemmWgrad = 6,
-                     kNumTimers = 8 };
+                     kTAggregateFeat = 7, kNumTimers = 8 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;

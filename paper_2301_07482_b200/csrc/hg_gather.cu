@@ -160,6 +160,62 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_load_rows(const int32_t* n_l
   kt_end(kt);
 }
 
+// Layer-0 input by reference (K5 fused into K6): instead of copying every
+// live source's feature row into an fp32 matrix, resolve its address once
+// (region row, local table row, or owner shard row) into rowp[loc]; the
+// layer-0 aggregation (k_aggregate<kSrc = 1 / 2>) reads the rows in place.
+// Same I/O accounting as k_load_rows (feature hits / misses, remote and
+// per-owner rows). One thread per live source.
+template <bool kShard>
+__global__ void k_resolve_rows(const int32_t* n_live_dev, const int32_t* __restrict__ live,
+                               const int32_t* __restrict__ src_nodes, const int32_t* __restrict__ feature_row_of,
+                               const char* __restrict__ region, const char* __restrict__ feats, long long row_bytes,
+                               unsigned long long* __restrict__ rowp, unsigned long long* __restrict__ gctr,
+                               Shards sh) {
+  pdl_wait();
+  const int n = *n_live_dev;
+  const int lane = threadIdx.x & 31;
+  for (int i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; i0 < n; i0 += gridDim.x * blockDim.x) {
+    const int i = i0 + lane;
+    const bool ok = i < n;
+    int own = -1;
+    bool remote = false, hit = false;
+    if (ok) {
+      const int loc = live[i];
+      const int id = src_nodes[loc];
+      const int fr = feature_row_of ? feature_row_of[id] : -1;
+      const char* p;
+      hit = fr >= 0;
+      if (hit) {
+        p = region + (long long)fr * row_bytes;
+      } else if (kShard) {
+        int o = 0;
+        while (o + 1 < sh.P && id >= sh.bounds[o + 1]) ++o;
+        p = static_cast<const char*>(sh.ptr[o]) + (long long)(id - sh.bounds[o]) * row_bytes;
+        remote = o != sh.local;
+        own = o;
+      } else {
+        p = feats + (long long)id * row_bytes;
+      }
+      rowp[loc] = reinterpret_cast<unsigned long long>(p);
+    }
+    const unsigned valid = __ballot_sync(0xffffffffu, ok);
+    const unsigned hits = __ballot_sync(0xffffffffu, hit);
+    const unsigned remotes = __ballot_sync(0xffffffffu, remote);
+    if (lane == 0) {
+      if (hits) atomicAdd(gctr + kGCtrFeatureHits, (unsigned long long)__popc(hits));
+      if (valid & ~hits) atomicAdd(gctr + kGCtrFeatureMisses, (unsigned long long)__popc(valid & ~hits));
+      if (remotes) atomicAdd(gctr + kGCtrRemoteRows, (unsigned long long)__popc(remotes));
+    }
+    if (kShard && sh.owner_rows) {
+      for (int o = 0; o < sh.P; ++o) {
+        const unsigned m = __ballot_sync(0xffffffffu, own == o);
+        if (lane == 0 && m) atomicAdd(sh.owner_rows + o, (unsigned long long)__popc(m));
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // fp32 sources: the gather is a pure row copy, done by the TMA engine.
 // Each warp streams groups of R rows (lane r < R owns row r of the group):
@@ -372,6 +428,35 @@ int hg_load_features_sharded(const int32_t* n_live_dev, long long n_live_max, co
     { const cudaError_t _pe = hg::launch_pdl(k_load_rows<float, 8, true>, dim3(grid), dim3(kWarps * 32), 0, stream, n_live_dev, live, src_nodes, feature_row_of,
                                                                  static_cast<const float*>(region), nullptr, dim,
                                                                  h_out, g, sh); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  HG_LAUNCHED(W);
+  return kOk;
+}
+
+// K5 by reference: rowp[live[i]] = address of live source i's feature row
+// (region / table / owner shard), with k_load_rows' accounting; the layer-0
+// aggregation reads the rows in place (hg_aggregate_fwd_rows). shard_ptrs
+// NULL = an unsharded table `feats`.
+int hg_resolve_feature_rows(const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
+                            const int32_t* src_nodes, const int32_t* feature_row_of, const void* region,
+                            const void* feats, const void* const* shard_ptrs, const long long* shard_bounds,
+                            int num_shards, int local_shard, int dim, int dtype, unsigned long long* rowp,
+                            long long* global_ctr, long long* owner_rows, cudaStream_t stream) {
+  const char* W = "hg_resolve_feature_rows";
+  const long long row_bytes = (long long)dim * (dtype == 1 ? 2 : 4);
+  if (row_bytes % 16) return fail(W, kBadArg, "feature row bytes must be a multiple of 16");
+  if (shard_ptrs && (num_shards < 1 || num_shards > kMaxShards)) return fail(W, kBadArg, "num_shards must be in [1, 16]");
+  auto* g = reinterpret_cast<unsigned long long*>(global_ctr);
+  const unsigned grid = grid_for(n_live_max, 256, 148 * 8);
+  const Shards sh{shard_ptrs, shard_bounds, num_shards, local_shard, reinterpret_cast<unsigned long long*>(owner_rows)};
+  cudaError_t pe;
+  if (shard_ptrs)
+    pe = hg::launch_pdl(k_resolve_rows<true>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, src_nodes,
+                        feature_row_of, static_cast<const char*>(region), nullptr, row_bytes, rowp, g, sh);
+  else
+    pe = hg::launch_pdl(k_resolve_rows<false>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, src_nodes,
+                        feature_row_of, static_cast<const char*>(region), static_cast<const char*>(feats), row_bytes,
+                        rowp, g, sh);
+  if (pe != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(pe));
   HG_LAUNCHED(W);
   return kOk;
 }

@@ -18,6 +18,7 @@
 // CSR order forward and ascending dst-row order backward; fixed-order warp
 // trees for the fp64 norms, so every run is bit-identical.
 #include "hgb200.h"
+#include <cuda_fp16.h>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "hg_scan.cuh"
@@ -58,14 +59,36 @@ __device__ __forceinline__ float gcn_coef(int dd, int sd) {
   return (float)(1.0 / sqrt(((double)dd + 1.0) * ((double)sd + 1.0)));
 }
 
+// Source rows of the aggregation: kSrc 0 = rows of the fp32 matrix h_in
+// (layers >= 1, or a gathered layer-0 input); kSrc 1 / 2 = layer-0 feature
+// rows read in place through per-source addresses rowp[c] (fp32 / fp16
+// tables, hg_resolve_feature_rows): the fp32 copy of every live feature row
+// and its re-read are gone (K5 fused into K6). fp16 -> fp32 is exact, so the
+// sums are bit-identical to the gathered path.
+template <int kSrc>
+__device__ __forceinline__ const void* src_row(const float* __restrict__ h_in,
+                                               const unsigned long long* __restrict__ rowp, int c, int d) {
+  if (kSrc == 0) return h_in + (long long)c * d;
+  return reinterpret_cast<const void*>(rowp[c]);
+}
+template <int kSrc>
+__device__ __forceinline__ float4 row_vec(const void* base, int v) {
+  if (kSrc <= 1) return reinterpret_cast<const float4*>(base)[v];
+  const uint2 u = reinterpret_cast<const uint2*>(base)[v];
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
 // one warp per compute row; kT = float4 vectors per lane (d <= 128 kT); the
 // [self | agg | 1 | pad] row is staged in dynamic shared memory (row_floats
 // per warp) before it is emitted as TS core rows
-template <int kKind, int kT>
+template <int kKind, int kT, int kSrc>
 __global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
+                                                   const unsigned long long* __restrict__ rowp,
                                                    int d, uint8_t* __restrict__ A_ts, long long plane, int row_floats) {
   pdl_wait();
   extern __shared__ __align__(16) float agg_smem[];
@@ -76,7 +99,7 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(co
   const int nK = (K + 1 + 31) / 32;          // TS column chunks of [. | 1 | 0 pad]
   float* srow = agg_smem + (size_t)(threadIdx.x >> 5) * row_floats;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  KTimer* kt = g_kt ? g_kt + kTAggregate : nullptr;
+  KTimer* kt = g_kt ? g_kt + (kSrc ? kTAggregateFeat : kTAggregate) : nullptr;
   kt_begin(kt);
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < R; i += warps) {
     const int r = rows[i];
@@ -92,18 +115,21 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(co
     for (; e + 4 <= e1; e += 4) {
       int c[4];
       float w[4];
+      const void* bp[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         c[q] = col[e + q];
         w[q] = kKind == kKindSAGE ? cs : gcn_coef(dd, src_deg[c[q]]);
       }
 #pragma unroll
+      for (int q = 0; q < 4; ++q) bp[q] = src_row<kSrc>(h_in, rowp, c[q], d);
+#pragma unroll
       for (int t = 0; t < kT; ++t) {
         const int v = lane + 32 * t;
         if (v < nv) {
           float4 x[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) x[q] = reinterpret_cast<const float4*>(h_in + (long long)c[q] * d)[v];
+          for (int q = 0; q < 4; ++q) x[q] = row_vec<kSrc>(bp[q], v);
 #pragma unroll
           for (int q = 0; q < 4; ++q) acc[t] = f4_fmadd_rn(acc[t], w[q], x[q]);
         }
@@ -112,25 +138,27 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(co
     for (; e < e1; ++e) {
       const int c0 = col[e];
       const float w0 = kKind == kKindSAGE ? cs : gcn_coef(dd, src_deg[c0]);
+      const void* b0 = src_row<kSrc>(h_in, rowp, c0, d);
 #pragma unroll
       for (int t = 0; t < kT; ++t) {
         const int v = lane + 32 * t;
-        if (v < nv) acc[t] = f4_fmadd_rn(acc[t], w0, reinterpret_cast<const float4*>(h_in + (long long)c0 * d)[v]);
+        if (v < nv) acc[t] = f4_fmadd_rn(acc[t], w0, row_vec<kSrc>(b0, v));
       }
     }
     // assemble [self | agg | 1 | 0...] (SAGE) or [agg | 1 | 0...] (GCN) in smem,
     // then emit it as bf16 hi/lo TS core-matrix rows (hg_ts.cuh)
-    const float4* hs = reinterpret_cast<const float4*>(h_in + (long long)r * d);
+    const void* hs = src_row<kSrc>(h_in, rowp, r, d);
 #pragma unroll
     for (int t = 0; t < kT; ++t) {
       const int v = lane + 32 * t;
       if (v < nv) {
+        const float4 xs = row_vec<kSrc>(hs, v);
         if (kKind == kKindSAGE) {
-          reinterpret_cast<float4*>(srow)[v] = hs[v];
+          reinterpret_cast<float4*>(srow)[v] = xs;
           reinterpret_cast<float4*>(srow + d)[v] = acc[t];
         } else {
           const float ws = gcn_coef(dd, src_deg[r]);
-          reinterpret_cast<float4*>(srow)[v] = f4_fmadd_rn(acc[t], ws, hs[v]);
+          reinterpret_cast<float4*>(srow)[v] = f4_fmadd_rn(acc[t], ws, xs);
         }
       }
     }
@@ -325,7 +353,8 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_a
     const int32_t* __restrict__ seg_hi, const unsigned* __restrict__ srt_vals, const int32_t* __restrict__ rows,
     const int32_t* __restrict__ start, const int32_t* __restrict__ end, const int32_t* __restrict__ dst_deg,
     const int32_t* __restrict__ src_deg, const int32_t* n_dst_dev, const int32_t* __restrict__ pos_of,
-    const float* __restrict__ SG, int ldSG, int d, float* __restrict__ d_in, double* __restrict__ norms) {
+    const float* __restrict__ SG, int ldSG, int d, float* __restrict__ d_in, double* __restrict__ norms,
+    const uint8_t* __restrict__ need_row) {
   pdl_wait();
   const int n = *n_live_dev;
   const int n_dst = *n_dst_dev;
@@ -379,11 +408,14 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_a
     }
     double sq = 0.0;
     float4* out = reinterpret_cast<float4*>(d_in + (long long)c * d);
+    // rows the next layer does not compute (cache-injected) need only their
+    // norm (the admission key, cache.py:188-191), not the gradient row itself
+    const bool write = !need_row || need_row[c];
 #pragma unroll
     for (int t = 0; t < kT; ++t) {
       const int v = lane + 32 * t;
       if (v < nv) {
-        out[v] = acc[t];
+        if (write) out[v] = acc[t];
         sq += (double)acc[t].x * acc[t].x + (double)acc[t].y * acc[t].y + (double)acc[t].z * acc[t].z +
               (double)acc[t].w * acc[t].w;
       }
@@ -423,10 +455,10 @@ using namespace hg;
 
 extern "C" {
 
-int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
-                     const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
-                     const float* h_in, int d, void* A_ts, cudaStream_t stream) {
-  const char* W = "hg_aggregate_fwd";
+static int aggregate_launch(const char* W, int kind, int src, const int32_t* R_dev, long long R_max,
+                            const int32_t* rows, const int32_t* start, const int32_t* end, const int32_t* col,
+                            const int32_t* dst_deg, const int32_t* src_deg, const float* h_in,
+                            const unsigned long long* rowp, int d, void* A_ts, cudaStream_t stream) {
   if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 1024");
   // grid covers the compute rows and the zero padding up to the next 128-row tile
   const long long rows_pad = (R_max + kTsRows - 1) / kTsRows * kTsRows;
@@ -438,28 +470,48 @@ int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int3
   const size_t smem = (size_t)8 * row_floats * 4;
   const int vpl = (d / 4 + 31) / 32;
   cudaError_t pe = cudaSuccess;
-#define HG_AGG(KIND, T)                                                                                           \
+#define HG_AGG(KIND, T, S)                                                                                        \
   {                                                                                                              \
     if (smem > 48 * 1024) {                                                                                      \
-      pe = cudaFuncSetAttribute(k_aggregate<KIND, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+      pe = cudaFuncSetAttribute(k_aggregate<KIND, T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (pe != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(pe));                                      \
     }                                                                                                            \
-    pe = hg::launch_pdl(k_aggregate<KIND, T>, dim3(grid), dim3(256), smem, stream, R_dev, rows, start, end, col,  \
-                        dst_deg, src_deg, h_in, d, a, plane, row_floats);                                        \
+    pe = hg::launch_pdl(k_aggregate<KIND, T, S>, dim3(grid), dim3(256), smem, stream, R_dev, rows, start, end,    \
+                        col, dst_deg, src_deg, h_in, rowp, d, a, plane, row_floats);                             \
   }
-#define HG_AGG_T(KIND)                                                                                            \
-  if (vpl <= 1) HG_AGG(KIND, 1) else if (vpl <= 2) HG_AGG(KIND, 2) else if (vpl <= 4) HG_AGG(KIND, 4)           \
-  else HG_AGG(KIND, 8)
+#define HG_AGG_T(KIND, S)                                                                                         \
+  if (vpl <= 1) HG_AGG(KIND, 1, S) else if (vpl <= 2) HG_AGG(KIND, 2, S) else if (vpl <= 4) HG_AGG(KIND, 4, S)   \
+  else HG_AGG(KIND, 8, S)
+#define HG_AGG_S(KIND)                                                                                            \
+  if (src == 0) { HG_AGG_T(KIND, 0) } else if (src == 1) { HG_AGG_T(KIND, 1) } else { HG_AGG_T(KIND, 2) }
   if (kind == kKindSAGE) {
-    HG_AGG_T(kKindSAGE)
+    HG_AGG_S(kKindSAGE)
   } else {
-    HG_AGG_T(kKindGCN)
+    HG_AGG_S(kKindGCN)
   }
+#undef HG_AGG_S
 #undef HG_AGG_T
 #undef HG_AGG
   if (pe != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(pe));
   HG_LAUNCHED(W);
   return kOk;
+}
+
+int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
+                     const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
+                     const float* h_in, int d, void* A_ts, cudaStream_t stream) {
+  return aggregate_launch("hg_aggregate_fwd", kind, 0, R_dev, R_max, rows, start, end, col, dst_deg, src_deg, h_in,
+                          nullptr, d, A_ts, stream);
+}
+
+// layer 0 over feature rows read in place (rowp from hg_resolve_feature_rows);
+// dtype 0 = fp32 table, 1 = fp16; d = the table's (padded) row width
+int hg_aggregate_fwd_rows(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
+                          const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
+                          const unsigned long long* rowp, int dtype, int d, void* A_ts, cudaStream_t stream) {
+  if (dtype == 1 && d % 8) return fail("hg_aggregate_fwd_rows", kBadArg, "fp16 rows need d % 8 == 0");
+  return aggregate_launch("hg_aggregate_fwd_rows", kind, dtype == 1 ? 2 : 1, R_dev, R_max, rows, start, end, col,
+                          dst_deg, src_deg, nullptr, rowp, d, A_ts, stream);
 }
 
 int hg_scatter_rows(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* Z, int dout, int relu,
@@ -537,7 +589,7 @@ int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, 
                      const int32_t* seg_lo, const int32_t* seg_hi, const unsigned* vals_sorted, const int32_t* rows,
                      const int32_t* start, const int32_t* end, const int32_t* dst_deg, const int32_t* src_deg,
                      const int32_t* n_dst_dev, const int32_t* pos_of, const float* SG, int ldSG, int d,
-                     float* d_in, double* norms, cudaStream_t stream) {
+                     float* d_in, double* norms, const uint8_t* need_row, cudaStream_t stream) {
   const char* W = "hg_transpose_agg";
   if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 1024");
   const unsigned grid = grid_for(n_live_max * 32, 256, 148 * 16);
@@ -545,7 +597,8 @@ int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, 
   cudaError_t pe = cudaSuccess;
 #define HG_TA(KIND, T)                                                                                            \
   pe = hg::launch_pdl(k_transpose_agg<KIND, T>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, seg_lo, seg_hi,  \
-                      vals_sorted, rows, start, end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d, d_in, norms)
+                      vals_sorted, rows, start, end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d, d_in, norms, \
+                      need_row)
 #define HG_TA_T(KIND)                                                                                             \
   if (vpl <= 1) HG_TA(KIND, 1); else if (vpl <= 2) HG_TA(KIND, 2); else if (vpl <= 4) HG_TA(KIND, 4);           \
   else HG_TA(KIND, 8);

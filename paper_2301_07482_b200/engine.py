@@ -38,7 +38,7 @@ import torch
 
 from . import _lib
 from .distributed import apply_sgd
-from .nn import (Injection, LayerKind, build_csc, cross_entropy_dev, inject_rows_dev, layer_backward_dev,
+from .nn import (FeatureRows, Injection, LayerKind, build_csc, resolve_features_dev, cross_entropy_dev, inject_rows_dev, layer_backward_dev,
                  layer_forward_dev,
                  load_features_dev, pack_dgrad_weights, pack_forward_weights, ts_bytes)
 from .sampler import SamplerWorkspace, SampleSlot, layer_bounds, pcg_words, sample_blocks_dev
@@ -155,6 +155,16 @@ class StepEngine:
         self.timeline_names = []
         self.captures = 0         # graph (re-)captures so far
         self.up_ring = PinnedRing(4, 12 + 2 * self.B, torch.int32)   # input words, host -> HBM
+        # the step's IterMetrics row, written on the device at its end (hg_metrics_row)
+        cache = trainer.cache
+        vecs = [lc.ctr for lc in cache.layers.values()] + [cache.gctr]
+        self.m_vecs = torch.tensor([v.data_ptr() for v in vecs], dtype=torch.int64, device=self.dev)
+        self.m_lens = torch.tensor([v.numel() for v in vecs], dtype=torch.int32, device=self.dev)
+        self.m_nv = sum(v.numel() for v in vecs)
+        self.m_prev = torch.zeros(self.m_nv, dtype=torch.int64, device=self.dev)
+        self.m_row = torch.zeros(1 + self.m_nv + len(vecs) - 1 + 1 + 2 * self.L, dtype=torch.float64,
+                                 device=self.dev)
+        self.m_key = None          # (trainer generation) the prev snapshot is valid for
 
     @property
     def graph(self):
@@ -360,10 +370,17 @@ class StepEngine:
             self._mark("backward_prep (side)", prep)
         # ---- layer-0 input (trainer.py:326-343) ----
         b0 = blocks[0]
-        h = torch.empty((b0.num_src, tr.feature_dim), dtype=torch.float32, device=dev)
         region = cache.feature_table if cache.feature_table is not None else tr.features
-        load_features_dev(n_live_dev(0), b0.num_src, live[0], b0.src_nodes, cache.feature_row_of_dev, region,
-                          tr.features, tr.feature_dim, tr._dtype_code, h, cache.gctr, sp)
+        if tr.fused_input:
+            # K5 fused into K6: only the row addresses; layer 0 reads the rows in place
+            rowp = torch.empty(b0.num_src, dtype=torch.int64, device=dev)
+            resolve_features_dev(n_live_dev(0), b0.num_src, live[0], b0.src_nodes, cache.feature_row_of_dev,
+                                 region, tr.features, tr.feature_dim, tr._dtype_code, rowp, cache.gctr, sp)
+            h = FeatureRows(rowp, tr._dtype_code, tr.feature_dim, b0.num_src)
+        else:
+            h = torch.empty((b0.num_src, tr.feature_dim), dtype=torch.float32, device=dev)
+            load_features_dev(n_live_dev(0), b0.num_src, live[0], b0.src_nodes, cache.feature_row_of_dev, region,
+                              tr.features, tr.feature_dim, tr._dtype_code, h, cache.gctr, sp)
 
         self._mark("loaded", stream)
         # injected (cache-hit) rows of every layer output depend only on the
@@ -413,7 +430,8 @@ class StepEngine:
                 stream.wait_event(prep_done[l])
             d_prev, nrm = layer_backward_dev(net, l, blk, tapes[l], d_h, grads, l >= 1, keep[l], pos[l], live[l],
                                              blk.num_src, sp, blk.n_dst_dev, n_live_dev(l), csc=cscs[l],
-                                             W_ts=w_ts[l], wgrad_stream=self.wgrad_stream, keepalive=keepalive)
+                                             W_ts=w_ts[l], wgrad_stream=self.wgrad_stream, keepalive=keepalive,
+                                             need_rows=keep[l - 1] if l >= 1 else None)
             norms[l] = nrm
             d_h = d_prev
             self._mark(f"backward{l}", stream)
@@ -441,6 +459,10 @@ class StepEngine:
         if ahead:
             stream.wait_stream(self.samp_stream)
         self._mark("joined", stream)
+        from ._state import CTR_VALID
+        _lib.call("hg_metrics_row", _lib.ptr(self.m_vecs), _lib.ptr(self.m_lens), int(self.m_lens.numel()),
+                  _lib.ptr(self.m_prev), _lib.ptr(loss), _lib.ptr(blocks[0].n_src_dev), _lib.ptr(counts), 2 * L,
+                  CTR_VALID, _lib.ptr(self.m_row), sp)
         return dict(loss=loss, counts=counts, blocks=blocks, live=live, rows=rows, keep=keep, tapes=tapes,
                     norms=norms, grads=grads, injected=injected, keepalive=(keepalive, cscs, w_ts))
 

@@ -322,6 +322,41 @@ def load_features_dev(n_live_dev, n_max: int, live, src_nodes, feature_row_of, r
               _lib.ptr(gctr), _lib.ptr(scratch), sb, stream)
 
 
+@dataclass
+class FeatureRows:
+    """Layer-0 input by reference (K5 fused into K6): rowp[loc] is the address
+    of local source loc's feature row (region row, table row or owner-shard
+    row); the layer-0 aggregation reads the rows in place."""
+
+    rowp: torch.Tensor          # int64 [n_src]
+    dtype_code: int             # 0 fp32, 1 fp16
+    dim: int                    # (padded) row width
+    num_rows: int
+
+    @property
+    def shape(self):
+        return (self.num_rows, self.dim)
+
+    @property
+    def device(self):
+        return self.rowp.device
+
+
+def resolve_features_dev(n_live_dev, n_max: int, live, src_nodes, feature_row_of, region, feats, dim: int,
+                         dtype_code: int, rowp: torch.Tensor, gctr, stream) -> None:
+    """hg_resolve_feature_rows: rowp[live[i]] = address of the row (the
+    accounting of load_features_dev, no row copied)."""
+    if hasattr(feats, "load_rows"):   # sharding.ShardedFeatures
+        _lib.call("hg_resolve_feature_rows", _lib.ptr(n_live_dev), n_max, _lib.ptr(live), _lib.ptr(src_nodes),
+                  _lib.ptr(feature_row_of), _lib.ptr(region if feature_row_of is not None else None), None,
+                  _lib.ptr(feats.ptrs_dev), _lib.ptr(feats.bounds_dev), feats.num_shards, feats.local_shard, dim,
+                  dtype_code, _lib.ptr(rowp), _lib.ptr(gctr), _lib.ptr(feats.owner_rows), stream)
+        return
+    _lib.call("hg_resolve_feature_rows", _lib.ptr(n_live_dev), n_max, _lib.ptr(live), _lib.ptr(src_nodes),
+              _lib.ptr(feature_row_of), _lib.ptr(region), _lib.ptr(feats), None, None, 0, 0, dim, dtype_code,
+              _lib.ptr(rowp), _lib.ptr(gctr), None, stream)
+
+
 def _dev_count(n: int, dev) -> torch.Tensor:
     return torch.tensor([n], dtype=torch.int32, device=dev)
 
@@ -480,9 +515,14 @@ def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch
     # GEMM operand [self | agg | 1] written by the aggregation directly as TS
     # (bf16 hi/lo core-matrix tiles, csrc/hg_ts.cuh)
     A = torch.empty(ts_bytes(R, K + 1), dtype=torch.uint8, device=dev)
-    _lib.call("hg_aggregate_fwd", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(blk.adj.start),
-              _lib.ptr(blk.adj.end), _lib.ptr(blk.adj.col_indices), _lib.ptr(blk.dst_deg), _lib.ptr(blk.src_deg),
-              _lib.ptr(h_in), d_in, _lib.ptr(A), stream)
+    if isinstance(h_in, FeatureRows):     # layer 0 reading the feature rows in place
+        _lib.call("hg_aggregate_fwd_rows", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(blk.adj.start),
+                  _lib.ptr(blk.adj.end), _lib.ptr(blk.adj.col_indices), _lib.ptr(blk.dst_deg),
+                  _lib.ptr(blk.src_deg), _lib.ptr(h_in.rowp), h_in.dtype_code, d_in, _lib.ptr(A), stream)
+    else:
+        _lib.call("hg_aggregate_fwd", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(blk.adj.start),
+                  _lib.ptr(blk.adj.end), _lib.ptr(blk.adj.col_indices), _lib.ptr(blk.dst_deg),
+                  _lib.ptr(blk.src_deg), _lib.ptr(h_in), d_in, _lib.ptr(A), stream)
     if PT is None:
         PT = pack_forward_weights(net, l, stream)
     n_dst = blk.num_dst
@@ -600,7 +640,7 @@ def pack_dgrad_weights(net: Network, l: int, stream) -> torch.Tensor:
 def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tensor, grads: Grads,
                        need_input: bool, keep, pos_of, live, n_live, stream, n_dst_dev=None, n_live_dev=None,
                        csc: BlockCsc | None = None, W_ts: torch.Tensor | None = None, wgrad_stream=None,
-                       keepalive: list | None = None):
+                       keepalive: list | None = None, need_rows=None):
     """Writes dP into grads; returns (d_in [n_src, d_in] with rows valid on
     `live`, fp64 norms aligned with `live`) or (None, None).
 
@@ -608,7 +648,9 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
     depend only on the pruned block / the weights), and `wgrad_stream`: the
     weight-gradient GEMM forks onto it (only SGD waits for it) while the
     input-gradient chain continues; buffers it reads are appended to
-    `keepalive`, which the caller holds until the streams are joined."""
+    `keepalive`, which the caller holds until the streams are joined;
+    `need_rows` (uint8 per input row): only rows the previous layer computes
+    get a gradient row, the others only their norm."""
     if net.kind is LayerKind.GAT:
         return gat_layer_backward_dev(net, l, blk, t, d_h, grads, need_input, keep, pos_of, stream, n_dst_dev,
                                       csc, wgrad_stream, keepalive)
@@ -655,7 +697,7 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
               _lib.ptr(csc.seg_lo), _lib.ptr(csc.seg_hi), _lib.ptr(csc.vals), _lib.ptr(t.rows),
               _lib.ptr(blk.adj.start), _lib.ptr(blk.adj.end), _lib.ptr(blk.dst_deg), _lib.ptr(blk.src_deg),
               _lib.ptr(n_dst_dev), _lib.ptr(pos_of), _lib.ptr(SG), K, d_in_dim, _lib.ptr(d_in), _lib.ptr(norms),
-              stream)
+              _lib.ptr(need_rows), stream)
     return d_in, norms[:n_live]
 
 

@@ -219,6 +219,7 @@ class ShardedHistCache(HistCache):
         self.feature_table = None
         self.feature_row_of_dev = torch.full((self.num_nodes,), -1, dtype=torch.int32, device=self.device)
         self.gctr = torch.zeros(GLOBAL_CTR_LEN, dtype=torch.int64, device=self.device)
+        self._ops = 0
         # one IPC block per rank: every layer's sections + the barrier flag
         offs, o = [], 0
         for lc in self.layers.values():

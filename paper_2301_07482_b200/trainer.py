@@ -29,7 +29,7 @@ from .distributed import apply_sgd
 from .engine import StepEngine
 from .cache import COUNTER_NAMES, CachePolicy, HistCache
 from .graphs import Csr2Graph, _np, csr2_from_arrays
-from .nn import (Injection, LayerKind, Network, backward, cross_entropy_dev, forward_pass, init_network, pad_columns,
+from .nn import (FeatureRows, Injection, LayerKind, Network, resolve_features_dev, backward, cross_entropy_dev, forward_pass, init_network, pad_columns,
                  pad_width,
                  layer_backward_dev, layer_forward_dev, load_features_dev, sgd_step, _dev_count)
 from .sharding import ShardedFeatures
@@ -423,23 +423,39 @@ class Trainer:
         self._probe_record = None
         self.grad_hook = None   # callable(Grads) run between backward and SGD (data parallel)
         self.use_graphs = os.environ.get("HG_GRAPHS", "1") != "0"
+        # layer 0 reads the feature rows in place (no fp32 copy of the input
+        # frontier) unless they sit in host memory (UVA: one gather over PCIe
+        # beats one read per edge) or the layer is GAT (its transform runs
+        # over all live sources); HG_FUSED_INPUT=0 restores the gather (A/B)
+        self.fused_input = (cfg.kind is not LayerKind.GAT and cfg.feature_placement == "hbm"
+                            and os.environ.get("HG_FUSED_INPUT", "1") != "0")
         self._engines = {}
         self._ahead = None     # (key, device words) of the batch announced by the last step
+        self._ctr_gen = 0      # bumped by every counter-moving step (engine metric rows re-sync on change)
+        self._ctr_owner = None
 
     # ------------------------------------------------------------ pieces
 
     def sample(self, iteration: int, seeds) -> LayeredSubgraph:
         return sample_layered(self.graph, seeds, self.plan, batch_rng(self.cfg.seed, iteration))
 
-    def _load_input(self, pruned: PrunedBatch, current_iter: int, stream=None):
+    def _load_input(self, pruned: PrunedBatch, current_iter: int, stream=None, by_reference: bool = False):
         """trainer.py:326-343: feature-region hits + source fetches into the
-        block-0 input matrix; returns (h, baseline_bytes)."""
+        block-0 input matrix; returns (h, baseline_bytes). by_reference: the
+        rows are not copied, h is a FeatureRows (their addresses) that the
+        layer-0 aggregation reads in place."""
         b0 = pruned.sub.layers[0]
         dev = self.device
         sp = _lib.stream_ptr(stream)
-        h = torch.empty((b0.num_src, self.feature_dim), dtype=torch.float32, device=dev)
         n_live0 = pruned.counts[0][1]
         region = self.cache.feature_table if self.cache.feature_table is not None else self.features
+        if by_reference:
+            rowp = torch.empty(b0.num_src, dtype=torch.int64, device=dev)
+            resolve_features_dev(pruned.n_live_dev(0), n_live0, pruned.layer_live[0], b0.src_nodes,
+                                 self.cache.feature_row_of_dev, region, self.features, self.feature_dim,
+                                 self._dtype_code, rowp, self.cache.gctr, sp)
+            return FeatureRows(rowp, self._dtype_code, self.feature_dim, b0.num_src), b0.num_src * self.row_bytes
+        h = torch.empty((b0.num_src, self.feature_dim), dtype=torch.float32, device=dev)
         load_features_dev(pruned.n_live_dev(0), n_live0, pruned.layer_live[0], b0.src_nodes,
                           self.cache.feature_row_of_dev, region, self.features, self.feature_dim, self._dtype_code, h,
                           self.cache.gctr, sp)
@@ -454,6 +470,7 @@ class Trainer:
         before = cache.counters_vector().clone()
         labels_dev = torch.from_numpy(self.labels[sub.seeds].astype(np.int32)).pin_memory().to(dev, non_blocking=True)
         exact_sub = sub.copy() if probe else None      # before pruning mutates the CSR2 ends
+        self._ctr_gen += 1
         self._probe_err = None
         loss_dev, baseline = self._step(iteration, sub, labels_dev, exact_sub=exact_sub)
         after = cache.counters_vector()
@@ -505,6 +522,19 @@ class Trainer:
         return eng.pack_inputs(iteration, seeds.astype(np.int32), self.labels[seeds].astype(np.int32),
                                (int(bg["state"]), int(bg["inc"])))
 
+    def _ctr_key(self, eng):
+        return (self._ctr_gen, self.cache._ops, id(eng))
+
+    def _ctr_sync(self, eng) -> None:
+        """The engine's metric row reports counter deltas since its previous
+        row; re-base it when anything else moved the counters in between."""
+        if eng.m_key != self._ctr_key(eng):
+            eng.m_prev.copy_(self.cache.counters_vector())
+
+    def _ctr_done(self, eng) -> None:
+        self._ctr_gen += 1
+        eng.m_key = self._ctr_key(eng)
+
     def _engine_step(self, iteration: int, seeds, next_batch=None):
         """Run one engine step; `next_batch=(iteration, seeds)` announces the
         following batch so the step samples it ahead (pipelined)."""
@@ -523,7 +553,9 @@ class Trainer:
             if len(nseeds) == len(seeds):   # same engine (batch size): pipeline it
                 nxt = eng.upload(self._words(eng, nit, nseeds))
                 self._ahead = ((len(nseeds), int(nit), hash(nseeds.tobytes())), nxt)
+        self._ctr_sync(eng)
         out = eng.step_words(words, nxt)
+        self._ctr_done(eng)
         return eng, out
 
     def train_step_device(self, iteration: int, seeds, next_batch=None) -> torch.Tensor:
@@ -551,7 +583,9 @@ class Trainer:
         it, B, words = staged
         eng = self._engine(B)
         nxt = next_staged[2] if next_staged is not None and next_staged[1] == B else None
+        self._ctr_sync(eng)
         out = eng.step_words(words, nxt)
+        self._ctr_done(eng)
         self.cache.end_iteration(it)
         self._last_engine = (eng, out)
         return out["loss"]
@@ -565,16 +599,12 @@ class Trainer:
         `.result()` or on first attribute access), so the host can enqueue
         the next step while this one runs."""
         cache = self.cache
-        before = cache.counters_vector().clone()
         eng, out = self._engine_step(iteration, seeds, next_batch)
-        after = cache.counters_vector()
-        n_src0 = out["blocks"][0].n_src_dev
-        dev_buf = torch.cat([out["loss"].view(1), (after - before).double(),
-                             after[CTR_VALID::LAYER_CTR_LEN][:cache.num_layers].double(), n_src0.double(),
-                             out["counts"].double()])
+        dev_buf = eng.m_row            # written by the step itself (hg_metrics_row)
+        nv = eng.m_nv
         if not sync:
             ring = self._metrics_ring(eng, dev_buf.numel())
-            pm = PendingMetrics(self, None, None, iteration, epoch, len(seeds), after.numel())
+            pm = PendingMetrics(self, None, None, iteration, epoch, len(seeds), nv)
             i, host_buf = ring.acquire(pm)
             host_buf.copy_(dev_buf, non_blocking=True)
             pm._buf, pm._ev = host_buf, ring.issued(i)
@@ -582,7 +612,6 @@ class Trainer:
             self._last_engine = (eng, out)
             return pm
         host = dev_buf.cpu().tolist()
-        nv = after.numel()
         loss, delta = host[0], [int(x) for x in host[1:1 + nv]]
         valid = int(sum(host[1 + nv:1 + nv + cache.num_layers]))
         n_src0 = int(host[1 + nv + cache.num_layers])
@@ -616,7 +645,7 @@ class Trainer:
         it_dev = torch.tensor([int(iteration)], dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
         cache.begin_step(it_dev, sp)
         pruned = prune_with_cache(sub, cache, iteration, stream)
-        h0, baseline = self._load_input(pruned, iteration, stream)
+        h0, baseline = self._load_input(pruned, iteration, stream, by_reference=self.fused_input)
         L = sub.num_layers
         tapes = []
         h = h0
@@ -637,7 +666,8 @@ class Trainer:
             n_live = pruned.counts[l][1]
             d_prev, nrm = layer_backward_dev(net, l, sub.layers[l], tapes[l], d_h, grads, l >= 1, pruned.keep[l],
                                              pruned.pos_of[l], pruned.layer_live[l], n_live, sp,
-                                             pruned.n_dst_dev(l), pruned.n_live_dev(l))
+                                             pruned.n_dst_dev(l), pruned.n_live_dev(l),
+                                             need_rows=pruned.keep[l - 1] if l >= 1 else None)
             norms[l] = nrm
             d_h = d_prev
         apply_sgd(self.grad_hook, net, grads, cfg.eta)   # e.g. NCCL all-reduce of the flat bucket, then SGD
