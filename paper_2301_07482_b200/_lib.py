@@ -15,6 +15,8 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhgb200.so")
+if os.environ.get("HG_LIB_PATH"):          # A/B variants (tools/build_variant.sh); diagnostics only
+    LIB_PATH = os.path.abspath(os.environ["HG_LIB_PATH"])
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int

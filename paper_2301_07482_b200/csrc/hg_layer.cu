@@ -48,6 +48,9 @@ constexpr int kMaxRowFloats = 1056;
 #endif
 #ifndef HG_TAGG_MINB
 #define HG_TAGG_MINB 8
+#endif
+#ifndef HG_AGG_PIPE
+#define HG_AGG_PIPE 1
 #endif // k_gather_dz staging: d_out <= 1056
 
 __device__ __forceinline__ float4 f4_fmadd_rn(float4 acc, float c, float4 x) {
@@ -101,10 +104,32 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(co
   const int warps = (gridDim.x * blockDim.x) >> 5;
   KTimer* kt = g_kt ? g_kt + (kSrc ? kTAggregateFeat : kTAggregate) : nullptr;
   kt_begin(kt);
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < R; i += warps) {
-    const int r = rows[i];
-    const int e0 = start[r], e1 = end[r];
+  // software-pipelined over the warp's rows: the next row's id is fetched at
+  // the start of a row and its extents after the edge loads, and a row's own
+  // (self) feature row is loaded before its edges, so per row only the
+  // col -> (rowp ->) neighbour-row chain is exposed (HG_AGG_PIPE=0: the
+  // unpipelined loop, A/B)
+  int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int r = 0, e0 = 0, e1 = 0;
+  if (i < R) {
+    r = rows[i];
+    e0 = start[r];
+    e1 = end[r];
+  }
+  // measured (C2): the pipelined loop helps the layer-0 rows-in-place variant
+  // (one more dependent hop per edge) and costs the matrix variant ~20 %
+  constexpr bool kPipe = HG_AGG_PIPE && kSrc >= 1;
+  for (; i < R; i += warps) {
+    const int i_next = i + warps;
+    const int r_next = kPipe && i_next < R ? rows[i_next] : 0;
     const int cnt = e1 - e0;
+    const void* hs = src_row<kSrc>(h_in, rowp, r, d);
+    float4 xs[kT];
+#pragma unroll
+    for (int t = 0; t < kT; ++t) {
+      const int v = lane + 32 * t;
+      xs[t] = v < nv ? row_vec<kSrc>(hs, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     float4 acc[kT];
 #pragma unroll
     for (int t = 0; t < kT; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -145,20 +170,24 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(co
         if (v < nv) acc[t] = f4_fmadd_rn(acc[t], w0, row_vec<kSrc>(b0, v));
       }
     }
+    const int r_cur = r;
+    if (i_next < R) {
+      r = kPipe ? r_next : rows[i_next];
+      e0 = start[r];
+      e1 = end[r];
+    }
     // assemble [self | agg | 1 | 0...] (SAGE) or [agg | 1 | 0...] (GCN) in smem,
     // then emit it as bf16 hi/lo TS core-matrix rows (hg_ts.cuh)
-    const void* hs = src_row<kSrc>(h_in, rowp, r, d);
 #pragma unroll
     for (int t = 0; t < kT; ++t) {
       const int v = lane + 32 * t;
       if (v < nv) {
-        const float4 xs = row_vec<kSrc>(hs, v);
         if (kKind == kKindSAGE) {
-          reinterpret_cast<float4*>(srow)[v] = xs;
+          reinterpret_cast<float4*>(srow)[v] = xs[t];
           reinterpret_cast<float4*>(srow + d)[v] = acc[t];
         } else {
-          const float ws = gcn_coef(dd, src_deg[r]);
-          reinterpret_cast<float4*>(srow)[v] = f4_fmadd_rn(acc[t], ws, xs);
+          const float ws = gcn_coef(dd, src_deg[r_cur]);
+          reinterpret_cast<float4*>(srow)[v] = f4_fmadd_rn(acc[t], ws, xs[t]);
         }
       }
     }

@@ -665,7 +665,7 @@ extern "C" {
 
 long long hg_sample_layer_scratch_bytes(long long F_max, long long num_nodes) {
   long long words = (num_nodes + 31) / 32;
-  return (scan_tiles(F_max) + 1) * (long long)sizeof(I64x2) + (scan_tiles(words) + 1) * 4 + 256 +
+  return (scan_tiles(F_max) + 1) * (long long)sizeof(I64x2) + (scan_tiles(words, 1) + 1) * 4 + 256 +
          (long long)(kMaxTasks + 2) * 4 + 64 + huge_scratch_bytes(F_max);
 }
 
@@ -683,7 +683,7 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   const long long words = (num_nodes + 31) / 32;
   I64x2* part_dc = reinterpret_cast<I64x2*>(scratch);
   int* part_w = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + (scan_tiles(F_max) + 1) * sizeof(I64x2));
-  long long* task_meta = reinterpret_cast<long long*>(part_w + scan_tiles(words) + 2);
+  long long* task_meta = reinterpret_cast<long long*>(part_w + scan_tiles(words, 1) + 2);
   task_meta = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(task_meta) + 15) & ~uintptr_t(15));
   int32_t* task_row = reinterpret_cast<int32_t*>(task_meta + 2);
   // hub-row state after the task table (16-byte aligned pieces)
@@ -737,7 +737,9 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   { const cudaError_t _pe = hg::launch_pdl(k_pick, dim3(grid_for(F_max * (long long)fanout, 256)), dim3(256), 0, stream, g_col, counts_dev, ss, g2l, bitmap, src_flat,
                                                                        col_local); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
-  st = scan_launch<int>(W, PopWord{bitmap}, ConstCount{words}, words, part_w,
+  // one bitmap word per thread: a dense word emits up to 32 ids serially,
+  // so short threads and many CTAs (words / 256) keep the emission parallel
+  st = scan_launch<int, 1>(W, PopWord{bitmap}, ConstCount{words}, words, part_w,
                         EmitNew{bitmap, F_dev, ss, g2l, src_out},
                         TotalNew{F_dev, counts_dev, ss, cand_off}, stream);
   if (st) return st;

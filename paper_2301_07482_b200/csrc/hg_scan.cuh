@@ -83,14 +83,14 @@ __device__ __forceinline__ T block_exclusive(T v, T* block_total) {
   return warp_prefix + inc - v;
 }
 
-template <typename T, typename F, typename NC>
+template <typename T, typename F, typename NC, int kItems = kScanItems>
 __global__ void __launch_bounds__(kScanThreads) k_tile_reduce(F f, NC nc, T* partials) {
   pdl_wait();
   const long long n = nc.get();
-  const long long base = (long long)blockIdx.x * kScanTile;
+  const long long base = (long long)blockIdx.x * (kScanThreads * kItems);
   T acc = zero_of<T>();
   if (base < n) {
-    for (int k = 0; k < kScanItems; ++k) {
+    for (int k = 0; k < kItems; ++k) {
       long long i = base + (long long)k * kScanThreads + threadIdx.x;
       if (i < n) acc = acc + f(i);
     }
@@ -136,23 +136,23 @@ __global__ void __launch_bounds__(1024) k_scan_partials(T* partials, int tiles) 
   }
 }
 
-template <typename T, typename F, typename NC, typename Emit, typename Total>
+template <typename T, typename F, typename NC, typename Emit, typename Total, int kItems = kScanItems>
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(F f, NC nc, const T* partials, Emit emit,
                                                             Total total) {
   pdl_wait();
   const long long n = nc.get();
-  const long long base = (long long)blockIdx.x * kScanTile;
+  const long long base = (long long)blockIdx.x * (kScanThreads * kItems);
   if (n == 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) total(zero_of<T>());
     return;
   }
   if (base >= n) return;
-  // each thread owns kScanItems consecutive items
-  const long long tb = base + (long long)threadIdx.x * kScanItems;
-  T v[kScanItems];
+  // each thread owns kItems consecutive items
+  const long long tb = base + (long long)threadIdx.x * kItems;
+  T v[kItems];
   T sum = zero_of<T>();
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
+  for (int k = 0; k < kItems; ++k) {
     long long i = tb + k;
     v[k] = i < n ? f(i) : zero_of<T>();
     sum = sum + v[k];
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(F f, NC nc, const T*
   T tot;
   T run = partials[blockIdx.x] + block_exclusive(sum, &tot);
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
+  for (int k = 0; k < kItems; ++k) {
     long long i = tb + k;
     if (i < n) {
       emit(i, run, v[k]);
@@ -170,21 +170,25 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(F f, NC nc, const T*
   }
 }
 
-// Launch the three-kernel scan. partials must hold >= scan_tiles(n_max) T.
-inline long long scan_tiles(long long n_max) { return (n_max + kScanTile - 1) / kScanTile; }
+// Launch the three-kernel scan. partials must hold >= scan_tiles(n_max) T
+// (tiles of kScanThreads x kItems items; kItems < kScanItems for items whose
+// emit is heavy, e.g. the sampler's bitmap words: more, shorter threads).
+inline long long scan_tiles(long long n_max, int items = kScanItems) {
+  return (n_max + (long long)kScanThreads * items - 1) / ((long long)kScanThreads * items);
+}
 
-template <typename T, typename F, typename NC, typename Emit, typename Total>
+template <typename T, int kItems = kScanItems, typename F, typename NC, typename Emit, typename Total>
 int scan_launch(const char* where, F f, NC nc, long long n_max, T* partials, Emit emit, Total total,
                 cudaStream_t s) {
-  long long tiles = scan_tiles(n_max);
+  long long tiles = scan_tiles(n_max, kItems);
   if (tiles < 1) tiles = 1;
-  HG_CHECK_CUDA(where, launch_pdl(k_tile_reduce<T, F, NC>, dim3((unsigned)tiles), dim3(kScanThreads), 0, s, f, nc,
-                                   partials));
+  HG_CHECK_CUDA(where, launch_pdl(k_tile_reduce<T, F, NC, kItems>, dim3((unsigned)tiles), dim3(kScanThreads), 0, s,
+                                   f, nc, partials));
   HG_LAUNCHED(where);
   HG_CHECK_CUDA(where, launch_pdl(k_scan_partials<T>, dim3(1), dim3(1024), 0, s, partials, (int)tiles));
   HG_LAUNCHED(where);
-  HG_CHECK_CUDA(where, launch_pdl(k_tile_scan<T, F, NC, Emit, Total>, dim3((unsigned)tiles), dim3(kScanThreads), 0, s,
-                                   f, nc, (const T*)partials, emit, total));
+  HG_CHECK_CUDA(where, launch_pdl(k_tile_scan<T, F, NC, Emit, Total, kItems>, dim3((unsigned)tiles),
+                                   dim3(kScanThreads), 0, s, f, nc, (const T*)partials, emit, total));
   HG_LAUNCHED(where);
   return kOk;
 }
