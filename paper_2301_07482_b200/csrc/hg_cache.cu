@@ -65,7 +65,14 @@ inline int sort_mode(long long n_max) {
 // the CUB merge / radix sorts, in 6 launches instead of ~19, O(n) work.
 // Buckets above kBucketCap items (e.g. masses of equal norms) are sorted by
 // one CTA each with a chunk sort + global merge passes (k_bs_big).
-constexpr int kNB = 4096;
+// 16K buckets: norms concentrate in a few binades, so at 4096 buckets each
+// held hundreds of keys and the per-bucket shared-memory bitonic sorts
+// dominated the update (HG_CACHE_NB overrides at build time, A/B)
+#ifndef HG_CACHE_NB
+#define HG_CACHE_NB 16384
+#endif
+constexpr int kNB = HG_CACHE_NB;
+static_assert((kNB & (kNB - 1)) == 0 && kNB >= 1024, "bucket count: a power of two >= 1024");
 constexpr int kBucketCap = 2048;
 
 struct BucketState {            // device scratch
@@ -81,7 +88,8 @@ __device__ __forceinline__ int bucket_of(unsigned long long bits, unsigned long 
 __device__ __forceinline__ int bucket_shift(unsigned long long lo, unsigned long long hi) {
   const unsigned long long r = hi - lo;
   const int bits = r ? 64 - __clzll((long long)r) : 0;
-  return bits > 12 ? bits - 12 : 0;
+  constexpr int kLog = __builtin_ctz(kNB);
+  return bits > kLog ? bits - kLog : 0;
 }
 __device__ __forceinline__ bool key_less(unsigned long long an, unsigned ai, unsigned long long bn, unsigned bi) {
   return an < bn || (an == bn && ai < bi);
@@ -90,7 +98,7 @@ __device__ __forceinline__ bool key_less(unsigned long long an, unsigned ai, uns
 __global__ void k_bs_hist(const int32_t* n_dev, const NormKey* __restrict__ keys, const BucketState* st,
                           int* __restrict__ count) {
   pdl_wait();
-  __shared__ int h[kNB];
+  extern __shared__ int h[];   // kNB counters (dynamic shared memory)
   for (int b = threadIdx.x; b < kNB; b += blockDim.x) h[b] = 0;
   __syncthreads();
   const int n = *n_dev;
@@ -646,7 +654,14 @@ int bucket_rank(const char* W, const int32_t* n_dev, int n_max, double p_grad, c
   // keys -> k2 / v2; bucketed -> keys_in / vals_in; sorted -> keys_out / vals_out
   HG_L(k_norm_keys, grid_for(n_max, 256), 256, n_dev, n_max, p_grad, live, src_nodes, norms, k2, v2, k_out);
   HG_L(k_bs_minmax, g, 256, n_dev, (const NormKey*)k2, bst);
-  HG_L(k_bs_hist, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, count);
+  {
+    const int hs = ensure_smem_attr((const void*)k_bs_hist, 4 * kNB, W);
+    if (hs) return hs;
+    const cudaError_t _pe = hg::launch_pdl(k_bs_hist, dim3(g), dim3(256), (size_t)4 * kNB, stream, n_dev,
+                                           (const NormKey*)k2, (const BucketState*)bst, count);
+    if (_pe != cudaSuccess) return hg::fail(W, hg::kCuda, cudaGetErrorString(_pe));
+    HG_LAUNCHED(W);
+  }
   HG_L(k_bs_scan, 1, 1024, (const int*)count, off, cursor, big, bst);
   HG_L(k_bs_scatter, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, cursor, rb.keys_in, rb.vals_in);
   HG_L(k_bs_small, 148 * 8, 256, (const int*)off, (const NormKey*)rb.keys_in, (const int32_t*)rb.vals_in,
