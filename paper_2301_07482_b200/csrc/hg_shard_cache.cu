@@ -189,13 +189,12 @@ struct StoreNW {
   __device__ void operator()(int t) const { ctr[kCtrNWrite] = t; }
 };
 
-// first use of the owner's ring (cache.py:79-91 on the owner's node count)
-__global__ void k_sc_first_cap(long long* ctr, long long cap_fixed, long long window, long long n_owned,
-                               long long limit, long long min_cap) {
-  pdl_wait();
-  const long long nw = ctr[kCtrNWrite];
-  if (ctr[kCtrCapacity] != 0 || nw == 0) return;
-  long long cap;
+// first use of the owner's ring (cache.py:79-91 on the owner's node count):
+// every thread derives the same capacity; one writes it
+__device__ __forceinline__ long long sc_capacity(long long* ctr, long long nw, long long cap_fixed, long long window,
+                                                 long long n_owned, long long limit, long long min_cap) {
+  long long cap = ctr[kCtrCapacity];
+  if (cap != 0 || nw == 0) return cap;
   if (cap_fixed > 0) {
     cap = cap_fixed;
   } else if (window == 0) {   // t_stale = inf
@@ -207,16 +206,18 @@ __global__ void k_sc_first_cap(long long* ctr, long long cap_fixed, long long wi
     cap = cap > top ? top : cap;
   }
   if (cap > limit) cap = limit;
-  ctr[kCtrCapacity] = cap > 1 ? cap : 1;
+  return cap > 1 ? cap : 1;
 }
 
 __global__ void k_sc_release_writes(const int32_t* __restrict__ wlist, const int32_t* __restrict__ req_id,
                                     long long lo, int32_t* __restrict__ row_of, int32_t* __restrict__ row_owner,
-                                    long long* ctr) {
+                                    long long* ctr, long long cap_fixed, long long window, long long n_owned,
+                                    long long limit) {
   pdl_wait();
   const long long nw = ctr[kCtrNWrite];
   if (nw == 0) return;
-  const long long cap = ctr[kCtrCapacity];
+  const long long cap = sc_capacity(ctr, nw, cap_fixed, window, n_owned, limit, 64);
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr[kCtrCapacity] = cap;
   const long long w0 = nw >= cap ? nw - cap : 0;
   for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < nw - w0;
        w += (long long)gridDim.x * blockDim.x) {
@@ -292,36 +293,33 @@ __global__ void k_sc_write_rows(const int32_t* __restrict__ wlist, const int32_t
   }
 }
 
-__global__ void k_sc_commit(long long* ctr) {
+// commit (header, admissions, window, valid), retained refreshes and that
+// batch's end_iteration sweep (cache.py:206-211,330-334: t_int = 0 never)
+__global__ void k_sc_finish(const long long* __restrict__ hdr, const int32_t* __restrict__ req_id,
+                            const uint8_t* __restrict__ req_act, long long lo, long long hi,
+                            const int32_t* __restrict__ row_of, int32_t* __restrict__ admit_iter, int refresh,
+                            long long t_int, long long* ctr, long long limit) {
   pdl_wait();
-  const long long nw = ctr[kCtrNWrite];
-  if (nw == 0) return;
-  const long long cap = ctr[kCtrCapacity];
-  const bool wrap_all = nw >= cap;
-  const long long neff = wrap_all ? cap : nw;
-  ctr[kCtrHeader] = wrap_all ? neff % cap : (ctr[kCtrHeader] + nw) % cap;
-  ctr[kCtrAdmissions] += neff;
-  ctr[kCtrWindowAdmissions] += neff;
-  ctr[kCtrValid] += neff;
-}
-
-__global__ void k_sc_refresh(const long long* __restrict__ hdr, const int32_t* __restrict__ req_id,
-                             const uint8_t* __restrict__ req_act, long long lo, long long hi,
-                             const int32_t* __restrict__ row_of, int32_t* __restrict__ admit_iter) {
-  pdl_wait();
-  const long long k = __ldcg(hdr + 1);
-  const int it = (int)__ldcg(hdr + 2);
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (long long)gridDim.x * blockDim.x) {
-    if (__ldcg(req_act + j) != 2) continue;
-    const long long v = __ldcg(req_id + j);
-    if (v >= lo && v < hi && row_of[v - lo] >= 0) admit_iter[v - lo] = it;
+  if (refresh) {
+    const long long k = __ldcg(hdr + 1);
+    const int it = (int)__ldcg(hdr + 2);
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (long long)gridDim.x * blockDim.x) {
+      if (__ldcg(req_act + j) != 2) continue;
+      const long long v = __ldcg(req_id + j);
+      if (v >= lo && v < hi && row_of[v - lo] >= 0) admit_iter[v - lo] = it;
+    }
   }
-}
-
-// end_iteration(it) of the request's batch (cache.py:330-334): sweep when
-// t >= 1 and (it + 1) % t == 0 (t_int = 0: never)
-__global__ void k_sc_sweep(const long long* __restrict__ hdr, long long t_int, long long* ctr, long long limit) {
-  pdl_wait();
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const long long nw = ctr[kCtrNWrite];
+  if (nw != 0) {
+    const long long cap = ctr[kCtrCapacity];
+    const bool wrap_all = nw >= cap;
+    const long long neff = wrap_all ? cap : nw;
+    ctr[kCtrHeader] = wrap_all ? neff % cap : (ctr[kCtrHeader] + nw) % cap;
+    ctr[kCtrAdmissions] += neff;
+    ctr[kCtrWindowAdmissions] += neff;
+    ctr[kCtrValid] += neff;
+  }
   if (t_int < 1) return;
   const long long it = __ldcg(hdr + 2);
   if ((it + 1) % t_int != 0) return;
@@ -433,18 +431,14 @@ int hg_cache_apply(const long long* req_hdr, const int32_t* req_id, const uint8_
   const int s = scan_launch<int>(W, FlagU8{wflag}, HdrCount{req_hdr}, n_max, part, EmitCompact{wlist},
                                  StoreNW{layer_ctr}, stream);
   if (s) return s;
-  HG_SC_LAUNCH(W, k_sc_first_cap, 1, 1, layer_ctr, cap_fixed, window, n_owned, limit, 64ll);
   HG_SC_LAUNCH(W, k_sc_release_writes, grid_for(n_max, 256), 256, (const int32_t*)wlist, req_id, lo, row_of,
-               row_owner, layer_ctr);
+               row_owner, layer_ctr, cap_fixed, window, n_owned, limit);
   HG_SC_LAUNCH(W, k_sc_ring_scan, grid_for(n_max, 256), 256, req_hdr, t_stale, t_inf, lo, row_of, row_owner,
                (const int32_t*)admit_iter, layer_ctr);
   HG_SC_LAUNCH(W, k_sc_write_rows, grid_for(n_max * 32, 256, 148 * 16), 256, (const int32_t*)wlist, req_id, req_emb,
                req_hdr, row_words, lo, table, row_of, row_owner, admit_iter, layer_ctr);
-  HG_SC_LAUNCH(W, k_sc_commit, 1, 1, layer_ctr);
-  if (refresh_retained)
-    HG_SC_LAUNCH(W, k_sc_refresh, grid_for(n_max, 256), 256, req_hdr, req_id, req_act, lo, hi,
-                 (const int32_t*)row_of, admit_iter);
-  HG_SC_LAUNCH(W, k_sc_sweep, 1, 1, req_hdr, t_int, layer_ctr, limit);
+  HG_SC_LAUNCH(W, k_sc_finish, refresh_retained ? grid_for(n_max, 256) : 1u, refresh_retained ? 256 : 32, req_hdr,
+               req_id, req_act, lo, hi, (const int32_t*)row_of, admit_iter, refresh_retained, t_int, layer_ctr, limit);
   return kOk;
 }
 

@@ -255,6 +255,7 @@ class ShardedHistCache(HistCache):
         self.flags_dev = torch.tensor([b + flag_off for b in bases], dtype=torch.int64, device=self.device)
         self.bstate = torch.zeros(4, dtype=torch.int64, device=self.device)
         self.bstate[2] = int(timeout_s * 1e9)
+        self._streams = None
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
 
@@ -277,8 +278,16 @@ class ShardedHistCache(HistCache):
         requests and embedding rows, which the next step may overwrite, and
         the next lookups see the committed state)."""
         self._barrier(stream)
-        for lc in self.layers.values():
-            lc.commit_dev(stream)
+        # the layers' caches share no state: their apply chains run side by side
+        cur = torch.cuda.current_stream(self.device)
+        if self._streams is None:
+            self._streams = [torch.cuda.Stream(self.device) for _ in self.layers]
+        for cs, lc in zip(self._streams, self.layers.values()):
+            cs.wait_stream(cur)
+            with torch.cuda.stream(cs):
+                lc.commit_dev(_lib.stream_ptr(cs))
+        for cs in self._streams:
+            cur.wait_stream(cs)
         self._barrier(stream)
 
     @property
