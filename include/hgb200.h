@@ -272,9 +272,11 @@ int hg_cache_sweep(long long* layer_ctr, long long limit, cudaStream_t stream);
  *
  * hg_cache_request_reset: start of a step (hdr = {0, 0, *it_dev, 0}).
  * hg_cache_lookup_sharded: cache.py:103-129 as a pure read of every owner's
- *   state (pointer tables of P entries, peer mappings over CUDA IPC); hit rows
- *   copied to staging[loc] (hit_row[loc] = loc), expired ids appended to
- *   exp_ids (not invalidated: the owners apply them at commit).
+ *   state (pointer tables of P <= 32 entries, peer mappings over CUDA IPC);
+ *   hit_row[loc] = owner << 26 | ring row, expired ids appended to exp_ids
+ *   (not invalidated: the owners apply them at commit).
+ * hg_inject_rows_sharded: h_out[r] = the owner ring row of every flagged r
+ *   (tables = the P ring base pointers).
  * hg_cache_request: cache.py:188-191's admission rank of one batch as actions
  *   (0 evict-if-held, 1 write, 2 retained) in rank order; touches no state.
  * hg_cache_invalidate / hg_cache_apply: owner side of the commit: all ranks'
@@ -287,10 +289,11 @@ int hg_cache_sweep(long long* layer_ctr, long long limit, cudaStream_t stream);
 int hg_cache_request_reset(long long* req_hdr, const int32_t* it_dev, cudaStream_t stream);
 int hg_cache_lookup_sharded(const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
                             const int32_t* src_nodes, long long n_src_max, int P, const long long* bounds,
-                            const int32_t* const* row_of, const int32_t* const* admit_iter, const float* const* tables,
-                            int row_words, const int32_t* it_dev, double t_stale, uint8_t* hit_flag, int32_t* hit_row,
-                            float* staging, int32_t* exp_ids, long long* req_hdr, long long* layer_ctr,
-                            cudaStream_t stream);
+                            const int32_t* const* row_of, const int32_t* const* admit_iter, const int32_t* it_dev,
+                            double t_stale, uint8_t* hit_flag, int32_t* hit_row, int32_t* exp_ids, long long* req_hdr,
+                            long long* layer_ctr, cudaStream_t stream);
+int hg_inject_rows_sharded(const int32_t* n_dev, long long n_max, const uint8_t* flag, const int32_t* hit_row,
+                           const float* const* tables, int dim, float* h_out, cudaStream_t stream);
 int hg_cache_request(const int32_t* n_dev, int n_max, double p_grad, const int32_t* live, const int32_t* src_nodes,
                      const double* norms, const uint8_t* computed_flag, const float* emb, int row_words,
                      int32_t* req_id, uint8_t* req_act, int32_t* req_src, float* req_emb, long long* req_hdr,

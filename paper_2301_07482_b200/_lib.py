@@ -79,7 +79,8 @@ SIGNATURES = {
     "hg_cache_write": (I32, [I32, I32, I32, P, F64, I32, P, P, P, P, P, P, P, P, I64, P]),
     "hg_cache_sweep": (I32, [P, I64, P]),
     "hg_cache_request_reset": (I32, [P, P, P]),
-    "hg_cache_lookup_sharded": (I32, [P, I64, P, P, I64, I32, P, P, P, P, I32, P, F64, P, P, P, P, P, P, P]),
+    "hg_cache_lookup_sharded": (I32, [P, I64, P, P, I64, I32, P, P, P, P, F64, P, P, P, P, P, P]),
+    "hg_inject_rows_sharded": (I32, [P, I64, P, P, P, I32, P, P]),
     "hg_cache_request": (I32, [P, I32, F64, P, P, P, P, P, I32, P, P, P, P, P, P, I64, P]),
     "hg_cache_apply_scratch_bytes": (I64, [I64]),
     "hg_cache_invalidate": (I32, [I32, P, P, I64, I64, I64, P, P, P, P]),

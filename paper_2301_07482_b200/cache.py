@@ -218,6 +218,11 @@ class _LayerCache:
                   _lib.ptr(self.row_of_dev), _lib.ptr(self.admit_iter_dev), _lib.ptr(owner), _lib.ptr(it_dev),
                   self._t_stale(), _lib.ptr(hit_flag), _lib.ptr(hit_row), _lib.ptr(self.ctr), stream)
 
+    def injection(self, hit_flag, hit_row):
+        """The forward's Injection for this layer's hits (None before any admission)."""
+        from .nn import Injection
+        return None if self.table is None else Injection(hit_flag, hit_row, self.table)
+
     def _dummy_owner(self):
         if getattr(self, "_dummy", None) is None:
             self._dummy = torch.full((1,), -1, dtype=torch.int32, device=self.device)

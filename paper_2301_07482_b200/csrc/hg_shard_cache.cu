@@ -7,9 +7,9 @@
 // CUDA-IPC memory that every peer maps. One step:
 //   lookups   k_shard_lookup: pure reads of the owners' state after the
 //             previous step (cache.py:103-129 judged at the rank's own
-//             iteration), hit rows copied from the owner's table (NVLink on a
-//             multi-GPU box) into a rank-local staging table that the forward
-//             injects from; expired entries are only reported (exp list)
+//             iteration); hits are recorded as (owner, row) and injected by
+//             k_inject_sharded straight from the owner's ring (NVLink on a
+//             multi-GPU box); expired entries are only reported (exp list)
 //   request   hg_cache_request (hg_cache.cu): the batch-wide admission rank
 //             (cache.py:188-191) as per-position actions, in this rank's memory
 //   barrier A every rank's lookups and request done (hg_peer_barrier)
@@ -56,35 +56,31 @@ __device__ __forceinline__ int owner_of(const long long* __restrict__ bounds, in
 }
 
 // ---------------------------------------------------------------- lookups
-// one warp per 32 live positions: lane j resolves its id's owner / row /
-// freshness, then the warp copies the fresh rows (16-byte vectors) from the
-// owners' tables into staging[loc]
+// one thread per live position: owner, row and freshness of its id; a hit
+// is recorded as hit_row[loc] = owner << kOwnerShift | row and its row is
+// injected straight from the owner's ring (k_inject_sharded, one-sided NVLink
+// reads on a multi-GPU box); expired entries are only reported
+constexpr int kOwnerShift = 26;   // rows < 2^26 per owner ring, owners < 32
 __global__ void __launch_bounds__(256) k_shard_lookup(const int32_t* n_live_dev, const int32_t* __restrict__ live,
                                                       const int32_t* __restrict__ src_nodes, int P,
                                                       const long long* __restrict__ bounds,
                                                       const int32_t* const* __restrict__ row_of,
                                                       const int32_t* const* __restrict__ admit_iter,
-                                                      const float* const* __restrict__ tables, int row_words,
                                                       const int32_t* it_dev, double t_stale, int t_inf,
                                                       uint8_t* __restrict__ hit_flag, int32_t* __restrict__ hit_row,
-                                                      float* __restrict__ staging, int32_t* __restrict__ exp_ids,
-                                                      long long* req_hdr, long long* ctr) {
+                                                      int32_t* __restrict__ exp_ids, long long* req_hdr, long long* ctr) {
   pdl_wait();
   const int n = *n_live_dev;
   const int it = *it_dev;
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
   unsigned long long* c = reinterpret_cast<unsigned long long*>(ctr);
-  for (int j0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; j0 < n; j0 += warps * 32) {
-    const int j = j0 + lane;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j - (threadIdx.x & 31) < n; j += gridDim.x * blockDim.x) {
     bool fresh = false, expired = false;
-    int loc = 0, o = 0, row = -1;
     if (j < n) {
-      loc = live[j];
+      const int loc = live[j];
       const int v = src_nodes[loc];
-      o = owner_of(bounds, P, v);
+      const int o = owner_of(bounds, P, v);
       const long long li = (long long)v - bounds[o];
-      row = __ldcg(row_of[o] + li);
+      const int row = __ldcg(row_of[o] + li);
       if (row >= 0) {
         fresh = true;
         if (!t_inf) {
@@ -96,7 +92,7 @@ __global__ void __launch_bounds__(256) k_shard_lookup(const int32_t* n_live_dev,
         }
       }
       hit_flag[loc] = fresh;
-      hit_row[loc] = fresh ? loc : -1;
+      hit_row[loc] = fresh ? (int32_t)(((unsigned)o << kOwnerShift) | (unsigned)row) : -1;
       if (expired) {
         const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(req_hdr) + 3, 1ull);
         exp_ids[slot] = v;
@@ -104,17 +100,32 @@ __global__ void __launch_bounds__(256) k_shard_lookup(const int32_t* n_live_dev,
     }
     warp_count_add(c + kCtrHits, j < n && fresh);
     warp_count_add(c + kCtrMisses, j < n && !fresh);
-    unsigned m = __ballot_sync(0xffffffffu, fresh);
-    const int nv = row_words >> 2;
+  }
+}
+
+// h_out[r] = owner ring row of hit r (rows decoded from hit_row), a warp per
+// 32 output rows, 16-byte pieces
+__global__ void k_inject_sharded(const int32_t* n_dev, const uint8_t* __restrict__ flag,
+                                 const int32_t* __restrict__ hit_row, const float* const* __restrict__ tables, int dim,
+                                 float* __restrict__ h_out) {
+  pdl_wait();
+  const int n = *n_dev;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int nv = dim >> 2;
+  for (int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < n; r0 += warps * 32) {
+    const int r = r0 + lane;
+    const bool f = r < n && flag[r];
+    const int hr = f ? hit_row[r] : 0;
+    unsigned m = __ballot_sync(0xffffffffu, f);
     while (m) {
       const int q = __ffs(m) - 1;
       m &= m - 1;
-      const int qo = __shfl_sync(0xffffffffu, o, q);
-      const int qr = __shfl_sync(0xffffffffu, row, q);
-      const int ql = __shfl_sync(0xffffffffu, loc, q);
-      const uint4* s = reinterpret_cast<const uint4*>(tables[qo] + (long long)qr * row_words);
-      uint4* d = reinterpret_cast<uint4*>(staging + (long long)ql * row_words);
-      for (int x = lane; x < nv; x += 32) d[x] = __ldcg(s + x);
+      const unsigned code = (unsigned)__shfl_sync(0xffffffffu, hr, q);
+      const float* src = tables[code >> kOwnerShift] + (long long)(code & ((1u << kOwnerShift) - 1)) * dim;
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
+      uint4* d4 = reinterpret_cast<uint4*>(h_out + (long long)(r0 + q) * dim);
+      for (int x = lane; x < nv; x += 32) d4[x] = __ldcg(s4 + x);
     }
   }
 }
@@ -381,17 +392,24 @@ int hg_cache_request_reset(long long* req_hdr, const int32_t* it_dev, cudaStream
 
 int hg_cache_lookup_sharded(const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
                             const int32_t* src_nodes, long long n_src_max, int P, const long long* bounds,
-                            const int32_t* const* row_of, const int32_t* const* admit_iter, const float* const* tables,
-                            int row_words, const int32_t* it_dev, double t_stale, uint8_t* hit_flag, int32_t* hit_row,
-                            float* staging, int32_t* exp_ids, long long* req_hdr, long long* layer_ctr,
-                            cudaStream_t stream) {
+                            const int32_t* const* row_of, const int32_t* const* admit_iter, const int32_t* it_dev,
+                            double t_stale, uint8_t* hit_flag, int32_t* hit_row, int32_t* exp_ids, long long* req_hdr,
+                            long long* layer_ctr, cudaStream_t stream) {
   const char* W = "hg_cache_lookup_sharded";
-  if (P < 1 || P > 64 || row_words < 4 || (row_words & 3)) return fail(W, kBadArg, "bad world size / row width");
+  if (P < 1 || P > 32) return fail(W, kBadArg, "bad world size (1..32)");
   HG_CHECK_CUDA(W, cudaMemsetAsync(hit_flag, 0, (size_t)(n_src_max > 0 ? n_src_max : 1), stream));
   if (n_live_max <= 0) return kOk;
-  HG_SC_LAUNCH(W, k_shard_lookup, grid_for(n_live_max, 256, 148 * 8), 256, n_live_dev, live, src_nodes, P, bounds,
-               row_of, admit_iter, tables, row_words, it_dev, t_stale, std::isinf(t_stale) ? 1 : 0, hit_flag, hit_row,
-               staging, exp_ids, req_hdr, layer_ctr);
+  HG_SC_LAUNCH(W, k_shard_lookup, grid_for(n_live_max, 256), 256, n_live_dev, live, src_nodes, P, bounds, row_of,
+               admit_iter, it_dev, t_stale, std::isinf(t_stale) ? 1 : 0, hit_flag, hit_row, exp_ids, req_hdr,
+               layer_ctr);
+  return kOk;
+}
+
+int hg_inject_rows_sharded(const int32_t* n_dev, long long n_max, const uint8_t* flag, const int32_t* hit_row,
+                           const float* const* tables, int dim, float* h_out, cudaStream_t stream) {
+  if (dim < 4 || (dim & 3)) return fail("hg_inject_rows_sharded", kBadArg, "rows must be a multiple of 4 floats");
+  HG_SC_LAUNCH("hg_inject_rows_sharded", k_inject_sharded, grid_for(n_max * 32, 256, 148 * 16), 256, n_dev, flag,
+               hit_row, tables, dim, h_out);
   return kOk;
 }
 

@@ -339,9 +339,10 @@ class StepEngine:
                 hit_row = torch.empty(blk.num_src, dtype=torch.int32, device=dev)
                 lc.lookup_dev(counts[2 * b + 1:2 * b + 2], blk.num_src, live[b], blk.src_nodes, blk.num_src, self.it,
                               hit_flag, hit_row, sp)
-                if lc.table is not None:
+                inj = lc.injection(hit_flag, hit_row)
+                if inj is not None:
                     inj_flag = hit_flag
-                    injected[b - 1] = Injection(hit_flag, hit_row, lc.table)
+                    injected[b - 1] = inj
             self._mark(f"pruned{b}", stream)
 
         def R_dev(b):

@@ -302,9 +302,11 @@ class Injection:
     """Rows of a block output served from a table instead of computed."""
 
     flag: torch.Tensor          # uint8 [n_dst]
-    row: torch.Tensor           # int32 [n_dst] row in `table`
-    table: torch.Tensor         # [*, d_out] fp32
+    row: torch.Tensor           # int32 [n_dst] row in `table` (owner << 26 | row with `tables`)
+    table: torch.Tensor         # [*, d_out] fp32 (None when the rows live in the owners' rings)
     locals_dev: torch.Tensor | None = None
+    tables: torch.Tensor | None = None   # int64 [P] ring base pointers (owner-sharded cache)
+    dim: int = 0                          # row width of the rings (with `tables`)
 
 
 def load_features_dev(n_live_dev, n_max: int, live, src_nodes, feature_row_of, region, feats, dim: int,
@@ -413,8 +415,7 @@ def gat_layer_forward_dev(net: Network, l: int, blk, h_in, rows, R, R_dev, act, 
               _lib.ptr(h_out), _lib.ptr(mx), _lib.ptr(ssum), stream)
     if inj is not None:
         nd = n_dst_dev if n_dst_dev is not None else _dev_count(n_dst, dev)
-        _lib.call("hg_inject_rows", _lib.ptr(nd), n_dst, _lib.ptr(inj.flag),
-                  _lib.ptr(inj.row), _lib.ptr(inj.table), HF, _lib.ptr(h_out), stream)
+        inject_rows_dev(inj, h_out, n_dst, nd, stream)
     return GatTape(rows, R, R_dev, A, d_in, act, h_out, inj, z=z, el=el, er=er, mx=mx, ssum=ssum, live=live,
                    n_live=n_live, n_live_dev=n_live_dev, heads=H)
 
@@ -487,6 +488,10 @@ def gat_layer_backward_dev(net: Network, l: int, blk, t: GatTape, d_h, grads, ne
 
 
 def inject_rows_dev(inj: Injection, h_out: torch.Tensor, n_dst: int, n_dst_dev, stream) -> None:
+    if inj.tables is not None:       # owner-sharded cache: straight from the owners' rings
+        _lib.call("hg_inject_rows_sharded", _lib.ptr(n_dst_dev), n_dst, _lib.ptr(inj.flag), _lib.ptr(inj.row),
+                  _lib.ptr(inj.tables), int(h_out.shape[1]), _lib.ptr(h_out), stream)
+        return
     """h_out[r] = table[row[r]] for the injected rows (nn.py:290-293)."""
     _lib.call("hg_inject_rows", _lib.ptr(n_dst_dev), n_dst, _lib.ptr(inj.flag), _lib.ptr(inj.row),
               _lib.ptr(inj.table), int(h_out.shape[1]), _lib.ptr(h_out), stream)

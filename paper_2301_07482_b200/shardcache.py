@@ -8,9 +8,9 @@ rank's per-step request area (admission actions, expired ids, header). The
 semantics (oracle/shardcache.py, the oracle the tests pin this against):
 
   lookups   pure reads of the owners' state after the previous step, at the
-            rank's own iteration; hit rows are copied from the owner's table
-            (one-sided NVLink reads on a multi-GPU box) into a rank-local
-            staging table the forward injects from; expiries are reported
+            rank's own iteration; hits are injected straight from the owner's
+            ring (one-sided NVLink reads on a multi-GPU box); expiries are
+            reported
   request   the batch-wide admission rank, published in the rank's memory
   commit    after a device barrier: each owner applies every rank's expiries,
             then the P requests in rank (= batch index) order restricted to
@@ -66,8 +66,11 @@ class ShardedLayerCache(_LayerCache):
         self.cap_fixed = -1 if self.policy.capacity is None else min(-(-self.policy.capacity // P), self.limit_rows)
         self.rows_alloc = self.limit_rows
         self.ctr = torch.zeros(LAYER_CTR_LEN, dtype=torch.int64, device=self.device)
-        # rank-local staging of this step's hit rows (the forward's injection table)
-        self.table = torch.zeros((max(1, self.n_req), dim), dtype=torch.float32, device=self.device)
+        if self.limit_rows >= 1 << 26 or owner.world > 32:
+            raise ValueError("the sharded cache encodes hits as owner << 26 | row: rings < 2^26 rows, <= 32 ranks")
+        # hits are injected straight from the owners' rings (hg_inject_rows_sharded);
+        # `table` is a placeholder so a captured step sees a stable key
+        self.table = torch.zeros((1, dim), dtype=torch.float32, device=self.device)
 
     # section sizes of this layer in the IPC block (bytes)
     def sections(self):
@@ -143,9 +146,12 @@ class ShardedLayerCache(_LayerCache):
         o = self.owner
         _lib.call("hg_cache_lookup_sharded", _lib.ptr(n_dev), n_max, _lib.ptr(live), _lib.ptr(src_nodes), n_src_max,
                   o.world, _lib.ptr(o.bounds_dev), _lib.ptr(self.peer_row_of), _lib.ptr(self.peer_admit),
-                  _lib.ptr(self.peer_ring), self.dim, _lib.ptr(it_dev), float(self.policy.t_stale),
-                  _lib.ptr(hit_flag), _lib.ptr(hit_row), _lib.ptr(self.table), _lib.ptr(self.exp_ids),
-                  _lib.ptr(self.hdr), _lib.ptr(self.ctr), stream)
+                  _lib.ptr(it_dev), float(self.policy.t_stale), _lib.ptr(hit_flag), _lib.ptr(hit_row),
+                  _lib.ptr(self.exp_ids), _lib.ptr(self.hdr), _lib.ptr(self.ctr), stream)
+
+    def injection(self, hit_flag, hit_row):
+        from .nn import Injection
+        return Injection(hit_flag, hit_row, None, tables=self.peer_ring, dim=self.dim)
 
     def update_dev(self, n_dev, n_max, live, src_nodes, norms, computed_flag, emb, it_dev, refresh_retained,
                    stream, allow_alloc=True, mark=None):

@@ -218,7 +218,14 @@ class PrunedBatch:
             return None
         f = inj.flag.bool()
         loc = torch.nonzero(f).flatten()
-        vals = inj.table[inj.row[loc].long()]
+        if inj.tables is not None:       # owner-sharded: read the rows through the injection kernel
+            from .nn import inject_rows_dev
+            n = int(inj.flag.shape[0])
+            buf = torch.empty((n, inj.dim), dtype=torch.float32, device=inj.flag.device)
+            inject_rows_dev(inj, buf, n, torch.tensor([n], dtype=torch.int32, device=buf.device), _lib.stream_ptr())
+            vals = buf[loc]
+        else:
+            vals = inj.table[inj.row[loc].long()]
         return _np(loc).astype(np.int64), _np(vals)
 
 
@@ -263,9 +270,10 @@ def prune_with_cache(sub: LayeredSubgraph, cache: HistCache, current_iter: int, 
             hit_row = torch.empty(n_src, dtype=torch.int32, device=dev)
             lc.lookup_dev(counts[2 * b + 1:2 * b + 2], n_src, lv, blk.src_nodes, n_src, it_dev, hit_flag,
                           hit_row, sp)
-            if lc.table is not None:
+            inj = lc.injection(hit_flag, hit_row)
+            if inj is not None:
                 inj_flag = hit_flag
-                injected[b - 1] = Injection(hit_flag, hit_row, lc.table)
+                injected[b - 1] = inj
     host = counts.cpu().tolist()
     cnt = []
     for b in range(L):
