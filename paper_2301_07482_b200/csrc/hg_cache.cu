@@ -111,38 +111,57 @@ __global__ void k_bs_hist(const int32_t* n_dev, const NormKey* __restrict__ keys
     if (h[b]) atomicAdd(&count[b], h[b]);
 }
 
-// exclusive offsets of the kNB bucket counts (one CTA), cursors, big-bucket list
+// exclusive offsets of the kNB bucket counts (one CTA), cursors, big-bucket
+// list. Warp w owns buckets [w kNB/32, (w+1) kNB/32), read 32 at a time
+// (coalesced) and scanned with shuffles; one shared-memory pass over the 32
+// warp totals
 __global__ void __launch_bounds__(1024) k_bs_scan(const int* __restrict__ count, int* __restrict__ off,
                                                   int* __restrict__ cursor, int* __restrict__ big, BucketState* st) {
   pdl_wait();
-  __shared__ int part[1024];
+  constexpr int kPerWarp = kNB / 32;
+  constexpr int kRounds = kPerWarp / 32;
+  __shared__ int wtot[32];
   __shared__ int nbig;
-  constexpr int kPer = kNB / 1024;
-  int v[kPer], s = 0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) nbig = 0;
+  int v[kRounds], incl[kRounds];
+  int carry = 0;
 #pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    v[q] = count[threadIdx.x * kPer + q];
-    s += v[q];
+  for (int q = 0; q < kRounds; ++q) {
+    const int x = count[w * kPerWarp + q * 32 + lane];
+    int xs = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, xs, d);
+      if (lane >= d) xs += t;
+    }
+    v[q] = x;
+    incl[q] = carry + xs;
+    carry += __shfl_sync(0xffffffffu, xs, 31);
   }
-  part[threadIdx.x] = s;
+  if (lane == 0) wtot[w] = carry;
   __syncthreads();
-  for (int d = 1; d < 1024; d <<= 1) {
-    const int t = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
-    __syncthreads();
-    part[threadIdx.x] += t;
-    __syncthreads();
-  }
-  int run = part[threadIdx.x] - s;
+  if (w == 0) {
+    const int t = wtot[lane];
+    int ts = t;
 #pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    const int b = threadIdx.x * kPer + q;
-    off[b] = run;
-    cursor[b] = run;
-    if (v[q] > kBucketCap) big[atomicAdd(&nbig, 1)] = b;
-    run += v[q];
+    for (int d = 1; d < 32; d <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, ts, d);
+      if (lane >= d) ts += u;
+    }
+    wtot[lane] = ts - t;   // exclusive prefix of the warps
   }
-  if (threadIdx.x == 1023) off[kNB] = run;
+  __syncthreads();
+  const int base = wtot[w];
+#pragma unroll
+  for (int q = 0; q < kRounds; ++q) {
+    const int b = w * kPerWarp + q * 32 + lane;
+    const int e = base + incl[q] - v[q];
+    off[b] = e;
+    cursor[b] = e;
+    if (v[q] > kBucketCap) big[atomicAdd(&nbig, 1)] = b;
+  }
+  if (w == 31 && lane == 31) off[kNB] = base + incl[kRounds - 1];
   __syncthreads();
   if (threadIdx.x == 0) st->n_big = nbig;
 }
