@@ -40,6 +40,10 @@ from .sharding import _DevBuf
 _HDR_WORDS = 8
 
 
+class ShardingUnavailable(RuntimeError):
+    """Raised on every rank when some rank cannot map its peers' cache shards."""
+
+
 def _align(n: int, a: int = 256) -> int:
     return (n + a - 1) // a * a
 
@@ -247,14 +251,32 @@ class ShardedHistCache(HistCache):
         handles = [None] * self.world
         dist.all_gather_object(handles, bytes(h.raw), group=group)
         bases, self._opened = [], []
+        err = None
         for r in range(self.world):
             if r == self.rank:
                 bases.append(p.value)
                 continue
             q = ctypes.c_void_p()
-            _lib.call("hg_ipc_open", ctypes.create_string_buffer(handles[r], hb), ctypes.byref(q))
+            try:
+                _lib.call("hg_ipc_open", ctypes.create_string_buffer(handles[r], hb), ctypes.byref(q))
+            except _lib.HgError as e:       # e.g. no peer access between these GPUs
+                err = e
+                break
             bases.append(q.value)
             self._opened.append(q.value)
+        # every rank learns whether every rank mapped every peer, so all fall back together
+        ok = torch.tensor([0 if err is not None else 1], dtype=torch.int32,
+                          device=self.device if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            for q in self._opened:
+                _lib.call("hg_ipc_close", ctypes.c_void_p(q))
+            self._opened = []
+            dist.barrier(group=group)
+            _lib.call("hg_device_free", ctypes.c_void_p(self._owned))
+            self._owned = None
+            raise ShardingUnavailable(f"owner-sharded cache needs CUDA IPC peer mappings on every rank "
+                                      f"({err if err is not None else 'failed on a peer rank'})")
         for lc, d in zip(self.layers.values(), offs):
             lc.bind(p.value, d, bases)
         self.my_flag = p.value + flag_off
