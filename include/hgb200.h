@@ -210,7 +210,7 @@ int hg_cross_entropy(const float* logits, const int32_t* labels, int B, int C, f
 /* ---- K8 backward: nn.py:166-177,300-320 (_layer_backward, backward) */
 int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* d_h, const float* h_out,
                  int dout, int relu, void* dz_ts, cudaStream_t stream);
-long long hg_csc_scratch_bytes(long long E_max);
+long long hg_csc_scratch_bytes(long long E_max, long long n_src_max);
 int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t* keep, const int32_t* pos_of,
                  const int32_t* col, long long E_max, long long n_src_max, unsigned* keys_sorted,
                  unsigned* vals_sorted, int32_t* seg_lo, int32_t* seg_hi, void* scratch, long long scratch_bytes,

@@ -19,7 +19,6 @@
 // trees for the fp64 norms, so every run is bit-identical.
 #include "hgb200.h"
 #include <cuda_fp16.h>
-#include <cub/device/device_radix_sort.cuh>
 
 #include "hg_scan.cuh"
 #include "hg_state.h"
@@ -338,40 +337,161 @@ __global__ void __launch_bounds__(256) k_gather_dz(const int32_t* R_dev, const i
     for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK * 4, plane, i, g, zeros);
 }
 
-// CSC keys over the block's original edge extents: surviving edges keep their
-// source column, pruned rows' edges (and the tail up to E_max) get the sentinel.
-__global__ void k_csc_keys(const int32_t* n_dst_dev, const int32_t* __restrict__ blk_off,
-                           const uint8_t* __restrict__ keep, const int32_t* __restrict__ pos_of,
-                           const int32_t* __restrict__ col, long long E_max, unsigned sentinel,
-                           unsigned* __restrict__ keys, unsigned* __restrict__ vals) {
+// Transposed (CSC) view of the surviving edges of a pruned block, built
+// without a library sort and sized by the surviving edges (not the block's
+// upper bound): per-source counts (atomics), their exclusive scan (segment
+// offsets), placement of each surviving edge's dst position at an atomic
+// cursor, then every segment sorted ascending. The values of a segment are
+// the compute positions pos_of[row], increasing with the dst row, so the
+// sorted segment is the stable CSR-order transpose (ascending dst rows, the
+// order the fixed-order accumulation of k_transpose_agg relies on).
+constexpr int kCscSmall = 16;     // segments up to this length: one thread sorts in registers
+constexpr int kCscChunk = 4096;   // CTA shared-memory sort of larger segments
+
+__global__ void k_csc_count(const int32_t* n_dst_dev, const int32_t* __restrict__ blk_off,
+                            const uint8_t* __restrict__ keep, const int32_t* __restrict__ col,
+                            int32_t* __restrict__ cnt) {
   pdl_wait();
   const int n = *n_dst_dev;
-  const long long E = blk_off[n];
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long str = (long long)gridDim.x * blockDim.x;
-  for (long long r = tid; r < n; r += str) {
-    const bool k = keep[r];
-    const unsigned p = (unsigned)pos_of[r];
-    for (int e = blk_off[r]; e < blk_off[r + 1]; ++e) {
-      keys[e] = k ? (unsigned)col[e] : sentinel;
-      vals[e] = p;
-    }
-  }
-  for (long long e = E + tid; e < E_max; e += str) {
-    keys[e] = sentinel;
-    vals[e] = 0u;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    if (!keep[r]) continue;
+    for (int e = blk_off[r]; e < blk_off[r + 1]; ++e) atomicAdd(&cnt[col[e]], 1);
   }
 }
 
-__global__ void k_csc_segments(const unsigned* __restrict__ keys, long long E_max, unsigned sentinel,
-                               int32_t* __restrict__ seg_lo, int32_t* __restrict__ seg_hi) {
+struct CscCount {
+  const int32_t* cnt;
+  __device__ int operator()(long long i) const { return cnt[i]; }
+};
+struct EmitCsc {
+  int32_t* seg_lo;
+  int32_t* seg_hi;
+  int32_t* cursor;
+  __device__ void operator()(long long i, int excl, int v) const {
+    seg_lo[i] = excl;
+    cursor[i] = excl;
+    seg_hi[i] = excl + v;
+  }
+};
+struct NoTotal {
+  __device__ void operator()(int) const {}
+};
+
+__global__ void k_csc_place(const int32_t* n_dst_dev, const int32_t* __restrict__ blk_off,
+                            const uint8_t* __restrict__ keep, const int32_t* __restrict__ pos_of,
+                            const int32_t* __restrict__ col, int32_t* __restrict__ cursor,
+                            unsigned* __restrict__ vals) {
   pdl_wait();
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < E_max;
-       p += (long long)gridDim.x * blockDim.x) {
-    const unsigned k = keys[p];
-    if (k == sentinel) continue;
-    if (p == 0 || keys[p - 1] != k) seg_lo[k] = (int32_t)p;
-    if (p == E_max - 1 || keys[p + 1] != k) seg_hi[k] = (int32_t)(p + 1);
+  const int n = *n_dst_dev;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    if (!keep[r]) continue;
+    const unsigned p = (unsigned)pos_of[r];
+    for (int e = blk_off[r]; e < blk_off[r + 1]; ++e) vals[atomicAdd(&cursor[col[e]], 1)] = p;
+  }
+}
+
+// segments of <= kCscSmall values: insertion sort in registers, one thread
+// each; longer ones are listed for k_csc_sort_big
+__global__ void k_csc_sort_small(long long n_src, const int32_t* __restrict__ seg_lo,
+                                 const int32_t* __restrict__ seg_hi, unsigned* __restrict__ vals,
+                                 int32_t* __restrict__ big, int32_t* n_big) {
+  pdl_wait();
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n_src; c += (long long)gridDim.x * blockDim.x) {
+    const int lo = seg_lo[c], len = seg_hi[c] - lo;
+    if (len < 2) continue;
+    if (len > kCscSmall) {
+      big[atomicAdd(n_big, 1)] = (int32_t)c;
+      continue;
+    }
+    unsigned v[kCscSmall];
+#pragma unroll
+    for (int k = 0; k < kCscSmall; ++k) v[k] = k < len ? vals[lo + k] : 0xffffffffu;
+#pragma unroll
+    for (int k = 1; k < kCscSmall; ++k) {
+#pragma unroll
+      for (int q = k; q > 0; --q) {
+        const unsigned a = v[q - 1], b = v[q];
+        v[q - 1] = a < b ? a : b;
+        v[q] = a < b ? b : a;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kCscSmall; ++k)
+      if (k < len) vals[lo + k] = v[k];
+  }
+}
+
+__device__ __forceinline__ void smem_bitonic_u32(unsigned* sv, int m) {
+  for (int size = 2; size <= m; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (m >> 1); t += blockDim.x) {
+        const int a = 2 * t - (t & (stride - 1));
+        const int b = a + stride;
+        const bool up = (a & size) == 0;
+        if ((sv[b] < sv[a]) == up) {
+          const unsigned x = sv[a];
+          sv[a] = sv[b];
+          sv[b] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// one CTA per long segment: chunks of kCscChunk sorted in shared memory,
+// then bottom-up merge passes between vals and tmp (merge path split per thread)
+__global__ void __launch_bounds__(512) k_csc_sort_big(const int32_t* __restrict__ big, const int32_t* n_big,
+                                                      const int32_t* __restrict__ seg_lo,
+                                                      const int32_t* __restrict__ seg_hi, unsigned* __restrict__ vals,
+                                                      unsigned* __restrict__ tmp) {
+  pdl_wait();
+  __shared__ unsigned sv[kCscChunk];
+  const int nb = *n_big;
+  for (int q = blockIdx.x; q < nb; q += gridDim.x) {
+    const int c = big[q];
+    const int lo = seg_lo[c], len = seg_hi[c] - lo;
+    for (int c0 = 0; c0 < len; c0 += kCscChunk) {
+      const int n = len - c0 < kCscChunk ? len - c0 : kCscChunk;
+      int m = 32;
+      while (m < n) m <<= 1;
+      for (int t = threadIdx.x; t < m; t += blockDim.x) sv[t] = t < n ? vals[lo + c0 + t] : 0xffffffffu;
+      __syncthreads();
+      smem_bitonic_u32(sv, m);
+      for (int t = threadIdx.x; t < n; t += blockDim.x) vals[lo + c0 + t] = sv[t];
+      __syncthreads();
+    }
+    unsigned* src = vals + lo;
+    unsigned* dst = tmp + lo;
+    bool in_tmp = false;
+    for (int w = kCscChunk; w < len; w <<= 1) {
+      for (int p0 = 0; p0 < len; p0 += 2 * w) {
+        const int na = len - p0 < w ? len - p0 : w;
+        const int nb2 = len - p0 - na < w ? (len - p0 - na > 0 ? len - p0 - na : 0) : w;
+        const unsigned* A = src + p0;
+        const unsigned* B = A + na;
+        const int tot = na + nb2;
+        const int per = (tot + blockDim.x - 1) / blockDim.x;
+        const int d0 = threadIdx.x * per < tot ? threadIdx.x * per : tot;
+        const int d1 = d0 + per < tot ? d0 + per : tot;
+        int l2 = d0 > nb2 ? d0 - nb2 : 0, h2 = d0 < na ? d0 : na;
+        while (l2 < h2) {      // merge path: items of A among the first d0
+          const int mid = (l2 + h2) >> 1;
+          if (A[mid] <= B[d0 - 1 - mid]) l2 = mid + 1;
+          else h2 = mid;
+        }
+        int ia = l2, ib = d0 - l2;
+        for (int d = d0; d < d1; ++d) dst[p0 + d] = (ib >= nb2 || (ia < na && A[ia] <= B[ib])) ? A[ia++] : B[ib++];
+      }
+      __syncthreads();
+      unsigned* t2 = src;
+      src = dst;
+      dst = t2;
+      in_tmp = !in_tmp;
+    }
+    if (in_tmp)
+      for (int t = threadIdx.x; t < len; t += blockDim.x) vals[lo + t] = tmp[lo + t];
+    __syncthreads();
   }
 }
 
@@ -577,39 +697,49 @@ int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, con
   return kOk;
 }
 
-long long hg_csc_scratch_bytes(long long E_max) {
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const unsigned*)nullptr, (unsigned*)nullptr,
-                                  (const unsigned*)nullptr, (unsigned*)nullptr, (int)(E_max > 0 ? E_max : 1), 0, 32);
-  // keys_in, vals_in, keys_out, vals_out + cub temp
-  return (long long)(4 * 4 * (E_max + 16)) + (long long)tmp + 1024;
+long long hg_csc_scratch_bytes(long long E_max, long long n_src_max) {
+  // cursors + long-segment list + its count + scan partials + merge buffer
+  return (n_src_max + 16) * 4 * 2 + 64 + (scan_tiles(n_src_max) + 1) * 4 + (E_max + 16) * 4 + 1024;
 }
 
-// Transposed (CSC) view of the surviving edges of a pruned block, sorted by
-// source column (stable: ascending dst-row order inside every segment).
+// Transposed (CSC) view of the surviving edges of a pruned block: for every
+// source c, vals[seg_lo[c] .. seg_hi[c]) = the compute positions of the kept
+// dst rows that sampled it, ascending (k_csc_count / scan / k_csc_place /
+// k_csc_sort_small / k_csc_sort_big; no library sort, work sized by the
+// surviving edges). keys_sorted is unused (kept for the ABI).
 int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t* keep, const int32_t* pos_of,
                  const int32_t* col, long long E_max, long long n_src_max, unsigned* keys_sorted,
                  unsigned* vals_sorted, int32_t* seg_lo, int32_t* seg_hi, void* scratch, long long scratch_bytes,
                  cudaStream_t stream) {
   const char* W = "hg_build_csc";
-  if (scratch_bytes < hg_csc_scratch_bytes(E_max)) return fail(W, kBadArg, "scratch too small");
-  unsigned* keys_in = reinterpret_cast<unsigned*>(scratch);
-  unsigned* vals_in = keys_in + (E_max + 16);
-  void* tmp = vals_in + (E_max + 16);
-  size_t tmp_bytes = (size_t)(scratch_bytes - 2 * 4 * (E_max + 16));
-  const unsigned sentinel = (unsigned)n_src_max;
-  int bits = 1;
-  while ((1ll << bits) <= (long long)sentinel) ++bits;
-  HG_CHECK_CUDA(W, cudaMemsetAsync(seg_lo, 0, (size_t)n_src_max * 4, stream));
+  (void)keys_sorted;
+  if (scratch_bytes < hg_csc_scratch_bytes(E_max, n_src_max)) return fail(W, kBadArg, "scratch too small");
+  if (n_src_max <= 0) return kOk;
+  char* p = reinterpret_cast<char*>(scratch);
+  int32_t* cursor = reinterpret_cast<int32_t*>(p);
+  int32_t* big = cursor + (n_src_max + 16);
+  int32_t* n_big = big + (n_src_max + 16);
+  int* part = reinterpret_cast<int*>(reinterpret_cast<char*>(n_big) + 64);
+  unsigned* tmp = reinterpret_cast<unsigned*>(part + scan_tiles(n_src_max) + 1);
+  // counts accumulate in seg_hi (overwritten by the scan's emit)
   HG_CHECK_CUDA(W, cudaMemsetAsync(seg_hi, 0, (size_t)n_src_max * 4, stream));
-  if (E_max == 0) return kOk;
-  { const cudaError_t _pe = hg::launch_pdl(k_csc_keys, dim3(grid_for(E_max, 256)), dim3(256), 0, stream, n_dst_dev, blk_off, keep, pos_of, col, E_max, sentinel,
-                                                       keys_in, vals_in); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  HG_CHECK_CUDA(W, cudaMemsetAsync(n_big, 0, 4, stream));
+  const long long n_dst_max = n_src_max;   // dst rows are a prefix of the sources
+  HG_CHECK_CUDA(W, hg::launch_pdl(k_csc_count, dim3(grid_for(n_dst_max, 256)), dim3(256), 0, stream, n_dst_dev,
+                                  blk_off, keep, col, seg_hi));
   HG_LAUNCHED(W);
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_sorted, vals_in, vals_sorted,
-                                                  (int)E_max, 0, bits, stream);
-  if (e != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(e));
-  { const cudaError_t _pe = hg::launch_pdl(k_csc_segments, dim3(grid_for(E_max, 256)), dim3(256), 0, stream, keys_sorted, E_max, sentinel, seg_lo, seg_hi); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  const int sc = scan_launch<int>(W, CscCount{seg_hi}, ConstCount{n_src_max}, n_src_max, part,
+                                  EmitCsc{seg_lo, seg_hi, cursor}, NoTotal{}, stream);
+  if (sc) return sc;
+  HG_CHECK_CUDA(W, hg::launch_pdl(k_csc_place, dim3(grid_for(n_dst_max, 256)), dim3(256), 0, stream, n_dst_dev,
+                                  blk_off, keep, pos_of, col, cursor, vals_sorted));
+  HG_LAUNCHED(W);
+  HG_CHECK_CUDA(W, hg::launch_pdl(k_csc_sort_small, dim3(grid_for(n_src_max, 256)), dim3(256), 0, stream, n_src_max,
+                                  (const int32_t*)seg_lo, (const int32_t*)seg_hi, vals_sorted, big, n_big));
+  HG_LAUNCHED(W);
+  HG_CHECK_CUDA(W, hg::launch_pdl(k_csc_sort_big, dim3(148), dim3(512), 0, stream, (const int32_t*)big,
+                                  (const int32_t*)n_big, (const int32_t*)seg_lo, (const int32_t*)seg_hi, vals_sorted,
+                                  tmp));
   HG_LAUNCHED(W);
   return kOk;
 }

@@ -614,7 +614,7 @@ def build_csc(blk, keep: torch.Tensor, pos_of: torch.Tensor, n_dst_dev, stream, 
     vals = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
     seg_lo = torch.empty(max(n_src, 1), dtype=torch.int32, device=dev)
     seg_hi = torch.empty(max(n_src, 1), dtype=torch.int32, device=dev)
-    sb = _lib.query("hg_csc_scratch_bytes", E)
+    sb = _lib.query("hg_csc_scratch_bytes", E, n_src)
     if scratch is None or scratch.numel() < sb:
         scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
     _lib.call("hg_build_csc", _lib.ptr(n_dst_dev), _lib.ptr(blk.blk_off), _lib.ptr(keep), _lib.ptr(pos_of),
