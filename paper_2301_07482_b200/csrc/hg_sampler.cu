@@ -23,6 +23,10 @@
 #include <cstdlib>
 #include <mutex>
 #include "hg_pcg.cuh"
+
+#ifndef HG_SEL_PREFIX
+#define HG_SEL_PREFIX 1
+#endif
 #include "hg_scan.cuh"
 
 namespace hg {
@@ -171,6 +175,51 @@ __device__ __forceinline__ void sort_first_chunk(unsigned long long& k, long lon
   else if (deg > 2) bitonic_sort_u64<4>(k);
   else bitonic_sort_u64<2>(k);
 }
+
+// ascending bitonic sort of every group of kSpan lanes of 32-bit values
+template <int kSpan>
+__device__ __forceinline__ void bitonic_sort_u32(unsigned& v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= kSpan; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const bool ascending = size == kSpan || (lane & size) == 0;
+      const unsigned p = __shfl_xor_sync(0xffffffffu, v, stride);
+      const bool keep_min = ((lane & stride) == 0) == ascending;
+      if (keep_min ? (p < v) : (v < p)) v = p;
+    }
+  }
+}
+
+// The first chunk of a row (lane j holds key53 << 11 | j, lanes >= deg ~0),
+// sorted ascending. Sorts 32-bit (top 27 key bits, lane) words -- half the
+// shuffles and compares of the 64-bit network -- then fetches each rank's
+// full key from its lane. Two valid keys sharing their top 27 bits (about
+// 1 row in 10^5) make the order ambiguous: then the exact 64-bit network
+// runs instead, so the result is always the (key53, j) order.
+#if HG_SEL_PREFIX
+__device__ __forceinline__ void sort_first_chunk_fast(unsigned long long& key, long long deg) {
+  const int lane = threadIdx.x & 31;
+  unsigned v = ((unsigned)(key >> 37) << 5) | (unsigned)lane;
+  if (deg > 16) bitonic_sort_u32<32>(v);
+  else if (deg > 8) bitonic_sort_u32<16>(v);
+  else if (deg > 4) bitonic_sort_u32<8>(v);
+  else if (deg > 2) bitonic_sort_u32<4>(v);
+  else bitonic_sort_u32<2>(v);
+  const unsigned prev = __shfl_up_sync(0xffffffffu, v, 1);
+  const bool tie = lane > 0 && lane < deg && (prev >> 5) == (v >> 5);
+  if (__any_sync(0xffffffffu, tie)) {
+    sort_first_chunk(key, deg);
+    return;
+  }
+  key = __shfl_sync(0xffffffffu, key, (int)(v & 31u));
+}
+#else
+__device__ __forceinline__ void sort_first_chunk_fast(unsigned long long& key, long long deg) {
+  sort_first_chunk(key, deg);
+}
+#endif
 
 // jump with the per-batch constants C = inc * S precomputed (one 128-bit
 // multiply-add per non-zero nibble of the offset)
@@ -365,7 +414,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select(
             unsigned long long key = valid ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
             if (c + 32 < deg) s = fma128(a32, s, c32);
             if (c == 0) {
-              sort_first_chunk(key, deg);
+              sort_first_chunk_fast(key, deg);
               best = key;
               continue;
             }
@@ -490,7 +539,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select_huge(
       unsigned long long key = valid ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
       if (c + 32 < len) s = fma128(a32, s, c32);
       if (c == 0) {
-        sort_first_chunk(key, len);
+        sort_first_chunk_fast(key, len);
         best = key;
         continue;
       }
