@@ -27,6 +27,9 @@
 #ifndef HG_SEL_PREFIX
 #define HG_SEL_PREFIX 1
 #endif
+#ifndef HG_SEL_PAIRS
+#define HG_SEL_PAIRS 1
+#endif
 #include "hg_scan.cuh"
 
 namespace hg {
@@ -221,6 +224,29 @@ __device__ __forceinline__ void sort_first_chunk_fast(unsigned long long& key, l
 }
 #endif
 
+// Two short rows in one warp pass (lanes 0-15 row q, 16-31 row q+1; each
+// row's lanes j < deg valid): every kSpan group sorted ascending by (key53, j),
+// via the 32-bit prefix words with the same exact fallback on prefix ties.
+__device__ __forceinline__ void sort_pair_fast(unsigned long long& key, long long span, long long dh) {
+  const int lane = threadIdx.x & 31;
+  unsigned v = ((unsigned)(key >> 37) << 5) | (unsigned)lane;
+  if (span > 8) bitonic_sort_u32<16>(v);
+  else if (span > 4) bitonic_sort_u32<8>(v);
+  else if (span > 2) bitonic_sort_u32<4>(v);
+  else bitonic_sort_u32<2>(v);
+  const unsigned prev = __shfl_up_sync(0xffffffffu, v, 1);
+  const int jl = lane & 15;
+  const bool tie = jl > 0 && jl < dh && (prev >> 5) == (v >> 5);
+  if (__any_sync(0xffffffffu, tie)) {
+    if (span > 8) bitonic_sort_u64<16>(key);
+    else if (span > 4) bitonic_sort_u64<8>(key);
+    else if (span > 2) bitonic_sort_u64<4>(key);
+    else bitonic_sort_u64<2>(key);
+    return;
+  }
+  key = __shfl_sync(0xffffffffu, key, (int)(v & 31u));
+}
+
 // jump with the per-batch constants C = inc * S precomputed (one 128-bit
 // multiply-add per non-zero nibble of the offset)
 struct JumpTableC {
@@ -404,6 +430,36 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select(
           first = delta <= 32ull ? fma128(dA[delta], cur, dC[delta]) : pcg_jump_c(tab, cur, delta);
         }
         have = false;
+#if HG_SEL_PAIRS
+        // two short consecutive rows share one pass: their candidates are
+        // consecutive in the stream, so row q+1's lanes take the states of
+        // lanes deg .. deg+15 of this jump (the layouts of C3-like graphs,
+        // m = 7, are dominated by rows of <= 16 candidates)
+        if (kSmallFanout && deg <= 16 && q + 1 < nr) {
+          const long long deg2 = __shfl_sync(0xffffffffu, deg_l, q + 1);
+          if (deg2 >= 1 && deg2 <= 16) {
+            const long long lo2 = __shfl_sync(0xffffffffu, lo_l, q + 1);
+            const int out2 = __shfl_sync(0xffffffffu, out_l, q + 1);
+            const int count2 = (int)(deg2 < fanout ? deg2 : fanout);
+            const int srcl = lane < 16 ? lane : (int)deg + lane - 16;
+            u128 st;
+            st.hi = __shfl_sync(0xffffffffu, first.hi, srcl);
+            st.lo = __shfl_sync(0xffffffffu, first.lo, srcl);
+            const int jl = lane & 15;
+            const long long dh = lane < 16 ? deg : deg2;
+            unsigned long long key = jl < dh ? ((pcg_key53(st) << 11) | (unsigned long long)jl) : ~0ull;
+            sort_pair_fast(key, deg > deg2 ? deg : deg2, dh);
+            const int ch = lane < 16 ? count : count2;
+            if (jl < ch)
+              put_pick(src_flat, col_local, (lane < 16 ? out0 : out2) + jl, (lane < 16 ? lo : lo2) + (long long)(key & 2047ull));
+            cur = first;
+            cur_pos = k0;
+            have = true;
+            ++q;     // row q+1 done
+            continue;
+          }
+        }
+#endif
         if (kSmallFanout && deg <= 2048) {
           // fast path: (key53, j) packed into one u64, j < 2^11
           unsigned long long best = ~0ull;
