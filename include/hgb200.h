@@ -310,6 +310,14 @@ int hg_cache_apply(const long long* req_hdr, const int32_t* req_id, const uint8_
 int hg_peer_signal(unsigned long long* my_flag, unsigned long long* state, cudaStream_t stream);
 int hg_peer_wait(unsigned long long* const* flags, int P, unsigned long long* state, cudaStream_t stream);
 
+/* ---- full-graph CSR2 on the device: histgnn/graphs.py:161-172 (build_csr2):
+ * rows by destination, input edge order inside a row; counts + scan + atomic
+ * placement + per-row sort of the edge indices (csrc/hg_graph.cu), no library
+ * sort. src / dst int32 device arrays of E edges (N < 2^31, E < 2^32). */
+long long hg_build_csr2_scratch_bytes(long long E, long long N);
+int hg_build_csr2(const int32_t* src, const int32_t* dst, long long E, long long N, int64_t* start, int64_t* end,
+                  int32_t* col, void* scratch, long long scratch_bytes, cudaStream_t stream);
+
 /* ---- dataset ingest, host side (csrc/hg_ingest.cu):
  * multi-threaded parsers of the reference's text formats over a read-only
  * mapping of the file. Call once with out / src / dst = NULL to count, then

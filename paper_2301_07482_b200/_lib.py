@@ -90,6 +90,8 @@ SIGNATURES = {
     "hg_degree_order_scratch_bytes": (I64, [I64]),
     "hg_feature_region": (I32, [P, P, I64, I64, P, P, P, I64, P]),
     "hg_synth_power_law": (I64, [I64, I32, P, P, P]),
+    "hg_build_csr2_scratch_bytes": (I64, [I64, I64]),
+    "hg_build_csr2": (I32, [P, P, I64, I64, P, P, P, P, I64, P]),
     "hg_parse_int_lines": (I32, [S, I64, P, P, P, P, P, I32]),
     "hg_parse_edge_list": (I32, [S, P, P, P, P, P, P, P, I32]),
     "hg_ts_bytes": (I64, [I64, I32]),

@@ -21,6 +21,7 @@
 #include <cuda_fp16.h>
 
 #include "hg_scan.cuh"
+#include "hg_segsort.cuh"
 #include "hg_state.h"
 #include "hg_ts.cuh"
 
@@ -345,8 +346,6 @@ __global__ void __launch_bounds__(256) k_gather_dz(const int32_t* R_dev, const i
 // the compute positions pos_of[row], increasing with the dst row, so the
 // sorted segment is the stable CSR-order transpose (ascending dst rows, the
 // order the fixed-order accumulation of k_transpose_agg relies on).
-constexpr int kCscSmall = 16;     // segments up to this length: one thread sorts in registers
-constexpr int kCscChunk = 4096;   // CTA shared-memory sort of larger segments
 
 __global__ void k_csc_count(const int32_t* n_dst_dev, const int32_t* __restrict__ blk_off,
                             const uint8_t* __restrict__ keep, const int32_t* __restrict__ col,
@@ -387,111 +386,6 @@ __global__ void k_csc_place(const int32_t* n_dst_dev, const int32_t* __restrict_
     if (!keep[r]) continue;
     const unsigned p = (unsigned)pos_of[r];
     for (int e = blk_off[r]; e < blk_off[r + 1]; ++e) vals[atomicAdd(&cursor[col[e]], 1)] = p;
-  }
-}
-
-// segments of <= kCscSmall values: insertion sort in registers, one thread
-// each; longer ones are listed for k_csc_sort_big
-__global__ void k_csc_sort_small(long long n_src, const int32_t* __restrict__ seg_lo,
-                                 const int32_t* __restrict__ seg_hi, unsigned* __restrict__ vals,
-                                 int32_t* __restrict__ big, int32_t* n_big) {
-  pdl_wait();
-  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n_src; c += (long long)gridDim.x * blockDim.x) {
-    const int lo = seg_lo[c], len = seg_hi[c] - lo;
-    if (len < 2) continue;
-    if (len > kCscSmall) {
-      big[atomicAdd(n_big, 1)] = (int32_t)c;
-      continue;
-    }
-    unsigned v[kCscSmall];
-#pragma unroll
-    for (int k = 0; k < kCscSmall; ++k) v[k] = k < len ? vals[lo + k] : 0xffffffffu;
-#pragma unroll
-    for (int k = 1; k < kCscSmall; ++k) {
-#pragma unroll
-      for (int q = k; q > 0; --q) {
-        const unsigned a = v[q - 1], b = v[q];
-        v[q - 1] = a < b ? a : b;
-        v[q] = a < b ? b : a;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kCscSmall; ++k)
-      if (k < len) vals[lo + k] = v[k];
-  }
-}
-
-__device__ __forceinline__ void smem_bitonic_u32(unsigned* sv, int m) {
-  for (int size = 2; size <= m; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < (m >> 1); t += blockDim.x) {
-        const int a = 2 * t - (t & (stride - 1));
-        const int b = a + stride;
-        const bool up = (a & size) == 0;
-        if ((sv[b] < sv[a]) == up) {
-          const unsigned x = sv[a];
-          sv[a] = sv[b];
-          sv[b] = x;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// one CTA per long segment: chunks of kCscChunk sorted in shared memory,
-// then bottom-up merge passes between vals and tmp (merge path split per thread)
-__global__ void __launch_bounds__(512) k_csc_sort_big(const int32_t* __restrict__ big, const int32_t* n_big,
-                                                      const int32_t* __restrict__ seg_lo,
-                                                      const int32_t* __restrict__ seg_hi, unsigned* __restrict__ vals,
-                                                      unsigned* __restrict__ tmp) {
-  pdl_wait();
-  __shared__ unsigned sv[kCscChunk];
-  const int nb = *n_big;
-  for (int q = blockIdx.x; q < nb; q += gridDim.x) {
-    const int c = big[q];
-    const int lo = seg_lo[c], len = seg_hi[c] - lo;
-    for (int c0 = 0; c0 < len; c0 += kCscChunk) {
-      const int n = len - c0 < kCscChunk ? len - c0 : kCscChunk;
-      int m = 32;
-      while (m < n) m <<= 1;
-      for (int t = threadIdx.x; t < m; t += blockDim.x) sv[t] = t < n ? vals[lo + c0 + t] : 0xffffffffu;
-      __syncthreads();
-      smem_bitonic_u32(sv, m);
-      for (int t = threadIdx.x; t < n; t += blockDim.x) vals[lo + c0 + t] = sv[t];
-      __syncthreads();
-    }
-    unsigned* src = vals + lo;
-    unsigned* dst = tmp + lo;
-    bool in_tmp = false;
-    for (int w = kCscChunk; w < len; w <<= 1) {
-      for (int p0 = 0; p0 < len; p0 += 2 * w) {
-        const int na = len - p0 < w ? len - p0 : w;
-        const int nb2 = len - p0 - na < w ? (len - p0 - na > 0 ? len - p0 - na : 0) : w;
-        const unsigned* A = src + p0;
-        const unsigned* B = A + na;
-        const int tot = na + nb2;
-        const int per = (tot + blockDim.x - 1) / blockDim.x;
-        const int d0 = threadIdx.x * per < tot ? threadIdx.x * per : tot;
-        const int d1 = d0 + per < tot ? d0 + per : tot;
-        int l2 = d0 > nb2 ? d0 - nb2 : 0, h2 = d0 < na ? d0 : na;
-        while (l2 < h2) {      // merge path: items of A among the first d0
-          const int mid = (l2 + h2) >> 1;
-          if (A[mid] <= B[d0 - 1 - mid]) l2 = mid + 1;
-          else h2 = mid;
-        }
-        int ia = l2, ib = d0 - l2;
-        for (int d = d0; d < d1; ++d) dst[p0 + d] = (ib >= nb2 || (ia < na && A[ia] <= B[ib])) ? A[ia++] : B[ib++];
-      }
-      __syncthreads();
-      unsigned* t2 = src;
-      src = dst;
-      dst = t2;
-      in_tmp = !in_tmp;
-    }
-    if (in_tmp)
-      for (int t = threadIdx.x; t < len; t += blockDim.x) vals[lo + t] = tmp[lo + t];
-    __syncthreads();
   }
 }
 
@@ -734,14 +628,7 @@ int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t
   HG_CHECK_CUDA(W, hg::launch_pdl(k_csc_place, dim3(grid_for(n_dst_max, 256)), dim3(256), 0, stream, n_dst_dev,
                                   blk_off, keep, pos_of, col, cursor, vals_sorted));
   HG_LAUNCHED(W);
-  HG_CHECK_CUDA(W, hg::launch_pdl(k_csc_sort_small, dim3(grid_for(n_src_max, 256)), dim3(256), 0, stream, n_src_max,
-                                  (const int32_t*)seg_lo, (const int32_t*)seg_hi, vals_sorted, big, n_big));
-  HG_LAUNCHED(W);
-  HG_CHECK_CUDA(W, hg::launch_pdl(k_csc_sort_big, dim3(148), dim3(512), 0, stream, (const int32_t*)big,
-                                  (const int32_t*)n_big, (const int32_t*)seg_lo, (const int32_t*)seg_hi, vals_sorted,
-                                  tmp));
-  HG_LAUNCHED(W);
-  return kOk;
+  return segsort_launch<int32_t>(W, n_src_max, seg_lo, seg_hi, vals_sorted, tmp, big, n_big, stream);
 }
 
 int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, const int32_t* live,

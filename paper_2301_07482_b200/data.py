@@ -90,16 +90,25 @@ def synth_power_law_host(n: int, rng: np.random.Generator, m: int = 3, feature_d
 
 
 def csr2_from_edges_device(src: np.ndarray, dst: np.ndarray, n: int, device="cuda") -> Csr2Graph:
-    """In-neighbour CSR2 with stable in-row order (graphs.py:161-172), on the GPU."""
-    d = torch.as_tensor(dst, device=device).long()
-    s = torch.as_tensor(src, device=device)
-    counts = torch.bincount(d, minlength=n)
-    ptr = torch.zeros(n + 1, dtype=torch.int64, device=device)
-    torch.cumsum(counts, 0, out=ptr[1:])
-    order = torch.sort(d, stable=True).indices
-    col = s[order].to(torch.int32).contiguous()
-    del d, s, order
-    return Csr2Graph(ptr[:-1].clone(), ptr[1:].clone(), col, n)
+    """In-neighbour CSR2 with stable in-row order (graphs.py:161-172), built on
+    the GPU by hg_build_csr2 (counts, scan, placement, per-row sort of the
+    edge indices; no library sort)."""
+    _lib.require_cuda()
+    dev = torch.device(device)
+    s = torch.as_tensor(np.ascontiguousarray(src, dtype=np.int32) if isinstance(src, np.ndarray) else src,
+                        device=dev).to(torch.int32).contiguous()
+    d = torch.as_tensor(np.ascontiguousarray(dst, dtype=np.int32) if isinstance(dst, np.ndarray) else dst,
+                        device=dev).to(torch.int32).contiguous()
+    E = int(s.numel())
+    start = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    end = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    col = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+    sb = _lib.query("hg_build_csr2_scratch_bytes", E, max(n, 1))
+    scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+    _lib.call("hg_build_csr2", _lib.ptr(s), _lib.ptr(d), E, max(n, 1), _lib.ptr(start), _lib.ptr(end),
+              _lib.ptr(col), _lib.ptr(scratch), sb, _lib.stream_ptr())
+    del scratch, s, d
+    return Csr2Graph(start[:n], end[:n], col[:E], n)
 
 
 def synth_power_law_native(n: int, m: int, feature_dim: int, classes: int, seed: int = 0,

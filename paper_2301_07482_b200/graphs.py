@@ -127,20 +127,13 @@ class Csr2Graph:
 
 def build_csr2(edges: CooGraph, device=None) -> Csr2Graph:
     """graphs.py:161-172 — group edges by destination, stable within a row,
-    built on the GPU (counting by bincount, stable sort by destination)."""
+    built on the GPU (hg_build_csr2: counts, scan, placement, per-row sort)."""
     _lib.require_cuda()
-    dev = torch.device(device or "cuda")
     n = edges.num_nodes
     if n >= 2**31:
         raise ValueError("node ids must fit int32 on the device")
-    dst = torch.as_tensor(edges.dst, device=dev)
-    src = torch.as_tensor(edges.src, device=dev)
-    counts = torch.bincount(dst, minlength=n)
-    ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    torch.cumsum(counts, 0, out=ptr[1:])
-    order = torch.sort(dst, stable=True).indices
-    col = src[order].to(torch.int32)
-    return Csr2Graph(ptr[:-1].clone(), ptr[1:].clone(), col, n)
+    from .data import csr2_from_edges_device
+    return csr2_from_edges_device(edges.src, edges.dst, n, torch.device(device or "cuda"))
 
 
 def csr2_from_arrays(start, end, col, device=None) -> Csr2Graph:
