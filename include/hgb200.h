@@ -128,7 +128,7 @@ int hg_ipc_close(void* p);
  * _mean_matrix, _layer_forward_ctx). kind 0 = GCN, 1 = SAGE_MEAN. */
 int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
                      const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
-                     const float* h_in, int d, void* A_ts, cudaStream_t stream);
+                     const float* h_in, int d, void* A_ts, float* row_w, cudaStream_t stream);
 /* K5 fused into K6 (layer 0): hg_resolve_feature_rows writes rowp[live[i]]
  * = the address of live source i's feature row (static region row, table row
  * or owner-shard row over NVLink; shard_ptrs NULL = unsharded `feats`) with
@@ -143,7 +143,8 @@ int hg_resolve_feature_rows(const int32_t* n_live_dev, long long n_live_max, con
                             long long* global_ctr, long long* owner_rows, cudaStream_t stream);
 int hg_aggregate_fwd_rows(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
                           const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
-                          const unsigned long long* rowp, int dtype, int d, void* A_ts, cudaStream_t stream);
+                          const unsigned long long* rowp, int dtype, int d, void* A_ts, float* row_w,
+                          cudaStream_t stream);
 
 /* ---- K7 on tcgen05 over TS operands (bf16 hi/lo core-matrix tiles in HBM, written by
  * hg_aggregate_fwd / hg_gather_dz / hg_ts_pack; layout in csrc/hg_ts.cuh). Each K-chunk
@@ -217,12 +218,15 @@ int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t
                  cudaStream_t stream);
 /* K8 + K9 fused: transposed aggregation + nn.py:346-349 (node_grad_norms) */
 /* need_row (uint8 per source row, may be NULL): rows with 0 get their fp64
- * norm only, no gradient row (the next layer does not compute them) */
+ * norm only, no gradient row (the next layer does not compute them);
+ * row_w (SAGE, may be NULL): the per-compute-row mean weights 1/cnt written
+ * by hg_aggregate_fwd[_rows] (row_w there, may be NULL) */
 int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
                      const int32_t* seg_lo, const int32_t* seg_hi, const unsigned* vals_sorted, const int32_t* rows,
                      const int32_t* start, const int32_t* end, const int32_t* dst_deg, const int32_t* src_deg,
                      const int32_t* n_dst_dev, const int32_t* pos_of, const float* SG, int ldSG, int d,
-                     float* d_in, double* norms, const uint8_t* need_row, cudaStream_t stream);
+                     float* d_in, double* norms, const uint8_t* need_row, const float* row_w,
+                     cudaStream_t stream);
 int hg_row_norms(const float* x, long long n, int d, double* out, cudaStream_t stream);
 
 /* ---- K11 optimizer: nn.py:355-360 (sgd_step) */

@@ -61,8 +61,8 @@ SIGNATURES = {
     "hg_gat_param_scratch_bytes": (I64, [I32]),
     "hg_gat_param_grads": (I32, [I64, I64, I32, P, P, P, P, P, P]),
     "hg_gat_scatter_norms": (I32, [P, I64, P, P, I32, P, P, P]),
-    "hg_aggregate_fwd": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, P, P]),
-    "hg_aggregate_fwd_rows": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, I32, P, P]),
+    "hg_aggregate_fwd": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, P, P, P]),
+    "hg_aggregate_fwd_rows": (I32, [I32, P, I64, P, P, P, P, P, P, P, I32, I32, P, P, P]),
     "hg_resolve_feature_rows": (I32, [P, I64, P, P, P, P, P, P, P, I32, I32, I32, I32, P, P, P, P]),
     "hg_scatter_rows": (I32, [P, I64, P, P, I32, I32, P, P]),
     "hg_inject_rows": (I32, [P, I64, P, P, P, I32, P, P]),
@@ -70,7 +70,7 @@ SIGNATURES = {
     "hg_gather_dz": (I32, [P, I64, P, P, P, I32, I32, P, P]),
     "hg_csc_scratch_bytes": (I64, [I64, I64]),
     "hg_build_csc": (I32, [P, P, P, P, P, I64, I64, P, P, P, P, P, I64, P]),
-    "hg_transpose_agg": (I32, [I32, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P, P]),
+    "hg_transpose_agg": (I32, [I32, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P, P, P]),
     "hg_row_norms": (I32, [P, I64, I32, P, P]),
     "hg_sgd": (I32, [P, P, I64, F32, P]),
     "hg_p2p_allreduce_sgd": (I32, [P, P, I64, P, P, P, P, I32, P, F32, P]),

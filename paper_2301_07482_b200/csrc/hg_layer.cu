@@ -86,13 +86,19 @@ __device__ __forceinline__ float4 row_vec(const void* base, int v) {
 // one warp per compute row; kT = float4 vectors per lane (d <= 128 kT); the
 // [self | agg | 1 | pad] row is staged in dynamic shared memory (row_floats
 // per warp) before it is emitted as TS core rows
+// HG_ROW_W=0: the transposed SAGE aggregation recomputes 1/cnt per edge (A/B)
+#ifndef HG_ROW_W
+#define HG_ROW_W 1
+#endif
+
 template <int kKind, int kT, int kSrc>
 __global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
                                                    const unsigned long long* __restrict__ rowp,
-                                                   int d, uint8_t* __restrict__ A_ts, long long plane, int row_floats) {
+                                                   int d, uint8_t* __restrict__ A_ts, long long plane, int row_floats,
+                                                   float* __restrict__ row_w) {
   pdl_wait();
   extern __shared__ __align__(16) float agg_smem[];
   const int R = *R_dev;
@@ -134,7 +140,10 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(co
 #pragma unroll
     for (int t = 0; t < kT; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     float cs = 0.f;
-    if (kKind == kKindSAGE) cs = cnt > 0 ? (float)(1.0 / (double)cnt) : 0.f;
+    if (kKind == kKindSAGE) {
+      cs = cnt > 0 ? (float)(1.0 / (double)cnt) : 0.f;
+      if (row_w && lane == 0) row_w[i] = cs;   // the backward's per-row mean weight
+    }
     const int dd = kKind == kKindGCN ? dst_deg[r] : 0;
     int e = e0;
     for (; e + 4 <= e1; e += 4) {
@@ -397,7 +406,7 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_a
     const int32_t* __restrict__ start, const int32_t* __restrict__ end, const int32_t* __restrict__ dst_deg,
     const int32_t* __restrict__ src_deg, const int32_t* n_dst_dev, const int32_t* __restrict__ pos_of,
     const float* __restrict__ SG, int ldSG, int d, float* __restrict__ d_in, double* __restrict__ norms,
-    const uint8_t* __restrict__ need_row) {
+    const uint8_t* __restrict__ need_row, const float* __restrict__ row_w) {
   pdl_wait();
   const int n = *n_live_dev;
   const int n_dst = *n_dst_dev;
@@ -416,13 +425,15 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_a
     const int sd = kKind == kKindGCN ? src_deg[c] : 0;
     for (int p = p0; p < p1; ++p) {
       const int pos = (int)srt_vals[p];
-      const int r = rows[pos];
       float w;
-      if (kKind == kKindSAGE) {
+      if (kKind == kKindSAGE && HG_ROW_W && row_w) {
+        w = row_w[pos];                       // 1 / cnt of the row, from the forward
+      } else if (kKind == kKindSAGE) {
+        const int r = rows[pos];
         const int cnt = end[r] - start[r];
         w = (float)(1.0 / (double)cnt);
       } else {
-        w = gcn_coef(dst_deg[r], sd);
+        w = gcn_coef(dst_deg[rows[pos]], sd);
       }
       const float4* g = reinterpret_cast<const float4*>(SG + (long long)pos * ldSG + goff);
 #pragma unroll
@@ -501,7 +512,7 @@ extern "C" {
 static int aggregate_launch(const char* W, int kind, int src, const int32_t* R_dev, long long R_max,
                             const int32_t* rows, const int32_t* start, const int32_t* end, const int32_t* col,
                             const int32_t* dst_deg, const int32_t* src_deg, const float* h_in,
-                            const unsigned long long* rowp, int d, void* A_ts, cudaStream_t stream) {
+                            const unsigned long long* rowp, int d, void* A_ts, float* row_w, cudaStream_t stream) {
   if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 1024");
   // grid covers the compute rows and the zero padding up to the next 128-row tile
   const long long rows_pad = (R_max + kTsRows - 1) / kTsRows * kTsRows;
@@ -520,7 +531,7 @@ static int aggregate_launch(const char* W, int kind, int src, const int32_t* R_d
       if (pe != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(pe));                                      \
     }                                                                                                            \
     pe = hg::launch_pdl(k_aggregate<KIND, T, S>, dim3(grid), dim3(256), smem, stream, R_dev, rows, start, end,    \
-                        col, dst_deg, src_deg, h_in, rowp, d, a, plane, row_floats);                             \
+                        col, dst_deg, src_deg, h_in, rowp, d, a, plane, row_floats, row_w);                      \
   }
 #define HG_AGG_T(KIND, S)                                                                                         \
   if (vpl <= 1) HG_AGG(KIND, 1, S) else if (vpl <= 2) HG_AGG(KIND, 2, S) else if (vpl <= 4) HG_AGG(KIND, 4, S)   \
@@ -542,19 +553,20 @@ static int aggregate_launch(const char* W, int kind, int src, const int32_t* R_d
 
 int hg_aggregate_fwd(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
                      const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
-                     const float* h_in, int d, void* A_ts, cudaStream_t stream) {
+                     const float* h_in, int d, void* A_ts, float* row_w, cudaStream_t stream) {
   return aggregate_launch("hg_aggregate_fwd", kind, 0, R_dev, R_max, rows, start, end, col, dst_deg, src_deg, h_in,
-                          nullptr, d, A_ts, stream);
+                          nullptr, d, A_ts, row_w, stream);
 }
 
 // layer 0 over feature rows read in place (rowp from hg_resolve_feature_rows);
 // dtype 0 = fp32 table, 1 = fp16; d = the table's (padded) row width
 int hg_aggregate_fwd_rows(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
                           const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
-                          const unsigned long long* rowp, int dtype, int d, void* A_ts, cudaStream_t stream) {
+                          const unsigned long long* rowp, int dtype, int d, void* A_ts, float* row_w,
+                          cudaStream_t stream) {
   if (dtype == 1 && d % 8) return fail("hg_aggregate_fwd_rows", kBadArg, "fp16 rows need d % 8 == 0");
   return aggregate_launch("hg_aggregate_fwd_rows", kind, dtype == 1 ? 2 : 1, R_dev, R_max, rows, start, end, col,
-                          dst_deg, src_deg, nullptr, rowp, d, A_ts, stream);
+                          dst_deg, src_deg, nullptr, rowp, d, A_ts, row_w, stream);
 }
 
 int hg_scatter_rows(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* Z, int dout, int relu,
@@ -635,7 +647,8 @@ int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, 
                      const int32_t* seg_lo, const int32_t* seg_hi, const unsigned* vals_sorted, const int32_t* rows,
                      const int32_t* start, const int32_t* end, const int32_t* dst_deg, const int32_t* src_deg,
                      const int32_t* n_dst_dev, const int32_t* pos_of, const float* SG, int ldSG, int d,
-                     float* d_in, double* norms, const uint8_t* need_row, cudaStream_t stream) {
+                     float* d_in, double* norms, const uint8_t* need_row, const float* row_w,
+                     cudaStream_t stream) {
   const char* W = "hg_transpose_agg";
   if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 1024");
   const unsigned grid = grid_for(n_live_max * 32, 256, 148 * 16);
@@ -644,7 +657,7 @@ int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, 
 #define HG_TA(KIND, T)                                                                                            \
   pe = hg::launch_pdl(k_transpose_agg<KIND, T>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, seg_lo, seg_hi,  \
                       vals_sorted, rows, start, end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d, d_in, norms, \
-                      need_row)
+                      need_row, row_w)
 #define HG_TA_T(KIND)                                                                                             \
   if (vpl <= 1) HG_TA(KIND, 1); else if (vpl <= 2) HG_TA(KIND, 2); else if (vpl <= 4) HG_TA(KIND, 4);           \
   else HG_TA(KIND, 8);

@@ -268,6 +268,7 @@ class LayerTape:
     relu: bool
     h_out: torch.Tensor         # [n_dst, d_out] (dead rows unwritten)
     inj: object = None          # Injection or None
+    row_w: torch.Tensor | None = None   # fp32 [R] SAGE mean weights 1/cnt (the backward's edge weights)
 
     @property
     def valid_rows(self) -> torch.Tensor:
@@ -520,14 +521,17 @@ def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch
     # GEMM operand [self | agg | 1] written by the aggregation directly as TS
     # (bf16 hi/lo core-matrix tiles, csrc/hg_ts.cuh)
     A = torch.empty(ts_bytes(R, K + 1), dtype=torch.uint8, device=dev)
+    # SAGE: the forward hands the backward its per-row weights 1/cnt
+    row_w = torch.empty(max(R, 1), dtype=torch.float32, device=dev) if kind == KIND_SAGE and l > 0 else None
     if isinstance(h_in, FeatureRows):     # layer 0 reading the feature rows in place
         _lib.call("hg_aggregate_fwd_rows", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(blk.adj.start),
                   _lib.ptr(blk.adj.end), _lib.ptr(blk.adj.col_indices), _lib.ptr(blk.dst_deg),
-                  _lib.ptr(blk.src_deg), _lib.ptr(h_in.rowp), h_in.dtype_code, d_in, _lib.ptr(A), stream)
+                  _lib.ptr(blk.src_deg), _lib.ptr(h_in.rowp), h_in.dtype_code, d_in, _lib.ptr(A),
+                  _lib.ptr(row_w), stream)
     else:
         _lib.call("hg_aggregate_fwd", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(blk.adj.start),
                   _lib.ptr(blk.adj.end), _lib.ptr(blk.adj.col_indices), _lib.ptr(blk.dst_deg),
-                  _lib.ptr(blk.src_deg), _lib.ptr(h_in), d_in, _lib.ptr(A), stream)
+                  _lib.ptr(blk.src_deg), _lib.ptr(h_in), d_in, _lib.ptr(A), _lib.ptr(row_w), stream)
     if PT is None:
         PT = pack_forward_weights(net, l, stream)
     n_dst = blk.num_dst
@@ -539,7 +543,7 @@ def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch
     if inj is not None and not injected_already:
         nd = n_dst_dev if n_dst_dev is not None else _dev_count(n_dst, dev)
         inject_rows_dev(inj, h_out, n_dst, nd, stream)
-    return LayerTape(rows, R, R_dev, A, K, act, h_out, inj)
+    return LayerTape(rows, R, R_dev, A, K, act, h_out, inj, row_w)
 
 
 def ts_bytes(rows: int, cols: int) -> int:
@@ -702,7 +706,7 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
               _lib.ptr(csc.seg_lo), _lib.ptr(csc.seg_hi), _lib.ptr(csc.vals), _lib.ptr(t.rows),
               _lib.ptr(blk.adj.start), _lib.ptr(blk.adj.end), _lib.ptr(blk.dst_deg), _lib.ptr(blk.src_deg),
               _lib.ptr(n_dst_dev), _lib.ptr(pos_of), _lib.ptr(SG), K, d_in_dim, _lib.ptr(d_in), _lib.ptr(norms),
-              _lib.ptr(need_rows), stream)
+              _lib.ptr(need_rows), _lib.ptr(t.row_w), stream)
     return d_in, norms[:n_live]
 
 

@@ -853,7 +853,7 @@ def full_graph_logits(network: Network, graph, features, chunk_rows: int | None 
             rows = every[r0:r0 + R]
             _lib.call("hg_aggregate_fwd", kind, _lib.ptr(R_dev), R, _lib.ptr(rows), _lib.ptr(start), _lib.ptr(end),
                       _lib.ptr(g.col_indices), _lib.ptr(deg), _lib.ptr(zero if l == 0 else deg), _lib.ptr(h), d_in,
-                      _lib.ptr(A), sp)
+                      _lib.ptr(A), None, sp)
             _lib.call("hg_ts_linear_fwd", _lib.ptr(R_dev), R, _lib.ptr(A), K + 1, _lib.ptr(PT), d_out, _lib.ptr(rows),
                       int(l < L - 1), _lib.ptr(h_out), sp)
         h = h_out
