@@ -27,9 +27,6 @@
 #ifndef HG_SEL_PREFIX
 #define HG_SEL_PREFIX 1
 #endif
-#ifndef HG_SEL_PAIRS
-#define HG_SEL_PAIRS 1
-#endif
 #include "hg_scan.cuh"
 
 namespace hg {
@@ -224,29 +221,6 @@ __device__ __forceinline__ void sort_first_chunk_fast(unsigned long long& key, l
 }
 #endif
 
-// Two short rows in one warp pass (lanes 0-15 row q, 16-31 row q+1; each
-// row's lanes j < deg valid): every kSpan group sorted ascending by (key53, j),
-// via the 32-bit prefix words with the same exact fallback on prefix ties.
-__device__ __forceinline__ void sort_pair_fast(unsigned long long& key, long long span, long long dh) {
-  const int lane = threadIdx.x & 31;
-  unsigned v = ((unsigned)(key >> 37) << 5) | (unsigned)lane;
-  if (span > 8) bitonic_sort_u32<16>(v);
-  else if (span > 4) bitonic_sort_u32<8>(v);
-  else if (span > 2) bitonic_sort_u32<4>(v);
-  else bitonic_sort_u32<2>(v);
-  const unsigned prev = __shfl_up_sync(0xffffffffu, v, 1);
-  const int jl = lane & 15;
-  const bool tie = jl > 0 && jl < dh && (prev >> 5) == (v >> 5);
-  if (__any_sync(0xffffffffu, tie)) {
-    if (span > 8) bitonic_sort_u64<16>(key);
-    else if (span > 4) bitonic_sort_u64<8>(key);
-    else if (span > 2) bitonic_sort_u64<4>(key);
-    else bitonic_sort_u64<2>(key);
-    return;
-  }
-  key = __shfl_sync(0xffffffffu, key, (int)(v & 31u));
-}
-
 // jump with the per-batch constants C = inc * S precomputed (one 128-bit
 // multiply-add per non-zero nibble of the offset)
 struct JumpTableC {
@@ -264,83 +238,10 @@ __device__ __forceinline__ u128 pcg_jump_c(const JumpTableC& tab, u128 s, unsign
   return s;
 }
 
-// Warp tasks of k_select: contiguous frontier rows grouped by where their
-// candidate stretch STARTS in the layer's PCG64 stream (tasks of C draws), so
-// tasks are balanced by candidates, not rows (low ids = hubs cluster in the
-// sorted-unique frontier). task_row[t] = first row whose stream offset is
-// >= t*C (a lower bound on cand_off), task_row[T] = F; meta = {T, C}.
-constexpr int kMaxTasks = 1 << 18;
-
-// Hub rows (more than kHuge candidates, fanout <= 32) are split into
-// segments of kSegC candidates, one warp each (k_select_huge: exact top-fanout
-// of the segment by (key53, j)), then merged per row (k_merge_huge). The
-// top-fanout of a row is contained in the union of its segments' top-fanout,
-// so the result is exact; without the split one warp walks a 56K-candidate
-// hub alone (papers100M shape) and sets the layer's duration.
-constexpr long long kHuge = 4096;
-constexpr int kSegC = 2048;
-constexpr int kMaxSegs = 1 << 16;     // per layer; hubs beyond stay on the warp path
-struct HugeState {
-  int* ctr;             // [0] accepted hub rows, [1] segments claimed
-  int32_t* rows;        // [F_max] accepted hub rows
-  int32_t* base;        // [F_max] first segment of each accepted hub
-  uint8_t* flag;        // [F_max] 1 = row handled by the hub path
-  int32_t* seg_row;     // [kMaxSegs] row of each segment (-1 unused)
-  int32_t* seg_s;       // [kMaxSegs] segment index within its row
-  unsigned long long* seg_key;   // [kMaxSegs * 32] key53 of the segment's picks
-  int32_t* seg_j;       // [kMaxSegs * 32] row-global candidate position
-};
-
-__global__ void k_task_bounds(const int32_t* F_dev, const int64_t* __restrict__ cand_off, int32_t* __restrict__ task_row,
-                              long long* __restrict__ meta, int fanout, HugeState hs) {
-  pdl_wait();
-  const int F = *F_dev;
-  const long long total = cand_off[F];
-  long long C = (total + 148 * 32 - 1) / (148 * 32);       // aim for >= 32 tasks per SM
-  C = C < 64 ? 64 : (C > 512 ? 512 : C);
-  const long long cmin = (total + kMaxTasks - 1) / kMaxTasks;
-  if (C < cmin) C = cmin;
-  const long long T = (total + C - 1) / C;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    meta[0] = T;
-    meta[1] = C;
-    task_row[0] = 0;
-    task_row[T] = F;
-  }
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
-    const long long a = cand_off[j], b = cand_off[j + 1];
-    for (long long t = a / C + 1; t * C <= b && t < T; ++t) task_row[t] = j + 1;
-    uint8_t huge = 0;
-    if (fanout <= 32 && b - a > kHuge) {
-      const int nseg = (int)((b - a + kSegC - 1) / kSegC);
-      const int base = atomicAdd(&hs.ctr[1], nseg);
-      if (base + nseg <= kMaxSegs) {
-        huge = 1;
-        const int i = atomicAdd(&hs.ctr[0], 1);
-        hs.rows[i] = j;
-        hs.base[i] = base;
-        for (int q = 0; q < nseg; ++q) {
-          hs.seg_row[base + q] = j;
-          hs.seg_s[base + q] = q;
-        }
-      } else {
-        for (int q = base; q < kMaxSegs && q < base + nseg; ++q) hs.seg_row[q] = -1;
-      }
-    }
-    hs.flag[j] = huge;
-  }
-}
-
-
-// One warp per task of kRowsPerTask consecutive frontier rows. Consecutive
-// rows draw consecutive stretches of the PCG64 stream, so only a task's first
-// row jumps from the batch state (O(log offset) table steps); each later row
-// advances the lane states by the 1..32 draws left over from the previous row
-// with a single precomputed multiply-add (tables D[d] = jump by d).
-// k_select records each pick as its global edge index, split into the low
-// (src_flat) and high (col_local) 32-bit words; k_pick resolves the column
-// (a random read of the full graph's col) and marks non-frontier sources with
-// full memory-level parallelism, off k_select's per-row critical path.
+// k_pick resolves each pick (global edge index, split into the low
+// (src_flat) and high (col_local) 32-bit words) to its column -- a random read
+// of the full graph's col -- and marks non-frontier sources, with full
+// memory-level parallelism, off the selection's per-row critical path.
 __device__ __forceinline__ void put_pick(int32_t* src_flat, int32_t* col_local, int e, long long pos) {
   src_flat[e] = (int32_t)(unsigned)(pos & 0xffffffffll);
   col_local[e] = (int32_t)(unsigned)((unsigned long long)pos >> 32);
@@ -360,211 +261,370 @@ __global__ void k_pick(const int32_t* __restrict__ g_col, const int32_t* counts_
   }
 }
 
-template <bool kSmallFanout>
-__global__ void __launch_bounds__(kSelThreads, 4) k_select(
-    const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end,
-    const int32_t* __restrict__ frontier, const int32_t* F_dev, int fanout, const SampState* ss,
-    const int64_t* __restrict__ cand_off, const int32_t* __restrict__ blk_off, int32_t* __restrict__ src_flat,
-    int32_t* __restrict__ col_local, const int32_t* __restrict__ task_row, const long long* __restrict__ task_meta,
-    const uint8_t* __restrict__ huge_flag) {
+// ------------------------------------------------------------------------
+// Selection, fanout <= 32: one persistent launch over a work list.
+//
+// k_plan (thread per row): the PCG64 state just before the row's first draw
+// (jump from the batch state, so no selector ever jumps far), hub rows
+// (> kHuge candidates) split into segments of kSegC candidates, and a
+// histogram of the other rows by candidate count. k_order lists those rows
+// by descending count. k_select_all's warps then pull work items from one
+// atomic counter, longest first:
+//   hub segments   exact top-fanout of kSegC candidates (packed key53 << 11 |
+//                  j); the warp finishing a row's last segment merges them
+//   warp rows      rows of > lane_max candidates: lane = candidate, 32 keys
+//                  per chunk, the first chunk sorted by a bitonic network, later
+//                  ones inserted by ballot rank against the fanout-th key
+//   lane groups    32 rows of <= lane_max candidates (fanout <= 16), one per
+//                  THREAD: the row's keys drawn one after the other and the
+//                  top-fanout kept sorted in registers by an unrolled
+//                  compare-select network. The ordering groups rows of equal
+//                  count, so the 32 loops of a warp have the same length.
+// Every path keeps the (key53, j) order of the reference's argsort.
+// ------------------------------------------------------------------------
+constexpr long long kHuge = 4096;
+constexpr int kSegC = 2048;
+constexpr int kMaxSegs = 1 << 16;     // per layer; hubs beyond are warp rows
+constexpr int kBins = 320;            // candidate counts 0..255 exact, then 64 wide, last bin open
+constexpr int kLaneCap = 255;         // lane_max <= kLaneCap
+
+__device__ __forceinline__ int deg_bin(long long d) {
+  if (d < 256) return (int)d;
+  const long long b = 256 + ((d - 256) >> 6);
+  return b > kBins - 1 ? kBins - 1 : (int)b;
+}
+
+struct Plan {
+  int* ctr;            // [0] hub rows [1] segments claimed [2] item counter [3] items [4] warp rows [5] lane rows [6] segments
+  int* hist;           // [kBins] rows per bin
+  int* cursor;         // [kBins]
+  int32_t* order;      // [F_max] non-hub rows, descending candidate count
+  u128* row_state;     // [F_max] PCG64 state before the row's first draw
+  int32_t* hub_row;    // [F_max]
+  int32_t* hub_base;   // [F_max] first segment of the hub
+  int* hub_done;       // [F_max] segments finished
+  int32_t* seg_hub;    // [kMaxSegs] hub of the segment (-1: unused)
+  u128* seg_state;     // [kMaxSegs] state before the segment's first draw
+  unsigned long long* seg_key;  // [kMaxSegs * 32] key53 of the segment's picks
+  int32_t* seg_j;      // [kMaxSegs * 32] row-global candidate position
+  uint8_t* flag;       // [F_max] 1 = hub row
+};
+
+__global__ void __launch_bounds__(256) k_plan(const int32_t* F_dev, const int64_t* __restrict__ cand_off,
+                                              const SampState* ss, Plan P) {
   pdl_wait();
-  __shared__ JumpTableC tab;
-  __shared__ u128 dA[33], dC[33];
+  __shared__ int lh[kBins];
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x) lh[b] = 0;
+  __syncthreads();
+  const int F = *F_dev;
   const u128 s0{ss->st_hi, ss->st_lo}, inc{ss->inc_hi, ss->inc_lo};
-  for (int t = threadIdx.x; t < 256; t += blockDim.x) {
-    (&tab.A[0][0])[t] = (&g_jump.A[0][0])[t];
-    (&tab.C[0][0])[t] = mul128(inc, (&g_jump.S[0][0])[t]);
+  const unsigned long long base0 = ss->stream_pos;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
+    const long long a = cand_off[j], d = cand_off[j + 1] - a;
+    const u128 st = pcg_jump(g_jump, s0, inc, base0 + (unsigned long long)a);
+    P.row_state[j] = st;
+    uint8_t hub = 0;
+    if (d > kHuge) {
+      const int nseg = (int)((d + kSegC - 1) / kSegC);
+      const int base = atomicAdd(&P.ctr[1], nseg);
+      if (base + nseg <= kMaxSegs) {
+        hub = 1;
+        const int i = atomicAdd(&P.ctr[0], 1);
+        P.hub_row[i] = j;
+        P.hub_base[i] = base;
+        P.hub_done[i] = 0;
+        u128 ss_q = st;
+        for (int q = 0; q < nseg; ++q) {
+          P.seg_hub[base + q] = i;
+          P.seg_state[base + q] = ss_q;
+          if (q + 1 < nseg) ss_q = pcg_jump(g_jump, ss_q, inc, (unsigned long long)kSegC);
+        }
+      } else {
+        for (int q = base; q < kMaxSegs && q < base + nseg; ++q) P.seg_hub[q] = -1;
+      }
+    }
+    P.flag[j] = hub;
+    if (!hub && d >= 1) atomicAdd(&lh[deg_bin(d)], 1);
   }
   __syncthreads();
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+    if (lh[b]) atomicAdd(&P.hist[b], lh[b]);
+}
+
+// non-hub rows -> P.order by descending bin (block scan of the histogram,
+// per-CTA ranks by shared-memory atomics, one cursor reservation per CTA and
+// bin); block 0 publishes the work-list sizes
+__global__ void __launch_bounds__(kBins) k_order(const int32_t* F_dev, const int64_t* __restrict__ cand_off,
+                                                 int lane_max, Plan P) {
+  pdl_wait();
+  __shared__ int off[kBins], cnt[kBins], res[kBins], wsum[kBins / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int bin = kBins - 1 - t;            // descending
+  const int h = P.hist[bin];
+  int x = h;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  int pre = 0;
+  for (int q = 0; q < w; ++q) pre += wsum[q];
+  off[bin] = pre + x - h;
+  __syncthreads();
+  if (blockIdx.x == 0 && t == 0) {
+    int total = 0;
+    for (int q = 0; q < kBins / 32; ++q) total += wsum[q];
+    const int n_warp = lane_max > 0 ? off[lane_max] : total;   // bins above lane_max come first
+    const int n_lane = total - n_warp;
+    const int nseg = P.ctr[1] < kMaxSegs ? P.ctr[1] : kMaxSegs;
+    P.ctr[4] = n_warp;
+    P.ctr[5] = n_lane;
+    P.ctr[6] = nseg;
+    P.ctr[3] = nseg + n_warp + (n_lane + 31) / 32;
+  }
+  const int F = *F_dev;
+  for (int base = blockIdx.x * kBins; base < F; base += gridDim.x * kBins) {
+    cnt[t] = 0;
+    __syncthreads();
+    const int j = base + t;
+    int b = -1, r = 0;
+    if (j < F && !P.flag[j]) {
+      const long long d = cand_off[j + 1] - cand_off[j];
+      if (d >= 1) {
+        b = deg_bin(d);
+        r = atomicAdd(&cnt[b], 1);
+      }
+    }
+    __syncthreads();
+    if (cnt[t]) res[t] = atomicAdd(&P.cursor[t], cnt[t]);
+    __syncthreads();
+    if (b >= 0) P.order[off[b] + res[b] + r] = j;
+    __syncthreads();
+  }
+}
+
+// sorted insertion of key into b[0..kF) (ascending), no data-dependent
+// indexing, so the list stays in registers
+template <int kF>
+__device__ __forceinline__ void lane_insert(unsigned long long (&b)[kF], unsigned long long key) {
+  bool c[kF];
+#pragma unroll
+  for (int i = 0; i < kF; ++i) c[i] = key < b[i];
+#pragma unroll
+  for (int i = kF - 1; i > 0; --i) b[i] = c[i - 1] ? b[i - 1] : (c[i] ? key : b[i]);
+  b[0] = c[0] ? key : b[0];
+}
+
+// top-fanout of `len` (<= 2048) consecutive candidates starting at lane state
+// s (lane l at candidate l): packed (key53 << 11 | j) words, ascending, one
+// per lane (lanes >= min(len, fanout) hold larger keys or ~0)
+__device__ __forceinline__ unsigned long long warp_topk_packed(u128 s, long long len, int fanout, u128 a32, u128 c32) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long best = ~0ull;
+  for (long long c = 0; c < len; c += 32) {
+    const long long jj = c + lane;
+    unsigned long long key = jj < len ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
+    if (c + 32 < len) s = fma128(a32, s, c32);
+    if (c == 0) {
+      sort_first_chunk_fast(key, len);
+      best = key;
+      continue;
+    }
+    // later chunks: insert only the candidates that beat the current
+    // fanout-th key, one at a time (rank by ballot, shift by shfl_up)
+    unsigned long long thr = __shfl_sync(0xffffffffu, best, fanout - 1);
+    unsigned m = __ballot_sync(0xffffffffu, key < thr);
+    while (m) {
+      const int l = __ffs(m) - 1;
+      const unsigned long long cand = __shfl_sync(0xffffffffu, key, l);
+      const int pos = __popc(__ballot_sync(0xffffffffu, best < cand));
+      const unsigned long long up = __shfl_up_sync(0xffffffffu, best, 1);
+      if (lane == pos) best = cand;
+      else if (lane > pos) best = up;
+      thr = __shfl_sync(0xffffffffu, best, fanout - 1);
+      m &= ~(1u << l);
+      m &= __ballot_sync(0xffffffffu, key < thr);
+    }
+  }
+  return best;
+}
+
+template <int kF>
+__global__ void __launch_bounds__(kSelThreads, 4) k_select_all(
+    const int64_t* __restrict__ g_start, const int32_t* __restrict__ frontier, int fanout, const SampState* ss,
+    const int64_t* __restrict__ cand_off, const int32_t* __restrict__ blk_off, int32_t* __restrict__ src_flat,
+    int32_t* __restrict__ col_local, Plan P) {
+  pdl_wait();
+  __shared__ u128 dA[33], dC[33];          // jump by d = 0..32 steps
+  const u128 inc{ss->inc_hi, ss->inc_lo};
   if (threadIdx.x <= 32) {
-    // jump by d = 16*h + l: low nibble first, then the high one
     const int d = threadIdx.x, l = d & 15, h = d >> 4;
-    u128 a = tab.A[0][l], c = tab.C[0][l];
+    u128 a = g_jump.A[0][l], c = mul128(inc, g_jump.S[0][l]);
     if (h) {
-      c = fma128(tab.A[1][h], c, tab.C[1][h]);
-      a = mul128(tab.A[1][h], a);
+      const u128 ah = g_jump.A[1][h];
+      c = fma128(ah, c, mul128(inc, g_jump.S[1][h]));
+      a = mul128(ah, a);
     }
     dA[d] = a;
     dC[d] = c;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  const unsigned long long base0 = ss->stream_pos;
+  const int n_items = P.ctr[3], nseg = P.ctr[6], n_warp = P.ctr[4], n_lane = P.ctr[5];
+  const u128 a32 = dA[32], c32 = dC[32], a1 = dA[lane + 1], c1 = dC[lane + 1];
+  const u128 mult{kMultHi, kMultLo};
   KTimer* kt = g_kt ? g_kt + kTSelect : nullptr;
   kt_begin(kt);
-  const u128 a32 = tab.A[1][2];            // MULT^32 and its increment term
-  const u128 c32 = tab.C[1][2];
-  const long long ntask = task_meta[0];
-  for (long long task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < ntask; task += warps) {
-    const int r_begin = task_row[task], r_end = task_row[task + 1];
-    bool have = false;                     // cur = lane state at stream index cur_pos + lane
-    u128 cur{0, 0};
-    unsigned long long cur_pos = 0;
-    for (int r0 = r_begin; r0 < r_end; r0 += 32) {
-      const int nr = r_end - r0 < 32 ? r_end - r0 : 32;
-      // the rows' metadata, fetched by lanes < nr at once
-      long long lo_l = 0, deg_l = 0, off_l = 0;
-      int out_l = 0;
-      if (lane < nr) {
-        const int v = frontier[r0 + lane];
-        lo_l = g_start[v];
-        deg_l = g_end[v] - lo_l;
-        off_l = cand_off[r0 + lane];
-        out_l = blk_off[r0 + lane];
-        if (huge_flag && huge_flag[r0 + lane]) deg_l = 0;   // selected by k_select_huge / k_merge_huge
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(&P.ctr[2], 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    if (item < nseg) {
+      // ---- hub segment
+      const int i = P.seg_hub[item];
+      if (i < 0) continue;
+      const int row = P.hub_row[i];
+      const long long a = cand_off[row], deg = cand_off[row + 1] - a;
+      const int sidx = item - P.hub_base[i];
+      const long long j0 = (long long)sidx * kSegC;
+      const long long len = deg - j0 < kSegC ? deg - j0 : kSegC;
+      const unsigned long long best = warp_topk_packed(fma128(a1, P.seg_state[item], c1), len, fanout, a32, c32);
+      const int cnt = (int)(len < fanout ? len : fanout);
+      P.seg_key[(long long)item * 32 + lane] = lane < cnt ? (best >> 11) : ~0ull;
+      P.seg_j[(long long)item * 32 + lane] = lane < cnt ? (int32_t)(j0 + (long long)(best & 2047ull)) : 0x7fffffff;
+      __syncwarp();
+      const int nsr = (int)((deg + kSegC - 1) / kSegC);
+      int last = 0;
+      if (lane == 0) {
+        __threadfence();
+        last = atomicAdd(&P.hub_done[i], 1) == nsr - 1;
       }
-      for (int q = 0; q < nr; ++q) {
-        const long long lo = __shfl_sync(0xffffffffu, lo_l, q);
-        const long long deg = __shfl_sync(0xffffffffu, deg_l, q);
-        const int out0 = __shfl_sync(0xffffffffu, out_l, q);
-        const int count = (int)(deg < fanout ? deg : fanout);
-        if (deg == 0) continue;
-        const unsigned long long k0 = base0 + (unsigned long long)__shfl_sync(0xffffffffu, off_l, q);
-        // lane state: output index k0+lane needs k0+lane+1 steps
-        u128 first;
-        if (!have) {
-          first = pcg_jump_c(tab, s0, k0 + (unsigned long long)lane + 1ull);
-        } else {
-          const unsigned long long delta = k0 - cur_pos;
-          first = delta <= 32ull ? fma128(dA[delta], cur, dC[delta]) : pcg_jump_c(tab, cur, delta);
+      if (!__shfl_sync(0xffffffffu, last, 0)) continue;
+      __threadfence();
+      // the row's last segment: merge the segments' sorted picks
+      const int sb = P.hub_base[i];
+      unsigned long long bk = ~0ull;
+      unsigned bj = ~0u;
+      for (int g = sb; g < sb + nsr; ++g) {
+        unsigned long long key = __ldcg(&P.seg_key[(long long)g * 32 + lane]);
+        unsigned j = (unsigned)__ldcg(&P.seg_j[(long long)g * 32 + lane]);
+        if (lane >= fanout) {
+          key = ~0ull;
+          j = ~0u;
         }
-        have = false;
-#if HG_SEL_PAIRS
-        // two short consecutive rows share one pass: their candidates are
-        // consecutive in the stream, so row q+1's lanes take the states of
-        // lanes deg .. deg+15 of this jump (the layouts of C3-like graphs,
-        // m = 7, are dominated by rows of <= 16 candidates)
-        if (kSmallFanout && deg <= 16 && q + 1 < nr) {
-          const long long deg2 = __shfl_sync(0xffffffffu, deg_l, q + 1);
-          if (deg2 >= 1 && deg2 <= 16) {
-            const long long lo2 = __shfl_sync(0xffffffffu, lo_l, q + 1);
-            const int out2 = __shfl_sync(0xffffffffu, out_l, q + 1);
-            const int count2 = (int)(deg2 < fanout ? deg2 : fanout);
-            const int srcl = lane < 16 ? lane : (int)deg + lane - 16;
-            u128 st;
-            st.hi = __shfl_sync(0xffffffffu, first.hi, srcl);
-            st.lo = __shfl_sync(0xffffffffu, first.lo, srcl);
-            const int jl = lane & 15;
-            const long long dh = lane < 16 ? deg : deg2;
-            unsigned long long key = jl < dh ? ((pcg_key53(st) << 11) | (unsigned long long)jl) : ~0ull;
-            sort_pair_fast(key, deg > deg2 ? deg : deg2, dh);
-            const int ch = lane < 16 ? count : count2;
-            if (jl < ch)
-              put_pick(src_flat, col_local, (lane < 16 ? out0 : out2) + jl, (lane < 16 ? lo : lo2) + (long long)(key & 2047ull));
-            cur = first;
-            cur_pos = k0;
-            have = true;
-            ++q;     // row q+1 done
-            continue;
-          }
+        const unsigned long long k0 = __shfl_sync(0xffffffffu, key, 0);
+        const unsigned j0s = __shfl_sync(0xffffffffu, j, 0);
+        const unsigned long long tk = __shfl_sync(0xffffffffu, bk, fanout - 1);
+        const unsigned tj = __shfl_sync(0xffffffffu, bj, fanout - 1);
+        if (!kj_less(k0, j0s, tk, tj)) continue;        // nothing of it enters the top-fanout
+        const unsigned long long rk = __shfl_sync(0xffffffffu, key, 31 - lane);
+        const unsigned rj = __shfl_sync(0xffffffffu, j, 31 - lane);
+        if (kj_less(rk, rj, bk, bj)) {
+          bk = rk;
+          bj = rj;
         }
-#endif
-        if (kSmallFanout && deg <= 2048) {
-          // fast path: (key53, j) packed into one u64, j < 2^11
-          unsigned long long best = ~0ull;
-          u128 s = first;
-          for (long long c = 0; c < deg; c += 32) {
-            const long long jj = c + lane;
-            const bool valid = jj < deg;
-            unsigned long long key = valid ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
-            if (c + 32 < deg) s = fma128(a32, s, c32);
-            if (c == 0) {
-              sort_first_chunk_fast(key, deg);
-              best = key;
-              continue;
-            }
-            // later chunks: insert only the candidates that beat the current
-            // fanout-th key, one at a time (rank by ballot, shift by shfl_up)
-            unsigned long long thr = __shfl_sync(0xffffffffu, best, fanout - 1);
-            unsigned m = __ballot_sync(0xffffffffu, key < thr);
-            while (m) {
-              const int l = __ffs(m) - 1;
-              const unsigned long long cand = __shfl_sync(0xffffffffu, key, l);
-              const int pos = __popc(__ballot_sync(0xffffffffu, best < cand));
-              const unsigned long long up = __shfl_up_sync(0xffffffffu, best, 1);
-              if (lane == pos) best = cand;
-              else if (lane > pos) best = up;
-              thr = __shfl_sync(0xffffffffu, best, fanout - 1);
-              m &= ~(1u << l);
-              m &= __ballot_sync(0xffffffffu, key < thr);
-            }
-          }
-          cur = s;
-          cur_pos = k0 + 32ull * (unsigned long long)((deg - 1) / 32);
-          have = true;
-          if (lane < count) put_pick(src_flat, col_local, out0 + lane, lo + (long long)(best & 2047ull));
-        } else if (kSmallFanout) {
-          unsigned long long bk = ~0ull;
-          unsigned bj = ~0u;
-          u128 s = first;
-          for (long long c = 0; c < deg; c += 32) {
-            const long long jj = c + lane;
-            const bool valid = jj < deg;
-            unsigned long long key = valid ? pcg_key53(s) : ~0ull;
-            unsigned j = valid ? (unsigned)jj : ~0u;
-            if (c + 32 < deg) s = fma128(a32, s, c32);
-            const unsigned long long tk = __shfl_sync(0xffffffffu, bk, fanout - 1);
-            const unsigned tj = __shfl_sync(0xffffffffu, bj, fanout - 1);
-            if (!__ballot_sync(0xffffffffu, valid && kj_less(key, j, tk, tj))) continue;
-            bitonic_sort32(key, j);
-            unsigned long long rk = __shfl_sync(0xffffffffu, key, 31 - lane);
-            unsigned rj = __shfl_sync(0xffffffffu, j, 31 - lane);
-            if (kj_less(rk, rj, bk, bj)) {
-              bk = rk;
-              bj = rj;
-            }
-            bitonic_merge32(bk, bj);
-          }
-          if (lane < count) put_pick(src_flat, col_local, out0 + lane, lo + bj);
-        } else {
-          // generic fanout: repeated warp-min selection (O(count * deg / 32))
-          unsigned long long pk = 0;
-          unsigned pj = 0;
-          bool have_prev = false;
-          for (int r = 0; r < count; ++r) {
-            unsigned long long bk = ~0ull;
-            unsigned bj = ~0u;
-            u128 s = first;
-            for (long long c = 0; c < deg; c += 32) {
-              const long long jj = c + lane;
-              if (jj < deg) {
-                unsigned long long key = pcg_key53(s);
-                unsigned j = (unsigned)jj;
-                bool after = !have_prev || kj_less(pk, pj, key, j);
-                if (after && kj_less(key, j, bk, bj)) {
-                  bk = key;
-                  bj = j;
-                }
-              }
-              if (c + 32 < deg) s = fma128(a32, s, c32);
-            }
-    #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-              unsigned oj = __shfl_xor_sync(0xffffffffu, bj, o);
-              if (kj_less(ok, oj, bk, bj)) {
-                bk = ok;
-                bj = oj;
-              }
-            }
-            pk = bk;
-            pj = bj;
-            have_prev = true;
-            if (lane == 0) put_pick(src_flat, col_local, out0 + r, lo + pj);
-          }
-        }
+        bitonic_merge32(bk, bj);
       }
+      if (lane < fanout) put_pick(src_flat, col_local, blk_off[row] + lane, g_start[frontier[row]] + (long long)bj);
+    } else if (item < nseg + n_warp) {
+      // ---- one row per warp
+      const int j = P.order[item - nseg];
+      const long long a = cand_off[j], deg = cand_off[j + 1] - a;
+      const long long lo = g_start[frontier[j]];
+      const int out0 = blk_off[j];
+      const int count = (int)(deg < fanout ? deg : fanout);
+      u128 s = fma128(a1, P.row_state[j], c1);
+      if (deg <= 2048) {
+        const unsigned long long best = warp_topk_packed(s, deg, fanout, a32, c32);
+        if (lane < count) put_pick(src_flat, col_local, out0 + lane, lo + (long long)(best & 2047ull));
+      } else {
+        // (key53, j) pairs: rows too long for the 11-bit packing
+        unsigned long long bk = ~0ull;
+        unsigned bj = ~0u;
+        for (long long c = 0; c < deg; c += 32) {
+          const long long jj = c + lane;
+          const bool valid = jj < deg;
+          unsigned long long key = valid ? pcg_key53(s) : ~0ull;
+          unsigned jv = valid ? (unsigned)jj : ~0u;
+          if (c + 32 < deg) s = fma128(a32, s, c32);
+          const unsigned long long tk = __shfl_sync(0xffffffffu, bk, fanout - 1);
+          const unsigned tj = __shfl_sync(0xffffffffu, bj, fanout - 1);
+          if (!__ballot_sync(0xffffffffu, valid && kj_less(key, jv, tk, tj))) continue;
+          bitonic_sort32(key, jv);
+          const unsigned long long rk = __shfl_sync(0xffffffffu, key, 31 - lane);
+          const unsigned rj = __shfl_sync(0xffffffffu, jv, 31 - lane);
+          if (kj_less(rk, rj, bk, bj)) {
+            bk = rk;
+            bj = rj;
+          }
+          bitonic_merge32(bk, bj);
+        }
+        if (lane < count) put_pick(src_flat, col_local, out0 + lane, lo + bj);
+      }
+    } else if (kF > 0) {
+      // ---- one row per thread
+      const int idx = n_warp + (item - nseg - n_warp) * 32 + lane;
+      if (idx >= n_warp + n_lane) continue;
+      const int j = P.order[idx];
+      const long long a = cand_off[j];
+      const int deg = (int)(cand_off[j + 1] - a);
+      const long long lo = g_start[frontier[j]];
+      const int out0 = blk_off[j];
+      constexpr int kK = kF > 0 ? kF : 1;
+      unsigned long long b[kK];
+#pragma unroll
+      for (int q = 0; q < kK; ++q) b[q] = ~0ull;
+      u128 s = fma128(mult, P.row_state[j], inc);   // one step: draw 0
+      for (int c = 0; c < deg; ++c) {
+        const unsigned long long key = (pcg_key53(s) << 11) | (unsigned long long)c;
+        s = fma128(mult, s, inc);
+        if (key < b[kK - 1]) lane_insert<kK>(b, key);
+      }
+      const int count = deg < fanout ? deg : fanout;
+#pragma unroll
+      for (int q = 0; q < kK; ++q)
+        if (q < count) put_pick(src_flat, col_local, out0 + q, lo + (long long)(b[q] & 2047ull));
     }
   }
   kt_end(kt);
 }
 
-// one warp per hub segment: exact top-fanout (packed key53 << 11 | j_local)
-// of kSegC consecutive candidates, written as (key53, row-global j)
-__global__ void __launch_bounds__(kSelThreads, 4) k_select_huge(
-    const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end, const int32_t* __restrict__ frontier,
-    int fanout, const SampState* ss, const int64_t* __restrict__ cand_off, HugeState hs) {
+// ------------------------------------------------------------------------
+// fanout > 32: warp tasks of contiguous rows (balanced by candidates: task
+// t starts at the first row whose stream offset is >= t*C) and repeated
+// warp-min selection, O(count * deg / 32) per row.
+constexpr int kMaxTasks = 1 << 18;
+
+__global__ void k_task_bounds(const int32_t* F_dev, const int64_t* __restrict__ cand_off, int32_t* __restrict__ task_row,
+                              long long* __restrict__ meta) {
+  pdl_wait();
+  const int F = *F_dev;
+  const long long total = cand_off[F];
+  long long C = (total + 148 * 32 - 1) / (148 * 32);       // aim for >= 32 tasks per SM
+  C = C < 64 ? 64 : (C > 512 ? 512 : C);
+  const long long cmin = (total + kMaxTasks - 1) / kMaxTasks;
+  if (C < cmin) C = cmin;
+  const long long T = (total + C - 1) / C;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    meta[0] = T;
+    meta[1] = C;
+    task_row[0] = 0;
+    task_row[T] = F;
+  }
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
+    const long long a = cand_off[j], b = cand_off[j + 1];
+    for (long long t = a / C + 1; t * C <= b && t < T; ++t) task_row[t] = j + 1;
+  }
+}
+
+__global__ void __launch_bounds__(kSelThreads, 4) k_select_generic(
+    const int64_t* __restrict__ g_start, const int64_t* __restrict__ g_end,
+    const int32_t* __restrict__ frontier, int fanout, const SampState* ss,
+    const int64_t* __restrict__ cand_off, const int32_t* __restrict__ blk_off, int32_t* __restrict__ src_flat,
+    int32_t* __restrict__ col_local, const int32_t* __restrict__ task_row, const long long* __restrict__ task_meta) {
   pdl_wait();
   __shared__ JumpTableC tab;
   const u128 s0{ss->st_hi, ss->st_lo}, inc{ss->inc_hi, ss->inc_lo};
@@ -573,95 +633,60 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select_huge(
     (&tab.C[0][0])[t] = mul128(inc, (&g_jump.S[0][0])[t]);
   }
   __syncthreads();
-  const int nseg = min(hs.ctr[1], kMaxSegs);
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  const u128 a32 = tab.A[1][2];
+  const unsigned long long base0 = ss->stream_pos;
+  const u128 a32 = tab.A[1][2];            // MULT^32 and its increment term
   const u128 c32 = tab.C[1][2];
-  for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < nseg; g += warps) {
-    const int row = hs.seg_row[g];
-    if (row < 0) continue;
-    const int sidx = hs.seg_s[g];
-    const int v = frontier[row];
-    const long long deg = g_end[v] - g_start[v];
-    const long long j0 = (long long)sidx * kSegC;
-    const long long len = deg - j0 < kSegC ? deg - j0 : kSegC;
-    const unsigned long long k0 = ss->stream_pos + (unsigned long long)cand_off[row] + (unsigned long long)j0;
-    u128 s = pcg_jump_c(tab, s0, k0 + (unsigned long long)lane + 1ull);
-    unsigned long long best = ~0ull;
-    for (long long c = 0; c < len; c += 32) {
-      const long long jj = c + lane;
-      const bool valid = jj < len;
-      unsigned long long key = valid ? ((pcg_key53(s) << 11) | (unsigned long long)jj) : ~0ull;
-      if (c + 32 < len) s = fma128(a32, s, c32);
-      if (c == 0) {
-        sort_first_chunk_fast(key, len);
-        best = key;
-        continue;
-      }
-      unsigned long long thr = __shfl_sync(0xffffffffu, best, fanout - 1);
-      unsigned m = __ballot_sync(0xffffffffu, key < thr);
-      while (m) {
-        const int l = __ffs(m) - 1;
-        const unsigned long long cand = __shfl_sync(0xffffffffu, key, l);
-        const int pos = __popc(__ballot_sync(0xffffffffu, best < cand));
-        const unsigned long long up = __shfl_up_sync(0xffffffffu, best, 1);
-        if (lane == pos) best = cand;
-        else if (lane > pos) best = up;
-        thr = __shfl_sync(0xffffffffu, best, fanout - 1);
-        m &= ~(1u << l);
-        m &= __ballot_sync(0xffffffffu, key < thr);
+  KTimer* kt = g_kt ? g_kt + kTSelect : nullptr;
+  kt_begin(kt);
+  const long long ntask = task_meta[0];
+  for (long long task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < ntask; task += warps) {
+    for (int r = task_row[task]; r < task_row[task + 1]; ++r) {
+      const int v = frontier[r];
+      const long long lo = g_start[v], deg = g_end[v] - lo;
+      if (deg == 0) continue;
+      const int out0 = blk_off[r];
+      const int count = (int)(deg < fanout ? deg : fanout);
+      // lane state: stream index k0 + lane needs k0 + lane + 1 steps
+      const u128 first = pcg_jump_c(tab, s0, base0 + (unsigned long long)cand_off[r] + (unsigned long long)lane + 1ull);
+      unsigned long long pk = 0;
+      unsigned pj = 0;
+      bool have_prev = false;
+      for (int q = 0; q < count; ++q) {
+        unsigned long long bk = ~0ull;
+        unsigned bj = ~0u;
+        u128 s = first;
+        for (long long c = 0; c < deg; c += 32) {
+          const long long jj = c + lane;
+          if (jj < deg) {
+            const unsigned long long key = pcg_key53(s);
+            const unsigned j = (unsigned)jj;
+            const bool after = !have_prev || kj_less(pk, pj, key, j);
+            if (after && kj_less(key, j, bk, bj)) {
+              bk = key;
+              bj = j;
+            }
+          }
+          if (c + 32 < deg) s = fma128(a32, s, c32);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+          const unsigned oj = __shfl_xor_sync(0xffffffffu, bj, o);
+          if (kj_less(ok, oj, bk, bj)) {
+            bk = ok;
+            bj = oj;
+          }
+        }
+        pk = bk;
+        pj = bj;
+        have_prev = true;
+        if (lane == 0) put_pick(src_flat, col_local, out0 + q, lo + pj);
       }
     }
-    const int cnt = (int)(len < fanout ? len : fanout);
-    hs.seg_key[(long long)g * 32 + lane] = lane < cnt ? (best >> 11) : ~0ull;
-    hs.seg_j[(long long)g * 32 + lane] = lane < cnt ? (int32_t)(j0 + (long long)(best & 2047ull)) : 0x7fffffff;
   }
-}
-
-// one warp per accepted hub row: top-fanout by (key53, j) over its segments'
-// picks, emitted in key order like every other row
-__global__ void __launch_bounds__(256) k_merge_huge(const int64_t* __restrict__ g_start,
-                                                    const int32_t* __restrict__ frontier, int fanout,
-                                                    const int64_t* __restrict__ cand_off,
-                                                    const int32_t* __restrict__ blk_off, int32_t* __restrict__ src_flat,
-                                                    int32_t* __restrict__ col_local, HugeState hs) {
-  pdl_wait();
-  const int nh = hs.ctr[0];
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nh; i += warps) {
-    const int row = hs.rows[i];
-    const int base = hs.base[i];
-    const long long deg = cand_off[row + 1] - cand_off[row];
-    const int nseg = (int)((deg + kSegC - 1) / kSegC);
-    unsigned long long bk = ~0ull;
-    unsigned bj = ~0u;
-    for (int g = base; g < base + nseg; ++g) {
-      unsigned long long key = hs.seg_key[(long long)g * 32 + lane];
-      unsigned j = (unsigned)hs.seg_j[(long long)g * 32 + lane];
-      if (lane >= fanout) {
-        key = ~0ull;
-        j = ~0u;
-      }
-      // a segment's picks are sorted: skip it when its best does not beat
-      // the current fanout-th pick (nothing of it can enter the top-fanout)
-      const unsigned long long k0 = __shfl_sync(0xffffffffu, key, 0);
-      const unsigned j0 = __shfl_sync(0xffffffffu, j, 0);
-      const unsigned long long tk = __shfl_sync(0xffffffffu, bk, fanout - 1);
-      const unsigned tj = __shfl_sync(0xffffffffu, bj, fanout - 1);
-      if (!kj_less(k0, j0, tk, tj)) continue;
-      // (already ascending across lanes: k_select_huge stores its sorted picks)
-      unsigned long long rk = __shfl_sync(0xffffffffu, key, 31 - lane);
-      unsigned rj = __shfl_sync(0xffffffffu, j, 31 - lane);
-      if (kj_less(rk, rj, bk, bj)) {
-        bk = rk;
-        bj = rj;
-      }
-      bitonic_merge32(bk, bj);
-    }
-    if (lane < fanout) put_pick(src_flat, col_local, blk_off[row] + lane, g_start[frontier[row]] + (long long)bj);
-  }
+  kt_end(kt);
 }
 
 struct PopWord {
@@ -762,8 +787,48 @@ int ensure_jump_table() {
 
 using namespace hg;
 
-static long long huge_scratch_bytes(long long F_max) {
-  return 64 + (F_max + 16) * 9 + (long long)kMaxSegs * (4 + 4 + 32 * 8 + 32 * 4) + 256;
+static long long a16(long long x) { return (x + 15) & ~15ll; }
+static long long plan_scratch_bytes(long long F_max) {
+  const long long F = F_max + 16;
+  return a16((16 + 2 * kBins) * 4) + a16(F * 4) + a16(F * 16) + 3 * a16(F * 4) + a16((long long)kMaxSegs * 4) +
+         a16((long long)kMaxSegs * 16) + a16((long long)kMaxSegs * 32 * 8) + a16((long long)kMaxSegs * 32 * 4) +
+         a16(F) + 64;
+}
+
+static Plan carve_plan(char* p, long long F_max) {
+  const long long F = F_max + 16;
+  p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  Plan P;
+  auto take = [&](long long bytes) {
+    char* q = p;
+    p += a16(bytes);
+    return q;
+  };
+  P.ctr = reinterpret_cast<int*>(take((16 + 2 * kBins) * 4));   // ctr, hist, cursor: one memset
+  P.hist = P.ctr + 16;
+  P.cursor = P.hist + kBins;
+  P.order = reinterpret_cast<int32_t*>(take(F * 4));
+  P.row_state = reinterpret_cast<u128*>(take(F * 16));
+  P.hub_row = reinterpret_cast<int32_t*>(take(F * 4));
+  P.hub_base = reinterpret_cast<int32_t*>(take(F * 4));
+  P.hub_done = reinterpret_cast<int*>(take(F * 4));
+  P.seg_hub = reinterpret_cast<int32_t*>(take((long long)kMaxSegs * 4));
+  P.seg_state = reinterpret_cast<u128*>(take((long long)kMaxSegs * 16));
+  P.seg_key = reinterpret_cast<unsigned long long*>(take((long long)kMaxSegs * 32 * 8));
+  P.seg_j = reinterpret_cast<int32_t*>(take((long long)kMaxSegs * 32 * 4));
+  P.flag = reinterpret_cast<uint8_t*>(take(F));
+  return P;
+}
+
+// HG_SEL_LANE_MAX: longest row (candidates) selected one row per thread
+// (fanout <= 16); 0 = one row per warp throughout (A/B)
+static int lane_max_env() {
+  static const int v = [] {
+    const char* e = std::getenv("HG_SEL_LANE_MAX");
+    const int x = e ? std::atoi(e) : 128;
+    return x < 0 ? 0 : (x > kLaneCap ? kLaneCap : x);
+  }();
+  return v;
 }
 
 extern "C" {
@@ -771,7 +836,7 @@ extern "C" {
 long long hg_sample_layer_scratch_bytes(long long F_max, long long num_nodes) {
   long long words = (num_nodes + 31) / 32;
   return (scan_tiles(F_max) + 1) * (long long)sizeof(I64x2) + (scan_tiles(words, 1) + 1) * 4 + 256 +
-         (long long)(kMaxTasks + 2) * 4 + 64 + huge_scratch_bytes(F_max);
+         (long long)(kMaxTasks + 2) * 4 + 64 + plan_scratch_bytes(F_max);
 }
 
 int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t* g_col, long long num_nodes,
@@ -791,18 +856,7 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
   long long* task_meta = reinterpret_cast<long long*>(part_w + scan_tiles(words, 1) + 2);
   task_meta = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(task_meta) + 15) & ~uintptr_t(15));
   int32_t* task_row = reinterpret_cast<int32_t*>(task_meta + 2);
-  // hub-row state after the task table (16-byte aligned pieces)
-  char* hp = reinterpret_cast<char*>(task_row + kMaxTasks + 2);
-  hp = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(hp) + 15) & ~uintptr_t(15));
-  HugeState hs;
-  hs.ctr = reinterpret_cast<int*>(hp);
-  hs.seg_key = reinterpret_cast<unsigned long long*>(hp + 64);
-  hs.seg_j = reinterpret_cast<int32_t*>(hs.seg_key + (long long)kMaxSegs * 32);
-  hs.seg_row = hs.seg_j + (long long)kMaxSegs * 32;
-  hs.seg_s = hs.seg_row + kMaxSegs;
-  hs.rows = hs.seg_s + kMaxSegs;
-  hs.base = hs.rows + (F_max + 16);
-  hs.flag = reinterpret_cast<uint8_t*>(hs.base + (F_max + 16));
+  Plan P = carve_plan(reinterpret_cast<char*>(task_row + kMaxTasks + 2), F_max);
 
   SampState* ss = reinterpret_cast<SampState*>(state_dev);
   { const cudaError_t _pe = hg::launch_pdl(k_stamp, dim3(grid_for(F_max, 256)), dim3(256), 0, stream, frontier, F_dev, ss, g2l, src_out); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
@@ -812,31 +866,49 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
                           EmitDegCount{cand_off, blk_off, blk_end, dst_deg, fanout, g_start, g_end, frontier},
                           TotalDegCount{F_dev, cand_off, blk_off, counts_dev}, stream);
   if (st) return st;
-  HG_CHECK_CUDA(W, cudaMemsetAsync(hs.ctr, 0, 8, stream));
-  { const cudaError_t _pe = hg::launch_pdl(k_task_bounds, dim3(grid_for(F_max, 256)), dim3(256), 0, stream, F_dev, cand_off, task_row, task_meta, fanout, hs); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
-  HG_LAUNCHED(W);
-  // persistent warps over the tasks; HG_SEL_BLOCKS caps the grid (leaves SMs
-  // to the training stream that runs concurrently with the pipelined sampler)
-  // 4 CTAs (32 warps) per SM: the selection is latency-bound per row, so
-  // more rows in flight help (C2: k_select 81 -> 59 ms / 200 steps; C3
-  // step 1.29 -> 1.23 ms); 6/SM gains little more (profiles/r01/notes)
-  static const long long sel_cap = [] {
-    const char* e = std::getenv("HG_SEL_BLOCKS");
-    const long long v = e ? std::atoll(e) : 148 * 4;
-    return v < 1 ? 148ll * 4 : v;
-  }();
-  const unsigned sel_grid = (unsigned)sel_cap;
+  cudaError_t e;
   if (fanout <= 32) {
-    { const cudaError_t _pe = hg::launch_pdl(k_select<true>, dim3(sel_grid), dim3(kSelThreads), 0, stream, g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
-                                                          blk_off, src_flat, col_local, task_row, task_meta, hs.flag); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+    const int lane_max = fanout <= 16 ? lane_max_env() : 0;
+    HG_CHECK_CUDA(W, cudaMemsetAsync(P.ctr, 0, (16 + 2 * kBins) * 4, stream));
+    e = hg::launch_pdl(k_plan, dim3(grid_for(F_max, 256)), dim3(256), 0, stream, F_dev, (const int64_t*)cand_off,
+                       (const SampState*)ss, P);
+    if (e != cudaSuccess) return fail("launch", kCuda, cudaGetErrorString(e));
     HG_LAUNCHED(W);
-    { const cudaError_t _pe = hg::launch_pdl(k_select_huge, dim3(148 * 4), dim3(kSelThreads), 0, stream, g_start, g_end, frontier, fanout, ss, cand_off, hs); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+    e = hg::launch_pdl(k_order, dim3(grid_for(F_max, kBins, 148u * 4u)), dim3(kBins), 0, stream, F_dev,
+                       (const int64_t*)cand_off, lane_max, P);
+    if (e != cudaSuccess) return fail("launch", kCuda, cudaGetErrorString(e));
     HG_LAUNCHED(W);
-    { const cudaError_t _pe = hg::launch_pdl(k_merge_huge, dim3(148), dim3(256), 0, stream, g_start, frontier, fanout, cand_off, blk_off, src_flat, col_local, hs); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+    // persistent: 4 CTAs (32 warps) per SM pulling work items; HG_SEL_BLOCKS
+    // caps the grid (the sampler runs beside the training stream)
+    static const long long sel_cap = [] {
+      const char* v = std::getenv("HG_SEL_BLOCKS");
+      const long long x = v ? std::atoll(v) : 148 * 4;
+      return x < 1 ? 148ll * 4 : x;
+    }();
+    const int fk = lane_max == 0 ? 0 : fanout <= 2 ? 2 : fanout <= 4 ? 4 : fanout <= 5 ? 5 : fanout <= 6 ? 6
+                 : fanout <= 8 ? 8 : fanout <= 10 ? 10 : fanout <= 12 ? 12 : fanout <= 15 ? 15 : 16;
+#define HG_SEL_CASE(K)                                                                                          \
+  case K:                                                                                                       \
+    e = hg::launch_pdl(k_select_all<K>, dim3((unsigned)sel_cap), dim3(kSelThreads), 0, stream, g_start, frontier, \
+                       fanout, (const SampState*)ss, (const int64_t*)cand_off, (const int32_t*)blk_off, src_flat, \
+                       col_local, P);                                                                           \
+    break;
+    switch (fk) {
+      HG_SEL_CASE(0) HG_SEL_CASE(2) HG_SEL_CASE(4) HG_SEL_CASE(5) HG_SEL_CASE(6) HG_SEL_CASE(8) HG_SEL_CASE(10)
+      HG_SEL_CASE(12) HG_SEL_CASE(15) HG_SEL_CASE(16)
+    }
+#undef HG_SEL_CASE
+    if (e != cudaSuccess) return fail("launch", kCuda, cudaGetErrorString(e));
     HG_LAUNCHED(W);
   } else {
-    { const cudaError_t _pe = hg::launch_pdl(k_select<false>, dim3(sel_grid), dim3(kSelThreads), 0, stream, g_start, g_end, frontier, F_dev, fanout, ss, cand_off,
-                                                           blk_off, src_flat, col_local, task_row, task_meta, nullptr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+    e = hg::launch_pdl(k_task_bounds, dim3(grid_for(F_max, 256)), dim3(256), 0, stream, F_dev,
+                       (const int64_t*)cand_off, task_row, task_meta);
+    if (e != cudaSuccess) return fail("launch", kCuda, cudaGetErrorString(e));
+    HG_LAUNCHED(W);
+    e = hg::launch_pdl(k_select_generic, dim3(148 * 4), dim3(kSelThreads), 0, stream, g_start, g_end, frontier,
+                       fanout, (const SampState*)ss, (const int64_t*)cand_off, (const int32_t*)blk_off, src_flat,
+                       col_local, (const int32_t*)task_row, (const long long*)task_meta);
+    if (e != cudaSuccess) return fail("launch", kCuda, cudaGetErrorString(e));
     HG_LAUNCHED(W);
   }
   { const cudaError_t _pe = hg::launch_pdl(k_pick, dim3(grid_for(F_max * (long long)fanout, 256)), dim3(256), 0, stream, g_col, counts_dev, ss, g2l, bitmap, src_flat,

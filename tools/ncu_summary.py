@@ -1,49 +1,23 @@
-#!/usr/bin/env python
-"""Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list:
-per-kernel launch count, total device time and share (cold-cache, serialised
-by ncu, so compare SHARES, not absolute times)."""
-import collections
+"""Summarise an ncu --page details CSV: one line per launch (kernel, duration, key metrics)."""
 import csv
-import re
 import sys
 
-
-def load(path):
-    lines = [l for l in open(path) if l.startswith('"')]
-    rows = list(csv.reader(lines))
-    hdr = rows[0]
-    iname, ival = hdr.index("Kernel Name"), hdr.index("Metric Value")
-    out = []
-    for r in rows[1:]:
-        if r[0] == "ID":
-            continue
-        out.append((r[iname], float(r[ival].replace(",", ""))))
-    return out
-
-
-def short(name):
-    name = name.replace("(anonymous namespace)::", "")
-    name = re.sub(r"\(.*", "", name)
-    name = re.sub(r"<([^<>]{0,12})>", r"[\1]", name)
-    name = re.sub(r"<.*>", "<..>", name)
-    return name.replace("void ", "")[:70]
-
-
-def main():
-    path = sys.argv[1]
-    first = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-    recs = load(path)[first:]
-    tot = collections.defaultdict(lambda: [0, 0.0])
-    for n, v in recs:
-        k = short(n)
-        tot[k][0] += 1
-        tot[k][1] += v
-    s = sum(v for _, v in tot.values())
-    print(f"{'us':>10} {'share':>6} {'n':>5}  kernel")
-    for k, (n, v) in sorted(tot.items(), key=lambda x: -x[1][1]):
-        print(f"{v / 1e3:10.1f} {100 * v / s:5.1f}% {n:5d}  {k}")
-    print(f"total {s / 1e3:.1f} us over {len(recs)} launches")
-
-
-if __name__ == "__main__":
-    main()
+KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "Issued Ipc Active", "Achieved Occupancy",
+        "Eligible Warps Per Scheduler", "No Eligible", "Registers Per Thread", "Grid Size", "Block Size",
+        "Warp Cycles Per Issued Instruction", "Executed Instructions", "Avg. Active Threads Per Warp"]
+rows = list(csv.reader(open(sys.argv[1])))
+hdr = rows[0]
+ix = {h: i for i, h in enumerate(hdr)}
+cur = None
+out = {}
+order = []
+for r in rows[1:]:
+    key = (r[ix["ID"]], r[ix["Kernel Name"]][:60])
+    if key not in out:
+        out[key] = {}
+        order.append(key)
+    n = r[ix["Metric Name"]]
+    if n in KEYS and n not in out[key]:
+        out[key][n] = r[ix["Metric Value"]] + " " + r[ix["Metric Unit"]]
+for k in order:
+    print(k[0], k[1], "|", "; ".join(f"{n}={v}" for n, v in out[k].items()))
