@@ -1,10 +1,9 @@
 // K10: historical-cache admission / eviction / ring scatter-update for one
 // layer, bit-exact with histgnn/cache.py:131-204 (oracle: oracle/histcache.py).
 //
-//   U1  keys (norm fp64 bits, node id) for the live nodes; one device sort
-//       (merge sort, or 96-bit LSD radix at large n) ranks them "norm
-//       ascending, ties by id" (cache.py:191); ids are unique, so the order is
-//       total and independent of the algorithm
+//   U1  keys (norm fp64 bits, node id) for the live nodes; a device bucket
+//       sort ranks them "norm ascending, ties by id" (cache.py:191); ids are
+//       unique, so the order is total and independent of the algorithm
 //   U2  rank j >= k (k = floor(p_grad * n)): gradient eviction of cached nodes;
 //       rank j < k: admitted; admitted & computed -> write flag
 //   U3  compaction of write flags in rank order -> write list, n_write
@@ -17,8 +16,7 @@
 //   U7  header update; U8 optional refresh of retained timestamps
 // Norms are non-negative, so their IEEE bit patterns order like the values.
 #include "hgb200.h"
-#include <cub/device/device_merge_sort.cuh>
-#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_radix_sort.cuh>   // setup only: the feature-region degree sort
 #include <cstdlib>
 #include <cstring>
 
@@ -33,52 +31,41 @@ struct NormKey {
   unsigned id;
 };
 
-struct NormKeyLess {
-  __device__ bool operator()(const NormKey& a, const NormKey& b) const {
-    return a.norm < b.norm || (a.norm == b.norm && a.id < b.id);
-  }
-};
-
-// rank sort: CUB merge sort (block sort + merge-path passes) up to kMergeMaxN
-// live nodes, CUB 96-bit LSD radix sort above (12 onesweep passes, better at
-// large n). HG_CACHE_SORT=radix|merge overrides (A/B measurements).
-enum SortMode { kSortMerge = 1, kSortRadix = 2, kSortBucket = 3 };
-inline int sort_mode(long long n_max) {
-  static const int v = [] {
-    const char* e = std::getenv("HG_CACHE_SORT");
-    return !e ? -1
-              : (std::strcmp(e, "radix") == 0 ? kSortRadix
-                                              : (std::strcmp(e, "merge") == 0 ? kSortMerge
-                                                                              : (std::strcmp(e, "bucket") == 0 ? kSortBucket : -1)));
-  }();
-  if (v >= 0) return v;
-  return kSortBucket;
-}
-
 // ---------------------------------------------------------------------------
-// Bucket sort of the (norm bits, id) keys (kSortBucket, the default).
-// fp64 norms are >= 0, so their bit patterns order like the values. The
-// occupied bit range [lo, hi] is cut into kNB buckets by (bits - lo) >> shift
-// (monotone; equal norms share a bucket), items are scattered to their
-// buckets, and every bucket is sorted by (norm, id) on chip. Keys are
-// distinct (ids are), so the result is the unique sorted order: identical to
-// the CUB merge / radix sorts, in 6 launches instead of ~19, O(n) work.
-// Buckets above kBucketCap items (e.g. masses of equal norms) are sorted by
-// one CTA each with a chunk sort + global merge passes (k_bs_big).
-// 16K buckets: norms concentrate in a few binades, so at 4096 buckets each
-// held hundreds of keys and the per-bucket shared-memory bitonic sorts
-// dominated the update (HG_CACHE_NB overrides at build time, A/B)
+// Bucket sort of the (norm bits, id) keys. fp64 norms are >= 0, so their bit
+// patterns order like the values. The occupied bit range [lo, hi] is cut into
+// kNB buckets by (bits - lo) >> shift (monotone; equal norms share a bucket).
+// Keys are distinct (ids are), so the result is the unique sorted order.
+//   k_norm_keys   keys + the min / max norm bits (block-reduced)
+//   k_bs_count    bucket of every key, its arrival rank in the bucket, the
+//                 bucket and super-bucket (256 buckets) counts
+//   k_bs_offsets  one CTA per super-bucket: bucket offsets (prefix of the
+//                 super totals + the in-super prefix), lists of the buckets
+//                 too long for a warp
+//   k_bs_place    keys to their bucket slots (offset + arrival rank)
+//   k_bs_warp     one warp per bucket of <= kWarpSortMax keys: each key's final
+//                 position = its bucket offset + the number of bucket keys
+//                 below it (all-pairs count; exact because keys are distinct)
+//   k_bs_small    one CTA per listed bucket of <= kBucketCap keys (bitonic
+//                 in shared memory); k_bs_big above (chunk sorts + merges)
+// 64K buckets: the C2 layer-1 norms (~130K, 2.4 decades) leave buckets of
+// median 2 / 99th percentile ~65 keys (tools/norm_dist.py); at 16K buckets
+// 77 % of the keys sat in buckets of > 32 that needed CTA sorts.
 #ifndef HG_CACHE_NB
-#define HG_CACHE_NB 16384
+#define HG_CACHE_NB 65536
 #endif
 constexpr int kNB = HG_CACHE_NB;
-static_assert((kNB & (kNB - 1)) == 0 && kNB >= 1024, "bucket count: a power of two >= 1024");
+static_assert((kNB & (kNB - 1)) == 0 && kNB >= 65536 / 64 && kNB % 256 == 0, "bucket count: a power of two");
+constexpr int kSuperB = 256;                 // buckets per super-bucket
+constexpr int kNSuper = kNB / kSuperB;
+static_assert(kNSuper <= 1024, "super-bucket scan: one CTA");
 constexpr int kBucketCap = 2048;
+constexpr int kWarpSortMax = 128;
 
 struct BucketState {            // device scratch
   unsigned long long lo, hi;    // min / max norm bits over the n live keys
   int n_big;                    // buckets above kBucketCap
-  int pad;
+  int n_mid;                    // buckets of (kWarpSortMax, kBucketCap]
 };
 
 __device__ __forceinline__ int bucket_of(unsigned long long bits, unsigned long long lo, int shift) {
@@ -95,88 +82,145 @@ __device__ __forceinline__ bool key_less(unsigned long long an, unsigned ai, uns
   return an < bn || (an == bn && ai < bi);
 }
 
-__global__ void k_bs_hist(const int32_t* n_dev, const NormKey* __restrict__ keys, const BucketState* st,
-                          int* __restrict__ count) {
+__global__ void k_bs_count(const int32_t* n_dev, const NormKey* __restrict__ keys, const BucketState* st,
+                           int* __restrict__ count, int* __restrict__ scount, int* __restrict__ arrival) {
   pdl_wait();
-  extern __shared__ int h[];   // kNB counters (dynamic shared memory)
-  for (int b = threadIdx.x; b < kNB; b += blockDim.x) h[b] = 0;
-  __syncthreads();
   const int n = *n_dev;
   const unsigned long long lo = st->lo;
   const int shift = bucket_shift(lo, st->hi);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    atomicAdd(&h[bucket_of(keys[i].norm, lo, shift)], 1);
-  __syncthreads();
-  for (int b = threadIdx.x; b < kNB; b += blockDim.x)
-    if (h[b]) atomicAdd(&count[b], h[b]);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int b = bucket_of(keys[i].norm, lo, shift);
+    arrival[i] = atomicAdd(&count[b], 1);
+    atomicAdd(&scount[b / kSuperB], 1);
+  }
 }
 
-// exclusive offsets of the kNB bucket counts (one CTA), cursors, big-bucket
-// list. Warp w owns buckets [w kNB/32, (w+1) kNB/32), read 32 at a time
-// (coalesced) and scanned with shuffles; one shared-memory pass over the 32
-// warp totals
-__global__ void __launch_bounds__(1024) k_bs_scan(const int* __restrict__ count, int* __restrict__ off,
-                                                  int* __restrict__ cursor, int* __restrict__ big, BucketState* st) {
-  pdl_wait();
-  constexpr int kPerWarp = kNB / 32;
-  constexpr int kRounds = kPerWarp / 32;
-  __shared__ int wtot[32];
-  __shared__ int nbig;
+// exclusive block scan of one int per thread (blockDim.x <= 1024)
+__device__ __forceinline__ int block_excl_scan(int x, int* wsum) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) nbig = 0;
-  int v[kRounds], incl[kRounds];
-  int carry = 0;
+  int xs = x;
 #pragma unroll
-  for (int q = 0; q < kRounds; ++q) {
-    const int x = count[w * kPerWarp + q * 32 + lane];
-    int xs = x;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, xs, d);
-      if (lane >= d) xs += t;
-    }
-    v[q] = x;
-    incl[q] = carry + xs;
-    carry += __shfl_sync(0xffffffffu, xs, 31);
+  for (int d = 1; d < 32; d <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, xs, d);
+    if (lane >= d) xs += t;
   }
-  if (lane == 0) wtot[w] = carry;
+  if (lane == 31) wsum[w] = xs;
   __syncthreads();
   if (w == 0) {
-    const int t = wtot[lane];
+    const int nw = blockDim.x >> 5;
+    const int t = lane < nw ? wsum[lane] : 0;
     int ts = t;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int u = __shfl_up_sync(0xffffffffu, ts, d);
       if (lane >= d) ts += u;
     }
-    wtot[lane] = ts - t;   // exclusive prefix of the warps
+    if (lane < nw) wsum[lane] = ts - t;
   }
   __syncthreads();
-  const int base = wtot[w];
-#pragma unroll
-  for (int q = 0; q < kRounds; ++q) {
-    const int b = w * kPerWarp + q * 32 + lane;
-    const int e = base + incl[q] - v[q];
-    off[b] = e;
-    cursor[b] = e;
-    if (v[q] > kBucketCap) big[atomicAdd(&nbig, 1)] = b;
-  }
-  if (w == 31 && lane == 31) off[kNB] = base + incl[kRounds - 1];
+  const int r = wsum[w] + xs - x;
   __syncthreads();
-  if (threadIdx.x == 0) st->n_big = nbig;
+  return r;
 }
 
-__global__ void k_bs_scatter(const int32_t* n_dev, const NormKey* __restrict__ keys, const BucketState* st,
-                             int* __restrict__ cursor, NormKey* __restrict__ tkeys, int32_t* __restrict__ tvals) {
+__global__ void __launch_bounds__(kSuperB) k_bs_offsets(const int* __restrict__ count, const int* __restrict__ scount,
+                                                        int* __restrict__ off, int* __restrict__ mid,
+                                                        int* __restrict__ big, BucketState* st) {
+  pdl_wait();
+  __shared__ int wsum[32];
+  __shared__ int sbase;
+  const int s = blockIdx.x, t = threadIdx.x;
+  // prefix of the super-bucket totals before s (kNSuper <= 1024: strided)
+  int acc = 0;
+  for (int q = t; q < s; q += kSuperB) acc += scount[q];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  if ((t & 31) == 0) wsum[t >> 5] = acc;
+  __syncthreads();
+  if (t == 0) {
+    int b0 = 0;
+    for (int q = 0; q < kSuperB / 32; ++q) b0 += wsum[q];
+    sbase = b0;
+  }
+  __syncthreads();
+  const int b = s * kSuperB + t;
+  const int c = count[b];
+  const int e = sbase + block_excl_scan(c, wsum);
+  off[b] = e;
+  if (b == kNB - 1) off[kNB] = e + c;
+  if (c > kBucketCap) big[atomicAdd(&st->n_big, 1)] = b;
+  else if (c > kWarpSortMax) mid[atomicAdd(&st->n_mid, 1)] = b;
+}
+
+__global__ void k_bs_place(const int32_t* n_dev, const NormKey* __restrict__ keys, const BucketState* st,
+                           const int* __restrict__ off, const int* __restrict__ arrival, NormKey* __restrict__ tkeys,
+                           int32_t* __restrict__ tvals) {
   pdl_wait();
   const int n = *n_dev;
   const unsigned long long lo = st->lo;
   const int shift = bucket_shift(lo, st->hi);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const NormKey k = keys[i];
-    const int pos = atomicAdd(&cursor[bucket_of(k.norm, lo, shift)], 1);
+    const int pos = off[bucket_of(k.norm, lo, shift)] + arrival[i];
     tkeys[pos] = k;
     tvals[pos] = i;
+  }
+}
+
+// one warp per bucket of <= kWarpSortMax keys: position = offset + number of
+// the bucket's keys below this one
+__global__ void __launch_bounds__(256) k_bs_warp(const int* __restrict__ off, const NormKey* __restrict__ tkeys,
+                                                 const int32_t* __restrict__ tvals, NormKey* __restrict__ okeys,
+                                                 int32_t* __restrict__ ovals) {
+  pdl_wait();
+  __shared__ unsigned long long sn[8][kWarpSortMax];
+  __shared__ unsigned si[8][kWarpSortMax];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < kNB; b += warps) {
+    const int o = off[b], c = off[b + 1] - o;
+    if (c == 0 || c > kWarpSortMax) continue;
+    if (c <= 32) {
+      unsigned long long nm = ~0ull;
+      unsigned id = ~0u;
+      int v = 0;
+      if (lane < c) {
+        const NormKey k = tkeys[o + lane];
+        nm = k.norm;
+        id = k.id;
+        v = tvals[o + lane];
+      }
+      int r = 0;
+      for (int q = 0; q < c; ++q) {
+        const unsigned long long qn = __shfl_sync(0xffffffffu, nm, q);
+        const unsigned qi = __shfl_sync(0xffffffffu, id, q);
+        r += key_less(qn, qi, nm, id);
+      }
+      if (lane < c) {
+        okeys[o + r] = NormKey{nm, id};
+        ovals[o + r] = v;
+      }
+      continue;
+    }
+    for (int q = lane; q < c; q += 32) {
+      const NormKey k = tkeys[o + q];
+      sn[wl][q] = k.norm;
+      si[wl][q] = k.id;
+    }
+    __syncwarp();
+    for (int q0 = 0; q0 < c; q0 += 32) {
+      const int q = q0 + lane;
+      const bool mine = q < c;
+      const unsigned long long nm = mine ? sn[wl][q] : ~0ull;
+      const unsigned id = mine ? si[wl][q] : ~0u;
+      int r = 0;
+      for (int u = 0; u < c; ++u) r += key_less(sn[wl][u], si[wl][u], nm, id);
+      if (mine) {
+        okeys[o + r] = NormKey{nm, id};
+        ovals[o + r] = tvals[o + q];
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -201,24 +245,20 @@ __device__ __forceinline__ void smem_bitonic(unsigned long long* sn, unsigned* s
   }
 }
 
-// one CTA per bucket of <= kBucketCap items: sort in shared memory, write back
-__global__ void __launch_bounds__(256) k_bs_small(const int* __restrict__ off, const NormKey* __restrict__ tkeys,
+// one CTA per listed bucket of (kWarpSortMax, kBucketCap] keys: sort in
+// shared memory, write back
+__global__ void __launch_bounds__(256) k_bs_small(const int* __restrict__ off, const int* __restrict__ mid,
+                                                  const BucketState* st, const NormKey* __restrict__ tkeys,
                                                   const int32_t* __restrict__ tvals, NormKey* __restrict__ okeys,
                                                   int32_t* __restrict__ ovals) {
   pdl_wait();
   __shared__ unsigned long long sn[kBucketCap];
   __shared__ unsigned si[kBucketCap];
   __shared__ int sv[kBucketCap];
-  for (int b = blockIdx.x; b < kNB; b += gridDim.x) {
+  const int nmid = st->n_mid;
+  for (int q = blockIdx.x; q < nmid; q += gridDim.x) {
+    const int b = mid[q];
     const int o = off[b], cnt = off[b + 1] - o;
-    if (cnt == 0 || cnt > kBucketCap) continue;   // uniform per CTA
-    if (cnt == 1) {
-      if (threadIdx.x == 0) {
-        okeys[o] = tkeys[o];
-        ovals[o] = tvals[o];
-      }
-      continue;
-    }
     int m = 2;
     while (m < cnt) m <<= 1;
     for (int t = threadIdx.x; t < m; t += blockDim.x) {
@@ -332,15 +372,30 @@ __global__ void __launch_bounds__(256) k_bs_big(const int* __restrict__ off, con
   }
 }
 
-__global__ void k_bs_minmax(const int32_t* n_dev, const NormKey* __restrict__ keys, BucketState* st) {
+// keys for i < n (the tail up to n_max gets sentinels that sort last) and the
+// min / max norm bits over the n keys (one atomic pair per CTA)
+__global__ void __launch_bounds__(256) k_norm_keys(const int32_t* n_dev, int n_max, double p_grad,
+                                                   const int32_t* __restrict__ live,
+                                                   const int32_t* __restrict__ src_nodes,
+                                                   const double* __restrict__ norms, NormKey* __restrict__ keys,
+                                                   int32_t* __restrict__ vals, long long* k_out, BucketState* st) {
   pdl_wait();
+  __shared__ unsigned long long smn[8], smx[8];
   const int n = *n_dev;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *k_out = (long long)floor(p_grad * (double)n);  // cache.py:190
   unsigned long long mn = ~0ull, mx = 0ull;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const unsigned long long v = keys[i].norm;
-    mn = v < mn ? v : mn;
-    mx = v > mx ? v : mx;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_max; i += gridDim.x * blockDim.x) {
+    if (i < n) {
+      const unsigned long long v = (unsigned long long)__double_as_longlong(norms[i]);
+      keys[i] = NormKey{v, (unsigned)src_nodes[live[i]]};
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+    } else {
+      keys[i] = NormKey{~0ull, ~0u};
+    }
+    vals[i] = i;
   }
+  if (!st) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o), c = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -348,31 +403,19 @@ __global__ void k_bs_minmax(const int32_t* n_dev, const NormKey* __restrict__ ke
     mx = c > mx ? c : mx;
   }
   if ((threadIdx.x & 31) == 0) {
-    atomicMin(&st->lo, mn);
-    atomicMax(&st->hi, mx);
+    smn[threadIdx.x >> 5] = mn;
+    smx[threadIdx.x >> 5] = mx;
   }
-}
-
-struct NormKeyDecomposer {
-  __host__ __device__ ::cuda::std::tuple<unsigned long long&, unsigned&> operator()(NormKey& k) const {
-    return {k.norm, k.id};
-  }
-};
-
-// keys for i < n; the tail up to n_max gets sentinels that sort last
-__global__ void k_norm_keys(const int32_t* n_dev, int n_max, double p_grad, const int32_t* __restrict__ live,
-                            const int32_t* __restrict__ src_nodes, const double* __restrict__ norms,
-                            NormKey* __restrict__ keys, int32_t* __restrict__ vals, long long* k_out) {
-  pdl_wait();
-  const int n = *n_dev;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *k_out = (long long)floor(p_grad * (double)n);  // cache.py:190
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_max; i += gridDim.x * blockDim.x) {
-    if (i < n) {
-      keys[i] = NormKey{(unsigned long long)__double_as_longlong(norms[i]), (unsigned)src_nodes[live[i]]};
-    } else {
-      keys[i] = NormKey{~0ull, ~0u};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      mn = smn[w] < mn ? smn[w] : mn;
+      mx = smx[w] > mx ? smx[w] : mx;
     }
-    vals[i] = i;
+    if (mn != ~0ull) {
+      atomicMin(&st->lo, mn);
+      atomicMax(&st->hi, mx);
+    }
   }
 }
 
@@ -600,18 +643,16 @@ using namespace hg;
 
 extern "C" {
 
+static long long bucket_tail_bytes(long long nn) {
+  // k2 (16 B), v2, arrival (4 B each), state, count + scount, off, mid, big
+  return nn * 24 + 64 + 4LL * (kNB + kNSuper + (kNB + 1) + 2 * kNB) + 64;
+}
+
 long long hg_cache_update_scratch_bytes(long long n_max) {
-  size_t tmp = 0, tmp2 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const NormKey*)nullptr, (NormKey*)nullptr, (const int32_t*)nullptr,
-                                  (int32_t*)nullptr, (int)(n_max > 0 ? n_max : 1), NormKeyDecomposer{});
-  cub::DeviceMergeSort::SortPairs(nullptr, tmp2, (NormKey*)nullptr, (int32_t*)nullptr, (int)(n_max > 0 ? n_max : 1),
-                                  NormKeyLess{});
-  if (tmp2 > tmp) tmp = tmp2;
   const long long n = n_max + 16;
   // keys_in, keys_out (16 B), vals_in, vals_out, wlist (4 B), wflag, retained (1 B), scan partials,
-  // bucket sort: second key/val buffers + state + count/off/cursor/big
-  return n * 16 * 2 + n * 4 * 3 + n * 2 + (scan_tiles(n_max) + 1) * 4 + (long long)tmp + 2048 + n * 20 + 64 +
-         4LL * (4 * kNB + 16);
+  // bucket-sort tail
+  return n * 16 * 2 + n * 4 * 3 + n * 2 + (scan_tiles(n_max) + 1) * 4 + 2048 + bucket_tail_bytes(n);
 }
 
 }  // extern "C"
@@ -645,24 +686,26 @@ RankBufs carve(void* scratch, long long scratch_bytes, long long n_max) {
 }
 
 // U1: (norm bits, id) keys of the n live nodes sorted into keys_out /
-// vals_out by the bucket sort (6 launches); *k_out = floor(p_grad * n)
+// vals_out by the bucket sort; *k_out = floor(p_grad * n)
 int bucket_rank(const char* W, const int32_t* n_dev, int n_max, double p_grad, const int32_t* live,
                 const int32_t* src_nodes, const double* norms, long long* k_out, const RankBufs& rb,
                 cudaStream_t stream) {
   const long long nn = n_max + 16;
-  const size_t need = (size_t)nn * 20 + 64 + 4 * (4 * kNB + 16);
+  const size_t need = (size_t)bucket_tail_bytes(nn);
   const uintptr_t end = reinterpret_cast<uintptr_t>(rb.tmp) + rb.tmp_bytes;
   char* bp = reinterpret_cast<char*>((end - need - 16) & ~uintptr_t(15));   // 16-byte aligned tail region
   NormKey* k2 = reinterpret_cast<NormKey*>(bp);
   int32_t* v2 = reinterpret_cast<int32_t*>(k2 + nn);
-  BucketState* bst = reinterpret_cast<BucketState*>((reinterpret_cast<uintptr_t>(v2 + nn) + 15) & ~uintptr_t(15));
+  int* arrival = v2 + nn;
+  BucketState* bst = reinterpret_cast<BucketState*>((reinterpret_cast<uintptr_t>(arrival + nn) + 15) & ~uintptr_t(15));
   int* count = reinterpret_cast<int*>(bst + 1);
-  int* off = count + kNB;
-  int* cursor = off + kNB + 1;
-  int* big = cursor + kNB;
+  int* scount = count + kNB;
+  int* off = scount + kNSuper;
+  int* mid = off + kNB + 1;
+  int* big = mid + kNB;
   HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->lo, 0xFF, 8, stream));
-  HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->hi, 0x00, 8, stream));
-  HG_CHECK_CUDA(W, cudaMemsetAsync(count, 0, 4 * kNB, stream));
+  // hi, n_big, n_mid, count, scount: one zero fill
+  HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->hi, 0x00, 16 + 4 * ((size_t)kNB + kNSuper), stream));
   const unsigned g = grid_for(n_max, 256, 148 * 4);
 #define HG_L(K, G, B, ...)                                                                   \
   {                                                                                          \
@@ -671,20 +714,15 @@ int bucket_rank(const char* W, const int32_t* n_dev, int n_max, double p_grad, c
     HG_LAUNCHED(W);                                                                          \
   }
   // keys -> k2 / v2; bucketed -> keys_in / vals_in; sorted -> keys_out / vals_out
-  HG_L(k_norm_keys, grid_for(n_max, 256), 256, n_dev, n_max, p_grad, live, src_nodes, norms, k2, v2, k_out);
-  HG_L(k_bs_minmax, g, 256, n_dev, (const NormKey*)k2, bst);
-  {
-    const int hs = ensure_smem_attr((const void*)k_bs_hist, 4 * kNB, W);
-    if (hs) return hs;
-    const cudaError_t _pe = hg::launch_pdl(k_bs_hist, dim3(g), dim3(256), (size_t)4 * kNB, stream, n_dev,
-                                           (const NormKey*)k2, (const BucketState*)bst, count);
-    if (_pe != cudaSuccess) return hg::fail(W, hg::kCuda, cudaGetErrorString(_pe));
-    HG_LAUNCHED(W);
-  }
-  HG_L(k_bs_scan, 1, 1024, (const int*)count, off, cursor, big, bst);
-  HG_L(k_bs_scatter, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, cursor, rb.keys_in, rb.vals_in);
-  HG_L(k_bs_small, 148 * 8, 256, (const int*)off, (const NormKey*)rb.keys_in, (const int32_t*)rb.vals_in,
+  HG_L(k_norm_keys, grid_for(n_max, 256), 256, n_dev, n_max, p_grad, live, src_nodes, norms, k2, v2, k_out, bst);
+  HG_L(k_bs_count, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, count, scount, arrival);
+  HG_L(k_bs_offsets, kNSuper, kSuperB, (const int*)count, (const int*)scount, off, mid, big, bst);
+  HG_L(k_bs_place, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, (const int*)off, (const int*)arrival,
+       rb.keys_in, rb.vals_in);
+  HG_L(k_bs_warp, 148 * 8, 256, (const int*)off, (const NormKey*)rb.keys_in, (const int32_t*)rb.vals_in,
        rb.keys_out, rb.vals_out);
+  HG_L(k_bs_small, 148 * 2, 256, (const int*)off, (const int*)mid, (const BucketState*)bst,
+       (const NormKey*)rb.keys_in, (const int32_t*)rb.vals_in, rb.keys_out, rb.vals_out);
   HG_L(k_bs_big, 64, 256, (const int*)off, (const int*)big, (const BucketState*)bst, rb.keys_in, rb.vals_in, k2, v2,
        rb.keys_out, rb.vals_out);
 #undef HG_L
@@ -706,24 +744,8 @@ int hg_cache_rank(const int32_t* n_dev, int n_max, double p_grad, const int32_t*
   if (scratch_bytes < hg_cache_update_scratch_bytes(n_max)) return fail(W, kBadArg, "scratch too small");
   if (n_max <= 0) return kOk;
   const RankBufs rb = carve(scratch, scratch_bytes, n_max);
-  const int mode = sort_mode(n_max);
-  if (mode == kSortBucket) {
-    const int s = bucket_rank(W, n_dev, n_max, p_grad, live, src_nodes, norms, layer_ctr + kCtrK, rb, stream);
-    if (s) return s;
-  } else {
-    const bool radix = mode == kSortRadix;
-    // the merge sort is in place: keys go straight to keys_out / vals_out
-    HG_CHECK_CUDA(W, hg::launch_pdl(k_norm_keys, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev, n_max,
-                                    p_grad, live, src_nodes, norms, radix ? rb.keys_in : rb.keys_out,
-                                    radix ? rb.vals_in : rb.vals_out, layer_ctr + kCtrK));
-    HG_LAUNCHED(W);
-    size_t tb = rb.tmp_bytes;
-    cudaError_t e = radix ? cub::DeviceRadixSort::SortPairs(rb.tmp, tb, rb.keys_in, rb.keys_out, rb.vals_in,
-                                                            rb.vals_out, n_max, NormKeyDecomposer{}, stream)
-                          : cub::DeviceMergeSort::SortPairs(rb.tmp, tb, rb.keys_out, rb.vals_out, n_max,
-                                                            NormKeyLess{}, stream);
-    if (e != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(e));
-  }
+  const int s = bucket_rank(W, n_dev, n_max, p_grad, live, src_nodes, norms, layer_ctr + kCtrK, rb, stream);
+  if (s) return s;
   HG_CHECK_CUDA(W, hg::launch_pdl(k_rank_admit, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev,
                                   (const NormKey*)rb.keys_out, (const int32_t*)rb.vals_out, live, computed_flag,
                                   row_of, row_owner, rb.wflag, rb.retained, layer_ctr));

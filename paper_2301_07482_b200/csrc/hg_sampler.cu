@@ -282,8 +282,18 @@ __global__ void k_pick(const int32_t* __restrict__ g_col, const int32_t* counts_
 //                  count, so the 32 loops of a warp have the same length.
 // Every path keeps the (key53, j) order of the reference's argsort.
 // ------------------------------------------------------------------------
-constexpr long long kHuge = 4096;
-constexpr int kSegC = 2048;
+// rows of more than kHuge candidates are split into segments of kSegC: a
+// warp's item is then at most ~kHuge candidates long, which bounds the
+// latency tail of the small layers (1024 seeds: a few long rows per layer)
+#ifndef HG_SEL_HUGE
+#define HG_SEL_HUGE 1024
+#endif
+#ifndef HG_SEL_SEG
+#define HG_SEL_SEG 512
+#endif
+constexpr long long kHuge = HG_SEL_HUGE;
+constexpr int kSegC = HG_SEL_SEG;
+static_assert(kSegC <= 2048 && kSegC >= 32 && kHuge >= kSegC, "segments are packed with 11-bit positions");
 constexpr int kMaxSegs = 1 << 16;     // per layer; hubs beyond are warp rows
 constexpr int kBins = 320;            // candidate counts 0..255 exact, then 64 wide, last bin open
 constexpr int kLaneCap = 255;         // lane_max <= kLaneCap
@@ -304,7 +314,6 @@ struct Plan {
   int32_t* hub_base;   // [F_max] first segment of the hub
   int* hub_done;       // [F_max] segments finished
   int32_t* seg_hub;    // [kMaxSegs] hub of the segment (-1: unused)
-  u128* seg_state;     // [kMaxSegs] state before the segment's first draw
   unsigned long long* seg_key;  // [kMaxSegs * 32] key53 of the segment's picks
   int32_t* seg_j;      // [kMaxSegs * 32] row-global candidate position
   uint8_t* flag;       // [F_max] 1 = hub row
@@ -333,12 +342,7 @@ __global__ void __launch_bounds__(256) k_plan(const int32_t* F_dev, const int64_
         P.hub_row[i] = j;
         P.hub_base[i] = base;
         P.hub_done[i] = 0;
-        u128 ss_q = st;
-        for (int q = 0; q < nseg; ++q) {
-          P.seg_hub[base + q] = i;
-          P.seg_state[base + q] = ss_q;
-          if (q + 1 < nseg) ss_q = pcg_jump(g_jump, ss_q, inc, (unsigned long long)kSegC);
-        }
+        for (int q = 0; q < nseg; ++q) P.seg_hub[base + q] = i;
       } else {
         for (int q = base; q < kMaxSegs && q < base + nseg; ++q) P.seg_hub[q] = -1;
       }
@@ -491,7 +495,9 @@ __global__ void __launch_bounds__(kSelThreads, 4) k_select_all(
       const int sidx = item - P.hub_base[i];
       const long long j0 = (long long)sidx * kSegC;
       const long long len = deg - j0 < kSegC ? deg - j0 : kSegC;
-      const unsigned long long best = warp_topk_packed(fma128(a1, P.seg_state[item], c1), len, fanout, a32, c32);
+      // the segment's start state: a short jump from the row's
+      const u128 sst = pcg_jump(g_jump, P.row_state[row], inc, (unsigned long long)j0);
+      const unsigned long long best = warp_topk_packed(fma128(a1, sst, c1), len, fanout, a32, c32);
       const int cnt = (int)(len < fanout ? len : fanout);
       P.seg_key[(long long)item * 32 + lane] = lane < cnt ? (best >> 11) : ~0ull;
       P.seg_j[(long long)item * 32 + lane] = lane < cnt ? (int32_t)(j0 + (long long)(best & 2047ull)) : 0x7fffffff;
@@ -791,7 +797,7 @@ static long long a16(long long x) { return (x + 15) & ~15ll; }
 static long long plan_scratch_bytes(long long F_max) {
   const long long F = F_max + 16;
   return a16((16 + 2 * kBins) * 4) + a16(F * 4) + a16(F * 16) + 3 * a16(F * 4) + a16((long long)kMaxSegs * 4) +
-         a16((long long)kMaxSegs * 16) + a16((long long)kMaxSegs * 32 * 8) + a16((long long)kMaxSegs * 32 * 4) +
+         a16((long long)kMaxSegs * 32 * 8) + a16((long long)kMaxSegs * 32 * 4) +
          a16(F) + 64;
 }
 
@@ -813,7 +819,6 @@ static Plan carve_plan(char* p, long long F_max) {
   P.hub_base = reinterpret_cast<int32_t*>(take(F * 4));
   P.hub_done = reinterpret_cast<int*>(take(F * 4));
   P.seg_hub = reinterpret_cast<int32_t*>(take((long long)kMaxSegs * 4));
-  P.seg_state = reinterpret_cast<u128*>(take((long long)kMaxSegs * 16));
   P.seg_key = reinterpret_cast<unsigned long long*>(take((long long)kMaxSegs * 32 * 8));
   P.seg_j = reinterpret_cast<int32_t*>(take((long long)kMaxSegs * 32 * 4));
   P.flag = reinterpret_cast<uint8_t*>(take(F));
@@ -825,7 +830,7 @@ static Plan carve_plan(char* p, long long F_max) {
 static int lane_max_env() {
   static const int v = [] {
     const char* e = std::getenv("HG_SEL_LANE_MAX");
-    const int x = e ? std::atoi(e) : 128;
+    const int x = e ? std::atoi(e) : 64;
     return x < 0 ? 0 : (x > kLaneCap ? kLaneCap : x);
   }();
   return v;
