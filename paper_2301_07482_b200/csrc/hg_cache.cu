@@ -37,36 +37,78 @@ struct NormKey {
 // kNB buckets by (bits - lo) >> shift (monotone; equal norms share a bucket).
 // Keys are distinct (ids are), so the result is the unique sorted order.
 //   k_norm_keys   keys + the min / max norm bits (block-reduced)
-//   k_bs_count    bucket of every key, its arrival rank in the bucket, the
-//                 bucket and super-bucket (256 buckets) counts
-//   k_bs_offsets  one CTA per super-bucket: bucket offsets (prefix of the
-//                 super totals + the in-super prefix), lists of the buckets
-//                 too long for a warp
+//   k_bs_count    bucket of every key and its arrival rank in the bucket
+//   k_bs_offsets  one CTA per super-bucket of 256: in-super offsets, the
+//                 super total; the last CTA to finish scans the super totals
+//                 (offset of bucket b = loc[b] + spre[b / 256])
 //   k_bs_place    keys to their bucket slots (offset + arrival rank)
-//   k_bs_warp     one warp per bucket of <= kWarpSortMax keys: each key's final
-//                 position = its bucket offset + the number of bucket keys
-//                 below it (all-pairs count; exact because keys are distinct)
-//   k_bs_small    one CTA per listed bucket of <= kBucketCap keys (bitonic
-//                 in shared memory); k_bs_big above (chunk sorts + merges)
-// 64K buckets: the C2 layer-1 norms (~130K, 2.4 decades) leave buckets of
-// median 2 / 99th percentile ~65 keys (tools/norm_dist.py); at 16K buckets
-// 77 % of the keys sat in buckets of > 32 that needed CTA sorts.
+//   k_bs_rank     one thread per key of a bucket of <= kShortMax keys: its
+//                 final position = bucket offset + the number of the bucket's
+//                 keys below it (exact because keys are distinct)
+//   k_bs_long     one CTA per longer bucket: bitonic sort in shared memory up
+//                 to kBucketCap keys, chunk sorts + merge passes above
+// The writers of the sorted positions also apply U2 (admission / gradient
+// eviction flags) when an Admit is given, so no separate pass reads the
+// sorted keys back. 64K buckets: the C2 layer-1 norms (~130K over 2.4
+// decades) leave buckets of median 2 / 99th percentile ~65 keys
+// (tools/norm_dist.py); at 16K buckets 77 % of them sat in buckets of > 32.
 #ifndef HG_CACHE_NB
 #define HG_CACHE_NB 65536
 #endif
 constexpr int kNB = HG_CACHE_NB;
-static_assert((kNB & (kNB - 1)) == 0 && kNB >= 65536 / 64 && kNB % 256 == 0, "bucket count: a power of two");
 constexpr int kSuperB = 256;                 // buckets per super-bucket
 constexpr int kNSuper = kNB / kSuperB;
-static_assert(kNSuper <= 1024, "super-bucket scan: one CTA");
+static_assert((kNB & (kNB - 1)) == 0 && kNSuper >= 1 && kNSuper <= kSuperB,
+              "bucket count: a power of two, at most 256 super-buckets");
 constexpr int kBucketCap = 2048;
-constexpr int kWarpSortMax = 128;
+constexpr int kShortMax = 128;
 
 struct BucketState {            // device scratch
   unsigned long long lo, hi;    // min / max norm bits over the n live keys
-  int n_big;                    // buckets above kBucketCap
-  int n_mid;                    // buckets of (kWarpSortMax, kBucketCap]
+  int n_long;                   // buckets above kShortMax
+  int ticket;                   // k_bs_offsets CTAs done
+  int pad[2];
 };
+
+struct Admit {                  // U2 applied by the sort's writers (ctr null: off)
+  const int32_t* live;
+  const uint8_t* computed;
+  int32_t* row_of;
+  int32_t* row_owner;
+  uint8_t* wflag;
+  uint8_t* retained;
+  long long* ctr;
+};
+
+// sorted position j holds key id (input index i): admission (j < k), write /
+// retained flags, gradient eviction of a cached loser; returns evicted
+__device__ __forceinline__ bool admit_pos(const Admit& A, long long k, int j, unsigned id, int i) {
+  const bool admitted = j < k;
+  const bool computed = A.computed[A.live[i]] != 0;
+  bool evicted = false;
+  if (!admitted) {
+    const int r = A.row_of[id];
+    if (r >= 0) {
+      A.row_owner[r] = -1;
+      A.row_of[id] = -1;
+      evicted = true;
+    }
+  }
+  A.wflag[j] = admitted && computed;
+  A.retained[j] = admitted && !computed;
+  return evicted;
+}
+// every thread of the CTA: add the evictions counted by its threads
+__device__ __forceinline__ void admit_flush(const Admit& A, int evicted) {
+  if (!A.ctr) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) evicted += __shfl_xor_sync(0xffffffffu, evicted, o);
+  if ((threadIdx.x & 31) == 0 && evicted) {
+    unsigned long long* c = reinterpret_cast<unsigned long long*>(A.ctr);
+    atomicAdd(c + kCtrGradientEvictions, (unsigned long long)evicted);
+    atomicAdd(c + kCtrValid, (unsigned long long)(-(long long)evicted));
+  }
+}
 
 __device__ __forceinline__ int bucket_of(unsigned long long bits, unsigned long long lo, int shift) {
   const unsigned long long b = (bits - lo) >> shift;
@@ -81,18 +123,18 @@ __device__ __forceinline__ int bucket_shift(unsigned long long lo, unsigned long
 __device__ __forceinline__ bool key_less(unsigned long long an, unsigned ai, unsigned long long bn, unsigned bi) {
   return an < bn || (an == bn && ai < bi);
 }
+__device__ __forceinline__ int bucket_off(const int* loc, const int* spre, int b) {
+  return loc[b] + spre[b / kSuperB];
+}
 
 __global__ void k_bs_count(const int32_t* n_dev, const NormKey* __restrict__ keys, const BucketState* st,
-                           int* __restrict__ count, int* __restrict__ scount, int* __restrict__ arrival) {
+                           int* __restrict__ count, int* __restrict__ arrival) {
   pdl_wait();
   const int n = *n_dev;
   const unsigned long long lo = st->lo;
   const int shift = bucket_shift(lo, st->hi);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int b = bucket_of(keys[i].norm, lo, shift);
-    arrival[i] = atomicAdd(&count[b], 1);
-    atomicAdd(&scount[b / kSuperB], 1);
-  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    arrival[i] = atomicAdd(&count[bucket_of(keys[i].norm, lo, shift)], 1);
 }
 
 // exclusive block scan of one int per thread (blockDim.x <= 1024)
@@ -123,105 +165,76 @@ __device__ __forceinline__ int block_excl_scan(int x, int* wsum) {
   return r;
 }
 
-__global__ void __launch_bounds__(kSuperB) k_bs_offsets(const int* __restrict__ count, const int* __restrict__ scount,
-                                                        int* __restrict__ off, int* __restrict__ mid,
-                                                        int* __restrict__ big, BucketState* st) {
+__global__ void __launch_bounds__(kSuperB) k_bs_offsets(const int* __restrict__ count, int* __restrict__ loc,
+                                                        int* __restrict__ stot, int* __restrict__ spre,
+                                                        int* __restrict__ longl, BucketState* st) {
   pdl_wait();
   __shared__ int wsum[32];
-  __shared__ int sbase;
+  __shared__ int last;
   const int s = blockIdx.x, t = threadIdx.x;
-  // prefix of the super-bucket totals before s (kNSuper <= 1024: strided)
-  int acc = 0;
-  for (int q = t; q < s; q += kSuperB) acc += scount[q];
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-  if ((t & 31) == 0) wsum[t >> 5] = acc;
-  __syncthreads();
-  if (t == 0) {
-    int b0 = 0;
-    for (int q = 0; q < kSuperB / 32; ++q) b0 += wsum[q];
-    sbase = b0;
-  }
-  __syncthreads();
   const int b = s * kSuperB + t;
   const int c = count[b];
-  const int e = sbase + block_excl_scan(c, wsum);
-  off[b] = e;
-  if (b == kNB - 1) off[kNB] = e + c;
-  if (c > kBucketCap) big[atomicAdd(&st->n_big, 1)] = b;
-  else if (c > kWarpSortMax) mid[atomicAdd(&st->n_mid, 1)] = b;
+  const int e = block_excl_scan(c, wsum);
+  loc[b] = e;
+  if (c > kShortMax) longl[atomicAdd(&st->n_long, 1)] = b;
+  if (t == kSuperB - 1) {
+    stot[s] = e + c;
+    __threadfence();
+    last = atomicAdd(&st->ticket, 1) == kNSuper - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int v = t < kNSuper ? __ldcg(&stot[t]) : 0;
+  const int pe = block_excl_scan(v, wsum);
+  if (t < kNSuper) spre[t] = pe;
 }
 
 __global__ void k_bs_place(const int32_t* n_dev, const NormKey* __restrict__ keys, const BucketState* st,
-                           const int* __restrict__ off, const int* __restrict__ arrival, NormKey* __restrict__ tkeys,
-                           int32_t* __restrict__ tvals) {
+                           const int* __restrict__ loc, const int* __restrict__ spre, const int* __restrict__ arrival,
+                           NormKey* __restrict__ tkeys, int32_t* __restrict__ tvals) {
   pdl_wait();
   const int n = *n_dev;
   const unsigned long long lo = st->lo;
   const int shift = bucket_shift(lo, st->hi);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const NormKey k = keys[i];
-    const int pos = off[bucket_of(k.norm, lo, shift)] + arrival[i];
+    const int pos = bucket_off(loc, spre, bucket_of(k.norm, lo, shift)) + arrival[i];
     tkeys[pos] = k;
     tvals[pos] = i;
   }
 }
 
-// one warp per bucket of <= kWarpSortMax keys: position = offset + number of
-// the bucket's keys below this one
-__global__ void __launch_bounds__(256) k_bs_warp(const int* __restrict__ off, const NormKey* __restrict__ tkeys,
+// one thread per key of a short bucket (<= kShortMax keys)
+__global__ void __launch_bounds__(256) k_bs_rank(const int32_t* n_dev, const BucketState* st,
+                                                 const int* __restrict__ count, const int* __restrict__ loc,
+                                                 const int* __restrict__ spre, const NormKey* __restrict__ tkeys,
                                                  const int32_t* __restrict__ tvals, NormKey* __restrict__ okeys,
-                                                 int32_t* __restrict__ ovals) {
+                                                 int32_t* __restrict__ ovals, Admit A) {
   pdl_wait();
-  __shared__ unsigned long long sn[8][kWarpSortMax];
-  __shared__ unsigned si[8][kWarpSortMax];
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < kNB; b += warps) {
-    const int o = off[b], c = off[b + 1] - o;
-    if (c == 0 || c > kWarpSortMax) continue;
-    if (c <= 32) {
-      unsigned long long nm = ~0ull;
-      unsigned id = ~0u;
-      int v = 0;
-      if (lane < c) {
-        const NormKey k = tkeys[o + lane];
-        nm = k.norm;
-        id = k.id;
-        v = tvals[o + lane];
-      }
-      int r = 0;
-      for (int q = 0; q < c; ++q) {
-        const unsigned long long qn = __shfl_sync(0xffffffffu, nm, q);
-        const unsigned qi = __shfl_sync(0xffffffffu, id, q);
-        r += key_less(qn, qi, nm, id);
-      }
-      if (lane < c) {
-        okeys[o + r] = NormKey{nm, id};
-        ovals[o + r] = v;
-      }
-      continue;
+  const int n = *n_dev;
+  const unsigned long long lo = st->lo;
+  const int shift = bucket_shift(lo, st->hi);
+  const long long k = A.ctr ? A.ctr[kCtrK] : 0;
+  int evicted = 0;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const NormKey key = tkeys[p];
+    const int b = bucket_of(key.norm, lo, shift);
+    const int c = count[b];
+    if (c > kShortMax) continue;
+    const int o = bucket_off(loc, spre, b);
+    int r = 0;
+    for (int q = 0; q < c; ++q) {
+      const NormKey x = tkeys[o + q];
+      r += key_less(x.norm, x.id, key.norm, key.id);
     }
-    for (int q = lane; q < c; q += 32) {
-      const NormKey k = tkeys[o + q];
-      sn[wl][q] = k.norm;
-      si[wl][q] = k.id;
-    }
-    __syncwarp();
-    for (int q0 = 0; q0 < c; q0 += 32) {
-      const int q = q0 + lane;
-      const bool mine = q < c;
-      const unsigned long long nm = mine ? sn[wl][q] : ~0ull;
-      const unsigned id = mine ? si[wl][q] : ~0u;
-      int r = 0;
-      for (int u = 0; u < c; ++u) r += key_less(sn[wl][u], si[wl][u], nm, id);
-      if (mine) {
-        okeys[o + r] = NormKey{nm, id};
-        ovals[o + r] = tvals[o + q];
-      }
-    }
-    __syncwarp();
+    const int j = o + r;
+    const int i = tvals[p];
+    okeys[j] = key;
+    ovals[j] = i;
+    if (A.ctr) evicted += admit_pos(A, k, j, key.id, i);
   }
+  admit_flush(A, evicted);
 }
 
 // in-smem bitonic sort of m (power of 2) (norm, id, val) items
@@ -245,43 +258,6 @@ __device__ __forceinline__ void smem_bitonic(unsigned long long* sn, unsigned* s
   }
 }
 
-// one CTA per listed bucket of (kWarpSortMax, kBucketCap] keys: sort in
-// shared memory, write back
-__global__ void __launch_bounds__(256) k_bs_small(const int* __restrict__ off, const int* __restrict__ mid,
-                                                  const BucketState* st, const NormKey* __restrict__ tkeys,
-                                                  const int32_t* __restrict__ tvals, NormKey* __restrict__ okeys,
-                                                  int32_t* __restrict__ ovals) {
-  pdl_wait();
-  __shared__ unsigned long long sn[kBucketCap];
-  __shared__ unsigned si[kBucketCap];
-  __shared__ int sv[kBucketCap];
-  const int nmid = st->n_mid;
-  for (int q = blockIdx.x; q < nmid; q += gridDim.x) {
-    const int b = mid[q];
-    const int o = off[b], cnt = off[b + 1] - o;
-    int m = 2;
-    while (m < cnt) m <<= 1;
-    for (int t = threadIdx.x; t < m; t += blockDim.x) {
-      if (t < cnt) {
-        sn[t] = tkeys[o + t].norm;
-        si[t] = tkeys[o + t].id;
-        sv[t] = tvals[o + t];
-      } else {
-        sn[t] = ~0ull;
-        si[t] = ~0u;
-        sv[t] = -1;
-      }
-    }
-    __syncthreads();
-    smem_bitonic(sn, si, sv, m);
-    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
-      okeys[o + t] = NormKey{sn[t], si[t]};
-      ovals[o + t] = sv[t];
-    }
-    __syncthreads();
-  }
-}
-
 // merge path: number of items taken from A among the first d of merge(A, B)
 __device__ __forceinline__ int merge_split(const NormKey* A, int na, const NormKey* B, int nb, int d) {
   int lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
@@ -294,25 +270,32 @@ __device__ __forceinline__ int merge_split(const NormKey* A, int na, const NormK
   return lo;
 }
 
-// big buckets (> kBucketCap items): one CTA each; chunk sort in shared memory,
-// then bottom-up merge passes between tkeys/tvals and the b2 buffers
-__global__ void __launch_bounds__(256) k_bs_big(const int* __restrict__ off, const int* __restrict__ big,
-                                                const BucketState* st, NormKey* __restrict__ tkeys,
-                                                int32_t* __restrict__ tvals, NormKey* __restrict__ k2,
-                                                int32_t* __restrict__ v2, NormKey* __restrict__ okeys,
-                                                int32_t* __restrict__ ovals) {
+// one CTA per listed bucket of > kShortMax keys: up to kBucketCap keys one
+// shared-memory bitonic sort; above, sorted chunks of kBucketCap and
+// bottom-up merge passes ping-ponging between tkeys/tvals and k2/v2
+__global__ void __launch_bounds__(256) k_bs_long(const int* __restrict__ count, const int* __restrict__ loc,
+                                                 const int* __restrict__ spre, const int* __restrict__ longl,
+                                                 const BucketState* st, NormKey* __restrict__ tkeys,
+                                                 int32_t* __restrict__ tvals, NormKey* __restrict__ k2,
+                                                 int32_t* __restrict__ v2, NormKey* __restrict__ okeys,
+                                                 int32_t* __restrict__ ovals, Admit A) {
   pdl_wait();
   __shared__ unsigned long long sn[kBucketCap];
   __shared__ unsigned si[kBucketCap];
   __shared__ int sv[kBucketCap];
-  const int nbig = st->n_big;
-  for (int q = blockIdx.x; q < nbig; q += gridDim.x) {
-    const int b = big[q];
-    const int o = off[b], cnt = off[b + 1] - o;
-    // 1. sorted chunks of kBucketCap
+  const int nlong = st->n_long;
+  const long long k = A.ctr ? A.ctr[kCtrK] : 0;
+  int evicted = 0;
+  for (int q = blockIdx.x; q < nlong; q += gridDim.x) {
+    const int b = longl[q];
+    const int o = bucket_off(loc, spre, b), cnt = count[b];
+    // 1. sorted chunks of up to kBucketCap (one chunk: straight to the output)
+    const bool one = cnt <= kBucketCap;
     for (int c0 = 0; c0 < cnt; c0 += kBucketCap) {
       const int len = cnt - c0 < kBucketCap ? cnt - c0 : kBucketCap;
-      for (int t = threadIdx.x; t < kBucketCap; t += blockDim.x) {
+      int m = 2;
+      while (m < len) m <<= 1;
+      for (int t = threadIdx.x; t < m; t += blockDim.x) {
         if (t < len) {
           sn[t] = tkeys[o + c0 + t].norm;
           si[t] = tkeys[o + c0 + t].id;
@@ -324,14 +307,21 @@ __global__ void __launch_bounds__(256) k_bs_big(const int* __restrict__ off, con
         }
       }
       __syncthreads();
-      smem_bitonic(sn, si, sv, kBucketCap);
+      smem_bitonic(sn, si, sv, m);
       for (int t = threadIdx.x; t < len; t += blockDim.x) {
-        tkeys[o + c0 + t] = NormKey{sn[t], si[t]};
-        tvals[o + c0 + t] = sv[t];
+        if (one) {
+          okeys[o + t] = NormKey{sn[t], si[t]};
+          ovals[o + t] = sv[t];
+          if (A.ctr) evicted += admit_pos(A, k, o + t, si[t], sv[t]);
+        } else {
+          tkeys[o + c0 + t] = NormKey{sn[t], si[t]};
+          tvals[o + c0 + t] = sv[t];
+        }
       }
       __syncthreads();
     }
-    // 2. merge passes: runs of width w -> 2w, ping-pong between t* and *2
+    if (one) continue;
+    // 2. merge passes: runs of width w -> 2w
     NormKey* sk = tkeys + o;
     int32_t* svv = tvals + o;
     NormKey* dk = k2 + o;
@@ -340,17 +330,17 @@ __global__ void __launch_bounds__(256) k_bs_big(const int* __restrict__ off, con
       for (int p0 = 0; p0 < cnt; p0 += 2 * w) {
         const int na = cnt - p0 < w ? cnt - p0 : w;
         const int nb = cnt - p0 - na < w ? (cnt - p0 - na > 0 ? cnt - p0 - na : 0) : w;
-        const NormKey* A = sk + p0;
-        const NormKey* B = A + na;
+        const NormKey* Aa = sk + p0;
+        const NormKey* B = Aa + na;
         const int tot = na + nb;
         const int per = (tot + blockDim.x - 1) / blockDim.x;
         const int d0 = threadIdx.x * per < tot ? threadIdx.x * per : tot;
         const int d1 = d0 + per < tot ? d0 + per : tot;
-        int ia = merge_split(A, na, B, nb, d0), ib = d0 - ia;
+        int ia = merge_split(Aa, na, B, nb, d0), ib = d0 - ia;
         for (int d = d0; d < d1; ++d) {
-          const bool takeA = ib >= nb || (ia < na && key_less(A[ia].norm, A[ia].id, B[ib].norm, B[ib].id));
+          const bool takeA = ib >= nb || (ia < na && key_less(Aa[ia].norm, Aa[ia].id, B[ib].norm, B[ib].id));
           if (takeA) {
-            dk[p0 + d] = A[ia];
+            dk[p0 + d] = Aa[ia];
             dvv[p0 + d] = svv[p0 + ia];
             ++ia;
           } else {
@@ -365,11 +355,14 @@ __global__ void __launch_bounds__(256) k_bs_big(const int* __restrict__ off, con
       int32_t* tv = svv; svv = dvv; dvv = tv;
     }
     for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
-      okeys[o + t] = sk[t];
+      const NormKey x = sk[t];
+      okeys[o + t] = x;
       ovals[o + t] = svv[t];
+      if (A.ctr) evicted += admit_pos(A, k, o + t, x.id, svv[t]);
     }
     __syncthreads();
   }
+  admit_flush(A, evicted);
 }
 
 // keys for i < n (the tail up to n_max gets sentinels that sort last) and the
@@ -416,36 +409,6 @@ __global__ void __launch_bounds__(256) k_norm_keys(const int32_t* n_dev, int n_m
       atomicMin(&st->lo, mn);
       atomicMax(&st->hi, mx);
     }
-  }
-}
-
-__global__ void k_rank_admit(const int32_t* n_dev, const NormKey* __restrict__ skeys,
-                             const int32_t* __restrict__ svals, const int32_t* __restrict__ live,
-                             const uint8_t* __restrict__ computed_flag, int32_t* __restrict__ row_of,
-                             int32_t* __restrict__ row_owner, uint8_t* __restrict__ wflag,
-                             uint8_t* __restrict__ retained, long long* ctr) {
-  pdl_wait();
-  unsigned long long* c = reinterpret_cast<unsigned long long*>(ctr);
-  const int n = *n_dev;
-  const long long k = ctr[kCtrK];
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const int id = (int)skeys[j].id;
-    const int i = svals[j];
-    const bool admitted = j < k;
-    const bool computed = computed_flag[live[i]] != 0;
-    bool evicted = false;
-    if (!admitted) {
-      const int r = row_of[id];
-      if (r >= 0) {
-        row_owner[r] = -1;
-        row_of[id] = -1;
-        evicted = true;
-      }
-    }
-    wflag[j] = admitted && computed;
-    retained[j] = admitted && !computed;
-    warp_count_add(c + kCtrGradientEvictions, evicted);
-    if (evicted) atomicAdd(c + kCtrValid, (unsigned long long)-1ll);
   }
 }
 
@@ -542,7 +505,10 @@ __global__ void k_ring_scan(int cap, const int32_t* it_dev, double t_stale, int 
   }
 }
 
-// one warp per written row
+// a warp takes 32 consecutive write slots: the lanes resolve their slot's
+// node, source row and ring row at once (and set the ownership maps), then
+// the warp copies the rows four at a time with 16-byte vectors (rows of up to
+// 256 floats held in registers, so 8 loads per lane are in flight)
 __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* __restrict__ skeys,
                              const int32_t* __restrict__ svals, const int32_t* __restrict__ live,
                              const float* __restrict__ emb, int H, int cap, const int32_t* it_dev,
@@ -559,23 +525,61 @@ __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* _
   const int lane = threadIdx.x & 31;
   const int it = *it_dev;
   const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < neff; w += warps) {
-    const int j = wlist[w0 + w];
-    const int id = (int)skeys[j].id;
-    const int i = svals[j];
-    const int row = wrap_all ? (int)w : (int)((header + w) % cap);
-    const float* src = emb + (long long)live[i] * H;
-    float* dst = table + (long long)row * H;
-    if ((H & 3) == 0) {
-      for (int v = lane; v < (H >> 2); v += 32)
-        reinterpret_cast<float4*>(dst)[v] = reinterpret_cast<const float4*>(src)[v];
-    } else {
-      for (int v = lane; v < H; v += 32) dst[v] = src[v];
-    }
-    if (lane == 0) {
+  const bool vec = (H & 3) == 0;
+  const int nv = H >> 2;
+  for (long long g = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; g < neff; g += warps * 32) {
+    const long long w = g + lane;
+    long long srow = 0, drow = 0;
+    if (w < neff) {
+      const int j = wlist[w0 + w];
+      const int id = (int)skeys[j].id;
+      const int row = wrap_all ? (int)w : (int)((header + w) % cap);
+      srow = live[svals[j]];
+      drow = row;
       row_owner[row] = id;
       row_of[id] = row;
       admit_iter[id] = it;
+    }
+    const int cnt = neff - g < 32 ? (int)(neff - g) : 32;
+    if (vec && nv <= 64) {
+      for (int q = 0; q < cnt; q += 4) {
+        float4 x[4][2];
+        long long d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int qq = q + u < cnt ? q + u : q;
+          const long long sr = __shfl_sync(0xffffffffu, srow, qq);
+          d[u] = __shfl_sync(0xffffffffu, drow, qq);
+          const float4* src = reinterpret_cast<const float4*>(emb + sr * H);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int v = lane + 32 * h;
+            if (v < nv && q + u < cnt) x[u][h] = src[v];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float4* dst = reinterpret_cast<float4*>(table + d[u] * H);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int v = lane + 32 * h;
+            if (v < nv && q + u < cnt) dst[v] = x[u][h];
+          }
+        }
+      }
+    } else {
+      for (int q = 0; q < cnt; ++q) {
+        const long long sr = __shfl_sync(0xffffffffu, srow, q);
+        const long long dr = __shfl_sync(0xffffffffu, drow, q);
+        const float* src = emb + sr * H;
+        float* dst = table + dr * H;
+        if (vec) {
+          for (int v = lane; v < nv; v += 32)
+            reinterpret_cast<float4*>(dst)[v] = reinterpret_cast<const float4*>(src)[v];
+        } else {
+          for (int v = lane; v < H; v += 32) dst[v] = src[v];
+        }
+      }
     }
   }
 }
@@ -644,8 +648,8 @@ using namespace hg;
 extern "C" {
 
 static long long bucket_tail_bytes(long long nn) {
-  // k2 (16 B), v2, arrival (4 B each), state, count + scount, off, mid, big
-  return nn * 24 + 64 + 4LL * (kNB + kNSuper + (kNB + 1) + 2 * kNB) + 64;
+  // k2 (16 B), v2, arrival (4 B each), state, count, loc, stot, spre, long list
+  return nn * 24 + 64 + 4LL * (3 * kNB + 2 * kNSuper) + 64;
 }
 
 long long hg_cache_update_scratch_bytes(long long n_max) {
@@ -685,10 +689,10 @@ RankBufs carve(void* scratch, long long scratch_bytes, long long n_max) {
   return b;
 }
 
-// U1: (norm bits, id) keys of the n live nodes sorted into keys_out /
-// vals_out by the bucket sort; *k_out = floor(p_grad * n)
+// U1 (+ U2 when A.ctr is set): (norm bits, id) keys of the n live nodes
+// sorted into keys_out / vals_out by the bucket sort; *k_out = floor(p_grad * n)
 int bucket_rank(const char* W, const int32_t* n_dev, int n_max, double p_grad, const int32_t* live,
-                const int32_t* src_nodes, const double* norms, long long* k_out, const RankBufs& rb,
+                const int32_t* src_nodes, const double* norms, long long* k_out, const RankBufs& rb, const Admit& A,
                 cudaStream_t stream) {
   const long long nn = n_max + 16;
   const size_t need = (size_t)bucket_tail_bytes(nn);
@@ -699,13 +703,13 @@ int bucket_rank(const char* W, const int32_t* n_dev, int n_max, double p_grad, c
   int* arrival = v2 + nn;
   BucketState* bst = reinterpret_cast<BucketState*>((reinterpret_cast<uintptr_t>(arrival + nn) + 15) & ~uintptr_t(15));
   int* count = reinterpret_cast<int*>(bst + 1);
-  int* scount = count + kNB;
-  int* off = scount + kNSuper;
-  int* mid = off + kNB + 1;
-  int* big = mid + kNB;
+  int* loc = count + kNB;
+  int* stot = loc + kNB;
+  int* spre = stot + kNSuper;
+  int* longl = spre + kNSuper;
   HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->lo, 0xFF, 8, stream));
-  // hi, n_big, n_mid, count, scount: one zero fill
-  HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->hi, 0x00, 16 + 4 * ((size_t)kNB + kNSuper), stream));
+  // hi, n_long, ticket, pad, count: one zero fill
+  HG_CHECK_CUDA(W, cudaMemsetAsync(&bst->hi, 0x00, 24 + 4 * (size_t)kNB, stream));
   const unsigned g = grid_for(n_max, 256, 148 * 4);
 #define HG_L(K, G, B, ...)                                                                   \
   {                                                                                          \
@@ -715,16 +719,14 @@ int bucket_rank(const char* W, const int32_t* n_dev, int n_max, double p_grad, c
   }
   // keys -> k2 / v2; bucketed -> keys_in / vals_in; sorted -> keys_out / vals_out
   HG_L(k_norm_keys, grid_for(n_max, 256), 256, n_dev, n_max, p_grad, live, src_nodes, norms, k2, v2, k_out, bst);
-  HG_L(k_bs_count, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, count, scount, arrival);
-  HG_L(k_bs_offsets, kNSuper, kSuperB, (const int*)count, (const int*)scount, off, mid, big, bst);
-  HG_L(k_bs_place, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, (const int*)off, (const int*)arrival,
-       rb.keys_in, rb.vals_in);
-  HG_L(k_bs_warp, 148 * 8, 256, (const int*)off, (const NormKey*)rb.keys_in, (const int32_t*)rb.vals_in,
-       rb.keys_out, rb.vals_out);
-  HG_L(k_bs_small, 148 * 2, 256, (const int*)off, (const int*)mid, (const BucketState*)bst,
-       (const NormKey*)rb.keys_in, (const int32_t*)rb.vals_in, rb.keys_out, rb.vals_out);
-  HG_L(k_bs_big, 64, 256, (const int*)off, (const int*)big, (const BucketState*)bst, rb.keys_in, rb.vals_in, k2, v2,
-       rb.keys_out, rb.vals_out);
+  HG_L(k_bs_count, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, count, arrival);
+  HG_L(k_bs_offsets, kNSuper, kSuperB, (const int*)count, loc, stot, spre, longl, bst);
+  HG_L(k_bs_place, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, (const int*)loc, (const int*)spre,
+       (const int*)arrival, rb.keys_in, rb.vals_in);
+  HG_L(k_bs_rank, g, 256, n_dev, (const BucketState*)bst, (const int*)count, (const int*)loc, (const int*)spre,
+       (const NormKey*)rb.keys_in, (const int32_t*)rb.vals_in, rb.keys_out, rb.vals_out, A);
+  HG_L(k_bs_long, 148, 256, (const int*)count, (const int*)loc, (const int*)spre, (const int*)longl,
+       (const BucketState*)bst, rb.keys_in, rb.vals_in, k2, v2, rb.keys_out, rb.vals_out, A);
 #undef HG_L
   return kOk;
 }
@@ -744,12 +746,9 @@ int hg_cache_rank(const int32_t* n_dev, int n_max, double p_grad, const int32_t*
   if (scratch_bytes < hg_cache_update_scratch_bytes(n_max)) return fail(W, kBadArg, "scratch too small");
   if (n_max <= 0) return kOk;
   const RankBufs rb = carve(scratch, scratch_bytes, n_max);
-  const int s = bucket_rank(W, n_dev, n_max, p_grad, live, src_nodes, norms, layer_ctr + kCtrK, rb, stream);
+  const Admit A{live, computed_flag, row_of, row_owner, rb.wflag, rb.retained, layer_ctr};
+  const int s = bucket_rank(W, n_dev, n_max, p_grad, live, src_nodes, norms, layer_ctr + kCtrK, rb, A, stream);
   if (s) return s;
-  HG_CHECK_CUDA(W, hg::launch_pdl(k_rank_admit, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev,
-                                  (const NormKey*)rb.keys_out, (const int32_t*)rb.vals_out, live, computed_flag,
-                                  row_of, row_owner, rb.wflag, rb.retained, layer_ctr));
-  HG_LAUNCHED(W);
   return scan_launch<int>(W, FlagU8{rb.wflag}, DevCount{n_dev}, n_max, rb.part, EmitCompact{rb.wlist},
                           StoreNWrite{layer_ctr}, stream);
 }
@@ -768,7 +767,7 @@ int hg_cache_request(const int32_t* n_dev, int n_max, double p_grad, const int32
   if (row_words < 4 || (row_words & 3)) return fail(W, kBadArg, "rows must be a multiple of 4 words");
   if (n_max <= 0) return kOk;
   const RankBufs rb = carve(scratch, scratch_bytes, n_max);
-  const int s = bucket_rank(W, n_dev, n_max, p_grad, live, src_nodes, norms, req_hdr + 1, rb, stream);
+  const int s = bucket_rank(W, n_dev, n_max, p_grad, live, src_nodes, norms, req_hdr + 1, rb, Admit{}, stream);
   if (s) return s;
   HG_CHECK_CUDA(W, hg::launch_pdl(k_request, dim3(grid_for((long long)n_max * 32, 256, 148 * 16)), dim3(256), 0,
                                   stream, n_dev, (const NormKey*)rb.keys_out, (const int32_t*)rb.vals_out, live,
@@ -799,7 +798,7 @@ int hg_cache_write(int n_max, int cap, int H, const int32_t* it_dev, double t_st
   { const cudaError_t _pe = hg::launch_pdl(k_ring_scan, dim3(grid_for(nmax, 256)), dim3(256), 0, stream, cap, it_dev, t_stale, t_inf, row_of, row_owner, admit_iter,
                                                        layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
-  { const cudaError_t _pe = hg::launch_pdl(k_write_rows, dim3(grid_for((long long)n_max * 32, 256, 148 * 16)), dim3(256), 0, stream, 
+  { const cudaError_t _pe = hg::launch_pdl(k_write_rows, dim3(grid_for((long long)n_max, 256, 148 * 16)), dim3(256), 0, stream, 
       wlist, keys_out, vals_out, live, emb, H, cap, it_dev, table, row_of, row_owner, admit_iter, layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   { const cudaError_t _pe = hg::launch_pdl(k_commit, dim3(1), dim3(1), 0, stream, cap, layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
