@@ -51,6 +51,18 @@ constexpr int kMaxRowFloats = 1056;
 #endif
 #ifndef HG_AGG_PIPE
 #define HG_AGG_PIPE 1
+#endif
+// matrix sources (layers >= 1): 8 edge rows in flight per warp at 4 CTAs / SM
+// (measured C2: 63 -> 56 us / step); the layer-0 in-place variant keeps 4
+// rows at 6 CTAs / SM (8 rows at 4 CTAs: 66 -> 89 us)
+#ifndef HG_AGG_EB
+#define HG_AGG_EB 4
+#endif
+#ifndef HG_AGG_EB0
+#define HG_AGG_EB0 8
+#endif
+#ifndef HG_AGG_MINB0
+#define HG_AGG_MINB0 4
 #endif // k_gather_dz staging: d_out <= 1056
 
 __device__ __forceinline__ float4 f4_fmadd_rn(float4 acc, float c, float4 x) {
@@ -92,7 +104,7 @@ __device__ __forceinline__ float4 row_vec(const void* base, int v) {
 #endif
 
 template <int kKind, int kT, int kSrc>
-__global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, kT <= 2 ? (kSrc ? HG_AGG_MINB : HG_AGG_MINB0) : 1) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
@@ -125,6 +137,7 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(co
   // measured (C2): the pipelined loop helps the layer-0 rows-in-place variant
   // (one more dependent hop per edge) and costs the matrix variant ~20 %
   constexpr bool kPipe = HG_AGG_PIPE && kSrc >= 1;
+  constexpr int kEB = kSrc ? HG_AGG_EB : HG_AGG_EB0;   // edges in flight per warp
   for (; i < R; i += warps) {
     const int i_next = i + warps;
     const int r_next = kPipe && i_next < R ? rows[i_next] : 0;
@@ -146,26 +159,26 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_AGG_MINB : 1) k_aggregate(co
     }
     const int dd = kKind == kKindGCN ? dst_deg[r] : 0;
     int e = e0;
-    for (; e + 4 <= e1; e += 4) {
-      int c[4];
-      float w[4];
-      const void* bp[4];
+    for (; e + kEB <= e1; e += kEB) {
+      int c[kEB];
+      float w[kEB];
+      const void* bp[kEB];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kEB; ++q) {
         c[q] = col[e + q];
         w[q] = kKind == kKindSAGE ? cs : gcn_coef(dd, src_deg[c[q]]);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) bp[q] = src_row<kSrc>(h_in, rowp, c[q], d);
+      for (int q = 0; q < kEB; ++q) bp[q] = src_row<kSrc>(h_in, rowp, c[q], d);
 #pragma unroll
       for (int t = 0; t < kT; ++t) {
         const int v = lane + 32 * t;
         if (v < nv) {
-          float4 x[4];
+          float4 x[kEB];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) x[q] = row_vec<kSrc>(bp[q], v);
+          for (int q = 0; q < kEB; ++q) x[q] = row_vec<kSrc>(bp[q], v);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[t] = f4_fmadd_rn(acc[t], w[q], x[q]);
+          for (int q = 0; q < kEB; ++q) acc[t] = f4_fmadd_rn(acc[t], w[q], x[q]);
         }
       }
     }
