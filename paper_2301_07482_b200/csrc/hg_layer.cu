@@ -49,6 +49,9 @@ constexpr int kMaxRowFloats = 1056;
 #ifndef HG_TAGG_MINB
 #define HG_TAGG_MINB 8
 #endif
+#ifndef HG_TAGG_EB
+#define HG_TAGG_EB 2
+#endif
 #ifndef HG_AGG_PIPE
 #define HG_AGG_PIPE 1
 #endif
@@ -427,6 +430,7 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_a
   const int nv = d >> 2;
   const int goff = kKind == kKindSAGE ? d : 0;  // neighbour half of [S | G]
   const int warps = (gridDim.x * blockDim.x) >> 5;
+  constexpr int kTEB = HG_TAGG_EB;
   KTimer* kt = g_kt ? g_kt + kTTransposeAgg : nullptr;
   kt_begin(kt);
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
@@ -436,7 +440,32 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_a
     for (int t = 0; t < kT; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int p0 = seg_lo[c], p1 = seg_hi[c];
     const int sd = kKind == kKindGCN ? src_deg[c] : 0;
-    for (int p = p0; p < p1; ++p) {
+    int p = p0;
+    if (kKind == kKindSAGE && HG_ROW_W && row_w) {
+      // kTEB edges per batch: their positions, weights and gradient rows are
+      // loaded before any is accumulated (same summation order as one by one)
+      for (; p + kTEB <= p1; p += kTEB) {
+        int pos[kTEB];
+        float w[kTEB];
+#pragma unroll
+        for (int q = 0; q < kTEB; ++q) pos[q] = (int)srt_vals[p + q];
+#pragma unroll
+        for (int q = 0; q < kTEB; ++q) w[q] = row_w[pos[q]];
+#pragma unroll
+        for (int t = 0; t < kT; ++t) {
+          const int v = lane + 32 * t;
+          if (v < nv) {
+            float4 x[kTEB];
+#pragma unroll
+            for (int q = 0; q < kTEB; ++q)
+              x[q] = reinterpret_cast<const float4*>(SG + (long long)pos[q] * ldSG + goff)[v];
+#pragma unroll
+            for (int q = 0; q < kTEB; ++q) acc[t] = f4_fmadd_rn(acc[t], w[q], x[q]);
+          }
+        }
+      }
+    }
+    for (; p < p1; ++p) {
       const int pos = (int)srt_vals[p];
       float w;
       if (kKind == kKindSAGE && HG_ROW_W && row_w) {
