@@ -220,13 +220,18 @@ int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t
 /* need_row (uint8 per source row, may be NULL): rows with 0 get their fp64
  * norm only, no gradient row (the next layer does not compute them);
  * row_w (SAGE, may be NULL): the per-compute-row mean weights 1/cnt written
- * by hg_aggregate_fwd[_rows] (row_w there, may be NULL) */
+ * by hg_aggregate_fwd[_rows] (row_w there, may be NULL);
+ * dz_ts (may be NULL): instead of d_in rows, write the previous layer's dz
+ * operand (hg_gather_dz fused): row pos_prev[c] = d_in[c] masked by
+ * h_prev[c] > 0 when relu_prev, TS layout for R_prev_max rows, padding rows
+ * of the last tile up to the device count *R_prev_dev zeroed */
 int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, const int32_t* live,
                      const int32_t* seg_lo, const int32_t* seg_hi, const unsigned* vals_sorted, const int32_t* rows,
                      const int32_t* start, const int32_t* end, const int32_t* dst_deg, const int32_t* src_deg,
                      const int32_t* n_dst_dev, const int32_t* pos_of, const float* SG, int ldSG, int d,
                      float* d_in, double* norms, const uint8_t* need_row, const float* row_w,
-                     cudaStream_t stream);
+                     void* dz_ts, const int32_t* R_prev_dev, long long R_prev_max, const int32_t* pos_prev,
+                     const float* h_prev, int relu_prev, cudaStream_t stream);
 int hg_row_norms(const float* x, long long n, int d, double* out, cudaStream_t stream);
 
 /* ---- K11 optimizer: nn.py:355-360 (sgd_step) */

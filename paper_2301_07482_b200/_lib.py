@@ -70,7 +70,8 @@ SIGNATURES = {
     "hg_gather_dz": (I32, [P, I64, P, P, P, I32, I32, P, P]),
     "hg_csc_scratch_bytes": (I64, [I64, I64]),
     "hg_build_csc": (I32, [P, P, P, P, P, I64, I64, P, P, P, P, P, I64, P]),
-    "hg_transpose_agg": (I32, [I32, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P, P, P]),
+    "hg_transpose_agg": (I32, [I32, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P, P,
+                               P, P, I64, P, P, I32, P]),
     "hg_row_norms": (I32, [P, I64, I32, P, P]),
     "hg_sgd": (I32, [P, P, I64, F32, P]),
     "hg_p2p_allreduce_sgd": (I32, [P, P, I64, P, P, P, P, I32, P, F32, P]),

@@ -415,6 +415,18 @@ __global__ void k_csc_place(const int32_t* n_dst_dev, const int32_t* __restrict_
 }
 
 // d_in rows for the live sources of block l + their fp64 norms (one warp per source)
+// the previous layer's dz operand written by the transposed aggregation
+// (ts null: d_in rows are written instead and k_gather_dz builds dz)
+struct DzOut {
+  uint8_t* ts;            // TS operand [R_pad x nK*32] (hg_ts.cuh)
+  long long plane;
+  int nK;
+  const int32_t* pos;     // compute position of each source in the previous layer (-1: none)
+  const float* h;         // the previous layer's output rows (ReLU mask)
+  int relu;
+  const int32_t* R_dev;   // the previous layer's compute-row count
+};
+
 template <int kKind, int kT>
 __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_agg(
     const int32_t* n_live_dev, const int32_t* __restrict__ live, const int32_t* __restrict__ seg_lo,
@@ -422,8 +434,9 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_a
     const int32_t* __restrict__ start, const int32_t* __restrict__ end, const int32_t* __restrict__ dst_deg,
     const int32_t* __restrict__ src_deg, const int32_t* n_dst_dev, const int32_t* __restrict__ pos_of,
     const float* __restrict__ SG, int ldSG, int d, float* __restrict__ d_in, double* __restrict__ norms,
-    const uint8_t* __restrict__ need_row, const float* __restrict__ row_w) {
+    const uint8_t* __restrict__ need_row, const float* __restrict__ row_w, DzOut dzo) {
   pdl_wait();
+  extern __shared__ __align__(16) float ta_smem[];
   const int n = *n_live_dev;
   const int n_dst = *n_dst_dev;
   const int lane = threadIdx.x & 31;
@@ -506,7 +519,7 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_a
     float4* out = reinterpret_cast<float4*>(d_in + (long long)c * d);
     // rows the next layer does not compute (cache-injected) need only their
     // norm (the admission key, cache.py:188-191), not the gradient row itself
-    const bool write = !need_row || need_row[c];
+    const bool write = !dzo.ts && (!need_row || need_row[c]);
 #pragma unroll
     for (int t = 0; t < kT; ++t) {
       const int v = lane + 32 * t;
@@ -516,8 +529,43 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_a
               (double)acc[t].w * acc[t].w;
       }
     }
+    if (dzo.ts) {
+      // the previous layer's dz row (k_gather_dz fused): ReLU-masked by its
+      // output, emitted as TS at its compute position
+      const int pn = dzo.pos[c];
+      if (pn >= 0) {
+        float* srow = ta_smem + (threadIdx.x >> 5) * (dzo.nK * 32);
+        const float4* hp = reinterpret_cast<const float4*>(dzo.h + (long long)c * d);
+#pragma unroll
+        for (int t = 0; t < kT; ++t) {
+          const int v = lane + 32 * t;
+          if (v < nv) {
+            float4 g = acc[t];
+            if (dzo.relu) {
+              const float4 h = hp[v];
+              g = make_float4(h.x > 0.f ? g.x : 0.f, h.y > 0.f ? g.y : 0.f, h.z > 0.f ? g.z : 0.f,
+                              h.w > 0.f ? g.w : 0.f);
+            }
+            reinterpret_cast<float4*>(srow)[v] = g;
+          }
+        }
+        for (int j = d + lane; j < dzo.nK * 32; j += 32) srow[j] = 0.f;
+        __syncwarp();
+        for (int g = lane; g < dzo.nK * 4; g += 32) ts_store8(dzo.ts, dzo.nK * 4, dzo.plane, pn, g, srow + g * 8);
+        __syncwarp();
+      }
+    }
     sq = warp_sum_fixed(sq);
     if (lane == 0) norms[i] = sqrt(sq);
+  }
+  if (dzo.ts) {
+    // zero the padding rows of dz's last 128-row tile (the weight-gradient
+    // GEMM reduces over rows)
+    const int R = *dzo.R_dev;
+    const int R_pad = (R + kTsRows - 1) / kTsRows * kTsRows;
+    const float zeros[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int r = R + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < R_pad; r += warps)
+      for (int g = lane; g < dzo.nK * 4; g += 32) ts_store8(dzo.ts, dzo.nK * 4, dzo.plane, r, g, zeros);
   }
   kt_end(kt);
 }
@@ -690,19 +738,28 @@ int hg_transpose_agg(int kind, const int32_t* n_live_dev, long long n_live_max, 
                      const int32_t* start, const int32_t* end, const int32_t* dst_deg, const int32_t* src_deg,
                      const int32_t* n_dst_dev, const int32_t* pos_of, const float* SG, int ldSG, int d,
                      float* d_in, double* norms, const uint8_t* need_row, const float* row_w,
-                     cudaStream_t stream) {
+                     void* dz_ts, const int32_t* R_prev_dev, long long R_prev_max, const int32_t* pos_prev,
+                     const float* h_prev, int relu_prev, cudaStream_t stream) {
   const char* W = "hg_transpose_agg";
   if (d % 4 || d > 32 * 4 * kMaxVecPerLane) return fail(W, kBadArg, "d must be a multiple of 4 and <= 1024");
+  if (dz_ts && (!R_prev_dev || !pos_prev || !h_prev)) return fail(W, kBadArg, "dz output needs R, pos and h");
   const unsigned grid = grid_for(n_live_max * 32, 256, 148 * 16);
   const int vpl = (d / 4 + 31) / 32;
+  DzOut dzo{static_cast<uint8_t*>(dz_ts), dz_ts ? ts_plane_bytes(R_prev_max, d) : 0, (d + 31) / 32, pos_prev,
+            h_prev, relu_prev, R_prev_dev};
+  const size_t smem = dz_ts ? (size_t)8 * dzo.nK * 32 * 4 : 0;
   cudaError_t pe = cudaSuccess;
 #define HG_TA(KIND, T)                                                                                            \
-  pe = hg::launch_pdl(k_transpose_agg<KIND, T>, dim3(grid), dim3(256), 0, stream, n_live_dev, live, seg_lo, seg_hi,  \
-                      vals_sorted, rows, start, end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d, d_in, norms, \
-                      need_row, row_w)
+  {                                                                                                              \
+    const int sa = ensure_smem_attr((const void*)k_transpose_agg<KIND, T>, (int)smem, W);                      \
+    if (sa) return sa;                                                                                           \
+    pe = hg::launch_pdl(k_transpose_agg<KIND, T>, dim3(grid), dim3(256), smem, stream, n_live_dev, live, seg_lo,  \
+                        seg_hi, vals_sorted, rows, start, end, dst_deg, src_deg, n_dst_dev, pos_of, SG, ldSG, d,  \
+                        d_in, norms, need_row, row_w, dzo);                                                      \
+  }
 #define HG_TA_T(KIND)                                                                                             \
-  if (vpl <= 1) HG_TA(KIND, 1); else if (vpl <= 2) HG_TA(KIND, 2); else if (vpl <= 4) HG_TA(KIND, 4);           \
-  else HG_TA(KIND, 8);
+  if (vpl <= 1) HG_TA(KIND, 1) else if (vpl <= 2) HG_TA(KIND, 2) else if (vpl <= 4) HG_TA(KIND, 4)              \
+  else HG_TA(KIND, 8)
   if (kind == kKindSAGE) {
     HG_TA_T(kKindSAGE)
   } else {

@@ -76,6 +76,8 @@ class DevBlock:
 # HG_NODE_PRIO=1: streams get priorities (cache updates > training > lookahead
 # sampler) and the captured step is instantiated with per-node priorities
 _NODE_PRIO = os.environ.get("HG_NODE_PRIO") == "1"
+# HG_FUSED_DZ=0: d_in rows + a separate dz gather per layer (A/B)
+_FUSED_DZ = os.environ.get("HG_FUSED_DZ", "1") != "0"
 
 
 class _Graph:
@@ -432,7 +434,8 @@ class StepEngine:
             d_prev, nrm = layer_backward_dev(net, l, blk, tapes[l], d_h, grads, l >= 1, keep[l], pos[l], live[l],
                                              blk.num_src, sp, blk.n_dst_dev, n_live_dev(l), csc=cscs[l],
                                              W_ts=w_ts[l], wgrad_stream=self.wgrad_stream, keepalive=keepalive,
-                                             need_rows=keep[l - 1] if l >= 1 else None)
+                                             need_rows=keep[l - 1] if l >= 1 else None,
+                                             dz_prev=(tapes[l - 1], pos[l - 1]) if l >= 1 and _FUSED_DZ else None)
             norms[l] = nrm
             d_h = d_prev
             self._mark(f"backward{l}", stream)

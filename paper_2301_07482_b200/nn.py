@@ -649,9 +649,14 @@ def pack_dgrad_weights(net: Network, l: int, stream) -> torch.Tensor:
 def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tensor, grads: Grads,
                        need_input: bool, keep, pos_of, live, n_live, stream, n_dst_dev=None, n_live_dev=None,
                        csc: BlockCsc | None = None, W_ts: torch.Tensor | None = None, wgrad_stream=None,
-                       keepalive: list | None = None, need_rows=None):
+                       keepalive: list | None = None, need_rows=None, dz_prev=None, dz=None):
     """Writes dP into grads; returns (d_in [n_src, d_in] with rows valid on
     `live`, fp64 norms aligned with `live`) or (None, None).
+
+    `dz_prev` = (tape, pos_of) of layer l-1: instead of d_in, the transposed
+    aggregation writes that layer's ReLU-masked dz operand directly (its
+    hg_gather_dz fused away) and returns it as `DzOperand` in place of d_in;
+    `dz`: this layer's dz operand, already built that way by layer l+1.
 
     Engine options: `csc` / `W_ts` prebuilt off the critical path (they
     depend only on the pruned block / the weights), and `wgrad_stream`: the
@@ -663,13 +668,18 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
     if net.kind is LayerKind.GAT:
         return gat_layer_backward_dev(net, l, blk, t, d_h, grads, need_input, keep, pos_of, stream, n_dst_dev,
                                       csc, wgrad_stream, keepalive)
-    dev = d_h.device
+    dev = t.h_out.device
     d_in_dim, d_out = net.dims[l], net.dims[l + 1]
     R, K = t.R, t.K
-    # dz (ReLU-masked output gradient of the compute rows) as a TS operand
-    dz = torch.empty(ts_bytes(R, d_out), dtype=torch.uint8, device=dev)
-    _lib.call("hg_gather_dz", _lib.ptr(t.R_dev), R, _lib.ptr(t.rows), _lib.ptr(d_h), _lib.ptr(t.h_out), d_out,
-              int(t.relu), _lib.ptr(dz), stream)
+    if isinstance(d_h, DzOperand):
+        dz = d_h
+    if isinstance(dz, DzOperand):
+        dz = dz.ts
+    else:
+        # dz (ReLU-masked output gradient of the compute rows) as a TS operand
+        dz = torch.empty(ts_bytes(R, d_out), dtype=torch.uint8, device=dev)
+        _lib.call("hg_gather_dz", _lib.ptr(t.R_dev), R, _lib.ptr(t.rows), _lib.ptr(d_h), _lib.ptr(t.h_out), d_out,
+                  int(t.relu), _lib.ptr(dz), stream)
     dP = grads.slab(l)
     splits = _wgrad_splits(R, K + 1, d_out)
 
@@ -700,14 +710,29 @@ def layer_backward_dev(net: Network, l: int, blk, t: LayerTape, d_h: torch.Tenso
         n_live_dev = _dev_count(n_live, dev)
     if csc is None:
         csc = build_csc(blk, keep, pos_of, n_dst_dev, stream)
-    d_in = torch.empty((blk.num_src, d_in_dim), dtype=torch.float32, device=dev)
     norms = torch.empty(max(n_live, 1), dtype=torch.float64, device=dev)
+    if dz_prev is not None:
+        tp, pos_prev = dz_prev
+        d_in = None
+        dzp = DzOperand(torch.empty(ts_bytes(tp.R, d_in_dim), dtype=torch.uint8, device=dev))
+        dz_args = (_lib.ptr(dzp.ts), _lib.ptr(tp.R_dev), tp.R, _lib.ptr(pos_prev), _lib.ptr(tp.h_out), int(tp.relu))
+    else:
+        d_in = torch.empty((blk.num_src, d_in_dim), dtype=torch.float32, device=dev)
+        dzp = None
+        dz_args = (None, None, 0, None, None, 0)
     _lib.call("hg_transpose_agg", _kind_code(net.kind), _lib.ptr(n_live_dev), n_live, _lib.ptr(live),
               _lib.ptr(csc.seg_lo), _lib.ptr(csc.seg_hi), _lib.ptr(csc.vals), _lib.ptr(t.rows),
               _lib.ptr(blk.adj.start), _lib.ptr(blk.adj.end), _lib.ptr(blk.dst_deg), _lib.ptr(blk.src_deg),
               _lib.ptr(n_dst_dev), _lib.ptr(pos_of), _lib.ptr(SG), K, d_in_dim, _lib.ptr(d_in), _lib.ptr(norms),
-              _lib.ptr(need_rows), _lib.ptr(t.row_w), stream)
-    return d_in, norms[:n_live]
+              _lib.ptr(need_rows), _lib.ptr(t.row_w), *dz_args, stream)
+    return (dzp if dzp is not None else d_in), norms[:n_live]
+
+
+@dataclass
+class DzOperand:
+    """A layer's dz operand (TS bytes) built by the next layer's transposed
+    aggregation (hg_transpose_agg with dz output)."""
+    ts: torch.Tensor
 
 
 def _keep_pos(rows: torch.Tensor, R: int, n_dst: int, dev):
