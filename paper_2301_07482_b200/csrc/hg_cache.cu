@@ -505,10 +505,11 @@ __global__ void k_ring_scan(int cap, const int32_t* it_dev, double t_stale, int 
   }
 }
 
-// a warp takes 32 consecutive write slots: the lanes resolve their slot's
-// node, source row and ring row at once (and set the ownership maps), then
-// the warp copies the rows four at a time with 16-byte vectors (rows of up to
-// 256 floats held in registers, so 8 loads per lane are in flight)
+// a warp takes kWSlots consecutive write slots: lanes < kWSlots resolve their
+// slot's node, source row and ring row (and set the ownership maps), then the
+// warp copies the rows at once, lane group q (32 / kWSlots lanes) on row q
+// with 16-byte vectors (all of a warp's rows in flight; many warps per SM)
+constexpr int kWSlots = 4;
 __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* __restrict__ skeys,
                              const int32_t* __restrict__ svals, const int32_t* __restrict__ live,
                              const float* __restrict__ emb, int H, int cap, const int32_t* it_dev,
@@ -527,10 +528,13 @@ __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* _
   const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
   const bool vec = (H & 3) == 0;
   const int nv = H >> 2;
-  for (long long g = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; g < neff; g += warps * 32) {
-    const long long w = g + lane;
-    long long srow = 0, drow = 0;
-    if (w < neff) {
+  constexpr int kGL = 32 / kWSlots;   // lanes per row
+  const int q = lane / kGL, gl = lane % kGL;
+  for (long long g = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kWSlots; g < neff;
+       g += warps * kWSlots) {
+    long long srow = -1, drow = 0;
+    if (lane < kWSlots && g + lane < neff) {
+      const long long w = g + lane;
       const int j = wlist[w0 + w];
       const int id = (int)skeys[j].id;
       const int row = wrap_all ? (int)w : (int)((header + w) % cap);
@@ -540,46 +544,27 @@ __global__ void k_write_rows(const int32_t* __restrict__ wlist, const NormKey* _
       row_of[id] = row;
       admit_iter[id] = it;
     }
-    const int cnt = neff - g < 32 ? (int)(neff - g) : 32;
-    if (vec && nv <= 64) {
-      for (int q = 0; q < cnt; q += 4) {
-        float4 x[4][2];
-        long long d[4];
+    const long long sr = __shfl_sync(0xffffffffu, srow, q);
+    const long long dr = __shfl_sync(0xffffffffu, drow, q);
+    if (sr < 0) continue;
+    const float* src = emb + sr * H;
+    float* dst = table + dr * H;
+    if (vec && nv <= 8 * kGL) {
+      float4 x[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int qq = q + u < cnt ? q + u : q;
-          const long long sr = __shfl_sync(0xffffffffu, srow, qq);
-          d[u] = __shfl_sync(0xffffffffu, drow, qq);
-          const float4* src = reinterpret_cast<const float4*>(emb + sr * H);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int v = lane + 32 * h;
-            if (v < nv && q + u < cnt) x[u][h] = src[v];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          float4* dst = reinterpret_cast<float4*>(table + d[u] * H);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int v = lane + 32 * h;
-            if (v < nv && q + u < cnt) dst[v] = x[u][h];
-          }
-        }
+      for (int u = 0; u < 8; ++u) {
+        const int v = gl + kGL * u;
+        if (v < nv) x[u] = reinterpret_cast<const float4*>(src)[v];
       }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = gl + kGL * u;
+        if (v < nv) reinterpret_cast<float4*>(dst)[v] = x[u];
+      }
+    } else if (vec) {
+      for (int v = gl; v < nv; v += kGL) reinterpret_cast<float4*>(dst)[v] = reinterpret_cast<const float4*>(src)[v];
     } else {
-      for (int q = 0; q < cnt; ++q) {
-        const long long sr = __shfl_sync(0xffffffffu, srow, q);
-        const long long dr = __shfl_sync(0xffffffffu, drow, q);
-        const float* src = emb + sr * H;
-        float* dst = table + dr * H;
-        if (vec) {
-          for (int v = lane; v < nv; v += 32)
-            reinterpret_cast<float4*>(dst)[v] = reinterpret_cast<const float4*>(src)[v];
-        } else {
-          for (int v = lane; v < H; v += 32) dst[v] = src[v];
-        }
-      }
+      for (int v = gl; v < H; v += kGL) dst[v] = src[v];
     }
   }
 }
@@ -798,7 +783,7 @@ int hg_cache_write(int n_max, int cap, int H, const int32_t* it_dev, double t_st
   { const cudaError_t _pe = hg::launch_pdl(k_ring_scan, dim3(grid_for(nmax, 256)), dim3(256), 0, stream, cap, it_dev, t_stale, t_inf, row_of, row_owner, admit_iter,
                                                        layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
-  { const cudaError_t _pe = hg::launch_pdl(k_write_rows, dim3(grid_for((long long)n_max, 256, 148 * 16)), dim3(256), 0, stream, 
+  { const cudaError_t _pe = hg::launch_pdl(k_write_rows, dim3(grid_for((long long)n_max * 8, 256, 148 * 16)), dim3(256), 0, stream, 
       wlist, keys_out, vals_out, live, emb, H, cap, it_dev, table, row_of, row_owner, admit_iter, layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED(W);
   { const cudaError_t _pe = hg::launch_pdl(k_commit, dim3(1), dim3(1), 0, stream, cap, layer_ctr); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }

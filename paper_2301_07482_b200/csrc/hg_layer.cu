@@ -245,43 +245,40 @@ __global__ void k_scatter_rows(const int32_t* R_dev, const int32_t* __restrict__
 __global__ void k_inject(const int32_t* n_dev, const uint8_t* __restrict__ flag, const int32_t* __restrict__ hit_row,
                          const float* __restrict__ table, int dim, float* __restrict__ h_out) {
   pdl_wait();
-  // a warp takes 32 rows at once (flags / cache rows read lane-parallel), then
-  // copies the injected ones with 128-bit accesses, two rows in flight
+  // a warp takes 4 rows: lanes < 4 read their flag / cache row, then lane
+  // group q (8 lanes) copies row q if it is injected, 16-byte vectors, all
+  // four rows in flight
+  constexpr int kRows = 4, kGL = 32 / kRows;
   const int n = *n_dev;
   const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int q = lane / kGL, gl = lane % kGL;
+  const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
   const bool vec = (dim & 3) == 0;
-  const int nv = vec ? dim >> 2 : dim;
-  for (int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < n; r0 += warps * 32) {
-    const int r = r0 + lane;
-    const bool f = r < n && flag[r];
-    const int hr = f ? hit_row[r] : 0;
-    unsigned m = __ballot_sync(0xffffffffu, f);
-    while (m) {
-      const int q0 = __ffs(m) - 1;
-      m &= m - 1;
-      const int q1 = m ? __ffs(m) - 1 : -1;
-      if (q1 >= 0) m &= m - 1;
-      const int h0 = __shfl_sync(0xffffffffu, hr, q0);
-      const int h1 = __shfl_sync(0xffffffffu, hr, q1 < 0 ? q0 : q1);
-      if (vec) {
-        const float4* s0 = reinterpret_cast<const float4*>(table + (long long)h0 * dim);
-        const float4* s1 = reinterpret_cast<const float4*>(table + (long long)h1 * dim);
-        float4* d0 = reinterpret_cast<float4*>(h_out + (long long)(r0 + q0) * dim);
-        float4* d1 = reinterpret_cast<float4*>(h_out + (long long)(r0 + (q1 < 0 ? q0 : q1)) * dim);
-        for (int j = lane; j < nv; j += 32) {
-          const float4 a = s0[j];
-          float4 b;
-          if (q1 >= 0) b = s1[j];
-          d0[j] = a;
-          if (q1 >= 0) d1[j] = b;
-        }
-      } else {
-        for (int j = lane; j < nv; j += 32) {
-          h_out[(long long)(r0 + q0) * dim + j] = table[(long long)h0 * dim + j];
-          if (q1 >= 0) h_out[(long long)(r0 + q1) * dim + j] = table[(long long)h1 * dim + j];
-        }
+  const int nv = dim >> 2;
+  for (long long r0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRows; r0 < n;
+       r0 += warps * kRows) {
+    int hr = -1;
+    if (lane < kRows && r0 + lane < n && flag[r0 + lane]) hr = hit_row[r0 + lane];
+    const int h = __shfl_sync(0xffffffffu, hr, q);
+    if (h < 0) continue;
+    const float* src = table + (long long)h * dim;
+    float* dst = h_out + (r0 + q) * dim;
+    if (vec && nv <= 8 * kGL) {
+      float4 x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = gl + kGL * u;
+        if (v < nv) x[u] = reinterpret_cast<const float4*>(src)[v];
       }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = gl + kGL * u;
+        if (v < nv) reinterpret_cast<float4*>(dst)[v] = x[u];
+      }
+    } else if (vec) {
+      for (int v = gl; v < nv; v += kGL) reinterpret_cast<float4*>(dst)[v] = reinterpret_cast<const float4*>(src)[v];
+    } else {
+      for (int v = gl; v < dim; v += kGL) dst[v] = src[v];
     }
   }
 }
@@ -668,7 +665,7 @@ int hg_scatter_rows(const int32_t* R_dev, long long R_max, const int32_t* rows, 
 
 int hg_inject_rows(const int32_t* n_dev, long long n_max, const uint8_t* flag, const int32_t* hit_row,
                    const float* table, int dim, float* h_out, cudaStream_t stream) {
-  { const cudaError_t _pe = hg::launch_pdl(k_inject, dim3(grid_for(n_max * 32, 256, 148 * 16)), dim3(256), 0, stream, n_dev, flag, hit_row, table, dim, h_out); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  { const cudaError_t _pe = hg::launch_pdl(k_inject, dim3(grid_for(n_max * 8, 256, 148 * 16)), dim3(256), 0, stream, n_dev, flag, hit_row, table, dim, h_out); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_inject_rows");
   return kOk;
 }
