@@ -170,16 +170,26 @@ __global__ void __launch_bounds__(256, kT <= 8 ? HG_GAT_FWD_MINB : 1) k_gat_aggr
     float acc[kT];
 #pragma unroll
     for (int t = 0; t < kT; ++t) acc[t] = 0.f;
+    // software-pipelined: the next edge's source id is fetched while this
+    // edge's z row is accumulated (same order)
+    int j_n = e0 < e1 ? col[e0] : i;
     for (int e = e0; e <= e1; ++e) {
-      const int j = e < e1 ? col[e] : i;
+      const int j = j_n;
+      if (e + 1 <= e1) j_n = e + 1 < e1 ? col[e + 1] : i;
+      const float* zj = z + (long long)j * HF;
+      float zv[kT];
+#pragma unroll
+      for (int t = 0; t < kT; ++t) {
+        const int c = lane + 32 * t;
+        zv[t] = c < HF ? zj[c] : 0.f;
+      }
       const float w = lane < H ? expf(leaky(el[(long long)j * H + lane] + eri) - m) : 0.f;
       s += w;
-      const float* zj = z + (long long)j * HF;
 #pragma unroll
       for (int t = 0; t < kT; ++t) {
         const int c = lane + 32 * t;
         const float wh = head_val(w, c < HF ? Heads<kT, kH>::of(t, c, F) : 0);
-        if (c < HF) acc[t] = __fmaf_rn(wh, zj[c], acc[t]);
+        if (c < HF) acc[t] = __fmaf_rn(wh, zv[t], acc[t]);
       }
     }
     float* out = h_out + (long long)i * HF;
@@ -263,6 +273,7 @@ __global__ void __launch_bounds__(256, kT <= 8 ? HG_GAT_MINB : 1) k_gat_bwd_dst(
     // shared memory for the second pass instead of recomputing it
     const bool cached = e1 - e0 + 1 <= 32;
     for (int pass = 0; pass < 2; ++pass) {
+      int j_n = e0 < e1 ? col[e0] : i;    // next edge's source, fetched one edge ahead
       for (int e = e0; e <= e1; ++e) {
         const int ei = e - e0;
         if (pass == 1 && cached) {
@@ -272,7 +283,8 @@ __global__ void __launch_bounds__(256, kT <= 8 ? HG_GAT_MINB : 1) k_gat_bwd_dst(
           }
           continue;
         }
-        const int j = e < e1 ? col[e] : i;
+        const int j = j_n;
+        if (e + 1 <= e1) j_n = e + 1 < e1 ? col[e + 1] : i;
         const float* zj = z + (long long)j * HF;
         using HM = Heads<kT, kH>;
         float p[HM::N];
@@ -360,13 +372,26 @@ __global__ void __launch_bounds__(256, kT <= 8 ? HG_GAT_MINB : 1) k_gat_bwd_src(
     float dl = 0.f;
     const int self = j < n_dst ? pos_of[j] : -1;
     const int p0 = seg_lo[j], p1 = seg_hi[j];
-    // CSC edges (ascending dst row), then the self loop
-    for (int p = p0; p <= p1; ++p) {
-      int pos;
-      if (p < p1) pos = (int)csc_pos[p];
-      else if (self >= 0) pos = self;
-      else break;
-      const int i = rows[pos];
+    // CSC edges (ascending dst row), then the self loop. Software-pipelined:
+    // the next edge's position, dst row and per-head terms are fetched while
+    // the current edge's gradient row is reduced (same summation order)
+    const int p_end = self >= 0 ? p1 + 1 : p1;
+    auto edge_pos = [&](int p) { return p < p1 ? (int)csc_pos[p] : self; };
+    int pos_n = p0 < p_end ? edge_pos(p0) : 0;
+    int i_n = p0 < p_end ? rows[pos_n] : 0;
+    for (int p = p0; p < p_end; ++p) {
+      const int pos = pos_n, i = i_n;
+      float er_i = 0.f, mx_p = 0.f, ss_p = 1.f, cc_p = 0.f;
+      if (lane < H) {
+        er_i = er[(long long)i * H + lane];
+        mx_p = mx[(long long)pos * H + lane];
+        ss_p = ssum[(long long)pos * H + lane];
+        cc_p = cc[(long long)pos * H + lane];
+      }
+      if (p + 1 < p_end) {
+        pos_n = edge_pos(p + 1);
+        i_n = rows[pos_n];
+      }
       const float* gi = gz + (long long)pos * HF;
       using HM = Heads<kT, kH>;
       float gv[kT];
@@ -377,14 +402,18 @@ __global__ void __launch_bounds__(256, kT <= 8 ? HG_GAT_MINB : 1) k_gat_bwd_src(
       for (int t = 0; t < kT; ++t) {
         const int c = lane + 32 * t;
         gv[t] = c < HF ? gi[c] : 0.f;
+      }
+#pragma unroll
+      for (int t = 0; t < kT; ++t) {
+        const int c = lane + 32 * t;
         if (c < HF) HM::add(q8, t, c, F, gv[t] * zr[t]);
       }
       const float da = HM::sum_to_lanes(q8, lane);
       float a = 0.f;
       if (lane < H) {
-        const float pre = elj + er[(long long)i * H + lane];
-        a = expf(leaky(pre) - mx[(long long)pos * H + lane]) / ssum[(long long)pos * H + lane];
-        dl += a * (da - cc[(long long)pos * H + lane]) * leaky_d(pre);
+        const float pre = elj + er_i;
+        a = expf(leaky(pre) - mx_p) / ss_p;
+        dl += a * (da - cc_p) * leaky_d(pre);
       }
 #pragma unroll
       for (int t = 0; t < kT; ++t) {
