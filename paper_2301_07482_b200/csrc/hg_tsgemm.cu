@@ -235,8 +235,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tsgemm(const __grid_constant__ 
   const int n0 = blockIdx.y * N_pad;
   const int n_valid = min(N_pad, sh.N - n0);
   const int chunks = (K + kBK - 1) / kBK;
-  const int c_begin = blockIdx.z * sh.chunks_per_split;
-  const int c_end = min(chunks, c_begin + sh.chunks_per_split);
+  // split-K (weight gradient): the device count of reduction rows is shared
+  // evenly by the splits (the host's upper bound would leave the trailing
+  // splits idle and the others each a bound-sized share)
+  const int per = kMN && sh.K_dev ? (chunks + (int)gridDim.z - 1) / (int)gridDim.z : sh.chunks_per_split;
+  const int c_begin = blockIdx.z * per;
+  const int c_end = min(chunks, c_begin + per);
   const int nc = c_end > c_begin ? c_end - c_begin : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t a_half = 8192;                     // 128 x 32 bf16
