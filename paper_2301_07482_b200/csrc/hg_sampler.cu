@@ -883,12 +883,14 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
                        (const int64_t*)cand_off, lane_max, P);
     if (e != cudaSuccess) return fail("launch", kCuda, cudaGetErrorString(e));
     HG_LAUNCHED(W);
-    // persistent: 4 CTAs (32 warps) per SM pulling work items; HG_SEL_BLOCKS
-    // caps the grid (the sampler runs beside the training stream)
+    // persistent: 3 CTAs (24 warps) per SM pulling work items -- the
+    // selection's CTAs hold their slots until the queue drains, and the
+    // forward runs beside them (C2: 444 CTAs 1.533 / 1.540e6 seeds/s vs
+    // 592: 1.521e6, 296: 1.531e6, 148: 1.458e6); HG_SEL_BLOCKS overrides
     static const long long sel_cap = [] {
       const char* v = std::getenv("HG_SEL_BLOCKS");
-      const long long x = v ? std::atoll(v) : 148 * 4;
-      return x < 1 ? 148ll * 4 : x;
+      const long long x = v ? std::atoll(v) : 148 * 3;
+      return x < 1 ? 148ll * 3 : x;
     }();
     const int fk = lane_max == 0 ? 0 : fanout <= 2 ? 2 : fanout <= 4 ? 4 : fanout <= 5 ? 5 : fanout <= 6 ? 6
                  : fanout <= 8 ? 8 : fanout <= 10 ? 10 : fanout <= 12 ? 12 : fanout <= 15 ? 15 : 16;
