@@ -44,9 +44,9 @@ struct NormKey {
 //   k_bs_place    keys to their bucket slots (offset + arrival rank)
 //   k_bs_rank     one thread per key of a bucket of <= kShortMax keys: its
 //                 final position = bucket offset + the number of the bucket's
-//                 keys below it (exact because keys are distinct)
-//   k_bs_long     one CTA per longer bucket: bitonic sort in shared memory up
-//                 to kBucketCap keys, chunk sorts + merge passes above
+//                 keys below it (exact because keys are distinct); then one
+//                 CTA per longer bucket: bitonic sort in shared memory up to
+//                 kBucketCap keys, chunk sorts + merge passes above
 // The writers of the sorted positions also apply U2 (admission / gradient
 // eviction flags) when an Admit is given, so no separate pass reads the
 // sorted keys back. 64K buckets: the C2 layer-1 norms (~130K over 2.4
@@ -205,38 +205,6 @@ __global__ void k_bs_place(const int32_t* n_dev, const NormKey* __restrict__ key
   }
 }
 
-// one thread per key of a short bucket (<= kShortMax keys)
-__global__ void __launch_bounds__(256) k_bs_rank(const int32_t* n_dev, const BucketState* st,
-                                                 const int* __restrict__ count, const int* __restrict__ loc,
-                                                 const int* __restrict__ spre, const NormKey* __restrict__ tkeys,
-                                                 const int32_t* __restrict__ tvals, NormKey* __restrict__ okeys,
-                                                 int32_t* __restrict__ ovals, Admit A) {
-  pdl_wait();
-  const int n = *n_dev;
-  const unsigned long long lo = st->lo;
-  const int shift = bucket_shift(lo, st->hi);
-  const long long k = A.ctr ? A.ctr[kCtrK] : 0;
-  int evicted = 0;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    const NormKey key = tkeys[p];
-    const int b = bucket_of(key.norm, lo, shift);
-    const int c = count[b];
-    if (c > kShortMax) continue;
-    const int o = bucket_off(loc, spre, b);
-    int r = 0;
-    for (int q = 0; q < c; ++q) {
-      const NormKey x = tkeys[o + q];
-      r += key_less(x.norm, x.id, key.norm, key.id);
-    }
-    const int j = o + r;
-    const int i = tvals[p];
-    okeys[j] = key;
-    ovals[j] = i;
-    if (A.ctr) evicted += admit_pos(A, k, j, key.id, i);
-  }
-  admit_flush(A, evicted);
-}
-
 // in-smem bitonic sort of m (power of 2) (norm, id, val) items
 __device__ __forceinline__ void smem_bitonic(unsigned long long* sn, unsigned* si, int* sv, int m) {
   for (int size = 2; size <= m; size <<= 1) {
@@ -273,19 +241,17 @@ __device__ __forceinline__ int merge_split(const NormKey* A, int na, const NormK
 // one CTA per listed bucket of > kShortMax keys: up to kBucketCap keys one
 // shared-memory bitonic sort; above, sorted chunks of kBucketCap and
 // bottom-up merge passes ping-ponging between tkeys/tvals and k2/v2
-__global__ void __launch_bounds__(256) k_bs_long(const int* __restrict__ count, const int* __restrict__ loc,
-                                                 const int* __restrict__ spre, const int* __restrict__ longl,
-                                                 const BucketState* st, NormKey* __restrict__ tkeys,
-                                                 int32_t* __restrict__ tvals, NormKey* __restrict__ k2,
-                                                 int32_t* __restrict__ v2, NormKey* __restrict__ okeys,
-                                                 int32_t* __restrict__ ovals, Admit A) {
-  pdl_wait();
+__device__ __forceinline__ void sort_long_buckets(const int* __restrict__ count, const int* __restrict__ loc,
+                                                  const int* __restrict__ spre, const int* __restrict__ longl,
+                                                  const BucketState* st, NormKey* __restrict__ tkeys,
+                                                  int32_t* __restrict__ tvals, NormKey* __restrict__ k2,
+                                                  int32_t* __restrict__ v2, NormKey* __restrict__ okeys,
+                                                  int32_t* __restrict__ ovals, const Admit& A, long long k,
+                                                  int& evicted) {
   __shared__ unsigned long long sn[kBucketCap];
   __shared__ unsigned si[kBucketCap];
   __shared__ int sv[kBucketCap];
   const int nlong = st->n_long;
-  const long long k = A.ctr ? A.ctr[kCtrK] : 0;
-  int evicted = 0;
   for (int q = blockIdx.x; q < nlong; q += gridDim.x) {
     const int b = longl[q];
     const int o = bucket_off(loc, spre, b), cnt = count[b];
@@ -362,6 +328,42 @@ __global__ void __launch_bounds__(256) k_bs_long(const int* __restrict__ count, 
     }
     __syncthreads();
   }
+}
+
+// one thread per key of a short bucket (<= kShortMax keys): its position is
+// the bucket offset + the number of the bucket's keys below it; then the
+// CTAs take the listed longer buckets one each (sort_long_buckets)
+__global__ void __launch_bounds__(256) k_bs_rank(const int32_t* n_dev, const BucketState* st,
+                                                 const int* __restrict__ count, const int* __restrict__ loc,
+                                                 const int* __restrict__ spre, const int* __restrict__ longl,
+                                                 NormKey* __restrict__ tkeys, int32_t* __restrict__ tvals,
+                                                 NormKey* __restrict__ k2, int32_t* __restrict__ v2,
+                                                 NormKey* __restrict__ okeys, int32_t* __restrict__ ovals, Admit A) {
+  pdl_wait();
+  const int n = *n_dev;
+  const unsigned long long lo = st->lo;
+  const int shift = bucket_shift(lo, st->hi);
+  const long long k = A.ctr ? A.ctr[kCtrK] : 0;
+  int evicted = 0;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const NormKey key = tkeys[p];
+    const int b = bucket_of(key.norm, lo, shift);
+    const int c = count[b];
+    if (c > kShortMax) continue;
+    const int o = bucket_off(loc, spre, b);
+    int r = 0;
+#pragma unroll 4
+    for (int q = 0; q < c; ++q) {
+      const NormKey x = tkeys[o + q];
+      r += key_less(x.norm, x.id, key.norm, key.id);
+    }
+    const int j = o + r;
+    const int i = tvals[p];
+    okeys[j] = key;
+    ovals[j] = i;
+    if (A.ctr) evicted += admit_pos(A, k, j, key.id, i);
+  }
+  sort_long_buckets(count, loc, spre, longl, st, tkeys, tvals, k2, v2, okeys, ovals, A, k, evicted);
   admit_flush(A, evicted);
 }
 
@@ -709,9 +711,7 @@ int bucket_rank(const char* W, const int32_t* n_dev, int n_max, double p_grad, c
   HG_L(k_bs_place, g, 256, n_dev, (const NormKey*)k2, (const BucketState*)bst, (const int*)loc, (const int*)spre,
        (const int*)arrival, rb.keys_in, rb.vals_in);
   HG_L(k_bs_rank, g, 256, n_dev, (const BucketState*)bst, (const int*)count, (const int*)loc, (const int*)spre,
-       (const NormKey*)rb.keys_in, (const int32_t*)rb.vals_in, rb.keys_out, rb.vals_out, A);
-  HG_L(k_bs_long, 148, 256, (const int*)count, (const int*)loc, (const int*)spre, (const int*)longl,
-       (const BucketState*)bst, rb.keys_in, rb.vals_in, k2, v2, rb.keys_out, rb.vals_out, A);
+       (const int*)longl, rb.keys_in, rb.vals_in, k2, v2, rb.keys_out, rb.vals_out, A);
 #undef HG_L
   return kOk;
 }
