@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
+#include <map>
 #include <set>
 #include <tuple>
 #include <string>
@@ -69,18 +70,22 @@ bool node_prio_enabled() {
 
 const char* env_knob(const char* name) { return std::getenv(name); }
 
+// raise (never lower) a kernel's dynamic shared-memory limit to >= bytes;
+// launches below the 48 KB default need nothing
 int ensure_smem_attr(const void* kernel, int bytes, const char* where) {
+  if (bytes <= 48 * 1024) return kOk;
   static std::mutex mu;
-  static std::set<std::tuple<const void*, int, int>> done;
+  static std::map<std::pair<const void*, int>, int> set_to;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return fail(where, kCuda, cudaGetErrorString(e));
   std::lock_guard<std::mutex> lk(mu);
-  const auto key = std::make_tuple(kernel, dev, bytes);
-  if (done.count(key)) return kOk;
+  const auto key = std::make_pair(kernel, dev);
+  const auto it = set_to.find(key);
+  if (it != set_to.end() && it->second >= bytes) return kOk;
   e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return fail(where, kCuda, cudaGetErrorString(e));
-  done.insert(key);
+  set_to[key] = bytes;
   return kOk;
 }
 
