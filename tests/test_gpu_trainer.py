@@ -296,3 +296,33 @@ def test_unaligned_feature_width_lockstep(kind, dim, fp16):
     assert not slab[dim:fs].any()
     if kind == SAGE:
         assert not slab[fs + dim:2 * fs].any()
+
+
+@pytest.mark.parametrize("kind", [SAGE, GCN])
+def test_eager_and_engine_paths_interleave(kind):
+    """The eager iteration (transposed aggregation writing d_in rows) and the
+    engine step (the same kernel writing the previous layer's dz operand)
+    alternate in one process: launch configuration set by one path must not
+    break the other (regression: a 0-byte shared-memory request once lowered
+    the limit a later dz launch needed). Both paths keep matching the oracle
+    in lockstep."""
+    import paper_2301_07482_b200 as hg
+    ds, g = _pl3000()
+    lk, ok = _kinds(kind)
+    common = dict(fanouts=(10, 5, 3), hidden=32, batch_size=128, epochs=1, eta=0.05, p_grad=0.9, t_stale=4,
+                  seed=11)
+    tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, hg.TrainConfig(kind=lk, **common), ds.num_classes)
+    otr = OTrainer(g, ds.features, ds.labels, ds.train_ids, OTrainConfig(kind=ok, **common), ds.num_classes)
+    batches = hg.make_batches(ds.train_ids, tr.cfg)
+    for it in range(8):
+        osub = otr.sample(it, batches[it])
+        if it % 2 == 0:
+            m = tr.train_iteration(it, 0, tr.sample(it, batches[it]))
+        else:
+            nxt = (it + 1, batches[it + 1])
+            m = tr.train_step(it, 0, batches[it], next_batch=nxt)
+        norms = {l: tr.last[3][l].cpu().numpy() for l in range(1, 3)}
+        om = otr.train_iteration(it, 0, osub, norms_override=norms)
+        for f in INT_FIELDS:
+            assert getattr(m, f) == getattr(om, f), (it, f)
+        assert abs(m.loss - om.loss) <= 1e-3 * abs(om.loss), it
