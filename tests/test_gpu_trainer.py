@@ -316,7 +316,7 @@ def test_eager_and_engine_paths_interleave(kind):
     batches = hg.make_batches(ds.train_ids, tr.cfg)
     for it in range(8):
         osub = otr.sample(it, batches[it])
-        if it % 2 == 0:
+        if it % 2 == 1:      # engine first, then eager, then engine again
             m = tr.train_iteration(it, 0, tr.sample(it, batches[it]))
         else:
             nxt = (it + 1, batches[it + 1])
