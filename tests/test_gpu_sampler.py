@@ -153,9 +153,10 @@ def test_producer_matches_sequential():
 
 @pytest.mark.parametrize("fanouts", [(5, 3), (15, 10), (32,)])
 def test_hub_rows_split_across_warps_vs_oracle(fanouts):
-    """Rows with more than 4096 candidates take the segmented hub path
-    (k_select_huge + k_merge_huge): several hubs of 4097 .. 30000 in-edges
-    (multi-edges and ties included) must sample bit-exactly like the oracle."""
+    """Rows with more than 1024 candidates take the segmented hub path
+    (512-candidate segments, merged by the warp finishing a row's last
+    segment): several hubs of 4097 .. 30000 in-edges (multi-edges and ties
+    included) must sample bit-exactly like the oracle."""
     hg = _hg()
     rng = np.random.default_rng(77)
     n = 40000
@@ -171,6 +172,30 @@ def test_hub_rows_split_across_warps_vs_oracle(fanouts):
         seeds = np.concatenate([hubs, rng.choice(np.arange(10, n), size=59, replace=False)])
         want = osample(s, e, c, n, seeds, fanouts, obatch_rng(9, idx))
         got = hg.sample_layered(g, seeds, hg.SamplePlan(fanouts, len(seeds), 9), hg.batch_rng(9, idx))
+        assert_sub_equal(_np_blocks(got), [
+            {"dst": b.dst_nodes, "src": b.src_nodes, "start": b.start, "end": b.end, "col": b.col,
+             "dst_deg": b.dst_deg, "src_deg": b.src_deg} for b in want.layers])
+
+
+@pytest.mark.parametrize("fanout", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 31, 32])
+def test_every_selection_path_vs_oracle(fanout):
+    """In-degrees spread over 0 .. 3000 so one layer mixes rows on every
+    selection path of k_select_all -- one row per thread (<= 64 candidates,
+    each register-network width kF), one row per warp (65 .. 1024, packed and
+    first-chunk paths) and 512-candidate hub segments (> 1024) -- for every
+    fanout the templates distinguish; bit-exact with the oracle."""
+    hg = _hg()
+    rng = np.random.default_rng(1000 + fanout)
+    n = 6000
+    degs = np.concatenate([rng.integers(0, 70, n - 60), rng.integers(60, 1100, 50), rng.integers(1000, 3000, 10)])
+    dst = np.repeat(np.arange(n), degs)
+    src = rng.integers(0, n, len(dst))
+    s, e, c = csr2_from_edges(src, dst, n)
+    g = hg.csr2_from_arrays(s, e, c)
+    for idx in range(2):
+        seeds = np.concatenate([np.arange(n - 60, n), rng.choice(n - 60, size=200, replace=False)])
+        want = osample(s, e, c, n, seeds, (fanout, 2), obatch_rng(3, idx))
+        got = hg.sample_layered(g, seeds, hg.SamplePlan((fanout, 2), len(seeds), 3), hg.batch_rng(3, idx))
         assert_sub_equal(_np_blocks(got), [
             {"dst": b.dst_nodes, "src": b.src_nodes, "start": b.start, "end": b.end, "col": b.col,
              "dst_deg": b.dst_deg, "src_deg": b.src_deg} for b in want.layers])
