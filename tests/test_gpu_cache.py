@@ -115,7 +115,7 @@ def test_large_updates_with_ties_match_oracle(n, ties):
         assert cache.counters() == ocache.counters()
 
 
-@pytest.mark.parametrize("case", ["random", "few_values", "all_equal", "zeros_and_tail"])
+@pytest.mark.parametrize("case", ["random", "few_values", "all_equal", "zeros_and_tail", "clusters"])
 @pytest.mark.parametrize("n", [3000, 40000])
 def test_large_updates_match_oracle(case, n):
     """Admission ranking at sizes and tie structures the scripted sequences do
@@ -138,6 +138,10 @@ def test_large_updates_match_oracle(case, n):
             norms = rng.integers(0, 4, n) * 0.25
         elif case == "all_equal":
             norms = np.full(n, 0.125)
+        elif case == "clusters":
+            # ~40 tight clusters decades apart: buckets of ~n/40 keys each
+            # (the rank kernel's CTA-sorted buckets of 129 .. 2048 keys at n = 40000)
+            norms = 10.0 ** rng.integers(-20, 20, n) * (1.0 + rng.random(n) * 1e-9)
         else:
             norms = np.where(rng.random(n) < 0.7, 0.0, rng.random(n))
         emb = rng.standard_normal((n, dim)).astype(np.float32)
