@@ -211,6 +211,13 @@ int hg_cross_entropy(const float* logits, const int32_t* labels, int B, int C, f
 /* ---- K8 backward: nn.py:166-177,300-320 (_layer_backward, backward) */
 int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, const float* d_h, const float* h_out,
                  int dout, int relu, void* dz_ts, cudaStream_t stream);
+/* GAT layer-0 transform operand read in place: row k of A_ts (TS layout for
+ * n_max rows) = the feature row at rowp[rows[k]] (dtype 0 fp32, 1 fp16 -> fp32),
+ * for k < *n_dev; padding rows of the last tile zeroed. The fp32 copy of the
+ * input frontier (hg_load_features) and its re-gather are not needed.
+ * Reference: oracle/gat.py layer_forward (z = h_in[live] W). */
+int hg_gather_rows_ts(const int32_t* n_dev, long long n_max, const int32_t* rows, const unsigned long long* rowp,
+                      int dtype, int d, void* A_ts, cudaStream_t stream);
 long long hg_csc_scratch_bytes(long long E_max, long long n_src_max);
 int hg_build_csc(const int32_t* n_dst_dev, const int32_t* blk_off, const uint8_t* keep, const int32_t* pos_of,
                  const int32_t* col, long long E_max, long long n_src_max, unsigned* keys_sorted,

@@ -68,6 +68,7 @@ SIGNATURES = {
     "hg_inject_rows": (I32, [P, I64, P, P, P, I32, P, P]),
     "hg_cross_entropy": (I32, [P, P, I32, I32, P, P, P, P]),
     "hg_gather_dz": (I32, [P, I64, P, P, P, I32, I32, P, P]),
+    "hg_gather_rows_ts": (I32, [P, I64, P, P, I32, I32, P, P]),
     "hg_csc_scratch_bytes": (I64, [I64, I64]),
     "hg_build_csc": (I32, [P, P, P, P, P, I64, I64, P, P, P, P, P, I64, P]),
     "hg_transpose_agg": (I32, [I32, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P, P,

@@ -360,6 +360,57 @@ __global__ void __launch_bounds__(256) k_gather_dz(const int32_t* R_dev, const i
     for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK * 4, plane, i, g, zeros);
 }
 
+// GAT layer 0: the transform operand from feature rows read in place
+// (hg_gather_rows_ts), one thread per (row, 8-column group): load 8 values
+// (fp32 or fp16 -> fp32), split, store -- no staging, every row's groups in
+// flight at once; padding rows / columns zero
+template <int kSrc>
+__global__ void __launch_bounds__(256) k_gather_ts_flat(const int32_t* R_dev, const int32_t* __restrict__ rows,
+                                                        const unsigned long long* __restrict__ rowp, int d,
+                                                        uint8_t* __restrict__ A_ts, long long plane) {
+  pdl_wait();
+  const int R = *R_dev;
+  const int nK = (d + 31) / 32;
+  const int nG = nK * 4;
+  const long long total = (long long)((R + kTsRows - 1) / kTsRows * kTsRows) * nG;
+  KTimer* kt = g_kt ? g_kt + kTLoadRows : nullptr;
+  kt_begin(kt);
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / nG), g = (int)(t - (long long)i * nG);
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int c0 = g * 8;
+    if (i < R && c0 < d) {
+      const char* src = reinterpret_cast<const char*>(rowp[rows[i]]);
+      if (kSrc == 2) {
+        if (c0 + 8 <= d) {
+          const uint4 u = *reinterpret_cast<const uint4*>(src + (size_t)c0 * 2);
+          const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = __half22float2(h[q]);
+            v[2 * q] = f.x;
+            v[2 * q + 1] = f.y;
+          }
+        } else {
+          const __half* h = reinterpret_cast<const __half*>(src);
+          for (int q = 0; q < 8 && c0 + q < d; ++q) v[q] = __half2float(h[c0 + q]);
+        }
+      } else {
+        const float* f = reinterpret_cast<const float*>(src);
+        const float4 a = *reinterpret_cast<const float4*>(f + c0);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        if (c0 + 8 <= d) {
+          const float4 b = *reinterpret_cast<const float4*>(f + c0 + 4);
+          v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        }
+      }
+    }
+    ts_store8(A_ts, nG, plane, i, g, v);
+  }
+  kt_end(kt);
+}
+
 // Transposed (CSC) view of the surviving edges of a pruned block, built
 // without a library sort and sized by the surviving edges (not the block's
 // upper bound): per-source counts (atomics), their exclusive scan (segment
@@ -684,9 +735,27 @@ int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, con
                  int dout, int relu, void* dz_ts, cudaStream_t stream) {
   if (dout > kMaxRowFloats) return fail("hg_gather_dz", kBadArg, "row too wide");
   const long long rows_pad = (R_max + kTsRows - 1) / kTsRows * kTsRows;
-  { const cudaError_t _pe = hg::launch_pdl(k_gather_dz, dim3(grid_for(rows_pad * 32, 256, 148 * 16)), dim3(256), 0, stream, 
-      R_dev, rows, d_h, h_out, dout, relu, static_cast<uint8_t*>(dz_ts), ts_plane_bytes(R_max, dout)); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  { const cudaError_t _pe = hg::launch_pdl(k_gather_dz, dim3(grid_for(rows_pad * 32, 256, 148 * 16)), dim3(256), 0,
+      stream, R_dev, rows, d_h, h_out, dout, relu, static_cast<uint8_t*>(dz_ts), ts_plane_bytes(R_max, dout));
+    if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_gather_dz");
+  return kOk;
+}
+
+int hg_gather_rows_ts(const int32_t* n_dev, long long n_max, const int32_t* rows, const unsigned long long* rowp,
+                      int dtype, int d, void* A_ts, cudaStream_t stream) {
+  const char* W = "hg_gather_rows_ts";
+  if (d > kMaxRowFloats || d % 4 || (dtype == 1 && d % 8)) return fail(W, kBadArg, "row width");
+  const long long rows_pad = (n_max + kTsRows - 1) / kTsRows * kTsRows;
+  const int nG = (d + 31) / 32 * 4;
+  const unsigned fgrid = grid_for(rows_pad * nG, 256, 148 * 32);
+  const cudaError_t pe =
+      dtype == 1 ? hg::launch_pdl(k_gather_ts_flat<2>, dim3(fgrid), dim3(256), 0, stream, n_dev, rows, rowp, d,
+                                  static_cast<uint8_t*>(A_ts), ts_plane_bytes(n_max, d))
+                 : hg::launch_pdl(k_gather_ts_flat<1>, dim3(fgrid), dim3(256), 0, stream, n_dev, rows, rowp, d,
+                                  static_cast<uint8_t*>(A_ts), ts_plane_bytes(n_max, d));
+  if (pe != cudaSuccess) return fail(W, kCuda, cudaGetErrorString(pe));
+  HG_LAUNCHED(W);
   return kOk;
 }
 

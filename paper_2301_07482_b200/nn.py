@@ -394,8 +394,14 @@ def gat_layer_forward_dev(net: Network, l: int, blk, h_in, rows, R, R_dev, act, 
         live = torch.arange(blk.num_src, dtype=torch.int32, device=dev)
         n_live, n_live_dev = blk.num_src, _dev_count(blk.num_src, dev)
     A = torch.empty(ts_bytes(n_live, d_in), dtype=torch.uint8, device=dev)
-    _lib.call("hg_gather_dz", _lib.ptr(n_live_dev), n_live, _lib.ptr(live), _lib.ptr(h_in), None, d_in, 0,
-              _lib.ptr(A), stream)
+    if isinstance(h_in, FeatureRows):     # layer 0: the transform operand straight from the feature rows
+        if h_in.dim != d_in:
+            raise ValueError(f"feature rows of width {h_in.dim} for a layer of input width {d_in}")
+        _lib.call("hg_gather_rows_ts", _lib.ptr(n_live_dev), n_live, _lib.ptr(live), _lib.ptr(h_in.rowp),
+                  h_in.dtype_code, d_in, _lib.ptr(A), stream)
+    else:
+        _lib.call("hg_gather_dz", _lib.ptr(n_live_dev), n_live, _lib.ptr(live), _lib.ptr(h_in), None, d_in, 0,
+                  _lib.ptr(A), stream)
     slab = net.slab(l)
     PT = torch.empty(ts_bytes(HF, d_in), dtype=torch.uint8, device=dev)      # TS(W^T)
     _lib.call("hg_ts_pack", _lib.ptr(slab), HF, 1, HF, d_in, HF, _lib.ptr(PT), stream)

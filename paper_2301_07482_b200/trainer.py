@@ -432,11 +432,11 @@ class Trainer:
         self.grad_hook = None   # callable(Grads) run between backward and SGD (data parallel)
         self.use_graphs = os.environ.get("HG_GRAPHS", "1") != "0"
         # layer 0 reads the feature rows in place (no fp32 copy of the input
-        # frontier) unless they sit in host memory (UVA: one gather over PCIe
-        # beats one read per edge) or the layer is GAT (its transform runs
-        # over all live sources); HG_FUSED_INPUT=0 restores the gather (A/B)
-        self.fused_input = (cfg.kind is not LayerKind.GAT and cfg.feature_placement == "hbm"
-                            and os.environ.get("HG_FUSED_INPUT", "1") != "0")
+        # frontier: SAGE / GCN aggregate them directly, GAT gathers them
+        # straight into its transform operand) unless they sit in host memory
+        # (UVA: one gather over PCIe beats one read per edge);
+        # HG_FUSED_INPUT=0 restores the gather (A/B)
+        self.fused_input = (cfg.feature_placement == "hbm" and os.environ.get("HG_FUSED_INPUT", "1") != "0")
         self._engines = {}
         self._ahead = None     # (key, device words) of the batch announced by the last step
         self._ctr_gen = 0      # bumped by every counter-moving step (engine metric rows re-sync on change)
