@@ -328,36 +328,52 @@ __global__ void __launch_bounds__(1024) k_ce_loss(const double* __restrict__ row
 }
 
 // dz[i] = d_h[rows[i]] * (h_out[rows[i]] > 0), emitted as TS (hg_ts.cuh): one
-// warp per row, staged through smem; padding rows of the last tile are zeroed.
+// thread per (row, 8-column group) -- 8 gradients (and 8 outputs for the
+// ReLU mask) loaded, split, stored; padding rows / columns zero. Rows whose
+// width is not a multiple of 4 take the scalar loads.
 __global__ void __launch_bounds__(256) k_gather_dz(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const float* __restrict__ d_h, const float* __restrict__ h_out,
                                                    int dout, int relu, uint8_t* __restrict__ dz_ts, long long plane) {
   pdl_wait();
-  __shared__ __align__(16) float s_rows[8][kMaxRowFloats];
   const int R = *R_dev;
-  const int lane = threadIdx.x & 31;
-  const int nK = (dout + 31) / 32;
-  float* srow = s_rows[threadIdx.x >> 5];
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  for (int i = w0; i < R; i += warps) {
-    const long long base = (long long)rows[i] * dout;
-    for (int j = lane; j < nK * 32; j += 32) {
-      float g = 0.f;
-      if (j < dout) {
-        g = d_h[base + j];
-        if (relu && !(h_out[base + j] > 0.f)) g = 0.f;
+  const int nG = (dout + 31) / 32 * 4;
+  const long long total = (long long)((R + kTsRows - 1) / kTsRows * kTsRows) * nG;
+  const bool vec = (dout & 3) == 0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / nG), g = (int)(t - (long long)i * nG);
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int c0 = g * 8;
+    if (i < R && c0 < dout) {
+      const long long base = (long long)rows[i] * dout + c0;
+      if (vec) {
+        const float4 a = *reinterpret_cast<const float4*>(d_h + base);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        if (c0 + 8 <= dout) {
+          const float4 b = *reinterpret_cast<const float4*>(d_h + base + 4);
+          v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        }
+        if (relu) {
+          const float4 ha = *reinterpret_cast<const float4*>(h_out + base);
+          const float hv[8] = {ha.x, ha.y, ha.z, ha.w, 0.f, 0.f, 0.f, 0.f};
+          float hb[4] = {0.f, 0.f, 0.f, 0.f};
+          if (c0 + 8 <= dout) {
+            const float4 h2 = *reinterpret_cast<const float4*>(h_out + base + 4);
+            hb[0] = h2.x; hb[1] = h2.y; hb[2] = h2.z; hb[3] = h2.w;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (!((q < 4 ? hv[q] : hb[q - 4]) > 0.f)) v[q] = 0.f;
+        }
+      } else {
+        for (int q = 0; q < 8 && c0 + q < dout; ++q) {
+          v[q] = d_h[base + q];
+          if (relu && !(h_out[base + q] > 0.f)) v[q] = 0.f;
+        }
       }
-      srow[j] = g;
     }
-    __syncwarp();
-    for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK * 4, plane, i, g, srow + g * 8);
-    __syncwarp();
+    ts_store8(dz_ts, nG, plane, i, g, v);
   }
-  const int R_pad = (R + kTsRows - 1) / kTsRows * kTsRows;
-  const float zeros[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int i = R + w0; i < R_pad; i += warps)
-    for (int g = lane; g < nK * 4; g += 32) ts_store8(dz_ts, nK * 4, plane, i, g, zeros);
 }
 
 // GAT layer 0: the transform operand from feature rows read in place
@@ -735,7 +751,7 @@ int hg_gather_dz(const int32_t* R_dev, long long R_max, const int32_t* rows, con
                  int dout, int relu, void* dz_ts, cudaStream_t stream) {
   if (dout > kMaxRowFloats) return fail("hg_gather_dz", kBadArg, "row too wide");
   const long long rows_pad = (R_max + kTsRows - 1) / kTsRows * kTsRows;
-  { const cudaError_t _pe = hg::launch_pdl(k_gather_dz, dim3(grid_for(rows_pad * 32, 256, 148 * 16)), dim3(256), 0,
+  { const cudaError_t _pe = hg::launch_pdl(k_gather_dz, dim3(grid_for(rows_pad * ((dout + 31) / 32 * 4), 256, 148 * 32)), dim3(256), 0,
       stream, R_dev, rows, d_h, h_out, dout, relu, static_cast<uint8_t*>(dz_ts), ts_plane_bytes(R_max, dout));
     if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_gather_dz");
