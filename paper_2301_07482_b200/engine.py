@@ -76,6 +76,9 @@ class DevBlock:
 # HG_NODE_PRIO=1: streams get priorities (cache updates > training > lookahead
 # sampler) and the captured step is instantiated with per-node priorities
 _NODE_PRIO = os.environ.get("HG_NODE_PRIO") == "1"
+# HG_SAMP_AT: where the lookahead sampler forks off the step (start | pruned |
+# forward0 | forward1 | loss); later forks keep it off the early critical path
+_SAMP_AT = os.environ.get("HG_SAMP_AT", "start")
 # HG_FUSED_DZ=0: d_in rows + a separate dz gather per layer (A/B)
 _FUSED_DZ = os.environ.get("HG_FUSED_DZ", "1") != "0"
 
@@ -292,12 +295,17 @@ class StepEngine:
         stream = torch.cuda.current_stream(dev)
         sp = _lib.stream_ptr(stream)
         self._mark("start", stream)
-        if ahead:
+
+        def launch_ahead():
+            # the next batch, sampled on the side stream from this point on
             samp = self.samp_stream
             samp.wait_stream(stream)
             with torch.cuda.stream(samp):
                 sample_blocks_dev(tr.graph, self.seeds, self.F0, B, cfg.fanouts, self.ws, samp, self.slots[1 - s])
                 self._mark("next_sampled (side)", samp)
+
+        if ahead and _SAMP_AT == "start":
+            launch_ahead()
         # forward weight operands (depend only on the weights): packed on the
         # injection stream concurrently with the prune walk
         PTs = [None] * L
@@ -354,6 +362,8 @@ class StepEngine:
             return counts[2 * b + 1:2 * b + 2]
 
         self._mark("pruned", stream)
+        if ahead and _SAMP_AT == "pruned":
+            launch_ahead()
         # ---- off-critical-path backward prep (overlaps the forward) ----
         prep = self.prep_stream
         prep.wait_stream(stream)
@@ -417,8 +427,12 @@ class StepEngine:
             tapes.append(t)
             h = t.h_out
             self._mark(f"forward{b}", stream)
+            if ahead and _SAMP_AT == f"forward{b}":
+                launch_ahead()
         d_h, loss = cross_entropy_dev(tapes[-1].h_out, self.labels, B, net.dims[-1], sp)
         self._mark("forward+loss", stream)
+        if ahead and _SAMP_AT == "loss":
+            launch_ahead()
 
         # ---- backward (nn.py:300-320) + SGD, cache updates (cache.py:188-204) ----
         # layer l's admission/ring update (l >= 1) is forked onto its own
