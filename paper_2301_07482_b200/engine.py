@@ -79,6 +79,9 @@ _NODE_PRIO = os.environ.get("HG_NODE_PRIO") == "1"
 # HG_SAMP_AT: where the lookahead sampler forks off the step (start | pruned |
 # forward0 | forward1 | loss); later forks keep it off the early critical path
 _SAMP_AT = os.environ.get("HG_SAMP_AT", "start")
+# HG_SAMP_L0_AT: with the sampler forked at the start, where its innermost
+# (widest, most expensive) layer forks (start | forward0 | forward1 | loss)
+_SAMP_L0_AT = os.environ.get("HG_SAMP_L0_AT", "start")
 # HG_FUSED_DZ=0: d_in rows + a separate dz gather per layer (A/B)
 _FUSED_DZ = os.environ.get("HG_FUSED_DZ", "1") != "0"
 
@@ -296,16 +299,19 @@ class StepEngine:
         sp = _lib.stream_ptr(stream)
         self._mark("start", stream)
 
-        def launch_ahead():
-            # the next batch, sampled on the side stream from this point on
+        def launch_ahead(layers=None):
+            # the next batch (or some of its layers), sampled on the side
+            # stream from this point on
             samp = self.samp_stream
             samp.wait_stream(stream)
             with torch.cuda.stream(samp):
-                sample_blocks_dev(tr.graph, self.seeds, self.F0, B, cfg.fanouts, self.ws, samp, self.slots[1 - s])
-                self._mark("next_sampled (side)", samp)
+                sample_blocks_dev(tr.graph, self.seeds, self.F0, B, cfg.fanouts, self.ws, samp, self.slots[1 - s],
+                                  layers=layers)
+                if layers is None or layers[1] == L:
+                    self._mark("next_sampled (side)", samp)
 
         if ahead and _SAMP_AT == "start":
-            launch_ahead()
+            launch_ahead(None if _SAMP_L0_AT == "start" else (0, L - 1))
         # forward weight operands (depend only on the weights): packed on the
         # injection stream concurrently with the prune walk
         PTs = [None] * L
@@ -429,10 +435,14 @@ class StepEngine:
             self._mark(f"forward{b}", stream)
             if ahead and _SAMP_AT == f"forward{b}":
                 launch_ahead()
+            if ahead and _SAMP_AT == "start" and _SAMP_L0_AT == f"forward{b}":
+                launch_ahead((L - 1, L))
         d_h, loss = cross_entropy_dev(tapes[-1].h_out, self.labels, B, net.dims[-1], sp)
         self._mark("forward+loss", stream)
         if ahead and _SAMP_AT == "loss":
             launch_ahead()
+        if ahead and _SAMP_AT == "start" and _SAMP_L0_AT == "loss":
+            launch_ahead((L - 1, L))
 
         # ---- backward (nn.py:300-320) + SGD, cache updates (cache.py:188-204) ----
         # layer l's admission/ring update (l >= 1) is forked onto its own

@@ -199,18 +199,24 @@ class SampleSlot:
 
 
 def sample_blocks_dev(g: Csr2Graph, frontier: torch.Tensor, F0_dev: torch.Tensor, B: int, fanouts,
-                      ws: SamplerWorkspace, stream, slot: SampleSlot | None = None) -> list:
+                      ws: SamplerWorkspace, stream, slot: SampleSlot | None = None, layers=None) -> list:
     """Launch every sampling layer with host upper bounds and device counts
     (no host synchronisation). ws.state must hold the batch's PCG64 state.
     Returns per layer (outermost first): dict of device buffers (the slot's
-    preallocated ones when `slot` is given)."""
+    preallocated ones when `slot` is given). `layers` = (first, stop): only
+    those layers (outermost = 0); a later call continues where an earlier
+    one stopped (the engine forks the innermost, widest layer later)."""
     N = g.num_nodes
     sp = _lib.stream_ptr(stream)
     if slot is None:
         slot = SampleSlot(g, B, fanouts)
+    first, stop = layers if layers is not None else (0, len(slot.layers))
     F_dev = F0_dev
+    if first > 0:
+        prev = slot.layers[first - 1]
+        frontier, F_dev = prev["src"], prev["counts"][1:2]
     raw = []
-    for L in slot.layers:
+    for L in slot.layers[first:stop]:
         _lib.call("hg_sample_layer", _lib.ptr(g.start), _lib.ptr(g.end), _lib.ptr(g.col_indices), N,
                   _lib.ptr(frontier), _lib.ptr(F_dev), L["F_max"], L["fanout"], _lib.ptr(ws.state),
                   _lib.ptr(ws.g2l), _lib.ptr(ws.bitmap), _lib.ptr(L["cand_off"]), _lib.ptr(L["blk_off"]),
