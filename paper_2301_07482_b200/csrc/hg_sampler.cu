@@ -4,13 +4,15 @@
 // Per layer (frontier F rows, device-side counts):
 //   k_stamp     g2l[frontier[i]] = epoch<<32 | i ; src_out[i] = frontier[i]
 //   scan        (deg, min(deg,fanout)) -> cand_off (PCG stream offsets), blk_off
-//   k_task_bounds  split the layer's stream into warp tasks of ~C draws
-//               (contiguous rows, balanced by candidates)
-//   k_select    one warp per task: jump the PCG64 stream to the task's first
-//               candidate (later rows: one multiply-add), draw one 53-bit key
-//               per candidate in-edge, keep the `fanout` smallest (key,
-//               position) pairs (warp bitonic network + ballot insertion) and
-//               record the picked edge indices in key order
+//   k_plan      per row: the PCG64 state before its first draw, hub rows
+//               (> kHuge candidates) cut into segments, a histogram of the
+//               other rows by candidate count                 (fanout <= 32)
+//   k_order     rows by descending candidate count
+//   k_select_all  one persistent launch over a longest-first work list: hub
+//               segments, one row per warp, short rows one per thread; one
+//               53-bit key per candidate in-edge, the `fanout` smallest
+//               (key, position) pairs recorded in key order
+//   (fanout > 32: k_task_bounds + k_select_generic, repeated warp minima)
 //   k_pick      picked edge -> global source id; non-frontier sources are
 //               marked in a node bitmap
 //   bitmap scan sorted-unique "new" nodes fall out of the bitmap in id order:
@@ -42,11 +44,6 @@ int set_timers_sampler(void* p) {
   return e == cudaSuccess ? kOk : fail("set_timers_sampler", kCuda, cudaGetErrorString(e));
 }
 namespace {
-
-struct KeyJ {
-  unsigned long long k;
-  unsigned j;
-};
 
 __device__ __forceinline__ bool kj_less(unsigned long long ak, unsigned aj, unsigned long long bk, unsigned bj) {
   return ak < bk || (ak == bk && aj < bj);
