@@ -3,7 +3,8 @@
 //   _mean_matrix / _gcn_matrix + a @ h_in   nn.py:101-128,148-156  -> k_aggregate
 //   h_full[rows] = z ; h_full[inj] = cached  nn.py:288-293          -> k_scatter_rows, k_inject
 //   cross_entropy (fp64 log-sum-exp)         nn.py:326-343          -> k_ce_rows, k_ce_loss
-//   dz = relu_mask * d_out                   nn.py:167              -> k_gather_dz
+//   dz = relu_mask * d_out                   nn.py:167              -> k_gather_dz (top layer); below it
+//                                                                      written by the next layer's k_transpose_agg
 //   d_in = A^T (dz W^T) (+ self)             nn.py:171,175-176      -> CSC build + k_transpose_agg
 //   node_grad_norms (fp64)                   nn.py:346-349          -> fused in k_transpose_agg
 //   sgd_step                                 nn.py:355-360          -> k_sgd
