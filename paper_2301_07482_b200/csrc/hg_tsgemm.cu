@@ -8,7 +8,7 @@
 // mbarrier) into a kStages-deep shared-memory ring; a single thread issues
 // tcgen05.mma kind::f16 (bf16 x bf16 -> fp32 in TMEM) for the 3-term split
 //   a.b ~= hi(a).hi(b) + hi(a).lo(b) + lo(a).hi(b)   (relative error ~1e-5)
-// and releases each stage with tcgen05.commit; all four warps drain TMEM
+// and releases each stage with tcgen05.commit; 4 x kEpiHalves warps drain TMEM
 // through shared memory in the epilogue (coalesced row stores).
 //   kMN = false: D = A . B^T, both operands K-major      (forward, data grad)
 //   kMN = true : D = A^T . B over the stored rows, both read as MN-major
@@ -37,7 +37,15 @@ namespace {
 
 constexpr int kTM = 128;       // tile rows (MMA M)
 constexpr int kBK = 32;        // K elements per stage
-constexpr int kThreads = 128;
+// Epilogue warps split a tile's columns in kEpiHalves parts per TMEM lane
+// quadrant (4 * kEpiHalves epilogue warps): the drain is issue-latency bound
+// (ncu: ~8 cycles per issued instruction, one epilogue warp per scheduler).
+#ifndef HG_EPI_HALVES
+#define HG_EPI_HALVES 2
+#endif
+constexpr int kEpiHalves = HG_EPI_HALVES;
+constexpr int kEpiWarps = 4 * kEpiHalves;
+constexpr int kThreads = 32 * kEpiWarps;   // one-tile kernel: every warp drains
 constexpr int kStages = 4;
 
 // ---------------------------------------------------------------- PTX helpers
@@ -86,17 +94,19 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
+// 32 consecutive accumulator columns of this thread's TMEM lane, one wait
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+
 // no-swizzle UMMA shared-memory descriptor, Blackwell version bit
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -175,9 +185,14 @@ struct EpiPartial {      // part[z][i][n] = acc
   }
 };
 
-// Store one staged 32 x 32 chunk (stage_f[r * 33 + c], r = tile row, c =
-// column in the chunk). Vector path: a warp instruction writes 4 rows x 128 B
-// (8 lanes x 16 B per row), 8 instructions per chunk instead of 32; columns
+// Epilogue staging: a warp moves its 32 tile rows x 32 columns through a
+// 4 KB shared-memory chunk, float4 j of row r at slot j ^ (r & 7) (XOR
+// swizzle, no padding): the row-per-lane STS.128 writes and the
+// 4-rows-per-instruction LDS.128 reads are both bank-conflict free.
+__device__ __forceinline__ int stage_at(int r, int c) { return r * 32 + ((((c >> 2) ^ r) & 7) << 2) + (c & 3); }
+
+// Store one staged 32 x 32 chunk. Vector path: a warp instruction writes
+// 4 rows x 128 B (8 lanes x 16 B per row), 8 instructions per chunk; columns
 // past n_valid fall back to scalar stores.
 template <typename Epi>
 __device__ __forceinline__ void store_chunk(const Epi& epi, const float* stage_f, typename Epi::Key my_key,
@@ -190,12 +205,13 @@ __device__ __forceinline__ void store_chunk(const Epi& epi, const float* stage_f
       const int r = rr + rsub;
       const long long k = epi.expand(__shfl_sync(0xffffffffu, my_key, r));
       if (row0 + r < M) {
-        const float* sp = stage_f + r * 33 + c4;
+        const float4 v = *reinterpret_cast<const float4*>(stage_f + stage_at(r, c4));
         if (col + 3 < n_valid) {
-          epi.store4(k, n0 + col, make_float4(sp[0], sp[1], sp[2], sp[3]));
+          epi.store4(k, n0 + col, v);
         } else {
+          const float e4[4] = {v.x, v.y, v.z, v.w};
           for (int e = 0; e < 4; ++e)
-            if (col + e < n_valid) epi.store(k, n0 + col + e, sp[e]);
+            if (col + e < n_valid) epi.store(k, n0 + col + e, e4[e]);
         }
       }
     }
@@ -203,9 +219,41 @@ __device__ __forceinline__ void store_chunk(const Epi& epi, const float* stage_f
     const int col = c0 + lane;
     for (int r = 0; r < 32; ++r) {
       const long long k = epi.expand(__shfl_sync(0xffffffffu, my_key, r));
-      if (row0 + r < M && col < n_valid) epi.store(k, n0 + col, stage_f[r * 33 + lane]);
+      if (row0 + r < M && col < n_valid) epi.store(k, n0 + col, stage_f[stage_at(r, lane)]);
     }
   }
+}
+
+// Drain accumulator columns [cb, ce) (multiples of 32 from cb) of the
+// warp's TMEM lane quadrant: tmem_row = TMEM address of (quadrant lane 0,
+// column 0 of the accumulator); zero = no K chunk was accumulated.
+template <typename Epi>
+__device__ __forceinline__ void drain_cols(const Epi& epi, uint32_t tmem_row, float* stage_f,
+                                           typename Epi::Key my_key, int row0, int M, int cb, int ce, int n0,
+                                           int n_valid, int lane, bool zero) {
+  for (int c0 = cb; c0 < ce; c0 += 32) {
+    uint32_t acc[32];
+    if (!zero) {
+      tmem_ld32(tmem_row + (uint32_t)c0, acc);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<float4*>(stage_f + stage_at(lane, 4 * j)) =
+          make_float4(__uint_as_float(acc[4 * j]), __uint_as_float(acc[4 * j + 1]), __uint_as_float(acc[4 * j + 2]),
+                      __uint_as_float(acc[4 * j + 3]));
+    __syncwarp();
+    store_chunk(epi, stage_f, my_key, row0, M, c0, n0, n_valid, lane);
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ void epi_cols(int h, int n_valid, int& cb, int& ce) {
+  const int per = ((n_valid + 32 * kEpiHalves - 1) / (32 * kEpiHalves)) * 32;
+  cb = h * per;
+  ce = min(n_valid, cb + per);
 }
 
 struct Shape {
@@ -312,27 +360,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_tsgemm(const __grid_constant__ 
     mma_commit(&done_bar);
   }
   __syncwarp();
-  // epilogue: TMEM lane = tile row; stage 32 x 32 sub-tiles through smem so
-  // every global store instruction writes one contiguous 128 B row segment
+  // epilogue (every warp): TMEM lane = tile row, warp w drains lane quadrant
+  // w % 4, column part w / 4; 32 x 32 sub-tiles staged through smem so every
+  // global store instruction writes contiguous 128 B row segments
   if (nc > 0) mbar_wait(&done_bar, 0);
   tc_fence_after();
   __syncthreads();
-  float* stage_f = reinterpret_cast<float*>(smem) + warp * 32 * 33;
-  const typename Epi::Key my_key = (m0 + warp * 32 + lane < M) ? epi.key(m0 + warp * 32 + lane) : 0;
-  for (int c0 = 0; c0 < n_valid; c0 += 32) {
-    float acc[32];
-    if (nc > 0) {
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, acc);
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c0 + 16), acc + 16);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) stage_f[lane * 33 + j] = acc[j];
-    __syncwarp();
-    store_chunk(epi, stage_f, my_key, m0 + warp * 32, M, c0, n0, n_valid, lane);
-    __syncwarp();
+  {
+    const int q = warp & 3;
+    int cb, ce;
+    epi_cols(warp >> 2, n_valid, cb, ce);
+    float* stage_f = reinterpret_cast<float*>(smem) + warp * 32 * 32;
+    const typename Epi::Key my_key = (m0 + q * 32 + lane < M) ? epi.key(m0 + q * 32 + lane) : 0;
+    drain_cols(epi, tmem + ((uint32_t)(q * 32) << 16), stage_f, my_key, m0 + q * 32, M, cb, ce, n0, n_valid, lane,
+               nc == 0);
   }
   tc_fence_before();
   __syncthreads();
@@ -348,11 +389,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tsgemm(const __grid_constant__ 
 //                   tile boundaries
 //   warp 1 lane 0 : tcgen05.mma issuer into one of TWO TMEM accumulators
 //                   (2 x N_pad columns), tcgen05.commit -> acc_full[buf]
-//   warps 2..5    : epilogue (TMEM lane quadrant = warp % 4), drain tile i
+//   warps 2..     : epilogue (TMEM lane quadrant = warp % 4, column part
+//                   (warp - 2) / 4), drain tile i
 //                   while the MMAs of tile i+1 run; arrive acc_empty[buf]
 // The grid is sized to the SMs, so a row bound far above the actual count
 // costs no empty waves of 200 KB CTAs.
-constexpr int kPThreads = 192;
+constexpr int kPThreads = 64 + 32 * kEpiWarps;
 
 template <typename Epi>
 __global__ void __launch_bounds__(kPThreads, 1) k_tsgemm_p(const __grid_constant__ CUtensorMap tmA,
@@ -380,7 +422,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tsgemm_p(const __grid_constant
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 4);
+      mbar_init(&acc_empty[b], kEpiWarps);
     }
     fence_mbar_init();
   }
@@ -439,28 +481,22 @@ __global__ void __launch_bounds__(kPThreads, 1) k_tsgemm_p(const __grid_constant
       }
     }
   } else {
-    // epilogue warps 2..5: TMEM lanes [32 q, 32 q + 32), q = warp % 4
+    // epilogue warps 2 .. 2 + kEpiWarps: TMEM lanes [32 q, 32 q + 32),
+    // q = warp % 4, column part (warp - 2) / 4
     const int q = warp & 3;
-    float* stage_f = reinterpret_cast<float*>(smem + (size_t)kStages * stage_bytes) + (warp - 2) * 32 * 33;
+    float* stage_f = reinterpret_cast<float*>(smem + (size_t)kStages * stage_bytes) + (warp - 2) * 32 * 32;
     int lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
       const int buf = lt & 1;
       const int m0 = (t / n_tiles) * kTM, n0 = (t % n_tiles) * N_pad;
       const int n_valid = min(N_pad, sh.N - n0);
+      int cb, ce;
+      epi_cols((warp - 2) >> 2, n_valid, cb, ce);
       const typename Epi::Key my_key = (m0 + q * 32 + lane < M) ? epi.key(m0 + q * 32 + lane) : 0;
       mbar_wait(&acc_full[buf], (lt >> 1) & 1);
       tc_fence_after();
-      for (int c0 = 0; c0 < n_valid; c0 += 32) {
-        float acc[32];
-        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * N_pad + c0);
-        tmem_ld16(ta, acc);
-        tmem_ld16(ta + 16, acc + 16);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) stage_f[lane * 33 + j] = acc[j];
-        __syncwarp();
-        store_chunk(epi, stage_f, my_key, m0 + q * 32, M, c0, n0, n_valid, lane);
-        __syncwarp();
-      }
+      drain_cols(epi, tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * N_pad), stage_f, my_key, m0 + q * 32, M,
+                 cb, ce, n0, n_valid, lane, false);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
@@ -558,9 +594,9 @@ template <typename Epi>
 int launch_persistent(const char* W, const CUtensorMap& a, const CUtensorMap& b, Shape sh, Epi e, int n_tile,
                       cudaStream_t stream) {
   const int n_tiles = (sh.N + n_tile - 1) / n_tile;
-  const size_t smem = (size_t)kStages * (2 * 8192 + 2 * (size_t)n_tile * 64) + 4 * 32 * 33 * 4;
+  const size_t smem = (size_t)kStages * (2 * 8192 + 2 * (size_t)n_tile * 64) + kEpiWarps * 32 * 32 * 4;
   {
-    const int max_smem = kStages * (2 * 8192 + 2 * 256 * 64) + 4 * 32 * 33 * 4;
+    const int max_smem = kStages * (2 * 8192 + 2 * 256 * 64) + kEpiWarps * 32 * 32 * 4;
     const int sa = ensure_smem_attr((const void*)k_tsgemm_p<Epi>, max_smem, W);
     if (sa) return sa;
   }
@@ -647,8 +683,13 @@ int hg_ts_linear_dgrad(const int32_t* R_dev, long long R_max, const void* dz_ts,
   if (!st) st = make_map(W, &b, W_ts, K, N, 4, nt / 8);
   if (st) return st;
   Shape sh{(int)R_max, K, N, R_dev, nullptr, (N + kBK - 1) / kBK};
-  // dgrad keeps scalar row stores: measured 0.034 vs 0.036 ms/step (C2)
-  return launch<false>(W, a, b, sh, EpiStore{SG, K, false}, nt, 1, stream);
+  // dgrad row stores: with the 8-warp swizzled-stage epilogue the 16-byte
+  // vector stores win (C2 dgrad 0.040 -> 0.025 ms/step, step 0.663 -> 0.655
+  // ms); with the old 4-warp padded stage, scalar stores had measured better
+#ifndef HG_DGRAD_VEC
+#define HG_DGRAD_VEC 1
+#endif
+  return launch<false>(W, a, b, sh, EpiStore{SG, K, HG_DGRAD_VEC ? vec_ok(SG, K) : false}, nt, 1, stream);
 }
 
 // dP[K1 x N] = A[:R, :K1]^T . dz[:R, :N]  (split-K over the rows, fixed-order sum)

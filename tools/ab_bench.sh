@@ -14,5 +14,6 @@ for v in sys.argv[1].split():
         print(v, "failed", e); continue
     pk = {k: round(x["ms_per_step"], 4) for k, x in d["per_kernel"].items() if x["launches"]}
     print(f"{v:10s} value {d['value']:.4g} e2e {d['e2e']['value']:.4g} ms {d['ms_per_step']:.4f} "
-          f"roof {d['roofline']['frac']:.3f} agg {d['aggregate_roofline']['frac']:.3f} {pk}")
+          f"roof {d['roofline']['frac']:.3f} agg {(d.get('aggregate_roofline') or {}).get('frac', 0):.3f} {pk}")
+    print("   timeline", {k: round(x, 3) for k, x in d.get("timeline_ms", {}).items()})
 PY
