@@ -47,6 +47,17 @@ constexpr int kMaxRowFloats = 1056;
 #ifndef HG_AGG_MINB
 #define HG_AGG_MINB 6
 #endif
+// wide rows: kT 4 (d <= 512) / kT 8 (d <= 1024) resident CTAs; fp16 rows
+// (MAG240M 768-d) fit 4 CTAs in 64 registers without spills
+#ifndef HG_AGG_MINB4
+#define HG_AGG_MINB4 4
+#endif
+#ifndef HG_AGG_MINB8
+#define HG_AGG_MINB8 3
+#endif
+#ifndef HG_AGG_MINB8H
+#define HG_AGG_MINB8H 4
+#endif
 #ifndef HG_TAGG_MINB
 #define HG_TAGG_MINB 8
 #endif
@@ -108,7 +119,7 @@ __device__ __forceinline__ float4 row_vec(const void* base, int v) {
 #endif
 
 template <int kKind, int kT, int kSrc>
-__global__ void __launch_bounds__(256, kT <= 2 ? (kSrc ? HG_AGG_MINB : HG_AGG_MINB0) : 1) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, kT <= 2 ? (kSrc ? HG_AGG_MINB : HG_AGG_MINB0) : (kT <= 4 ? HG_AGG_MINB4 : (kSrc == 2 ? HG_AGG_MINB8H : HG_AGG_MINB8))) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
@@ -147,11 +158,20 @@ __global__ void __launch_bounds__(256, kT <= 2 ? (kSrc ? HG_AGG_MINB : HG_AGG_MI
     const int r_next = kPipe && i_next < R ? rows[i_next] : 0;
     const int cnt = e1 - e0;
     const void* hs = src_row<kSrc>(h_in, rowp, r, d);
-    float4 xs[kT];
+    // wide rows (kT >= 4) park the self row in the warp's staging row right
+    // away instead of holding kT float4 registers across the edge loop
+    // (K<SAGE, 8, fp16> needed 154 registers = one CTA per SM)
+    constexpr bool kSelfSmem = kT >= 4;
+    float4 xs[kSelfSmem ? 1 : kT];
 #pragma unroll
     for (int t = 0; t < kT; ++t) {
       const int v = lane + 32 * t;
-      xs[t] = v < nv ? row_vec<kSrc>(hs, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 x = v < nv ? row_vec<kSrc>(hs, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (kSelfSmem) {
+        if (v < nv) reinterpret_cast<float4*>(srow)[v] = x;
+      } else {
+        xs[t] = x;
+      }
     }
     float4 acc[kT];
 #pragma unroll
@@ -208,12 +228,13 @@ __global__ void __launch_bounds__(256, kT <= 2 ? (kSrc ? HG_AGG_MINB : HG_AGG_MI
     for (int t = 0; t < kT; ++t) {
       const int v = lane + 32 * t;
       if (v < nv) {
+        const float4 x_self = kSelfSmem ? reinterpret_cast<const float4*>(srow)[v] : xs[kSelfSmem ? 0 : t];
         if (kKind == kKindSAGE) {
-          reinterpret_cast<float4*>(srow)[v] = xs[t];
+          if (!kSelfSmem) reinterpret_cast<float4*>(srow)[v] = x_self;
           reinterpret_cast<float4*>(srow + d)[v] = acc[t];
         } else {
           const float ws = gcn_coef(dd, src_deg[r_cur]);
-          reinterpret_cast<float4*>(srow)[v] = f4_fmadd_rn(acc[t], ws, xs[t]);
+          reinterpret_cast<float4*>(srow)[v] = f4_fmadd_rn(acc[t], ws, x_self);
         }
       }
     }

@@ -239,18 +239,20 @@ def test_async_metrics_equal_sync_metrics():
     assert runs[0] == runs[1]
 
 
-@pytest.mark.parametrize("kind,dim", [(SAGE, 768), (GCN, 600)])
-def test_wide_feature_rows_lockstep(kind, dim):
+@pytest.mark.parametrize("kind,dim,fp16", [(SAGE, 768, False), (GCN, 600, False), (SAGE, 768, True),
+                                           (GCN, 384, True)])
+def test_wide_feature_rows_lockstep(kind, dim, fp16):
     """Input rows wider than 512 floats (MAG240M-like 768-d features): the
     aggregation / transposed-aggregation kernels stage up to 1024 floats per
     lane group; lockstep with the oracle as in test_lockstep_with_oracle."""
     import paper_2301_07482_b200 as hg
     ds = power_law_dataset(1500, np.random.default_rng(5), m=3, feature_dim=dim)
+    feats = ds.features.astype(np.float16) if fp16 else ds.features   # fp16: the MAG240M storage type
     g = csr2_from_edges(ds.src, ds.dst, ds.num_nodes)
     lk, ok = _kinds(kind)
     common = dict(fanouts=(6, 4, 3), hidden=32, batch_size=96, epochs=1, eta=0.05, p_grad=0.9, t_stale=4, seed=7)
-    tr = hg.Trainer(g, ds.features, ds.labels, ds.train_ids, hg.TrainConfig(kind=lk, **common), ds.num_classes)
-    otr = OTrainer(g, ds.features, ds.labels, ds.train_ids, OTrainConfig(kind=ok, **common), ds.num_classes)
+    tr = hg.Trainer(g, feats, ds.labels, ds.train_ids, hg.TrainConfig(kind=lk, **common), ds.num_classes)
+    otr = OTrainer(g, feats, ds.labels, ds.train_ids, OTrainConfig(kind=ok, **common), ds.num_classes)
     batches = hg.make_batches(ds.train_ids, tr.cfg)[:8]
     for it, seeds in enumerate(batches):
         m = tr.train_iteration(it, 0, tr.sample(it, seeds))
