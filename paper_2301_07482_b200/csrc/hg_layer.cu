@@ -47,6 +47,9 @@ constexpr int kMaxRowFloats = 1056;
 #ifndef HG_AGG_MINB
 #define HG_AGG_MINB 6
 #endif
+#ifndef HG_AGG_MINBH       // layer 0 over fp16 rows (papers100M shape)
+#define HG_AGG_MINBH 8
+#endif
 // wide rows: kT 4 (d <= 512) / kT 8 (d <= 1024) resident CTAs; fp16 rows
 // (MAG240M 768-d) fit 4 CTAs in 64 registers without spills
 #ifndef HG_AGG_MINB4
@@ -119,7 +122,7 @@ __device__ __forceinline__ float4 row_vec(const void* base, int v) {
 #endif
 
 template <int kKind, int kT, int kSrc>
-__global__ void __launch_bounds__(256, kT <= 2 ? (kSrc ? HG_AGG_MINB : HG_AGG_MINB0) : (kT <= 4 ? HG_AGG_MINB4 : (kSrc == 2 ? HG_AGG_MINB8H : HG_AGG_MINB8))) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, kT <= 2 ? (kSrc == 2 ? HG_AGG_MINBH : kSrc ? HG_AGG_MINB : HG_AGG_MINB0) : (kT <= 4 ? HG_AGG_MINB4 : (kSrc == 2 ? HG_AGG_MINB8H : HG_AGG_MINB8))) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
