@@ -141,6 +141,8 @@ int hg_resolve_feature_rows(const int32_t* n_live_dev, long long n_live_max, con
                             const void* feats, const void* const* shard_ptrs, const long long* shard_bounds,
                             int num_shards, int local_shard, int dim, int dtype, unsigned long long* rowp,
                             long long* global_ctr, long long* owner_rows, cudaStream_t stream);
+/* hg_aggregate_fwd_rows: dtype 0 fp32 / 1 fp16 feature rows; dtype 2 = fp32
+ * rows of a hidden layer (layer output + cache-hit rows, hg_resolve_hit_rows) */
 int hg_aggregate_fwd_rows(int kind, const int32_t* R_dev, long long R_max, const int32_t* rows, const int32_t* start,
                           const int32_t* end, const int32_t* col, const int32_t* dst_deg, const int32_t* src_deg,
                           const unsigned long long* rowp, int dtype, int d, void* A_ts, float* row_w,
@@ -203,6 +205,14 @@ int hg_scatter_rows(const int32_t* R_dev, long long R_max, const int32_t* rows, 
                     float* h_out, cudaStream_t stream);
 int hg_inject_rows(const int32_t* n_dev, long long n_max, const uint8_t* flag, const int32_t* hit_row,
                    const float* table, int dim, float* h_out, cudaStream_t stream);
+/* cache-hit rows read in place (the engine's alternative to hg_inject_rows for
+ * layers >= 1): rowp[r] = flagged r ? address of its cache row (table row, or
+ * with `tables` the owner ring row of owner << 26 | row) : h_out + r * dim;
+ * the next layer's aggregation reads its sources through rowp
+ * (hg_aggregate_fwd_rows, dtype 0), so no hit row is copied. */
+int hg_resolve_hit_rows(const int32_t* n_dev, long long n_max, const uint8_t* flag, const int32_t* hit_row,
+                        const float* table, const float* const* tables, int dim, const float* h_out,
+                        unsigned long long* rowp, cudaStream_t stream);
 
 /* ---- loss: nn.py:326-343 (cross_entropy, fp64) */
 int hg_cross_entropy(const float* logits, const int32_t* labels, int B, int C, float* dlogits, double* row_logp,

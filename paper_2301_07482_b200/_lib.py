@@ -66,6 +66,7 @@ SIGNATURES = {
     "hg_resolve_feature_rows": (I32, [P, I64, P, P, P, P, P, P, P, I32, I32, I32, I32, P, P, P, P]),
     "hg_scatter_rows": (I32, [P, I64, P, P, I32, I32, P, P]),
     "hg_inject_rows": (I32, [P, I64, P, P, P, I32, P, P]),
+    "hg_resolve_hit_rows": (I32, [P, I64, P, P, P, P, I32, P, P, P]),
     "hg_cross_entropy": (I32, [P, P, I32, I32, P, P, P, P]),
     "hg_gather_dz": (I32, [P, I64, P, P, P, I32, I32, P, P]),
     "hg_gather_rows_ts": (I32, [P, I64, P, P, I32, I32, P, P]),

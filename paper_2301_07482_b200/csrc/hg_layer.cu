@@ -95,7 +95,9 @@ __device__ __forceinline__ float gcn_coef(int dd, int sd) {
 // Source rows of the aggregation: kSrc 0 = rows of the fp32 matrix h_in
 // (layers >= 1, or a gathered layer-0 input); kSrc 1 / 2 = layer-0 feature
 // rows read in place through per-source addresses rowp[c] (fp32 / fp16
-// tables, hg_resolve_feature_rows): the fp32 copy of every live feature row
+// tables, hg_resolve_feature_rows); kSrc 3 = a hidden layer's fp32 rows
+// through rowp (layer output rows, cache-hit rows in place in the ring:
+// hg_resolve_hit_rows): the fp32 copy of every live feature row
 // and its re-read are gone (K5 fused into K6). fp16 -> fp32 is exact, so the
 // sums are bit-identical to the gathered path.
 template <int kSrc>
@@ -106,7 +108,7 @@ __device__ __forceinline__ const void* src_row(const float* __restrict__ h_in,
 }
 template <int kSrc>
 __device__ __forceinline__ float4 row_vec(const void* base, int v) {
-  if (kSrc <= 1) return reinterpret_cast<const float4*>(base)[v];
+  if (kSrc != 2) return reinterpret_cast<const float4*>(base)[v];
   const uint2 u = reinterpret_cast<const uint2*>(base)[v];
   const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
   const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(256, kT <= 2 ? (kSrc == 2 ? HG_AGG_MINBH : kSr
   const int nK = (K + 1 + 31) / 32;          // TS column chunks of [. | 1 | 0 pad]
   float* srow = agg_smem + (size_t)(threadIdx.x >> 5) * row_floats;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  KTimer* kt = g_kt ? g_kt + (kSrc ? kTAggregateFeat : kTAggregate) : nullptr;
+  KTimer* kt = g_kt ? g_kt + (kSrc == 1 || kSrc == 2 ? kTAggregateFeat : kTAggregate) : nullptr;
   kt_begin(kt);
   // software-pipelined over the warp's rows: the next row's id is fetched at
   // the start of a row and its extents after the edge loads, and a row's own
@@ -264,6 +266,25 @@ __global__ void k_scatter_rows(const int32_t* R_dev, const int32_t* __restrict__
     float z = Z[t];
     if (relu) z = z > 0.f ? z : 0.f;
     h_out[(long long)rows[i] * dout + j] = z;
+  }
+}
+
+// rowp[r] = address of source row r of the next layer: its cache row when
+// flagged (local table, or owner ring: owner << 26 | row), else h_out row r
+__global__ void k_resolve_hits(const int32_t* n_dev, const uint8_t* __restrict__ flag,
+                               const int32_t* __restrict__ hit_row, const float* __restrict__ table,
+                               const float* const* __restrict__ tables, int dim, const float* __restrict__ h_out,
+                               unsigned long long* __restrict__ rowp) {
+  pdl_wait();
+  const int n = *n_dev;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const float* p = h_out + (long long)r * dim;
+    if (flag[r]) {
+      const int h = hit_row[r];
+      p = tables ? tables[(unsigned)h >> 26] + (long long)((unsigned)h & ((1u << 26) - 1)) * dim
+                 : table + (long long)h * dim;
+    }
+    rowp[r] = reinterpret_cast<unsigned long long>(p);
   }
 }
 
@@ -716,7 +737,8 @@ static int aggregate_launch(const char* W, int kind, int src, const int32_t* R_d
   if (vpl <= 1) HG_AGG(KIND, 1, S) else if (vpl <= 2) HG_AGG(KIND, 2, S) else if (vpl <= 4) HG_AGG(KIND, 4, S)   \
   else HG_AGG(KIND, 8, S)
 #define HG_AGG_S(KIND)                                                                                            \
-  if (src == 0) { HG_AGG_T(KIND, 0) } else if (src == 1) { HG_AGG_T(KIND, 1) } else { HG_AGG_T(KIND, 2) }
+  if (src == 0) { HG_AGG_T(KIND, 0) } else if (src == 1) { HG_AGG_T(KIND, 1) } else if (src == 2) {            \
+    HG_AGG_T(KIND, 2) } else { HG_AGG_T(KIND, 3) }
   if (kind == kKindSAGE) {
     HG_AGG_S(kKindSAGE)
   } else {
@@ -744,7 +766,8 @@ int hg_aggregate_fwd_rows(int kind, const int32_t* R_dev, long long R_max, const
                           const unsigned long long* rowp, int dtype, int d, void* A_ts, float* row_w,
                           cudaStream_t stream) {
   if (dtype == 1 && d % 8) return fail("hg_aggregate_fwd_rows", kBadArg, "fp16 rows need d % 8 == 0");
-  return aggregate_launch("hg_aggregate_fwd_rows", kind, dtype == 1 ? 2 : 1, R_dev, R_max, rows, start, end, col,
+  if (dtype < 0 || dtype > 2) return fail("hg_aggregate_fwd_rows", kBadArg, "dtype must be 0, 1 or 2");
+  return aggregate_launch("hg_aggregate_fwd_rows", kind, dtype == 1 ? 2 : dtype == 2 ? 3 : 1, R_dev, R_max, rows, start, end, col,
                           dst_deg, src_deg, nullptr, rowp, d, A_ts, row_w, stream);
 }
 
@@ -752,6 +775,20 @@ int hg_scatter_rows(const int32_t* R_dev, long long R_max, const int32_t* rows, 
                     float* h_out, cudaStream_t stream) {
   { const cudaError_t _pe = hg::launch_pdl(k_scatter_rows, dim3(grid_for(R_max * dout, 256)), dim3(256), 0, stream, R_dev, rows, Z, dout, relu, h_out); if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
   HG_LAUNCHED("hg_scatter_rows");
+  return kOk;
+}
+
+int hg_resolve_hit_rows(const int32_t* n_dev, long long n_max, const uint8_t* flag, const int32_t* hit_row,
+                        const float* table, const float* const* tables, int dim, const float* h_out,
+                        unsigned long long* rowp, cudaStream_t stream) {
+  const char* W = "hg_resolve_hit_rows";
+  if (dim < 4 || (dim & 3)) return fail(W, kBadArg, "rows must be a multiple of 4 floats");
+  if (!table && !tables) return fail(W, kBadArg, "no cache table");
+  if (n_max <= 0) return kOk;
+  { const cudaError_t _pe = hg::launch_pdl(k_resolve_hits, dim3(grid_for(n_max, 256)), dim3(256), 0, stream, n_dev,
+                                           flag, hit_row, table, tables, dim, h_out, rowp);
+    if (_pe != cudaSuccess) return hg::fail("launch", hg::kCuda, cudaGetErrorString(_pe)); }
+  HG_LAUNCHED(W);
   return kOk;
 }
 

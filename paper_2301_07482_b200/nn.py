@@ -332,7 +332,7 @@ class FeatureRows:
     row); the layer-0 aggregation reads the rows in place."""
 
     rowp: torch.Tensor          # int64 [n_src]
-    dtype_code: int             # 0 fp32, 1 fp16
+    dtype_code: int             # 0 fp32, 1 fp16 feature rows; 2 fp32 hidden-layer rows
     dim: int                    # (padded) row width
     num_rows: int
 
@@ -502,6 +502,17 @@ def inject_rows_dev(inj: Injection, h_out: torch.Tensor, n_dst: int, n_dst_dev, 
     """h_out[r] = table[row[r]] for the injected rows (nn.py:290-293)."""
     _lib.call("hg_inject_rows", _lib.ptr(n_dst_dev), n_dst, _lib.ptr(inj.flag), _lib.ptr(inj.row),
               _lib.ptr(inj.table), int(h_out.shape[1]), _lib.ptr(h_out), stream)
+
+
+def resolve_hit_rows_dev(inj: Injection, h_out: torch.Tensor, n_dst: int, n_dst_dev, rowp: torch.Tensor,
+                         stream) -> FeatureRows:
+    """The next layer's input by reference: rowp[r] = the cache row of every
+    injected r (local table or owner ring), else h_out row r; the layer reads
+    its sources in place (hg_aggregate_fwd_rows), no hit row is copied."""
+    _lib.call("hg_resolve_hit_rows", _lib.ptr(n_dst_dev), n_dst, _lib.ptr(inj.flag), _lib.ptr(inj.row),
+              _lib.ptr(inj.table if inj.tables is None else None), _lib.ptr(inj.tables), int(h_out.shape[1]),
+              _lib.ptr(h_out), _lib.ptr(rowp), stream)
+    return FeatureRows(rowp, 2, int(h_out.shape[1]), n_dst)   # dtype 2: hidden-layer fp32 rows
 
 
 def layer_forward_dev(net: Network, l: int, blk, h_in: torch.Tensor, rows: torch.Tensor, R: int,
