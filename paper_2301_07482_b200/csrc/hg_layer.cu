@@ -47,6 +47,16 @@ constexpr int kMaxRowFloats = 1056;
 #ifndef HG_AGG_MINB
 #define HG_AGG_MINB 6
 #endif
+// hidden-layer rows through rowp (cache-hit rows in place, kSrc 3)
+#ifndef HG_AGG_MINB3
+#define HG_AGG_MINB3 6
+#endif
+#ifndef HG_AGG_EB3
+#define HG_AGG_EB3 4
+#endif
+#ifndef HG_AGG_PIPE3
+#define HG_AGG_PIPE3 1
+#endif
 #ifndef HG_AGG_MINBH       // layer 0 over fp16 rows (papers100M shape)
 #define HG_AGG_MINBH 8
 #endif
@@ -124,7 +134,7 @@ __device__ __forceinline__ float4 row_vec(const void* base, int v) {
 #endif
 
 template <int kKind, int kT, int kSrc>
-__global__ void __launch_bounds__(256, kT <= 2 ? (kSrc == 2 ? HG_AGG_MINBH : kSrc ? HG_AGG_MINB : HG_AGG_MINB0) : (kT <= 4 ? HG_AGG_MINB4 : (kSrc == 2 ? HG_AGG_MINB8H : HG_AGG_MINB8))) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, kT <= 2 ? (kSrc == 2 ? HG_AGG_MINBH : kSrc == 3 ? HG_AGG_MINB3 : kSrc ? HG_AGG_MINB : HG_AGG_MINB0) : (kT <= 4 ? HG_AGG_MINB4 : (kSrc == 2 ? HG_AGG_MINB8H : HG_AGG_MINB8))) k_aggregate(const int32_t* R_dev, const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ start, const int32_t* __restrict__ end,
                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ dst_deg,
                                                    const int32_t* __restrict__ src_deg, const float* __restrict__ h_in,
@@ -156,8 +166,8 @@ __global__ void __launch_bounds__(256, kT <= 2 ? (kSrc == 2 ? HG_AGG_MINBH : kSr
   }
   // measured (C2): the pipelined loop helps the layer-0 rows-in-place variant
   // (one more dependent hop per edge) and costs the matrix variant ~20 %
-  constexpr bool kPipe = HG_AGG_PIPE && kSrc >= 1;
-  constexpr int kEB = kSrc ? HG_AGG_EB : HG_AGG_EB0;   // edges in flight per warp
+  constexpr bool kPipe = HG_AGG_PIPE && kSrc >= 1 && (kSrc != 3 || HG_AGG_PIPE3);
+  constexpr int kEB = kSrc == 3 ? HG_AGG_EB3 : kSrc ? HG_AGG_EB : HG_AGG_EB0;   // edges in flight per warp
   for (; i < R; i += warps) {
     const int i_next = i + warps;
     const int r_next = kPipe && i_next < R ? rows[i_next] : 0;
