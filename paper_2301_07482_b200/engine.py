@@ -160,7 +160,11 @@ class StepEngine:
         self.cur = 0                     # slot of the next batch to train
         # block 0's sources carry no in-edges (src_deg = 0): one persistent zero vector
         self.zero_deg = torch.zeros(self.slots[0].layers[-1]["Fn_max"], dtype=torch.int32, device=self.dev)
-        pr = (lambda p: dict(priority=p)) if _NODE_PRIO else (lambda p: {})
+        # role priorities under HG_NODE_PRIO=1 (lower = served first):
+        # HG_PRIO_SAMP / HG_PRIO_MAIN / HG_PRIO_CACHE, default 0 / -1 / -2
+        roles = {0: int(os.environ.get("HG_PRIO_SAMP", "0")), -1: int(os.environ.get("HG_PRIO_MAIN", "-1")),
+                 -2: int(os.environ.get("HG_PRIO_CACHE", "-2"))}
+        pr = (lambda p: dict(priority=roles[p])) if _NODE_PRIO else (lambda p: {})
         self._prio = pr
         self.samp_stream = torch.cuda.Stream(self.dev, **pr(0))
         # backward inputs that depend only on the pruned blocks / the weights

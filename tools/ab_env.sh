@@ -17,5 +17,6 @@ for spec in sys.argv[1:]:
     tl = d["timeline_ms"]
     print(f"{v:10s} value {d['value']:.4g} e2e {d['e2e']['value']:.4g} ms {d['ms_per_step']:.4f} "
           f"select {d['per_kernel']['k_select']['ms_per_step']:.4f} samp {tl.get('next_sampled (side)')} "
-          f"c1 {tl.get('cache_update1 (side)')} sgd {tl.get('sgd')} joined {tl.get('joined')}")
+          f"c1 {tl.get('cache_update1 (side)')} sgd {tl.get('sgd')} joined {tl.get('joined')} "
+          f"sus {d['sustained']['value']:.4g} ({d['sustained']['seconds']:.2f} s, caps {d['sustained'].get('graph_captures')})")
 PY
