@@ -2,7 +2,8 @@
 //
 // The element count lives in device memory (`n_dev`), the host only supplies an
 // upper bound that sizes the grid, so scans chain after kernels whose output
-// size is not yet known on the host. Three launches:
+// size is not yet known on the host. Three launches (the second folded into
+// the third for scans of <= kSelfPrefixTiles tiles):
 //   1. per-tile reduction of f(i) into partials[tile]
 //   2. single-CTA exclusive scan of the partials (sequential carry over chunks)
 //   3. per-tile block scan; emit(i, exclusive_prefix, f(i)) for every i < n and
@@ -136,7 +137,11 @@ __global__ void __launch_bounds__(1024) k_scan_partials(T* partials, int tiles) 
   }
 }
 
-template <typename T, typename F, typename NC, typename Emit, typename Total, int kItems = kScanItems>
+// kSelfPrefix: `partials` holds the raw tile totals of k_tile_reduce and each
+// CTA sums the ones before it itself (short scans: no single-CTA
+// k_scan_partials launch between the two passes)
+template <typename T, typename F, typename NC, typename Emit, typename Total, int kItems = kScanItems,
+          bool kSelfPrefix = false>
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(F f, NC nc, const T* partials, Emit emit,
                                                             Total total) {
   pdl_wait();
@@ -158,7 +163,15 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(F f, NC nc, const T*
     sum = sum + v[k];
   }
   T tot;
-  T run = partials[blockIdx.x] + block_exclusive(sum, &tot);
+  T prefix;
+  if constexpr (kSelfPrefix) {
+    T acc = zero_of<T>();
+    for (int t = threadIdx.x; t < (int)blockIdx.x; t += kScanThreads) acc = acc + partials[t];
+    block_exclusive(acc, &prefix);
+  } else {
+    prefix = partials[blockIdx.x];
+  }
+  T run = prefix + block_exclusive(sum, &tot);
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
     long long i = tb + k;
@@ -170,7 +183,14 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(F f, NC nc, const T*
   }
 }
 
-// Launch the three-kernel scan. partials must hold >= scan_tiles(n_max) T
+// scans of at most this many tiles run in two launches (k_tile_scan sums the
+// tile totals before its own tile); longer ones keep the single-CTA pass
+#ifndef HG_SCAN_SELF_PREFIX_TILES
+#define HG_SCAN_SELF_PREFIX_TILES 1024
+#endif
+constexpr long long kSelfPrefixTiles = HG_SCAN_SELF_PREFIX_TILES;
+
+// Launch the three-kernel scan (two kernels up to kSelfPrefixTiles tiles). partials must hold >= scan_tiles(n_max) T
 // (tiles of kScanThreads x kItems items; kItems < kScanItems for items whose
 // emit is heavy, e.g. the sampler's bitmap words: more, shorter threads).
 inline long long scan_tiles(long long n_max, int items = kScanItems) {
@@ -185,6 +205,12 @@ int scan_launch(const char* where, F f, NC nc, long long n_max, T* partials, Emi
   HG_CHECK_CUDA(where, launch_pdl(k_tile_reduce<T, F, NC, kItems>, dim3((unsigned)tiles), dim3(kScanThreads), 0, s,
                                    f, nc, partials));
   HG_LAUNCHED(where);
+  if (tiles <= kSelfPrefixTiles) {
+    HG_CHECK_CUDA(where, launch_pdl(k_tile_scan<T, F, NC, Emit, Total, kItems, true>, dim3((unsigned)tiles),
+                                     dim3(kScanThreads), 0, s, f, nc, (const T*)partials, emit, total));
+    HG_LAUNCHED(where);
+    return kOk;
+  }
   HG_CHECK_CUDA(where, launch_pdl(k_scan_partials<T>, dim3(1), dim3(1024), 0, s, partials, (int)tiles));
   HG_LAUNCHED(where);
   HG_CHECK_CUDA(where, launch_pdl(k_tile_scan<T, F, NC, Emit, Total, kItems>, dim3((unsigned)tiles),
