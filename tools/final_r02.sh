@@ -21,6 +21,7 @@ cap() {   # name regex count skip [bench args]
   ncu -i $OUT/ncu_$1.ncu-rep --page raw --csv > $OUT/ncu_$1_raw.csv 2>/dev/null
   rm -f $OUT/ncu_$1.ncu-rep
 }
+if [ "${SKIP_NCU:-0}" != 1 ]; then
 cap k_aggregate_c2 "^k_aggregate" 3 30
 cap k_tsgemm_c2 "k_tsgemm" 8 60
 cap k_aggregate_c3 "^k_aggregate" 1 30 "--config c3"
@@ -55,6 +56,7 @@ json.dump(out, open("profiles/r02/traffic.json", "w"), indent=1)
 json.dump(out, open("gpurun_out/final/traffic.json", "w"), indent=1)
 print("traffic", {k: (v["kernel_name"][:40], v["traffic_bytes"]) for k, v in out.items()})
 PY
+fi
 timeout 1200 python bench.py > $OUT/bench_c2.json 2> $OUT/bench_c2.err
 for c in c3 c5 c4s; do timeout 1500 python bench.py --config $c > $OUT/bench_$c.json 2> $OUT/bench_$c.err; done
 timeout 1200 python bench.py --impl reference > $OUT/bench_reference_arm.json 2> $OUT/bench_reference_arm.err
