@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256, kT <= 2 ? (kSrc == 2 ? HG_AGG_MINBH : kSr
       const int v = lane + 32 * t;
       const float4 x = v < nv ? row_vec<kSrc>(hs, v) : make_float4(0.f, 0.f, 0.f, 0.f);
       if constexpr (kSelfSmem) {
-        if (v < nv) reinterpret_cast<float4*>(srow)[v] = x;
+        if (v < nv) stage_put4(srow, v, x);
       } else {
         xs[t] = x;
       }
@@ -243,19 +243,19 @@ __global__ void __launch_bounds__(256, kT <= 2 ? (kSrc == 2 ? HG_AGG_MINBH : kSr
     for (int t = 0; t < kT; ++t) {
       const int v = lane + 32 * t;
       if (v < nv) {
-        const float4 x_self = kSelfSmem ? reinterpret_cast<const float4*>(srow)[v] : xs[kSelfSmem ? 0 : t];
+        const float4 x_self = kSelfSmem ? stage_get4(srow, v) : xs[kSelfSmem ? 0 : t];
         if (kKind == kKindSAGE) {
-          if (!kSelfSmem) reinterpret_cast<float4*>(srow)[v] = x_self;
-          reinterpret_cast<float4*>(srow + d)[v] = acc[t];
+          if (!kSelfSmem) stage_put4(srow, v, x_self);
+          stage_put4(srow, (d >> 2) + v, acc[t]);
         } else {
           const float ws = gcn_coef(dd, src_deg[r_cur]);
-          reinterpret_cast<float4*>(srow)[v] = f4_fmadd_rn(acc[t], ws, x_self);
+          stage_put4(srow, v, f4_fmadd_rn(acc[t], ws, x_self));
         }
       }
     }
-    for (int c = K + lane; c < nK * 32; c += 32) srow[c] = c == K ? 1.f : 0.f;
+    for (int c = K + lane; c < nK * 32; c += 32) stage_put1(srow, c, c == K ? 1.f : 0.f);
     __syncwarp();
-    for (int g = lane; g < nK * 4; g += 32) ts_store8(A_ts, nK * 4, plane, i, g, srow + g * 8);
+    for (int g = lane; g < nK * 4; g += 32) ts_store8_staged(A_ts, nK * 4, plane, i, g, srow);
     __syncwarp();
   }
   // zero the padding rows of the last 128-row tile (the weight-gradient GEMM
@@ -666,12 +666,12 @@ __global__ void __launch_bounds__(256, kT <= 2 ? HG_TAGG_MINB : 1) k_transpose_a
               g = make_float4(h.x > 0.f ? g.x : 0.f, h.y > 0.f ? g.y : 0.f, h.z > 0.f ? g.z : 0.f,
                               h.w > 0.f ? g.w : 0.f);
             }
-            reinterpret_cast<float4*>(srow)[v] = g;
+            stage_put4(srow, v, g);
           }
         }
-        for (int j = d + lane; j < dzo.nK * 32; j += 32) srow[j] = 0.f;
+        for (int j = d + lane; j < dzo.nK * 32; j += 32) stage_put1(srow, j, 0.f);
         __syncwarp();
-        for (int g = lane; g < dzo.nK * 4; g += 32) ts_store8(dzo.ts, dzo.nK * 4, dzo.plane, pn, g, srow + g * 8);
+        for (int g = lane; g < dzo.nK * 4; g += 32) ts_store8_staged(dzo.ts, dzo.nK * 4, dzo.plane, pn, g, srow);
         __syncwarp();
       }
     }

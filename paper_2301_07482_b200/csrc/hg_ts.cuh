@@ -69,4 +69,27 @@ __device__ __forceinline__ void ts_store8(uint8_t* ts, int nCG, long long plane,
   *reinterpret_cast<uint4*>(ts + plane + off) = lo;
 }
 
+// A warp's staging row for TS emission (aggregation / transposed aggregation):
+// logical float4 chunk j lives at j ^ ((j >> 3) & 1). The emission reads a
+// 32-byte column group per lane (chunks 2g, 2g + 1); unswizzled, the 8 lanes
+// of an LDS.128 phase hit every bank pair twice (ncu: 3.6M shared-load bank
+// conflicts, 7.4 wavefronts per load in the C2 layer-0 aggregation); the
+// swizzle spreads them over all banks, and lane-per-chunk writes stay
+// conflict-free (the XOR stays inside each aligned group of 8 chunks).
+__device__ __forceinline__ int stage_chunk(int j) { return j ^ ((j >> 3) & 1); }
+__device__ __forceinline__ void stage_put4(float* row, int j, float4 v) {
+  reinterpret_cast<float4*>(row)[stage_chunk(j)] = v;
+}
+__device__ __forceinline__ float4 stage_get4(const float* row, int j) {
+  return reinterpret_cast<const float4*>(row)[stage_chunk(j)];
+}
+__device__ __forceinline__ void stage_put1(float* row, int c, float x) { row[stage_chunk(c >> 2) * 4 + (c & 3)] = x; }
+// emit column group g (logical columns 8g .. 8g + 7) of a staged row
+__device__ __forceinline__ void ts_store8_staged(uint8_t* ts, int nCG, long long plane, int r, int g,
+                                                 const float* row) {
+  const float4 a = stage_get4(row, 2 * g), b = stage_get4(row, 2 * g + 1);
+  const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  ts_store8(ts, nCG, plane, r, g, v);
+}
+
 }  // namespace hg

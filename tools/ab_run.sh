@@ -4,3 +4,4 @@ bash tools/ab_bench.sh "default prev" --steps 300 2>&1 | grep -v timeline | tail
 cp gpurun_out/ab_default.json gpurun_out/ab_default_c2.json; cp gpurun_out/ab_prev.json gpurun_out/ab_prev_c2.json
 bash tools/ab_bench.sh "default prev" --steps 300 2>&1 | grep -v timeline | tail -2
 bash tools/ab_bench.sh "default prev" --config c3 --steps 200 2>&1 | grep -v timeline | tail -2
+bash tools/ab_bench.sh "default prev" --config c4s --steps 200 2>&1 | grep -v timeline | tail -2
