@@ -41,7 +41,8 @@ def _ts_T(lib, P):
 
 @pytest.mark.parametrize("R,R_max,K1,N,relu", [(1000, 1000, 201, 256, 1), (777, 1024, 513, 256, 1),
                                                (130, 200, 513, 47, 0), (1, 128, 33, 8, 0), (4096, 5000, 257, 172, 1),
-                                               # row bounds >= 256K select the persistent kernel
+                                               # tall row bounds (the persistent kernel loops over many tiles
+                                               # per CTA; a bound far above the device count)
                                                (300000, 330000, 129, 256, 1), (1000, 300000, 201, 256, 0)])
 def test_ts_forward_scatter(R, R_max, K1, N, relu):
     lib = _lib()
@@ -62,6 +63,29 @@ def test_ts_forward_scatter(R, R_max, K1, N, relu):
     mask = torch.ones(R_max, dtype=torch.bool, device="cuda")
     mask[rows.long()] = False
     assert torch.isnan(out[mask]).all()
+
+
+def test_ts_empty_row_range():
+    """R = 0 on the device (everything pruned or served from the cache): the
+    forward and data-gradient GEMMs launch, touch no output row and return."""
+    lib = _lib()
+    R_max, K1, N = 256, 201, 256
+    A = torch.randn(R_max, K1, device="cuda")
+    P = torch.randn(K1, N, device="cuda")
+    rows = torch.zeros(R_max, dtype=torch.int32, device="cuda")
+    out = torch.full((R_max, N), float("nan"), device="cuda")
+    R_dev = torch.zeros(1, dtype=torch.int32, device="cuda")
+    A_ts, PT_ts = _ts(lib, A, R_max), _ts_T(lib, P)
+    lib.call("hg_ts_linear_fwd", lib.ptr(R_dev), R_max, lib.ptr(A_ts), K1, lib.ptr(PT_ts), N,
+             lib.ptr(rows), 1, lib.ptr(out), lib.stream_ptr())
+    dz = torch.randn(R_max, N, device="cuda")
+    W = torch.randn(K1 - 1, N, device="cuda")
+    SG = torch.full((R_max, K1 - 1), float("nan"), device="cuda")
+    dz_ts, W_ts = _ts(lib, dz, R_max), _ts(lib, W)
+    lib.call("hg_ts_linear_dgrad", lib.ptr(R_dev), R_max, lib.ptr(dz_ts), N, lib.ptr(W_ts), K1 - 1, lib.ptr(SG),
+             lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.isnan(out).all() and torch.isnan(SG).all()
 
 
 @pytest.mark.parametrize("R,R_max,N,K", [(1000, 1000, 256, 512), (333, 600, 47, 256), (5, 128, 8, 64),

@@ -1,3 +1,3 @@
 set -u
-BENCH_ARGS="--steps 200 --config c3" bash tools/ab_env.sh "c3auto:" "c3inpl:HG_INPLACE_HITS=1" "c3auto2:" "c3inpl2:HG_INPLACE_HITS=1" 2>&1 | tail -4
-BENCH_ARGS="--steps 200 --config c4s" bash tools/ab_env.sh "c4auto:" "c4inpl:HG_INPLACE_HITS=1" 2>&1 | tail -2
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
