@@ -884,11 +884,16 @@ int hg_sample_layer(const int64_t* g_start, const int64_t* g_end, const int32_t*
     // selection's CTAs hold their slots until the queue drains, and the
     // forward runs beside them (C2: 444 CTAs 1.533 / 1.540e6 seeds/s vs
     // 592: 1.521e6, 296: 1.531e6, 148: 1.458e6); HG_SEL_BLOCKS overrides
-    static const long long sel_cap = [] {
+    // (C3, 111M nodes: 2 CTAs per SM measured better -- 1.324-1.326e6 vs
+    // 1.299-1.307e6 seeds/s -- the selection's random candidate reads over
+    // a multi-GB graph contend less with the training kernels; C2 keeps 3:
+    // 1.609-1.612e6 vs 1.586e6 with 2)
+    static const long long sel_env = [] {
       const char* v = std::getenv("HG_SEL_BLOCKS");
-      const long long x = v ? std::atoll(v) : 148 * 3;
-      return x < 1 ? 148ll * 3 : x;
+      const long long x = v ? std::atoll(v) : 0;
+      return x < 1 ? 0ll : x;
     }();
+    const long long sel_cap = sel_env ? sel_env : (num_nodes >= (32ll << 20) ? 148 * 2 : 148 * 3);
     const int fk = lane_max == 0 ? 0 : fanout <= 2 ? 2 : fanout <= 4 ? 4 : fanout <= 5 ? 5 : fanout <= 6 ? 6
                  : fanout <= 8 ? 8 : fanout <= 10 ? 10 : fanout <= 12 ? 12 : fanout <= 15 ? 15 : 16;
 #define HG_SEL_CASE(K)                                                                                          \
